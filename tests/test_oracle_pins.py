@@ -1,0 +1,244 @@
+"""Pins of the CPU oracle against things other than itself (no GPU needed).
+
+Each test names what fixes the oracle: a library routine (numpy sort /
+searchsorted / cumsum / stable argsort), brute force over all small inputs,
+a closed form or invariant from PAPER.md, or a SPEC.md worked example stored
+under tests/golden/ with its citation.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+U64_MAX = (1 << 64) - 1
+U32_MAX = (1 << 32) - 1
+
+
+def _props(inp, out, pivot, split):
+    """(1)-(3) of SURVEY §8(c), checked with numpy only."""
+    inp = np.asarray(inp)
+    out = np.asarray(out)
+    K = int(np.searchsorted(np.sort(inp), np.array(pivot, dtype=inp.dtype), side="left"))
+    assert split == K
+    assert np.all(out[:K] < pivot) and np.all(out[K:] >= pivot)
+    assert np.array_equal(np.sort(out), np.sort(inp))
+
+
+# ----------------------------------------------------------------------------
+# SPEC.md worked examples (tests/golden/spec_examples.json)
+# ----------------------------------------------------------------------------
+
+def test_golden_partition(golden):
+    for ex in golden["partition"]:
+        for dt in (np.uint64, np.uint32):
+            a = np.array(ex["keys"], dtype=dt)
+            b = a.copy()
+            assert oracle.partition_two_pointer(b, ex["pivot"]) == ex["split"], ex["cite"]
+            _props(a, b, ex["pivot"], ex["split"])
+            c = a.copy()
+            assert oracle.partition_standard(c, ex["pivot"]) == ex["split"], ex["cite"]
+            assert c.tolist() == ex["stable_output"], ex["cite"]
+            assert oracle.count(a, ex["pivot"]) == ex["split"]
+
+
+def test_golden_is_partitioned(golden):
+    for ex in golden["is_partitioned"]:
+        a = np.array(ex["keys"], dtype=np.uint64)
+        assert oracle.is_partitioned(a, ex["pivot"], ex["k"]) == ex["expect"], ex["cite"]
+
+
+def test_golden_prefix_sum(golden):
+    for ex in golden["prefix_sum"]:
+        assert oracle.prefix_sum(ex["input"]).tolist() == ex["output"], ex["cite"]
+
+
+def test_golden_block_start_index(golden):
+    """Fig. 3 GetBlockStartIndex through ss_groups: with all keys successors,
+    v_i is the start of U_i's first line; with U_i's first line all
+    predecessors (T_i = b), v_i is the start of its second line.  The oracle's
+    0-based offsets are X0 = (X + 1) mod g (reading: 1-based i, X)."""
+    for ex in golden["block_start_index"]:
+        g, b, i1, j1 = ex["g"], ex["b"], ex["i"], ex["j"]
+        X0 = [(x + 1) % g for x in ex["X_1based"]]
+        n_lines = g * len(X0)
+        a = np.full(n_lines * b, 100, dtype=np.uint64)       # all successors (pivot 50)
+        if j1 == 2:
+            # make U_i's first line (found with j=1 on an all-successor array) predecessors
+            T, vlo, _ = oracle.ss_groups(a, 0, n_lines, b, g, X0, 50)
+            first = int(vlo[i1 - 1])
+            a[first:first + b] = 1
+        T, vlo, vhi = oracle.ss_groups(a, 0, n_lines, b, g, X0, 50)
+        assert int(vlo[i1 - 1]) + 1 == ex["start_1based"], ex["cite"]
+        assert vlo[i1 - 1] == vhi[i1 - 1]
+
+
+# ----------------------------------------------------------------------------
+# count: closed form vs a library routine
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
+def test_count_vs_searchsorted(dt, mx):
+    rng = np.random.default_rng(1)
+    for n in (0, 1, 2, 7, 1000, 4097):
+        a = rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
+        for p in (0, 1, mx // 2, mx, int(a[0]) if n else 5):
+            ref = int(np.searchsorted(np.sort(a), np.array(p, dtype=dt), side="left"))
+            assert oracle.count(a, p) == ref
+
+
+# ----------------------------------------------------------------------------
+# two-pointer and standard partitions: brute force over all tiny inputs
+# ----------------------------------------------------------------------------
+
+def test_bruteforce_alphabet4():
+    """Every array over {0,1,2,3} with n <= 6 (5461 arrays) x pivots 0..4."""
+    for n in range(0, 7):
+        for tup in itertools.product(range(4), repeat=n):
+            a = np.array(tup, dtype=np.uint64)
+            for p in range(5):
+                b = a.copy()
+                k = oracle.partition_two_pointer(b, p)
+                _props(a, b, p, k)
+                c = a.copy()
+                k2 = oracle.partition_standard(c, p)
+                assert k2 == k
+                # stable => unique: a library stable sort by the predicate
+                ref = a[np.argsort(~(a < p), kind="stable")]
+                assert np.array_equal(c, ref)
+
+
+def test_bruteforce_patterns_tagged():
+    """All 2^n predecessor/successor patterns for n <= 12 with distinct keys
+    (identity of each key tracked by value)."""
+    for n in range(0, 13):
+        for mask in range(1 << n):
+            bits = np.array([(mask >> i) & 1 for i in range(n)], dtype=bool)
+            idx = np.arange(n, dtype=np.uint32)
+            a = np.where(bits, idx, idx + 1000).astype(np.uint32)   # pred < 1000 <= succ
+            b = a.copy()
+            k = oracle.partition_two_pointer(b, 1000)
+            _props(a, b, 1000, k)
+            c = a.copy()
+            assert oracle.partition_standard(c, 1000) == k
+            assert np.array_equal(c, a[np.argsort(~bits, kind="stable")])
+
+
+@pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
+def test_random_partitions_vs_library(dt, mx):
+    rng = np.random.default_rng(7)
+    for n in (1, 2, 3, 100, 5000, 65537):
+        a = rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
+        for p in (0, 1, mx, mx // 3, int(a[n // 2])):
+            b = a.copy()
+            k = oracle.partition_two_pointer(b, p)
+            _props(a, b, p, k)
+            c = a.copy()
+            assert oracle.partition_standard(c, p) == k
+            assert np.array_equal(c, a[np.argsort(~(a < p), kind="stable")])
+
+
+# ----------------------------------------------------------------------------
+# prefix sum: library cumsum
+# ----------------------------------------------------------------------------
+
+def test_prefix_sum_vs_cumsum():
+    rng = np.random.default_rng(3)
+    for n in list(range(0, 40)) + [1023, 1024, 1025, 99991]:
+        d = rng.integers(0, 2, size=n).astype(np.uint64)
+        assert np.array_equal(oracle.prefix_sum(d), np.cumsum(d, dtype=np.uint64))
+        w = rng.integers(0, 1 << 20, size=n).astype(np.uint64)     # general summands
+        assert np.array_equal(oracle.prefix_sum(w), np.cumsum(w, dtype=np.uint64))
+
+
+# ----------------------------------------------------------------------------
+# quicksort: unique output => numpy.sort byte for byte
+# ----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
+def test_quicksort_vs_numpy(dt, mx):
+    rng = np.random.default_rng(11)
+    cases = []
+    for n in (0, 1, 2, 3, 15, 16, 17, 33, 1000, 100003):
+        cases.append(rng.integers(0, mx, size=n, dtype=dt, endpoint=True))
+        cases.append(rng.integers(0, 1000, size=n).astype(dt))        # duplicate-heavy
+        cases.append(np.full(n, 7, dtype=dt))                         # all equal
+        cases.append(np.full(n, mx, dtype=dt))                        # all MAX
+        cases.append(np.arange(n, dtype=dt))                          # sorted
+        cases.append(np.arange(n, dtype=dt)[::-1].copy())             # reverse
+        cases.append(rng.integers(0, 2, size=n).astype(dt) * dt(mx))  # {0, MAX}
+    for a in cases:
+        b = a.copy()
+        oracle.quicksort(b)
+        assert np.array_equal(b, np.sort(a))
+
+
+# ----------------------------------------------------------------------------
+# Smoothed Striding group statistics
+# ----------------------------------------------------------------------------
+
+def _groups_bruteforce(a, base, n_lines, b, g, X, pivot):
+    """Independent enumeration: line q of chunk j belongs to group
+    i = (q - X[j]) mod g (inverse of the Fig. 3 map); the group's elements in
+    group order are its positions in ascending order."""
+    members = [[] for _ in range(g)]
+    for line in range(n_lines):
+        j, q = divmod(line, g)
+        i = (q - int(X[j])) % g
+        members[i].extend(range(base + line * b, base + line * b + b))
+    T = np.zeros(g, dtype=np.uint64)
+    vlo = np.zeros(g, dtype=np.uint64)
+    vhi = np.zeros(g, dtype=np.uint64)
+    for i in range(g):
+        pos = sorted(members[i])
+        t = sum(1 for x in pos if a[x] < pivot)
+        T[i] = t
+        if not pos:
+            vlo[i], vhi[i] = base + n_lines * b, base
+        elif t == len(pos):
+            vlo[i] = vhi[i] = pos[-1] + 1
+        else:
+            vlo[i] = vhi[i] = pos[t]
+    return T, vlo, vhi, members
+
+
+@pytest.mark.parametrize("g,b,n_lines,base", [(4, 2, 8, 0), (4, 2, 9, 3), (7, 4, 40, 1),
+                                              (16, 8, 100, 0), (3, 16, 2, 5), (5, 4, 0, 0)])
+def test_ss_groups_bruteforce(g, b, n_lines, base):
+    rng = np.random.default_rng(g * 1000 + b)
+    s = (n_lines + g - 1) // g
+    for trial in range(20):
+        n = base + n_lines * b + 3
+        a = rng.integers(0, 100, size=n).astype(np.uint64)
+        X = rng.integers(0, g, size=max(1, s))
+        p = int(rng.integers(0, 101))
+        T, vlo, vhi = oracle.ss_groups(a, base, n_lines, b, g, X, p)
+        T2, vlo2, vhi2, members = _groups_bruteforce(a, base, n_lines, b, g, X, p)
+        assert np.array_equal(T, T2) and np.array_equal(vlo, vlo2) and np.array_equal(vhi, vhi2)
+        # window invariant: partition each group (stably,
+        # in group order) and check A[x] pred for x < v_min, succ for x >= v_max
+        if n_lines:
+            c = a.copy()
+            for i in range(g):
+                pos = sorted(members[i])
+                vals = c[pos]
+                c[pos] = vals[np.argsort(~(vals < p), kind="stable")]
+            vmin, vmax = int(vlo.min()), int(vhi.max())
+            region = slice(base, base + n_lines * b)
+            r = c[region]
+            lo, hi = vmin - base, vmax - base
+            assert np.all(r[:lo] < p) and np.all(r[hi:] >= p)
+            assert lo <= int(T.sum()) <= hi
+
+
+def test_ss_offsets_generator():
+    """Range and determinism of the counter-based offset generator."""
+    for g in (1, 2, 7, 444, 1 << 20):
+        X = synth.ss_offsets(0xABC, 1000, g)
+        assert X.dtype == np.uint64 and X.min() >= 0 and X.max() < g
+        assert np.array_equal(X, synth.ss_offsets(0xABC, 1000, g))
+    X = synth.ss_offsets(5, 200000, 8)
+    counts = np.bincount(X.astype(np.int64), minlength=8)
+    assert counts.min() > 0.9 * 25000 and counts.max() < 1.1 * 25000
