@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""bench.py -- BASELINE metric: partition keys/s and GB/s (fraction of the HBM
+read+write roofline) on B200; quicksort keys/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): in-place
+partition of n = 2^27 uint64 keys, i.i.d. uniform from the splitmix64 stream
+(seed c2), pivot 2^63 (mu = 0.5).  One step = one full pp_partition (all
+kernels of the hot path) over a fresh copy of the input resident in HBM.
+Before every step (untimed) the input is restored from a pristine copy and a
+512 MiB scratch buffer is written to flush L2 (126 MB).  Each step is timed
+with CUDA events on the launching stream; the K step times are summed.
+
+N > 1 (torchrun): each rank partitions its own contiguous 2^27-key shard of
+one global array (weak scaling) and the ranks exchange misplaced ranges over
+NCCL to complete the GLOBAL partition (paper_2004_12532_b200.dist); the step
+time is the max over ranks.
+
+--impl reference: the CPU oracle (oracle/, serial two-pointer partition,
+PAPER.md:1433-1436) on the host cores, same workload and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_KEYS = 1 << 27
+PIVOT = 1 << 63
+L2_FLUSH_BYTES = 512 << 20
+METRIC = "partition keys/s and GB/s (fraction of HBM roofline) at 1/2/4/8 B200; quicksort keys/s"
+WORKLOAD = "c2: in-place partition, n=2^27 uint64 uniform keys (1 GiB), pivot 2^63 (mu=0.5), 1 GPU per rank"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the group kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("ss_group_kernel", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """CPU oracle arm: serial two-pointer partition on the host."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    import synth
+    pristine = synth.uniform_u64_np(N_KEYS, synth.SEEDS["c2"])
+    work = np.empty_like(pristine)
+    for _ in range(args.warmup):
+        np.copyto(work, pristine)
+        oracle.partition_two_pointer(work, PIVOT)
+    times = []
+    for _ in range(args.steps):
+        np.copyto(work, pristine)
+        t0 = time.perf_counter()
+        split = oracle.partition_two_pointer(work, PIVOT)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = N_KEYS * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": N_KEYS, "pivot": PIVOT, "split": split},
+        "gbs": 2 * 8 * N_KEYS * args.steps / tot / 1e9,
+        "cpu_baseline": {"value": value, "unit": "keys/s", "cores": 1, "kind": "oracle",
+                         "sample": f"full c2 input (2^27 keys), {args.steps} timed steps, fresh copy each"},
+        "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline(budget_s: float = 12.0):
+    import oracle
+    import synth
+    pristine = synth.uniform_u64_np(N_KEYS, synth.SEEDS["c2"])
+    work = np.empty_like(pristine)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < 2 or (time.perf_counter() - t_start < budget_s and len(times) < 40):
+        np.copyto(work, pristine)
+        t0 = time.perf_counter()
+        oracle.partition_two_pointer(work, PIVOT)
+        times.append(time.perf_counter() - t0)
+    v = N_KEYS * len(times) / sum(times)
+    return {"value": v, "unit": "keys/s", "cores": 1, "kind": "oracle",
+            "sample": f"full c2 input (2^27 keys), {len(times)} runs of the serial two-pointer oracle, "
+                      f"fresh copy each, 1 host thread"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the mu sweep and quicksort lines")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2004_12532_b200 as pp
+    import synth
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    pp.load(build_if_missing=False)
+    pp.reset_params()
+    stream = torch.cuda.current_stream()
+
+    n = N_KEYS
+    pristine = synth.uniform_u64_torch(n, synth.SEEDS["c2"], dev, offset=rank * n)
+    buf = torch.empty_like(pristine)
+    flush = torch.empty(L2_FLUSH_BYTES // 8, dtype=torch.int64, device=dev)
+    d_split = torch.zeros(1, dtype=torch.int64, device=dev)
+    if ws > 1:
+        from paper_2004_12532_b200 import dist as ppdist
+        comm = ppdist.Partitioner(dev)
+
+    def step():
+        if ws > 1:
+            comm.partition_u64(buf, PIVOT)
+        else:
+            pp.pp_partition_async_u64(buf, PIVOT, d_split)
+
+    def restore():
+        buf.copy_(pristine)
+        flush.fill_(1)
+
+    # warm-up (and clock settle: untimed repeats for ~0.5 s so the clock
+    # sampler sees the GPU under this load before and during the timed region)
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(args.warmup):
+        restore()
+        step()
+    torch.cuda.synchronize()
+    t_end = time.perf_counter() + 0.5
+    while time.perf_counter() < t_end:
+        restore()
+        step()
+        torch.cuda.synchronize()
+
+    # ---- timed region ----
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    pp.pp_launch_count(reset=True)
+    pp.pp_timing(True)
+    for i in range(args.steps):
+        restore()
+        ev_s[i].record(stream)
+        step()
+        ev_e[i].record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches = pp.pp_launch_count()
+    tim = pp.pp_timing_read()
+    pp.pp_timing(False)
+    clocks = sampler.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(ev_s, ev_e)]
+    tot_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+
+    # sanity: the split equals the oracle's count on this input (cheap check)
+    split = int(d_split.item()) if ws == 1 else comm.last_global_split
+    stats = pp.pp_last_stats() if ws == 1 else {}
+
+    value = ws * n * args.steps / (tot_ms / 1e3)
+    ms_per_step = tot_ms / args.steps
+    bytes_step = 2 * 8 * n
+    peak, peak_kind = peaks()
+    # dominant kernel: the Smoothed Striding group kernel (every full line
+    # read once + written once): algorithmic bytes per launch
+    line_keys = stats.get("line_keys", 1024)
+    grp_bytes = 2 * 8 * stats.get("n_lines", n // 1024) * line_keys
+    grp_ms = tim["group_ms"] / max(tim["calls"], 1)
+    achieved = grp_bytes / (grp_ms / 1e3) / 1e9 if grp_ms > 0 else None
+    traffic = ncu_traffic()
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_per_gpu": n, "pivot": PIVOT, "mu": 0.5,
+                   "parallelism": f"dp{ws}" if ws > 1 else "single",
+                   "l2": "input 1 GiB > L2; before each step (untimed) input restored + 512 MiB L2 flush write"},
+        "gbs": ws * bytes_step * args.steps / (tot_ms / 1e3) / 1e9,
+        "frac_of_8tbs": (bytes_step / (ms_per_step / 1e3) / 1e9) / 8000.0,
+        "frac_of_measured_hbm": (bytes_step / (ms_per_step / 1e3) / 1e9) / peak,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "kernel": "ss_group_kernel", "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": grp_bytes, "avg_launch_ms": grp_ms,
+                     "kernel_share_of_step": (tim["group_ms"] / tim["total_ms"]) if tim["total_ms"] else None},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "split": split,
+        "window_frac": (stats.get("W", 0) / n) if stats else None,
+        "aux_bytes": stats.get("aux_bytes"),
+        "aux_frac": (stats.get("aux_bytes", 0) / (8 * n)) if stats else None,
+    }
+
+    if rank == 0 and ws == 1:
+        if not args.no_e2e:
+            out["e2e"] = e2e(pp, n, args)
+        if not args.no_extras:
+            out["extras"] = extras(pp, torch, synth, dev, stream, flush)
+        if not args.no_cpu_baseline:
+            cb = cpu_baseline()
+            out["cpu_baseline"] = cb
+        # split sanity vs oracle count (oracle used only as a reported check)
+        import oracle
+        out["split_ok"] = (split == oracle.count(pristine.cpu().numpy().view(np.uint64), PIVOT))
+    if rank == 0:
+        print(json.dumps(out))
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e(pp, n, args):
+    """End to end through the public host API: pinned host buffer -> H2D ->
+    partition -> D2H of the whole array and the split, every step
+    (wall clock around the synchronous call)."""
+    import torch
+    import synth
+    pristine = synth.uniform_u64_np(n, synth.SEEDS["c2"])
+    host = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    hv = host.numpy().view(np.uint64)
+    steps = max(3, min(args.steps, 8))
+    np.copyto(hv, pristine)
+    pp.pp_partition_host_u64(hv, PIVOT)  # warm
+    times = []
+    for _ in range(steps):
+        np.copyto(hv, pristine)
+        t0 = time.perf_counter()
+        pp.pp_partition_host_u64(hv, PIVOT)
+        times.append(time.perf_counter() - t0)
+    v = n * steps / sum(times)
+    return {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 8,
+            "steps": steps, "ms_per_step": 1e3 * sum(times) / steps, "api": "pp_partition_host_u64 (pinned host)",
+            "timing": "host wall clock around the synchronous call"}
+
+
+def extras(pp, torch, synth, dev, stream, flush):
+    """Secondary numbers: mu = 0.01 / 0.99 partition and the config-5 quicksort."""
+    res = {}
+    n = N_KEYS
+    pristine = synth.uniform_u64_torch(n, synth.SEEDS["c2"], dev)
+    buf = torch.empty_like(pristine)
+    d = torch.zeros(1, dtype=torch.int64, device=dev)
+    for mu in (0.01, 0.99):
+        p = synth.PIVOT_MU[mu]
+        ts = []
+        for i in range(8):
+            buf.copy_(pristine)
+            flush.fill_(1)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            pp.pp_partition_async_u64(buf, p, d)
+            e.record(stream)
+            torch.cuda.synchronize()
+            if i >= 3:
+                ts.append(s.elapsed_time(e))
+        ms = statistics.mean(ts)
+        st = pp.pp_last_stats()
+        res[f"partition_mu{mu}"] = {"keys_per_s": n / (ms / 1e3), "ms": ms,
+                                    "gbs": 16 * n / (ms / 1e3) / 1e9, "window_frac": st["W"] / n}
+    del pristine, buf
+    nq = 1 << 28
+    for kind in ("uniform", "dup1000"):
+        if kind == "uniform":
+            q0 = synth.uniform_u64_torch(nq, synth.SEEDS["c5"], dev)
+        else:
+            q0 = synth.mod_range_u64_torch(nq, synth.SEEDS["c5"], 1000, dev)
+        q = torch.empty_like(q0)
+        ts = []
+        for i in range(3):
+            q.copy_(q0)
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            pp.pp_quicksort_u64(q)
+            e.record(stream)
+            torch.cuda.synchronize()
+            if i >= 1:
+                ts.append(s.elapsed_time(e))
+        ms = statistics.mean(ts)
+        res[f"quicksort_{kind}_2^28"] = {"keys_per_s": nq / (ms / 1e3), "ms": ms}
+        del q0, q
+    return res
+
+
+if __name__ == "__main__":
+    sys.exit(main())

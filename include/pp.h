@@ -1,0 +1,140 @@
+/*
+ * pp.h -- C ABI of the B200-native in-place parallel partition and quicksort
+ * (arxiv 2004.12532, "In-place parallel partition"; PAPER.md below means the
+ * paper's text).  Plain C: pointers and integer sizes only, no CUDA or torch
+ * types in the signatures (streams are passed as `void*` = cudaStream_t).
+ *
+ * Problem (§2 "The Parallel Partition Problem"): reorder an
+ * array so that predecessors precede successors.  Here predecessor <=>
+ * key < pivot, unsigned compare; indices are 0-based; the returned split is
+ * K = #{i : keys[i] < pivot}, i.e. the index of the first successor.
+ *
+ * Method: the Smoothed Striding Partial Partition Step
+ * (Fig. 3) realised as one CTA per group
+ * U_i, followed by a parallel rank-matched cleanup of the window
+ * [v_min, v_max) (the paper recurses or uses the Blocked-Prefix-Sum
+ * partition there).  Quicksort is
+ * layered on the same kernels.
+ *
+ * Ownership: `keys` is owned by the caller and is never allocated, freed or
+ * reallocated by the library.  The library owns an internal device
+ * workspace (o(n) bytes, reported by pp_last_aux_bytes) and one small pinned
+ * host word; calls from several host threads are serialised by a mutex.
+ *
+ * Errors: every call returns a pp_status.  PP_E_INVAL: NULL pointer with
+ * n > 0, `keys` not aligned to the key size, or a host pointer passed where a
+ * device pointer is required (or vice versa).  PP_E_CUDA: a CUDA call or
+ * kernel failed (message in pp_last_error(); the array is then unspecified
+ * but remains a permutation of the input if the failure came after launch).
+ * PP_E_INTERNAL: a device-side invariant check failed (never expected).
+ *
+ * Determinism: output bytes are a pure function of (input bytes, n, pivot,
+ * library build): no atomics, fixed thread mappings, a fixed offset seed.
+ */
+#ifndef PP_H_
+#define PP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PP_OK = 0,
+    PP_E_INVAL = 1,
+    PP_E_CUDA = 2,
+    PP_E_NOMEM = 3,
+    PP_E_NCCL = 4,
+    PP_E_INTERNAL = 5
+} pp_status;
+
+/* ---- single-GPU partition ------------------------------------------------
+ * keys: DEVICE pointer to n keys (uint64 / uint32), aligned to the key size
+ *       (any such alignment; 16-B vector I/O peels the unaligned head).
+ * pivot: predecessor <=> key < pivot (unsigned).
+ * stream: cudaStream_t (NULL = legacy default stream).  All work is enqueued
+ *       on it; the synchronous variants then wait for it.
+ * split_out: HOST pointer, receives K (sync variants).
+ * d_split:  DEVICE pointer to one uint64, receives K (async variants; the
+ *       call returns after enqueueing; no host synchronisation at all).
+ * n == 0 returns K = 0.  Cites: PAPER.md:272-281 (problem), 953-1015
+ * (Smoothed Striding partial step + cleanup). */
+pp_status pp_partition_u64(uint64_t *keys, uint64_t n, uint64_t pivot, void *stream, uint64_t *split_out);
+pp_status pp_partition_u32(uint32_t *keys, uint64_t n, uint32_t pivot, void *stream, uint64_t *split_out);
+pp_status pp_partition_async_u64(uint64_t *keys, uint64_t n, uint64_t pivot, void *stream, uint64_t *d_split);
+pp_status pp_partition_async_u32(uint32_t *keys, uint64_t n, uint32_t pivot, void *stream, uint64_t *d_split);
+
+/* ---- single-GPU quicksort ----------------------------
+ * Sorts n DEVICE keys ascending (unsigned), in place; synchronises `stream`
+ * (the level loop reads the per-level segment count).  Median-of-3 pivot,
+ * strict split, "x <= p" progress step when the pivot is the minimum
+ * (reading R14); small segments are sorted in shared memory. */
+pp_status pp_quicksort_u64(uint64_t *keys, uint64_t n, void *stream);
+pp_status pp_quicksort_u32(uint32_t *keys, uint64_t n, void *stream);
+
+/* ---- host-buffer (end-to-end) variants ------------------------------------
+ * host_keys: HOST pointer (pinned or pageable) to n keys, partitioned / sorted
+ * in place: copied to a library-owned device buffer, processed, copied back.
+ * These are what an application with host-resident data calls; bench.py's
+ * "e2e" number times them (H2D + kernels + D2H). */
+pp_status pp_partition_host_u64(uint64_t *host_keys, uint64_t n, uint64_t pivot, uint64_t *split_out);
+pp_status pp_partition_host_u32(uint32_t *host_keys, uint64_t n, uint32_t pivot, uint64_t *split_out);
+pp_status pp_quicksort_host_u64(uint64_t *host_keys, uint64_t n);
+
+/* ---- north-star names ------------------------------------------------------
+ * pp_partition(keys, n, pivot) -> split: uint64 DEVICE keys on the legacy
+ * default stream; returns UINT64_MAX on error (see pp_last_error()).
+ * pp_quicksort(keys, n): uint64 DEVICE keys on the legacy default stream. */
+uint64_t pp_partition(uint64_t *keys, uint64_t n, uint64_t pivot);
+pp_status pp_quicksort(uint64_t *keys, uint64_t n);
+
+/* ---- Smoothed Striding partial partition step alone (parity of internals) --
+ * Runs only the group kernel on the 16-B aligned region of `keys` with g
+ * groups (g = 0: the library's automatic choice) and copies the per-group
+ * statistics to HOST arrays T, vlo, vhi (g entries each; allocate
+ * pp_max_groups() entries if g = 0).  info[0..5] receives
+ * {g, head, n_lines, line_keys, seed, 0}: the region is keys[head ..
+ * head + n_lines*line_keys), X[j] = ((fmix64(seed + (j+1)*0x9E3779B97F4A7C15)
+ * >> 32) * g) >> 32.  vlo/vhi are region-relative positions.
+ * The array is left partially partitioned. */
+pp_status pp_ss_groups_u64(uint64_t *keys, uint64_t n, uint64_t pivot, uint64_t g, void *stream,
+                           uint64_t *T, uint64_t *vlo, uint64_t *vhi, uint64_t *info);
+pp_status pp_ss_groups_u32(uint32_t *keys, uint64_t n, uint32_t pivot, uint64_t g, void *stream,
+                           uint64_t *T, uint64_t *vlo, uint64_t *vhi, uint64_t *info);
+uint64_t pp_max_groups(void);
+
+/* ---- workspace / statistics / tuning --------------------------------------- */
+/* Bytes of device workspace a call on n keys of key_bytes (4 or 8) may use;
+ * op 0 = partition, 1 = quicksort. */
+uint64_t pp_workspace_bytes(uint64_t n, int key_bytes, int op);
+/* Device bytes besides `keys` touched by the last call (aux memory). */
+uint64_t pp_last_aux_bytes(void);
+/* Statistics of the last partition call: out[0..12] = {n, K, W(dirty-set
+ * size), v_min, v_max, M (misplaced pairs in the cleanup), g, line_keys,
+ * n_lines, head, aux_bytes, path, nTasks}.  Reads device memory: synchronous. */
+pp_status pp_last_stats(uint64_t *out13);
+/* Tunables (tests / benchmarks): "g", "min_lines_per_group", "small_n",
+ * "path" (0 auto, 1 single-CTA, 2 smoothed striding, 3 cleanup only), "tile",
+ * "ranks", "seed", "leaf", "qs_cta_max", "variant".  Returns PP_E_INVAL for an unknown
+ * name.  pp_get_param returns INT64_MIN for an unknown name. */
+pp_status pp_set_param(const char *name, int64_t value);
+int64_t pp_get_param(const char *name);
+
+const char *pp_status_string(pp_status s);
+const char *pp_last_error(void);
+/* Number of kernel launches enqueued by the library since the last reset. */
+uint64_t pp_launch_count(int reset);
+/* Phase timing of partition calls with CUDA events recorded on each call's
+ * stream: pp_timing(1) starts (and clears) recording; pp_timing_read(out)
+ * waits for the recorded events and writes {calls, group-kernel ms total,
+ * rest-of-pipeline ms total, total ms}, then clears.  For single-CTA /
+ * cleanup-only calls the "group" phase is the whole first kernel(s). */
+void pp_timing(int enable);
+pp_status pp_timing_read(double *out4);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PP_H_ */

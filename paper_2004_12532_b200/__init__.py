@@ -1,0 +1,273 @@
+"""B200-native in-place parallel partition and quicksort (arxiv 2004.12532).
+
+Thin Python binding over the C ABI in ``include/pp.h`` (``libpp.so``, built
+in-tree by ``_build.py``).  Argument marshalling only: every step of the
+partition / quicksort runs in the library's CUDA kernels.  There is no CPU
+fallback: if ``libpp.so`` is missing or fails to load, every call raises.
+
+Function names mirror the C ABI:
+
+    pp_partition_u64(keys, pivot) -> split        (keys: CUDA int64/uint64 tensor)
+    pp_partition_u32(keys, pivot) -> split        (keys: CUDA int32/uint32 tensor)
+    pp_partition_async_u64/u32(keys, pivot, d_split)
+    pp_quicksort_u64/u32(keys)
+    pp_partition_host_u64/u32(np_array, pivot) -> split   (host buffers)
+    pp_quicksort_host_u64(np_array)
+    pp_partition(keys, pivot) / pp_quicksort(keys)         (dtype dispatch)
+    pp_ss_groups(keys, pivot, g=0) -> (T, vlo, vhi, info)
+
+int64/int32 tensors are treated as their unsigned bit patterns (torch lacks
+most uint64 ops); pivots are Python ints in the unsigned range.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+LIB_PATH = os.path.join(_PKG, "libpp.so")
+HEADER = os.path.join(_ROOT, "include", "pp.h")
+
+PP_OK = 0
+STATUS = {0: "PP_OK", 1: "PP_E_INVAL", 2: "PP_E_CUDA", 3: "PP_E_NOMEM", 4: "PP_E_NCCL", 5: "PP_E_INTERNAL"}
+
+_lib = None
+
+
+class PPError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def load(build_if_missing: bool = True):
+    """Load libpp.so (building it in-tree first if it is missing/stale and
+    nvcc is available).  Raises if the library cannot be loaded."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing:
+        from . import _build
+        if not _build.up_to_date():
+            try:
+                _build.build()
+            except Exception as e:  # no nvcc: only acceptable if a built .so exists
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(f"libpp.so missing and build failed: {e}") from e
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libpp.so not found at {LIB_PATH}; run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    u64, u32, vp, i64 = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_int64
+    P64 = ctypes.POINTER(ctypes.c_uint64)
+    st = ctypes.c_int
+    sig = {
+        "pp_partition_u64": ([vp, u64, u64, vp, P64], st),
+        "pp_partition_u32": ([vp, u64, u32, vp, P64], st),
+        "pp_partition_async_u64": ([vp, u64, u64, vp, vp], st),
+        "pp_partition_async_u32": ([vp, u64, u32, vp, vp], st),
+        "pp_quicksort_u64": ([vp, u64, vp], st),
+        "pp_quicksort_u32": ([vp, u64, vp], st),
+        "pp_partition_host_u64": ([vp, u64, u64, P64], st),
+        "pp_partition_host_u32": ([vp, u64, u32, P64], st),
+        "pp_quicksort_host_u64": ([vp, u64], st),
+        "pp_partition": ([vp, u64, u64], u64),
+        "pp_quicksort": ([vp, u64], st),
+        "pp_ss_groups_u64": ([vp, u64, u64, u64, vp, P64, P64, P64, P64], st),
+        "pp_ss_groups_u32": ([vp, u64, u32, u64, vp, P64, P64, P64, P64], st),
+        "pp_max_groups": ([], u64),
+        "pp_workspace_bytes": ([u64, ctypes.c_int, ctypes.c_int], u64),
+        "pp_last_aux_bytes": ([], u64),
+        "pp_last_stats": ([P64], st),
+        "pp_set_param": ([ctypes.c_char_p, i64], st),
+        "pp_get_param": ([ctypes.c_char_p], i64),
+        "pp_status_string": ([st], ctypes.c_char_p),
+        "pp_last_error": ([], ctypes.c_char_p),
+        "pp_launch_count": ([ctypes.c_int], u64),
+        "pp_timing": ([ctypes.c_int], None),
+        "pp_timing_read": ([ctypes.POINTER(ctypes.c_double)], st),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def header_symbols() -> list[str]:
+    """Every function the public header declares."""
+    with open(HEADER) as f:
+        txt = f.read()
+    return sorted(set(re.findall(r"\b(pp_[a-z0-9_]+)\s*\(", txt)))
+
+
+def _check(status: int, where: str):
+    if status != PP_OK:
+        raise PPError(status, where, load().pp_last_error().decode())
+
+
+def _stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _key_kind(t) -> str:
+    import torch
+    if not t.is_cuda:
+        raise ValueError("keys must be a CUDA tensor (use pp_partition_host_* for host arrays)")
+    if not t.is_contiguous():
+        raise ValueError("keys must be contiguous")
+    if t.dtype in (torch.int64, torch.uint64):
+        return "u64"
+    if t.dtype in (torch.int32, torch.uint32):
+        return "u32"
+    raise TypeError(f"unsupported key dtype {t.dtype}")
+
+
+def _pivot(p: int, kind: str) -> int:
+    p = int(p)
+    hi = (1 << 64) if kind == "u64" else (1 << 32)
+    if not 0 <= p < hi:
+        raise ValueError(f"pivot {p} out of range for {kind}")
+    return p
+
+
+def pp_partition_u64(keys, pivot: int, stream=None) -> int:
+    assert _key_kind(keys) == "u64"
+    out = ctypes.c_uint64(0)
+    _check(load().pp_partition_u64(keys.data_ptr(), keys.numel(), _pivot(pivot, "u64"), _stream_ptr(stream),
+                                   ctypes.byref(out)), "pp_partition_u64")
+    return int(out.value)
+
+
+def pp_partition_u32(keys, pivot: int, stream=None) -> int:
+    assert _key_kind(keys) == "u32"
+    out = ctypes.c_uint64(0)
+    _check(load().pp_partition_u32(keys.data_ptr(), keys.numel(), _pivot(pivot, "u32"), _stream_ptr(stream),
+                                   ctypes.byref(out)), "pp_partition_u32")
+    return int(out.value)
+
+
+def pp_partition_async_u64(keys, pivot: int, d_split, stream=None) -> None:
+    assert _key_kind(keys) == "u64" and d_split.is_cuda and d_split.numel() >= 1
+    _check(load().pp_partition_async_u64(keys.data_ptr(), keys.numel(), _pivot(pivot, "u64"), _stream_ptr(stream),
+                                         d_split.data_ptr()), "pp_partition_async_u64")
+
+
+def pp_partition_async_u32(keys, pivot: int, d_split, stream=None) -> None:
+    assert _key_kind(keys) == "u32" and d_split.is_cuda and d_split.numel() >= 1
+    _check(load().pp_partition_async_u32(keys.data_ptr(), keys.numel(), _pivot(pivot, "u32"), _stream_ptr(stream),
+                                         d_split.data_ptr()), "pp_partition_async_u32")
+
+
+def pp_quicksort_u64(keys, stream=None) -> None:
+    assert _key_kind(keys) == "u64"
+    _check(load().pp_quicksort_u64(keys.data_ptr(), keys.numel(), _stream_ptr(stream)), "pp_quicksort_u64")
+
+
+def pp_quicksort_u32(keys, stream=None) -> None:
+    assert _key_kind(keys) == "u32"
+    _check(load().pp_quicksort_u32(keys.data_ptr(), keys.numel(), _stream_ptr(stream)), "pp_quicksort_u32")
+
+
+def pp_partition(keys, pivot: int, stream=None) -> int:
+    return (pp_partition_u64 if _key_kind(keys) == "u64" else pp_partition_u32)(keys, pivot, stream)
+
+
+def pp_quicksort(keys, stream=None) -> None:
+    (pp_quicksort_u64 if _key_kind(keys) == "u64" else pp_quicksort_u32)(keys, stream)
+
+
+def pp_partition_host_u64(a: np.ndarray, pivot: int) -> int:
+    assert a.dtype == np.uint64 and a.flags["C_CONTIGUOUS"]
+    out = ctypes.c_uint64(0)
+    _check(load().pp_partition_host_u64(a.ctypes.data, a.size, _pivot(pivot, "u64"), ctypes.byref(out)),
+           "pp_partition_host_u64")
+    return int(out.value)
+
+
+def pp_partition_host_u32(a: np.ndarray, pivot: int) -> int:
+    assert a.dtype == np.uint32 and a.flags["C_CONTIGUOUS"]
+    out = ctypes.c_uint64(0)
+    _check(load().pp_partition_host_u32(a.ctypes.data, a.size, _pivot(pivot, "u32"), ctypes.byref(out)),
+           "pp_partition_host_u32")
+    return int(out.value)
+
+
+def pp_quicksort_host_u64(a: np.ndarray) -> None:
+    assert a.dtype == np.uint64 and a.flags["C_CONTIGUOUS"]
+    _check(load().pp_quicksort_host_u64(a.ctypes.data, a.size), "pp_quicksort_host_u64")
+
+
+def pp_ss_groups(keys, pivot: int, g: int = 0, stream=None):
+    """Run only the Smoothed Striding partial partition step; returns numpy
+    (T, vlo, vhi) per group and info = {g, head, n_lines, line_keys, seed}."""
+    kind = _key_kind(keys)
+    L = load()
+    cap = max(int(g), int(L.pp_max_groups()), 1)
+    T = np.zeros(cap, dtype=np.uint64)
+    vlo = np.zeros(cap, dtype=np.uint64)
+    vhi = np.zeros(cap, dtype=np.uint64)
+    info = np.zeros(6, dtype=np.uint64)
+    P = ctypes.POINTER(ctypes.c_uint64)
+    f = L.pp_ss_groups_u64 if kind == "u64" else L.pp_ss_groups_u32
+    _check(f(keys.data_ptr(), keys.numel(), _pivot(pivot, kind), int(g), _stream_ptr(stream),
+             T.ctypes.data_as(P), vlo.ctypes.data_as(P), vhi.ctypes.data_as(P), info.ctypes.data_as(P)),
+           "pp_ss_groups")
+    gg = int(info[0])
+    return T[:gg], vlo[:gg], vhi[:gg], {"g": gg, "head": int(info[1]), "n_lines": int(info[2]),
+                                        "line_keys": int(info[3]), "seed": int(info[4])}
+
+
+STAT_KEYS = ("n", "K", "W", "vmin", "vmax", "M", "g", "line_keys", "n_lines", "head", "aux_bytes", "path",
+             "nTasks")
+
+
+def pp_last_stats() -> dict:
+    out = (ctypes.c_uint64 * 13)()
+    _check(load().pp_last_stats(out), "pp_last_stats")
+    return dict(zip(STAT_KEYS, [int(v) for v in out]))
+
+
+def pp_set_param(name: str, value: int) -> None:
+    _check(load().pp_set_param(name.encode(), int(value)), "pp_set_param")
+
+
+def pp_get_param(name: str) -> int:
+    return int(load().pp_get_param(name.encode()))
+
+
+def pp_last_aux_bytes() -> int:
+    return int(load().pp_last_aux_bytes())
+
+
+def pp_workspace_bytes(n: int, key_bytes: int = 8, op: int = 0) -> int:
+    return int(load().pp_workspace_bytes(n, key_bytes, op))
+
+
+def pp_launch_count(reset: bool = False) -> int:
+    return int(load().pp_launch_count(1 if reset else 0))
+
+
+def pp_timing(enable: bool) -> None:
+    load().pp_timing(1 if enable else 0)
+
+
+def pp_timing_read() -> dict:
+    out = (ctypes.c_double * 4)()
+    _check(load().pp_timing_read(out), "pp_timing_read")
+    return {"calls": int(out[0]), "group_ms": out[1], "rest_ms": out[2], "total_ms": out[3]}
+
+
+DEFAULT_PARAMS = {"g": 0, "min_lines_per_group": 16, "small_n": 1 << 15, "path": 0, "tile": 0, "ranks": 0, "variant": 0,
+                  "leaf": 0, "qs_cta_max": 0}
+
+
+def reset_params() -> None:
+    for k, v in DEFAULT_PARAMS.items():
+        pp_set_param(k, v)

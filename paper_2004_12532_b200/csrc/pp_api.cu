@@ -1,0 +1,403 @@
+// pp_api.cu -- the C ABI (include/pp.h): argument checks, workspace, error
+// reporting, host-buffer variants.  Every compute step runs in the kernels of
+// pp_partition.cu / pp_quicksort.cu; there is no CPU fallback.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "pp_internal.h"
+
+namespace pp {
+
+uint64_t launch_count(int reset);
+uint64_t max_groups();
+void timing_enable(int on);
+int timing_read(double* out);
+
+static std::mutex g_mu;
+static std::string g_err;
+static Params g_params;
+static LastStats g_stats;
+static Ctl* g_last_ctl = nullptr;
+
+Params& params() { return g_params; }
+LastStats& last_stats() { return g_stats; }
+
+void set_error(const std::string& msg) { g_err = msg; }
+pp_status cuda_fail(cudaError_t e, const char* what) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return PP_E_CUDA;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// One growing device workspace.  Growth synchronises the stream first so an
+// in-flight call never loses its buffer.
+static void* g_ws = nullptr;
+static size_t g_ws_bytes = 0;
+void* workspace(size_t bytes, cudaStream_t st) {
+    if (bytes <= g_ws_bytes) return g_ws;
+    if (g_ws) {
+        cudaStreamSynchronize(st);
+        cudaDeviceSynchronize();
+        cudaFree(g_ws);
+        g_ws = nullptr;
+        g_ws_bytes = 0;
+    }
+    size_t want = bytes + (bytes >> 2);
+    if (cudaMalloc(&g_ws, want) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("workspace cudaMalloc failed");
+        return nullptr;
+    }
+    g_ws_bytes = want;
+    return g_ws;
+}
+
+// pinned host word for split readback
+static uint64_t* pinned_word() {
+    static uint64_t* p = nullptr;
+    if (!p && cudaMallocHost(&p, 64) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+    }
+    return p;
+}
+
+template <typename K>
+static pp_status check_device_keys(const K* keys, uint64_t n) {
+    if (n == 0) return PP_OK;
+    if (!keys) {
+        set_error("keys is NULL with n > 0");
+        return PP_E_INVAL;
+    }
+    if ((uintptr_t)keys % sizeof(K)) {
+        set_error("keys not aligned to the key size");
+        return PP_E_INVAL;
+    }
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, keys);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("keys is not a CUDA-visible pointer");
+        return PP_E_INVAL;
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) {
+        set_error("keys must be a device pointer (use the *_host variants for host memory)");
+        return PP_E_INVAL;
+    }
+    return PP_OK;
+}
+
+template <typename K>
+static pp_status partition_sync(K* keys, uint64_t n, K pivot, void* stream, uint64_t* split_out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!split_out) {
+        set_error("split_out is NULL");
+        return PP_E_INVAL;
+    }
+    pp_status s = check_device_keys(keys, n);
+    if (s != PP_OK) return s;
+    if (n == 0) {
+        *split_out = 0;
+        g_stats = LastStats();
+        return PP_OK;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    uint64_t* pw = pinned_word();
+    if (!pw) {
+        set_error("cudaMallocHost failed");
+        return PP_E_NOMEM;
+    }
+    Ctl* ctl = nullptr;
+    s = partition_device<K>(keys, n, pivot, st, nullptr, &ctl);
+    if (s != PP_OK) return s;
+    g_last_ctl = ctl;
+    cudaError_t e = cudaMemcpyAsync(pw, &ctl->K, sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "partition");
+    *split_out = *pw;
+    return PP_OK;
+}
+
+template <typename K>
+static pp_status partition_async(K* keys, uint64_t n, K pivot, void* stream, uint64_t* d_split) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    pp_status s = check_device_keys(keys, n);
+    if (s != PP_OK) return s;
+    if (!d_split) {
+        set_error("d_split is NULL");
+        return PP_E_INVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n == 0) {
+        cudaError_t e = cudaMemsetAsync(d_split, 0, sizeof(uint64_t), st);
+        return e == cudaSuccess ? PP_OK : cuda_fail(e, "memset");
+    }
+    Ctl* ctl = nullptr;
+    s = partition_device<K>(keys, n, pivot, st, d_split, &ctl);
+    g_last_ctl = ctl;
+    return s;
+}
+
+template <typename K>
+static pp_status quicksort_sync(K* keys, uint64_t n, void* stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    pp_status s = check_device_keys(keys, n);
+    if (s != PP_OK) return s;
+    if (n <= 1) return PP_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    s = quicksort_device<K>(keys, n, st);
+    if (s != PP_OK) return s;
+    cudaError_t e = cudaStreamSynchronize(st);
+    return e == cudaSuccess ? PP_OK : cuda_fail(e, "quicksort");
+}
+
+// host-buffer variants: library-owned device buffer, H2D, work, D2H
+static void* g_hbuf = nullptr;
+static size_t g_hbuf_bytes = 0;
+static cudaStream_t g_hstream = nullptr;
+static void* host_device_buffer(size_t bytes) {
+    if (!g_hstream) cudaStreamCreateWithFlags(&g_hstream, cudaStreamNonBlocking);
+    if (bytes <= g_hbuf_bytes) return g_hbuf;
+    if (g_hbuf) cudaFree(g_hbuf);
+    g_hbuf = nullptr;
+    g_hbuf_bytes = 0;
+    if (cudaMalloc(&g_hbuf, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    g_hbuf_bytes = bytes;
+    return g_hbuf;
+}
+
+template <typename K>
+static pp_status partition_host(K* host_keys, uint64_t n, K pivot, uint64_t* split_out) {
+    if (!split_out || (n > 0 && !host_keys)) {
+        set_error("NULL argument");
+        return PP_E_INVAL;
+    }
+    if (n == 0) {
+        *split_out = 0;
+        return PP_OK;
+    }
+    K* d;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        d = static_cast<K*>(host_device_buffer(n * sizeof(K)));
+        if (!d) {
+            set_error("device buffer allocation failed");
+            return PP_E_NOMEM;
+        }
+        cudaError_t e = cudaMemcpyAsync(d, host_keys, n * sizeof(K), cudaMemcpyHostToDevice, g_hstream);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D");
+    }
+    uint64_t split = 0;
+    pp_status s = partition_sync<K>(d, n, pivot, g_hstream, &split);
+    if (s != PP_OK) return s;
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaError_t e = cudaMemcpyAsync(host_keys, d, n * sizeof(K), cudaMemcpyDeviceToHost, g_hstream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g_hstream);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H");
+    *split_out = split;
+    return PP_OK;
+}
+
+template <typename K>
+static pp_status quicksort_host(K* host_keys, uint64_t n) {
+    if (n > 0 && !host_keys) {
+        set_error("NULL argument");
+        return PP_E_INVAL;
+    }
+    if (n <= 1) return PP_OK;
+    K* d;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        d = static_cast<K*>(host_device_buffer(n * sizeof(K)));
+        if (!d) {
+            set_error("device buffer allocation failed");
+            return PP_E_NOMEM;
+        }
+        cudaError_t e = cudaMemcpyAsync(d, host_keys, n * sizeof(K), cudaMemcpyHostToDevice, g_hstream);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D");
+    }
+    pp_status s = quicksort_sync<K>(d, n, g_hstream);
+    if (s != PP_OK) return s;
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaError_t e = cudaMemcpyAsync(host_keys, d, n * sizeof(K), cudaMemcpyDeviceToHost, g_hstream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g_hstream);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H");
+    return PP_OK;
+}
+
+template <typename K>
+static pp_status ss_groups(K* keys, uint64_t n, K pivot, uint64_t g, void* stream, uint64_t* T, uint64_t* vlo,
+                           uint64_t* vhi, uint64_t* info) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    pp_status s = check_device_keys(keys, n);
+    if (s != PP_OK) return s;
+    if (!T || !vlo || !vhi || !info) {
+        set_error("NULL output array");
+        return PP_E_INVAL;
+    }
+    return ss_groups_device<K>(keys, n, pivot, g, (cudaStream_t)stream, T, vlo, vhi, info);
+}
+
+}  // namespace pp
+
+using namespace pp;
+
+extern "C" {
+
+pp_status pp_partition_u64(uint64_t* keys, uint64_t n, uint64_t pivot, void* stream, uint64_t* split_out) {
+    return partition_sync<uint64_t>(keys, n, pivot, stream, split_out);
+}
+pp_status pp_partition_u32(uint32_t* keys, uint64_t n, uint32_t pivot, void* stream, uint64_t* split_out) {
+    return partition_sync<uint32_t>(keys, n, pivot, stream, split_out);
+}
+pp_status pp_partition_async_u64(uint64_t* keys, uint64_t n, uint64_t pivot, void* stream, uint64_t* d_split) {
+    return partition_async<uint64_t>(keys, n, pivot, stream, d_split);
+}
+pp_status pp_partition_async_u32(uint32_t* keys, uint64_t n, uint32_t pivot, void* stream, uint64_t* d_split) {
+    return partition_async<uint32_t>(keys, n, pivot, stream, d_split);
+}
+pp_status pp_quicksort_u64(uint64_t* keys, uint64_t n, void* stream) {
+    return quicksort_sync<uint64_t>(keys, n, stream);
+}
+pp_status pp_quicksort_u32(uint32_t* keys, uint64_t n, void* stream) {
+    return quicksort_sync<uint32_t>(keys, n, stream);
+}
+pp_status pp_partition_host_u64(uint64_t* host_keys, uint64_t n, uint64_t pivot, uint64_t* split_out) {
+    return partition_host<uint64_t>(host_keys, n, pivot, split_out);
+}
+pp_status pp_partition_host_u32(uint32_t* host_keys, uint64_t n, uint32_t pivot, uint64_t* split_out) {
+    return partition_host<uint32_t>(host_keys, n, pivot, split_out);
+}
+pp_status pp_quicksort_host_u64(uint64_t* host_keys, uint64_t n) { return quicksort_host<uint64_t>(host_keys, n); }
+
+uint64_t pp_partition(uint64_t* keys, uint64_t n, uint64_t pivot) {
+    uint64_t k = 0;
+    return pp_partition_u64(keys, n, pivot, nullptr, &k) == PP_OK ? k : UINT64_MAX;
+}
+pp_status pp_quicksort(uint64_t* keys, uint64_t n) { return pp_quicksort_u64(keys, n, nullptr); }
+
+pp_status pp_ss_groups_u64(uint64_t* keys, uint64_t n, uint64_t pivot, uint64_t g, void* stream, uint64_t* T,
+                           uint64_t* vlo, uint64_t* vhi, uint64_t* info) {
+    return ss_groups<uint64_t>(keys, n, pivot, g, stream, T, vlo, vhi, info);
+}
+pp_status pp_ss_groups_u32(uint32_t* keys, uint64_t n, uint32_t pivot, uint64_t g, void* stream, uint64_t* T,
+                           uint64_t* vlo, uint64_t* vhi, uint64_t* info) {
+    return ss_groups<uint32_t>(keys, n, pivot, g, stream, T, vlo, vhi, info);
+}
+uint64_t pp_max_groups(void) { return max_groups(); }
+
+uint64_t pp_workspace_bytes(uint64_t n, int key_bytes, int op) {
+    // tile/task arrays (<= 2^18 entries each side) + groups + control
+    uint64_t tiles = n / 4096 + 2, tasks = n / 8192 + 2;
+    if (tiles > (1u << 18) + 2) tiles = (1u << 18) + 2;
+    if (tasks > (1u << 18) + 2) tasks = (1u << 18) + 2;
+    uint64_t b = 24 * tiles + 16 * tasks + 24 * 4096 + 4096;
+    if (op == 1) b += (n / 1024 + 16) * 64;  // quicksort segment descriptors
+    (void)key_bytes;
+    return b;
+}
+uint64_t pp_last_aux_bytes(void) { return g_stats.aux_bytes; }
+
+pp_status pp_last_stats(uint64_t* out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!out) return PP_E_INVAL;
+    Ctl c;
+    memset(&c, 0, sizeof(c));
+    if (g_last_ctl) {
+        cudaError_t e = cudaMemcpy(&c, g_last_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(e, "stats");
+    }
+    const LastStats& S = g_stats;
+    uint64_t v[13] = {S.n, c.K, c.W, c.vmin, c.vmax, c.ML, S.g, S.line_keys, S.n_lines, S.head,
+                      S.aux_bytes, S.path, c.nTasks};
+    memcpy(out, v, sizeof(v));
+    if (c.err) {
+        set_error("device invariant check failed (misplaced counts differ)");
+        return PP_E_INTERNAL;
+    }
+    return PP_OK;
+}
+
+pp_status pp_set_param(const char* name, int64_t value) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!name) return PP_E_INVAL;
+    Params& P = g_params;
+    std::string k(name);
+    if (k == "g") P.g = value;
+    else if (k == "min_lines_per_group") P.min_lines_per_group = value;
+    else if (k == "small_n") P.small_n = value;
+    else if (k == "path") P.path = value;
+    else if (k == "tile") P.tile = value;
+    else if (k == "ranks") P.ranks = value;
+    else if (k == "seed") P.seed = (uint64_t)value;
+    else if (k == "leaf") P.leaf = value;
+    else if (k == "qs_cta_max") P.qs_cta_max = value;
+    else if (k == "variant") P.variant = value;
+    else {
+        set_error("unknown parameter " + k);
+        return PP_E_INVAL;
+    }
+    return PP_OK;
+}
+int64_t pp_get_param(const char* name) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!name) return INT64_MIN;
+    const Params& P = g_params;
+    std::string k(name);
+    if (k == "g") return P.g;
+    if (k == "min_lines_per_group") return P.min_lines_per_group;
+    if (k == "small_n") return P.small_n;
+    if (k == "path") return P.path;
+    if (k == "tile") return P.tile;
+    if (k == "ranks") return P.ranks;
+    if (k == "seed") return (int64_t)P.seed;
+    if (k == "leaf") return P.leaf;
+    if (k == "qs_cta_max") return P.qs_cta_max;
+    if (k == "variant") return P.variant;
+    return INT64_MIN;
+}
+
+const char* pp_status_string(pp_status s) {
+    switch (s) {
+        case PP_OK: return "PP_OK";
+        case PP_E_INVAL: return "PP_E_INVAL";
+        case PP_E_CUDA: return "PP_E_CUDA";
+        case PP_E_NOMEM: return "PP_E_NOMEM";
+        case PP_E_NCCL: return "PP_E_NCCL";
+        case PP_E_INTERNAL: return "PP_E_INTERNAL";
+    }
+    return "PP_E_UNKNOWN";
+}
+const char* pp_last_error(void) { return g_err.c_str(); }
+uint64_t pp_launch_count(int reset) { return launch_count(reset); }
+void pp_timing(int enable) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    timing_enable(enable);
+}
+pp_status pp_timing_read(double* out4) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!out4) return PP_E_INVAL;
+    int r = timing_read(out4);
+    if (r) {
+        set_error("timing events incomplete or failed");
+        return r == 1 ? PP_E_INVAL : PP_E_CUDA;
+    }
+    return PP_OK;
+}
+
+}  // extern "C"

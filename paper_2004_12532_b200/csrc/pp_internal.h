@@ -1,0 +1,74 @@
+// pp_internal.h -- host-side internals shared by the C-ABI (pp_api.cu), the
+// partition driver (pp_partition.cu) and the quicksort driver (pp_quicksort.cu).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <cuda_runtime.h>
+
+#include "../../include/pp.h"
+
+namespace pp {
+
+// Per-segment control block, resident in device workspace.  Written by the
+// window-reduce kernel, read by the cleanup kernels (no host round trip).
+struct Ctl {
+    uint64_t n;          // segment length
+    uint64_t K;          // split = #keys < pivot in the segment
+    uint64_t W;          // |D|, size of the dirty set
+    uint64_t Kv;         // #dirty positions < K
+    uint64_t ds[3];      // dirty intervals [ds, ds+dl), sorted, disjoint
+    uint64_t dl[3];
+    uint64_t vmin, vmax; // window of the partial partition step (absolute)
+    uint64_t ML, MR;     // misplaced falses left of K / trues right of K (equal)
+    uint64_t nL, nR;     // cleanup tiles on each side
+    uint64_t nTasks;     // rank-matched swap tasks
+    uint64_t tile;       // tile size (keys) of the cleanup count
+    uint64_t R;          // ranks per swap task
+    uint64_t err;        // nonzero = internal invariant violated
+};
+
+// Per-group output of the Smoothed Striding partial partition step.
+struct GroupOut {
+    uint64_t T;    // #predecessors in the group
+    uint64_t vlo;  // first successor position (region-relative), or sentinel
+    uint64_t vhi;
+};
+
+struct Params {
+    int64_t g = 0;                 // 0 = auto
+    int64_t min_lines_per_group = 16;
+    int64_t small_n = 1 << 15;     // below: single-CTA path
+    int64_t path = 0;              // 0 auto, 1 single-CTA, 2 smoothed-striding, 3 cleanup-only
+    int64_t tile = 0;              // 0 = auto
+    int64_t ranks = 0;             // 0 = auto (ranks per swap task)
+    uint64_t seed = 0x5EEDC0DE2004ULL;  // Smoothed Striding offset seed (fixed => deterministic)
+    int64_t leaf = 0;              // quicksort: 0 = auto smem leaf size
+    int64_t qs_cta_max = 0;        // quicksort: 0 = auto segment size handled by one CTA
+    int64_t variant = 0;           // group-kernel configuration (pp_partition.cu VariantCfg)
+};
+Params& params();
+
+struct LastStats {
+    uint64_t n = 0, K = 0, W = 0, vmin = 0, vmax = 0, M = 0, g = 0, line_keys = 0;
+    uint64_t n_lines = 0, head = 0, aux_bytes = 0, path = 0, nTasks = 0;
+};
+LastStats& last_stats();
+
+void set_error(const std::string& msg);
+pp_status cuda_fail(cudaError_t e, const char* what);
+
+// device workspace (grows; one per process / device)
+void* workspace(size_t bytes, cudaStream_t st);
+int sm_count();
+
+template <typename K>
+pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split, Ctl** ctl_out);
+
+template <typename K>
+pp_status ss_groups_device(K* keys, uint64_t n, K pivot, uint64_t g, cudaStream_t st, uint64_t* T_host,
+                           uint64_t* vlo_host, uint64_t* vhi_host, uint64_t* info_host);
+
+template <typename K>
+pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st);
+
+}  // namespace pp

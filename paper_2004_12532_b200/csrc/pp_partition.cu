@@ -1,0 +1,624 @@
+// pp_partition.cu -- B200 (sm_100a) in-place parallel partition.
+//
+// Pipeline for one array:
+//   K3 ss_group_kernel   Smoothed Striding Partial Partition Step
+//                        (Fig. 3): one CTA
+//                        per group U_i, a two-ended in-place partition of the
+//                        group's lines staged through shared memory by the TMA
+//                        bulk-copy engine; every line read once, written once.
+//   K4 window_reduce     K = sum T_i, v_min, v_max and the
+//                        dirty set D = head U [v_min,v_max) U tail.
+//   K1 tile_count        per-tile misplaced counts over D (PAPER.md:288-291 D
+//                        array, counted per tile like the paper's per-64/4096
+//                        chunk counts PAPER.md:1443-1450, 1479-1486).
+//   K2 tile_scan         deterministic exclusive scan of the tile counts
+//                        (PAPER.md:288-297, 1488-1496).
+//   K5a locate / K5b swap  rank-matched cleanup: the r-th misplaced
+//                        successor left of K is swapped with the r-th
+//                        misplaced predecessor right of K; each pair owned by
+//                        exactly one CTA (EREW).
+// No atomics anywhere; all reductions are fixed-order.
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "pp_engine.cuh"
+
+namespace pp {
+
+template <typename C>
+__global__ void __launch_bounds__(C::NT) ss_group_kernel(typename C::Key* __restrict__ region, uint64_t n_lines,
+                                                         uint32_t g, uint64_t seed, typename C::Key pivot,
+                                                         GroupOut* __restrict__ out) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    ss_group_engine<C>(region, n_lines, g, blockIdx.x, seed, pivot, out + blockIdx.x, smem);
+}
+
+// ===========================================================================
+// K4: window reduction (1 CTA).  K = head_T + sum T_i + tail_T.
+// ===========================================================================
+template <typename K>
+__global__ void __launch_bounds__(256) window_reduce_kernel(const K* __restrict__ keys, uint64_t n, uint64_t h,
+                                                            uint64_t n_lines, uint32_t LK,
+                                                            const GroupOut* __restrict__ go, uint32_t g,
+                                                            K pivot, Ctl* __restrict__ ctl, uint64_t tile,
+                                                            uint64_t R, uint64_t* __restrict__ d_split) {
+    __shared__ uint64_t sT[8], sMin[8], sMax[8], sHT[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t region_end = n_lines * LK;
+    uint64_t T = 0, vmin = region_end, vmax = 0, ht = 0;
+    for (uint32_t i = tid; i < g; i += 256) {
+        GroupOut o = go[i];
+        T += o.T;
+        vmin = o.vlo < vmin ? o.vlo : vmin;
+        vmax = o.vhi > vmax ? o.vhi : vmax;
+    }
+    // head [0,h) and tail [h + region_end, n) predecessors
+    const uint64_t tail0 = h + region_end;
+    for (uint64_t x = tid; x < h; x += 256) ht += is_pred(keys[x], pivot) ? 1 : 0;
+    for (uint64_t x = tail0 + tid; x < n; x += 256) ht += is_pred(keys[x], pivot) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T += __shfl_xor_sync(0xffffffffu, T, o);
+        ht += __shfl_xor_sync(0xffffffffu, ht, o);
+        uint64_t a = __shfl_xor_sync(0xffffffffu, vmin, o);
+        uint64_t b = __shfl_xor_sync(0xffffffffu, vmax, o);
+        vmin = a < vmin ? a : vmin;
+        vmax = b > vmax ? b : vmax;
+    }
+    if (lane == 0) {
+        sT[warp] = T;
+        sMin[warp] = vmin;
+        sMax[warp] = vmax;
+        sHT[warp] = ht;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < 8; ++w) {
+            T += sT[w];
+            ht += sHT[w];
+            vmin = sMin[w] < vmin ? sMin[w] : vmin;
+            vmax = sMax[w] > vmax ? sMax[w] : vmax;
+        }
+        const uint64_t Ksplit = T + ht;
+        uint64_t a[3], b[3];
+        a[0] = 0; b[0] = h;                                // head
+        const uint64_t lo = h + vmin, hi = h + vmax;       // partial-partition window
+        a[1] = lo < Ksplit ? lo : Ksplit;
+        b[1] = hi > Ksplit ? hi : Ksplit;
+        if (vmin > vmax) { a[1] = b[1] = 0; }             // no non-empty group: no window
+        a[2] = tail0; b[2] = n;                            // tail
+        finish_ctl(ctl, n, Ksplit, a, b, tile, R);
+        ctl->vmin = lo;
+        ctl->vmax = hi;
+        if (d_split) *d_split = Ksplit;
+    }
+}
+
+// Cleanup-only path (SURVEY §7 minimum slice / ablation): K by a count pass.
+template <typename K>
+__global__ void __launch_bounds__(256) count_kernel(const K* __restrict__ keys, uint64_t n, K pivot,
+                                                    uint64_t* __restrict__ partial) {
+    __shared__ uint64_t s[8];
+    uint64_t c = 0;
+    for (uint64_t x = (uint64_t)blockIdx.x * 256 + threadIdx.x; x < n; x += (uint64_t)gridDim.x * 256)
+        c += is_pred(keys[x], pivot) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) c += s[w];
+        partial[blockIdx.x] = c;
+    }
+}
+__global__ void __launch_bounds__(256) count_finish_kernel(const uint64_t* __restrict__ partial, int np,
+                                                           uint64_t n, Ctl* __restrict__ ctl, uint64_t tile,
+                                                           uint64_t R, uint64_t* __restrict__ d_split) {
+    if (threadIdx.x == 0) {
+        uint64_t K = 0;
+        for (int i = 0; i < np; ++i) K += partial[i];
+        uint64_t a[3] = {0, n, n}, b[3] = {n, n, n};
+        finish_ctl(ctl, n, K, a, b, tile, R);
+        ctl->vmin = 0;
+        ctl->vmax = n;
+        if (d_split) *d_split = K;
+    }
+}
+
+// ===========================================================================
+// K1: tile counts over the dirty set (grid-stride, fixed mapping).
+//   left tiles  [t*T, min((t+1)T, Kv))      count successors (misplaced)
+//   right tiles [Kv + t*T, min(.., W))       count predecessors (misplaced)
+// 8 independent loads per thread in flight.
+// ===========================================================================
+template <typename K>
+__global__ void __launch_bounds__(256) tile_count_kernel(const K* __restrict__ keys, const Ctl* __restrict__ ctl,
+                                                         K pivot, uint32_t* __restrict__ cntL,
+                                                         uint32_t* __restrict__ cntR) {
+    __shared__ uint32_t s[8];
+    const Dirty d = load_dirty(ctl);
+    const uint64_t Kv = ctl->Kv, W = ctl->W, T = ctl->tile, nL = ctl->nL, nR = ctl->nR;
+    for (uint64_t t = blockIdx.x; t < nL + nR; t += gridDim.x) {
+        const bool left = t < nL;
+        const uint64_t u0 = left ? t * T : Kv + (t - nL) * T;
+        const uint64_t u1 = left ? min(u0 + T, Kv) : min(u0 + T, W);
+        uint32_t c = 0;
+        for (uint64_t ub = u0; ub < u1; ub += 8 * 256) {
+            K x[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint64_t u = ub + (uint64_t)k * 256 + threadIdx.x;
+                x[k] = u < u1 ? keys[vreal(d, u)] : (left ? (K)0 : pivot);  // neutral fill
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint64_t u = ub + (uint64_t)k * 256 + threadIdx.x;
+                const bool p = is_pred(x[k], pivot);
+                c += (u < u1 && (left ? !p : p)) ? 1u : 0u;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < 8; ++w) tot += s[w];
+            if (left) cntL[t] = tot; else cntR[t - nL] = tot;
+        }
+        __syncthreads();
+    }
+}
+
+// ===========================================================================
+// K2: exclusive scan of the tile counts (1 CTA, 1024 threads, fixed order).
+// ===========================================================================
+__device__ uint64_t block_exclusive_scan_1024(uint64_t v, uint64_t* sw, uint64_t& total) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sw[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t w = sw[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        sw[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    total = sw[31];
+    const uint64_t wpre = warp > 0 ? sw[warp - 1] : 0;
+    __syncthreads();
+    return wpre + x - v;
+}
+
+__global__ void __launch_bounds__(1024) tile_scan_kernel(Ctl* __restrict__ ctl, const uint32_t* __restrict__ cntL,
+                                                         const uint32_t* __restrict__ cntR,
+                                                         uint64_t* __restrict__ PL, uint64_t* __restrict__ PR) {
+    __shared__ uint64_t sw[32];
+    const uint64_t nL = ctl->nL, nR = ctl->nR;
+    uint64_t carry = 0;
+    for (uint64_t b = 0; b < nL; b += 1024) {
+        const uint64_t i = b + threadIdx.x;
+        uint64_t tot;
+        const uint64_t ex = block_exclusive_scan_1024(i < nL ? cntL[i] : 0, sw, tot);
+        if (i < nL) PL[i] = carry + ex;
+        carry += tot;
+    }
+    const uint64_t ML = carry;
+    carry = 0;
+    for (uint64_t b = 0; b < nR; b += 1024) {
+        const uint64_t i = b + threadIdx.x;
+        uint64_t tot;
+        const uint64_t ex = block_exclusive_scan_1024(i < nR ? cntR[i] : 0, sw, tot);
+        if (i < nR) PR[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) {
+        ctl->ML = ML;
+        ctl->MR = carry;
+        if (ML != carry) ctl->err = 1;  // #misplaced successors must equal #misplaced predecessors
+        const uint64_t M = ML < carry ? ML : carry;
+        ctl->nTasks = (M + ctl->R - 1) / ctl->R;
+    }
+}
+
+// ===========================================================================
+// K5a: locate the start of every swap task (one CTA per task, grid-stride).
+// posL[j] = virtual index of the (jR)-th misplaced successor in [0,Kv);
+// posR[j] = virtual index of the (jR)-th misplaced predecessor in [Kv,W);
+// posL[nTasks] = Kv, posR[nTasks] = W (sentinels).
+// ===========================================================================
+__device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__ a, uint64_t n, uint64_t x) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(SW_NT) locate_kernel(const K* __restrict__ keys, Ctl* __restrict__ ctl, K pivot,
+                                                       const uint64_t* __restrict__ PL,
+                                                       const uint64_t* __restrict__ PR,
+                                                       uint64_t* __restrict__ posL, uint64_t* __restrict__ posR) {
+    __shared__ WalkBuf<K> wb;
+    const Dirty d = load_dirty(ctl);
+    const uint64_t Kv = ctl->Kv, W = ctl->W, T = ctl->tile, nL = ctl->nL, nR = ctl->nR, R = ctl->R;
+    const uint64_t nTasks = ctl->nTasks;
+    for (uint64_t j = blockIdx.x; j <= nTasks; j += gridDim.x) {
+        uint64_t pl, pr;
+        if (j == nTasks) {
+            pl = Kv;
+            pr = W;
+        } else {
+            const uint64_t r = j * R;
+            const uint64_t tl = upper_bound_u64(PL, nL, r) - 1;
+            pl = select_item<K>(keys, d, pivot, false, tl * T, min(tl * T + T, Kv), r - PL[tl], wb);
+            const uint64_t tr = upper_bound_u64(PR, nR, r) - 1;
+            pr = select_item<K>(keys, d, pivot, true, Kv + tr * T, min(Kv + tr * T + T, W), r - PR[tr], wb);
+        }
+        if (threadIdx.x == 0) {
+            posL[j] = pl;
+            posR[j] = pr;
+        }
+    }
+}
+
+// ===========================================================================
+// K5b: rank-matched swap, one CTA per task (grid-stride).
+// ===========================================================================
+template <typename K>
+__global__ void __launch_bounds__(SW_NT) swap_kernel(K* __restrict__ keys, const Ctl* __restrict__ ctl, K pivot,
+                                                     const uint64_t* __restrict__ posL,
+                                                     const uint64_t* __restrict__ posR) {
+    __shared__ WalkBuf<K> wb;
+    const Dirty d = load_dirty(ctl);
+    const uint64_t nTasks = ctl->nTasks, R = ctl->R, M = ctl->ML;
+    for (uint64_t j = blockIdx.x; j < nTasks; j += gridDim.x) {
+        const uint64_t pairs = min(R, M - j * R);
+        walk_swap<K>(keys, d, pivot, posL[j], posL[j + 1], posR[j], posR[j + 1], pairs, wb);
+    }
+}
+
+// ===========================================================================
+// Single-CTA path for small n: count, then one walk over [0,K) x [K,n).
+// ===========================================================================
+template <typename K>
+__global__ void __launch_bounds__(SW_NT) small_partition_kernel(K* __restrict__ keys, uint64_t n, K pivot,
+                                                                Ctl* __restrict__ ctl,
+                                                                uint64_t* __restrict__ d_split) {
+    __shared__ WalkBuf<K> wb;
+    __shared__ uint64_t sK[SW_NT / 32];
+    uint64_t c = 0;
+    for (uint64_t x = threadIdx.x; x < n; x += SW_NT) c += is_pred(keys[x], pivot) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) sK[threadIdx.x >> 5] = c;
+    __syncthreads();
+    uint64_t Ksplit = 0;
+    for (int w = 0; w < SW_NT / 32; ++w) Ksplit += sK[w];
+    Dirty d;
+    d.s[0] = 0; d.l[0] = n;
+    d.s[1] = d.s[2] = n; d.l[1] = d.l[2] = 0;
+    walk_swap<K>(keys, d, pivot, 0, Ksplit, Ksplit, n, ~0ull, wb);
+    if (threadIdx.x == 0) {
+        if (ctl) {
+            uint64_t a[3] = {0, n, n}, b[3] = {n, n, n};
+            finish_ctl(ctl, n, Ksplit, a, b, 1, 1);
+            ctl->vmin = 0;
+            ctl->vmax = n;
+        }
+        if (d_split) *d_split = Ksplit;
+    }
+}
+
+// ===========================================================================
+// Host driver.
+// ===========================================================================
+static uint64_t g_launches = 0;
+uint64_t launch_count(int reset) {
+    uint64_t v = g_launches;
+    if (reset) g_launches = 0;
+    return v;
+}
+void note_launches(uint64_t k) { g_launches += k; }
+
+// Optional per-call phase timing with CUDA events recorded on the launch
+// stream (bench.py's roofline: the group kernel's live duration).
+static bool g_timing = false;
+static std::vector<cudaEvent_t> g_ev_pool;
+static size_t g_ev_used = 0;
+static cudaEvent_t timing_event() {
+    if (g_ev_used == g_ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        g_ev_pool.push_back(e);
+    }
+    return g_ev_pool[g_ev_used++];
+}
+static void timing_mark(cudaStream_t st) {
+    if (g_timing) cudaEventRecord(timing_event(), st);
+}
+void timing_enable(int on) {
+    g_timing = on != 0;
+    g_ev_used = 0;
+}
+// out = {calls, group_ms, rest_ms, total_ms}; events come in triples per call
+int timing_read(double* out) {
+    out[0] = out[1] = out[2] = out[3] = 0;
+    if (g_ev_used % 3) return 1;
+    for (size_t i = 0; i + 2 < g_ev_used; i += 3) {
+        float a = 0, b = 0;
+        if (cudaEventSynchronize(g_ev_pool[i + 2]) != cudaSuccess) return 2;
+        cudaEventElapsedTime(&a, g_ev_pool[i], g_ev_pool[i + 1]);
+        cudaEventElapsedTime(&b, g_ev_pool[i + 1], g_ev_pool[i + 2]);
+        out[0] += 1;
+        out[1] += a;
+        out[2] += b;
+        out[3] += a + b;
+    }
+    g_ev_used = 0;
+    return 0;
+}
+
+static uint64_t pow2ceil(uint64_t x) {
+    uint64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// ---------------------------------------------------------------------------
+// Group-kernel variants (line size, threads, prefetch depth, store path),
+// selectable with pp_set_param("variant", v) for tuning; 0 is the default.
+// ---------------------------------------------------------------------------
+template <typename C>
+static int occupancy_of() {
+    static int occ = -1;
+    if (occ < 0) {
+        cudaFuncSetAttribute(ss_group_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ss_group_kernel<C>, C::NT, C::SMEM);
+        occ = o > 0 ? o : 1;
+    }
+    return occ;
+}
+
+struct VariantInfo {
+    uint64_t LK;
+    int occ;
+};
+
+template <typename K, int V>
+struct VariantCfg;
+template <typename K> struct VariantCfg<K, 0> { using type = GroupCfg<K>; };
+template <typename K> struct VariantCfg<K, 1> { using type = GroupCfgT<K, 8192, 256, 4, false>; };
+template <typename K> struct VariantCfg<K, 2> { using type = GroupCfgT<K, 16384, 512, 3, true>; };
+template <typename K> struct VariantCfg<K, 3> { using type = GroupCfgT<K, 4096, 128, 6, true>; };
+template <typename K> struct VariantCfg<K, 4> { using type = GroupCfgT<K, 8192, 512, 4, true>; };
+template <typename K> struct VariantCfg<K, 5> { using type = GroupCfgT<K, 4096, 256, 8, true>; };
+template <typename K> struct VariantCfg<K, 6> { using type = GroupCfgT<K, 8192, 256, 6, true>; };
+constexpr int N_VARIANTS = 7;
+
+template <typename K, int V>
+static VariantInfo variant_info_t() {
+    using C = typename VariantCfg<K, V>::type;
+    return {(uint64_t)C::LK, occupancy_of<C>()};
+}
+template <typename K>
+static VariantInfo variant_info(int v) {
+    switch (v) {
+        case 1: return variant_info_t<K, 1>();
+        case 2: return variant_info_t<K, 2>();
+        case 3: return variant_info_t<K, 3>();
+        case 4: return variant_info_t<K, 4>();
+        case 5: return variant_info_t<K, 5>();
+        case 6: return variant_info_t<K, 6>();
+        default: return variant_info_t<K, 0>();
+    }
+}
+template <typename K, int V>
+static void launch_group_t(K* region, uint64_t n_lines, uint32_t g, uint64_t seed, K pivot, GroupOut* out,
+                           cudaStream_t st) {
+    using C = typename VariantCfg<K, V>::type;
+    occupancy_of<C>();
+    ss_group_kernel<C><<<g, C::NT, C::SMEM, st>>>(region, n_lines, g, seed, pivot, out);
+}
+template <typename K>
+static void launch_group(int v, K* region, uint64_t n_lines, uint32_t g, uint64_t seed, K pivot, GroupOut* out,
+                         cudaStream_t st) {
+    switch (v) {
+        case 1: launch_group_t<K, 1>(region, n_lines, g, seed, pivot, out, st); break;
+        case 2: launch_group_t<K, 2>(region, n_lines, g, seed, pivot, out, st); break;
+        case 3: launch_group_t<K, 3>(region, n_lines, g, seed, pivot, out, st); break;
+        case 4: launch_group_t<K, 4>(region, n_lines, g, seed, pivot, out, st); break;
+        case 5: launch_group_t<K, 5>(region, n_lines, g, seed, pivot, out, st); break;
+        case 6: launch_group_t<K, 6>(region, n_lines, g, seed, pivot, out, st); break;
+        default: launch_group_t<K, 0>(region, n_lines, g, seed, pivot, out, st); break;
+    }
+}
+
+static int cur_variant() {
+    const int v = (int)params().variant;
+    return (v >= 0 && v < N_VARIANTS) ? v : 0;
+}
+
+struct Layout {
+    size_t ctl, gout, cntL, cntR, PL, PR, posL, posR, partial, total;
+};
+
+static Layout make_layout(uint64_t g, uint64_t maxTiles, uint64_t maxTasks, uint64_t nPartial) {
+    Layout L;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = o;
+        o += (bytes + 255) & ~size_t(255);
+        return at;
+    };
+    L.ctl = take(sizeof(Ctl));
+    L.gout = take(sizeof(GroupOut) * std::max<uint64_t>(g, 1));
+    L.cntL = take(4 * maxTiles);
+    L.cntR = take(4 * maxTiles);
+    L.PL = take(8 * maxTiles);
+    L.PR = take(8 * maxTiles);
+    L.posL = take(8 * (maxTasks + 1));
+    L.posR = take(8 * (maxTasks + 1));
+    L.partial = take(8 * nPartial);
+    L.total = o;
+    return L;
+}
+
+// Cleanup geometry: tile T and ranks-per-task R grow with n so that the
+// tile and task arrays stay <= 2^18 entries (aux memory o(n)).
+static void cleanup_geometry(uint64_t n, uint64_t& tile, uint64_t& R, uint64_t& maxTiles, uint64_t& maxTasks) {
+    const Params& P = params();
+    const uint64_t scale = pow2ceil((n + (1u << 18) - 1) >> 18);
+    tile = P.tile > 0 ? (uint64_t)P.tile : std::max<uint64_t>(2048, scale);
+    R = P.ranks > 0 ? (uint64_t)P.ranks : std::max<uint64_t>(1024, scale);
+    maxTiles = n / tile + 2;
+    maxTasks = n / 2 / R + 2;
+}
+
+template <typename K>
+static uint64_t choose_groups(uint64_t n_lines, int occ) {
+    const Params& P = params();
+    if (P.g > 0) return std::min<uint64_t>((uint64_t)P.g, std::max<uint64_t>(n_lines, 1));
+    const uint64_t cap = (uint64_t)sm_count() * occ;
+    uint64_t g = n_lines / (uint64_t)std::max<int64_t>(P.min_lines_per_group, 1);
+    return std::max<uint64_t>(1, std::min(g, cap));
+}
+
+template <typename K>
+pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split, Ctl** ctl_out) {
+    const Params& P = params();
+    const int variant = cur_variant();
+    const VariantInfo vi = variant_info<K>(variant);
+    const uint64_t LK = vi.LK;
+    LastStats& S = last_stats();
+    S = LastStats();
+    S.n = n;
+    S.line_keys = LK;
+    const uint64_t addr = (uint64_t)(uintptr_t)keys;
+    uint64_t h = ((16 - (addr & 15)) & 15) / sizeof(K);
+    if (h > n) h = n;
+    const uint64_t n_lines = (n - h) / LK;
+
+    int path = (int)P.path;
+    if (path == 0) path = (n < (uint64_t)P.small_n || n_lines < 2) ? 1 : 2;
+    if (path == 2 && n_lines == 0) path = 1;
+    S.path = path;
+
+    uint64_t tile, R, maxTiles, maxTasks;
+    cleanup_geometry(n, tile, R, maxTiles, maxTasks);
+    const int grid_cleanup = sm_count() * 4;
+    const uint64_t g = path == 2 ? choose_groups<K>(n_lines, vi.occ) : 0;
+    const int nPartial = sm_count() * 2;
+    Layout L = make_layout(g, path == 1 ? 1 : maxTiles, path == 1 ? 1 : maxTasks, nPartial);
+    unsigned char* ws = static_cast<unsigned char*>(workspace(L.total, st));
+    if (!ws) return PP_E_NOMEM;
+    Ctl* ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
+    if (ctl_out) *ctl_out = ctl;
+    S.g = g;
+    S.head = h;
+    S.n_lines = n_lines;
+    S.aux_bytes = L.total;
+
+    timing_mark(st);
+    if (path == 1) {
+        small_partition_kernel<K><<<1, SW_NT, 0, st>>>(keys, n, pivot, ctl, d_split);
+        note_launches(1);
+        timing_mark(st);
+    } else {
+        if (path == 2) {
+            GroupOut* gout = reinterpret_cast<GroupOut*>(ws + L.gout);
+            launch_group<K>(variant, keys + h, n_lines, (uint32_t)g, P.seed, pivot, gout, st);
+            timing_mark(st);
+            window_reduce_kernel<K><<<1, 256, 0, st>>>(keys, n, h, n_lines, (uint32_t)LK, gout, (uint32_t)g, pivot,
+                                                       ctl, tile, R, d_split);
+            note_launches(2);
+        } else {
+            uint64_t* partial = reinterpret_cast<uint64_t*>(ws + L.partial);
+            count_kernel<K><<<nPartial, 256, 0, st>>>(keys, n, pivot, partial);
+            count_finish_kernel<<<1, 32, 0, st>>>(partial, nPartial, n, ctl, tile, R, d_split);
+            note_launches(2);
+            timing_mark(st);
+        }
+        uint32_t* cntL = reinterpret_cast<uint32_t*>(ws + L.cntL);
+        uint32_t* cntR = reinterpret_cast<uint32_t*>(ws + L.cntR);
+        uint64_t* PL = reinterpret_cast<uint64_t*>(ws + L.PL);
+        uint64_t* PR = reinterpret_cast<uint64_t*>(ws + L.PR);
+        uint64_t* posL = reinterpret_cast<uint64_t*>(ws + L.posL);
+        uint64_t* posR = reinterpret_cast<uint64_t*>(ws + L.posR);
+        tile_count_kernel<K><<<grid_cleanup, 256, 0, st>>>(keys, ctl, pivot, cntL, cntR);
+        tile_scan_kernel<<<1, 1024, 0, st>>>(ctl, cntL, cntR, PL, PR);
+        locate_kernel<K><<<grid_cleanup, SW_NT, 0, st>>>(keys, ctl, pivot, PL, PR, posL, posR);
+        swap_kernel<K><<<grid_cleanup, SW_NT, 0, st>>>(keys, ctl, pivot, posL, posR);
+        note_launches(4);
+    }
+    timing_mark(st);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "partition launch");
+    return PP_OK;
+}
+
+template <typename K>
+pp_status ss_groups_device(K* keys, uint64_t n, K pivot, uint64_t g_req, cudaStream_t st, uint64_t* T_host,
+                           uint64_t* vlo_host, uint64_t* vhi_host, uint64_t* info) {
+    const int variant = cur_variant();
+    const VariantInfo vi = variant_info<K>(variant);
+    const uint64_t addr = (uint64_t)(uintptr_t)keys;
+    uint64_t h = ((16 - (addr & 15)) & 15) / sizeof(K);
+    if (h > n) h = n;
+    const uint64_t n_lines = (n - h) / vi.LK;
+    const uint64_t g = g_req > 0 ? g_req : choose_groups<K>(n_lines, vi.occ);
+    info[0] = g;
+    info[1] = h;
+    info[2] = n_lines;
+    info[3] = vi.LK;
+    info[4] = params().seed;
+    info[5] = (uint64_t)variant;
+    if (n_lines == 0) return PP_OK;
+    GroupOut* gout = static_cast<GroupOut*>(workspace(sizeof(GroupOut) * g, st));
+    if (!gout) return PP_E_NOMEM;
+    launch_group<K>(variant, keys + h, n_lines, (uint32_t)g, params().seed, pivot, gout, st);
+    note_launches(1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "ss_group launch");
+    std::vector<GroupOut> host(g);
+    e = cudaMemcpyAsync(host.data(), gout, sizeof(GroupOut) * g, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "ss_group readback");
+    for (uint64_t i = 0; i < g; ++i) {
+        T_host[i] = host[i].T;
+        vlo_host[i] = host[i].vlo;
+        vhi_host[i] = host[i].vhi;
+    }
+    return PP_OK;
+}
+
+uint64_t max_groups() {
+    int occ = 1;
+    for (int v = 0; v < N_VARIANTS; ++v) {
+        occ = std::max(occ, variant_info<uint64_t>(v).occ);
+        occ = std::max(occ, variant_info<uint32_t>(v).occ);
+    }
+    return (uint64_t)sm_count() * (uint64_t)occ;
+}
+
+template pp_status partition_device<uint64_t>(uint64_t*, uint64_t, uint64_t, cudaStream_t, uint64_t*, Ctl**);
+template pp_status partition_device<uint32_t>(uint32_t*, uint64_t, uint32_t, cudaStream_t, uint64_t*, Ctl**);
+template pp_status ss_groups_device<uint64_t>(uint64_t*, uint64_t, uint64_t, uint64_t, cudaStream_t, uint64_t*,
+                                              uint64_t*, uint64_t*, uint64_t*);
+template pp_status ss_groups_device<uint32_t>(uint32_t*, uint64_t, uint32_t, uint64_t, cudaStream_t, uint64_t*,
+                                              uint64_t*, uint64_t*, uint64_t*);
+
+}  // namespace pp

@@ -1,0 +1,374 @@
+// pp_quicksort.cu -- in-place quicksort layered on the partition
+// (§5 "Example Application: A Full Quicksort").
+//
+// The paper runs the parallel partition at the top levels of the recursion
+// and a serial partition once subproblems are small.
+// The GPU analogue is a breadth-first level loop:
+//   - big segments (>= qs_big keys): the full multi-CTA partition pipeline of
+//     pp_partition.cu, one segment at a time;
+//   - mid segments: ONE launch for all of them: the Smoothed Striding group
+//     kernel with (segment, group) tasks, then one CTA per segment reduces its
+//     groups and cleans its (small) window by the rank-matched walk;
+//   - leaves (<= leaf keys): sorted entirely in shared memory (bitonic
+//     network), one CTA per leaf, all leaves in one launch at the end.
+// Pivot: median of A[lo], A[lo+(len-1)/2], A[hi-1]; split by x < p; when that
+// split is empty (p is the segment minimum) the next level splits by x <= p
+// and the left part (all == p) is final (reading R14).
+#include <algorithm>
+#include <vector>
+
+#include "pp_engine.cuh"
+
+namespace pp {
+
+void note_launches(uint64_t k);
+
+struct QSeg {
+    uint64_t lo, hi;   // [lo, hi)
+    uint64_t pivot;    // effective strict pivot (key < pivot goes left)
+    uint64_t gbase;    // first task (CTA) of this segment in the group launch
+    uint64_t g;        // groups of this segment
+    uint32_t mode;     // 0: pivot = median-of-3 (computed on device); 1: pivot given
+    uint32_t pad;
+};
+
+template <typename K>
+__device__ __forceinline__ K median3(K a, K b, K c) {
+    if (a > b) { K t = a; a = b; b = t; }
+    if (b > c) b = c;
+    return a > b ? a : b;
+}
+
+template <typename K>
+__global__ void qs_pivot_kernel(const K* __restrict__ keys, QSeg* __restrict__ segs, uint64_t nseg) {
+    for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += (uint64_t)gridDim.x * blockDim.x) {
+        QSeg q = segs[s];
+        if (q.mode == 0) {
+            const uint64_t len = q.hi - q.lo;
+            segs[s].pivot = (uint64_t)median3<K>(keys[q.lo], keys[q.lo + (len - 1) / 2], keys[q.hi - 1]);
+        }
+    }
+}
+
+template <typename K>
+__device__ __forceinline__ uint64_t seg_head(const K* keys, uint64_t lo, uint64_t len) {
+    const uint64_t addr = (uint64_t)(uintptr_t)(keys + lo);
+    uint64_t h = ((16 - (addr & 15)) & 15) / sizeof(K);
+    return h > len ? len : h;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(GroupCfg<K>::NT) qs_group_kernel(K* __restrict__ keys,
+                                                                   const QSeg* __restrict__ segs, uint64_t nseg,
+                                                                   uint64_t seed, GroupOut* __restrict__ gout) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    using C = GroupCfg<K>;
+    const uint64_t task = blockIdx.x;
+    // segment of this task: last s with gbase <= task
+    uint64_t lo = 0, hi = nseg;
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (segs[mid].gbase <= task) lo = mid; else hi = mid;
+    }
+    const QSeg q = segs[lo];
+    const uint64_t len = q.hi - q.lo;
+    const uint64_t h = seg_head<K>(keys, q.lo, len);
+    const uint64_t n_lines = (len - h) / C::LK;
+    ss_group_engine<GroupCfg<K>>(keys + q.lo + h, n_lines, (uint32_t)q.g, (uint32_t)(task - q.gbase), seed, (K)q.pivot,
+                       gout + task, smem);
+}
+
+// One CTA per mid segment: reduce the segment's group outputs, then clean its
+// dirty set with the single-CTA rank-matched walk; writes the split.
+template <typename K>
+__global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys, const QSeg* __restrict__ segs,
+                                                            const GroupOut* __restrict__ gout,
+                                                            uint64_t* __restrict__ splits) {
+    using C = GroupCfg<K>;
+    __shared__ WalkBuf<K> wb;
+    __shared__ uint64_t red[4][SW_NT / 32];
+    const QSeg q = segs[blockIdx.x];
+    K* seg = keys + q.lo;
+    const uint64_t len = q.hi - q.lo;
+    const K pivot = (K)q.pivot;
+    const uint64_t h = seg_head<K>(keys, q.lo, len);
+    const uint64_t n_lines = (len - h) / C::LK;
+    const uint64_t region_end = n_lines * C::LK;
+    uint64_t T = 0, vmin = region_end, vmax = 0, ht = 0;
+    for (uint64_t i = threadIdx.x; i < q.g; i += SW_NT) {
+        const GroupOut o = gout[q.gbase + i];
+        T += o.T;
+        vmin = o.vlo < vmin ? o.vlo : vmin;
+        vmax = o.vhi > vmax ? o.vhi : vmax;
+    }
+    for (uint64_t x = threadIdx.x; x < h; x += SW_NT) ht += is_pred(seg[x], pivot) ? 1 : 0;
+    for (uint64_t x = h + region_end + threadIdx.x; x < len; x += SW_NT) ht += is_pred(seg[x], pivot) ? 1 : 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T += __shfl_xor_sync(0xffffffffu, T, o);
+        ht += __shfl_xor_sync(0xffffffffu, ht, o);
+        const uint64_t a = __shfl_xor_sync(0xffffffffu, vmin, o);
+        const uint64_t b = __shfl_xor_sync(0xffffffffu, vmax, o);
+        vmin = a < vmin ? a : vmin;
+        vmax = b > vmax ? b : vmax;
+    }
+    if (lane == 0) {
+        red[0][warp] = T;
+        red[1][warp] = ht;
+        red[2][warp] = vmin;
+        red[3][warp] = vmax;
+    }
+    __syncthreads();
+    T = 0; ht = 0; vmin = region_end; vmax = 0;
+    for (int w = 0; w < SW_NT / 32; ++w) {
+        T += red[0][w];
+        ht += red[1][w];
+        vmin = red[2][w] < vmin ? red[2][w] : vmin;
+        vmax = red[3][w] > vmax ? red[3][w] : vmax;
+    }
+    const uint64_t Ks = T + ht;
+    uint64_t a[3], b[3];
+    a[0] = 0; b[0] = h;
+    a[1] = (h + vmin) < Ks ? (h + vmin) : Ks;
+    b[1] = (h + vmax) > Ks ? (h + vmax) : Ks;
+    if (vmin > vmax) { a[1] = b[1] = 0; }
+    a[2] = h + region_end; b[2] = len;
+    Ctl c;
+    finish_ctl(&c, len, Ks, a, b, 1, 1);
+    Dirty d;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { d.s[k] = c.ds[k]; d.l[k] = c.dl[k]; }
+    walk_swap<K>(seg, d, pivot, 0, c.Kv, c.Kv, c.W, ~0ull, wb);
+    if (threadIdx.x == 0) splits[blockIdx.x] = Ks;
+}
+
+// Leaf sort: one CTA sorts one segment of <= LEAF keys in shared memory with
+// a bitonic network (padding with the maximum key, never stored back).
+template <typename K, int LEAF, int NT>
+__global__ void __launch_bounds__(NT) qs_leaf_kernel(K* __restrict__ keys, const uint64_t* __restrict__ leaf_lo,
+                                                     const uint32_t* __restrict__ leaf_len) {
+    __shared__ K sk[LEAF];
+    const uint64_t lo = leaf_lo[blockIdx.x];
+    const uint32_t len = leaf_len[blockIdx.x];
+    uint32_t P = 2;
+    while (P < len) P <<= 1;
+    for (uint32_t i = threadIdx.x; i < P; i += NT) sk[i] = i < len ? keys[lo + i] : (K)~(K)0;
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t t = threadIdx.x; t < P / 2; t += NT) {
+                // comparator t: pair (i, i^j) with i having bit j clear
+                const uint32_t i = 2 * t - (t & (j - 1));
+                const uint32_t l = i + j;
+                const bool up = (i & k) == 0;
+                const K x = sk[i], y = sk[l];
+                if ((x > y) == up) {
+                    sk[i] = y;
+                    sk[l] = x;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < len; i += NT) keys[lo + i] = sk[i];
+}
+
+template <typename K>
+struct LeafCfg {
+    static constexpr int LEAF = (sizeof(K) == 8) ? 4096 : 8192;
+    static constexpr int NT = 512;
+};
+
+// quicksort workspace (separate from the partition workspace)
+static void* g_qws = nullptr;
+static size_t g_qws_bytes = 0;
+static void* qs_workspace(size_t bytes) {
+    if (bytes <= g_qws_bytes) return g_qws;
+    if (g_qws) {
+        cudaDeviceSynchronize();
+        cudaFree(g_qws);
+    }
+    g_qws = nullptr;
+    g_qws_bytes = 0;
+    size_t want = bytes + (bytes >> 1);
+    if (cudaMalloc(&g_qws, want) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    g_qws_bytes = want;
+    return g_qws;
+}
+
+template <typename K>
+pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
+    using C = GroupCfg<K>;
+    using LC = LeafCfg<K>;
+    const Params& P = params();
+    const uint64_t LEAF = (P.leaf > 0 && P.leaf <= LC::LEAF) ? (uint64_t)P.leaf : (uint64_t)LC::LEAF;
+    const uint64_t BIG = P.qs_cta_max > 0 ? (uint64_t)P.qs_cta_max : (uint64_t)1 << 25;
+    const uint64_t MINL = 64;  // lines per group for mid segments
+    const K KMAX = (K)~(K)0;
+
+    struct HSeg {
+        uint64_t lo, hi, pivot;
+        uint32_t mode;
+    };
+    std::vector<HSeg> cur{{0, n, 0, 0}}, next;
+    std::vector<uint64_t> leaf_lo;
+    std::vector<uint32_t> leaf_len;
+    auto add_child = [&](uint64_t lo, uint64_t hi) {
+        const uint64_t len = hi - lo;
+        if (len <= 1) return;
+        if (len <= LEAF) {
+            leaf_lo.push_back(lo);
+            leaf_len.push_back((uint32_t)len);
+        } else {
+            next.push_back({lo, hi, 0, 0});
+        }
+    };
+    if (n <= LEAF) {
+        cur.clear();
+        add_child(0, n);
+    }
+    std::vector<QSeg> mids;
+    std::vector<uint64_t> splits_h, pivots_h;
+    std::vector<size_t> order;  // cur index -> splits index
+    cudaError_t e;
+    cudaFuncSetAttribute(qs_group_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    while (!cur.empty()) {
+        // ---- classify ----
+        mids.clear();
+        std::vector<size_t> big_idx, mid_idx;
+        uint64_t gtot = 0;
+        for (size_t i = 0; i < cur.size(); ++i) {
+            const uint64_t len = cur[i].hi - cur[i].lo;
+            if (len >= BIG) {
+                big_idx.push_back(i);
+            } else {
+                mid_idx.push_back(i);
+                QSeg q;
+                q.lo = cur[i].lo;
+                q.hi = cur[i].hi;
+                q.pivot = cur[i].pivot;
+                q.mode = cur[i].mode;
+                q.pad = 0;
+                // lines of the aligned region (host mirror of seg_head)
+                const uint64_t addr = (uint64_t)(uintptr_t)(keys + q.lo);
+                uint64_t h = ((16 - (addr & 15)) & 15) / sizeof(K);
+                if (h > len) h = len;
+                const uint64_t nl = (len - h) / C::LK;
+                q.g = std::max<uint64_t>(1, nl / MINL);
+                q.gbase = gtot;
+                gtot += q.g;
+                mids.push_back(q);
+            }
+        }
+        const uint64_t nmid = mids.size(), nbig = big_idx.size();
+        // ---- workspace: [segs][gout][splits] ----
+        const size_t segB = ((sizeof(QSeg) * std::max<uint64_t>(nmid, 1)) + 255) & ~size_t(255);
+        const size_t goB = ((sizeof(GroupOut) * std::max<uint64_t>(gtot, 1)) + 255) & ~size_t(255);
+        const size_t spB = ((8 * (nmid + nbig + 1)) + 255) & ~size_t(255);
+        unsigned char* ws = static_cast<unsigned char*>(qs_workspace(segB + goB + spB));
+        if (!ws) return PP_E_NOMEM;
+        QSeg* d_segs = reinterpret_cast<QSeg*>(ws);
+        GroupOut* d_gout = reinterpret_cast<GroupOut*>(ws + segB);
+        uint64_t* d_splits = reinterpret_cast<uint64_t*>(ws + segB + goB);
+
+        // ---- big segments: full multi-CTA partition, one at a time ----
+        pivots_h.assign(cur.size(), 0);
+        for (size_t bi = 0; bi < nbig; ++bi) {
+            HSeg& s = cur[big_idx[bi]];
+            uint64_t p = s.pivot;
+            if (s.mode == 0) {
+                K three[3];
+                const uint64_t len = s.hi - s.lo;
+                e = cudaMemcpyAsync(&three[0], keys + s.lo, sizeof(K), cudaMemcpyDeviceToHost, st);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(&three[1], keys + s.lo + (len - 1) / 2, sizeof(K), cudaMemcpyDeviceToHost, st);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(&three[2], keys + s.hi - 1, sizeof(K), cudaMemcpyDeviceToHost, st);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+                if (e != cudaSuccess) return cuda_fail(e, "quicksort pivot");
+                K a = three[0], b = three[1], c = three[2];
+                if (a > b) std::swap(a, b);
+                if (b > c) b = c;
+                p = (uint64_t)(a > b ? a : b);
+            }
+            pivots_h[big_idx[bi]] = p;
+            pp_status ps = partition_device<K>(keys + s.lo, s.hi - s.lo, (K)p, st, d_splits + nmid + bi, nullptr);
+            if (ps != PP_OK) return ps;
+        }
+        // ---- mid segments: one batched pass ----
+        if (nmid > 0) {
+            e = cudaMemcpyAsync(d_segs, mids.data(), sizeof(QSeg) * nmid, cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort H2D");
+            qs_pivot_kernel<K><<<(unsigned)((nmid + 255) / 256), 256, 0, st>>>(keys, d_segs, nmid);
+            qs_group_kernel<K><<<(unsigned)gtot, C::NT, C::SMEM, st>>>(keys, d_segs, nmid, P.seed, d_gout);
+            qs_cleanup_kernel<K><<<(unsigned)nmid, SW_NT, 0, st>>>(keys, d_segs, d_gout, d_splits);
+            note_launches(3);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort mid launch");
+        }
+        // ---- read back splits (and mid pivots) ----
+        splits_h.assign(nmid + nbig, 0);
+        if (nmid + nbig > 0) {
+            e = cudaMemcpyAsync(splits_h.data(), d_splits, 8 * (nmid + nbig), cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort D2H");
+        }
+        if (nmid > 0) {
+            e = cudaMemcpyAsync(mids.data(), d_segs, sizeof(QSeg) * nmid, cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort D2H");
+        }
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort level");
+        for (size_t mi = 0; mi < nmid; ++mi) pivots_h[mid_idx[mi]] = mids[mi].pivot;
+        // ---- next level ----
+        next.clear();
+        auto visit = [&](const HSeg& s, uint64_t p, uint64_t k) {
+            if (s.mode == 0) {
+                if (k == 0) {
+                    // p is the segment minimum; split by x <= p next (unless all == MAX)
+                    if ((K)p != KMAX) next.push_back({s.lo, s.hi, (uint64_t)(K)(p + 1), 1});
+                } else {
+                    add_child(s.lo, s.lo + k);
+                    add_child(s.lo + k, s.hi);
+                }
+            } else {
+                add_child(s.lo + k, s.hi);  // [lo, lo+k) is all equal: final
+            }
+        };
+        for (size_t mi = 0; mi < nmid; ++mi) visit(cur[mid_idx[mi]], pivots_h[mid_idx[mi]], splits_h[mi]);
+        for (size_t bi = 0; bi < nbig; ++bi) visit(cur[big_idx[bi]], pivots_h[big_idx[bi]], splits_h[nmid + bi]);
+        cur.swap(next);
+    }
+    // ---- leaves ----
+    const uint64_t nleaf = leaf_lo.size();
+    if (nleaf > 0) {
+        const size_t loB = ((8 * nleaf) + 255) & ~size_t(255);
+        unsigned char* ws = static_cast<unsigned char*>(qs_workspace(loB + 4 * nleaf));
+        if (!ws) return PP_E_NOMEM;
+        uint64_t* d_lo = reinterpret_cast<uint64_t*>(ws);
+        uint32_t* d_len = reinterpret_cast<uint32_t*>(ws + loB);
+        e = cudaMemcpyAsync(d_lo, leaf_lo.data(), 8 * nleaf, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_len, leaf_len.data(), 4 * nleaf, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort leaves H2D");
+        for (uint64_t b0 = 0; b0 < nleaf; b0 += 65535u * 1024u) {
+            const uint64_t cnt = std::min<uint64_t>(nleaf - b0, 65535u * 1024u);
+            qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, 0, st>>>(keys, d_lo + b0, d_len + b0);
+            note_launches(1);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort leaf launch");
+        // the host vectors must outlive the async copies
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort leaves");
+    }
+    last_stats().aux_bytes = g_qws_bytes;
+    return PP_OK;
+}
+
+template pp_status quicksort_device<uint64_t>(uint64_t*, uint64_t, cudaStream_t);
+template pp_status quicksort_device<uint32_t>(uint32_t*, uint64_t, cudaStream_t);
+
+}  // namespace pp

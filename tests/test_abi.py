@@ -1,0 +1,67 @@
+"""The C-ABI library loads and exports every symbol include/pp.h declares
+(no GPU needed; no compute calls), plus host-side argument errors."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+
+import paper_2004_12532_b200 as pp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_builds_and_exports_header_symbols():
+    L = pp.load()
+    syms = pp.header_symbols()
+    assert "pp_partition" in syms and "pp_quicksort" in syms and len(syms) >= 20
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+    out = subprocess.check_output(["nm", "-D", "--defined-only", pp.LIB_PATH]).decode()
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    assert set(syms) <= exported
+
+
+def test_status_strings_and_params():
+    L = pp.load()
+    assert L.pp_status_string(0) == b"PP_OK"
+    assert L.pp_status_string(1) == b"PP_E_INVAL"
+    assert L.pp_set_param(b"no_such_param", 1) == 1
+    assert L.pp_get_param(b"no_such_param") == -(1 << 63)
+    old = pp.pp_get_param("min_lines_per_group")
+    pp.pp_set_param("min_lines_per_group", 33)
+    assert pp.pp_get_param("min_lines_per_group") == 33
+    pp.pp_set_param("min_lines_per_group", old)
+
+
+def test_null_arguments_rejected_without_gpu():
+    L = pp.load()
+    out = ctypes.c_uint64(123)
+    assert L.pp_partition_u64(None, 5, 1, None, ctypes.byref(out)) == 1   # NULL keys, n > 0
+    assert L.pp_partition_u32(None, 5, 1, None, ctypes.byref(out)) == 1
+    assert L.pp_partition_host_u64(None, 5, 1, ctypes.byref(out)) == 1
+    assert L.pp_partition_u64(None, 0, 1, None, ctypes.byref(out)) == 0 and out.value == 0
+    assert L.pp_partition(None, 5, 1) == (1 << 64) - 1
+
+
+def test_product_does_not_import_oracle():
+    """The product package never references oracle/ (grep gate)."""
+    pkg = os.path.join(ROOT, "paper_2004_12532_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                for bad in ("import oracle", "from oracle", "liboracle", "pp_oracle", "oracle/pp"):
+                    assert bad not in txt, (f, bad)
+
+
+def test_no_atomics_in_sass():
+    """EREW discipline: no atomic / reduction instructions in any kernel."""
+    pp.load()
+    try:
+        sass = subprocess.check_output(["cuobjdump", "-sass", pp.LIB_PATH], stderr=subprocess.STDOUT).decode()
+    except (OSError, subprocess.CalledProcessError):
+        pytest.skip("cuobjdump unavailable")
+    bad = [l for l in sass.splitlines() if any(m in l for m in (" ATOM", " RED.", " ATOMS", " ATOMG"))]
+    assert not bad, bad[:5]
+    assert "UBLKCP" in sass  # the group kernel stages lines with the bulk-copy (TMA) engine

@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA partition (through the C ABI) against the CPU oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+U64_MAX = (1 << 64) - 1
+U32_MAX = (1 << 32) - 1
+
+
+@pytest.fixture(scope="module")
+def pp():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2004_12532_b200 as m
+    m.load()
+    m.reset_params()
+    yield m
+    m.reset_params()
+
+
+def _run(pp, a: np.ndarray, pivot: int, offset: int = 0, **params):
+    from gpu_util import to_dev, to_host
+    for k, v in params.items():
+        pp.pp_set_param(k, v)
+    try:
+        pad = np.zeros(offset, dtype=a.dtype)
+        buf = to_dev(np.concatenate([pad, a, pad]))
+        view = buf[offset:offset + a.size]
+        split = pp.pp_partition(view, pivot)
+        out = to_host(view, a.dtype)
+        # the padding must be untouched
+        full = to_host(buf, a.dtype)
+        assert np.all(full[:offset] == 0) and np.all(full[offset + a.size:] == 0)
+        return split, out
+    finally:
+        pp.reset_params()
+
+
+def _pivots(a, mx):
+    ps = {0, 1, mx, mx // 2}
+    if a.size:
+        ps.add(int(np.sort(a)[a.size // 2]))
+        ps.add(int(a[0]))
+    return sorted(ps)
+
+
+SMALL_NS = list(range(0, 71)) + [127, 128, 129, 511, 512, 513, 1023, 1024, 1025, 2047, 2048, 2049, 4095, 4096,
+                                  4097, 8191, 8192, 8193, 10007, 32767, 32768, 32769, 65537]
+
+
+@pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
+@pytest.mark.parametrize("path", [1, 2, 3])
+def test_edge_sizes(pp, dt, mx, path):
+    rng = np.random.default_rng(100 + path)
+    for n in SMALL_NS:
+        a = rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
+        for p in _pivots(a, mx):
+            for off in (0, 1, 3):
+                split, out = _run(pp, a, p, off, path=path, small_n=0,
+                                  min_lines_per_group=1)
+                oracle.check_partition(a, out, p, split)
+
+
+@pytest.mark.parametrize("dt", [np.uint64, np.uint32])
+def test_all_patterns_small(pp, dt):
+    """All 2^n predecessor/successor patterns for n <= 10, tagged keys, all paths."""
+    for path in (1, 2, 3):
+        for n in range(0, 11):
+            for mask in range(1 << n):
+                bits = np.array([(mask >> i) & 1 for i in range(n)], dtype=bool)
+                idx = np.arange(n, dtype=dt)
+                a = np.where(bits, idx, idx + 1000).astype(dt)
+                split, out = _run(pp, a, 1000, 0, path=path, small_n=0, min_lines_per_group=1)
+                oracle.check_partition(a, out, 1000, split)
+
+
+@pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
+def test_alphabet_duplicates(pp, dt, mx):
+    """Duplicate-heavy keys over a tiny alphabet, pivots spanning all cases."""
+    rng = np.random.default_rng(5)
+    for n in (1000, 5000, 70001, 300007):
+        a = rng.integers(0, 4, size=n).astype(dt)
+        for p in range(5):
+            for path in (2, 3):
+                split, out = _run(pp, a, p, 1, path=path, small_n=0, min_lines_per_group=2)
+                oracle.check_partition(a, out, p, split)
+
+
+@pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
+@pytest.mark.parametrize("g", [1, 2, 7, 64, 0])
+def test_groups_and_windows(pp, dt, mx, g):
+    """Medium n, forced group counts (large windows exercise the multi-CTA
+    cleanup), several offsets and pivot fractions."""
+    rng = np.random.default_rng(g + 17)
+    for n in (100003, 1 << 20, 3000017):
+        a = rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
+        for frac in (0.0, 0.01, 0.5, 0.99, 1.0):
+            p = min(mx, int(frac * (mx + 1)))
+            split, out = _run(pp, a, p, 2, path=2, g=g, small_n=0)
+            oracle.check_partition(a, out, p, split)
+
+
+def test_structured_inputs(pp):
+    """Already partitioned / reverse / all-true / all-false / alternating (u32)
+    and whole-line adversarial patterns (u64)."""
+    n = 1_000_003
+    for pat in synth.ADV_PATTERNS:
+        a = synth.adversarial_u32_np(n, pat, 9)
+        split, out = _run(pp, a, synth.ADV_PIVOT_U32, 1)
+        oracle.check_partition(a, out, synth.ADV_PIVOT_U32, split)
+    # line-granular blocks of predecessors (window stress)
+    rng = np.random.default_rng(3)
+    line = 1024
+    nl = 3001
+    blocks = rng.integers(0, 2, size=nl).astype(bool)
+    a = np.where(np.repeat(blocks, line), np.uint64(5), np.uint64(1 << 40)).astype(np.uint64)
+    a ^= rng.integers(0, 4, size=a.size).astype(np.uint64)
+    for g in (0, 8, 1000):
+        split, out = _run(pp, a, 100, 0, g=g)
+        oracle.check_partition(a, out, 100, split)
+
+
+def test_determinism(pp):
+    n = 3_000_001
+    a = synth.uniform_u64_np(n, 42)
+    s1, o1 = _run(pp, a, 1 << 63, 1)
+    s2, o2 = _run(pp, a, 1 << 63, 1)
+    assert s1 == s2 and np.array_equal(o1, o2)
+
+
+@pytest.mark.parametrize("dt", [np.uint64, np.uint32])
+def test_ss_groups_parity(pp, dt):
+    """The Smoothed Striding partial partition step's per-group outputs (T_i,
+    v_i) equal the oracle's, and the array is partially partitioned
+     with v_min <= K <= v_max."""
+    from gpu_util import to_dev, to_host
+    rng = np.random.default_rng(8)
+    mx = U64_MAX if dt == np.uint64 else U32_MAX
+    for n, g, off in ((1 << 20, 0, 0), (1 << 20, 37, 1), (777777, 5, 3), (5_000_000, 0, 2)):
+        a = rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
+        p = int(np.sort(a)[n // 3])
+        buf = to_dev(np.concatenate([np.zeros(off, dtype=dt), a]))
+        view = buf[off:]
+        T, vlo, vhi, info = pp.pp_ss_groups(view, p, g)
+        h, nl, LK, gg = info["head"], info["n_lines"], info["line_keys"], info["g"]
+        s = (nl + gg - 1) // gg
+        X = synth.ss_offsets(info["seed"], s, gg)
+        T2, vlo2, vhi2 = oracle.ss_groups(a, h, nl, LK, gg, X, p)
+        assert np.array_equal(T, T2)
+        assert np.array_equal(vlo, vlo2 - h) and np.array_equal(vhi, vhi2 - h)
+        out = to_host(view, dt)
+        region = out[h:h + nl * LK]
+        vmin, vmax = int(vlo.min()), int(vhi.max())
+        assert np.all(region[:vmin] < p) and np.all(region[vmax:] >= p)
+        assert vmin <= int(T.sum()) <= vmax
+        assert np.array_equal(np.sort(out), np.sort(a))
+
+
+def test_async_and_stats(pp):
+    from gpu_util import to_dev
+    n = 1 << 20
+    a = synth.uniform_u64_np(n, 7)
+    t = to_dev(a)
+    d = torch.zeros(1, dtype=torch.int64, device="cuda")
+    pp.pp_partition_async_u64(t, 1 << 63, d)
+    torch.cuda.synchronize()
+    K = oracle.count(a, 1 << 63)
+    assert int(d.item()) == K
+    st = pp.pp_last_stats()
+    assert st["K"] == K and st["n"] == n
+    assert st["aux_bytes"] < 0.01 * n * 8
+
+
+def test_host_variant(pp):
+    for dt, p in ((np.uint64, 1 << 62), (np.uint32, 1 << 30)):
+        a = (synth.uniform_u64_np(200003, 11) if dt == np.uint64 else synth.uniform_u32_np(200003, 11))
+        b = a.copy()
+        f = pp.pp_partition_host_u64 if dt == np.uint64 else pp.pp_partition_host_u32
+        split = f(b, p)
+        oracle.check_partition(a, b, p, split)
+
+
+def test_invalid_args(pp):
+    import ctypes
+    L = pp.load()
+    out = ctypes.c_uint64(0)
+    # misaligned device pointer
+    t = torch.zeros(16, dtype=torch.int64, device="cuda")
+    assert L.pp_partition_u64(t.data_ptr() + 4, 8, 5, None, ctypes.byref(out)) == 1
+    # host pointer passed as device pointer
+    h = np.zeros(16, dtype=np.uint64)
+    assert L.pp_partition_u64(h.ctypes.data, 16, 5, None, ctypes.byref(out)) == 1
+    # empty
+    assert L.pp_partition_u64(None, 0, 5, None, ctypes.byref(out)) == 0 and out.value == 0
+
+
+# ----------------------------------------------------------------------------
+# BASELINE configs at full size (checks via oracle count + device properties)
+# ----------------------------------------------------------------------------
+
+def _full_check(pp, t, pivot, K_oracle):
+    from gpu_util import check_partition_device
+    inp = t.clone()
+    split = pp.pp_partition(t, pivot)
+    check_partition_device(inp, t, pivot, split, K_oracle)
+    return split
+
+
+def test_config1_exact(pp):
+    from gpu_util import to_dev
+    n = 1 << 20
+    a = synth.uniform_u64_np(n, synth.SEEDS["c1"])
+    t = to_dev(a)
+    split = pp.pp_partition(t, 1 << 63)
+    oracle.check_partition(a, t.cpu().numpy().view(np.uint64), 1 << 63, split)
+
+
+@pytest.mark.parametrize("mu", [0.01, 0.5, 0.99])
+def test_config2_full(pp, mu):
+    n = 1 << 27
+    p = synth.PIVOT_MU[mu]
+    t = synth.uniform_u64_torch(n, synth.SEEDS["c2"], "cuda")
+    host = t.cpu().numpy().view(np.uint64)
+    K = oracle.count(host, p)
+    _full_check(pp, t, p, K)
+    st = pp.pp_last_stats()
+    assert st["path"] == 2 and st["W"] < 0.05 * n
+    assert st["aux_bytes"] < 0.001 * n * 8
+
+
+@pytest.mark.parametrize("pat", list(synth.ADV_PATTERNS))
+def test_config4_adversarial_full(pp, pat):
+    n = 1_000_000_007
+    t = synth.adversarial_u32_torch(n, pat, synth.SEEDS["c4"], "cuda")
+    K = {"partitioned": n // 2, "reverse": n // 2, "all_true": n, "all_false": 0,
+         "alternating": (n + 1) // 2}[pat]
+    # the closed-form K is pinned against the oracle count on a prefix sample
+    host_prefix = t[:1_000_003].cpu().numpy().view(np.uint32)
+    Kp = oracle.count(host_prefix, synth.ADV_PIVOT_U32)
+    exp_p = {"partitioned": 1_000_003, "reverse": 0, "all_true": 1_000_003, "all_false": 0,
+             "alternating": 500_002}[pat]
+    assert Kp == exp_p
+    _full_check(pp, t, synth.ADV_PIVOT_U32, K)

@@ -1,0 +1,112 @@
+"""GPU parity: the CUDA quicksort (through the C ABI) against the CPU oracle sort."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+U64_MAX = (1 << 64) - 1
+U32_MAX = (1 << 32) - 1
+
+
+@pytest.fixture(scope="module")
+def pp():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2004_12532_b200 as m
+    m.load()
+    m.reset_params()
+    yield m
+    m.reset_params()
+
+
+def _sort_gpu(pp, a: np.ndarray, offset: int = 0, **params):
+    from gpu_util import to_dev, to_host
+    for k, v in params.items():
+        pp.pp_set_param(k, v)
+    try:
+        pad = np.zeros(offset, dtype=a.dtype)
+        buf = to_dev(np.concatenate([pad, a, pad]))
+        view = buf[offset:offset + a.size]
+        pp.pp_quicksort(view)
+        full = to_host(buf, a.dtype)
+        assert np.all(full[:offset] == 0) and np.all(full[offset + a.size:] == 0)
+        return full[offset:offset + a.size]
+    finally:
+        pp.reset_params()
+
+
+def _oracle_sorted(a):
+    b = a.copy()
+    oracle.quicksort(b)
+    return b
+
+
+def _cases(dt, mx, n, rng):
+    yield rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
+    yield rng.integers(0, 1000, size=n).astype(dt)
+    yield np.full(n, 7, dtype=dt)
+    yield np.full(n, mx, dtype=dt)
+    yield np.arange(n, dtype=dt)
+    yield np.arange(n, dtype=dt)[::-1].copy()
+    yield (rng.integers(0, 2, size=n).astype(dt) * dt(mx))
+
+
+@pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
+def test_small_sizes(pp, dt, mx):
+    rng = np.random.default_rng(1)
+    for n in list(range(0, 40)) + [255, 256, 257, 4095, 4096, 4097, 8191, 8192, 8193, 20000]:
+        for a in _cases(dt, mx, n, rng):
+            for off in (0, 1):
+                out = _sort_gpu(pp, a, off)
+                assert np.array_equal(out, _oracle_sorted(a)), (n, off)
+
+
+@pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
+def test_medium_sizes(pp, dt, mx):
+    rng = np.random.default_rng(2)
+    for n in (100_003, 1 << 20, 3_000_017):
+        for a in _cases(dt, mx, n, rng):
+            out = _sort_gpu(pp, a, 3)
+            assert np.array_equal(out, _oracle_sorted(a)), n
+
+
+def test_big_path_forced(pp):
+    """Force the multi-CTA partition for mid-size segments (qs_cta_max small)."""
+    rng = np.random.default_rng(3)
+    for a in (rng.integers(0, U64_MAX, size=2_000_003, dtype=np.uint64, endpoint=True),
+              rng.integers(0, 50, size=2_000_003).astype(np.uint64)):
+        out = _sort_gpu(pp, a, 1, qs_cta_max=1 << 16)
+        assert np.array_equal(out, _oracle_sorted(a))
+
+
+@pytest.mark.parametrize("kind", ["uniform", "dup1000"])
+def test_config5_full(pp, kind):
+    """n = 2^28 u64 (BASELINE config 5).  Checks: ascending order on every
+    adjacent pair; multiset equal to the input (library sort); sampled ranks
+    r: out[r] is the r-th smallest by the oracle's count
+    (count(in < out[r]) <= r < count(in <= out[r]))."""
+    from gpu_util import order_key
+    n = 1 << 28
+    if kind == "uniform":
+        t = synth.uniform_u64_torch(n, synth.SEEDS["c5"], "cuda")
+    else:
+        t = synth.mod_range_u64_torch(n, synth.SEEDS["c5"], 1000, "cuda")
+    inp_host = t.cpu().numpy().view(np.uint64).copy()
+    pp.pp_quicksort(t)
+    ko = order_key(t)
+    assert bool((ko[1:] >= ko[:-1]).all()), "not sorted"
+    ref = torch.sort(order_key(torch.from_numpy(inp_host.view(np.int64)).to("cuda"))).values
+    assert torch.equal(ref, ko), "multiset differs"
+    del ref
+    out = t.cpu().numpy().view(np.uint64)
+    rng = np.random.default_rng(0)
+    for r in list(rng.integers(0, n, size=6)) + [0, n - 1]:
+        v = int(out[r])
+        lo = oracle.count(inp_host, v)
+        hi = oracle.count(inp_host, v + 1) if v < U64_MAX else n
+        assert lo <= r < hi, r
