@@ -32,18 +32,21 @@ struct GroupCfgT {
     static constexpr int KPT = VPT * VEC;
     static constexpr int NW = NT / 32;
     static constexpr int POOL = 2 * LK;          // pool ring capacity (occupancy <= 2b)
-    static constexpr size_t SMEM = (size_t)(2 * PF * LK + 2 * POOL) * sizeof(K) + 2 * PF * 8 + NW * 4 + 16;
+    static constexpr int LTAB = 16;              // line-index table entries per end
+    static constexpr size_t SMEM =
+        (size_t)(2 * PF * LK + 2 * POOL) * sizeof(K) + 2 * PF * 8 + 4 * ((NW + 7) / 8 * 8) + 4 * 2 * LTAB + 16;
     static_assert(VPT >= 1 && VPT * NT * VEC == LK, "line must be a multiple of NT 16-B vectors");
     static_assert((POOL & (POOL - 1)) == 0, "pool ring must be a power of two");
+    static_assert(PF + 3 < LTAB, "line table too small for the prefetch depth");
 };
 
 // the default configuration (used by quicksort and by variant 0)
 template <typename K>
-using GroupCfg = GroupCfgT<K, 8192, 256, 4, true>;
+using GroupCfg = GroupCfgT<K, 8192, 256, 4, false>;
 
 // Line index of the j-th line (group order) of group gi: G_i(j) of
 // PAPER.md:963-969 in 0-based form, j*g + ((X[j] + i) mod g).
-__device__ __forceinline__ uint64_t group_line(uint64_t seed, uint32_t g, uint32_t gi, int64_t j) {
+__device__ __forceinline__ uint64_t group_line(uint64_t seed, uint32_t g, uint32_t gi, uint32_t j) {
     uint32_t x = ss_offset(seed, (uint64_t)j, g) + gi;
     if (x >= g) x -= g;
     return (uint64_t)j * g + x;
@@ -58,6 +61,10 @@ __device__ __forceinline__ uint64_t group_line(uint64_t seed, uint32_t g, uint32
 // predecessors then successors.  => the group's first T_i elements (group
 // order) are predecessors: exactly the Partial Partition Step's postcondition
 // (PAPER.md:979-1001), with every line read once and written once.
+//
+// Control state is uniform (every thread tracks it); only thread 0 issues the
+// bulk copies.  Line indices are hashed once, at claim time, into a small
+// shared table (ltab) that the write phase reads back.
 template <typename C>
 __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n_lines, uint32_t g, uint32_t gi,
                                 uint64_t seed, typename C::Key pivot, GroupOut* __restrict__ out,
@@ -66,20 +73,22 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
     constexpr int LK = C::LK, NT = C::NT, PF = C::PF, VEC = C::VEC, VPT = C::VPT, KPT = C::KPT, NW = C::NW;
     constexpr uint32_t PMASK = C::POOL - 1;
     constexpr uint32_t LBYTES = LK * sizeof(K);
+    constexpr int LT = C::LTAB;
 
     K* ring = reinterpret_cast<K*>(smem);         // [2][PF][LK]: front ring, back ring
     K* tpool = ring + 2 * PF * LK;                // predecessor pool (ring of 2 lines)
     K* fpool = tpool + C::POOL;                   // successor pool
     uint64_t* bars = reinterpret_cast<uint64_t*>(fpool + C::POOL);
     uint32_t* wtrue = reinterpret_cast<uint32_t*>(bars + 2 * PF);
+    uint32_t* ltab = wtrue + (NW + 7) / 8 * 8;    // [2][LT] line indices (front, back)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = lanemask_lt();
 
     // number of lines of this group: s-1 full chunks + the last chunk's line if it exists
-    const uint64_t s = (n_lines + g - 1) / g;
-    int64_t S = 0;
-    if (s > 0) S = (int64_t)s - 1 + (group_line(seed, g, gi, (int64_t)s - 1) < n_lines ? 1 : 0);
+    const uint32_t s = (uint32_t)((n_lines + g - 1) / g);
+    int S = 0;
+    if (s > 0) S = (int)s - 1 + (group_line(seed, g, gi, s - 1) < n_lines ? 1 : 0);
 
     if (tid == 0) {
         for (int k = 0; k < 2 * PF; ++k) mbar_init(&bars[k], 1);
@@ -87,31 +96,38 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
     }
     __syncthreads();
 
-    int64_t fpf = 0, bpf = S - 1;  // next line to claim for the front / back ring
-    int64_t fc = 0, bc = S - 1;    // next line to consume from the front / back
-    int64_t fw = 0, bw = S - 1;    // front lines [0,fw) and back lines (bw,S-1] are written
+    int fpf = 0, bpf = S - 1;  // next line to claim for the front / back ring
+    int fc = 0, bc = S - 1;    // next line to consume from the front / back
+    int fw = 0, bw = S - 1;    // front lines [0,fw) and back lines (bw,S-1] are written
     uint32_t th = 0, tt = 0, fh = 0, ft = 0;  // pool head/tail counters (mod 2^32)
 
     auto claim_front = [&]() {
         if (tid == 0) {
-            const int slot = (int)(fpf % PF);
-            uint64_t* bar = &bars[slot];
-            mbar_expect_tx(bar, LBYTES);
-            bulk_g2s(ring + slot * LK, region + group_line(seed, g, gi, fpf) * LK, LBYTES, bar);
+            const uint32_t slot = (uint32_t)fpf % PF;
+            const uint32_t line = (uint32_t)group_line(seed, g, gi, (uint32_t)fpf);
+            ltab[fpf & (LT - 1)] = line;
+            mbar_expect_tx(&bars[slot], LBYTES);
+            bulk_g2s(ring + slot * LK, region + (uint64_t)line * LK, LBYTES, &bars[slot]);
         }
         ++fpf;
     };
     auto claim_back = [&]() {
         if (tid == 0) {
-            const int slot = (int)((S - 1 - bpf) % PF);
-            uint64_t* bar = &bars[PF + slot];
-            mbar_expect_tx(bar, LBYTES);
-            bulk_g2s(ring + (PF + slot) * LK, region + group_line(seed, g, gi, bpf) * LK, LBYTES, bar);
+            const uint32_t kk = (uint32_t)(S - 1 - bpf);
+            const uint32_t slot = kk % PF;
+            const uint32_t line = (uint32_t)group_line(seed, g, gi, (uint32_t)bpf);
+            ltab[LT + (kk & (LT - 1))] = line;
+            mbar_expect_tx(&bars[PF + slot], LBYTES);
+            bulk_g2s(ring + (PF + slot) * LK, region + (uint64_t)line * LK, LBYTES, &bars[PF + slot]);
         }
         --bpf;
     };
-    auto store_line = [&](const K* pool, uint32_t head, int64_t j) {
-        K* dst = region + group_line(seed, g, gi, j) * LK;
+    // array line index of group line j (claimed by the front ring iff j < fpf)
+    auto line_index = [&](int j) -> uint32_t {
+        return j < fpf ? ltab[j & (LT - 1)] : ltab[LT + ((S - 1 - j) & (LT - 1))];
+    };
+    auto store_line = [&](const K* pool, uint32_t head, int j) {
+        K* dst = region + (uint64_t)line_index(j) * LK;
         const K* src = pool + (head & PMASK);
         if constexpr (C::TMA_STORE) {
             if (tid == 0) {
@@ -134,28 +150,23 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
     while (fc <= bc) {
         // ---- choose the end to consume (uniform across the CTA) ----
         const uint32_t tocc = tt - th, focc = ft - fh;
-        const int64_t nF = fc - fw, nB = bw - bc;  // consumed-but-unwritten slots
+        const int nF = fc - fw, nB = bw - bc;  // consumed-but-unwritten slots
         bool front;
         if (tocc >= (uint32_t)LK && nF == 0) front = true;
         else if (focc >= (uint32_t)LK && nB == 0) front = false;
         else front = (nF <= nB);
-        const int64_t l = front ? fc : bc;
-        const K* src;
-        uint64_t* bar;
-        uint32_t par;
+        const int l = front ? fc : bc;
+        uint32_t bi, par;
         if (l < fpf) {
-            const int slot = (int)(l % PF);
-            src = ring + slot * LK;
-            bar = &bars[slot];
-            par = (uint32_t)((l / PF) & 1);
+            bi = (uint32_t)l % PF;
+            par = ((uint32_t)l / PF) & 1u;
         } else {
-            const int64_t kk = S - 1 - l;
-            const int slot = (int)(kk % PF);
-            src = ring + (PF + slot) * LK;
-            bar = &bars[PF + slot];
-            par = (uint32_t)((kk / PF) & 1);
+            const uint32_t kk = (uint32_t)(S - 1 - l);
+            bi = PF + kk % PF;
+            par = (kk / PF) & 1u;
         }
-        mbar_wait(bar, par);
+        const K* src = ring + bi * LK;
+        mbar_wait(&bars[bi], par);
 
         // ---- classify: warp ballots, slot-major order within the warp ----
         K x[KPT];
@@ -227,12 +238,12 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
 
     // ---- final flush: open lines [fw, bw] get predecessors then successors ----
     const uint32_t tp = tt - th;
-    for (int64_t jl = fw; jl <= bw; ++jl) {
-        K* dst = region + group_line(seed, g, gi, jl) * LK;
-        const uint64_t base = (uint64_t)(jl - fw) * LK;
+    for (int jl = fw; jl <= bw; ++jl) {
+        K* dst = region + (uint64_t)line_index(jl) * LK;
+        const uint32_t base = (uint32_t)(jl - fw) * LK;
         for (int e = tid; e < LK; e += NT) {
-            const uint64_t q = base + e;
-            dst[e] = (q < tp) ? tpool[(th + (uint32_t)q) & PMASK] : fpool[(fh + (uint32_t)(q - tp)) & PMASK];
+            const uint32_t q = base + e;
+            dst[e] = (q < tp) ? tpool[(th + q) & PMASK] : fpool[(fh + (q - tp)) & PMASK];
         }
     }
     if constexpr (C::TMA_STORE) {
@@ -246,9 +257,9 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
             o.vlo = n_lines * LK;
             o.vhi = 0;
         } else if (T == (uint64_t)S * LK) {
-            o.vlo = o.vhi = group_line(seed, g, gi, S - 1) * LK + LK;
+            o.vlo = o.vhi = group_line(seed, g, gi, (uint32_t)(S - 1)) * LK + LK;
         } else {
-            o.vlo = o.vhi = group_line(seed, g, gi, (int64_t)(T / LK)) * LK + T % LK;
+            o.vlo = o.vhi = group_line(seed, g, gi, (uint32_t)(T / LK)) * LK + T % LK;
         }
         *out = o;
     }
@@ -277,10 +288,19 @@ __device__ __forceinline__ uint64_t vreal(const Dirty& d, uint64_t u) {
     return d.s[2] + u;
 }
 
+constexpr uint64_t CLEANUP_MIN_TILE = 2048;  // keys per cleanup tile (at least)
+constexpr uint64_t CLEANUP_MAX_TILES = 8192; // tiles per side, at most (=> O(1) aux)
+// tiles per side for an n-key segment: n/2^14 clamped to [64, 8192]
+__host__ __device__ __forceinline__ uint64_t cleanup_max_tiles(uint64_t n) {
+    uint64_t c = n >> 14;
+    return c < 64 ? 64 : (c > CLEANUP_MAX_TILES ? CLEANUP_MAX_TILES : c);
+}
+
 // Build the sorted, merged dirty set from up to 3 intervals [a,b) and fill
-// K, W, Kv and the cleanup geometry of the control block.
-static __device__ void finish_ctl(Ctl* c, uint64_t n, uint64_t K, uint64_t a[3], uint64_t b[3], uint64_t tile,
-                                  uint64_t R) {
+// K, W, Kv and the cleanup geometry of the control block.  The tile size
+// grows with the dirty-set size so that each side has <= CLEANUP_MAX_TILES
+// tiles (aux memory independent of n).
+static __device__ void finish_ctl(Ctl* c, uint64_t n, uint64_t K, uint64_t a[3], uint64_t b[3]) {
     // sort by start (3 elements), drop empties, merge overlaps / adjacency
     for (int i = 0; i < 3; ++i)
         for (int j = i + 1; j < 3; ++j)
@@ -312,12 +332,16 @@ static __device__ void finish_ctl(Ctl* c, uint64_t n, uint64_t K, uint64_t a[3],
             c->dl[i] = 0;
         }
     }
+    uint64_t side = Kv > W - Kv ? Kv : W - Kv;
+    const uint64_t cap = cleanup_max_tiles(n);
+    uint64_t tile = (side + cap - 1) / cap;
+    if (tile < CLEANUP_MIN_TILE) tile = CLEANUP_MIN_TILE;
     c->n = n;
     c->K = K;
     c->W = W;
     c->Kv = Kv;
     c->tile = tile;
-    c->R = R;
+    c->R = 0;
     c->nL = (Kv + tile - 1) / tile;
     c->nR = (W - Kv + tile - 1) / tile;
     c->ML = c->MR = 0;
@@ -361,12 +385,13 @@ __device__ __forceinline__ void scan_chunk(const K* __restrict__ keys, const Dir
 #pragma unroll
     for (int k = 0; k < SW_EPT; ++k) {
         const uint64_t uu = u + (uint64_t)k * SW_NT + tid;
-        bool f = false;
         it.x[k] = 0;
-        if (uu < uend) {
-            it.x[k] = keys[vreal(d, uu)];
-            f = (is_pred(it.x[k], pivot) == want_pred);
-        }
+        if (uu < uend) it.x[k] = keys[vreal(d, uu)];
+    }
+#pragma unroll
+    for (int k = 0; k < SW_EPT; ++k) {
+        const uint64_t uu = u + (uint64_t)k * SW_NT + tid;
+        const bool f = uu < uend && (is_pred(it.x[k], pivot) == want_pred);
         ball[k] = __ballot_sync(0xffffffffu, f);
         it.flags |= (f ? 1u : 0u) << k;
     }
@@ -375,7 +400,7 @@ __device__ __forceinline__ void scan_chunk(const K* __restrict__ keys, const Dir
         for (int k = 0; k < SW_EPT; ++k) cnt[k][warp] = __popc(ball[k]);
     }
     __syncthreads();
-    uint32_t before = 0, total = 0;
+    uint32_t before = 0;
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int k = 0; k < SW_EPT; ++k) {
@@ -389,13 +414,14 @@ __device__ __forceinline__ void scan_chunk(const K* __restrict__ keys, const Dir
         it.rank[k] = before + wbefore + __popc(ball[k] & lt);
         before += ktot;
     }
-    total = before;
-    it.total = total;
+    it.total = before;
     __syncthreads();  // cnt may be rewritten by the next chunk
 }
 
 // Collect up to `need` items from [u, uend) in order into pos/val; advances u
 // to just past the last collected item (or to the end of the scanned range).
+// Only elements at positions before the last collected item influence the
+// result, so elements past it may be concurrently rewritten by another CTA.
 template <typename K>
 __device__ uint32_t collect_items(const K* __restrict__ keys, const Dirty& d, K pivot, bool want_pred, uint64_t& u,
                                   uint64_t uend, uint32_t need, uint64_t* pos, K* val, WalkBuf<K>& wb) {
@@ -455,8 +481,8 @@ __device__ uint64_t select_item(const K* __restrict__ keys, const Dirty& d, K pi
 
 // Rank-matched walk: pairs the i-th misplaced successor of [uL, uLend) with
 // the i-th misplaced predecessor of [uR, uRend), for up to max_pairs pairs,
-// and swaps each pair (one thread per pair).  Only this CTA touches the two
-// ranges, so the swaps are exclusive (EREW).
+// and swaps each pair (one thread per pair).  Only this CTA writes inside
+// the two ranges, so the swaps are exclusive (EREW).
 template <typename K>
 __device__ void walk_swap(K* __restrict__ keys, const Dirty& d, K pivot, uint64_t uL, uint64_t uLend, uint64_t uR,
                           uint64_t uRend, uint64_t max_pairs, WalkBuf<K>& wb) {

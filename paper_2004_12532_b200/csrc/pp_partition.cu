@@ -41,8 +41,8 @@ template <typename K>
 __global__ void __launch_bounds__(256) window_reduce_kernel(const K* __restrict__ keys, uint64_t n, uint64_t h,
                                                             uint64_t n_lines, uint32_t LK,
                                                             const GroupOut* __restrict__ go, uint32_t g,
-                                                            K pivot, Ctl* __restrict__ ctl, uint64_t tile,
-                                                            uint64_t R, uint64_t* __restrict__ d_split) {
+                                                            K pivot, Ctl* __restrict__ ctl,
+                                                            uint64_t* __restrict__ d_split) {
     __shared__ uint64_t sT[8], sMin[8], sMax[8], sHT[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t region_end = n_lines * LK;
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) window_reduce_kernel(const K* __restrict_
         b[1] = hi > Ksplit ? hi : Ksplit;
         if (vmin > vmax) { a[1] = b[1] = 0; }             // no non-empty group: no window
         a[2] = tail0; b[2] = n;                            // tail
-        finish_ctl(ctl, n, Ksplit, a, b, tile, R);
+        finish_ctl(ctl, n, Ksplit, a, b);
         ctl->vmin = lo;
         ctl->vmax = hi;
         if (d_split) *d_split = Ksplit;
@@ -113,13 +113,13 @@ __global__ void __launch_bounds__(256) count_kernel(const K* __restrict__ keys, 
     }
 }
 __global__ void __launch_bounds__(256) count_finish_kernel(const uint64_t* __restrict__ partial, int np,
-                                                           uint64_t n, Ctl* __restrict__ ctl, uint64_t tile,
-                                                           uint64_t R, uint64_t* __restrict__ d_split) {
+                                                           uint64_t n, Ctl* __restrict__ ctl,
+                                                           uint64_t* __restrict__ d_split) {
     if (threadIdx.x == 0) {
         uint64_t K = 0;
         for (int i = 0; i < np; ++i) K += partial[i];
         uint64_t a[3] = {0, n, n}, b[3] = {n, n, n};
-        finish_ctl(ctl, n, K, a, b, tile, R);
+        finish_ctl(ctl, n, K, a, b);
         ctl->vmin = 0;
         ctl->vmax = n;
         if (d_split) *d_split = K;
@@ -226,16 +226,20 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(Ctl* __restrict__ ctl, 
         ctl->ML = ML;
         ctl->MR = carry;
         if (ML != carry) ctl->err = 1;  // #misplaced successors must equal #misplaced predecessors
-        const uint64_t M = ML < carry ? ML : carry;
-        ctl->nTasks = (M + ctl->R - 1) / ctl->R;
+        // one swap task per breakpoint of the merged tile rank boundaries
+        ctl->nTasks = (ML == carry && ML > 0) ? nL + nR : 0;
     }
 }
 
 // ===========================================================================
 // K5a: locate the start of every swap task (one CTA per task, grid-stride).
-// posL[j] = virtual index of the (jR)-th misplaced successor in [0,Kv);
-// posR[j] = virtual index of the (jR)-th misplaced predecessor in [Kv,W);
-// posL[nTasks] = Kv, posR[nTasks] = W (sentinels).
+// Tasks are the breakpoints of the merged rank boundaries of the left tiles
+// (PL) and the right tiles (PR): task k covers ranks [U_k, U_{k+1}) where U
+// is the sorted merge of PL[0..nL) and PR[0..nR) (duplicates kept: empty
+// tasks), so each task's items lie inside ONE left tile and ONE right tile
+// -- every walk is bounded by the tile size, whatever the item density.
+// rk[k] = U_k; posL[k] / posR[k] = virtual index of the misplaced
+// successor / predecessor of rank U_k (Kv / W if U_k = M): sentinels at k = nTasks.
 // ===========================================================================
 __device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__ a, uint64_t n, uint64_t x) {
     uint64_t lo = 0, hi = n;
@@ -246,22 +250,33 @@ __device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__
     return lo;
 }
 
+// k-th smallest (0-based) of the merge of sorted A[0..na) and B[0..nb) (merge path)
+__device__ __forceinline__ uint64_t merged_kth(const uint64_t* __restrict__ A, uint64_t na,
+                                               const uint64_t* __restrict__ B, uint64_t nb, uint64_t k) {
+    uint64_t lo = k > nb ? k - nb : 0, hi = k < na ? k : na;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (A[mid] <= B[k - 1 - mid]) lo = mid + 1; else hi = mid;
+    }
+    const uint64_t i = lo, j = k - lo;
+    if (i < na && (j >= nb || A[i] <= B[j])) return A[i];
+    return B[j];
+}
+
 template <typename K>
 __global__ void __launch_bounds__(SW_NT) locate_kernel(const K* __restrict__ keys, Ctl* __restrict__ ctl, K pivot,
                                                        const uint64_t* __restrict__ PL,
                                                        const uint64_t* __restrict__ PR,
-                                                       uint64_t* __restrict__ posL, uint64_t* __restrict__ posR) {
+                                                       uint64_t* __restrict__ posL, uint64_t* __restrict__ posR,
+                                                       uint64_t* __restrict__ rk) {
     __shared__ WalkBuf<K> wb;
     const Dirty d = load_dirty(ctl);
-    const uint64_t Kv = ctl->Kv, W = ctl->W, T = ctl->tile, nL = ctl->nL, nR = ctl->nR, R = ctl->R;
+    const uint64_t Kv = ctl->Kv, W = ctl->W, T = ctl->tile, nL = ctl->nL, nR = ctl->nR, M = ctl->ML;
     const uint64_t nTasks = ctl->nTasks;
     for (uint64_t j = blockIdx.x; j <= nTasks; j += gridDim.x) {
-        uint64_t pl, pr;
-        if (j == nTasks) {
-            pl = Kv;
-            pr = W;
-        } else {
-            const uint64_t r = j * R;
+        const uint64_t r = j < nTasks ? merged_kth(PL, nL, PR, nR, j) : M;
+        uint64_t pl = Kv, pr = W;
+        if (r < M) {
             const uint64_t tl = upper_bound_u64(PL, nL, r) - 1;
             pl = select_item<K>(keys, d, pivot, false, tl * T, min(tl * T + T, Kv), r - PL[tl], wb);
             const uint64_t tr = upper_bound_u64(PR, nR, r) - 1;
@@ -270,6 +285,7 @@ __global__ void __launch_bounds__(SW_NT) locate_kernel(const K* __restrict__ key
         if (threadIdx.x == 0) {
             posL[j] = pl;
             posR[j] = pr;
+            rk[j] = r;
         }
     }
 }
@@ -280,12 +296,14 @@ __global__ void __launch_bounds__(SW_NT) locate_kernel(const K* __restrict__ key
 template <typename K>
 __global__ void __launch_bounds__(SW_NT) swap_kernel(K* __restrict__ keys, const Ctl* __restrict__ ctl, K pivot,
                                                      const uint64_t* __restrict__ posL,
-                                                     const uint64_t* __restrict__ posR) {
+                                                     const uint64_t* __restrict__ posR,
+                                                     const uint64_t* __restrict__ rk) {
     __shared__ WalkBuf<K> wb;
     const Dirty d = load_dirty(ctl);
-    const uint64_t nTasks = ctl->nTasks, R = ctl->R, M = ctl->ML;
+    const uint64_t nTasks = ctl->nTasks;
     for (uint64_t j = blockIdx.x; j < nTasks; j += gridDim.x) {
-        const uint64_t pairs = min(R, M - j * R);
+        const uint64_t pairs = rk[j + 1] - rk[j];
+        if (pairs == 0) continue;
         walk_swap<K>(keys, d, pivot, posL[j], posL[j + 1], posR[j], posR[j + 1], pairs, wb);
     }
 }
@@ -314,7 +332,7 @@ __global__ void __launch_bounds__(SW_NT) small_partition_kernel(K* __restrict__ 
     if (threadIdx.x == 0) {
         if (ctl) {
             uint64_t a[3] = {0, n, n}, b[3] = {n, n, n};
-            finish_ctl(ctl, n, Ksplit, a, b, 1, 1);
+            finish_ctl(ctl, n, Ksplit, a, b);
             ctl->vmin = 0;
             ctl->vmax = n;
         }
@@ -371,11 +389,6 @@ int timing_read(double* out) {
     return 0;
 }
 
-static uint64_t pow2ceil(uint64_t x) {
-    uint64_t p = 1;
-    while (p < x) p <<= 1;
-    return p;
-}
 
 // ---------------------------------------------------------------------------
 // Group-kernel variants (line size, threads, prefetch depth, store path),
@@ -453,10 +466,15 @@ static int cur_variant() {
 }
 
 struct Layout {
-    size_t ctl, gout, cntL, cntR, PL, PR, posL, posR, partial, total;
+    size_t ctl, gout, cntL, cntR, PL, PR, posL, posR, rk, partial, total;
 };
 
-static Layout make_layout(uint64_t g, uint64_t maxTiles, uint64_t maxTasks, uint64_t nPartial) {
+// Workspace: fixed-size cleanup arrays (CLEANUP_MAX_TILES per side, the tile
+// size adapts to the dirty set on the device) + one GroupOut per group: the
+// auxiliary memory does not grow with n beyond the g <= #SM x occupancy groups.
+static Layout make_layout(uint64_t n, uint64_t g, bool cleanup, uint64_t nPartial) {
+    const uint64_t maxTiles = cleanup ? cleanup_max_tiles(n) + 1 : 1;
+    const uint64_t maxTasks = cleanup ? 2 * cleanup_max_tiles(n) + 1 : 1;
     Layout L;
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -472,20 +490,10 @@ static Layout make_layout(uint64_t g, uint64_t maxTiles, uint64_t maxTasks, uint
     L.PR = take(8 * maxTiles);
     L.posL = take(8 * (maxTasks + 1));
     L.posR = take(8 * (maxTasks + 1));
+    L.rk = take(8 * (maxTasks + 1));
     L.partial = take(8 * nPartial);
     L.total = o;
     return L;
-}
-
-// Cleanup geometry: tile T and ranks-per-task R grow with n so that the
-// tile and task arrays stay <= 2^18 entries (aux memory o(n)).
-static void cleanup_geometry(uint64_t n, uint64_t& tile, uint64_t& R, uint64_t& maxTiles, uint64_t& maxTasks) {
-    const Params& P = params();
-    const uint64_t scale = pow2ceil((n + (1u << 18) - 1) >> 18);
-    tile = P.tile > 0 ? (uint64_t)P.tile : std::max<uint64_t>(2048, scale);
-    R = P.ranks > 0 ? (uint64_t)P.ranks : std::max<uint64_t>(1024, scale);
-    maxTiles = n / tile + 2;
-    maxTasks = n / 2 / R + 2;
 }
 
 template <typename K>
@@ -517,12 +525,10 @@ pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64
     if (path == 2 && n_lines == 0) path = 1;
     S.path = path;
 
-    uint64_t tile, R, maxTiles, maxTasks;
-    cleanup_geometry(n, tile, R, maxTiles, maxTasks);
     const int grid_cleanup = sm_count() * 4;
     const uint64_t g = path == 2 ? choose_groups<K>(n_lines, vi.occ) : 0;
     const int nPartial = sm_count() * 2;
-    Layout L = make_layout(g, path == 1 ? 1 : maxTiles, path == 1 ? 1 : maxTasks, nPartial);
+    Layout L = make_layout(n, g, path != 1, nPartial);
     unsigned char* ws = static_cast<unsigned char*>(workspace(L.total, st));
     if (!ws) return PP_E_NOMEM;
     Ctl* ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
@@ -543,12 +549,12 @@ pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64
             launch_group<K>(variant, keys + h, n_lines, (uint32_t)g, P.seed, pivot, gout, st);
             timing_mark(st);
             window_reduce_kernel<K><<<1, 256, 0, st>>>(keys, n, h, n_lines, (uint32_t)LK, gout, (uint32_t)g, pivot,
-                                                       ctl, tile, R, d_split);
+                                                       ctl, d_split);
             note_launches(2);
         } else {
             uint64_t* partial = reinterpret_cast<uint64_t*>(ws + L.partial);
             count_kernel<K><<<nPartial, 256, 0, st>>>(keys, n, pivot, partial);
-            count_finish_kernel<<<1, 32, 0, st>>>(partial, nPartial, n, ctl, tile, R, d_split);
+            count_finish_kernel<<<1, 32, 0, st>>>(partial, nPartial, n, ctl, d_split);
             note_launches(2);
             timing_mark(st);
         }
@@ -558,10 +564,11 @@ pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64
         uint64_t* PR = reinterpret_cast<uint64_t*>(ws + L.PR);
         uint64_t* posL = reinterpret_cast<uint64_t*>(ws + L.posL);
         uint64_t* posR = reinterpret_cast<uint64_t*>(ws + L.posR);
+        uint64_t* rk = reinterpret_cast<uint64_t*>(ws + L.rk);
         tile_count_kernel<K><<<grid_cleanup, 256, 0, st>>>(keys, ctl, pivot, cntL, cntR);
         tile_scan_kernel<<<1, 1024, 0, st>>>(ctl, cntL, cntR, PL, PR);
-        locate_kernel<K><<<grid_cleanup, SW_NT, 0, st>>>(keys, ctl, pivot, PL, PR, posL, posR);
-        swap_kernel<K><<<grid_cleanup, SW_NT, 0, st>>>(keys, ctl, pivot, posL, posR);
+        locate_kernel<K><<<grid_cleanup, SW_NT, 0, st>>>(keys, ctl, pivot, PL, PR, posL, posR, rk);
+        swap_kernel<K><<<grid_cleanup, SW_NT, 0, st>>>(keys, ctl, pivot, posL, posR, rk);
         note_launches(4);
     }
     timing_mark(st);

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys,
     if (vmin > vmax) { a[1] = b[1] = 0; }
     a[2] = h + region_end; b[2] = len;
     Ctl c;
-    finish_ctl(&c, len, Ks, a, b, 1, 1);
+    finish_ctl(&c, len, Ks, a, b);
     Dirty d;
 #pragma unroll
     for (int k = 0; k < 3; ++k) { d.s[k] = c.ds[k]; d.l[k] = c.dl[k]; }
