@@ -1,7 +1,7 @@
 // pp_engine.cuh -- device building blocks shared by the partition and the
 // quicksort translation units:
-//   * ss_group_engine: one CTA's Smoothed Striding group partition
-//     (Fig. 3);
+//   * ss_group_engine (pp_group.cuh): one CTA's Smoothed Striding group
+//     partition (Fig. 3);
 //   * the dirty-set helpers and finish_ctl (window bookkeeping,
 //     PAPER.md:979-1001);
 //   * the CTA chunk scanner, select and the rank-matched walk used by the
@@ -9,261 +9,10 @@
 //     predecessor right of K).
 #pragma once
 #include "pp_device.cuh"
+#include "pp_group.cuh"
 #include "pp_internal.h"
 
 namespace pp {
-
-// ===========================================================================
-// K3: Smoothed Striding group partition.
-// ===========================================================================
-// LINE_BYTES = b * sizeof(K) (the paper's cache line of b elements,
-// PAPER.md:747, 814-816; b = 512 elements there).
-// NT threads; PF lines in flight per end; TMA_STORE: resolved lines leave
-// shared memory through the bulk-copy engine instead of thread stores.
-template <typename K, int LINE_BYTES, int NT_, int PF_, bool TMA_STORE_>
-struct GroupCfgT {
-    using Key = K;
-    static constexpr int LK = LINE_BYTES / (int)sizeof(K);
-    static constexpr int NT = NT_;
-    static constexpr int PF = PF_;
-    static constexpr bool TMA_STORE = TMA_STORE_;
-    static constexpr int VEC = 16 / (int)sizeof(K);
-    static constexpr int VPT = LK / (NT * VEC);  // 16-B vectors per thread per line
-    static constexpr int KPT = VPT * VEC;
-    static constexpr int NW = NT / 32;
-    static constexpr int POOL = 2 * LK;          // pool ring capacity (occupancy <= 2b)
-    static constexpr int LTAB = 16;              // line-index table entries per end
-    static constexpr size_t SMEM =
-        (size_t)(2 * PF * LK + 2 * POOL) * sizeof(K) + 2 * PF * 8 + 4 * ((NW + 7) / 8 * 8) + 4 * 2 * LTAB + 16;
-    static_assert(VPT >= 1 && VPT * NT * VEC == LK, "line must be a multiple of NT 16-B vectors");
-    static_assert((POOL & (POOL - 1)) == 0, "pool ring must be a power of two");
-    static_assert(PF + 3 < LTAB, "line table too small for the prefetch depth");
-};
-
-// the default configuration (used by quicksort and by variant 0)
-template <typename K>
-using GroupCfg = GroupCfgT<K, 8192, 256, 4, false>;
-
-// Line index of the j-th line (group order) of group gi: G_i(j) of
-// PAPER.md:963-969 in 0-based form, j*g + ((X[j] + i) mod g).
-__device__ __forceinline__ uint64_t group_line(uint64_t seed, uint32_t g, uint32_t gi, uint32_t j) {
-    uint32_t x = ss_offset(seed, (uint64_t)j, g) + gi;
-    if (x >= g) x -= g;
-    return (uint64_t)j * g + x;
-}
-
-// One CTA partitions group gi of the region (n_lines full lines of LK keys).
-// The group's lines in group order are consumed from both ends; predecessors
-// and successors are appended to two shared-memory pools; a front line is
-// written back (all predecessors) when the predecessor pool holds a line's
-// worth and a consumed-but-unwritten front slot exists, a back line likewise
-// with successors.  At the end the <= 2 open lines get the remaining
-// predecessors then successors.  => the group's first T_i elements (group
-// order) are predecessors: exactly the Partial Partition Step's postcondition
-// (PAPER.md:979-1001), with every line read once and written once.
-//
-// Control state is uniform (every thread tracks it); only thread 0 issues the
-// bulk copies.  Line indices are hashed once, at claim time, into a small
-// shared table (ltab) that the write phase reads back.
-template <typename C>
-__device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n_lines, uint32_t g, uint32_t gi,
-                                uint64_t seed, typename C::Key pivot, GroupOut* __restrict__ out,
-                                unsigned char* smem) {
-    using K = typename C::Key;
-    constexpr int LK = C::LK, NT = C::NT, PF = C::PF, VEC = C::VEC, VPT = C::VPT, KPT = C::KPT, NW = C::NW;
-    constexpr uint32_t PMASK = C::POOL - 1;
-    constexpr uint32_t LBYTES = LK * sizeof(K);
-    constexpr int LT = C::LTAB;
-
-    K* ring = reinterpret_cast<K*>(smem);         // [2][PF][LK]: front ring, back ring
-    K* tpool = ring + 2 * PF * LK;                // predecessor pool (ring of 2 lines)
-    K* fpool = tpool + C::POOL;                   // successor pool
-    uint64_t* bars = reinterpret_cast<uint64_t*>(fpool + C::POOL);
-    uint32_t* wtrue = reinterpret_cast<uint32_t*>(bars + 2 * PF);
-    uint32_t* ltab = wtrue + (NW + 7) / 8 * 8;    // [2][LT] line indices (front, back)
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t lt = lanemask_lt();
-
-    // number of lines of this group: s-1 full chunks + the last chunk's line if it exists
-    const uint32_t s = (uint32_t)((n_lines + g - 1) / g);
-    int S = 0;
-    if (s > 0) S = (int)s - 1 + (group_line(seed, g, gi, s - 1) < n_lines ? 1 : 0);
-
-    if (tid == 0) {
-        for (int k = 0; k < 2 * PF; ++k) mbar_init(&bars[k], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    int fpf = 0, bpf = S - 1;  // next line to claim for the front / back ring
-    int fc = 0, bc = S - 1;    // next line to consume from the front / back
-    int fw = 0, bw = S - 1;    // front lines [0,fw) and back lines (bw,S-1] are written
-    uint32_t th = 0, tt = 0, fh = 0, ft = 0;  // pool head/tail counters (mod 2^32)
-
-    auto claim_front = [&]() {
-        if (tid == 0) {
-            const uint32_t slot = (uint32_t)fpf % PF;
-            const uint32_t line = (uint32_t)group_line(seed, g, gi, (uint32_t)fpf);
-            ltab[fpf & (LT - 1)] = line;
-            mbar_expect_tx(&bars[slot], LBYTES);
-            bulk_g2s(ring + slot * LK, region + (uint64_t)line * LK, LBYTES, &bars[slot]);
-        }
-        ++fpf;
-    };
-    auto claim_back = [&]() {
-        if (tid == 0) {
-            const uint32_t kk = (uint32_t)(S - 1 - bpf);
-            const uint32_t slot = kk % PF;
-            const uint32_t line = (uint32_t)group_line(seed, g, gi, (uint32_t)bpf);
-            ltab[LT + (kk & (LT - 1))] = line;
-            mbar_expect_tx(&bars[PF + slot], LBYTES);
-            bulk_g2s(ring + (PF + slot) * LK, region + (uint64_t)line * LK, LBYTES, &bars[PF + slot]);
-        }
-        --bpf;
-    };
-    // array line index of group line j (claimed by the front ring iff j < fpf)
-    auto line_index = [&](int j) -> uint32_t {
-        return j < fpf ? ltab[j & (LT - 1)] : ltab[LT + ((S - 1 - j) & (LT - 1))];
-    };
-    auto store_line = [&](const K* pool, uint32_t head, int j) {
-        K* dst = region + (uint64_t)line_index(j) * LK;
-        const K* src = pool + (head & PMASK);
-        if constexpr (C::TMA_STORE) {
-            if (tid == 0) {
-                bulk_s2g(dst, src, LBYTES);
-                bulk_commit();
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < VPT; ++q) {
-                const int off = (q * NT + tid) * VEC;
-                *reinterpret_cast<uint4*>(dst + off) = *reinterpret_cast<const uint4*>(src + off);
-            }
-        }
-    };
-    for (int k = 0; k < PF; ++k) {
-        if (fpf <= bpf) claim_front();
-        if (fpf <= bpf) claim_back();
-    }
-
-    while (fc <= bc) {
-        // ---- choose the end to consume (uniform across the CTA) ----
-        const uint32_t tocc = tt - th, focc = ft - fh;
-        const int nF = fc - fw, nB = bw - bc;  // consumed-but-unwritten slots
-        bool front;
-        if (tocc >= (uint32_t)LK && nF == 0) front = true;
-        else if (focc >= (uint32_t)LK && nB == 0) front = false;
-        else front = (nF <= nB);
-        const int l = front ? fc : bc;
-        uint32_t bi, par;
-        if (l < fpf) {
-            bi = (uint32_t)l % PF;
-            par = ((uint32_t)l / PF) & 1u;
-        } else {
-            const uint32_t kk = (uint32_t)(S - 1 - l);
-            bi = PF + kk % PF;
-            par = (kk / PF) & 1u;
-        }
-        const K* src = ring + bi * LK;
-        mbar_wait(&bars[bi], par);
-
-        // ---- classify: warp ballots, slot-major order within the warp ----
-        K x[KPT];
-#pragma unroll
-        for (int q = 0; q < VPT; ++q) {
-            Vec16<K> v = *reinterpret_cast<const Vec16<K>*>(src + (q * NT + tid) * VEC);
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) x[q * VEC + e] = v.v[e];
-        }
-        uint32_t ball[KPT];
-        uint32_t wt = 0;
-#pragma unroll
-        for (int k = 0; k < KPT; ++k) {
-            ball[k] = __ballot_sync(0xffffffffu, is_pred(x[k], pivot));
-            wt += __popc(ball[k]);
-        }
-        if (lane == 0) wtrue[warp] = wt;
-        if constexpr (C::TMA_STORE) {
-            // pool slots written out by the bulk engine must be read before reuse
-            if (tid == 0) bulk_wait_read<0>();
-        }
-        __syncthreads();  // (A) warp totals visible; previous write phase finished
-        uint32_t woff = 0, tot = 0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            const uint32_t c = wtrue[w];
-            woff += (w < warp) ? c : 0u;
-            tot += c;
-        }
-        const uint32_t toff = tt + woff;
-        const uint32_t foff = ft + (uint32_t)(warp * 32 * KPT) - woff;
-        uint32_t acc = 0;
-#pragma unroll
-        for (int k = 0; k < KPT; ++k) {
-            const uint32_t b = ball[k];
-            const uint32_t rt = acc + __popc(b & lt);
-            const uint32_t before = (uint32_t)(k * 32 + lane);
-            if ((b >> lane) & 1u) tpool[(toff + rt) & PMASK] = x[k];
-            else fpool[(foff + before - rt) & PMASK] = x[k];
-            acc += __popc(b);
-        }
-        __syncthreads();  // (B) pools complete; ring slot free for reuse
-        tt += tot;
-        ft += (uint32_t)LK - tot;
-        if (front) ++fc; else --bc;
-
-        // ---- refill the rings (thread 0 issues, everyone tracks) ----
-        while (fpf <= bpf && fpf - fc < PF) claim_front();
-        while (bpf >= fpf && bc - bpf < PF) claim_back();
-
-        // ---- write resolved lines ----
-        if constexpr (C::TMA_STORE) {
-            if (tid == 0) fence_proxy_async();  // generic smem writes -> async-proxy reads
-        }
-        for (;;) {
-            if (tt - th >= (uint32_t)LK && fw < fc) {
-                store_line(tpool, th, fw);
-                th += LK;
-                ++fw;
-            } else if (ft - fh >= (uint32_t)LK && bw > bc) {
-                store_line(fpool, fh, bw);
-                fh += LK;
-                --bw;
-            } else {
-                break;
-            }
-        }
-    }
-
-    // ---- final flush: open lines [fw, bw] get predecessors then successors ----
-    const uint32_t tp = tt - th;
-    for (int jl = fw; jl <= bw; ++jl) {
-        K* dst = region + (uint64_t)line_index(jl) * LK;
-        const uint32_t base = (uint32_t)(jl - fw) * LK;
-        for (int e = tid; e < LK; e += NT) {
-            const uint32_t q = base + e;
-            dst[e] = (q < tp) ? tpool[(th + q) & PMASK] : fpool[(fh + (q - tp)) & PMASK];
-        }
-    }
-    if constexpr (C::TMA_STORE) {
-        if (tid == 0) bulk_wait<0>();
-    }
-    if (tid == 0) {
-        const uint64_t T = (uint64_t)fw * LK + tp;
-        GroupOut o;
-        o.T = T;
-        if (S == 0) {
-            o.vlo = n_lines * LK;
-            o.vhi = 0;
-        } else if (T == (uint64_t)S * LK) {
-            o.vlo = o.vhi = group_line(seed, g, gi, (uint32_t)(S - 1)) * LK + LK;
-        } else {
-            o.vlo = o.vhi = group_line(seed, g, gi, (uint32_t)(T / LK)) * LK + T % LK;
-        }
-        *out = o;
-    }
-}
 
 // ===========================================================================
 // Dirty set helpers.
@@ -477,6 +226,139 @@ __device__ uint64_t select_item(const K* __restrict__ keys, const Dirty& d, K pi
         u += SW_CH;
     }
     return u1;
+}
+
+// ===========================================================================
+// One-round-trip scan of a left range and a right range of <= SW_RNG
+// elements each (both sides' loads in flight together): the cleanup's fast
+// path when the tile size is CLEANUP_MIN_TILE.  Left items are successors,
+// right items predecessors; ranks in ascending position order per side.
+// ===========================================================================
+constexpr int SW_EPT2 = 8;
+constexpr int SW_RNG = SW_NT * SW_EPT2;  // == CLEANUP_MIN_TILE
+
+template <typename K>
+struct PairScan {
+    K xl[SW_EPT2], xr[SW_EPT2];
+    uint32_t rl[SW_EPT2], rr[SW_EPT2];
+    uint32_t fl, fr;     // item flags per element slot
+    uint32_t tl, tr;     // item totals
+};
+
+template <typename K>
+__device__ __forceinline__ void scan_pair(const K* __restrict__ keys, const Dirty& d, K pivot, uint64_t uL,
+                                          uint64_t uLend, uint64_t uR, uint64_t uRend,
+                                          uint32_t (*cnt)[SW_EPT2][SW_NT / 32], PairScan<K>& ps) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int k = 0; k < SW_EPT2; ++k) {
+        const uint64_t a = uL + (uint64_t)k * SW_NT + tid, b = uR + (uint64_t)k * SW_NT + tid;
+        ps.xl[k] = a < uLend ? keys[vreal(d, a)] : (K)0;
+        ps.xr[k] = b < uRend ? keys[vreal(d, b)] : (K)0;
+    }
+    uint32_t bl[SW_EPT2], br[SW_EPT2];
+    ps.fl = ps.fr = 0;
+#pragma unroll
+    for (int k = 0; k < SW_EPT2; ++k) {
+        const uint64_t a = uL + (uint64_t)k * SW_NT + tid, b = uR + (uint64_t)k * SW_NT + tid;
+        const bool fl = a < uLend && !is_pred(ps.xl[k], pivot);
+        const bool fr = b < uRend && is_pred(ps.xr[k], pivot);
+        bl[k] = __ballot_sync(0xffffffffu, fl);
+        br[k] = __ballot_sync(0xffffffffu, fr);
+        ps.fl |= (fl ? 1u : 0u) << k;
+        ps.fr |= (fr ? 1u : 0u) << k;
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < SW_EPT2; ++k) {
+            cnt[0][k][warp] = __popc(bl[k]);
+            cnt[1][k][warp] = __popc(br[k]);
+        }
+    }
+    __syncthreads();
+    const uint32_t lt = lanemask_lt();
+    uint32_t beforeL = 0, beforeR = 0;
+#pragma unroll
+    for (int k = 0; k < SW_EPT2; ++k) {
+        uint32_t wl = 0, wr = 0, kl = 0, kr = 0;
+#pragma unroll
+        for (int w = 0; w < SW_NT / 32; ++w) {
+            const uint32_t cl = cnt[0][k][w], cr = cnt[1][k][w];
+            wl += (w < warp) ? cl : 0u;
+            wr += (w < warp) ? cr : 0u;
+            kl += cl;
+            kr += cr;
+        }
+        ps.rl[k] = beforeL + wl + __popc(bl[k] & lt);
+        ps.rr[k] = beforeR + wr + __popc(br[k] & lt);
+        beforeL += kl;
+        beforeR += kr;
+    }
+    ps.tl = beforeL;
+    ps.tr = beforeR;
+    __syncthreads();  // cnt reusable
+}
+
+template <typename K>
+struct PairBuf {
+    K lval[SW_RNG], rval[SW_RNG];
+    uint32_t cnt[2][SW_EPT2][SW_NT / 32];
+    uint64_t sel[2];
+};
+
+// Positions of the left item of rank rl in [uL, uLend) and the right item of
+// rank rr in [uR, uRend) (ranges <= SW_RNG); returns uLend / uRend if absent.
+template <typename K>
+__device__ __forceinline__ void select_pair(const K* __restrict__ keys, const Dirty& d, K pivot, uint64_t uL,
+                                            uint64_t uLend, uint64_t rl, uint64_t uR, uint64_t uRend, uint64_t rr,
+                                            PairBuf<K>& pb, uint64_t& pl, uint64_t& pr) {
+    PairScan<K> ps;
+    if (threadIdx.x == 0) {
+        pb.sel[0] = uLend;
+        pb.sel[1] = uRend;
+    }
+    scan_pair<K>(keys, d, pivot, uL, uLend, uR, uRend, pb.cnt, ps);
+#pragma unroll
+    for (int k = 0; k < SW_EPT2; ++k) {
+        const uint64_t off = (uint64_t)k * SW_NT + threadIdx.x;
+        if (((ps.fl >> k) & 1u) && ps.rl[k] == rl) pb.sel[0] = uL + off;
+        if (((ps.fr >> k) & 1u) && ps.rr[k] == rr) pb.sel[1] = uR + off;
+    }
+    __syncthreads();
+    pl = pb.sel[0];
+    pr = pb.sel[1];
+    __syncthreads();
+}
+
+template <typename K>
+union CleanupSmem {
+    WalkBuf<K> wb;
+    PairBuf<K> pb;
+};
+
+// Swap the i-th misplaced successor of [uL, uLend) with the i-th misplaced
+// predecessor of [uR, uRend), for i < npairs (ranges <= SW_RNG; all items of
+// both ranges belong to this CTA).  Values cross through shared memory by
+// rank; each thread writes back its own items' positions.
+template <typename K>
+__device__ __forceinline__ void swap_pair(K* __restrict__ keys, const Dirty& d, K pivot, uint64_t uL,
+                                          uint64_t uLend, uint64_t uR, uint64_t uRend, uint64_t npairs,
+                                          PairBuf<K>& pb) {
+    PairScan<K> ps;
+    scan_pair<K>(keys, d, pivot, uL, uLend, uR, uRend, pb.cnt, ps);
+#pragma unroll
+    for (int k = 0; k < SW_EPT2; ++k) {
+        if (((ps.fl >> k) & 1u) && ps.rl[k] < npairs) pb.lval[ps.rl[k]] = ps.xl[k];
+        if (((ps.fr >> k) & 1u) && ps.rr[k] < npairs) pb.rval[ps.rr[k]] = ps.xr[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < SW_EPT2; ++k) {
+        const uint64_t off = (uint64_t)k * SW_NT + threadIdx.x;
+        if (((ps.fl >> k) & 1u) && ps.rl[k] < npairs) keys[vreal(d, uL + off)] = pb.rval[ps.rl[k]];
+        if (((ps.fr >> k) & 1u) && ps.rr[k] < npairs) keys[vreal(d, uR + off)] = pb.lval[ps.rr[k]];
+    }
+    __syncthreads();
 }
 
 // Rank-matched walk: pairs the i-th misplaced successor of [uL, uLend) with

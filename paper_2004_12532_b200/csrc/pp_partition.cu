@@ -6,18 +6,20 @@
 //                        per group U_i, a two-ended in-place partition of the
 //                        group's lines staged through shared memory by the TMA
 //                        bulk-copy engine; every line read once, written once.
-//   K4 window_reduce     K = sum T_i, v_min, v_max and the
-//                        dirty set D = head U [v_min,v_max) U tail.
-//   K1 tile_count        per-tile misplaced counts over D (PAPER.md:288-291 D
-//                        array, counted per tile like the paper's per-64/4096
-//                        chunk counts PAPER.md:1443-1450, 1479-1486).
+//   K4+K1 reduce_count   every CTA reduces the group outputs: K = sum T_i,
+//                        v_min, v_max and the dirty set
+//                        D = head U [v_min,v_max) U tail; then per-tile
+//                        misplaced counts over D (PAPER.md:288-291 D array,
+//                        counted per tile like the paper's per-64/4096 chunk
+//                        counts).
 //   K2 tile_scan         deterministic exclusive scan of the tile counts
 //                        (PAPER.md:288-297, 1488-1496).
 //   K5a locate / K5b swap  rank-matched cleanup: the r-th misplaced
 //                        successor left of K is swapped with the r-th
 //                        misplaced predecessor right of K; each pair owned by
 //                        exactly one CTA (EREW).
-// No atomics anywhere; all reductions are fixed-order.
+// No atomics anywhere; all reductions are fixed-order.  The cleanup kernels
+// are chained with programmatic dependent launch (griddepcontrol).
 #include <algorithm>
 #include <cstdio>
 #include <vector>
@@ -32,67 +34,6 @@ __global__ void __launch_bounds__(C::NT) ss_group_kernel(typename C::Key* __rest
                                                          GroupOut* __restrict__ out) {
     extern __shared__ __align__(128) unsigned char smem[];
     ss_group_engine<C>(region, n_lines, g, blockIdx.x, seed, pivot, out + blockIdx.x, smem);
-}
-
-// ===========================================================================
-// K4: window reduction (1 CTA).  K = head_T + sum T_i + tail_T.
-// ===========================================================================
-template <typename K>
-__global__ void __launch_bounds__(256) window_reduce_kernel(const K* __restrict__ keys, uint64_t n, uint64_t h,
-                                                            uint64_t n_lines, uint32_t LK,
-                                                            const GroupOut* __restrict__ go, uint32_t g,
-                                                            K pivot, Ctl* __restrict__ ctl,
-                                                            uint64_t* __restrict__ d_split) {
-    __shared__ uint64_t sT[8], sMin[8], sMax[8], sHT[8];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t region_end = n_lines * LK;
-    uint64_t T = 0, vmin = region_end, vmax = 0, ht = 0;
-    for (uint32_t i = tid; i < g; i += 256) {
-        GroupOut o = go[i];
-        T += o.T;
-        vmin = o.vlo < vmin ? o.vlo : vmin;
-        vmax = o.vhi > vmax ? o.vhi : vmax;
-    }
-    // head [0,h) and tail [h + region_end, n) predecessors
-    const uint64_t tail0 = h + region_end;
-    for (uint64_t x = tid; x < h; x += 256) ht += is_pred(keys[x], pivot) ? 1 : 0;
-    for (uint64_t x = tail0 + tid; x < n; x += 256) ht += is_pred(keys[x], pivot) ? 1 : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        T += __shfl_xor_sync(0xffffffffu, T, o);
-        ht += __shfl_xor_sync(0xffffffffu, ht, o);
-        uint64_t a = __shfl_xor_sync(0xffffffffu, vmin, o);
-        uint64_t b = __shfl_xor_sync(0xffffffffu, vmax, o);
-        vmin = a < vmin ? a : vmin;
-        vmax = b > vmax ? b : vmax;
-    }
-    if (lane == 0) {
-        sT[warp] = T;
-        sMin[warp] = vmin;
-        sMax[warp] = vmax;
-        sHT[warp] = ht;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        for (int w = 1; w < 8; ++w) {
-            T += sT[w];
-            ht += sHT[w];
-            vmin = sMin[w] < vmin ? sMin[w] : vmin;
-            vmax = sMax[w] > vmax ? sMax[w] : vmax;
-        }
-        const uint64_t Ksplit = T + ht;
-        uint64_t a[3], b[3];
-        a[0] = 0; b[0] = h;                                // head
-        const uint64_t lo = h + vmin, hi = h + vmax;       // partial-partition window
-        a[1] = lo < Ksplit ? lo : Ksplit;
-        b[1] = hi > Ksplit ? hi : Ksplit;
-        if (vmin > vmax) { a[1] = b[1] = 0; }             // no non-empty group: no window
-        a[2] = tail0; b[2] = n;                            // tail
-        finish_ctl(ctl, n, Ksplit, a, b);
-        ctl->vmin = lo;
-        ctl->vmax = hi;
-        if (d_split) *d_split = Ksplit;
-    }
 }
 
 // Cleanup-only path (SURVEY §7 minimum slice / ablation): K by a count pass.
@@ -112,57 +53,123 @@ __global__ void __launch_bounds__(256) count_kernel(const K* __restrict__ keys, 
         partial[blockIdx.x] = c;
     }
 }
-__global__ void __launch_bounds__(256) count_finish_kernel(const uint64_t* __restrict__ partial, int np,
-                                                           uint64_t n, Ctl* __restrict__ ctl,
-                                                           uint64_t* __restrict__ d_split) {
-    if (threadIdx.x == 0) {
-        uint64_t K = 0;
-        for (int i = 0; i < np; ++i) K += partial[i];
-        uint64_t a[3] = {0, n, n}, b[3] = {n, n, n};
-        finish_ctl(ctl, n, K, a, b);
-        ctl->vmin = 0;
-        ctl->vmax = n;
-        if (d_split) *d_split = K;
-    }
-}
 
 // ===========================================================================
-// K1: tile counts over the dirty set (grid-stride, fixed mapping).
+// K4 + K1: window reduction (redundantly in every CTA; CTA 0 publishes the
+// control block) fused with the tile counts over the dirty set:
 //   left tiles  [t*T, min((t+1)T, Kv))      count successors (misplaced)
 //   right tiles [Kv + t*T, min(.., W))       count predecessors (misplaced)
-// 8 independent loads per thread in flight.
+// FROM_GROUPS: K = head_T + sum T_i + tail_T from the group outputs;
+// otherwise (cleanup-only path) K = sum of the count_kernel partials and
+// D = [0, n).
 // ===========================================================================
-template <typename K>
-__global__ void __launch_bounds__(256) tile_count_kernel(const K* __restrict__ keys, const Ctl* __restrict__ ctl,
-                                                         K pivot, uint32_t* __restrict__ cntL,
-                                                         uint32_t* __restrict__ cntR) {
+template <typename K, bool FROM_GROUPS>
+__global__ void __launch_bounds__(256) reduce_count_kernel(const K* __restrict__ keys, uint64_t n, uint64_t h,
+                                                           uint64_t n_lines, uint32_t LK,
+                                                           const GroupOut* __restrict__ go, uint32_t g,
+                                                           const uint64_t* __restrict__ partial, int np, K pivot,
+                                                           Ctl* __restrict__ ctl, uint64_t* __restrict__ d_split,
+                                                           uint32_t* __restrict__ cntL, uint32_t* __restrict__ cntR) {
+    __shared__ uint64_t sT[8], sMin[8], sMax[8], sHT[8];
+    __shared__ Ctl sc;
     __shared__ uint32_t s[8];
-    const Dirty d = load_dirty(ctl);
-    const uint64_t Kv = ctl->Kv, W = ctl->W, T = ctl->tile, nL = ctl->nL, nR = ctl->nR;
+    griddep_wait();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t region_end = n_lines * LK;
+    uint64_t T = 0, vmin = region_end, vmax = 0, ht = 0;
+    if (FROM_GROUPS) {
+        for (uint32_t i = tid; i < g; i += 256) {
+            const GroupOut o = go[i];
+            T += o.T;
+            vmin = o.vlo < vmin ? o.vlo : vmin;
+            vmax = o.vhi > vmax ? o.vhi : vmax;
+        }
+        // head [0,h) and tail [h + region_end, n) predecessors
+        for (uint64_t x = tid; x < h; x += 256) ht += is_pred(keys[x], pivot) ? 1 : 0;
+        for (uint64_t x = h + region_end + tid; x < n; x += 256) ht += is_pred(keys[x], pivot) ? 1 : 0;
+    } else {
+        for (int i = tid; i < np; i += 256) T += partial[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T += __shfl_xor_sync(0xffffffffu, T, o);
+        ht += __shfl_xor_sync(0xffffffffu, ht, o);
+        const uint64_t a = __shfl_xor_sync(0xffffffffu, vmin, o);
+        const uint64_t b = __shfl_xor_sync(0xffffffffu, vmax, o);
+        vmin = a < vmin ? a : vmin;
+        vmax = b > vmax ? b : vmax;
+    }
+    if (lane == 0) {
+        sT[warp] = T;
+        sMin[warp] = vmin;
+        sMax[warp] = vmax;
+        sHT[warp] = ht;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < 8; ++w) {
+            T += sT[w];
+            ht += sHT[w];
+            vmin = sMin[w] < vmin ? sMin[w] : vmin;
+            vmax = sMax[w] > vmax ? sMax[w] : vmax;
+        }
+        const uint64_t Ksplit = T + ht;
+        uint64_t a[3], b[3];
+        if (FROM_GROUPS) {
+            a[0] = 0; b[0] = h;                                // head
+            const uint64_t lo = h + vmin, hi = h + vmax;       // partial-partition window
+            a[1] = lo < Ksplit ? lo : Ksplit;
+            b[1] = hi > Ksplit ? hi : Ksplit;
+            if (vmin > vmax) { a[1] = b[1] = 0; }             // no non-empty group: no window
+            a[2] = h + region_end; b[2] = n;                   // tail
+            finish_ctl(&sc, n, Ksplit, a, b);
+            sc.vmin = lo;
+            sc.vmax = hi;
+        } else {
+            a[0] = 0; b[0] = n;
+            a[1] = a[2] = b[1] = b[2] = n;
+            finish_ctl(&sc, n, Ksplit, a, b);
+            sc.vmin = 0;
+            sc.vmax = n;
+        }
+        if (blockIdx.x == 0) {
+            *ctl = sc;
+            if (d_split) *d_split = Ksplit;
+        }
+    }
+    __syncthreads();
+    griddep_launch();
+    Dirty d;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        d.s[k] = sc.ds[k];
+        d.l[k] = sc.dl[k];
+    }
+    const uint64_t Kv = sc.Kv, W = sc.W, TT = sc.tile, nL = sc.nL, nR = sc.nR;
     for (uint64_t t = blockIdx.x; t < nL + nR; t += gridDim.x) {
         const bool left = t < nL;
-        const uint64_t u0 = left ? t * T : Kv + (t - nL) * T;
-        const uint64_t u1 = left ? min(u0 + T, Kv) : min(u0 + T, W);
+        const uint64_t u0 = left ? t * TT : Kv + (t - nL) * TT;
+        const uint64_t u1 = left ? min(u0 + TT, Kv) : min(u0 + TT, W);
         uint32_t c = 0;
         for (uint64_t ub = u0; ub < u1; ub += 8 * 256) {
             K x[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const uint64_t u = ub + (uint64_t)k * 256 + threadIdx.x;
-                x[k] = u < u1 ? keys[vreal(d, u)] : (left ? (K)0 : pivot);  // neutral fill
+                const uint64_t u = ub + (uint64_t)k * 256 + tid;
+                x[k] = u < u1 ? keys[vreal(d, u)] : (K)0;
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const uint64_t u = ub + (uint64_t)k * 256 + threadIdx.x;
+                const uint64_t u = ub + (uint64_t)k * 256 + tid;
                 const bool p = is_pred(x[k], pivot);
                 c += (u < u1 && (left ? !p : p)) ? 1u : 0u;
             }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+        if (lane == 0) s[warp] = c;
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             uint32_t tot = 0;
             for (int w = 0; w < 8; ++w) tot += s[w];
             if (left) cntL[t] = tot; else cntR[t - nL] = tot;
@@ -200,17 +207,47 @@ __device__ uint64_t block_exclusive_scan_1024(uint64_t v, uint64_t* sw, uint64_t
     return wpre + x - v;
 }
 
+__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* a, uint64_t n, uint64_t x) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* a, uint64_t n, uint64_t x) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Scans the tile counts into PL / PR (exclusive rank starts of each tile)
+// and builds the swap task list: the stable merge of PL and PR (left entries
+// first on ties).  Left tile t lands at t + #{PR < PL[t]}, right tile t' at
+// t' + #{PL <= PR[t']} (binary searches in shared memory); each task stores
+// its start rank and the left / right tile holding that rank.
+// Dynamic shared memory: 2 * (cap + 1) u64.
 __global__ void __launch_bounds__(1024) tile_scan_kernel(Ctl* __restrict__ ctl, const uint32_t* __restrict__ cntL,
                                                          const uint32_t* __restrict__ cntR,
-                                                         uint64_t* __restrict__ PL, uint64_t* __restrict__ PR) {
+                                                         uint64_t* __restrict__ PL, uint64_t* __restrict__ PR,
+                                                         uint64_t* __restrict__ rk, uint32_t* __restrict__ ttl,
+                                                         uint32_t* __restrict__ ttr) {
     __shared__ uint64_t sw[32];
+    extern __shared__ uint64_t sp[];  // [nL] PL, then [nR] PR
+    griddep_wait();
+    griddep_launch();
     const uint64_t nL = ctl->nL, nR = ctl->nR;
+    uint64_t* sPL = sp;
+    uint64_t* sPR = sp + nL;
     uint64_t carry = 0;
     for (uint64_t b = 0; b < nL; b += 1024) {
         const uint64_t i = b + threadIdx.x;
         uint64_t tot;
         const uint64_t ex = block_exclusive_scan_1024(i < nL ? cntL[i] : 0, sw, tot);
-        if (i < nL) PL[i] = carry + ex;
+        if (i < nL) PL[i] = sPL[i] = carry + ex;
         carry += tot;
     }
     const uint64_t ML = carry;
@@ -219,15 +256,35 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(Ctl* __restrict__ ctl, 
         const uint64_t i = b + threadIdx.x;
         uint64_t tot;
         const uint64_t ex = block_exclusive_scan_1024(i < nR ? cntR[i] : 0, sw, tot);
-        if (i < nR) PR[i] = carry + ex;
+        if (i < nR) PR[i] = sPR[i] = carry + ex;
         carry += tot;
+    }
+    __syncthreads();
+    const bool ok = (ML == carry && ML > 0);
+    if (ok) {
+        for (uint64_t t = threadIdx.x; t < nL; t += 1024) {
+            const uint64_t r = sPL[t];
+            const uint64_t m = t + lower_bound_u64(sPR, nR, r);
+            rk[m] = r;
+            ttl[m] = (uint32_t)t;
+            ttr[m] = (uint32_t)(upper_bound_u64(sPR, nR, r) - 1);
+        }
+        for (uint64_t t = threadIdx.x; t < nR; t += 1024) {
+            const uint64_t r = sPR[t];
+            const uint64_t ub = upper_bound_u64(sPL, nL, r);
+            const uint64_t m = t + ub;
+            rk[m] = r;
+            ttl[m] = (uint32_t)(ub - 1);
+            ttr[m] = (uint32_t)t;
+        }
     }
     if (threadIdx.x == 0) {
         ctl->ML = ML;
         ctl->MR = carry;
         if (ML != carry) ctl->err = 1;  // #misplaced successors must equal #misplaced predecessors
         // one swap task per breakpoint of the merged tile rank boundaries
-        ctl->nTasks = (ML == carry && ML > 0) ? nL + nR : 0;
+        ctl->nTasks = ok ? nL + nR : 0;
+        rk[ok ? nL + nR : 0] = ML;  // sentinel
     }
 }
 
@@ -238,54 +295,40 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(Ctl* __restrict__ ctl, 
 // is the sorted merge of PL[0..nL) and PR[0..nR) (duplicates kept: empty
 // tasks), so each task's items lie inside ONE left tile and ONE right tile
 // -- every walk is bounded by the tile size, whatever the item density.
-// rk[k] = U_k; posL[k] / posR[k] = virtual index of the misplaced
-// successor / predecessor of rank U_k (Kv / W if U_k = M): sentinels at k = nTasks.
+// rk[k] = U_k (written by tile_scan with the tiles ttl[k] / ttr[k] holding
+// rank U_k); posL[k] / posR[k] = virtual index of the misplaced successor /
+// predecessor of rank U_k (Kv / W if U_k = M): sentinels at k = nTasks.
 // ===========================================================================
-__device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* __restrict__ a, uint64_t n, uint64_t x) {
-    uint64_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (a[mid] <= x) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
-// k-th smallest (0-based) of the merge of sorted A[0..na) and B[0..nb) (merge path)
-__device__ __forceinline__ uint64_t merged_kth(const uint64_t* __restrict__ A, uint64_t na,
-                                               const uint64_t* __restrict__ B, uint64_t nb, uint64_t k) {
-    uint64_t lo = k > nb ? k - nb : 0, hi = k < na ? k : na;
-    while (lo < hi) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (A[mid] <= B[k - 1 - mid]) lo = mid + 1; else hi = mid;
-    }
-    const uint64_t i = lo, j = k - lo;
-    if (i < na && (j >= nb || A[i] <= B[j])) return A[i];
-    return B[j];
-}
-
 template <typename K>
-__global__ void __launch_bounds__(SW_NT) locate_kernel(const K* __restrict__ keys, Ctl* __restrict__ ctl, K pivot,
-                                                       const uint64_t* __restrict__ PL,
-                                                       const uint64_t* __restrict__ PR,
-                                                       uint64_t* __restrict__ posL, uint64_t* __restrict__ posR,
-                                                       uint64_t* __restrict__ rk) {
-    __shared__ WalkBuf<K> wb;
+__global__ void __launch_bounds__(SW_NT, 3) locate_kernel(const K* __restrict__ keys, Ctl* __restrict__ ctl,
+                                                          K pivot, const uint64_t* __restrict__ PL,
+                                                          const uint64_t* __restrict__ PR,
+                                                          uint64_t* __restrict__ posL, uint64_t* __restrict__ posR,
+                                                          const uint64_t* __restrict__ rk,
+                                                          const uint32_t* __restrict__ ttl,
+                                                          const uint32_t* __restrict__ ttr) {
+    __shared__ CleanupSmem<K> sm;
+    griddep_wait();
+    griddep_launch();
     const Dirty d = load_dirty(ctl);
-    const uint64_t Kv = ctl->Kv, W = ctl->W, T = ctl->tile, nL = ctl->nL, nR = ctl->nR, M = ctl->ML;
+    const uint64_t Kv = ctl->Kv, W = ctl->W, T = ctl->tile, M = ctl->ML;
     const uint64_t nTasks = ctl->nTasks;
     for (uint64_t j = blockIdx.x; j <= nTasks; j += gridDim.x) {
-        const uint64_t r = j < nTasks ? merged_kth(PL, nL, PR, nR, j) : M;
+        const uint64_t r = rk[j];
         uint64_t pl = Kv, pr = W;
-        if (r < M) {
-            const uint64_t tl = upper_bound_u64(PL, nL, r) - 1;
-            pl = select_item<K>(keys, d, pivot, false, tl * T, min(tl * T + T, Kv), r - PL[tl], wb);
-            const uint64_t tr = upper_bound_u64(PR, nR, r) - 1;
-            pr = select_item<K>(keys, d, pivot, true, Kv + tr * T, min(Kv + tr * T + T, W), r - PR[tr], wb);
+        if (j < nTasks && r < M) {
+            const uint64_t tl = ttl[j], tr = ttr[j];
+            if (T == (uint64_t)SW_RNG) {  // one round trip for both tiles
+                select_pair<K>(keys, d, pivot, tl * T, min(tl * T + T, Kv), r - PL[tl], Kv + tr * T,
+                               min(Kv + tr * T + T, W), r - PR[tr], sm.pb, pl, pr);
+            } else {
+                pl = select_item<K>(keys, d, pivot, false, tl * T, min(tl * T + T, Kv), r - PL[tl], sm.wb);
+                pr = select_item<K>(keys, d, pivot, true, Kv + tr * T, min(Kv + tr * T + T, W), r - PR[tr], sm.wb);
+            }
         }
         if (threadIdx.x == 0) {
             posL[j] = pl;
             posR[j] = pr;
-            rk[j] = r;
         }
     }
 }
@@ -294,17 +337,25 @@ __global__ void __launch_bounds__(SW_NT) locate_kernel(const K* __restrict__ key
 // K5b: rank-matched swap, one CTA per task (grid-stride).
 // ===========================================================================
 template <typename K>
-__global__ void __launch_bounds__(SW_NT) swap_kernel(K* __restrict__ keys, const Ctl* __restrict__ ctl, K pivot,
+__global__ void __launch_bounds__(SW_NT, 3) swap_kernel(K* __restrict__ keys, const Ctl* __restrict__ ctl, K pivot,
                                                      const uint64_t* __restrict__ posL,
                                                      const uint64_t* __restrict__ posR,
                                                      const uint64_t* __restrict__ rk) {
-    __shared__ WalkBuf<K> wb;
+    __shared__ CleanupSmem<K> sm;
+    griddep_wait();
     const Dirty d = load_dirty(ctl);
-    const uint64_t nTasks = ctl->nTasks;
+    const uint64_t nTasks = ctl->nTasks, T = ctl->tile, Kv = ctl->Kv, W = ctl->W;
     for (uint64_t j = blockIdx.x; j < nTasks; j += gridDim.x) {
         const uint64_t pairs = rk[j + 1] - rk[j];
         if (pairs == 0) continue;
-        walk_swap<K>(keys, d, pivot, posL[j], posL[j + 1], posR[j], posR[j + 1], pairs, wb);
+        const uint64_t uL = posL[j], uR = posR[j];
+        if (T == (uint64_t)SW_RNG) {
+            // the task's items lie in the tiles of its first items: clamp to them
+            const uint64_t tle = min((uL / T + 1) * T, Kv), tre = min(Kv + ((uR - Kv) / T + 1) * T, W);
+            swap_pair<K>(keys, d, pivot, uL, min(posL[j + 1], tle), uR, min(posR[j + 1], tre), pairs, sm.pb);
+        } else {
+            walk_swap<K>(keys, d, pivot, uL, posL[j + 1], uR, posR[j + 1], pairs, sm.wb);
+        }
     }
 }
 
@@ -351,6 +402,30 @@ uint64_t launch_count(int reset) {
 }
 void note_launches(uint64_t k) { g_launches += k; }
 
+// launch with programmatic stream serialization (the kernel calls
+// griddep_wait() before touching its predecessor's results)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl_smem(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                                   cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    note_launches(1);
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
+                              Args... args) {
+    return launch_pdl_smem(kern, grid, block, 0, st, args...);
+}
+
 // Optional per-call phase timing with CUDA events recorded on the launch
 // stream (bench.py's roofline: the group kernel's live duration).
 static bool g_timing = false;
@@ -389,7 +464,6 @@ int timing_read(double* out) {
     return 0;
 }
 
-
 // ---------------------------------------------------------------------------
 // Group-kernel variants (line size, threads, prefetch depth, store path),
 // selectable with pp_set_param("variant", v) for tuning; 0 is the default.
@@ -415,11 +489,11 @@ template <typename K, int V>
 struct VariantCfg;
 template <typename K> struct VariantCfg<K, 0> { using type = GroupCfg<K>; };
 template <typename K> struct VariantCfg<K, 1> { using type = GroupCfgT<K, 8192, 256, 4, false>; };
-template <typename K> struct VariantCfg<K, 2> { using type = GroupCfgT<K, 16384, 512, 3, true>; };
-template <typename K> struct VariantCfg<K, 3> { using type = GroupCfgT<K, 4096, 128, 6, true>; };
-template <typename K> struct VariantCfg<K, 4> { using type = GroupCfgT<K, 8192, 512, 4, true>; };
-template <typename K> struct VariantCfg<K, 5> { using type = GroupCfgT<K, 4096, 256, 8, true>; };
-template <typename K> struct VariantCfg<K, 6> { using type = GroupCfgT<K, 8192, 256, 6, true>; };
+template <typename K> struct VariantCfg<K, 2> { using type = GroupCfgT<K, 4096, 128, 4, false>; };
+template <typename K> struct VariantCfg<K, 3> { using type = GroupCfgT<K, 8192, 64, 4, false>; };
+template <typename K> struct VariantCfg<K, 4> { using type = GroupCfgT<K, 8192, 128, 3, false>; };
+template <typename K> struct VariantCfg<K, 5> { using type = GroupCfgT<K, 4096, 64, 6, false>; };
+template <typename K> struct VariantCfg<K, 6> { using type = GroupCfgT<K, 8192, 128, 4, true>; };
 constexpr int N_VARIANTS = 7;
 
 template <typename K, int V>
@@ -445,6 +519,7 @@ static void launch_group_t(K* region, uint64_t n_lines, uint32_t g, uint64_t see
     using C = typename VariantCfg<K, V>::type;
     occupancy_of<C>();
     ss_group_kernel<C><<<g, C::NT, C::SMEM, st>>>(region, n_lines, g, seed, pivot, out);
+    note_launches(1);
 }
 template <typename K>
 static void launch_group(int v, K* region, uint64_t n_lines, uint32_t g, uint64_t seed, K pivot, GroupOut* out,
@@ -466,12 +541,13 @@ static int cur_variant() {
 }
 
 struct Layout {
-    size_t ctl, gout, cntL, cntR, PL, PR, posL, posR, rk, partial, total;
+    size_t ctl, gout, cntL, cntR, PL, PR, posL, posR, rk, ttl, ttr, partial, total;
 };
 
-// Workspace: fixed-size cleanup arrays (CLEANUP_MAX_TILES per side, the tile
-// size adapts to the dirty set on the device) + one GroupOut per group: the
-// auxiliary memory does not grow with n beyond the g <= #SM x occupancy groups.
+// Workspace: fixed-size cleanup arrays (cleanup_max_tiles(n) per side, the
+// tile size adapts to the dirty set on the device) + one GroupOut per group:
+// the auxiliary memory does not grow with n beyond the g <= #SM x occupancy
+// groups and the <= 8192 tiles per side.
 static Layout make_layout(uint64_t n, uint64_t g, bool cleanup, uint64_t nPartial) {
     const uint64_t maxTiles = cleanup ? cleanup_max_tiles(n) + 1 : 1;
     const uint64_t maxTasks = cleanup ? 2 * cleanup_max_tiles(n) + 1 : 1;
@@ -491,6 +567,8 @@ static Layout make_layout(uint64_t n, uint64_t g, bool cleanup, uint64_t nPartia
     L.posL = take(8 * (maxTasks + 1));
     L.posR = take(8 * (maxTasks + 1));
     L.rk = take(8 * (maxTasks + 1));
+    L.ttl = take(4 * (maxTasks + 1));
+    L.ttr = take(4 * (maxTasks + 1));
     L.partial = take(8 * nPartial);
     L.total = o;
     return L;
@@ -525,7 +603,7 @@ pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64
     if (path == 2 && n_lines == 0) path = 1;
     S.path = path;
 
-    const int grid_cleanup = sm_count() * 4;
+    const unsigned grid_cleanup = (unsigned)sm_count() * 4;
     const uint64_t g = path == 2 ? choose_groups<K>(n_lines, vi.occ) : 0;
     const int nPartial = sm_count() * 2;
     Layout L = make_layout(n, g, path != 1, nPartial);
@@ -538,26 +616,15 @@ pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64
     S.n_lines = n_lines;
     S.aux_bytes = L.total;
 
+    cudaError_t e = cudaSuccess;
     timing_mark(st);
     if (path == 1) {
         small_partition_kernel<K><<<1, SW_NT, 0, st>>>(keys, n, pivot, ctl, d_split);
         note_launches(1);
         timing_mark(st);
     } else {
-        if (path == 2) {
-            GroupOut* gout = reinterpret_cast<GroupOut*>(ws + L.gout);
-            launch_group<K>(variant, keys + h, n_lines, (uint32_t)g, P.seed, pivot, gout, st);
-            timing_mark(st);
-            window_reduce_kernel<K><<<1, 256, 0, st>>>(keys, n, h, n_lines, (uint32_t)LK, gout, (uint32_t)g, pivot,
-                                                       ctl, d_split);
-            note_launches(2);
-        } else {
-            uint64_t* partial = reinterpret_cast<uint64_t*>(ws + L.partial);
-            count_kernel<K><<<nPartial, 256, 0, st>>>(keys, n, pivot, partial);
-            count_finish_kernel<<<1, 32, 0, st>>>(partial, nPartial, n, ctl, d_split);
-            note_launches(2);
-            timing_mark(st);
-        }
+        GroupOut* gout = reinterpret_cast<GroupOut*>(ws + L.gout);
+        uint64_t* partial = reinterpret_cast<uint64_t*>(ws + L.partial);
         uint32_t* cntL = reinterpret_cast<uint32_t*>(ws + L.cntL);
         uint32_t* cntR = reinterpret_cast<uint32_t*>(ws + L.cntR);
         uint64_t* PL = reinterpret_cast<uint64_t*>(ws + L.PL);
@@ -565,14 +632,36 @@ pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64
         uint64_t* posL = reinterpret_cast<uint64_t*>(ws + L.posL);
         uint64_t* posR = reinterpret_cast<uint64_t*>(ws + L.posR);
         uint64_t* rk = reinterpret_cast<uint64_t*>(ws + L.rk);
-        tile_count_kernel<K><<<grid_cleanup, 256, 0, st>>>(keys, ctl, pivot, cntL, cntR);
-        tile_scan_kernel<<<1, 1024, 0, st>>>(ctl, cntL, cntR, PL, PR);
-        locate_kernel<K><<<grid_cleanup, SW_NT, 0, st>>>(keys, ctl, pivot, PL, PR, posL, posR, rk);
-        swap_kernel<K><<<grid_cleanup, SW_NT, 0, st>>>(keys, ctl, pivot, posL, posR, rk);
-        note_launches(4);
+        if (path == 2) {
+            launch_group<K>(variant, keys + h, n_lines, (uint32_t)g, P.seed, pivot, gout, st);
+            timing_mark(st);
+            e = launch_pdl(reduce_count_kernel<K, true>, grid_cleanup, 256, st, keys, n, h, n_lines, (uint32_t)LK,
+                           gout, (uint32_t)g, partial, nPartial, pivot, ctl, d_split, cntL, cntR);
+        } else {
+            count_kernel<K><<<nPartial, 256, 0, st>>>(keys, n, pivot, partial);
+            note_launches(1);
+            timing_mark(st);
+            e = launch_pdl(reduce_count_kernel<K, false>, grid_cleanup, 256, st, keys, n, (uint64_t)0, (uint64_t)0,
+                           (uint32_t)LK, gout, (uint32_t)0, partial, nPartial, pivot, ctl, d_split, cntL, cntR);
+        }
+        uint32_t* ttl = reinterpret_cast<uint32_t*>(ws + L.ttl);
+        uint32_t* ttr = reinterpret_cast<uint32_t*>(ws + L.ttr);
+        const size_t scan_smem = 2 * 8 * (cleanup_max_tiles(n) + 1);
+        static size_t scan_smem_set = 0;
+        if (scan_smem > 48 * 1024 && scan_smem > scan_smem_set) {
+            cudaFuncSetAttribute(tile_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem);
+            scan_smem_set = scan_smem;
+        }
+        if (e == cudaSuccess)
+            e = launch_pdl_smem(tile_scan_kernel, 1, 1024, scan_smem, st, ctl, cntL, cntR, PL, PR, rk, ttl, ttr);
+        if (e == cudaSuccess)
+            e = launch_pdl(locate_kernel<K>, grid_cleanup, SW_NT, st, keys, ctl, pivot, PL, PR, posL, posR, rk, ttl,
+                           ttr);
+        if (e == cudaSuccess) e = launch_pdl(swap_kernel<K>, grid_cleanup, SW_NT, st, keys, ctl, pivot, posL, posR, rk);
     }
     timing_mark(st);
-    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "partition launch");
+    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "partition launch");
     return PP_OK;
 }
@@ -597,7 +686,6 @@ pp_status ss_groups_device(K* keys, uint64_t n, K pivot, uint64_t g_req, cudaStr
     GroupOut* gout = static_cast<GroupOut*>(workspace(sizeof(GroupOut) * g, st));
     if (!gout) return PP_E_NOMEM;
     launch_group<K>(variant, keys + h, n_lines, (uint32_t)g, params().seed, pivot, gout, st);
-    note_launches(1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "ss_group launch");
     std::vector<GroupOut> host(g);

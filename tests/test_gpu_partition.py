@@ -106,6 +106,20 @@ def test_groups_and_windows(pp, dt, mx, g):
             oracle.check_partition(a, out, p, split)
 
 
+@pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
+def test_cleanup_only_large(pp, dt, mx):
+    """Cleanup-only path on whole arrays: dirty set = [0, n), tiles larger
+    than the one-round-trip size (exercises the general walk / select)."""
+    rng = np.random.default_rng(23)
+    for n in (3_000_017, 1 << 22):
+        a = rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
+        for frac in (0.3, 0.5):
+            p = int(frac * (mx + 1))
+            split, out = _run(pp, a, p, 3, path=3)
+            oracle.check_partition(a, out, p, split)
+            st = pp.pp_last_stats() if False else None
+
+
 def test_structured_inputs(pp):
     """Already partitioned / reverse / all-true / all-false / alternating (u32)
     and whole-line adversarial patterns (u64)."""
@@ -247,3 +261,18 @@ def test_config4_adversarial_full(pp, pat):
              "alternating": 500_002}[pat]
     assert Kp == exp_p
     _full_check(pp, t, synth.ADV_PIVOT_U32, K)
+
+
+@pytest.mark.parametrize("variant", list(range(7)))
+def test_group_variants(pp, variant):
+    """Every group-kernel configuration (line size, threads, prefetch depth,
+    store path) is parity-exact, including runs right after other kernels
+    (dirty shared memory)."""
+    rng = np.random.default_rng(variant)
+    for dt, mx in ((np.uint64, U64_MAX), (np.uint32, U32_MAX)):
+        for n in (3_000_017, 1 << 22):
+            a = rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
+            for frac in (0.01, 0.5):
+                p = int(frac * (mx + 1))
+                split, out = _run(pp, a, p, 1, variant=variant)
+                oracle.check_partition(a, out, p, split)
