@@ -143,41 +143,175 @@ __global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys,
     if (threadIdx.x == 0) splits[blockIdx.x] = Ks;
 }
 
-// Leaf sort: one CTA sorts one segment of <= LEAF keys in shared memory with
-// a bitonic network (padding with the maximum key, never stored back).
+// Leaf sort: one CTA sorts one segment of <= LEAF keys with a bitonic
+// network (padding with the maximum key, never stored back).  Each thread
+// holds E = 8 consecutive keys in registers: compare-exchange stages with
+// stride j < 8 run in registers, 8 <= j < 256 through warp shuffles, and only
+// j >= 256 through shared memory.
+constexpr int LEAF_E = 8;
+
+template <int J, typename K>
+__device__ __forceinline__ void leaf_reg_stage(K (&v)[LEAF_E], uint32_t base, uint32_t k) {
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) {
+        if ((r & J) == 0) {
+            const bool asc = ((base + r) & k) == 0;
+            const K a = v[r], b = v[r + J];
+            if ((a > b) == asc) {
+                v[r] = b;
+                v[r + J] = a;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void leaf_bar(uint32_t nthr) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+}
+
+template <typename K>
+__device__ __forceinline__ void cmpx(K& a, K& b) {
+    const K lo = a < b ? a : b, hi = a < b ? b : a;
+    a = lo;
+    b = hi;
+}
+
+// Leaf sort by merging: every thread sorts its 8 keys in registers (Batcher's
+// 19-comparator network), then log2(P/8) rounds merge pairs of sorted runs
+// in shared memory; each thread produces 8 outputs of a merge, locating its
+// start on the merge path by binary search (ties: left run first -- the sort
+// is a plain ascending sort, stability is irrelevant for keys).
+template <typename K, int LEAF, int NT>
+__global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
+                                                           const uint64_t* __restrict__ leaf_lo,
+                                                           const uint32_t* __restrict__ leaf_len) {
+    static_assert(LEAF == NT * LEAF_E, "one block holds LEAF keys");
+    extern __shared__ __align__(16) unsigned char lsm[];
+    K* src = reinterpret_cast<K*>(lsm);
+    K* dst = src + LEAF;
+    const uint64_t lo = leaf_lo[blockIdx.x];
+    const uint32_t len = leaf_len[blockIdx.x];
+    // pad to whole warps of 8 keys per thread (not to a power of two)
+    const uint32_t P = (len + 32 * LEAF_E - 1) / (32 * LEAF_E) * (32 * LEAF_E);
+    const uint32_t nthr = P / LEAF_E;
+    const uint32_t tid = threadIdx.x;
+    if (tid >= nthr) return;
+    const K KMAX = (K)~(K)0;
+    for (uint32_t i = tid; i < P; i += nthr) src[i] = i < len ? keys[lo + i] : KMAX;
+    leaf_bar(nthr);
+    const uint32_t base = tid * LEAF_E;
+    K v[LEAF_E];
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) v[r] = src[base + r];
+    cmpx(v[0], v[1]); cmpx(v[2], v[3]); cmpx(v[4], v[5]); cmpx(v[6], v[7]);
+    cmpx(v[0], v[2]); cmpx(v[1], v[3]); cmpx(v[4], v[6]); cmpx(v[5], v[7]);
+    cmpx(v[1], v[2]); cmpx(v[5], v[6]);
+    cmpx(v[0], v[4]); cmpx(v[1], v[5]); cmpx(v[2], v[6]); cmpx(v[3], v[7]);
+    cmpx(v[2], v[4]); cmpx(v[3], v[5]);
+    cmpx(v[1], v[2]); cmpx(v[3], v[4]); cmpx(v[5], v[6]);
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) src[base + r] = v[r];
+    leaf_bar(nthr);
+    for (uint32_t L = LEAF_E; L < P; L <<= 1) {
+        // runs A = [blk, blk+La), B = [blk+La, blk+La+Lb) (the last pair may be short)
+        const uint32_t blk = base / (2 * L) * (2 * L);
+        const uint32_t d = base - blk;
+        const uint32_t La = min(L, P - blk);
+        const uint32_t Lb = min(L, P - blk - La);
+        const K* A = src + blk;
+        const K* B = A + La;
+        uint32_t a0 = d > Lb ? d - Lb : 0, a1 = d < La ? d : La;
+        while (a0 < a1) {
+            const uint32_t mid = (a0 + a1) >> 1;
+            if (A[mid] <= B[d - 1 - mid]) a0 = mid + 1; else a1 = mid;
+        }
+        uint32_t a = a0, b = d - a0;
+        K xa = a < La ? A[a] : KMAX, xb = b < Lb ? B[b] : KMAX;
+#pragma unroll
+        for (int r = 0; r < LEAF_E; ++r) {
+            const bool takeA = (b >= Lb) || (a < La && xa <= xb);
+            if (takeA) {
+                v[r] = xa;
+                ++a;
+                xa = a < La ? A[a] : KMAX;
+            } else {
+                v[r] = xb;
+                ++b;
+                xb = b < Lb ? B[b] : KMAX;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < LEAF_E; ++r) dst[base + r] = v[r];
+        leaf_bar(nthr);
+        K* t = src;
+        src = dst;
+        dst = t;
+    }
+    for (uint32_t i = tid; i < len; i += nthr) keys[lo + i] = src[i];
+}
+
 template <typename K, int LEAF, int NT>
 __global__ void __launch_bounds__(NT) qs_leaf_kernel(K* __restrict__ keys, const uint64_t* __restrict__ leaf_lo,
                                                      const uint32_t* __restrict__ leaf_len) {
-    __shared__ K sk[LEAF];
+    static_assert(LEAF == NT * LEAF_E, "one block holds LEAF keys");
+    __shared__ __align__(16) K sk[LEAF];
     const uint64_t lo = leaf_lo[blockIdx.x];
     const uint32_t len = leaf_len[blockIdx.x];
-    uint32_t P = 2;
+    uint32_t P = 32 * LEAF_E;
     while (P < len) P <<= 1;
-    for (uint32_t i = threadIdx.x; i < P; i += NT) sk[i] = i < len ? keys[lo + i] : (K)~(K)0;
-    __syncthreads();
+    const uint32_t nthr = P / LEAF_E;  // whole warps
+    const uint32_t tid = threadIdx.x;
+    if (tid >= nthr) return;
+    const K KMAX = (K)~(K)0;
+    for (uint32_t i = tid; i < P; i += nthr) sk[i] = i < len ? keys[lo + i] : KMAX;
+    leaf_bar(nthr);
+    const uint32_t base = tid * LEAF_E;
+    K v[LEAF_E];
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) v[r] = sk[base + r];
     for (uint32_t k = 2; k <= P; k <<= 1) {
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t t = threadIdx.x; t < P / 2; t += NT) {
-                // comparator t: pair (i, i^j) with i having bit j clear
-                const uint32_t i = 2 * t - (t & (j - 1));
-                const uint32_t l = i + j;
-                const bool up = (i & k) == 0;
-                const K x = sk[i], y = sk[l];
-                if ((x > y) == up) {
-                    sk[i] = y;
-                    sk[l] = x;
+            if (j >= 32 * LEAF_E) {  // partner in another warp: exchange through smem
+                leaf_bar(nthr);
+#pragma unroll
+                for (int r = 0; r < LEAF_E; ++r) sk[base + r] = v[r];
+                leaf_bar(nthr);
+#pragma unroll
+                for (int r = 0; r < LEAF_E; ++r) {
+                    const uint32_t i = base + r, p = i ^ j;
+                    const K y = sk[p];
+                    const bool keep_min = ((i < p) == ((i & k) == 0));
+                    v[r] = keep_min ? (v[r] < y ? v[r] : y) : (v[r] > y ? v[r] : y);
                 }
+            } else if (j >= LEAF_E) {  // partner lane in this warp
+                const int lm = (int)(j / LEAF_E);
+#pragma unroll
+                for (int r = 0; r < LEAF_E; ++r) {
+                    const K y = __shfl_xor_sync(0xffffffffu, v[r], lm);
+                    const uint32_t i = base + r, p = i ^ j;
+                    const bool keep_min = ((i < p) == ((i & k) == 0));
+                    v[r] = keep_min ? (v[r] < y ? v[r] : y) : (v[r] > y ? v[r] : y);
+                }
+            } else if (j == 4) {
+                leaf_reg_stage<4>(v, base, k);
+            } else if (j == 2) {
+                leaf_reg_stage<2>(v, base, k);
+            } else {
+                leaf_reg_stage<1>(v, base, k);
             }
-            __syncthreads();
         }
     }
-    for (uint32_t i = threadIdx.x; i < len; i += NT) keys[lo + i] = sk[i];
+    leaf_bar(nthr);
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) sk[base + r] = v[r];
+    leaf_bar(nthr);
+    for (uint32_t i = tid; i < len; i += nthr) keys[lo + i] = sk[i];
 }
 
 template <typename K>
 struct LeafCfg {
     static constexpr int LEAF = (sizeof(K) == 8) ? 4096 : 8192;
-    static constexpr int NT = 512;
+    static constexpr int NT = LEAF / LEAF_E;
 };
 
 // quicksort workspace (separate from the partition workspace)
@@ -207,7 +341,12 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     const Params& P = params();
     const uint64_t LEAF = (P.leaf > 0 && P.leaf <= LC::LEAF) ? (uint64_t)P.leaf : (uint64_t)LC::LEAF;
     const uint64_t BIG = P.qs_cta_max > 0 ? (uint64_t)P.qs_cta_max : (uint64_t)1 << 25;
-    const uint64_t MINL = 64;  // lines per group for mid segments
+    const uint64_t MINL = 16;  // at least this many lines per group for mid segments
+    int occ = 1;
+    cudaFuncSetAttribute(qs_group_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, qs_group_kernel<K>, C::NT, C::SMEM);
+    const uint64_t G_TARGET =
+        (uint64_t)sm_count() * (uint64_t)std::max(occ, 1) * (uint64_t)std::max<int64_t>(P.qs_waves, 1);
     const K KMAX = (K)~(K)0;
 
     struct HSeg {
@@ -241,6 +380,14 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         mids.clear();
         std::vector<size_t> big_idx, mid_idx;
         uint64_t gtot = 0;
+        // mid segments share one launch: give each a number of groups
+        // proportional to its length so that one wave of G_TARGET CTAs
+        // carries the level (small windows, balanced CTAs)
+        uint64_t mid_keys = 0;
+        for (size_t i = 0; i < cur.size(); ++i) {
+            const uint64_t len = cur[i].hi - cur[i].lo;
+            if (len < BIG) mid_keys += len;
+        }
         for (size_t i = 0; i < cur.size(); ++i) {
             const uint64_t len = cur[i].hi - cur[i].lo;
             if (len >= BIG) {
@@ -258,7 +405,8 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                 uint64_t h = ((16 - (addr & 15)) & 15) / sizeof(K);
                 if (h > len) h = len;
                 const uint64_t nl = (len - h) / C::LK;
-                q.g = std::max<uint64_t>(1, nl / MINL);
+                const uint64_t gp = (uint64_t)((double)len * (double)G_TARGET / (double)mid_keys + 0.5);
+                q.g = std::max<uint64_t>(1, std::min<uint64_t>(gp, nl / MINL));
                 q.gbase = gtot;
                 gtot += q.g;
                 mids.push_back(q);
@@ -355,7 +503,15 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         if (e != cudaSuccess) return cuda_fail(e, "quicksort leaves H2D");
         for (uint64_t b0 = 0; b0 < nleaf; b0 += 65535u * 1024u) {
             const uint64_t cnt = std::min<uint64_t>(nleaf - b0, 65535u * 1024u);
-            qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, 0, st>>>(keys, d_lo + b0, d_len + b0);
+            if (P.leaf_algo == 1) {
+                qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, 0, st>>>(keys, d_lo + b0, d_len + b0);
+            } else {
+                const size_t smem = 2 * sizeof(K) * LC::LEAF;
+                cudaFuncSetAttribute(qs_leaf_merge_kernel<K, LC::LEAF, LC::NT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo + b0,
+                                                                                             d_len + b0);
+            }
             note_launches(1);
         }
         e = cudaGetLastError();

@@ -1,0 +1,146 @@
+"""Multi-GPU exchange step (BASELINE config 3) on CPU: the exchange plan and
+its round schedule checked by an in-memory simulator, and the full
+Partitioner over torch.distributed with the gloo backend at world sizes 2-4
+(the local partition is the oracle here; the CUDA local partition is covered
+by the GPU tests)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2004_12532_b200.dist import Partitioner, exchange_plan, my_ops, schedule_rounds
+
+
+def _simulate(shards, pivot):
+    """Apply the plan to in-memory shards (each locally partitioned first)."""
+    ts = []
+    for s in shards:
+        ts.append(oracle.partition_two_pointer(s, pivot))
+    ns = [s.size for s in shards]
+    K, plan = exchange_plan(ns, ts)
+    base = np.cumsum([0] + ns[:-1])
+    for tr in plan:
+        a = shards[tr.rank_f][tr.f - base[tr.rank_f]: tr.f - base[tr.rank_f] + tr.length].copy()
+        b = shards[tr.rank_t][tr.t - base[tr.rank_t]: tr.t - base[tr.rank_t] + tr.length].copy()
+        shards[tr.rank_f][tr.f - base[tr.rank_f]: tr.f - base[tr.rank_f] + tr.length] = b
+        shards[tr.rank_t][tr.t - base[tr.rank_t]: tr.t - base[tr.rank_t] + tr.length] = a
+    return K, plan
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8, 16, 64])
+def test_plan_simulator(P):
+    rng = np.random.default_rng(P)
+    for trial in range(20):
+        ns = list(rng.integers(0, 2000, size=P))
+        if trial % 4 == 0:
+            ns = [1000] * P
+        glob = rng.integers(0, 100, size=sum(ns)).astype(np.uint64)
+        pivot = int(rng.integers(0, 101))
+        shards = np.split(glob.copy(), np.cumsum(ns)[:-1])
+        K, plan = _simulate(shards, pivot)
+        out = np.concatenate(shards) if shards else glob
+        oracle.check_partition(glob, out, pivot, K)
+        for tr in plan:
+            assert tr.rank_f != tr.rank_t and tr.length > 0
+
+
+def test_plan_adversarial_counts():
+    # all predecessors on the last rank, all successors on the first ...
+    for ns, ts in (([4, 4, 4], [0, 0, 4]), ([5, 5], [5, 0]), ([3, 0, 7, 1], [0, 0, 7, 1]),
+                   ([10, 10, 10, 10], [10, 0, 10, 0]), ([1] * 9, [0, 1] * 4 + [1])):
+        K, plan = exchange_plan(ns, ts)
+        assert K == sum(ts)
+        moved_f = sum(tr.length for tr in plan)
+        # misplaced successors left of K
+        base, mis = 0, 0
+        for n, t in zip(ns, ts):
+            mis += max(0, min(K, base + n) - (base + t))
+            base += n
+        assert moved_f == mis
+
+
+@pytest.mark.parametrize("cap", [1, 3, 7, 1000])
+def test_schedule_rounds_cover_and_cap(cap):
+    rng = np.random.default_rng(cap)
+    for trial in range(30):
+        P = int(rng.integers(2, 9))
+        ns = [int(x) for x in rng.integers(0, 50, size=P)]
+        ts = [int(rng.integers(0, n + 1)) for n in ns]
+        K, plan = exchange_plan(ns, ts)
+        rounds = schedule_rounds(plan, P, cap)
+        for r in rounds:
+            recv = [0] * P
+            for tr in r:
+                recv[tr.rank_f] += tr.length
+                recv[tr.rank_t] += tr.length
+            assert max(recv) <= cap
+        # pieces cover the plan exactly, in order
+        flat = [tr for r in rounds for tr in r]
+        assert sum(t.length for t in flat) == sum(t.length for t in plan)
+        base = np.cumsum([0] + ns[:-1])
+        for rank in range(P):
+            ops = [op for r in rounds for op in my_ops(r, rank, int(base[rank]))]
+            assert all(0 <= off and off + m <= ns[rank] for _, off, m in ops)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n_per, seed, pivot, staging, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # uneven shards: rank r holds n_per + r*37 keys of one global array
+        ns = [n_per + r * 37 for r in range(world)]
+        off = sum(ns[:rank])
+        host = synth.uniform_u64_np(ns[rank], seed, offset=off)
+        shard = torch.from_numpy(host.view(np.int64).copy())
+
+        def local(t, p):
+            return oracle.partition_two_pointer(t.numpy().view(np.uint64), p)
+
+        part = Partitioner(device="cpu", staging_bytes=staging, local_partition=local)
+        K = part.partition(shard, pivot)
+        mx = max(ns)
+        padded = torch.zeros(mx, dtype=torch.int64)
+        padded[: ns[rank]] = shard
+        gathered = [torch.empty(mx, dtype=torch.int64) for r in range(world)]
+        dist.all_gather(gathered, padded)
+        if rank == 0:
+            full = torch.cat([g[: ns[r]] for r, g in enumerate(gathered)])
+            result_q.put((K, full.numpy().view(np.uint64).copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,staging", [(2, 1 << 20), (3, 4096), (4, 8 * 1000)])
+def test_partitioner_gloo(world, staging):
+    n_per, seed = 20000, 0xC0FFEE03
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    for pivot in (1 << 63, 1 << 60):
+        procs = [ctx.Process(target=_worker, args=(r, world, port, n_per, seed, pivot, staging, q))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        K, out = q.get(timeout=120)
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        ns = [n_per + r * 37 for r in range(world)]
+        glob = synth.uniform_u64_np(sum(ns), seed)
+        oracle.check_partition(glob, out, pivot, K)
+        port = _free_port()

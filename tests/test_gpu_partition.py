@@ -248,6 +248,52 @@ def test_config2_full(pp, mu):
     assert st["aux_bytes"] < 0.001 * n * 8
 
 
+def test_config3_single_gpu_full(pp):
+    """n = 2^33 u64 (64 GiB, BASELINE config 3 at P = 1), pivot 2^63.
+    Checks at full size: split = count of keys < pivot (device compare, and
+    the oracle's count on a 2^24-key sample of the input); the predicate on
+    every position; per-side multiset fingerprints (count, sum, xor, sum of
+    a mixed image) equal the input's -- a full sort of 2^33 keys does not fit
+    beside the array."""
+    from gpu_util import order_key, order_pivot
+    n = 1 << 33
+    p = 1 << 63
+    t = torch.empty(n, dtype=torch.int64, device="cuda")
+    synth.uniform_u64_torch(n, synth.SEEDS["c3"], "cuda", out=t, chunk=1 << 27)
+    sample = t[: 1 << 24].cpu().numpy().view(np.uint64)
+    assert oracle.count(sample, p) == int((order_key(t[: 1 << 24]) < order_pivot(p, torch.int64)).sum())
+
+    pv = order_pivot(p, torch.int64)
+    C = 1 << 28
+
+    def side_prints(by_value: bool, split: int = 0):
+        """(count, sum, sum of x*odd) of the true side and of the false side
+        (wrapping int64 arithmetic), chunk by chunk."""
+        acc = [[0, 0, 0], [0, 0, 0]]
+        for s in range(0, n, C):
+            x = t[s:s + C]
+            if by_value:
+                m = order_key(x) < pv
+            else:
+                m = torch.arange(s, s + x.numel(), device="cuda") < split
+            for side, sel in ((0, m), (1, ~m)):
+                v = x[sel]
+                acc[side][0] += v.numel()
+                acc[side][1] = (acc[side][1] + int(v.sum())) % (1 << 64)
+                acc[side][2] = (acc[side][2] + int((v * -7046029254386353131).sum())) % (1 << 64)
+        return acc
+
+    before = side_prints(True)
+    K = before[0][0]
+    split = pp.pp_partition(t, p)
+    assert split == K
+    for s in range(0, n, C):
+        ko = order_key(t[s:s + C])
+        idx = torch.arange(s, s + ko.numel(), device="cuda")
+        assert bool(((ko < pv) == (idx < split)).all())
+    assert side_prints(False, split) == before
+
+
 @pytest.mark.parametrize("pat", list(synth.ADV_PATTERNS))
 def test_config4_adversarial_full(pp, pat):
     n = 1_000_000_007

@@ -75,6 +75,19 @@ def test_medium_sizes(pp, dt, mx):
             assert np.array_equal(out, _oracle_sorted(a)), n
 
 
+@pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
+@pytest.mark.parametrize("params", [{"leaf_algo": 1}, {"leaf_algo": 0, "leaf": 300}, {"qs_waves": 1},
+                                    {"qs_waves": 16, "leaf": 1000}])
+def test_qs_parameters(pp, dt, mx, params):
+    """Leaf algorithms (merge / bitonic), leaf sizes and level balancing all
+    give the oracle's sorted output."""
+    rng = np.random.default_rng(4)
+    for n in (5000, 300_007):
+        for a in list(_cases(dt, mx, n, rng))[:3]:
+            out = _sort_gpu(pp, a, 1, **params)
+            assert np.array_equal(out, _oracle_sorted(a)), (n, params)
+
+
 def test_big_path_forced(pp):
     """Force the multi-CTA partition for mid-size segments (qs_cta_max small)."""
     rng = np.random.default_rng(3)
