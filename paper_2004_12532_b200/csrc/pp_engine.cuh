@@ -330,10 +330,68 @@ __device__ __forceinline__ void select_pair(const K* __restrict__ keys, const Di
     __syncthreads();
 }
 
+// ===========================================================================
+// Streaming rank-matched walk for one CTA over a whole (possibly long) left
+// range and right range: every round scans the next SW_RNG keys of BOTH
+// sides at once (one memory round trip), appends the misplaced keys'
+// offsets to two rings, and swaps min(#left, #right) pairs.  Offsets are
+// 32-bit relative to the range starts (ranges < 2^32 keys); values are
+// re-read at swap time.  Pairs the i-th item of each side, like walk_swap.
+// ===========================================================================
+constexpr uint32_t SWQ = 2 * SW_RNG;  // ring capacity per side
+
+struct StreamBuf {
+    uint32_t ql[SWQ], qr[SWQ];
+    uint32_t cnt[2][SW_EPT2][SW_NT / 32];
+};
+
+template <typename K>
+__device__ void walk_swap_stream(K* __restrict__ keys, const Dirty& d, K pivot, uint64_t uL0, uint64_t uLend,
+                                 uint64_t uR0, uint64_t uRend, StreamBuf& sb) {
+    uint64_t uL = uL0, uR = uR0;
+    uint32_t hl = 0, tl = 0, hr = 0, tr = 0;  // ring head / tail counters
+    for (;;) {
+        const bool scanL = (tl - hl) < SW_RNG && uL < uLend;
+        const bool scanR = (tr - hr) < SW_RNG && uR < uRend;
+        if (scanL || scanR) {
+            PairScan<K> ps;
+            scan_pair<K>(keys, d, pivot, uL, scanL ? min(uL + SW_RNG, uLend) : uL, uR,
+                         scanR ? min(uR + SW_RNG, uRend) : uR, sb.cnt, ps);
+#pragma unroll
+            for (int k = 0; k < SW_EPT2; ++k) {
+                const uint32_t off = (uint32_t)k * SW_NT + threadIdx.x;
+                if ((ps.fl >> k) & 1u) sb.ql[(tl + ps.rl[k]) % SWQ] = (uint32_t)(uL - uL0) + off;
+                if ((ps.fr >> k) & 1u) sb.qr[(tr + ps.rr[k]) % SWQ] = (uint32_t)(uR - uR0) + off;
+            }
+            tl += ps.tl;
+            tr += ps.tr;
+            if (scanL) uL = min(uL + SW_RNG, uLend);
+            if (scanR) uR = min(uR + SW_RNG, uRend);
+            __syncthreads();
+        }
+        const uint32_t m = min(tl - hl, tr - hr);
+        if (m == 0) {
+            if (!(uL < uLend && (tl - hl) < SW_RNG) && !(uR < uRend && (tr - hr) < SW_RNG)) break;
+            continue;
+        }
+        for (uint32_t t = threadIdx.x; t < m; t += SW_NT) {
+            const uint64_t pl = vreal(d, uL0 + sb.ql[(hl + t) % SWQ]);
+            const uint64_t pr = vreal(d, uR0 + sb.qr[(hr + t) % SWQ]);
+            const K a = keys[pl], b = keys[pr];
+            keys[pl] = b;
+            keys[pr] = a;
+        }
+        hl += m;
+        hr += m;
+        __syncthreads();
+    }
+}
+
 template <typename K>
 union CleanupSmem {
     WalkBuf<K> wb;
     PairBuf<K> pb;
+    StreamBuf sb;
 };
 
 // Swap the i-th misplaced successor of [uL, uLend) with the i-th misplaced

@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(SW_NT, 3) swap_kernel(K* __restrict__ keys, co
             const uint64_t tle = min((uL / T + 1) * T, Kv), tre = min(Kv + ((uR - Kv) / T + 1) * T, W);
             swap_pair<K>(keys, d, pivot, uL, min(posL[j + 1], tle), uR, min(posR[j + 1], tre), pairs, sm.pb);
         } else {
-            walk_swap<K>(keys, d, pivot, uL, posL[j + 1], uR, posR[j + 1], pairs, sm.wb);
+            walk_swap_stream<K>(keys, d, pivot, uL, posL[j + 1], uR, posR[j + 1], sm.sb);
         }
     }
 }
@@ -366,7 +366,7 @@ template <typename K>
 __global__ void __launch_bounds__(SW_NT) small_partition_kernel(K* __restrict__ keys, uint64_t n, K pivot,
                                                                 Ctl* __restrict__ ctl,
                                                                 uint64_t* __restrict__ d_split) {
-    __shared__ WalkBuf<K> wb;
+    __shared__ StreamBuf sb;
     __shared__ uint64_t sK[SW_NT / 32];
     uint64_t c = 0;
     for (uint64_t x = threadIdx.x; x < n; x += SW_NT) c += is_pred(keys[x], pivot) ? 1 : 0;
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(SW_NT) small_partition_kernel(K* __restrict__ 
     Dirty d;
     d.s[0] = 0; d.l[0] = n;
     d.s[1] = d.s[2] = n; d.l[1] = d.l[2] = 0;
-    walk_swap<K>(keys, d, pivot, 0, Ksplit, Ksplit, n, ~0ull, wb);
+    walk_swap_stream<K>(keys, d, pivot, 0, Ksplit, Ksplit, n, sb);
     if (threadIdx.x == 0) {
         if (ctl) {
             uint64_t a[3] = {0, n, n}, b[3] = {n, n, n};

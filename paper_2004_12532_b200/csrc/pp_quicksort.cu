@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys,
                                                             const GroupOut* __restrict__ gout,
                                                             uint64_t* __restrict__ splits) {
     using C = GroupCfg<K>;
-    __shared__ WalkBuf<K> wb;
+    __shared__ StreamBuf sb;
     __shared__ uint64_t red[4][SW_NT / 32];
     const QSeg q = segs[blockIdx.x];
     K* seg = keys + q.lo;
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys,
     Dirty d;
 #pragma unroll
     for (int k = 0; k < 3; ++k) { d.s[k] = c.ds[k]; d.l[k] = c.dl[k]; }
-    walk_swap<K>(seg, d, pivot, 0, c.Kv, c.Kv, c.W, ~0ull, wb);
+    walk_swap_stream<K>(seg, d, pivot, 0, c.Kv, c.Kv, c.W, sb);
     if (threadIdx.x == 0) splits[blockIdx.x] = Ks;
 }
 
@@ -254,7 +254,8 @@ template <typename K, int LEAF, int NT>
 __global__ void __launch_bounds__(NT) qs_leaf_kernel(K* __restrict__ keys, const uint64_t* __restrict__ leaf_lo,
                                                      const uint32_t* __restrict__ leaf_len) {
     static_assert(LEAF == NT * LEAF_E, "one block holds LEAF keys");
-    __shared__ __align__(16) K sk[LEAF];
+    extern __shared__ __align__(16) unsigned char lsm_b[];
+    K* sk = reinterpret_cast<K*>(lsm_b);  // LEAF keys (dynamic shared memory)
     const uint64_t lo = leaf_lo[blockIdx.x];
     const uint32_t len = leaf_len[blockIdx.x];
     uint32_t P = 32 * LEAF_E;
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(NT) qs_leaf_kernel(K* __restrict__ keys, const
 
 template <typename K>
 struct LeafCfg {
-    static constexpr int LEAF = (sizeof(K) == 8) ? 4096 : 8192;
+    static constexpr int LEAF = 8192;
     static constexpr int NT = LEAF / LEAF_E;
 };
 
@@ -339,7 +340,9 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     using C = GroupCfg<K>;
     using LC = LeafCfg<K>;
     const Params& P = params();
-    const uint64_t LEAF = (P.leaf > 0 && P.leaf <= LC::LEAF) ? (uint64_t)P.leaf : (uint64_t)LC::LEAF;
+    // leaf capacity: default LC::LEAF (8192 keys); "leaf" may lower it
+    const uint64_t LEAF = (P.leaf > 0 && (uint64_t)P.leaf <= (uint64_t)LC::LEAF) ? (uint64_t)P.leaf
+                                                                               : (uint64_t)LC::LEAF;
     const uint64_t BIG = P.qs_cta_max > 0 ? (uint64_t)P.qs_cta_max : (uint64_t)1 << 25;
     const uint64_t MINL = 16;  // at least this many lines per group for mid segments
     int occ = 1;
@@ -504,7 +507,17 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         for (uint64_t b0 = 0; b0 < nleaf; b0 += 65535u * 1024u) {
             const uint64_t cnt = std::min<uint64_t>(nleaf - b0, 65535u * 1024u);
             if (P.leaf_algo == 1) {
-                qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, 0, st>>>(keys, d_lo + b0, d_len + b0);
+                const size_t smem = sizeof(K) * LC::LEAF;
+                cudaFuncSetAttribute(qs_leaf_kernel<K, LC::LEAF, LC::NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+                qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo + b0,
+                                                                                       d_len + b0);
+            } else if (LEAF <= (uint64_t)LC::LEAF / 2) {  // small leaves: half-size CTAs, more per SM
+                constexpr int HL = LC::LEAF / 2, HN = HL / LEAF_E;
+                const size_t smem = 2 * sizeof(K) * HL;
+                cudaFuncSetAttribute(qs_leaf_merge_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+                qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, st>>>(keys, d_lo + b0, d_len + b0);
             } else {
                 const size_t smem = 2 * sizeof(K) * LC::LEAF;
                 cudaFuncSetAttribute(qs_leaf_merge_kernel<K, LC::LEAF, LC::NT>,
