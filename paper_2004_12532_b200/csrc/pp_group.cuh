@@ -272,6 +272,12 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
     if constexpr (C::TMA_STORE) {
         if (tid == 0) bulk_wait<0>();
     }
+    // all loads were waited for: retire the barriers so the shared memory
+    // may be reused by a caller (the fused kernel's later phases)
+    __syncthreads();
+    if (tid == 0) {
+        for (int k = 0; k < 2 * PF; ++k) mbar_inval(&bars[k]);
+    }
     if (tid == 0) {
         const uint64_t T = (uint64_t)fw * LK + tp;
         GroupOut o;

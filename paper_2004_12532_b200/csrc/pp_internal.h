@@ -46,6 +46,8 @@ struct Params {
     int64_t qs_cta_max = 0;        // quicksort: 0 = auto segment size handled by one CTA
     int64_t variant = 0;           // group-kernel configuration (pp_partition.cu VariantCfg)
     int64_t leaf_algo = 0;         // quicksort leaves: 0 merge sort, 1 bitonic network
+    int64_t fused = 0;             // path 2: one cooperative kernel (1) or the kernel chain (0, faster)
+    int64_t fused_stop = 0;        // debug/profiling: stop the fused kernel after this phase
     int64_t qs_waves = 2;          // quicksort mid levels: target CTA waves of the group launch
 };
 Params& params();

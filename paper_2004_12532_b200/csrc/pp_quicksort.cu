@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys,
                                                             const GroupOut* __restrict__ gout,
                                                             uint64_t* __restrict__ splits) {
     using C = GroupCfg<K>;
-    __shared__ StreamBuf sb;
+    __shared__ StreamBuf<SW_NT, SW_EPT2> sb;
     __shared__ uint64_t red[4][SW_NT / 32];
     const QSeg q = segs[blockIdx.x];
     K* seg = keys + q.lo;
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys,
     Dirty d;
 #pragma unroll
     for (int k = 0; k < 3; ++k) { d.s[k] = c.ds[k]; d.l[k] = c.dl[k]; }
-    walk_swap_stream<K>(seg, d, pivot, 0, c.Kv, c.Kv, c.W, sb);
+    walk_swap_stream<K, SW_NT, SW_EPT2>(seg, d, pivot, 0, c.Kv, c.Kv, c.W, sb);
     if (threadIdx.x == 0) splits[blockIdx.x] = Ks;
 }
 
