@@ -30,9 +30,11 @@ struct GroupCfgT {
     static_assert(NW <= 16, "warp totals are packed into at most two 16-byte words");
 };
 
-// the default configuration (used by quicksort and by variant 0)
+// the default configuration (used by quicksort and by variant 0), measured
+// fastest on B200 (tools/tune.py): 8 KiB lines for u64 (b = 1024 keys),
+// 4 KiB lines for u32 (b = 1024 keys, 4 CTAs per SM); 128 threads.
 template <typename K>
-using GroupCfg = GroupCfgT<K, 8192, 128, 4, false>;
+using GroupCfg = GroupCfgT<K, sizeof(K) == 8 ? 8192 : 4096, 128, 4, false>;
 
 // Line index of the j-th line (group order) of group gi: G_i(j) of
 // PAPER.md:963-969 in 0-based form, j*g + ((X[j] + i) mod g).
