@@ -49,6 +49,7 @@ struct Params {
     int64_t fused = 0;             // path 2: one cooperative kernel (1) or the kernel chain (0, faster)
     int64_t fused_stop = 0;        // debug/profiling: stop the fused kernel after this phase
     int64_t qs_waves = 2;          // quicksort mid levels: target CTA waves of the group launch
+    int64_t qs_small = 1 << 16;    // quicksort: segments <= this finish in one CTA (0 = off)
 };
 Params& params();
 

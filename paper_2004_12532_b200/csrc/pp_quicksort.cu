@@ -176,6 +176,56 @@ __device__ __forceinline__ void cmpx(K& a, K& b) {
     b = hi;
 }
 
+// Shared-memory index padding for the merge sorts: one spare slot per 8 keys,
+// so that a warp whose lanes each own 8 consecutive keys hits distinct banks
+// (stride 9 words instead of 8).
+__device__ __forceinline__ uint32_t lpad(uint32_t i) { return i + (i >> 3); }
+
+template <typename K>
+__device__ __forceinline__ void sort8(K (&v)[8]) {  // Batcher's 19-comparator network
+    cmpx(v[0], v[1]); cmpx(v[2], v[3]); cmpx(v[4], v[5]); cmpx(v[6], v[7]);
+    cmpx(v[0], v[2]); cmpx(v[1], v[3]); cmpx(v[4], v[6]); cmpx(v[5], v[7]);
+    cmpx(v[1], v[2]); cmpx(v[5], v[6]);
+    cmpx(v[0], v[4]); cmpx(v[1], v[5]); cmpx(v[2], v[6]); cmpx(v[3], v[7]);
+    cmpx(v[2], v[4]); cmpx(v[3], v[5]);
+    cmpx(v[1], v[2]); cmpx(v[3], v[4]); cmpx(v[5], v[6]);
+}
+
+// One merge step for the 8 outputs starting at `base`: runs of length L in
+// src (padded layout) -> dst.  Runs A = [blk, blk+La), B = [blk+La, +Lb)
+// (the last pair may be short); the start is found on the merge path by
+// binary search (ties: A first).
+template <typename K>
+__device__ __forceinline__ void merge_chunk(const K* __restrict__ src, K* __restrict__ dst, uint32_t base,
+                                            uint32_t L, uint32_t P) {
+    const K KMAX = (K)~(K)0;
+    const uint32_t blk = base / (2 * L) * (2 * L);
+    const uint32_t d = base - blk;
+    const uint32_t La = min(L, P - blk);
+    const uint32_t Lb = min(L, P - blk - La);
+    const uint32_t A0 = blk, B0 = blk + La;
+    uint32_t a0 = d > Lb ? d - Lb : 0, a1 = d < La ? d : La;
+    while (a0 < a1) {
+        const uint32_t mid = (a0 + a1) >> 1;
+        if (src[lpad(A0 + mid)] <= src[lpad(B0 + d - 1 - mid)]) a0 = mid + 1; else a1 = mid;
+    }
+    uint32_t a = a0, b = d - a0;
+    K xa = a < La ? src[lpad(A0 + a)] : KMAX, xb = b < Lb ? src[lpad(B0 + b)] : KMAX;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const bool takeA = (b >= Lb) || (a < La && xa <= xb);
+        if (takeA) {
+            dst[lpad(base + r)] = xa;
+            ++a;
+            xa = a < La ? src[lpad(A0 + a)] : KMAX;
+        } else {
+            dst[lpad(base + r)] = xb;
+            ++b;
+            xb = b < Lb ? src[lpad(B0 + b)] : KMAX;
+        }
+    }
+}
+
 // Leaf sort by merging: every thread sorts its 8 keys in registers (Batcher's
 // 19-comparator network), then log2(P/8) rounds merge pairs of sorted runs
 // in shared memory; each thread produces 8 outputs of a merge, locating its
@@ -188,7 +238,7 @@ __global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
     static_assert(LEAF == NT * LEAF_E, "one block holds LEAF keys");
     extern __shared__ __align__(16) unsigned char lsm[];
     K* src = reinterpret_cast<K*>(lsm);
-    K* dst = src + LEAF;
+    K* dst = src + lpad(LEAF);
     const uint64_t lo = leaf_lo[blockIdx.x];
     const uint32_t len = leaf_len[blockIdx.x];
     // pad to whole warps of 8 keys per thread (not to a power of two)
@@ -197,57 +247,192 @@ __global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
     const uint32_t tid = threadIdx.x;
     if (tid >= nthr) return;
     const K KMAX = (K)~(K)0;
-    for (uint32_t i = tid; i < P; i += nthr) src[i] = i < len ? keys[lo + i] : KMAX;
+    for (uint32_t i = tid; i < P; i += nthr) src[lpad(i)] = i < len ? keys[lo + i] : KMAX;
     leaf_bar(nthr);
     const uint32_t base = tid * LEAF_E;
     K v[LEAF_E];
 #pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) v[r] = src[base + r];
-    cmpx(v[0], v[1]); cmpx(v[2], v[3]); cmpx(v[4], v[5]); cmpx(v[6], v[7]);
-    cmpx(v[0], v[2]); cmpx(v[1], v[3]); cmpx(v[4], v[6]); cmpx(v[5], v[7]);
-    cmpx(v[1], v[2]); cmpx(v[5], v[6]);
-    cmpx(v[0], v[4]); cmpx(v[1], v[5]); cmpx(v[2], v[6]); cmpx(v[3], v[7]);
-    cmpx(v[2], v[4]); cmpx(v[3], v[5]);
-    cmpx(v[1], v[2]); cmpx(v[3], v[4]); cmpx(v[5], v[6]);
+    for (int r = 0; r < LEAF_E; ++r) v[r] = src[lpad(base + r)];
+    sort8(v);
 #pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) src[base + r] = v[r];
+    for (int r = 0; r < LEAF_E; ++r) src[lpad(base + r)] = v[r];
     leaf_bar(nthr);
     for (uint32_t L = LEAF_E; L < P; L <<= 1) {
-        // runs A = [blk, blk+La), B = [blk+La, blk+La+Lb) (the last pair may be short)
-        const uint32_t blk = base / (2 * L) * (2 * L);
-        const uint32_t d = base - blk;
-        const uint32_t La = min(L, P - blk);
-        const uint32_t Lb = min(L, P - blk - La);
-        const K* A = src + blk;
-        const K* B = A + La;
-        uint32_t a0 = d > Lb ? d - Lb : 0, a1 = d < La ? d : La;
-        while (a0 < a1) {
-            const uint32_t mid = (a0 + a1) >> 1;
-            if (A[mid] <= B[d - 1 - mid]) a0 = mid + 1; else a1 = mid;
-        }
-        uint32_t a = a0, b = d - a0;
-        K xa = a < La ? A[a] : KMAX, xb = b < Lb ? B[b] : KMAX;
-#pragma unroll
-        for (int r = 0; r < LEAF_E; ++r) {
-            const bool takeA = (b >= Lb) || (a < La && xa <= xb);
-            if (takeA) {
-                v[r] = xa;
-                ++a;
-                xa = a < La ? A[a] : KMAX;
-            } else {
-                v[r] = xb;
-                ++b;
-                xb = b < Lb ? B[b] : KMAX;
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < LEAF_E; ++r) dst[base + r] = v[r];
+        merge_chunk<K>(src, dst, base, L, P);
         leaf_bar(nthr);
         K* t = src;
         src = dst;
         dst = t;
     }
-    for (uint32_t i = tid; i < len; i += nthr) keys[lo + i] = src[i];
+    for (uint32_t i = tid; i < len; i += nthr) keys[lo + i] = src[lpad(i)];
+}
+
+// ===========================================================================
+// CTA-level quicksort of small segments (LEAF < len <= qs_small keys): one
+// CTA runs the whole remaining recursion of its segment -- partitions with
+// the group engine (g = 1: a plain two-ended line partition) plus the
+// streaming cleanup of its head / tail / open lines, depth first with an
+// explicit stack (smaller part first), and sorts pieces <= SMALL_LEAF keys in
+// shared memory by merging.  This removes the deepest, least efficient
+// levels of the breadth-first loop (many tiny CTAs, one launch + sync each).
+// ===========================================================================
+template <typename K>
+struct SmallCfg {
+    static constexpr int NT = 256;
+    using GC = GroupCfgT<K, 8192, 256, 4, false>;
+    static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 4096 : 8192;  // 2 x LEAFC keys <= 64 KiB
+    static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);  // two padded buffers
+    static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
+};
+
+// Merge sort of len <= NT*8*V keys held in global memory at g (in place),
+// through two shared-memory buffers A, B; all NT threads participate, each
+// handling chunks of 8 keys (thread t: chunks t, t+NT, ...).
+template <typename K, int NT>
+__device__ void cta_merge_sort(K* __restrict__ g, uint32_t len, K* A, K* B) {
+    const K KMAX = (K)~(K)0;
+    const uint32_t P = (len + 7) / 8 * 8, nch = P / 8;
+    for (uint32_t i = threadIdx.x; i < P; i += NT) A[lpad(i)] = i < len ? g[i] : KMAX;
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < nch; c += NT) {
+        K v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = A[lpad(8 * c + r)];
+        sort8(v);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) A[lpad(8 * c + r)] = v[r];
+    }
+    __syncthreads();
+    K* src = A;
+    K* dst = B;
+    for (uint32_t L = 8; L < P; L <<= 1) {
+        for (uint32_t c = threadIdx.x; c < nch; c += NT) merge_chunk<K>(src, dst, 8 * c, L, P);
+        __syncthreads();
+        K* t = src;
+        src = dst;
+        dst = t;
+    }
+    for (uint32_t i = threadIdx.x; i < len; i += NT) g[i] = src[lpad(i)];
+    __syncthreads();
+}
+
+// In-place partition of seg[0, len) by key < pivot with one CTA; returns K.
+template <typename K>
+__device__ uint64_t cta_partition(K* __restrict__ seg, uint64_t len, K pivot, uint64_t seed, unsigned char* smem,
+                                  GroupOut* scratch, Ctl* sc, uint64_t* red) {
+    using S = SmallCfg<K>;
+    using GC = typename S::GC;
+    constexpr int NT = S::NT, NW = NT / 32;
+    const uint64_t addr = (uint64_t)(uintptr_t)seg;
+    uint64_t h = ((16 - (addr & 15)) & 15) / sizeof(K);
+    if (h > len) h = len;
+    const uint64_t nl = (len - h) / GC::LK;
+    uint64_t T = 0, v = 0;
+    // this CTA's earlier generic-proxy stores to the segment must be visible
+    // to the engine's bulk-copy (async-proxy) loads
+    asm volatile("fence.proxy.async;" ::: "memory");
+    __syncthreads();
+    if (nl > 0) {
+        ss_group_engine<GC>(seg + h, nl, 1, 0, seed, pivot, scratch, smem);
+        __syncthreads();
+        T = scratch->T;
+        v = scratch->vlo;
+    }
+    const uint64_t region_end = nl * GC::LK;
+    uint64_t ht = 0;
+    for (uint64_t x = threadIdx.x; x < h; x += NT) ht += is_pred(seg[x], pivot) ? 1 : 0;
+    for (uint64_t x = h + region_end + threadIdx.x; x < len; x += NT) ht += is_pred(seg[x], pivot) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ht += __shfl_xor_sync(0xffffffffu, ht, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ht;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < NW; ++w) ht += red[w];
+        const uint64_t Ks = T + ht;
+        uint64_t a[3], b[3];
+        a[0] = 0; b[0] = h;
+        a[1] = (h + v) < Ks ? (h + v) : Ks;
+        b[1] = (h + v) > Ks ? (h + v) : Ks;
+        if (nl == 0) { a[1] = b[1] = 0; }
+        a[2] = h + region_end; b[2] = len;
+        finish_ctl(sc, len, Ks, a, b);
+    }
+    __syncthreads();
+    Dirty d;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        d.s[k] = sc->ds[k];
+        d.l[k] = sc->dl[k];
+    }
+    const uint64_t Ks = sc->K, Kv = sc->Kv, W = sc->W;
+    walk_swap_stream<K, NT, SW_EPT2>(seg, d, pivot, 0, Kv, Kv, W,
+                                     *reinterpret_cast<StreamBuf<NT, SW_EPT2>*>(smem));
+    __syncthreads();
+    return Ks;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(SmallCfg<K>::NT, 2) qs_small_kernel(K* __restrict__ keys,
+                                                                   const uint64_t* __restrict__ seg_lo,
+                                                                   const uint32_t* __restrict__ seg_len,
+                                                                   uint64_t seed, GroupOut* __restrict__ scratch) {
+    using S = SmallCfg<K>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ Ctl sc;
+    __shared__ uint64_t red[S::NT / 32];
+    __shared__ uint64_t st_lo[64], st_hi[64], st_p[64];
+    __shared__ int st_mode[64];
+    __shared__ int sp;
+    const K KMAX = (K)~(K)0;
+    K* A = reinterpret_cast<K*>(smem);
+    K* B = A + lpad(S::LEAFC);
+    if (threadIdx.x == 0) {
+        st_lo[0] = seg_lo[blockIdx.x];
+        st_hi[0] = st_lo[0] + seg_len[blockIdx.x];
+        st_mode[0] = 0;
+        st_p[0] = 0;
+        sp = 1;
+    }
+    __syncthreads();
+    while (sp > 0) {
+        const int top = sp - 1;
+        const uint64_t lo = st_lo[top], hi = st_hi[top], pm = st_p[top];
+        const int mode = st_mode[top];
+        __syncthreads();
+        if (threadIdx.x == 0) sp = top;
+        const uint64_t len = hi - lo;
+        if (len <= 1) {
+            __syncthreads();
+            continue;
+        }
+        if (len <= S::LEAFC) {
+            cta_merge_sort<K, S::NT>(keys + lo, (uint32_t)len, A, B);
+            continue;
+        }
+        K p;
+        if (mode == 0) p = median3<K>(keys[lo], keys[lo + (len - 1) / 2], keys[hi - 1]);
+        else p = (K)pm;
+        const uint64_t k = cta_partition<K>(keys + lo, len, p, seed, smem, scratch + blockIdx.x, &sc, red);
+        if (threadIdx.x == 0) {
+            int s = sp;
+            if (mode == 0 && k == 0) {
+                if (p != KMAX) {  // p is the minimum: split by x <= p next (reading R14)
+                    st_lo[s] = lo; st_hi[s] = hi; st_mode[s] = 1; st_p[s] = (uint64_t)(K)(p + 1); ++s;
+                }
+            } else if (mode == 1) {
+                st_lo[s] = lo + k; st_hi[s] = hi; st_mode[s] = 0; st_p[s] = 0; ++s;  // [lo, lo+k) all == p
+            } else {
+                // push the larger part first: the smaller is processed next (stack depth <= log2 len)
+                const bool left_small = k < len - k;
+                const uint64_t a0 = left_small ? lo + k : lo, a1 = left_small ? hi : lo + k;
+                const uint64_t b0 = left_small ? lo : lo + k, b1 = left_small ? lo + k : hi;
+                st_lo[s] = a0; st_hi[s] = a1; st_mode[s] = 0; st_p[s] = 0; ++s;
+                st_lo[s] = b0; st_hi[s] = b1; st_mode[s] = 0; st_p[s] = 0; ++s;
+            }
+            sp = s;
+        }
+        __syncthreads();
+    }
 }
 
 template <typename K, int LEAF, int NT>
@@ -357,19 +542,24 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         uint32_t mode;
     };
     std::vector<HSeg> cur{{0, n, 0, 0}}, next;
-    std::vector<uint64_t> leaf_lo;
-    std::vector<uint32_t> leaf_len;
+    std::vector<uint64_t> leaf_lo, small_lo;
+    std::vector<uint32_t> leaf_len, small_len;
+    // segments in (LEAF, SMALL] finish in one CTA each (qs_small_kernel)
+    const uint64_t SMALL = P.qs_small > 0 ? std::max<uint64_t>((uint64_t)P.qs_small, LEAF) : LEAF;
     auto add_child = [&](uint64_t lo, uint64_t hi) {
         const uint64_t len = hi - lo;
         if (len <= 1) return;
         if (len <= LEAF) {
             leaf_lo.push_back(lo);
             leaf_len.push_back((uint32_t)len);
+        } else if (len <= SMALL) {
+            small_lo.push_back(lo);
+            small_len.push_back((uint32_t)len);
         } else {
             next.push_back({lo, hi, 0, 0});
         }
     };
-    if (n <= LEAF) {
+    if (n <= SMALL) {
         cur.clear();
         add_child(0, n);
     }
@@ -493,12 +683,33 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         for (size_t bi = 0; bi < nbig; ++bi) visit(cur[big_idx[bi]], pivots_h[big_idx[bi]], splits_h[nmid + bi]);
         cur.swap(next);
     }
-    // ---- leaves ----
-    const uint64_t nleaf = leaf_lo.size();
+    // ---- small segments (one CTA each) and leaves: one workspace ----
+    const uint64_t nleaf = leaf_lo.size(), nsmall = small_lo.size();
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t loB = al(8 * nleaf), lnB = al(4 * nleaf), sloB = al(8 * nsmall), slnB = al(4 * nsmall);
+    const size_t scrB = al(sizeof(GroupOut) * nsmall);
+    unsigned char* qws = static_cast<unsigned char*>(qs_workspace(loB + lnB + sloB + slnB + scrB + 256));
+    if (!qws) return PP_E_NOMEM;
+    if (nsmall > 0) {
+        using S = SmallCfg<K>;
+        uint64_t* d_slo = reinterpret_cast<uint64_t*>(qws + loB + lnB);
+        uint32_t* d_sln = reinterpret_cast<uint32_t*>(qws + loB + lnB + sloB);
+        GroupOut* d_scr = reinterpret_cast<GroupOut*>(qws + loB + lnB + sloB + slnB);
+        e = cudaMemcpyAsync(d_slo, small_lo.data(), 8 * nsmall, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_sln, small_len.data(), 4 * nsmall, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort small H2D");
+        cudaFuncSetAttribute(qs_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+        for (uint64_t b0 = 0; b0 < nsmall; b0 += 65535u * 1024u) {
+            const uint64_t cnt = std::min<uint64_t>(nsmall - b0, 65535u * 1024u);
+            qs_small_kernel<K><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(keys, d_slo + b0, d_sln + b0, P.seed,
+                                                                      d_scr + b0);
+            note_launches(1);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort small launch");
+    }
     if (nleaf > 0) {
-        const size_t loB = ((8 * nleaf) + 255) & ~size_t(255);
-        unsigned char* ws = static_cast<unsigned char*>(qs_workspace(loB + 4 * nleaf));
-        if (!ws) return PP_E_NOMEM;
+        unsigned char* ws = qws;
         uint64_t* d_lo = reinterpret_cast<uint64_t*>(ws);
         uint32_t* d_len = reinterpret_cast<uint32_t*>(ws + loB);
         e = cudaMemcpyAsync(d_lo, leaf_lo.data(), 8 * nleaf, cudaMemcpyHostToDevice, st);
@@ -514,12 +725,12 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                                                                                        d_len + b0);
             } else if (LEAF <= (uint64_t)LC::LEAF / 2) {  // small leaves: half-size CTAs, more per SM
                 constexpr int HL = LC::LEAF / 2, HN = HL / LEAF_E;
-                const size_t smem = 2 * sizeof(K) * HL;
+                const size_t smem = 2 * sizeof(K) * (HL + HL / 8);
                 cudaFuncSetAttribute(qs_leaf_merge_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem);
                 qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, st>>>(keys, d_lo + b0, d_len + b0);
             } else {
-                const size_t smem = 2 * sizeof(K) * LC::LEAF;
+                const size_t smem = 2 * sizeof(K) * (LC::LEAF + LC::LEAF / 8);
                 cudaFuncSetAttribute(qs_leaf_merge_kernel<K, LC::LEAF, LC::NT>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo + b0,
@@ -529,10 +740,10 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         }
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "quicksort leaf launch");
-        // the host vectors must outlive the async copies
-        e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) return cuda_fail(e, "quicksort leaves");
     }
+    // the host vectors must outlive the async copies
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "quicksort leaves");
     last_stats().aux_bytes = g_qws_bytes;
     return PP_OK;
 }

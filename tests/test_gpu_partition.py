@@ -310,6 +310,23 @@ def test_config3_single_gpu_full(pp):
     assert side_prints(False, split) == before
 
 
+def test_config4_zipf_full(pp):
+    """BASELINE config 4 Zipf case: n = 1,000,000,007 u32 keys, Zipf(1.1)
+    ranks - 1 on [0, 2^32) (duplicate-heavy: ~10.5% of keys are 0), pivot =
+    the sample median (SURVEY §8(c) reading 17).  Split against the oracle's
+    count on the host; predicate and per-side multisets on the device."""
+    from gpu_util import check_partition_device
+    n = 1_000_000_007
+    t = synth.zipf_u32_torch(n, 1.1, synth.SEEDS["c4"], "cuda")
+    wide = t.to(torch.int64) & 0xFFFFFFFF
+    pivot = int(torch.sort(wide).values[n // 2])  # sample median (library sort)
+    del wide
+    K = oracle.count(t.cpu().numpy().view(np.uint32), pivot)
+    inp = t.clone()
+    split = pp.pp_partition(t, pivot)
+    check_partition_device(inp, t, pivot, split, K)
+
+
 @pytest.mark.parametrize("pat", list(synth.ADV_PATTERNS))
 def test_config4_adversarial_full(pp, pat):
     n = 1_000_000_007

@@ -31,6 +31,21 @@ def test_shard_offsets_compose():
     assert np.array_equal(full, np.concatenate(parts))
 
 
+def test_zipf_torch_matches_truncated_law():
+    """The device Zipf(1.1) sampler (rejection-inversion) against the exact
+    truncated law P(rank = k) = k^-1.1 / (zeta(1.1) - zeta(1.1, 2^32 + 1))
+    (Hurwitz zeta, scipy): P(key = 0), P(key < 7), P(key < 217) within 5 sigma."""
+    from scipy.special import zeta
+    s = 1.1
+    Z = zeta(s) - zeta(s, 2.0 ** 32 + 1)
+    n = 300_000
+    z = synth.zipf_u32_torch(n, s, 123, "cpu").numpy().view(np.uint32)
+    for thr in (1, 7, 217):
+        p = sum(k ** -s for k in range(1, thr + 1)) / Z
+        sigma = (p * (1 - p) / n) ** 0.5
+        assert abs((z < thr).mean() - p) < 5 * sigma, (thr, (z < thr).mean(), p)
+
+
 def test_adversarial_patterns():
     n = 1001
     for pat in synth.ADV_PATTERNS:
