@@ -15,8 +15,9 @@ stream (per-step events are recorded too).
 
 N > 1 (torchrun): each rank partitions its own contiguous 2^27-key shard of
 one global array (weak scaling) and the ranks exchange misplaced ranges over
-NCCL to complete the GLOBAL partition (paper_2004_12532_b200.dist); the step
-time is the max over ranks.
+NCCL to complete the GLOBAL partition (C ABI pp_partition_dist_u64: local
+partition, ncclAllGather of the counts, ncclSend/ncclRecv of misplaced
+ranges); the step time is the max over ranks.
 
 --impl reference: the CPU oracle (oracle/, serial two-pointer partition,
 PAPER.md:1433-1436) on the host cores, same workload and metric.
@@ -217,13 +218,17 @@ def main():
     work = torch.empty_like(pristine)
     flush = torch.ones(L2_FLUSH_BYTES // 8, dtype=torch.int64, device=dev)
     d_split = torch.zeros(1, dtype=torch.int64, device=dev)
+    last_split = [None]
     if ws > 1:
-        from paper_2004_12532_b200 import dist as ppdist
-        comm = ppdist.Partitioner(dev)
+        # the library's own NCCL communicator (C ABI pp_dist_*): rank 0 makes
+        # the unique id, the torch process group only carries its 128 bytes
+        uid = [pp.pp_dist_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        pp.pp_dist_init(uid[0], ws, rank, local)
 
     def step(buf):
         if ws > 1:
-            comm.partition_u64(buf, PIVOT)
+            last_split[0] = pp.pp_partition_dist(buf, PIVOT)
         else:
             pp.pp_partition_async_u64(buf, PIVOT, d_split)
 
@@ -271,7 +276,7 @@ def main():
         tot_ms = float(t.item())
 
     # sanity: the split equals the oracle's count on this input (cheap check)
-    split = int(d_split.item()) if ws == 1 else comm.last_global_split
+    split = int(d_split.item()) if ws == 1 else last_split[0]
     stats = pp.pp_last_stats() if ws == 1 else {}
 
     value = ws * n * args.steps / (tot_ms / 1e3)
@@ -324,6 +329,7 @@ def main():
     if rank == 0:
         print(json.dumps(out))
     if ws > 1:
+        pp.pp_dist_finalize()
         dist.destroy_process_group()
     return 0
 

@@ -89,6 +89,39 @@ pp_status pp_quicksort_host_u64(uint64_t *host_keys, uint64_t n);
 uint64_t pp_partition(uint64_t *keys, uint64_t n, uint64_t pivot);
 pp_status pp_quicksort(uint64_t *keys, uint64_t n);
 
+/* ---- multi-GPU partition (BASELINE config 3) ------------------
+ * One process per GPU; the global array is the concatenation of the ranks'
+ * shards in rank order.  Collective calls: every rank must call them, in
+ * the same order.
+ * pp_dist_unique_id: fills out128 (128 bytes) with a fresh NCCL unique id;
+ *   call on one rank and share the bytes with the others (any channel).
+ * pp_dist_init: creates the library's NCCL communicator (NCCL is loaded at
+ *   run time; the copy PyTorch already loaded is preferred).  device = the
+ *   CUDA device of this rank.  PP_E_NCCL on NCCL failure.
+ * pp_partition_dist_u64/u32: partitions the local DEVICE shard (n_local keys)
+ *   by key < pivot, then exchanges misplaced ranges so that the GLOBAL array
+ *   is partitioned; *global_split_out = K = #keys < pivot over all ranks
+ *   (HOST pointer).  The local step is pp_partition_*; then ncclAllGather of
+ *   (n_r, t_r, pivot), a plan computed identically on every rank, and
+ *   ncclSend/ncclRecv rounds through a staging buffer of <= the staging size
+ *   (default 256 MiB, pp_dist_set_staging).  Mismatched pivots or key types
+ *   across ranks -> PP_E_INVAL on every rank.  Synchronises `stream`.
+ * pp_dist_plan: the exchange plan alone (host arithmetic, no GPU): for shard
+ *   sizes ns[P] and local splits ts[P], writes *n_out pieces of 6 uint64
+ *   {round, rank_f, f, rank_t, t, len} (swap global [f, f+len) on rank_f with
+ *   [t, t+len) on rank_t) into out[6*out_cap] and K into *K_out.
+ * pp_dist_finalize: destroys the communicator and frees the buffers. */
+pp_status pp_dist_unique_id(void *out128);
+pp_status pp_dist_init(const void *id128, int nranks, int rank, int device);
+pp_status pp_partition_dist_u64(uint64_t *shard, uint64_t n_local, uint64_t pivot, void *stream,
+                                uint64_t *global_split_out);
+pp_status pp_partition_dist_u32(uint32_t *shard, uint64_t n_local, uint32_t pivot, void *stream,
+                                uint64_t *global_split_out);
+pp_status pp_dist_set_staging(uint64_t bytes);
+pp_status pp_dist_plan(const uint64_t *ns, const uint64_t *ts, int nranks, uint64_t cap, uint64_t *out,
+                       uint64_t out_cap, uint64_t *n_out, uint64_t *K_out);
+pp_status pp_dist_finalize(void);
+
 /* ---- Smoothed Striding partial partition step alone (parity of internals) --
  * Runs only the group kernel on the 16-B aligned region of `keys` with g
  * groups (g = 0: the library's automatic choice) and copies the per-group

@@ -89,6 +89,13 @@ def load(build_if_missing: bool = True):
         "pp_launch_count": ([ctypes.c_int], u64),
         "pp_timing": ([ctypes.c_int], None),
         "pp_timing_read": ([ctypes.POINTER(ctypes.c_double)], st),
+        "pp_dist_unique_id": ([vp], st),
+        "pp_dist_init": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int], st),
+        "pp_partition_dist_u64": ([vp, u64, u64, vp, P64], st),
+        "pp_partition_dist_u32": ([vp, u64, u32, vp, P64], st),
+        "pp_dist_set_staging": ([u64], st),
+        "pp_dist_plan": ([P64, P64, ctypes.c_int, u64, P64, u64, P64, P64], st),
+        "pp_dist_finalize": ([], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -252,6 +259,54 @@ def pp_workspace_bytes(n: int, key_bytes: int = 8, op: int = 0) -> int:
 
 def pp_launch_count(reset: bool = False) -> int:
     return int(load().pp_launch_count(1 if reset else 0))
+
+
+def pp_dist_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load().pp_dist_unique_id(buf), "pp_dist_unique_id")
+    return buf.raw
+
+
+def pp_dist_init(unique_id: bytes, nranks: int, rank: int, device: int) -> None:
+    assert len(unique_id) == 128
+    buf = ctypes.create_string_buffer(unique_id, 128)
+    _check(load().pp_dist_init(buf, nranks, rank, device), "pp_dist_init")
+
+
+def pp_partition_dist(shard, pivot: int, stream=None) -> int:
+    """Global partition of a sharded array (collective; see include/pp.h)."""
+    kind = _key_kind(shard)
+    out = ctypes.c_uint64(0)
+    f = load().pp_partition_dist_u64 if kind == "u64" else load().pp_partition_dist_u32
+    _check(f(shard.data_ptr(), shard.numel(), _pivot(pivot, kind), _stream_ptr(stream), ctypes.byref(out)),
+           "pp_partition_dist")
+    return int(out.value)
+
+
+def pp_dist_set_staging(nbytes: int) -> None:
+    _check(load().pp_dist_set_staging(int(nbytes)), "pp_dist_set_staging")
+
+
+def pp_dist_finalize() -> None:
+    _check(load().pp_dist_finalize(), "pp_dist_finalize")
+
+
+def pp_dist_plan(ns, ts, cap: int):
+    """The exchange plan (host arithmetic): (K, rows) with rows of
+    (round, rank_f, f, rank_t, t, len)."""
+    P = len(ns)
+    a = np.ascontiguousarray(np.asarray(ns, dtype=np.uint64))
+    b = np.ascontiguousarray(np.asarray(ts, dtype=np.uint64))
+    P64 = ctypes.POINTER(ctypes.c_uint64)
+    n_out = ctypes.c_uint64(0)
+    K = ctypes.c_uint64(0)
+    _check(load().pp_dist_plan(a.ctypes.data_as(P64), b.ctypes.data_as(P64), P, int(cap), None, 0,
+                               ctypes.byref(n_out), ctypes.byref(K)), "pp_dist_plan")
+    rows = np.zeros((max(1, n_out.value), 6), dtype=np.uint64)
+    _check(load().pp_dist_plan(a.ctypes.data_as(P64), b.ctypes.data_as(P64), P, int(cap),
+                               rows.ctypes.data_as(P64), n_out.value, ctypes.byref(n_out), ctypes.byref(K)),
+           "pp_dist_plan")
+    return int(K.value), [tuple(int(x) for x in r) for r in rows[: n_out.value]]
 
 
 def pp_timing(enable: bool) -> None:

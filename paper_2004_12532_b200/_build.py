@@ -35,11 +35,27 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
+def nccl_paths():
+    """(include dir, library file) of the NCCL that PyTorch ships (the one
+    loaded at run time), falling back to the system NCCL headers."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc, lib
+    except Exception:
+        pass
+    return "/usr/include", "libnccl.so.2"
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *sources()]
+    nccl_inc, nccl_lib = nccl_paths()
+    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", nccl_inc,
+           f'-DPP_NCCL_LIB="{nccl_lib}"', "-o", LIB + ".tmp", *sources(), "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

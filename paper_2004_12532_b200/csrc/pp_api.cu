@@ -301,6 +301,42 @@ pp_status pp_ss_groups_u32(uint32_t* keys, uint64_t n, uint32_t pivot, uint64_t 
 }
 uint64_t pp_max_groups(void) { return max_groups(); }
 
+pp_status pp_dist_unique_id(void* out128) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return dist_unique_id(out128);
+}
+pp_status pp_dist_init(const void* id128, int nranks, int rank, int device) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return dist_init(id128, nranks, rank, device);
+}
+pp_status pp_dist_finalize(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return dist_finalize();
+}
+pp_status pp_dist_set_staging(uint64_t bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    dist_set_staging(bytes);
+    return PP_OK;
+}
+pp_status pp_partition_dist_u64(uint64_t* shard, uint64_t n_local, uint64_t pivot, void* stream,
+                                uint64_t* global_split_out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    pp_status s = check_device_keys(shard, n_local);
+    if (s != PP_OK) return s;
+    return partition_dist<uint64_t>(shard, n_local, pivot, (cudaStream_t)stream, global_split_out);
+}
+pp_status pp_partition_dist_u32(uint32_t* shard, uint64_t n_local, uint32_t pivot, void* stream,
+                                uint64_t* global_split_out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    pp_status s = check_device_keys(shard, n_local);
+    if (s != PP_OK) return s;
+    return partition_dist<uint32_t>(shard, n_local, pivot, (cudaStream_t)stream, global_split_out);
+}
+pp_status pp_dist_plan(const uint64_t* ns, const uint64_t* ts, int nranks, uint64_t cap, uint64_t* out,
+                       uint64_t out_cap, uint64_t* n_out, uint64_t* K_out) {
+    return dist_plan(ns, ts, nranks, cap, out, out_cap, n_out, K_out);
+}
+
 uint64_t pp_workspace_bytes(uint64_t n, int key_bytes, int op) {
     // tile/task arrays (<= 2^18 entries each side) + groups + control
     uint64_t tiles = n / 4096 + 2, tasks = n / 8192 + 2;

@@ -1,0 +1,329 @@
+// pp_dist.cu -- multi-GPU partition of one array sharded contiguously over
+// ranks (BASELINE config 3): local partition on every
+// rank, ncclAllGather of (n_r, t_r, pivot), identical exchange plan on every
+// rank, and ncclSend/ncclRecv of matched misplaced ranges through a bounded
+// staging buffer.  NCCL is loaded at run time (dlopen) -- preferably the copy
+// already loaded by PyTorch in this process -- so libpp.so has no link-time
+// NCCL dependency and two NCCLs never end up in one process.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "pp_internal.h"
+
+namespace pp {
+
+// ---------------------------------------------------------------------------
+// The exchange plan (host arithmetic; mirrored independently in Python by
+// paper_2004_12532_b200/dist.py and cross-checked by tests/test_dist.py).
+// ---------------------------------------------------------------------------
+struct Piece {
+    uint64_t round, rank_f, f, rank_t, t, len;
+};
+
+// Pairs the i-th misplaced successor (global order, left of K) with the i-th
+// misplaced predecessor (right of K); splits transfers into pieces <= cap and
+// groups them into rounds where no rank moves more than cap keys.
+static uint64_t plan_pieces(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap,
+                            std::vector<Piece>& out) {
+    uint64_t K = 0;
+    for (int r = 0; r < P; ++r) K += ts[r];
+    struct Iv {
+        uint64_t rank, s, e;
+    };
+    std::vector<Iv> F, T;
+    uint64_t base = 0;
+    for (int r = 0; r < P; ++r) {
+        const uint64_t b = base, n = ns[r], t = ts[r];
+        const uint64_t fs = b + t, fe = std::min(K, b + n);
+        if (fs < fe) F.push_back({(uint64_t)r, fs, fe});
+        const uint64_t s2 = std::max(K, b), e2 = b + t;
+        if (s2 < e2) T.push_back({(uint64_t)r, s2, e2});
+        base += n;
+    }
+    out.clear();
+    std::vector<uint64_t> used(P, 0);
+    uint64_t round = 0;
+    size_t i = 0, j = 0;
+    while (i < F.size() && j < T.size()) {
+        const uint64_t m = std::min(F[i].e - F[i].s, T[j].e - T[j].s);
+        // split into pieces of <= cap, each placed in the current or a new round
+        uint64_t s = 0;
+        while (s < m) {
+            const uint64_t len = std::min(cap, m - s);
+            if (used[F[i].rank] + len > cap || used[T[j].rank] + len > cap) {
+                ++round;
+                std::fill(used.begin(), used.end(), 0);
+            }
+            out.push_back({round, F[i].rank, F[i].s + s, T[j].rank, T[j].s + s, len});
+            used[F[i].rank] += len;
+            used[T[j].rank] += len;
+            s += len;
+        }
+        F[i].s += m;
+        T[j].s += m;
+        if (F[i].s == F[i].e) ++i;
+        if (T[j].s == T[j].e) ++j;
+    }
+    return K;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time.
+// ---------------------------------------------------------------------------
+struct NcclApi {
+    void* lib = nullptr;
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclAllGather) AllGather = nullptr;
+    decltype(&ncclSend) Send = nullptr;
+    decltype(&ncclRecv) Recv = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+static NcclApi g_nccl;
+
+#ifndef PP_NCCL_LIB
+#define PP_NCCL_LIB "libnccl.so.2"
+#endif
+
+static bool nccl_load() {
+    if (g_nccl.lib) return true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // torch's copy, if loaded
+    if (!h) h = dlopen(PP_NCCL_LIB, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        set_error(std::string("cannot load NCCL: ") + dlerror());
+        return false;
+    }
+#define PP_SYM(field, name)                                              \
+    g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name)); \
+    if (!g_nccl.field) {                                                 \
+        set_error(std::string("NCCL symbol missing: ") + name);          \
+        return false;                                                    \
+    }
+    PP_SYM(GetUniqueId, "ncclGetUniqueId")
+    PP_SYM(CommInitRank, "ncclCommInitRank")
+    PP_SYM(CommDestroy, "ncclCommDestroy")
+    PP_SYM(AllGather, "ncclAllGather")
+    PP_SYM(Send, "ncclSend")
+    PP_SYM(Recv, "ncclRecv")
+    PP_SYM(GroupStart, "ncclGroupStart")
+    PP_SYM(GroupEnd, "ncclGroupEnd")
+    PP_SYM(GetErrorString, "ncclGetErrorString")
+#undef PP_SYM
+    g_nccl.lib = h;
+    return true;
+}
+
+static pp_status nccl_fail(ncclResult_t r, const char* what) {
+    set_error(std::string(what) + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error"));
+    return PP_E_NCCL;
+}
+
+struct DistState {
+    ncclComm_t comm = nullptr;
+    int nranks = 0, rank = 0, device = 0;
+    void* staging = nullptr;
+    size_t staging_bytes = 0;
+    uint64_t* d_info = nullptr;  // [P][4] gathered (n, t, pivot, key_bytes)
+    uint64_t staging_cap_bytes = 256ull << 20;
+};
+static DistState g_dist;
+
+pp_status dist_unique_id(void* out128) {
+    if (!out128) return PP_E_INVAL;
+    if (!nccl_load()) return PP_E_NCCL;
+    ncclUniqueId id;
+    ncclResult_t r = g_nccl.GetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(out128, &id, 128);
+    return PP_OK;
+}
+
+pp_status dist_init(const void* id128, int nranks, int rank, int device) {
+    if (!id128 || nranks < 1 || rank < 0 || rank >= nranks) {
+        set_error("pp_dist_init: bad arguments");
+        return PP_E_INVAL;
+    }
+    if (!nccl_load()) return PP_E_NCCL;
+    if (g_dist.comm) {
+        set_error("pp_dist_init: already initialised (call pp_dist_finalize first)");
+        return PP_E_INVAL;
+    }
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    ncclUniqueId id;
+    memcpy(&id, id128, 128);
+    ncclResult_t r = g_nccl.CommInitRank(&g_dist.comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        g_dist.comm = nullptr;
+        return nccl_fail(r, "ncclCommInitRank");
+    }
+    g_dist.nranks = nranks;
+    g_dist.rank = rank;
+    g_dist.device = device;
+    e = cudaMalloc(&g_dist.d_info, sizeof(uint64_t) * 4 * (nranks + 1));
+    if (e != cudaSuccess) return cuda_fail(e, "dist info alloc");
+    return PP_OK;
+}
+
+pp_status dist_finalize() {
+    if (g_dist.comm) g_nccl.CommDestroy(g_dist.comm);
+    g_dist.comm = nullptr;
+    if (g_dist.staging) cudaFree(g_dist.staging);
+    if (g_dist.d_info) cudaFree(g_dist.d_info);
+    g_dist.staging = nullptr;
+    g_dist.d_info = nullptr;
+    g_dist.staging_bytes = 0;
+    return PP_OK;
+}
+
+void dist_set_staging(uint64_t bytes) { g_dist.staging_cap_bytes = bytes < 16 ? 16 : bytes; }
+
+template <typename K>
+pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, uint64_t* global_split) {
+    if (!g_dist.comm) {
+        set_error("pp_partition_dist: call pp_dist_init first");
+        return PP_E_INVAL;
+    }
+    const int P = g_dist.nranks, me = g_dist.rank;
+    // 1. local partition (library kernels), split left in device memory
+    uint64_t* d_mine = g_dist.d_info + 4 * P;
+    pp_status s = PP_OK;
+    if (n_local > 0) {
+        s = partition_device<K>(shard, n_local, pivot, st, d_mine + 1, nullptr);
+    } else {
+        cudaMemsetAsync(d_mine + 1, 0, 8, st);
+    }
+    if (s != PP_OK) return s;
+    uint64_t info[3] = {n_local, (uint64_t)pivot, (uint64_t)sizeof(K)};
+    cudaError_t e = cudaMemcpyAsync(d_mine, &info[0], 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_mine + 2, &info[1], 16, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "dist info H2D");
+    // 2. allgather (n_r, t_r, pivot, key bytes)
+    ncclResult_t r = g_nccl.AllGather(d_mine, g_dist.d_info, 4, ncclUint64, g_dist.comm, st);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+    std::vector<uint64_t> all(4 * P);
+    e = cudaMemcpyAsync(all.data(), g_dist.d_info, 8 * 4 * P, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "dist gather");
+    std::vector<uint64_t> ns(P), ts(P);
+    for (int q = 0; q < P; ++q) {
+        ns[q] = all[4 * q];
+        ts[q] = all[4 * q + 1];
+        if (all[4 * q + 2] != (uint64_t)pivot || all[4 * q + 3] != sizeof(K)) {
+            set_error("pp_partition_dist: ranks passed different pivots or key types");
+            return PP_E_INVAL;
+        }
+    }
+    // 3. the same plan on every rank
+    const uint64_t cap = std::max<uint64_t>(1, g_dist.staging_cap_bytes / sizeof(K));
+    std::vector<Piece> pcs;
+    const uint64_t K_global = plan_pieces(ns.data(), ts.data(), P, cap, pcs);
+    uint64_t base = 0;
+    for (int q = 0; q < me; ++q) base += ns[q];
+    // staging: the most this rank receives in one round
+    uint64_t need = 0, cur = 0, rnd = ~0ull;
+    for (const Piece& p : pcs) {
+        if (p.round != rnd) {
+            rnd = p.round;
+            cur = 0;
+        }
+        if ((int)p.rank_f == me || (int)p.rank_t == me) cur += p.len;
+        need = std::max(need, cur);
+    }
+    if (need * sizeof(K) > g_dist.staging_bytes) {
+        if (g_dist.staging) cudaFree(g_dist.staging);
+        g_dist.staging = nullptr;
+        g_dist.staging_bytes = 0;
+        e = cudaMalloc(&g_dist.staging, need * sizeof(K));
+        if (e != cudaSuccess) return cuda_fail(e, "dist staging alloc");
+        g_dist.staging_bytes = need * sizeof(K);
+    }
+    K* staging = static_cast<K*>(g_dist.staging);
+    const ncclDataType_t dt = sizeof(K) == 8 ? ncclUint64 : ncclUint32;
+    // 4. rounds: send my range, receive the partner's into staging, copy back
+    size_t i = 0;
+    while (i < pcs.size()) {
+        const uint64_t round = pcs[i].round;
+        size_t j = i;
+        while (j < pcs.size() && pcs[j].round == round) ++j;
+        std::vector<uint64_t> offs, soffs, lens;
+        uint64_t soff = 0;
+        r = g_nccl.GroupStart();
+        if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+        for (size_t k = i; k < j; ++k) {
+            const Piece& p = pcs[k];
+            int peer = -1;
+            uint64_t off = 0;
+            if ((int)p.rank_f == me) {
+                peer = (int)p.rank_t;
+                off = p.f - base;
+            } else if ((int)p.rank_t == me) {
+                peer = (int)p.rank_f;
+                off = p.t - base;
+            }
+            if (peer < 0) continue;
+            r = g_nccl.Send(shard + off, p.len, dt, peer, g_dist.comm, st);
+            if (r == ncclSuccess) r = g_nccl.Recv(staging + soff, p.len, dt, peer, g_dist.comm, st);
+            if (r != ncclSuccess) {
+                g_nccl.GroupEnd();
+                return nccl_fail(r, "ncclSend/Recv");
+            }
+            offs.push_back(off);
+            soffs.push_back(soff);
+            lens.push_back(p.len);
+            soff += p.len;
+        }
+        r = g_nccl.GroupEnd();
+        if (r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
+        for (size_t k = 0; k < offs.size(); ++k) {
+            e = cudaMemcpyAsync(shard + offs[k], staging + soffs[k], lens[k] * sizeof(K), cudaMemcpyDeviceToDevice,
+                                st);
+            if (e != cudaSuccess) return cuda_fail(e, "dist place");
+        }
+        i = j;
+    }
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "dist exchange");
+    if (global_split) *global_split = K_global;
+    return PP_OK;
+}
+
+template pp_status partition_dist<uint64_t>(uint64_t*, uint64_t, uint64_t, cudaStream_t, uint64_t*);
+template pp_status partition_dist<uint32_t>(uint32_t*, uint64_t, uint32_t, cudaStream_t, uint64_t*);
+
+pp_status dist_plan(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap, uint64_t* out, uint64_t out_cap,
+                    uint64_t* n_out, uint64_t* K_out) {
+    if (!ns || !ts || P < 1 || cap < 1 || !n_out) return PP_E_INVAL;
+    for (int r = 0; r < P; ++r)
+        if (ts[r] > ns[r]) return PP_E_INVAL;
+    std::vector<Piece> pcs;
+    const uint64_t K = plan_pieces(ns, ts, P, cap, pcs);
+    *n_out = pcs.size();
+    if (K_out) *K_out = K;
+    if (out) {
+        for (size_t k = 0; k < pcs.size() && k < out_cap; ++k) {
+            const Piece& p = pcs[k];
+            uint64_t* o = out + 6 * k;
+            o[0] = p.round;
+            o[1] = p.rank_f;
+            o[2] = p.f;
+            o[3] = p.rank_t;
+            o[4] = p.t;
+            o[5] = p.len;
+        }
+    }
+    return pcs.size() <= out_cap || !out ? PP_OK : PP_E_INVAL;
+}
+
+}  // namespace pp

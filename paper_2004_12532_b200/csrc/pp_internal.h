@@ -76,4 +76,14 @@ pp_status ss_groups_device(K* keys, uint64_t n, K pivot, uint64_t g, cudaStream_
 template <typename K>
 pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st);
 
+// multi-GPU (pp_dist.cu)
+pp_status dist_unique_id(void* out128);
+pp_status dist_init(const void* id128, int nranks, int rank, int device);
+pp_status dist_finalize();
+void dist_set_staging(uint64_t bytes);
+template <typename K>
+pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, uint64_t* global_split);
+pp_status dist_plan(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap, uint64_t* out, uint64_t out_cap,
+                    uint64_t* n_out, uint64_t* K_out);
+
 }  // namespace pp

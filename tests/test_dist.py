@@ -89,6 +89,24 @@ def test_schedule_rounds_cover_and_cap(cap):
             assert all(0 <= off and off + m <= ns[rank] for _, off, m in ops)
 
 
+def test_c_plan_matches_python_plan():
+    """The C-ABI exchange plan (pp_dist_plan, C++) and the Python plan +
+    round schedule (two independent implementations) agree piece by piece."""
+    import paper_2004_12532_b200 as pp
+    rng = np.random.default_rng(99)
+    for trial in range(200):
+        P = int(rng.integers(1, 12))
+        ns = [int(x) for x in rng.integers(0, 300, size=P)]
+        ts = [int(rng.integers(0, n + 1)) for n in ns]
+        cap = int(rng.choice([1, 5, 17, 64, 1000]))
+        K, plan = exchange_plan(ns, ts)
+        rounds = schedule_rounds(plan, P, cap)
+        py = [(ri, t.rank_f, t.f, t.rank_t, t.t, t.length) for ri, r in enumerate(rounds) for t in r]
+        Kc, rows = pp.pp_dist_plan(ns, ts, cap)
+        assert Kc == K
+        assert rows == py
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))

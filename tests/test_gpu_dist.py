@@ -1,0 +1,44 @@
+"""GPU: the C-ABI multi-GPU partition (pp_dist_*) on a single-rank NCCL
+communicator (only one GPU is available to the tests; the exchange logic
+with several ranks is covered on CPU by tests/test_dist.py)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pp():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2004_12532_b200 as m
+    m.load()
+    m.reset_params()
+    uid = m.pp_dist_unique_id()
+    m.pp_dist_init(uid, 1, 0, torch.cuda.current_device())
+    yield m
+    m.pp_dist_finalize()
+
+
+def test_dist_single_rank(pp):
+    from gpu_util import to_dev
+    for dt, n, p in ((np.uint64, 1 << 20, 1 << 63), (np.uint64, 3_000_017, 1 << 61),
+                     (np.uint32, 2_000_003, 1 << 31), (np.uint64, 0, 5)):
+        a = (synth.uniform_u64_np(n, 77) if dt == np.uint64 else synth.uniform_u32_np(n, 77))
+        t = to_dev(a) if n else torch.empty(0, dtype=torch.int64, device="cuda")
+        K = pp.pp_partition_dist(t, p)
+        out = t.cpu().numpy().view(dt)
+        oracle.check_partition(a, out, p, K)
+
+
+def test_dist_finalize_and_reinit(pp):
+    pp.pp_dist_finalize()
+    uid = pp.pp_dist_unique_id()
+    pp.pp_dist_init(uid, 1, 0, torch.cuda.current_device())
+    with pytest.raises(pp.PPError):
+        pp.pp_dist_init(uid, 1, 0, torch.cuda.current_device())  # already initialised
