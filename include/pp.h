@@ -118,6 +118,15 @@ pp_status pp_partition_dist_u64(uint64_t *shard, uint64_t n_local, uint64_t pivo
 pp_status pp_partition_dist_u32(uint32_t *shard, uint64_t n_local, uint32_t pivot, void *stream,
                                 uint64_t *global_split_out);
 pp_status pp_dist_set_staging(uint64_t bytes);
+/* pp_quicksort_dist_u64/u32: sorts the GLOBAL array (shards in rank order)
+ * ascending, unsigned, in place (collective).  Segments spanning ranks are
+ * split by pp_partition_dist_* with a median-of-3 pivot gathered from the
+ * owning ranks (the "x <= p" step when the pivot is the minimum); spanning
+ * segments of <= 2^16 keys are all-gathered and sorted on every participating
+ * rank; finally each rank sorts its shard with pp_quicksort_*.  Shard sizes
+ * may differ.  Synchronises `stream`. */
+pp_status pp_quicksort_dist_u64(uint64_t *shard, uint64_t n_local, void *stream);
+pp_status pp_quicksort_dist_u32(uint32_t *shard, uint64_t n_local, void *stream);
 pp_status pp_dist_plan(const uint64_t *ns, const uint64_t *ts, int nranks, uint64_t cap, uint64_t *out,
                        uint64_t out_cap, uint64_t *n_out, uint64_t *K_out);
 pp_status pp_dist_finalize(void);

@@ -94,6 +94,8 @@ def load(build_if_missing: bool = True):
         "pp_partition_dist_u64": ([vp, u64, u64, vp, P64], st),
         "pp_partition_dist_u32": ([vp, u64, u32, vp, P64], st),
         "pp_dist_set_staging": ([u64], st),
+        "pp_quicksort_dist_u64": ([vp, u64, vp], st),
+        "pp_quicksort_dist_u32": ([vp, u64, vp], st),
         "pp_dist_plan": ([P64, P64, ctypes.c_int, u64, P64, u64, P64, P64], st),
         "pp_dist_finalize": ([], st),
     }
@@ -281,6 +283,13 @@ def pp_partition_dist(shard, pivot: int, stream=None) -> int:
     _check(f(shard.data_ptr(), shard.numel(), _pivot(pivot, kind), _stream_ptr(stream), ctypes.byref(out)),
            "pp_partition_dist")
     return int(out.value)
+
+
+def pp_quicksort_dist(shard, stream=None) -> None:
+    """Global sort of a sharded array (collective; see include/pp.h)."""
+    kind = _key_kind(shard)
+    f = load().pp_quicksort_dist_u64 if kind == "u64" else load().pp_quicksort_dist_u32
+    _check(f(shard.data_ptr(), shard.numel(), _stream_ptr(stream)), "pp_quicksort_dist")
 
 
 def pp_dist_set_staging(nbytes: int) -> None:

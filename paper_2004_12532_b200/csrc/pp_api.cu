@@ -332,6 +332,18 @@ pp_status pp_partition_dist_u32(uint32_t* shard, uint64_t n_local, uint32_t pivo
     if (s != PP_OK) return s;
     return partition_dist<uint32_t>(shard, n_local, pivot, (cudaStream_t)stream, global_split_out);
 }
+pp_status pp_quicksort_dist_u64(uint64_t* shard, uint64_t n_local, void* stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    pp_status s = check_device_keys(shard, n_local);
+    if (s != PP_OK) return s;
+    return quicksort_dist<uint64_t>(shard, n_local, (cudaStream_t)stream, 1u << 16);
+}
+pp_status pp_quicksort_dist_u32(uint32_t* shard, uint64_t n_local, void* stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    pp_status s = check_device_keys(shard, n_local);
+    if (s != PP_OK) return s;
+    return quicksort_dist<uint32_t>(shard, n_local, (cudaStream_t)stream, 1u << 16);
+}
 pp_status pp_dist_plan(const uint64_t* ns, const uint64_t* ts, int nranks, uint64_t cap, uint64_t* out,
                        uint64_t out_cap, uint64_t* n_out, uint64_t* K_out) {
     return dist_plan(ns, ts, nranks, cap, out, out_cap, n_out, K_out);

@@ -302,6 +302,164 @@ pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, u
 template pp_status partition_dist<uint64_t>(uint64_t*, uint64_t, uint64_t, cudaStream_t, uint64_t*);
 template pp_status partition_dist<uint32_t>(uint32_t*, uint64_t, uint32_t, cudaStream_t, uint64_t*);
 
+// ---------------------------------------------------------------------------
+// Distributed quicksort (BASELINE config 5 at P GPUs): segments spanning
+// several ranks are split by partition_dist (median-of-3 pivot gathered from
+// the owning ranks; "x <= p" step when the pivot is the minimum -- DESIGN.md
+// R14); spanning segments of <= `small` keys are all-gathered, sorted on
+// every participating rank, and each keeps its part.  When no segment spans
+// two ranks each shard is a concatenation of whole segments in key order:
+// one local quicksort per rank finishes.  Mirrors Partitioner.sort in
+// paper_2004_12532_b200/dist.py (tested there over gloo with P = 2..4).
+// ---------------------------------------------------------------------------
+static pp_status allgather_u64(const uint64_t* host_in, uint64_t count, std::vector<uint64_t>& host_out,
+                               cudaStream_t st) {
+    const int P = g_dist.nranks;
+    uint64_t* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 8 * count * (P + 1));
+    if (e != cudaSuccess) return cuda_fail(e, "allgather buffer");
+    e = cudaMemcpyAsync(d + count * P, host_in, 8 * count, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return cuda_fail(e, "allgather H2D");
+    }
+    ncclResult_t r = g_nccl.AllGather(d + count * P, d, count, ncclUint64, g_dist.comm, st);
+    if (r != ncclSuccess) {
+        cudaFree(d);
+        return nccl_fail(r, "ncclAllGather");
+    }
+    host_out.assign(count * P, 0);
+    e = cudaMemcpyAsync(host_out.data(), d, 8 * count * P, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d);
+    return e == cudaSuccess ? PP_OK : cuda_fail(e, "allgather D2H");
+}
+
+template <typename K>
+pp_status quicksort_dist(K* shard, uint64_t n_local, cudaStream_t st, uint64_t small) {
+    if (!g_dist.comm) {
+        set_error("pp_quicksort_dist: call pp_dist_init first");
+        return PP_E_INVAL;
+    }
+    const int P = g_dist.nranks, me = g_dist.rank;
+    const uint64_t KMAXU = (uint64_t)(K)~(K)0;
+    std::vector<uint64_t> all;
+    pp_status s = allgather_u64(&n_local, 1, all, st);
+    if (s != PP_OK) return s;
+    std::vector<uint64_t> ns(all), base(P, 0);
+    for (int r = 1; r < P; ++r) base[r] = base[r - 1] + ns[r - 1];
+    const uint64_t N = base[P - 1] + ns[P - 1], b0 = base[me];
+    auto owner = [&](uint64_t x) {
+        int r = 0;
+        while (r + 1 < P && base[r + 1] <= x) ++r;
+        return r;
+    };
+    auto piece = [&](uint64_t lo, uint64_t hi, uint64_t& pa, uint64_t& pb) {
+        const uint64_t a = std::max(lo, b0), b = std::min(hi, b0 + ns[me]);
+        if (a < b) { pa = a - b0; pb = b - b0; } else { pa = pb = 0; }
+    };
+    struct Seg {
+        uint64_t lo, hi;
+    };
+    std::vector<Seg> segs;
+    if (N > 1) segs.push_back({0, N});
+    cudaError_t e;
+    for (;;) {
+        std::vector<Seg> span, nxt;
+        for (const Seg& sg : segs)
+            if (sg.hi - sg.lo > 1 && owner(sg.lo) != owner(sg.hi - 1)) span.push_back(sg);
+        if (span.empty()) break;
+        for (const Seg& sg : span) {
+            const uint64_t lo = sg.lo, hi = sg.hi;
+            uint64_t pa, pb;
+            piece(lo, hi, pa, pb);
+            if (hi - lo <= small) {
+                // all-gather the segment, sort it everywhere, keep my part
+                std::vector<uint64_t> lens(P);
+                uint64_t mx = 0, off = 0;
+                for (int r = 0; r < P; ++r) {
+                    const uint64_t a = std::max(lo, base[r]), b = std::min(hi, base[r] + ns[r]);
+                    lens[r] = a < b ? b - a : 0;
+                    mx = std::max(mx, lens[r]);
+                    if (r < me) off += lens[r];
+                }
+                K* d = nullptr;
+                e = cudaMalloc(&d, sizeof(K) * (mx * (P + 1) + (hi - lo)));
+                if (e != cudaSuccess) return cuda_fail(e, "gather-sort buffer");
+                K* mine = d + mx * P;
+                K* full = mine + mx;
+                if (pb > pa) e = cudaMemcpyAsync(mine, shard + pa, sizeof(K) * (pb - pa), cudaMemcpyDeviceToDevice, st);
+                ncclResult_t r = g_nccl.AllGather(mine, d, mx, sizeof(K) == 8 ? ncclUint64 : ncclUint32, g_dist.comm,
+                                                  st);
+                if (r != ncclSuccess) {
+                    cudaFree(d);
+                    return nccl_fail(r, "ncclAllGather");
+                }
+                uint64_t at = 0;
+                for (int q = 0; q < P; ++q) {
+                    if (lens[q]) cudaMemcpyAsync(full + at, d + mx * q, sizeof(K) * lens[q], cudaMemcpyDeviceToDevice, st);
+                    at += lens[q];
+                }
+                s = quicksort_device<K>(full, hi - lo, st);
+                if (s == PP_OK && pb > pa)
+                    e = cudaMemcpyAsync(shard + pa, full + off, sizeof(K) * (pb - pa), cudaMemcpyDeviceToDevice, st);
+                if (s == PP_OK) e = cudaStreamSynchronize(st);
+                cudaFree(d);
+                if (s != PP_OK) return s;
+                if (e != cudaSuccess) return cuda_fail(e, "gather-sort");
+                continue;
+            }
+            // median of 3 from the owning ranks
+            const uint64_t pos[3] = {lo, lo + (hi - lo - 1) / 2, hi - 1};
+            uint64_t mv[6] = {0, 0, 0, 0, 0, 0};
+            for (int i = 0; i < 3; ++i) {
+                if (pos[i] >= b0 && pos[i] < b0 + ns[me]) {
+                    K v;
+                    e = cudaMemcpy(&v, shard + (pos[i] - b0), sizeof(K), cudaMemcpyDeviceToHost);
+                    if (e != cudaSuccess) return cuda_fail(e, "pivot read");
+                    mv[2 * i] = 1;
+                    mv[2 * i + 1] = (uint64_t)v;
+                }
+            }
+            s = allgather_u64(mv, 6, all, st);
+            if (s != PP_OK) return s;
+            uint64_t v3[3] = {0, 0, 0};
+            for (int i = 0; i < 3; ++i)
+                for (int q = 0; q < P; ++q)
+                    if (all[6 * q + 2 * i]) {
+                        v3[i] = all[6 * q + 2 * i + 1];
+                        break;
+                    }
+            std::sort(v3, v3 + 3);
+            const uint64_t p = v3[1];
+            uint64_t k = 0;
+            s = partition_dist<K>(shard + pa, pb - pa, (K)p, st, &k);
+            if (s != PP_OK) return s;
+            if (k == 0) {
+                if (p == KMAXU) continue;  // all keys equal the maximum
+                s = partition_dist<K>(shard + pa, pb - pa, (K)(p + 1), st, &k);
+                if (s != PP_OK) return s;
+                nxt.push_back({lo + k, hi});  // [lo, lo+k) all equal p
+            } else {
+                nxt.push_back({lo, lo + k});
+                nxt.push_back({lo + k, hi});
+            }
+        }
+        segs.clear();
+        for (const Seg& sg : nxt)
+            if (sg.hi - sg.lo > 1) segs.push_back(sg);
+    }
+    if (n_local > 1) {
+        s = quicksort_device<K>(shard, n_local, st);
+        if (s != PP_OK) return s;
+    }
+    e = cudaStreamSynchronize(st);
+    return e == cudaSuccess ? PP_OK : cuda_fail(e, "quicksort_dist");
+}
+
+template pp_status quicksort_dist<uint64_t>(uint64_t*, uint64_t, cudaStream_t, uint64_t);
+template pp_status quicksort_dist<uint32_t>(uint32_t*, uint64_t, cudaStream_t, uint64_t);
+
 pp_status dist_plan(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap, uint64_t* out, uint64_t out_cap,
                     uint64_t* n_out, uint64_t* K_out) {
     if (!ns || !ts || P < 1 || cap < 1 || !n_out) return PP_E_INVAL;

@@ -85,5 +85,7 @@ template <typename K>
 pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, uint64_t* global_split);
 pp_status dist_plan(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap, uint64_t* out, uint64_t out_cap,
                     uint64_t* n_out, uint64_t* K_out);
+template <typename K>
+pp_status quicksort_dist(K* shard, uint64_t n_local, cudaStream_t st, uint64_t small);
 
 }  // namespace pp

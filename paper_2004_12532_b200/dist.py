@@ -179,3 +179,104 @@ class Partitioner:
                 req.wait()
             for off, so, m in placed:
                 shard[off:off + m].copy_(staging[so:so + m])
+
+    # ------------------------------------------------------------------
+    # Distributed quicksort (BASELINE config 5 at P GPUs).
+    # ------------------------------------------------------------------
+    def sort(self, shard, local_sort: Optional[Callable] = None, small: int = 1 << 16) -> None:
+        """Sort the global array (shards in rank order) ascending, unsigned.
+
+        Segments spanning several ranks are split by the distributed
+        partition (median-of-3 pivot from the three owning ranks, the x <= p
+        progress step when the pivot is the minimum -- DESIGN.md reading
+        R14); spanning segments of <= `small` keys are gathered to every
+        participating rank, sorted there and each rank keeps its part.  Once
+        no segment spans two ranks, every shard is a concatenation of whole
+        segments in key order, so one local sort per rank finishes the job."""
+        torch, dist = self.torch, self.dist
+        if local_sort is None:
+            from . import pp_quicksort
+            local_sort = pp_quicksort
+        bits = 64 if shard.element_size() == 8 else 32
+        umask = (1 << bits) - 1
+        n_me = torch.tensor([shard.numel()], dtype=torch.int64, device=self.device)
+        alln = [torch.empty_like(n_me) for _ in range(self.world)]
+        dist.all_gather(alln, n_me, group=self.group)
+        ns = [int(v.item()) for v in alln]
+        base = [0] * self.world
+        for r in range(1, self.world):
+            base[r] = base[r - 1] + ns[r - 1]
+        N = sum(ns)
+        me, b0 = self.rank, base[self.rank]
+
+        def owner(x):
+            r = 0
+            while r + 1 < self.world and base[r + 1] <= x:
+                r += 1
+            return r
+
+        def spans(lo, hi):
+            return owner(lo) != owner(hi - 1)
+
+        def piece(lo, hi):  # my local slice of global [lo, hi)
+            a, b = max(lo, b0), min(hi, b0 + ns[me])
+            return (a - b0, b - b0) if a < b else (0, 0)
+
+        def values_at(positions):
+            """Unsigned key values at global positions (allgather; each rank
+            fills the positions it owns)."""
+            mine = torch.zeros(2 * len(positions), dtype=torch.int64, device=self.device)
+            for i, x in enumerate(positions):
+                if b0 <= x < b0 + ns[me]:
+                    mine[2 * i] = 1
+                    mine[2 * i + 1] = shard[x - b0].to(torch.int64)
+            allv = [torch.empty_like(mine) for _ in range(self.world)]
+            dist.all_gather(allv, mine, group=self.group)
+            out = []
+            for i in range(len(positions)):
+                for v in allv:
+                    if int(v[2 * i]) == 1:
+                        out.append(int(v[2 * i + 1]) & umask)
+                        break
+            return out
+
+        segs = [(0, N)] if N > 1 else []
+        while True:
+            span = [s for s in segs if s[1] - s[0] > 1 and spans(*s)]
+            if not span:
+                break
+            nxt = []
+            for lo, hi in span:
+                if hi - lo <= small:
+                    self._gather_sort(shard, lo, hi, piece, ns, base, local_sort)
+                    continue
+                a, b, c = values_at([lo, lo + (hi - lo - 1) // 2, hi - 1])
+                p = sorted([a, b, c])[1]
+                pa, pb = piece(lo, hi)
+                k = self.partition(shard[pa:pb], p)
+                if k == 0:  # p is the segment minimum: split by x <= p
+                    if p == umask:
+                        continue  # all keys equal the maximum
+                    k = self.partition(shard[pa:pb], p + 1)
+                    nxt.append((lo + k, hi))  # [lo, lo+k) all equal p
+                else:
+                    nxt += [(lo, lo + k), (lo + k, hi)]
+            segs = [s for s in nxt if s[1] - s[0] > 1]
+        if shard.numel() > 1:
+            local_sort(shard)
+
+    def _gather_sort(self, shard, lo, hi, piece, ns, base, local_sort):
+        """All ranks gather the (small) spanning segment, sort it, and each
+        keeps its own part."""
+        torch, dist = self.torch, self.dist
+        lens = [max(0, min(hi, base[r] + ns[r]) - max(lo, base[r])) for r in range(self.world)]
+        mx = max(lens)
+        pa, pb = piece(lo, hi)
+        buf = torch.zeros(mx, dtype=shard.dtype, device=shard.device)
+        buf[: pb - pa] = shard[pa:pb]
+        allv = [torch.empty_like(buf) for _ in range(self.world)]
+        dist.all_gather(allv, buf, group=self.group)
+        full = torch.cat([v[:l] for v, l in zip(allv, lens)])
+        local_sort(full)
+        off = sum(lens[: self.rank])
+        shard[pa:pb] = full[off:off + (pb - pa)]

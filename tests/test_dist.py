@@ -143,6 +143,69 @@ def _worker(rank, world, port, n_per, seed, pivot, staging, result_q):
         dist.destroy_process_group()
 
 
+def _sort_worker(rank, world, port, ns, seed, kind, small, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        off = sum(ns[:rank])
+        if kind == "uniform":
+            host = synth.uniform_u64_np(ns[rank], seed, offset=off)
+        elif kind == "dup":
+            host = synth.mod_range_u64_np(ns[rank], seed, 7, offset=off)
+        else:  # all equal, maximum key
+            host = np.full(ns[rank], (1 << 64) - 1, dtype=np.uint64)
+        shard = torch.from_numpy(host.view(np.int64).copy())
+
+        def local_part(t, p):
+            return oracle.partition_two_pointer(t.numpy().view(np.uint64), p)
+
+        def local_sort(t):
+            a = t.numpy().view(np.uint64)
+            oracle.quicksort(a)
+
+        part = Partitioner(device="cpu", staging_bytes=8 * 512, local_partition=local_part)
+        part.sort(shard, local_sort=local_sort, small=small)
+        mx = max(ns)
+        padded = torch.zeros(mx, dtype=torch.int64)
+        padded[: ns[rank]] = shard
+        gathered = [torch.empty(mx, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(gathered, padded)
+        if rank == 0:
+            full = torch.cat([g[: ns[r]] for r, g in enumerate(gathered)])
+            result_q.put(full.numpy().view(np.uint64).copy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind,small", [(2, "uniform", 64), (3, "dup", 100), (4, "uniform", 4096),
+                                              (3, "maxeq", 50)])
+def test_distributed_sort_gloo(world, kind, small):
+    """Distributed quicksort over gloo (oracle local ops): the concatenated
+    shards equal the oracle's sort of the global array."""
+    ns = [3000 + 211 * r for r in range(world)]
+    seed = 0xC0FFEE05
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sort_worker, args=(r, world, port, ns, seed, kind, small, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if kind == "uniform":
+        glob = synth.uniform_u64_np(sum(ns), seed)
+    elif kind == "dup":
+        glob = synth.mod_range_u64_np(sum(ns), seed, 7)
+    else:
+        glob = np.full(sum(ns), (1 << 64) - 1, dtype=np.uint64)
+    ref = glob.copy()
+    oracle.quicksort(ref)
+    assert np.array_equal(out, ref)
+
+
 @pytest.mark.parametrize("world,staging", [(2, 1 << 20), (3, 4096), (4, 8 * 1000)])
 def test_partitioner_gloo(world, staging):
     n_per, seed = 20000, 0xC0FFEE03

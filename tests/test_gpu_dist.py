@@ -36,6 +36,18 @@ def test_dist_single_rank(pp):
         oracle.check_partition(a, out, p, K)
 
 
+def test_quicksort_dist_single_rank(pp):
+    from gpu_util import to_dev
+    rng = np.random.default_rng(3)
+    for a in (synth.uniform_u64_np(1_000_003, 5), rng.integers(0, 9, size=200_001).astype(np.uint64),
+              synth.uniform_u32_np(300_007, 6)):
+        t = to_dev(a)
+        pp.pp_quicksort_dist(t)
+        ref = a.copy()
+        oracle.quicksort(ref)
+        assert np.array_equal(t.cpu().numpy().view(a.dtype), ref)
+
+
 def test_dist_finalize_and_reinit(pp):
     pp.pp_dist_finalize()
     uid = pp.pp_dist_unique_id()
