@@ -330,7 +330,7 @@ def pp_timing_read() -> dict:
 
 DEFAULT_PARAMS = {"g": 0, "min_lines_per_group": 16, "small_n": 1 << 15, "path": 0, "tile": 0, "ranks": 0, "variant": 0,
                   "leaf": 0, "qs_cta_max": 0, "leaf_algo": 0, "qs_waves": 2, "fused": 0,
-                  "fused_stop": 0, "qs_small": 1 << 16}
+                  "fused_stop": 0, "qs_small": 1 << 16, "qs_small_cfg": 1}
 
 
 def reset_params() -> None:

@@ -399,6 +399,7 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "leaf_algo") P.leaf_algo = value;
     else if (k == "fused") P.fused = value;
     else if (k == "qs_small") P.qs_small = value;
+    else if (k == "qs_small_cfg") P.qs_small_cfg = value;
     else if (k == "fused_stop") P.fused_stop = value;
     else if (k == "qs_waves") P.qs_waves = value;
     else {
@@ -425,6 +426,7 @@ int64_t pp_get_param(const char* name) {
     if (k == "leaf_algo") return P.leaf_algo;
     if (k == "fused") return P.fused;
     if (k == "qs_small") return P.qs_small;
+    if (k == "qs_small_cfg") return P.qs_small_cfg;
     if (k == "fused_stop") return P.fused_stop;
     if (k == "qs_waves") return P.qs_waves;
     return INT64_MIN;

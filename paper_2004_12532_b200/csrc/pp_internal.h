@@ -50,6 +50,7 @@ struct Params {
     int64_t fused_stop = 0;        // debug/profiling: stop the fused kernel after this phase
     int64_t qs_waves = 2;          // quicksort mid levels: target CTA waves of the group launch
     int64_t qs_small = 1 << 16;    // quicksort: segments <= this finish in one CTA (0 = off)
+    int64_t qs_small_cfg = 1;      // quicksort: per-CTA recursion config (pp_quicksort.cu SmallCfg)
 };
 Params& params();
 

@@ -276,12 +276,26 @@ __global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
 // shared memory by merging.  This removes the deepest, least efficient
 // levels of the breadth-first loop (many tiny CTAs, one launch + sync each).
 // ===========================================================================
+// V = 0: 256 threads, 8 KiB lines, 4 KiB... 64 KiB sort buffers (2 CTAs/SM);
+// V = 1: lean -- 128 threads, 4 KiB lines with 2 in flight per end, 32 KiB
+// sort buffers: ~37 KiB of shared memory, 4 CTAs per SM (more independent
+// recursions per SM to hide the latency-bound merge rounds).
+template <typename K, int V>
+struct SmallCfg;
 template <typename K>
-struct SmallCfg {
-    static constexpr int NT = 256;
+struct SmallCfg<K, 0> {
+    static constexpr int NT = 256, MINB = 2;
     using GC = GroupCfgT<K, 8192, 256, 4, false>;
     static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 4096 : 8192;  // 2 x LEAFC keys <= 64 KiB
     static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);  // two padded buffers
+    static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
+};
+template <typename K>
+struct SmallCfg<K, 1> {
+    static constexpr int NT = 128, MINB = 4;
+    using GC = GroupCfgT<K, 4096, 128, 2, false>;
+    static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 2048 : 4096;
+    static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);
     static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
 };
 
@@ -317,10 +331,10 @@ __device__ void cta_merge_sort(K* __restrict__ g, uint32_t len, K* A, K* B) {
 }
 
 // In-place partition of seg[0, len) by key < pivot with one CTA; returns K.
-template <typename K>
+template <typename K, int V>
 __device__ uint64_t cta_partition(K* __restrict__ seg, uint64_t len, K pivot, uint64_t seed, unsigned char* smem,
                                   GroupOut* scratch, Ctl* sc, uint64_t* red) {
-    using S = SmallCfg<K>;
+    using S = SmallCfg<K, V>;
     using GC = typename S::GC;
     constexpr int NT = S::NT, NW = NT / 32;
     const uint64_t addr = (uint64_t)(uintptr_t)seg;
@@ -371,12 +385,11 @@ __device__ uint64_t cta_partition(K* __restrict__ seg, uint64_t len, K pivot, ui
     return Ks;
 }
 
-template <typename K>
-__global__ void __launch_bounds__(SmallCfg<K>::NT, 2) qs_small_kernel(K* __restrict__ keys,
-                                                                   const uint64_t* __restrict__ seg_lo,
-                                                                   const uint32_t* __restrict__ seg_len,
-                                                                   uint64_t seed, GroupOut* __restrict__ scratch) {
-    using S = SmallCfg<K>;
+template <typename K, int V>
+__global__ void __launch_bounds__(SmallCfg<K, V>::NT, SmallCfg<K, V>::MINB)
+    qs_small_kernel(K* __restrict__ keys, const uint64_t* __restrict__ seg_lo, const uint32_t* __restrict__ seg_len,
+                    uint64_t seed, GroupOut* __restrict__ scratch) {
+    using S = SmallCfg<K, V>;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ Ctl sc;
     __shared__ uint64_t red[S::NT / 32];
@@ -412,7 +425,7 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, 2) qs_small_kernel(K* __restr
         K p;
         if (mode == 0) p = median3<K>(keys[lo], keys[lo + (len - 1) / 2], keys[hi - 1]);
         else p = (K)pm;
-        const uint64_t k = cta_partition<K>(keys + lo, len, p, seed, smem, scratch + blockIdx.x, &sc, red);
+        const uint64_t k = cta_partition<K, V>(keys + lo, len, p, seed, smem, scratch + blockIdx.x, &sc, red);
         if (threadIdx.x == 0) {
             int s = sp;
             if (mode == 0 && k == 0) {
@@ -691,18 +704,25 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     unsigned char* qws = static_cast<unsigned char*>(qs_workspace(loB + lnB + sloB + slnB + scrB + 256));
     if (!qws) return PP_E_NOMEM;
     if (nsmall > 0) {
-        using S = SmallCfg<K>;
         uint64_t* d_slo = reinterpret_cast<uint64_t*>(qws + loB + lnB);
         uint32_t* d_sln = reinterpret_cast<uint32_t*>(qws + loB + lnB + sloB);
         GroupOut* d_scr = reinterpret_cast<GroupOut*>(qws + loB + lnB + sloB + slnB);
         e = cudaMemcpyAsync(d_slo, small_lo.data(), 8 * nsmall, cudaMemcpyHostToDevice, st);
         if (e == cudaSuccess) e = cudaMemcpyAsync(d_sln, small_len.data(), 4 * nsmall, cudaMemcpyHostToDevice, st);
         if (e != cudaSuccess) return cuda_fail(e, "quicksort small H2D");
-        cudaFuncSetAttribute(qs_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
         for (uint64_t b0 = 0; b0 < nsmall; b0 += 65535u * 1024u) {
             const uint64_t cnt = std::min<uint64_t>(nsmall - b0, 65535u * 1024u);
-            qs_small_kernel<K><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(keys, d_slo + b0, d_sln + b0, P.seed,
-                                                                      d_scr + b0);
+            if (P.qs_small_cfg == 0) {
+                using S = SmallCfg<K, 0>;
+                cudaFuncSetAttribute(qs_small_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+                qs_small_kernel<K, 0><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(keys, d_slo + b0, d_sln + b0, P.seed,
+                                                                             d_scr + b0);
+            } else {
+                using S = SmallCfg<K, 1>;
+                cudaFuncSetAttribute(qs_small_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+                qs_small_kernel<K, 1><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(keys, d_slo + b0, d_sln + b0, P.seed,
+                                                                             d_scr + b0);
+            }
             note_launches(1);
         }
         e = cudaGetLastError();
