@@ -147,9 +147,20 @@ pp_status pp_ss_groups_u32(uint32_t *keys, uint64_t n, uint32_t pivot, uint64_t 
 uint64_t pp_max_groups(void);
 
 /* ---- workspace / statistics / tuning --------------------------------------- */
-/* Bytes of device workspace a call on n keys of key_bytes (4 or 8) may use;
- * op 0 = partition, 1 = quicksort. */
+/* Bytes of device workspace a call on n keys of key_bytes (4 or 8) may use,
+ * under the current tuning parameters; op 0 = partition, 1 = quicksort.
+ * o(n): the cleanup arrays are capped, quicksort segment
+ * lists are uploaded in chunks of 2^20 descriptors. */
 uint64_t pp_workspace_bytes(uint64_t n, int key_bytes, int op);
+/* Caller-owned device workspace (e.g. a torch tensor): when set, every
+ * partition / quicksort call uses it instead of the library's internal one,
+ * and fails with PP_E_NOMEM if a step needs more than it holds (a partition
+ * then leaves the array untouched; a quicksort leaves a permutation of the
+ * input).  pp_workspace_bytes(n, key_bytes, op) always suffices.  d_ws must be device memory, 256-byte
+ * aligned; the library never frees it.  d_ws = NULL reverts to the internal
+ * workspace.  Calls sharing one workspace must be stream-ordered.
+ * (Survey §8(b); o(n) aux memory per the "in-place" definition.) */
+pp_status pp_set_workspace(void *d_ws, uint64_t bytes);
 /* Device bytes besides `keys` touched by the last call (aux memory). */
 uint64_t pp_last_aux_bytes(void);
 /* Statistics of the last partition call: out[0..12] = {n, K, W(dirty-set

@@ -81,6 +81,7 @@ def load(build_if_missing: bool = True):
         "pp_max_groups": ([], u64),
         "pp_workspace_bytes": ([u64, ctypes.c_int, ctypes.c_int], u64),
         "pp_last_aux_bytes": ([], u64),
+        "pp_set_workspace": ([ctypes.c_void_p, u64], st),
         "pp_last_stats": ([P64], st),
         "pp_set_param": ([ctypes.c_char_p, i64], st),
         "pp_get_param": ([ctypes.c_char_p], i64),
@@ -257,6 +258,15 @@ def pp_last_aux_bytes() -> int:
 
 def pp_workspace_bytes(n: int, key_bytes: int = 8, op: int = 0) -> int:
     return int(load().pp_workspace_bytes(n, key_bytes, op))
+
+
+def pp_set_workspace(ws) -> None:
+    """Use a caller-owned device buffer (a CUDA tensor, 256-B aligned) as the
+    library workspace; None reverts to the internal one (pp.h)."""
+    if ws is None:
+        _check(load().pp_set_workspace(None, 0), "pp_set_workspace")
+    else:
+        _check(load().pp_set_workspace(ws.data_ptr(), ws.numel() * ws.element_size()), "pp_set_workspace")
 
 
 def pp_launch_count(reset: bool = False) -> int:

@@ -45,7 +45,23 @@ int sm_count() {
 // in-flight call never loses its buffer.
 static void* g_ws = nullptr;
 static size_t g_ws_bytes = 0;
+// Caller-owned workspace (pp_set_workspace); when set, it replaces the
+// internal one and is never grown or freed by the library.
+static void* g_user_ws = nullptr;
+static size_t g_user_ws_bytes = 0;
+bool user_workspace(void** p, size_t* bytes) {
+    if (!g_user_ws) return false;
+    *p = g_user_ws;
+    *bytes = g_user_ws_bytes;
+    return true;
+}
 void* workspace(size_t bytes, cudaStream_t st) {
+    if (g_user_ws) {
+        if (bytes <= g_user_ws_bytes) return g_user_ws;
+        set_error("caller workspace too small: need " + std::to_string(bytes) + " bytes, have " +
+                  std::to_string(g_user_ws_bytes) + " (pp_workspace_bytes)");
+        return nullptr;
+    }
     if (bytes <= g_ws_bytes) return g_ws;
     if (g_ws) {
         cudaStreamSynchronize(st);
@@ -350,14 +366,32 @@ pp_status pp_dist_plan(const uint64_t* ns, const uint64_t* ts, int nranks, uint6
 }
 
 uint64_t pp_workspace_bytes(uint64_t n, int key_bytes, int op) {
-    // tile/task arrays (<= 2^18 entries each side) + groups + control
-    uint64_t tiles = n / 4096 + 2, tasks = n / 8192 + 2;
-    if (tiles > (1u << 18) + 2) tiles = (1u << 18) + 2;
-    if (tasks > (1u << 18) + 2) tasks = (1u << 18) + 2;
-    uint64_t b = 24 * tiles + 16 * tasks + 24 * 4096 + 4096;
-    if (op == 1) b += (n / 1024 + 16) * 64;  // quicksort segment descriptors
-    (void)key_bytes;
-    return b;
+    std::lock_guard<std::mutex> lk(g_mu);
+    const uint64_t part = (partition_workspace_bound(n) + 255) & ~uint64_t(255);
+    if (op != 1) return part;
+    return part + (key_bytes == 4 ? quicksort_workspace_bound<uint32_t>(n) : quicksort_workspace_bound<uint64_t>(n));
+}
+pp_status pp_set_workspace(void* d_ws, uint64_t bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!d_ws) {
+        g_user_ws = nullptr;
+        g_user_ws_bytes = 0;
+        return PP_OK;
+    }
+    if (bytes == 0 || (uintptr_t)d_ws % 256) {
+        set_error("pp_set_workspace: workspace must be non-empty and 256-byte aligned");
+        return PP_E_INVAL;
+    }
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, d_ws);
+    if (e != cudaSuccess || (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)) {
+        cudaGetLastError();
+        set_error("pp_set_workspace: not a device pointer");
+        return PP_E_INVAL;
+    }
+    g_user_ws = d_ws;
+    g_user_ws_bytes = bytes;
+    return PP_OK;
 }
 uint64_t pp_last_aux_bytes(void) { return g_stats.aux_bytes; }
 

@@ -65,7 +65,13 @@ pp_status cuda_fail(cudaError_t e, const char* what);
 
 // device workspace (grows; one per process / device)
 void* workspace(size_t bytes, cudaStream_t st);
+// caller-owned workspace (pp_set_workspace), if one is set
+bool user_workspace(void** p, size_t* bytes);
 int sm_count();
+// upper bounds of the device workspace (current params), pp_workspace_bytes
+uint64_t partition_workspace_bound(uint64_t n);
+template <typename K>
+uint64_t quicksort_workspace_bound(uint64_t n);
 
 template <typename K>
 pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split, Ctl** ctl_out);

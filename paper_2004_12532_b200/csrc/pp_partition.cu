@@ -1045,6 +1045,16 @@ uint64_t max_groups() {
     return (uint64_t)sm_count() * (uint64_t)occ;
 }
 
+// Largest make_layout any partition_device / ss_groups_device call on <= n
+// keys requests: g <= max(max_groups(), min(param g, n)), the cleanup arrays
+// grow monotonically with n (cleanup_max_tiles).
+uint64_t partition_workspace_bound(uint64_t n) {
+    const Params& P = params();
+    uint64_t g = max_groups();
+    if (P.g > 0) g = std::max<uint64_t>(g, std::min<uint64_t>((uint64_t)P.g, n));
+    return make_layout(n, g, true, (uint64_t)sm_count() * 2).total;
+}
+
 template pp_status partition_device<uint64_t>(uint64_t*, uint64_t, uint64_t, cudaStream_t, uint64_t*, Ctl**);
 template pp_status partition_device<uint32_t>(uint32_t*, uint64_t, uint32_t, cudaStream_t, uint64_t*, Ctl**);
 template pp_status ss_groups_device<uint64_t>(uint64_t*, uint64_t, uint64_t, uint64_t, cudaStream_t, uint64_t*,

@@ -209,21 +209,30 @@ __device__ __forceinline__ void merge_chunk(const K* __restrict__ src, K* __rest
         const uint32_t mid = (a0 + a1) >> 1;
         if (src[lpad(A0 + mid)] <= src[lpad(B0 + d - 1 - mid)]) a0 = mid + 1; else a1 = mid;
     }
-    uint32_t a = a0, b = d - a0;
-    K xa = a < La ? src[lpad(A0 + a)] : KMAX, xb = b < Lb ? src[lpad(B0 + b)] : KMAX;
+    const uint32_t a = a0, b = d - a0;
+    // The 8 outputs are the 8 smallest of A[a, a+8) u B[b, b+8): load all 16
+    // at once (independent loads instead of a chain of 8 load->compare
+    // steps), keep c[i] = min(A[a+i], B[b+7-i]) (bitonic half-cleaner: the
+    // lower half of the bitonic sequence A ++ reverse(B)) and sort that
+    // bitonic sequence with 3 compare-exchange stages.
+    K c[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const bool takeA = (b >= Lb) || (a < La && xa <= xb);
-        if (takeA) {
-            dst[lpad(base + r)] = xa;
-            ++a;
-            xa = a < La ? src[lpad(A0 + a)] : KMAX;
-        } else {
-            dst[lpad(base + r)] = xb;
-            ++b;
-            xb = b < Lb ? src[lpad(B0 + b)] : KMAX;
-        }
+    for (int i = 0; i < 8; ++i) {
+        const K xa = a + i < La ? src[lpad(A0 + a + i)] : KMAX;
+        const K xb = b + 7 - i < Lb ? src[lpad(B0 + b + 7 - i)] : KMAX;
+        c[i] = xa < xb ? xa : xb;
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cmpx(c[i], c[i + 4]);
+#pragma unroll
+    for (int i = 0; i < 8; i += 4) {
+        cmpx(c[i], c[i + 2]);
+        cmpx(c[i + 1], c[i + 3]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) cmpx(c[i], c[i + 1]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[lpad(base + i)] = c[i];
 }
 
 // Leaf sort by merging: every thread sorts its 8 keys in registers (Batcher's
@@ -516,7 +525,24 @@ struct LeafCfg {
 // quicksort workspace (separate from the partition workspace)
 static void* g_qws = nullptr;
 static size_t g_qws_bytes = 0;
+// With a caller workspace (pp_set_workspace) the quicksort's region starts
+// after the partition region of the top-level call: [partition | quicksort].
+static size_t g_qs_user_base = 0;
+static size_t g_qs_peak = 0;
+static inline size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+// leaf / small-segment descriptor lists are uploaded in chunks of this many
+// entries, so the quicksort workspace stays o(n) however many leaves there are
+static constexpr uint64_t QS_LIST_CHUNK = 1u << 20;
+
 static void* qs_workspace(size_t bytes) {
+    g_qs_peak = std::max(g_qs_peak, bytes);
+    void* uw = nullptr;
+    size_t ub = 0;
+    if (user_workspace(&uw, &ub)) {
+        if (g_qs_user_base + bytes <= ub) return static_cast<unsigned char*>(uw) + g_qs_user_base;
+        set_error("caller workspace too small for quicksort (pp_workspace_bytes(n, key_bytes, 1))");
+        return nullptr;
+    }
     if (bytes <= g_qws_bytes) return g_qws;
     if (g_qws) {
         cudaDeviceSynchronize();
@@ -533,22 +559,60 @@ static void* qs_workspace(size_t bytes) {
     return g_qws;
 }
 
+// Size thresholds of the quicksort driver (current params).
+struct QsGeom {
+    uint64_t LEAF;      // segments <= LEAF: one smem sort
+    uint64_t SMALL;     // segments in (LEAF, SMALL]: per-CTA recursion
+    uint64_t BIG;       // segments >= BIG: full multi-CTA partition
+    uint64_t G_TARGET;  // CTAs of one batched mid-level group launch
+};
+template <typename K>
+static QsGeom qs_geom() {
+    using C = GroupCfg<K>;
+    using LC = LeafCfg<K>;
+    const Params& P = params();
+    QsGeom q;
+    // leaf capacity: default LC::LEAF (8192 keys); "leaf" may lower it
+    q.LEAF = (P.leaf > 0 && (uint64_t)P.leaf <= (uint64_t)LC::LEAF) ? (uint64_t)P.leaf : (uint64_t)LC::LEAF;
+    q.BIG = P.qs_cta_max > 0 ? (uint64_t)P.qs_cta_max : (uint64_t)1 << 25;
+    q.SMALL = P.qs_small > 0 ? std::max<uint64_t>((uint64_t)P.qs_small, q.LEAF) : q.LEAF;
+    int occ = 1;
+    cudaFuncSetAttribute(qs_group_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, qs_group_kernel<K>, C::NT, C::SMEM);
+    q.G_TARGET = (uint64_t)sm_count() * (uint64_t)std::max(occ, 1) * (uint64_t)std::max<int64_t>(P.qs_waves, 1);
+    return q;
+}
+
+// Upper bound of the quicksort's own workspace for n keys (excluding the
+// partition region used by big segments).  Per level: mid segments are
+// disjoint and longer than SMALL (<= n/SMALL + 1 of them), each gets
+// <= its proportional share of G_TARGET groups + 1 (rounding, the max(1,.)
+// floor), big ones number <= n/BIG + 1.  The final lists are chunked.
+template <typename K>
+uint64_t quicksort_workspace_bound(uint64_t n) {
+    const QsGeom q = qs_geom<K>();
+    const uint64_t nmid = n / (q.SMALL + 1) + 1, nbig = n / q.BIG + 1;
+    const uint64_t gtot = q.G_TARGET + 2 * nmid + 1;
+    const size_t level = al256(sizeof(QSeg) * nmid) + al256(sizeof(GroupOut) * gtot) + al256(8 * (nmid + nbig + 1));
+    const uint64_t cl = std::min<uint64_t>(n / 2 + 1, QS_LIST_CHUNK);
+    const uint64_t cs = std::min<uint64_t>(n / (q.LEAF + 1) + 1, QS_LIST_CHUNK);
+    const size_t lists = al256(8 * cl) + al256(4 * cl) + al256(8 * cs) + al256(4 * cs) + al256(sizeof(GroupOut) * cs) + 256;
+    return std::max(level, lists);
+}
+template uint64_t quicksort_workspace_bound<uint64_t>(uint64_t);
+template uint64_t quicksort_workspace_bound<uint32_t>(uint64_t);
+
 template <typename K>
 pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     using C = GroupCfg<K>;
     using LC = LeafCfg<K>;
     const Params& P = params();
-    // leaf capacity: default LC::LEAF (8192 keys); "leaf" may lower it
-    const uint64_t LEAF = (P.leaf > 0 && (uint64_t)P.leaf <= (uint64_t)LC::LEAF) ? (uint64_t)P.leaf
-                                                                               : (uint64_t)LC::LEAF;
-    const uint64_t BIG = P.qs_cta_max > 0 ? (uint64_t)P.qs_cta_max : (uint64_t)1 << 25;
+    const QsGeom geom = qs_geom<K>();
+    const uint64_t LEAF = geom.LEAF, BIG = geom.BIG, G_TARGET = geom.G_TARGET;
     const uint64_t MINL = 16;  // at least this many lines per group for mid segments
-    int occ = 1;
-    cudaFuncSetAttribute(qs_group_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, qs_group_kernel<K>, C::NT, C::SMEM);
-    const uint64_t G_TARGET =
-        (uint64_t)sm_count() * (uint64_t)std::max(occ, 1) * (uint64_t)std::max<int64_t>(P.qs_waves, 1);
     const K KMAX = (K)~(K)0;
+    g_qs_user_base = al256(partition_workspace_bound(n));
+    g_qs_peak = 0;
 
     struct HSeg {
         uint64_t lo, hi, pivot;
@@ -558,7 +622,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     std::vector<uint64_t> leaf_lo, small_lo;
     std::vector<uint32_t> leaf_len, small_len;
     // segments in (LEAF, SMALL] finish in one CTA each (qs_small_kernel)
-    const uint64_t SMALL = P.qs_small > 0 ? std::max<uint64_t>((uint64_t)P.qs_small, LEAF) : LEAF;
+    const uint64_t SMALL = geom.SMALL;
     auto add_child = [&](uint64_t lo, uint64_t hi) {
         const uint64_t len = hi - lo;
         if (len <= 1) return;
@@ -696,75 +760,76 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         for (size_t bi = 0; bi < nbig; ++bi) visit(cur[big_idx[bi]], pivots_h[big_idx[bi]], splits_h[nmid + bi]);
         cur.swap(next);
     }
-    // ---- small segments (one CTA each) and leaves: one workspace ----
+    // ---- small segments (one CTA each) and leaves: one workspace, lists
+    // uploaded in chunks of QS_LIST_CHUNK (stream order makes reuse safe) ----
     const uint64_t nleaf = leaf_lo.size(), nsmall = small_lo.size();
-    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    const size_t loB = al(8 * nleaf), lnB = al(4 * nleaf), sloB = al(8 * nsmall), slnB = al(4 * nsmall);
-    const size_t scrB = al(sizeof(GroupOut) * nsmall);
+    const uint64_t cl = std::min<uint64_t>(nleaf, QS_LIST_CHUNK), cs = std::min<uint64_t>(nsmall, QS_LIST_CHUNK);
+    const size_t loB = al256(8 * cl), lnB = al256(4 * cl), sloB = al256(8 * cs), slnB = al256(4 * cs);
+    const size_t scrB = al256(sizeof(GroupOut) * cs);
     unsigned char* qws = static_cast<unsigned char*>(qs_workspace(loB + lnB + sloB + slnB + scrB + 256));
     if (!qws) return PP_E_NOMEM;
     if (nsmall > 0) {
         uint64_t* d_slo = reinterpret_cast<uint64_t*>(qws + loB + lnB);
         uint32_t* d_sln = reinterpret_cast<uint32_t*>(qws + loB + lnB + sloB);
         GroupOut* d_scr = reinterpret_cast<GroupOut*>(qws + loB + lnB + sloB + slnB);
-        e = cudaMemcpyAsync(d_slo, small_lo.data(), 8 * nsmall, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(d_sln, small_len.data(), 4 * nsmall, cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) return cuda_fail(e, "quicksort small H2D");
-        for (uint64_t b0 = 0; b0 < nsmall; b0 += 65535u * 1024u) {
-            const uint64_t cnt = std::min<uint64_t>(nsmall - b0, 65535u * 1024u);
+        for (uint64_t b0 = 0; b0 < nsmall; b0 += QS_LIST_CHUNK) {
+            const uint64_t cnt = std::min<uint64_t>(nsmall - b0, QS_LIST_CHUNK);
+            e = cudaMemcpyAsync(d_slo, small_lo.data() + b0, 8 * cnt, cudaMemcpyHostToDevice, st);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(d_sln, small_len.data() + b0, 4 * cnt, cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort small H2D");
             if (P.qs_small_cfg == 0) {
                 using S = SmallCfg<K, 0>;
                 cudaFuncSetAttribute(qs_small_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-                qs_small_kernel<K, 0><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(keys, d_slo + b0, d_sln + b0, P.seed,
-                                                                             d_scr + b0);
+                qs_small_kernel<K, 0><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(keys, d_slo, d_sln, P.seed, d_scr);
             } else {
                 using S = SmallCfg<K, 1>;
                 cudaFuncSetAttribute(qs_small_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-                qs_small_kernel<K, 1><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(keys, d_slo + b0, d_sln + b0, P.seed,
-                                                                             d_scr + b0);
+                qs_small_kernel<K, 1><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(keys, d_slo, d_sln, P.seed, d_scr);
             }
             note_launches(1);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort small launch");
         }
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "quicksort small launch");
     }
     if (nleaf > 0) {
-        unsigned char* ws = qws;
-        uint64_t* d_lo = reinterpret_cast<uint64_t*>(ws);
-        uint32_t* d_len = reinterpret_cast<uint32_t*>(ws + loB);
-        e = cudaMemcpyAsync(d_lo, leaf_lo.data(), 8 * nleaf, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(d_len, leaf_len.data(), 4 * nleaf, cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) return cuda_fail(e, "quicksort leaves H2D");
-        for (uint64_t b0 = 0; b0 < nleaf; b0 += 65535u * 1024u) {
-            const uint64_t cnt = std::min<uint64_t>(nleaf - b0, 65535u * 1024u);
+        uint64_t* d_lo = reinterpret_cast<uint64_t*>(qws);
+        uint32_t* d_len = reinterpret_cast<uint32_t*>(qws + loB);
+        for (uint64_t b0 = 0; b0 < nleaf; b0 += QS_LIST_CHUNK) {
+            const uint64_t cnt = std::min<uint64_t>(nleaf - b0, QS_LIST_CHUNK);
+            e = cudaMemcpyAsync(d_lo, leaf_lo.data() + b0, 8 * cnt, cudaMemcpyHostToDevice, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(d_len, leaf_len.data() + b0, 4 * cnt, cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort leaves H2D");
             if (P.leaf_algo == 1) {
                 const size_t smem = sizeof(K) * LC::LEAF;
                 cudaFuncSetAttribute(qs_leaf_kernel<K, LC::LEAF, LC::NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem);
-                qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo + b0,
-                                                                                       d_len + b0);
+                qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo, d_len);
             } else if (LEAF <= (uint64_t)LC::LEAF / 2) {  // small leaves: half-size CTAs, more per SM
                 constexpr int HL = LC::LEAF / 2, HN = HL / LEAF_E;
                 const size_t smem = 2 * sizeof(K) * (HL + HL / 8);
                 cudaFuncSetAttribute(qs_leaf_merge_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem);
-                qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, st>>>(keys, d_lo + b0, d_len + b0);
+                qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, st>>>(keys, d_lo, d_len);
             } else {
                 const size_t smem = 2 * sizeof(K) * (LC::LEAF + LC::LEAF / 8);
                 cudaFuncSetAttribute(qs_leaf_merge_kernel<K, LC::LEAF, LC::NT>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo + b0,
-                                                                                             d_len + b0);
+                qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo, d_len);
             }
             note_launches(1);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort leaf launch");
         }
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "quicksort leaf launch");
     }
     // the host vectors must outlive the async copies
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "quicksort leaves");
-    last_stats().aux_bytes = g_qws_bytes;
+    {
+        void* uw = nullptr;
+        size_t ub = 0;
+        last_stats().aux_bytes = user_workspace(&uw, &ub) ? g_qs_user_base + g_qs_peak : g_qws_bytes;
+    }
     return PP_OK;
 }
 

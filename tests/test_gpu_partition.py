@@ -230,6 +230,48 @@ def test_invalid_args(pp):
     assert L.pp_partition_u64(None, 0, 5, None, ctypes.byref(out)) == 0 and out.value == 0
 
 
+def test_caller_workspace(pp):
+    """pp_set_workspace: a caller-owned buffer of
+    pp_workspace_bytes(n, ., op) suffices for partition and quicksort; a too
+    small one fails with PP_E_NOMEM and leaves a partition's array untouched."""
+    from gpu_util import to_dev
+    try:
+        for n, dt in ((3_000_017, np.uint64), (5_000_011, np.uint32), (1 << 15, np.uint64)):
+            a = synth.uniform_u64_np(n, 41) if dt == np.uint64 else synth.uniform_u32_np(n, 41)
+            kb = a.itemsize
+            p = (1 << 63) if dt == np.uint64 else (1 << 31)
+            wb = pp.pp_workspace_bytes(n, kb, 0)
+            assert 0 < wb < 0.05 * n * kb + (1 << 20)
+            ws = torch.empty(wb, dtype=torch.uint8, device="cuda")
+            pp.pp_set_workspace(ws)
+            t = to_dev(a)
+            K = pp.pp_partition(t, p)
+            oracle.check_partition(a, t.cpu().numpy().view(dt), p, K)
+            assert pp.pp_last_aux_bytes() <= wb
+            # quicksort: op 1 bound
+            wq = pp.pp_workspace_bytes(n, kb, 1)
+            assert wq >= wb
+            wsq = torch.empty(wq, dtype=torch.uint8, device="cuda")
+            pp.pp_set_workspace(wsq)
+            t = to_dev(a)
+            pp.pp_quicksort(t)
+            assert np.array_equal(t.cpu().numpy().view(dt), np.sort(a))
+            # too small: NOMEM, array untouched for a partition
+            tiny = torch.empty(256, dtype=torch.uint8, device="cuda")
+            pp.pp_set_workspace(tiny)
+            t = to_dev(a)
+            with pytest.raises(pp.PPError):
+                pp.pp_partition(t, p)
+            assert np.array_equal(t.cpu().numpy().view(dt), a)
+            pp.pp_set_workspace(None)
+        import ctypes
+        h = np.zeros(4096, dtype=np.uint8)
+        addr = (h.ctypes.data + 255) & ~255  # host memory is rejected
+        assert pp.load().pp_set_workspace(ctypes.c_void_p(addr), 1024) == 1
+    finally:
+        pp.pp_set_workspace(None)
+
+
 # ----------------------------------------------------------------------------
 # BASELINE configs at full size (checks via oracle count + device properties)
 # ----------------------------------------------------------------------------
