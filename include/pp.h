@@ -138,7 +138,9 @@ pp_status pp_dist_finalize(void);
  * pp_max_groups() entries if g = 0).  info[0..5] receives
  * {g, head, n_lines, line_keys, seed, 0}: the region is keys[head ..
  * head + n_lines*line_keys), X[j] = ((fmix64(seed + (j+1)*0x9E3779B97F4A7C15)
- * >> 32) * g) >> 32.  vlo/vhi are region-relative positions.
+ * >> 32) * g) >> 32; seed = 0 means X[j] = 0 for every j, the
+ * Strided Algorithm (param "strided").  vlo/vhi are
+ * region-relative positions.
  * The array is left partially partitioned. */
 pp_status pp_ss_groups_u64(uint64_t *keys, uint64_t n, uint64_t pivot, uint64_t g, void *stream,
                            uint64_t *T, uint64_t *vlo, uint64_t *vhi, uint64_t *info);
@@ -169,7 +171,9 @@ uint64_t pp_last_aux_bytes(void);
 pp_status pp_last_stats(uint64_t *out13);
 /* Tunables (tests / benchmarks): "g", "min_lines_per_group", "small_n",
  * "path" (0 auto, 1 single-CTA, 2 smoothed striding, 3 cleanup only), "tile",
- * "ranks", "seed", "leaf", "qs_cta_max", "variant".  Returns PP_E_INVAL for an unknown
+ * "ranks", "seed", "strided" (1: X = 0, the Strided Algorithm PAPER.md:796-825,
+ * i.e. seed 0; 0: back to the default seed), "leaf", "qs_cta_max", "variant",
+ * "leaf_algo", "fused", "qs_small", "qs_small_cfg", "qs_waves".  Returns PP_E_INVAL for an unknown
  * name.  pp_get_param returns INT64_MIN for an unknown name. */
 pp_status pp_set_param(const char *name, int64_t value);
 int64_t pp_get_param(const char *name);

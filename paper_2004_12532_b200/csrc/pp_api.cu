@@ -427,6 +427,7 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "tile") P.tile = value;
     else if (k == "ranks") P.ranks = value;
     else if (k == "seed") P.seed = (uint64_t)value;
+    else if (k == "strided") P.seed = value ? 0 : Params().seed;
     else if (k == "leaf") P.leaf = value;
     else if (k == "qs_cta_max") P.qs_cta_max = value;
     else if (k == "variant") P.variant = value;
@@ -436,6 +437,7 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "qs_small_cfg") P.qs_small_cfg = value;
     else if (k == "fused_stop") P.fused_stop = value;
     else if (k == "qs_waves") P.qs_waves = value;
+    else if (k == "qs_heavy") P.qs_heavy = value;
     else {
         set_error("unknown parameter " + k);
         return PP_E_INVAL;
@@ -454,6 +456,7 @@ int64_t pp_get_param(const char* name) {
     if (k == "tile") return P.tile;
     if (k == "ranks") return P.ranks;
     if (k == "seed") return (int64_t)P.seed;
+    if (k == "strided") return P.seed == 0 ? 1 : 0;
     if (k == "leaf") return P.leaf;
     if (k == "qs_cta_max") return P.qs_cta_max;
     if (k == "variant") return P.variant;
@@ -463,6 +466,7 @@ int64_t pp_get_param(const char* name) {
     if (k == "qs_small_cfg") return P.qs_small_cfg;
     if (k == "fused_stop") return P.fused_stop;
     if (k == "qs_waves") return P.qs_waves;
+    if (k == "qs_heavy") return P.qs_heavy;
     return INT64_MIN;
 }
 

@@ -45,12 +45,13 @@ struct Params {
     int64_t leaf = 0;              // quicksort: 0 = auto smem leaf size
     int64_t qs_cta_max = 0;        // quicksort: 0 = auto segment size handled by one CTA
     int64_t variant = 0;           // group-kernel configuration (pp_partition.cu VariantCfg)
-    int64_t leaf_algo = 0;         // quicksort leaves: 0 merge sort, 1 bitonic network
+    int64_t leaf_algo = 0;         // quicksort bins: 0 auto (= 2), 1 bitonic network, 2 LSD radix, 3 merge sort
     int64_t fused = 0;             // path 2: one cooperative kernel (1) or the kernel chain (0, faster)
     int64_t fused_stop = 0;        // debug/profiling: stop the fused kernel after this phase
     int64_t qs_waves = 2;          // quicksort mid levels: target CTA waves of the group launch
     int64_t qs_small = 1 << 16;    // quicksort: segments <= this finish in one CTA (0 = off)
     int64_t qs_small_cfg = 1;      // quicksort: per-CTA recursion config (pp_quicksort.cu SmallCfg)
+    int64_t qs_heavy = 1 << 21;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
 };
 Params& params();
 

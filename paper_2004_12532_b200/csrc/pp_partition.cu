@@ -70,222 +70,21 @@ __global__ void __launch_bounds__(256) reduce_count_kernel(const K* __restrict__
                                                            const uint64_t* __restrict__ partial, int np, K pivot,
                                                            Ctl* __restrict__ ctl, uint64_t* __restrict__ d_split,
                                                            uint32_t* __restrict__ cntL, uint32_t* __restrict__ cntR) {
-    __shared__ uint64_t sT[8], sMin[8], sMax[8], sHT[8];
-    __shared__ Ctl sc;
-    __shared__ uint32_t s[8];
-    griddep_wait();
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t region_end = n_lines * LK;
-    uint64_t T = 0, vmin = region_end, vmax = 0, ht = 0;
-    if (FROM_GROUPS) {
-        for (uint32_t i = tid; i < g; i += 256) {
-            const GroupOut o = go[i];
-            T += o.T;
-            vmin = o.vlo < vmin ? o.vlo : vmin;
-            vmax = o.vhi > vmax ? o.vhi : vmax;
-        }
-        // head [0,h) and tail [h + region_end, n) predecessors
-        for (uint64_t x = tid; x < h; x += 256) ht += is_pred(keys[x], pivot) ? 1 : 0;
-        for (uint64_t x = h + region_end + tid; x < n; x += 256) ht += is_pred(keys[x], pivot) ? 1 : 0;
-    } else {
-        for (int i = tid; i < np; i += 256) T += partial[i];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        T += __shfl_xor_sync(0xffffffffu, T, o);
-        ht += __shfl_xor_sync(0xffffffffu, ht, o);
-        const uint64_t a = __shfl_xor_sync(0xffffffffu, vmin, o);
-        const uint64_t b = __shfl_xor_sync(0xffffffffu, vmax, o);
-        vmin = a < vmin ? a : vmin;
-        vmax = b > vmax ? b : vmax;
-    }
-    if (lane == 0) {
-        sT[warp] = T;
-        sMin[warp] = vmin;
-        sMax[warp] = vmax;
-        sHT[warp] = ht;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        for (int w = 1; w < 8; ++w) {
-            T += sT[w];
-            ht += sHT[w];
-            vmin = sMin[w] < vmin ? sMin[w] : vmin;
-            vmax = sMax[w] > vmax ? sMax[w] : vmax;
-        }
-        const uint64_t Ksplit = T + ht;
-        uint64_t a[3], b[3];
-        if (FROM_GROUPS) {
-            a[0] = 0; b[0] = h;                                // head
-            const uint64_t lo = h + vmin, hi = h + vmax;       // partial-partition window
-            a[1] = lo < Ksplit ? lo : Ksplit;
-            b[1] = hi > Ksplit ? hi : Ksplit;
-            if (vmin > vmax) { a[1] = b[1] = 0; }             // no non-empty group: no window
-            a[2] = h + region_end; b[2] = n;                   // tail
-            finish_ctl(&sc, n, Ksplit, a, b);
-            sc.vmin = lo;
-            sc.vmax = hi;
-        } else {
-            a[0] = 0; b[0] = n;
-            a[1] = a[2] = b[1] = b[2] = n;
-            finish_ctl(&sc, n, Ksplit, a, b);
-            sc.vmin = 0;
-            sc.vmax = n;
-        }
-        if (blockIdx.x == 0) {
-            *ctl = sc;
-            if (d_split) *d_split = Ksplit;
-        }
-    }
-    __syncthreads();
-    griddep_launch();
-    Dirty d;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        d.s[k] = sc.ds[k];
-        d.l[k] = sc.dl[k];
-    }
-    const uint64_t Kv = sc.Kv, W = sc.W, TT = sc.tile, nL = sc.nL, nR = sc.nR;
-    for (uint64_t t = blockIdx.x; t < nL + nR; t += gridDim.x) {
-        const bool left = t < nL;
-        const uint64_t u0 = left ? t * TT : Kv + (t - nL) * TT;
-        const uint64_t u1 = left ? min(u0 + TT, Kv) : min(u0 + TT, W);
-        uint32_t c = 0;
-        for (uint64_t ub = u0; ub < u1; ub += 8 * 256) {
-            K x[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint64_t u = ub + (uint64_t)k * 256 + tid;
-                x[k] = u < u1 ? keys[vreal(d, u)] : (K)0;
-            }
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint64_t u = ub + (uint64_t)k * 256 + tid;
-                const bool p = is_pred(x[k], pivot);
-                c += (u < u1 && (left ? !p : p)) ? 1u : 0u;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) s[warp] = c;
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t tot = 0;
-            for (int w = 0; w < 8; ++w) tot += s[w];
-            if (left) cntL[t] = tot; else cntR[t - nL] = tot;
-        }
-        __syncthreads();
-    }
+    reduce_count_body<K, FROM_GROUPS>(keys, n, h, n_lines, LK, go, g, partial, np, pivot, ctl, d_split, cntL, cntR, 0,
+                                      blockIdx.x, gridDim.x);
 }
 
 // ===========================================================================
 // K2: exclusive scan of the tile counts (1 CTA, 1024 threads, fixed order).
 // ===========================================================================
-__device__ uint64_t block_exclusive_scan_1024(uint64_t v, uint64_t* sw, uint64_t& total) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint64_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) sw[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        uint64_t w = sw[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        sw[lane] = w;  // inclusive over warps
-    }
-    __syncthreads();
-    total = sw[31];
-    const uint64_t wpre = warp > 0 ? sw[warp - 1] : 0;
-    __syncthreads();
-    return wpre + x - v;
-}
-
-__device__ __forceinline__ uint64_t lower_bound_u64(const uint64_t* a, uint64_t n, uint64_t x) {
-    uint64_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (a[mid] < x) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-__device__ __forceinline__ uint64_t upper_bound_u64(const uint64_t* a, uint64_t n, uint64_t x) {
-    uint64_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (a[mid] <= x) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
-// Scans the tile counts into PL / PR (exclusive rank starts of each tile)
-// and builds the swap task list: the stable merge of PL and PR (left entries
-// first on ties).  Left tile t lands at t + #{PR < PL[t]}, right tile t' at
-// t' + #{PL <= PR[t']} (binary searches in shared memory); each task stores
-// its start rank and the left / right tile holding that rank.
 // Dynamic shared memory: 2 * (cap + 1) u64.
 __global__ void __launch_bounds__(1024) tile_scan_kernel(Ctl* __restrict__ ctl, const uint32_t* __restrict__ cntL,
                                                          const uint32_t* __restrict__ cntR,
                                                          uint64_t* __restrict__ PL, uint64_t* __restrict__ PR,
                                                          uint64_t* __restrict__ rk, uint32_t* __restrict__ ttl,
                                                          uint32_t* __restrict__ ttr) {
-    __shared__ uint64_t sw[32];
-    extern __shared__ uint64_t sp[];  // [nL] PL, then [nR] PR
-    griddep_wait();
-    griddep_launch();
-    const uint64_t nL = ctl->nL, nR = ctl->nR;
-    uint64_t* sPL = sp;
-    uint64_t* sPR = sp + nL;
-    uint64_t carry = 0;
-    for (uint64_t b = 0; b < nL; b += 1024) {
-        const uint64_t i = b + threadIdx.x;
-        uint64_t tot;
-        const uint64_t ex = block_exclusive_scan_1024(i < nL ? cntL[i] : 0, sw, tot);
-        if (i < nL) PL[i] = sPL[i] = carry + ex;
-        carry += tot;
-    }
-    const uint64_t ML = carry;
-    carry = 0;
-    for (uint64_t b = 0; b < nR; b += 1024) {
-        const uint64_t i = b + threadIdx.x;
-        uint64_t tot;
-        const uint64_t ex = block_exclusive_scan_1024(i < nR ? cntR[i] : 0, sw, tot);
-        if (i < nR) PR[i] = sPR[i] = carry + ex;
-        carry += tot;
-    }
-    __syncthreads();
-    const bool ok = (ML == carry && ML > 0);
-    if (ok) {
-        for (uint64_t t = threadIdx.x; t < nL; t += 1024) {
-            const uint64_t r = sPL[t];
-            const uint64_t m = t + lower_bound_u64(sPR, nR, r);
-            rk[m] = r;
-            ttl[m] = (uint32_t)t;
-            ttr[m] = (uint32_t)(upper_bound_u64(sPR, nR, r) - 1);
-        }
-        for (uint64_t t = threadIdx.x; t < nR; t += 1024) {
-            const uint64_t r = sPR[t];
-            const uint64_t ub = upper_bound_u64(sPL, nL, r);
-            const uint64_t m = t + ub;
-            rk[m] = r;
-            ttl[m] = (uint32_t)(ub - 1);
-            ttr[m] = (uint32_t)t;
-        }
-    }
-    if (threadIdx.x == 0) {
-        ctl->ML = ML;
-        ctl->MR = carry;
-        if (ML != carry) ctl->err = 1;  // #misplaced successors must equal #misplaced predecessors
-        // one swap task per breakpoint of the merged tile rank boundaries
-        ctl->nTasks = ok ? nL + nR : 0;
-        rk[ok ? nL + nR : 0] = ML;  // sentinel
-    }
+    extern __shared__ uint64_t sp[];
+    tile_scan_body(ctl, cntL, cntR, PL, PR, rk, ttl, ttr, sp);
 }
 
 // ===========================================================================
@@ -307,26 +106,7 @@ __global__ void __launch_bounds__(SW_NT, 3) locate_kernel(const K* __restrict__ 
                                                           const uint64_t* __restrict__ rk,
                                                           const uint32_t* __restrict__ ttl,
                                                           const uint32_t* __restrict__ ttr) {
-    __shared__ CleanupSmem<K, SW_NT, SW_EPT2> sm;
-    griddep_wait();
-    griddep_launch();
-    const Dirty d = load_dirty(ctl);
-    const uint64_t Kv = ctl->Kv, W = ctl->W, T = ctl->tile, M = ctl->ML;
-    const uint64_t nTasks = ctl->nTasks;
-    for (uint64_t j = blockIdx.x; j <= nTasks; j += gridDim.x) {
-        const uint64_t r = rk[j];
-        uint64_t pl = Kv, pr = W;
-        if (j < nTasks && r < M) {
-            const uint64_t tl = ttl[j], tr = ttr[j];
-            // one round trip per side when the tile is SW_RNG keys
-            select_pair<K, SW_NT, SW_EPT2>(keys, d, pivot, tl * T, min(tl * T + T, Kv), r - PL[tl], Kv + tr * T,
-                                           min(Kv + tr * T + T, W), r - PR[tr], sm.pb, pl, pr);
-        }
-        if (threadIdx.x == 0) {
-            posL[j] = pl;
-            posR[j] = pr;
-        }
-    }
+    locate_body<K>(keys, ctl, pivot, PL, PR, posL, posR, rk, ttl, ttr, blockIdx.x, gridDim.x);
 }
 
 // ===========================================================================
@@ -337,23 +117,7 @@ __global__ void __launch_bounds__(SW_NT, 3) swap_kernel(K* __restrict__ keys, co
                                                      const uint64_t* __restrict__ posL,
                                                      const uint64_t* __restrict__ posR,
                                                      const uint64_t* __restrict__ rk) {
-    __shared__ CleanupSmem<K, SW_NT, SW_EPT2> sm;
-    griddep_wait();
-    const Dirty d = load_dirty(ctl);
-    const uint64_t nTasks = ctl->nTasks, T = ctl->tile, Kv = ctl->Kv, W = ctl->W;
-    for (uint64_t j = blockIdx.x; j < nTasks; j += gridDim.x) {
-        const uint64_t pairs = rk[j + 1] - rk[j];
-        if (pairs == 0) continue;
-        const uint64_t uL = posL[j], uR = posR[j];
-        // the task's items lie in the tiles of its first items: clamp to them
-        const uint64_t tle = min((uL / T + 1) * T, Kv), tre = min(Kv + ((uR - Kv) / T + 1) * T, W);
-        const uint64_t eL = min(posL[j + 1], tle), eR = min(posR[j + 1], tre);
-        if (T == (uint64_t)SW_RNG) {
-            swap_pair<K, SW_NT, SW_EPT2>(keys, d, pivot, uL, eL, uR, eR, pairs, sm.pb);
-        } else {
-            walk_swap_stream<K, SW_NT, SW_EPT2>(keys, d, pivot, uL, eL, uR, eR, sm.sb);
-        }
-    }
+    swap_body<K>(keys, ctl, pivot, posL, posR, rk, blockIdx.x, gridDim.x);
 }
 
 // ===========================================================================

@@ -15,6 +15,8 @@
 // split is empty (p is the segment minimum) the next level splits by x <= p
 // and the left part (all == p) is final (reading R14).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "pp_engine.cuh"
@@ -80,13 +82,15 @@ __global__ void __launch_bounds__(GroupCfg<K>::NT) qs_group_kernel(K* __restrict
 
 // One CTA per mid segment: reduce the segment's group outputs, then clean its
 // dirty set with the single-CTA rank-matched walk; writes the split.
-template <typename K>
-__global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys, const QSeg* __restrict__ segs,
-                                                            const GroupOut* __restrict__ gout,
-                                                            uint64_t* __restrict__ splits) {
+template <typename K, int NT, int EPT>
+__global__ void __launch_bounds__(NT) qs_cleanup_kernel(K* __restrict__ keys, const QSeg* __restrict__ segs,
+                                                         const GroupOut* __restrict__ gout,
+                                                         uint64_t* __restrict__ splits, uint64_t heavy) {
     using C = GroupCfg<K>;
-    __shared__ StreamBuf<SW_NT, SW_EPT2> sb;
-    __shared__ uint64_t red[4][SW_NT / 32];
+    extern __shared__ __align__(16) unsigned char csm[];
+    if (heavy && segs[blockIdx.x].hi - segs[blockIdx.x].lo >= heavy) return;  // batched multi-CTA cleanup
+    StreamBuf<NT, EPT>& sb = *reinterpret_cast<StreamBuf<NT, EPT>*>(csm);
+    __shared__ uint64_t red[4][NT / 32];
     const QSeg q = segs[blockIdx.x];
     K* seg = keys + q.lo;
     const uint64_t len = q.hi - q.lo;
@@ -95,14 +99,14 @@ __global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys,
     const uint64_t n_lines = (len - h) / C::LK;
     const uint64_t region_end = n_lines * C::LK;
     uint64_t T = 0, vmin = region_end, vmax = 0, ht = 0;
-    for (uint64_t i = threadIdx.x; i < q.g; i += SW_NT) {
+    for (uint64_t i = threadIdx.x; i < q.g; i += NT) {
         const GroupOut o = gout[q.gbase + i];
         T += o.T;
         vmin = o.vlo < vmin ? o.vlo : vmin;
         vmax = o.vhi > vmax ? o.vhi : vmax;
     }
-    for (uint64_t x = threadIdx.x; x < h; x += SW_NT) ht += is_pred(seg[x], pivot) ? 1 : 0;
-    for (uint64_t x = h + region_end + threadIdx.x; x < len; x += SW_NT) ht += is_pred(seg[x], pivot) ? 1 : 0;
+    for (uint64_t x = threadIdx.x; x < h; x += NT) ht += is_pred(seg[x], pivot) ? 1 : 0;
+    for (uint64_t x = h + region_end + threadIdx.x; x < len; x += NT) ht += is_pred(seg[x], pivot) ? 1 : 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -121,7 +125,7 @@ __global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys,
     }
     __syncthreads();
     T = 0; ht = 0; vmin = region_end; vmax = 0;
-    for (int w = 0; w < SW_NT / 32; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
         T += red[0][w];
         ht += red[1][w];
         vmin = red[2][w] < vmin ? red[2][w] : vmin;
@@ -139,9 +143,92 @@ __global__ void __launch_bounds__(SW_NT) qs_cleanup_kernel(K* __restrict__ keys,
     Dirty d;
 #pragma unroll
     for (int k = 0; k < 3; ++k) { d.s[k] = c.ds[k]; d.l[k] = c.dl[k]; }
-    walk_swap_stream<K, SW_NT, SW_EPT2>(seg, d, pivot, 0, c.Kv, c.Kv, c.W, sb);
+    walk_swap_stream<K, NT, EPT>(seg, d, pivot, 0, c.Kv, c.Kv, c.W, sb);
     if (threadIdx.x == 0) splits[blockIdx.x] = Ks;
 }
+
+// ---------------------------------------------------------------------------
+// Heavy mid segments (>= qs_heavy keys): their dirty windows are long (the
+// window grows with the segment's chunk of g_s lines), so one CTA walking it
+// is latency bound.  They get the multi-CTA cleanup pipeline of the
+// partition (reduce+count, tile scan, locate, rank-matched swap; the device
+// bodies of pp_engine.cuh), batched: blockIdx.y = heavy segment, each with
+// its own control block and tile arrays (QS_HEAVY_TILES tiles per side, the
+// tile size grows with the window).
+// ---------------------------------------------------------------------------
+constexpr uint64_t QS_HEAVY_TILES = 512;
+struct HvLayout {
+    size_t ctl, cntL, cntR, PL, PR, posL, posR, rk, ttl, ttr, stride;
+};
+static HvLayout hv_layout() {
+    const uint64_t tiles = QS_HEAVY_TILES + 1, tasks = 2 * QS_HEAVY_TILES + 2;
+    HvLayout L;
+    size_t o = 0;
+    auto take = [&](size_t b) {
+        const size_t at = o;
+        o += (b + 255) & ~size_t(255);
+        return at;
+    };
+    L.ctl = take(sizeof(Ctl));
+    L.cntL = take(4 * tiles);
+    L.cntR = take(4 * tiles);
+    L.PL = take(8 * tiles);
+    L.PR = take(8 * tiles);
+    L.posL = take(8 * tasks);
+    L.posR = take(8 * tasks);
+    L.rk = take(8 * tasks);
+    L.ttl = take(4 * tasks);
+    L.ttr = take(4 * tasks);
+    L.stride = o;
+    return L;
+}
+#define HV_PTR(T, f) reinterpret_cast<T*>(w + L.f)
+
+template <typename K>
+__global__ void __launch_bounds__(256) qs_hv_reduce_kernel(K* __restrict__ keys, const QSeg* __restrict__ segs,
+                                                           const uint32_t* __restrict__ hidx,
+                                                           const GroupOut* __restrict__ gout,
+                                                           uint64_t* __restrict__ splits, unsigned char* ws,
+                                                           HvLayout L) {
+    using C = GroupCfg<K>;
+    const uint32_t si = hidx[blockIdx.y];
+    const QSeg q = segs[si];
+    unsigned char* w = ws + (size_t)blockIdx.y * L.stride;
+    const uint64_t len = q.hi - q.lo;
+    const uint64_t h = seg_head<K>(keys, q.lo, len);
+    reduce_count_body<K, true>(keys + q.lo, len, h, (len - h) / C::LK, (uint32_t)C::LK, gout + q.gbase,
+                               (uint32_t)q.g, nullptr, 0, (K)q.pivot, HV_PTR(Ctl, ctl), splits + si,
+                               HV_PTR(uint32_t, cntL), HV_PTR(uint32_t, cntR), QS_HEAVY_TILES, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(1024) qs_hv_scan_kernel(unsigned char* ws, HvLayout L) {
+    extern __shared__ uint64_t hsp[];
+    unsigned char* w = ws + (size_t)blockIdx.x * L.stride;
+    tile_scan_body(HV_PTR(Ctl, ctl), HV_PTR(uint32_t, cntL), HV_PTR(uint32_t, cntR), HV_PTR(uint64_t, PL),
+                   HV_PTR(uint64_t, PR), HV_PTR(uint64_t, rk), HV_PTR(uint32_t, ttl), HV_PTR(uint32_t, ttr), hsp);
+}
+
+template <typename K>
+__global__ void __launch_bounds__(SW_NT, 3) qs_hv_locate_kernel(K* __restrict__ keys, const QSeg* __restrict__ segs,
+                                                                const uint32_t* __restrict__ hidx,
+                                                                unsigned char* ws, HvLayout L) {
+    const QSeg q = segs[hidx[blockIdx.y]];
+    unsigned char* w = ws + (size_t)blockIdx.y * L.stride;
+    locate_body<K>(keys + q.lo, HV_PTR(Ctl, ctl), (K)q.pivot, HV_PTR(uint64_t, PL), HV_PTR(uint64_t, PR),
+                   HV_PTR(uint64_t, posL), HV_PTR(uint64_t, posR), HV_PTR(uint64_t, rk), HV_PTR(uint32_t, ttl),
+                   HV_PTR(uint32_t, ttr), blockIdx.x, gridDim.x);
+}
+
+template <typename K>
+__global__ void __launch_bounds__(SW_NT, 3) qs_hv_swap_kernel(K* __restrict__ keys, const QSeg* __restrict__ segs,
+                                                              const uint32_t* __restrict__ hidx, unsigned char* ws,
+                                                              HvLayout L) {
+    const QSeg q = segs[hidx[blockIdx.y]];
+    unsigned char* w = ws + (size_t)blockIdx.y * L.stride;
+    swap_body<K>(keys + q.lo, HV_PTR(Ctl, ctl), (K)q.pivot, HV_PTR(uint64_t, posL), HV_PTR(uint64_t, posR),
+                 HV_PTR(uint64_t, rk), blockIdx.x, gridDim.x);
+}
+#undef HV_PTR
 
 // Leaf sort: one CTA sorts one segment of <= LEAF keys with a bitonic
 // network (padding with the maximum key, never stored back).  Each thread
@@ -191,13 +278,13 @@ __device__ __forceinline__ void sort8(K (&v)[8]) {  // Batcher's 19-comparator n
     cmpx(v[1], v[2]); cmpx(v[3], v[4]); cmpx(v[5], v[6]);
 }
 
-// One merge step for the 8 outputs starting at `base`: runs of length L in
-// src (padded layout) -> dst.  Runs A = [blk, blk+La), B = [blk+La, +Lb)
+// The 8 outputs starting at `base` of one merge step: runs of length L in
+// src (padded layout) -> c[0..8).  Runs A = [blk, blk+La), B = [blk+La, +Lb)
 // (the last pair may be short); the start is found on the merge path by
 // binary search (ties: A first).
 template <typename K>
-__device__ __forceinline__ void merge_chunk(const K* __restrict__ src, K* __restrict__ dst, uint32_t base,
-                                            uint32_t L, uint32_t P) {
+__device__ __forceinline__ void merge_chunk_regs(const K* __restrict__ src, uint32_t base, uint32_t L, uint32_t P,
+                                                 K (&c)[8]) {
     const K KMAX = (K)~(K)0;
     const uint32_t blk = base / (2 * L) * (2 * L);
     const uint32_t d = base - blk;
@@ -215,7 +302,6 @@ __device__ __forceinline__ void merge_chunk(const K* __restrict__ src, K* __rest
     // steps), keep c[i] = min(A[a+i], B[b+7-i]) (bitonic half-cleaner: the
     // lower half of the bitonic sequence A ++ reverse(B)) and sort that
     // bitonic sequence with 3 compare-exchange stages.
-    K c[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const K xa = a + i < La ? src[lpad(A0 + a + i)] : KMAX;
@@ -231,23 +317,76 @@ __device__ __forceinline__ void merge_chunk(const K* __restrict__ src, K* __rest
     }
 #pragma unroll
     for (int i = 0; i < 8; i += 2) cmpx(c[i], c[i + 1]);
+}
+
+template <typename K>
+__device__ __forceinline__ void merge_chunk(const K* __restrict__ src, K* __restrict__ dst, uint32_t base,
+                                            uint32_t L, uint32_t P) {
+    K c[8];
+    merge_chunk_regs<K>(src, base, L, P, c);
 #pragma unroll
     for (int i = 0; i < 8; ++i) dst[lpad(base + i)] = c[i];
 }
 
-// Leaf sort by merging: every thread sorts its 8 keys in registers (Batcher's
-// 19-comparator network), then log2(P/8) rounds merge pairs of sorted runs
-// in shared memory; each thread produces 8 outputs of a merge, locating its
-// start on the merge path by binary search (ties: left run first -- the sort
-// is a plain ascending sort, stability is irrelevant for keys).
+// Sorts the 256 keys of a warp held as 8 consecutive keys per lane (lane l
+// holds positions 8l..8l+7, each lane's 8 already ascending) in registers:
+// bitonic merges of ascending runs 8 -> 16 -> ... -> 256.  Each merge of two
+// ascending runs of k/2 is a "flip" stage (position i against i ^ (k-1), the
+// reversed partner, so no descending runs are needed) then half-cleaners
+// i ^ j for j = k/4 .. 1; partners in other lanes come by __shfl_xor_sync,
+// j < 8 stays inside the lane.
+template <typename K>
+__device__ __forceinline__ void warp_sort256(K (&v)[8]) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (uint32_t k = 16; k <= 256; k <<= 1) {
+        {  // flip: element (lane, r) vs (lane ^ (k/8 - 1), 7 - r)
+            const uint32_t m = k / 8 - 1;
+            const bool lower = (lane & (k / 16)) == 0;
+            K y[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) y[r] = __shfl_xor_sync(0xffffffffu, v[7 - r], m);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v[r] = lower ? (v[r] < y[r] ? v[r] : y[r]) : (v[r] < y[r] ? y[r] : v[r]);
+        }
+#pragma unroll
+        for (uint32_t j = k / 4; j >= 8; j >>= 1) {  // half-cleaners across lanes
+            const uint32_t m = j / 8;
+            const bool lower = (lane & m) == 0;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const K y = __shfl_xor_sync(0xffffffffu, v[r], m);
+                v[r] = lower ? (v[r] < y ? v[r] : y) : (v[r] < y ? y : v[r]);
+            }
+        }
+        // half-cleaners j = 4, 2, 1 inside the lane
+#pragma unroll
+        for (int r = 0; r < 4; ++r) cmpx(v[r], v[r + 4]);
+#pragma unroll
+        for (int r = 0; r < 8; r += 4) {
+            cmpx(v[r], v[r + 2]);
+            cmpx(v[r + 1], v[r + 3]);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; r += 2) cmpx(v[r], v[r + 1]);
+    }
+}
+
+// Sort of one bin (a contiguous range of <= LEAF keys; len 0 = empty slot) by
+// merging in ONE padded shared-memory buffer: every thread loads its keys
+// (all loads in flight), sorts 8 consecutive keys in registers (Batcher's
+// 19-comparator network), then log2(P/8) merge rounds; in each round every
+// thread computes its 8 outputs on the merge path into registers, and they
+// are stored after a barrier (so the buffer is read and rewritten in place).
+// One buffer = ~74 KiB for 8192 u64 keys: two CTAs per SM.  Ties: left run
+// first (a plain ascending sort; stability is irrelevant for keys).
 template <typename K, int LEAF, int NT>
 __global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
                                                            const uint64_t* __restrict__ leaf_lo,
                                                            const uint32_t* __restrict__ leaf_len) {
     static_assert(LEAF == NT * LEAF_E, "one block holds LEAF keys");
     extern __shared__ __align__(16) unsigned char lsm[];
-    K* src = reinterpret_cast<K*>(lsm);
-    K* dst = src + lpad(LEAF);
+    K* buf = reinterpret_cast<K*>(lsm);
     const uint64_t lo = leaf_lo[blockIdx.x];
     const uint32_t len = leaf_len[blockIdx.x];
     // pad to whole warps of 8 keys per thread (not to a power of two)
@@ -256,24 +395,39 @@ __global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
     const uint32_t tid = threadIdx.x;
     if (tid >= nthr) return;
     const K KMAX = (K)~(K)0;
-    for (uint32_t i = tid; i < P; i += nthr) src[lpad(i)] = i < len ? keys[lo + i] : KMAX;
+    {
+        K v[LEAF_E];
+#pragma unroll
+        for (int r = 0; r < LEAF_E; ++r) {
+            const uint32_t i = (uint32_t)r * nthr + tid;
+            v[r] = i < len ? __ldcs(keys + lo + i) : KMAX;
+        }
+#pragma unroll
+        for (int r = 0; r < LEAF_E; ++r) buf[lpad((uint32_t)r * nthr + tid)] = v[r];
+    }
     leaf_bar(nthr);
     const uint32_t base = tid * LEAF_E;
     K v[LEAF_E];
 #pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) v[r] = src[lpad(base + r)];
+    for (int r = 0; r < LEAF_E; ++r) v[r] = buf[lpad(base + r)];
     sort8(v);
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) src[lpad(base + r)] = v[r];
+    warp_sort256(v);  // runs of 256 (one warp) sorted in registers
     leaf_bar(nthr);
-    for (uint32_t L = LEAF_E; L < P; L <<= 1) {
-        merge_chunk<K>(src, dst, base, L, P);
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) buf[lpad(base + r)] = v[r];
+    leaf_bar(nthr);
+    for (uint32_t L = 32 * LEAF_E; L < P; L <<= 1) {
+        merge_chunk_regs<K>(buf, base, L, P, v);
         leaf_bar(nthr);
-        K* t = src;
-        src = dst;
-        dst = t;
+#pragma unroll
+        for (int r = 0; r < LEAF_E; ++r) buf[lpad(base + r)] = v[r];
+        leaf_bar(nthr);
     }
-    for (uint32_t i = tid; i < len; i += nthr) keys[lo + i] = src[lpad(i)];
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) {
+        const uint32_t i = (uint32_t)r * nthr + tid;
+        if (i < len) __stcs(keys + lo + i, buf[lpad(i)]);
+    }
 }
 
 // ===========================================================================
@@ -342,7 +496,7 @@ __device__ void cta_merge_sort(K* __restrict__ g, uint32_t len, K* A, K* B) {
 // In-place partition of seg[0, len) by key < pivot with one CTA; returns K.
 template <typename K, int V>
 __device__ uint64_t cta_partition(K* __restrict__ seg, uint64_t len, K pivot, uint64_t seed, unsigned char* smem,
-                                  GroupOut* scratch, Ctl* sc, uint64_t* red) {
+                                  GroupOut* scratch, Ctl* sc, uint64_t* red, uint64_t* pr = nullptr) {
     using S = SmallCfg<K, V>;
     using GC = typename S::GC;
     constexpr int NT = S::NT, NW = NT / 32;
@@ -388,72 +542,290 @@ __device__ uint64_t cta_partition(K* __restrict__ seg, uint64_t len, K pivot, ui
         d.l[k] = sc->dl[k];
     }
     const uint64_t Ks = sc->K, Kv = sc->Kv, W = sc->W;
+    uint64_t tw = pr ? clock64() : 0;
     walk_swap_stream<K, NT, SW_EPT2>(seg, d, pivot, 0, Kv, Kv, W,
                                      *reinterpret_cast<StreamBuf<NT, SW_EPT2>*>(smem));
     __syncthreads();
+    if (pr) pr[3] += clock64() - tw;
     return Ks;
 }
 
+// Bin slots a small segment of len keys may fill: greedy packing of its
+// leaves (in array order) into bins of <= leaf keys leaves consecutive bins
+// summing to > leaf, so <= 2*ceil(len/leaf) + 1 bins, plus one per range that
+// is skipped (all keys equal) -- the rest of the slack; a CTA that runs out
+// sorts the overflowing bin itself (qs_small_kernel).
+__host__ __device__ __forceinline__ uint64_t qs_bin_cap(uint64_t len, uint64_t leaf) {
+    return 2 * ((len + leaf - 1) / leaf) + 4;
+}
+
+// Stack entry modes of qs_small_kernel.
+constexpr int QM_PIVOT = 0;   // pivot = median-of-3, split by x < p
+constexpr int QM_LE = 1;      // split by x < p with p = (segment minimum) + 1, i.e. x <= min
+constexpr int QM_INCTA = 2;   // flag: this range is sorted inside the CTA (bin slots exhausted)
+
+// One CTA per small segment (leaf < len <= qs_small): the rest of its
+// recursion, depth first with an explicit stack, left part first so that the
+// leaves (pieces <= leaf keys) appear in array order.  Leaves are not sorted
+// here: adjacent leaves are packed greedily into bins of <= leaf keys, and
+// each bin (a contiguous range that is a union of whole leaves, so sorting it
+// whole sorts each leaf) is written to this segment's slots [slot_base[i],
+// +qs_bin_cap); unused slots get length 0.  One wide shared-memory sort
+// launch then sorts every bin (qs_leaf_merge_kernel).  Ranges whose keys are
+// all equal (the x <= min split, reading R14) are final and skipped.  If the
+// slots run out, the overflowing bin is pushed back with QM_INCTA and sorted
+// by this CTA itself (partition down to LEAFC, merge sort in shared memory).
 template <typename K, int V>
 __global__ void __launch_bounds__(SmallCfg<K, V>::NT, SmallCfg<K, V>::MINB)
     qs_small_kernel(K* __restrict__ keys, const uint64_t* __restrict__ seg_lo, const uint32_t* __restrict__ seg_len,
-                    uint64_t seed, GroupOut* __restrict__ scratch) {
+                    const uint64_t* __restrict__ slot_base, uint64_t* __restrict__ bin_lo,
+                    uint32_t* __restrict__ bin_len, uint32_t leaf, uint64_t seed, GroupOut* __restrict__ scratch,
+                    uint64_t* __restrict__ prof) {
     using S = SmallCfg<K, V>;
+    constexpr int DEPTH = 64, LEFT_FIRST_MAX = 40;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ Ctl sc;
     __shared__ uint64_t red[S::NT / 32];
-    __shared__ uint64_t st_lo[64], st_hi[64], st_p[64];
-    __shared__ int st_mode[64];
+    __shared__ uint64_t st_lo[DEPTH], st_hi[DEPTH], st_p[DEPTH];
+    __shared__ int st_mode[DEPTH];
     __shared__ int sp;
     const K KMAX = (K)~(K)0;
     K* A = reinterpret_cast<K*>(smem);
     K* B = A + lpad(S::LEAFC);
+    // bin state (thread 0 only): open bin [blo, bhi), slots used
+    uint64_t blo = 0, bhi = 0;
+    uint32_t used = 0;
+    const uint64_t base = slot_base[blockIdx.x];
+    const uint32_t cap = (uint32_t)qs_bin_cap(seg_len[blockIdx.x], leaf);
+    auto push = [&](uint64_t lo, uint64_t hi, int mode, uint64_t p) {  // thread 0
+        const int s = sp;
+        st_lo[s] = lo; st_hi[s] = hi; st_mode[s] = mode; st_p[s] = p;
+        sp = s + 1;
+    };
+    auto emit = [&]() {  // thread 0: close the open bin
+        if (bhi > blo) {
+            if (used < cap) {
+                bin_lo[base + used] = blo;
+                bin_len[base + used] = (uint32_t)(bhi - blo);
+                ++used;
+            } else {
+                push(blo, bhi, QM_PIVOT | QM_INCTA, 0);
+            }
+        }
+        blo = bhi = 0;
+    };
     if (threadIdx.x == 0) {
-        st_lo[0] = seg_lo[blockIdx.x];
-        st_hi[0] = st_lo[0] + seg_len[blockIdx.x];
-        st_mode[0] = 0;
-        st_p[0] = 0;
-        sp = 1;
+        sp = 0;
+        push(seg_lo[blockIdx.x], seg_lo[blockIdx.x] + seg_len[blockIdx.x], QM_PIVOT, 0);
     }
     __syncthreads();
-    while (sp > 0) {
+    // optional phase profile (debug, PP_QS_PROF): cycles in pivot / partition / merge sort, counts
+    uint64_t pr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint64_t t0 = prof ? clock64() : 0;
+    for (;;) {
+        if (sp == 0) {  // uniform: sp is only written by thread 0 before a barrier
+            __syncthreads();
+            if (threadIdx.x == 0) emit();
+            __syncthreads();
+            if (sp == 0) break;
+        }
         const int top = sp - 1;
         const uint64_t lo = st_lo[top], hi = st_hi[top], pm = st_p[top];
         const int mode = st_mode[top];
         __syncthreads();
         if (threadIdx.x == 0) sp = top;
         const uint64_t len = hi - lo;
+        const int incta = mode & QM_INCTA;
+        if (!incta && len <= leaf) {  // a leaf: into the open bin (thread 0), or a new bin
+            if (threadIdx.x == 0 && len > 0) {
+                if (bhi == lo && hi - blo <= leaf) bhi = hi;
+                else if (blo == hi && bhi - lo <= leaf) blo = lo;
+                else { emit(); blo = lo; bhi = hi; }
+            }
+            __syncthreads();
+            continue;
+        }
         if (len <= 1) {
             __syncthreads();
             continue;
         }
-        if (len <= S::LEAFC) {
+        if (incta && len <= S::LEAFC) {
             cta_merge_sort<K, S::NT>(keys + lo, (uint32_t)len, A, B);
+            if (prof) { const uint64_t t1 = clock64(); pr[2] += t1 - t0; pr[5] += 1; pr[7] += len; t0 = t1; }
             continue;
         }
         K p;
-        if (mode == 0) p = median3<K>(keys[lo], keys[lo + (len - 1) / 2], keys[hi - 1]);
+        if ((mode & QM_LE) == 0) p = median3<K>(keys[lo], keys[lo + (len - 1) / 2], keys[hi - 1]);
         else p = (K)pm;
-        const uint64_t k = cta_partition<K, V>(keys + lo, len, p, seed, smem, scratch + blockIdx.x, &sc, red);
+        if (prof) { const uint64_t t1 = clock64(); pr[0] += t1 - t0; t0 = t1; }
+        const uint64_t k = cta_partition<K, V>(keys + lo, len, p, seed, smem, scratch + blockIdx.x, &sc, red,
+                                               prof ? pr : nullptr);
+        if (prof) { const uint64_t t1 = clock64(); pr[1] += t1 - t0; pr[4] += 1; pr[6] += len; t0 = t1; }
         if (threadIdx.x == 0) {
-            int s = sp;
-            if (mode == 0 && k == 0) {
-                if (p != KMAX) {  // p is the minimum: split by x <= p next (reading R14)
-                    st_lo[s] = lo; st_hi[s] = hi; st_mode[s] = 1; st_p[s] = (uint64_t)(K)(p + 1); ++s;
-                }
-            } else if (mode == 1) {
-                st_lo[s] = lo + k; st_hi[s] = hi; st_mode[s] = 0; st_p[s] = 0; ++s;  // [lo, lo+k) all == p
-            } else {
-                // push the larger part first: the smaller is processed next (stack depth <= log2 len)
+            if ((mode & QM_LE) == 0 && k == 0) {
+                // p is the minimum: split by x <= p next (reading R14); all == MAX: final
+                if (p != KMAX) push(lo, hi, QM_LE | incta, (uint64_t)(K)(p + 1));
+            } else if (mode & QM_LE) {
+                push(lo + k, hi, QM_PIVOT | incta, 0);  // [lo, lo+k) is all == p: final, skipped
+            } else if (incta || sp >= LEFT_FIRST_MAX) {
+                // smaller part first (stack depth <= log2 len from here)
                 const bool left_small = k < len - k;
-                const uint64_t a0 = left_small ? lo + k : lo, a1 = left_small ? hi : lo + k;
-                const uint64_t b0 = left_small ? lo : lo + k, b1 = left_small ? lo + k : hi;
-                st_lo[s] = a0; st_hi[s] = a1; st_mode[s] = 0; st_p[s] = 0; ++s;
-                st_lo[s] = b0; st_hi[s] = b1; st_mode[s] = 0; st_p[s] = 0; ++s;
+                if (left_small) { push(lo + k, hi, QM_PIVOT | incta, 0); push(lo, lo + k, QM_PIVOT | incta, 0); }
+                else { push(lo, lo + k, QM_PIVOT | incta, 0); push(lo + k, hi, QM_PIVOT | incta, 0); }
+            } else {
+                // left part first: leaves come out in array order
+                push(lo + k, hi, QM_PIVOT, 0);
+                push(lo, lo + k, QM_PIVOT, 0);
             }
-            sp = s;
         }
         __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (uint32_t u = used; u < cap; ++u) bin_len[base + u] = 0;
+    }
+    if (prof && threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) prof[8 * (uint64_t)blockIdx.x + i] = pr[i];
+    }
+}
+
+// Bin sort by a stable LSD radix sort over the bits the bin's keys actually
+// span (after ~15 quicksort levels a bin is narrow: ~49 bits for uniform u64
+// keys, ~10 for keys in [0,1000)): digit_p(x) = ((x - min) >> 8p) & 255 for
+// p < ceil(bits(max - min) / 8); a bin whose keys are all equal is left as is.
+// No comparisons (the merge sort is issue-bound on 64-bit compare-exchange)
+// and no atomics: warp w owns positions [256w, 256w+256) (8 rounds of 32
+// lanes), ranks its keys per digit against its own row
+// of u16 counters (peers found by 8 ballots, one per digit bit), a
+// fixed-order scan turns the counters into offsets
+// (digit-major, then warp), and the keys are scattered from registers into
+// one shared buffer and reloaded in position order.  Stable by construction
+// (position order within a warp, warps in order within a digit).  Positions
+// >= len are padded with the bin's maximum, which stays after the real
+// maxima (stability) and is never stored.  Registers hold the keys, so one
+// 64 KiB buffer + 16 KiB of counters suffices.
+template <typename K, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) qs_leaf_radix_kernel(K* __restrict__ keys,
+                                                                   const uint64_t* __restrict__ leaf_lo,
+                                                                   const uint32_t* __restrict__ leaf_len) {
+    extern __shared__ __align__(16) unsigned char lsm[];
+    K* buf = reinterpret_cast<K*>(lsm);                        // NW * 256 keys
+    uint16_t* cnt = reinterpret_cast<uint16_t*>(buf + NW * 256);  // [NW][256]
+    __shared__ uint32_t dbase[256];
+    __shared__ uint32_t dtot[256];
+    __shared__ K rmn[NW], rmx[NW];
+    const uint64_t lo = leaf_lo[blockIdx.x];
+    const uint32_t len = leaf_len[blockIdx.x];
+    if (len <= 1) return;
+    const uint32_t W = (len + 255) / 256;  // active warps
+    const uint32_t nthr = W * 32;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid >= nthr) return;
+    const uint32_t lt = lanemask_lt();
+    const K KMAX = (K)~(K)0;
+    K v[8];
+    K mn = KMAX, mx = 0;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const uint32_t p = 256 * w + 32 * r + lane;
+        v[r] = p < len ? __ldcs(keys + lo + p) : (K)0;
+        if (p < len) {
+            mn = v[r] < mn ? v[r] : mn;
+            mx = v[r] > mx ? v[r] : mx;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const K a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+    }
+    if (lane == 0) {
+        rmn[w] = mn;
+        rmx[w] = mx;
+    }
+    leaf_bar(nthr);
+    for (uint32_t i = 0; i < W; ++i) {
+        mn = rmn[i] < mn ? rmn[i] : mn;
+        mx = rmx[i] > mx ? rmx[i] : mx;
+    }
+    if (mn == mx) return;  // all keys equal: already sorted (uniform across the CTA)
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        if (256 * w + 32 * r + lane >= len) v[r] = mx;
+    const uint64_t range = (uint64_t)(mx - mn);
+    const int bits = 64 - __clzll((long long)range);
+    const int npass = (bits + 7) / 8;
+    uint16_t* row = cnt + 256 * w;
+    for (int pass = 0; pass < npass; ++pass) {
+        const int shift = 8 * pass;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) row[32 * k + lane] = 0;
+        __syncwarp();
+        uint32_t d[8], rk[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) d[r] = (uint32_t)((uint64_t)(v[r] - mn) >> shift) & 255u;
+        uint32_t peers[8];  // lanes of this round with the same digit (ballot multisplit, 8 ballots)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            uint32_t m = 0xffffffffu;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const bool bit = (d[r] >> b) & 1u;
+                const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+                m &= bit ? bb : ~bb;
+            }
+            peers[r] = m;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint32_t m = peers[r];
+            const uint32_t c = row[d[r]];
+            rk[r] = c + __popc(m & lt);
+            __syncwarp();
+            if (lane == (uint32_t)(__ffs(m) - 1)) row[d[r]] = (uint16_t)(c + __popc(m));
+            __syncwarp();
+        }
+        leaf_bar(nthr);
+        // per digit: exclusive prefix over the warps (in place) and the digit total
+        for (uint32_t dg = tid; dg < 256; dg += nthr) {
+            uint32_t acc = 0;
+            for (uint32_t i = 0; i < W; ++i) {
+                const uint32_t c = cnt[256 * i + dg];
+                cnt[256 * i + dg] = (uint16_t)acc;
+                acc += c;
+            }
+            dtot[dg] = acc;
+        }
+        leaf_bar(nthr);
+        if (w == 0) {  // exclusive scan of the 256 digit totals, 8 per lane
+            uint32_t t8[8], sacc = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                t8[k] = sacc;
+                sacc += dtot[8 * lane + k];
+            }
+            uint32_t x = sacc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            const uint32_t ex = x - sacc;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) dbase[8 * lane + k] = ex + t8[k];
+        }
+        leaf_bar(nthr);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) buf[dbase[d[r]] + row[d[r]] + rk[r]] = v[r];
+        leaf_bar(nthr);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = buf[256 * w + 32 * r + lane];
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const uint32_t p = 256 * w + 32 * r + lane;
+        if (p < len) __stcs(keys + lo + p, v[r]);
     }
 }
 
@@ -565,6 +937,7 @@ struct QsGeom {
     uint64_t SMALL;     // segments in (LEAF, SMALL]: per-CTA recursion
     uint64_t BIG;       // segments >= BIG: full multi-CTA partition
     uint64_t G_TARGET;  // CTAs of one batched mid-level group launch
+    uint64_t HEAVY;     // mid segments >= HEAVY: batched multi-CTA cleanup (0 = off)
 };
 template <typename K>
 static QsGeom qs_geom() {
@@ -576,6 +949,7 @@ static QsGeom qs_geom() {
     q.LEAF = (P.leaf > 0 && (uint64_t)P.leaf <= (uint64_t)LC::LEAF) ? (uint64_t)P.leaf : (uint64_t)LC::LEAF;
     q.BIG = P.qs_cta_max > 0 ? (uint64_t)P.qs_cta_max : (uint64_t)1 << 25;
     q.SMALL = P.qs_small > 0 ? std::max<uint64_t>((uint64_t)P.qs_small, q.LEAF) : q.LEAF;
+    q.HEAVY = P.qs_heavy > 0 ? std::max<uint64_t>((uint64_t)P.qs_heavy, q.SMALL + 1) : 0;
     int occ = 1;
     cudaFuncSetAttribute(qs_group_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, qs_group_kernel<K>, C::NT, C::SMEM);
@@ -593,10 +967,15 @@ uint64_t quicksort_workspace_bound(uint64_t n) {
     const QsGeom q = qs_geom<K>();
     const uint64_t nmid = n / (q.SMALL + 1) + 1, nbig = n / q.BIG + 1;
     const uint64_t gtot = q.G_TARGET + 2 * nmid + 1;
-    const size_t level = al256(sizeof(QSeg) * nmid) + al256(sizeof(GroupOut) * gtot) + al256(8 * (nmid + nbig + 1));
+    const uint64_t nh = q.HEAVY ? n / q.HEAVY + 1 : 0;
+    const size_t level = al256(sizeof(QSeg) * nmid) + al256(sizeof(GroupOut) * gtot) + al256(8 * (nmid + nbig + 1)) +
+                         al256(4 * (nh + 1)) + hv_layout().stride * nh;
     const uint64_t cl = std::min<uint64_t>(n / 2 + 1, QS_LIST_CHUNK);
     const uint64_t cs = std::min<uint64_t>(n / (q.LEAF + 1) + 1, QS_LIST_CHUNK);
-    const size_t lists = al256(8 * cl) + al256(4 * cl) + al256(8 * cs) + al256(4 * cs) + al256(sizeof(GroupOut) * cs) + 256;
+    // bin slots of one chunk of small segments: sum of qs_bin_cap <= 2 n / LEAF + 6 per segment
+    const uint64_t nslot = std::min<uint64_t>(2 * (n / q.LEAF) + 6 * cs, cs * qs_bin_cap(q.SMALL, q.LEAF));
+    const size_t lists = al256(8 * cl) + al256(4 * cl) + al256(8 * cs) + al256(4 * cs) + al256(8 * cs) +
+                         al256(sizeof(GroupOut) * cs) + al256(8 * nslot) + al256(4 * nslot) + 256;
     return std::max(level, lists);
 }
 template uint64_t quicksort_workspace_bound<uint64_t>(uint64_t);
@@ -608,7 +987,8 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     using LC = LeafCfg<K>;
     const Params& P = params();
     const QsGeom geom = qs_geom<K>();
-    const uint64_t LEAF = geom.LEAF, BIG = geom.BIG, G_TARGET = geom.G_TARGET;
+    const uint64_t LEAF = geom.LEAF, BIG = geom.BIG, G_TARGET = geom.G_TARGET, HEAVY = geom.HEAVY;
+    const HvLayout HVL = hv_layout();
     const uint64_t MINL = 16;  // at least this many lines per group for mid segments
     const K KMAX = (K)~(K)0;
     g_qs_user_base = al256(partition_workspace_bound(n));
@@ -645,53 +1025,112 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     std::vector<size_t> order;  // cur index -> splits index
     cudaError_t e;
     cudaFuncSetAttribute(qs_group_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    static const bool lvl_prof = getenv("PP_QS_PROF") != nullptr;
+    cudaEvent_t lev[3];
+    if (lvl_prof)
+        for (auto& x : lev) cudaEventCreate(&x);
     while (!cur.empty()) {
         // ---- classify ----
         mids.clear();
         std::vector<size_t> big_idx, mid_idx;
         uint64_t gtot = 0;
-        // mid segments share one launch: give each a number of groups
-        // proportional to its length so that one wave of G_TARGET CTAs
-        // carries the level (small windows, balanced CTAs)
-        uint64_t mid_keys = 0;
-        for (size_t i = 0; i < cur.size(); ++i) {
-            const uint64_t len = cur[i].hi - cur[i].lo;
-            if (len < BIG) mid_keys += len;
-        }
+        // mid segments share one launch.  Every CTA should carry about the
+        // same number of lines: L* = (lines of all mid segments) / G_TARGET,
+        // a segment gets round(lines / L*) groups (>= 1, <= lines / MINL);
+        // the tasks are then ordered by lines per group, longest first, so the
+        // in-order CTA dispatch approximates longest-processing-time-first
+        // scheduling over the SMs' slots (balanced waves, no straggler wave).
+        std::vector<uint64_t> seg_nl;
+        uint64_t mid_lines = 0;
         for (size_t i = 0; i < cur.size(); ++i) {
             const uint64_t len = cur[i].hi - cur[i].lo;
             if (len >= BIG) {
                 big_idx.push_back(i);
-            } else {
-                mid_idx.push_back(i);
-                QSeg q;
-                q.lo = cur[i].lo;
-                q.hi = cur[i].hi;
-                q.pivot = cur[i].pivot;
-                q.mode = cur[i].mode;
-                q.pad = 0;
-                // lines of the aligned region (host mirror of seg_head)
-                const uint64_t addr = (uint64_t)(uintptr_t)(keys + q.lo);
-                uint64_t h = ((16 - (addr & 15)) & 15) / sizeof(K);
-                if (h > len) h = len;
-                const uint64_t nl = (len - h) / C::LK;
-                const uint64_t gp = (uint64_t)((double)len * (double)G_TARGET / (double)mid_keys + 0.5);
-                q.g = std::max<uint64_t>(1, std::min<uint64_t>(gp, nl / MINL));
+                continue;
+            }
+            mid_idx.push_back(i);
+            QSeg q;
+            q.lo = cur[i].lo;
+            q.hi = cur[i].hi;
+            q.pivot = cur[i].pivot;
+            q.mode = cur[i].mode;
+            q.pad = 0;
+            // lines of the aligned region (host mirror of seg_head)
+            const uint64_t addr = (uint64_t)(uintptr_t)(keys + q.lo);
+            uint64_t h = ((16 - (addr & 15)) & 15) / sizeof(K);
+            if (h > len) h = len;
+            const uint64_t nl = (len - h) / C::LK;
+            seg_nl.push_back(nl);
+            mid_lines += nl;
+            mids.push_back(q);
+        }
+        {
+            const double Lstar = std::max(1.0, (double)mid_lines / (double)G_TARGET);
+            for (size_t i = 0; i < mids.size(); ++i) {
+                const uint64_t cap = std::max<uint64_t>(1, seg_nl[i] / MINL);
+                const uint64_t want = (uint64_t)((double)seg_nl[i] / Lstar + 0.5);
+                mids[i].g = std::max<uint64_t>(1, std::min<uint64_t>(cap, want));
+                gtot += mids[i].g;
+            }
+            // a few CTAs past a whole number of waves would run as a straggler
+            // wave: take them back from the segments with the most groups
+            const uint64_t slots = G_TARGET / (uint64_t)std::max<int64_t>(P.qs_waves, 1);
+            uint64_t excess = gtot > slots ? gtot % slots : 0;
+            if (excess > 0 && excess <= slots / 16) {
+                std::vector<size_t> byg(mids.size());
+                for (size_t i = 0; i < byg.size(); ++i) byg[i] = i;
+                std::stable_sort(byg.begin(), byg.end(), [&](size_t x, size_t y) { return mids[x].g > mids[y].g; });
+                for (bool any = true; excess > 0 && any;) {  // round robin, most groups first
+                    any = false;
+                    for (size_t k : byg) {
+                        if (excess == 0) break;
+                        if (mids[k].g > 1) {
+                            --mids[k].g;
+                            --excess;
+                            any = true;
+                        }
+                    }
+                }
+            }
+            gtot = 0;
+            std::vector<size_t> ord(mids.size());
+            for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+            std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) {
+                return seg_nl[x] * mids[y].g > seg_nl[y] * mids[x].g;  // lines per group, descending
+            });
+            std::vector<QSeg> m2;
+            std::vector<size_t> i2;
+            m2.reserve(mids.size());
+            for (size_t k : ord) {
+                m2.push_back(mids[k]);
+                i2.push_back(mid_idx[k]);
+            }
+            mids.swap(m2);
+            mid_idx.swap(i2);
+            for (QSeg& q : mids) {
                 q.gbase = gtot;
                 gtot += q.g;
-                mids.push_back(q);
             }
         }
         const uint64_t nmid = mids.size(), nbig = big_idx.size();
-        // ---- workspace: [segs][gout][splits] ----
-        const size_t segB = ((sizeof(QSeg) * std::max<uint64_t>(nmid, 1)) + 255) & ~size_t(255);
-        const size_t goB = ((sizeof(GroupOut) * std::max<uint64_t>(gtot, 1)) + 255) & ~size_t(255);
-        const size_t spB = ((8 * (nmid + nbig + 1)) + 255) & ~size_t(255);
-        unsigned char* ws = static_cast<unsigned char*>(qs_workspace(segB + goB + spB));
+        // heavy mid segments: batched multi-CTA cleanup
+        std::vector<uint32_t> hidx;
+        for (size_t mi = 0; mi < mids.size(); ++mi)
+            if (HEAVY && mids[mi].hi - mids[mi].lo >= HEAVY) hidx.push_back((uint32_t)mi);
+        const uint64_t nh = hidx.size();
+        // ---- workspace: [segs][gout][splits][heavy index][heavy blocks] ----
+        const size_t segB = al256(sizeof(QSeg) * std::max<uint64_t>(nmid, 1));
+        const size_t goB = al256(sizeof(GroupOut) * std::max<uint64_t>(gtot, 1));
+        const size_t spB = al256(8 * (nmid + nbig + 1));
+        const size_t hiB = al256(4 * std::max<uint64_t>(nh, 1));
+        const size_t hvB = HVL.stride * nh;
+        unsigned char* ws = static_cast<unsigned char*>(qs_workspace(segB + goB + spB + hiB + hvB));
         if (!ws) return PP_E_NOMEM;
         QSeg* d_segs = reinterpret_cast<QSeg*>(ws);
         GroupOut* d_gout = reinterpret_cast<GroupOut*>(ws + segB);
         uint64_t* d_splits = reinterpret_cast<uint64_t*>(ws + segB + goB);
+        uint32_t* d_hidx = reinterpret_cast<uint32_t*>(ws + segB + goB + spB);
+        unsigned char* d_hv = ws + segB + goB + spB + hiB;
 
         // ---- big segments: full multi-CTA partition, one at a time ----
         pivots_h.assign(cur.size(), 0);
@@ -722,8 +1161,36 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             e = cudaMemcpyAsync(d_segs, mids.data(), sizeof(QSeg) * nmid, cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort H2D");
             qs_pivot_kernel<K><<<(unsigned)((nmid + 255) / 256), 256, 0, st>>>(keys, d_segs, nmid);
+            if (lvl_prof) cudaEventRecord(lev[0], st);
             qs_group_kernel<K><<<(unsigned)gtot, C::NT, C::SMEM, st>>>(keys, d_segs, nmid, P.seed, d_gout);
-            qs_cleanup_kernel<K><<<(unsigned)nmid, SW_NT, 0, st>>>(keys, d_segs, d_gout, d_splits);
+            if (lvl_prof) cudaEventRecord(lev[1], st);
+            if (nh > 0) {
+                e = cudaMemcpyAsync(d_hidx, hidx.data(), 4 * nh, cudaMemcpyHostToDevice, st);
+                if (e != cudaSuccess) return cuda_fail(e, "quicksort H2D");
+                const unsigned X = (unsigned)std::min<uint64_t>(
+                    2 * QS_HEAVY_TILES, std::max<uint64_t>(2, ((uint64_t)sm_count() * 4 + nh - 1) / nh));
+                const dim3 grid(X, (unsigned)nh);
+                qs_hv_reduce_kernel<K><<<grid, 256, 0, st>>>(keys, d_segs, d_hidx, d_gout, d_splits, d_hv, HVL);
+                qs_hv_scan_kernel<<<(unsigned)nh, 1024, 2 * 8 * (QS_HEAVY_TILES + 1), st>>>(d_hv, HVL);
+                qs_hv_locate_kernel<K><<<grid, SW_NT, 0, st>>>(keys, d_segs, d_hidx, d_hv, HVL);
+                qs_hv_swap_kernel<K><<<grid, SW_NT, 0, st>>>(keys, d_segs, d_hidx, d_hv, HVL);
+                note_launches(4);
+            }
+            if (nh == nmid) {
+                // every mid segment was heavy
+            } else if (nmid <= (uint64_t)sm_count()) {
+                // few (large) segments, long walks: 512-thread CTAs, 4096 keys per side per round trip
+                constexpr int NT = 512, EPT = 8;
+                const size_t sm = sizeof(StreamBuf<NT, EPT>);
+                cudaFuncSetAttribute(qs_cleanup_kernel<K, NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sm);
+                qs_cleanup_kernel<K, NT, EPT><<<(unsigned)nmid, NT, sm, st>>>(keys, d_segs, d_gout, d_splits, HEAVY);
+            } else {
+                const size_t sm = sizeof(StreamBuf<SW_NT, SW_EPT2>);
+                qs_cleanup_kernel<K, SW_NT, SW_EPT2><<<(unsigned)nmid, SW_NT, sm, st>>>(keys, d_segs, d_gout,
+                                                                                         d_splits, HEAVY);
+            }
+            if (lvl_prof) cudaEventRecord(lev[2], st);
             note_launches(3);
             e = cudaGetLastError();
             if (e != cudaSuccess) return cuda_fail(e, "quicksort mid launch");
@@ -741,6 +1208,16 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return cuda_fail(e, "quicksort level");
         for (size_t mi = 0; mi < nmid; ++mi) pivots_h[mid_idx[mi]] = mids[mi].pivot;
+        if (lvl_prof && nmid > 0) {  // debug: per-level times of the batched mid pass
+            float tg = 0, tc = 0;
+            cudaEventElapsedTime(&tg, lev[0], lev[1]);
+            cudaEventElapsedTime(&tc, lev[1], lev[2]);
+            uint64_t mk = 0, mx = 0;
+            for (const QSeg& q : mids) { mk += q.hi - q.lo; mx = std::max<uint64_t>(mx, q.hi - q.lo); }
+            fprintf(stderr, "qs level: nmid=%llu nbig=%llu gtot=%llu keys=%llu maxseg=%llu group=%.3f ms (%.2f TB/s) cleanup=%.3f ms\n",
+                    (unsigned long long)nmid, (unsigned long long)nbig, (unsigned long long)gtot,
+                    (unsigned long long)mk, (unsigned long long)mx, tg, 16.0 * mk / (tg * 1e9), tc);
+        }
         // ---- next level ----
         next.clear();
         auto visit = [&](const HSeg& s, uint64_t p, uint64_t k) {
@@ -760,37 +1237,113 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         for (size_t bi = 0; bi < nbig; ++bi) visit(cur[big_idx[bi]], pivots_h[big_idx[bi]], splits_h[nmid + bi]);
         cur.swap(next);
     }
-    // ---- small segments (one CTA each) and leaves: one workspace, lists
-    // uploaded in chunks of QS_LIST_CHUNK (stream order makes reuse safe) ----
+    // ---- small segments (one CTA each: recursion down to leaves, packed into
+    //      bins) and leaves (sorted in shared memory, one CTA per bin); lists
+    //      uploaded in chunks of QS_LIST_CHUNK (stream order makes reuse safe) ----
     const uint64_t nleaf = leaf_lo.size(), nsmall = small_lo.size();
     const uint64_t cl = std::min<uint64_t>(nleaf, QS_LIST_CHUNK), cs = std::min<uint64_t>(nsmall, QS_LIST_CHUNK);
+    std::vector<uint64_t> small_base(nsmall + 1, 0);
+    uint64_t max_slots = 0;
+    for (uint64_t b0 = 0; b0 < nsmall; b0 += QS_LIST_CHUNK) {
+        const uint64_t cnt = std::min<uint64_t>(nsmall - b0, QS_LIST_CHUNK);
+        uint64_t acc = 0;
+        for (uint64_t i = 0; i < cnt; ++i) {
+            small_base[b0 + i] = acc;
+            acc += qs_bin_cap(small_len[b0 + i], LEAF);
+        }
+        max_slots = std::max(max_slots, acc);
+    }
     const size_t loB = al256(8 * cl), lnB = al256(4 * cl), sloB = al256(8 * cs), slnB = al256(4 * cs);
-    const size_t scrB = al256(sizeof(GroupOut) * cs);
-    unsigned char* qws = static_cast<unsigned char*>(qs_workspace(loB + lnB + sloB + slnB + scrB + 256));
+    const size_t sbB = al256(8 * cs), scrB = al256(sizeof(GroupOut) * cs);
+    const size_t bloB = al256(8 * max_slots), blnB = al256(4 * max_slots);
+    unsigned char* qws =
+        static_cast<unsigned char*>(qs_workspace(loB + lnB + sloB + slnB + sbB + scrB + bloB + blnB + 256));
     if (!qws) return PP_E_NOMEM;
+    // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot
+    auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt) -> cudaError_t {
+        const int64_t algo = P.leaf_algo == 0 ? 3 : P.leaf_algo;  // default: merge sort
+        if (algo == 2) {
+            constexpr int NW = LC::LEAF / 256;
+            const size_t smem = sizeof(K) * LC::LEAF + 2 * 256 * NW;
+            cudaFuncSetAttribute(qs_leaf_radix_kernel<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_radix_kernel<K, NW><<<(unsigned)cnt, NW * 32, smem, st>>>(keys, d_lo, d_len);
+        } else if (algo == 1) {
+            const size_t smem = sizeof(K) * LC::LEAF;
+            cudaFuncSetAttribute(qs_leaf_kernel<K, LC::LEAF, LC::NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo, d_len);
+        } else if (LEAF <= (uint64_t)LC::LEAF / 4) {  // small bins: quarter-size CTAs, more per SM
+            constexpr int QL = LC::LEAF / 4, QN = QL / LEAF_E;
+            const size_t smem = sizeof(K) * (QL + QL / 8);
+            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, QL, QN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            qs_leaf_merge_kernel<K, QL, QN><<<(unsigned)cnt, QN, smem, st>>>(keys, d_lo, d_len);
+        } else if (LEAF <= (uint64_t)LC::LEAF / 2) {  // half-size CTAs
+            constexpr int HL = LC::LEAF / 2, HN = HL / LEAF_E;
+            const size_t smem = sizeof(K) * (HL + HL / 8);
+            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, st>>>(keys, d_lo, d_len);
+        } else {
+            const size_t smem = sizeof(K) * (LC::LEAF + LC::LEAF / 8);
+            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, LC::LEAF, LC::NT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo, d_len);
+        }
+        note_launches(1);
+        return cudaGetLastError();
+    };
     if (nsmall > 0) {
-        uint64_t* d_slo = reinterpret_cast<uint64_t*>(qws + loB + lnB);
-        uint32_t* d_sln = reinterpret_cast<uint32_t*>(qws + loB + lnB + sloB);
-        GroupOut* d_scr = reinterpret_cast<GroupOut*>(qws + loB + lnB + sloB + slnB);
+        unsigned char* w = qws + loB + lnB;
+        uint64_t* d_slo = reinterpret_cast<uint64_t*>(w);
+        uint32_t* d_sln = reinterpret_cast<uint32_t*>(w + sloB);
+        uint64_t* d_sbase = reinterpret_cast<uint64_t*>(w + sloB + slnB);
+        GroupOut* d_scr = reinterpret_cast<GroupOut*>(w + sloB + slnB + sbB);
+        uint64_t* d_blo = reinterpret_cast<uint64_t*>(w + sloB + slnB + sbB + scrB);
+        uint32_t* d_bln = reinterpret_cast<uint32_t*>(w + sloB + slnB + sbB + scrB + bloB);
+        uint64_t* d_prof = nullptr;  // debug phase profile (env PP_QS_PROF)
+        static const bool qs_prof = getenv("PP_QS_PROF") != nullptr;
+        if (qs_prof) cudaMalloc(&d_prof, 64 * cs);
         for (uint64_t b0 = 0; b0 < nsmall; b0 += QS_LIST_CHUNK) {
             const uint64_t cnt = std::min<uint64_t>(nsmall - b0, QS_LIST_CHUNK);
+            const uint64_t nslots = small_base[b0 + cnt - 1] + qs_bin_cap(small_len[b0 + cnt - 1], LEAF);
             e = cudaMemcpyAsync(d_slo, small_lo.data() + b0, 8 * cnt, cudaMemcpyHostToDevice, st);
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(d_sln, small_len.data() + b0, 4 * cnt, cudaMemcpyHostToDevice, st);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(d_sbase, small_base.data() + b0, 8 * cnt, cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort small H2D");
             if (P.qs_small_cfg == 0) {
                 using S = SmallCfg<K, 0>;
                 cudaFuncSetAttribute(qs_small_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-                qs_small_kernel<K, 0><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(keys, d_slo, d_sln, P.seed, d_scr);
+                qs_small_kernel<K, 0><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(
+                    keys, d_slo, d_sln, d_sbase, d_blo, d_bln, (uint32_t)LEAF, P.seed, d_scr, d_prof);
             } else {
                 using S = SmallCfg<K, 1>;
                 cudaFuncSetAttribute(qs_small_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-                qs_small_kernel<K, 1><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(keys, d_slo, d_sln, P.seed, d_scr);
+                qs_small_kernel<K, 1><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(
+                    keys, d_slo, d_sln, d_sbase, d_blo, d_bln, (uint32_t)LEAF, P.seed, d_scr, d_prof);
             }
             note_launches(1);
             e = cudaGetLastError();
             if (e != cudaSuccess) return cuda_fail(e, "quicksort small launch");
+            if (d_prof) {
+                std::vector<uint64_t> h(8 * cnt);
+                cudaMemcpy(h.data(), d_prof, 64 * cnt, cudaMemcpyDeviceToHost);
+                uint64_t tot[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (uint64_t i = 0; i < cnt; ++i)
+                    for (int j = 0; j < 8; ++j) tot[j] += h[8 * i + j];
+                fprintf(stderr,
+                        "qs_small prof: ctas=%llu slots=%llu cycles pivot=%.3g part=%.3g (walk=%.3g) merge=%.3g; "
+                        "partitions=%llu merges=%llu part_keys=%llu merge_keys=%llu\n",
+                        (unsigned long long)cnt, (unsigned long long)nslots, (double)tot[0], (double)tot[1],
+                        (double)tot[3], (double)tot[2], (unsigned long long)tot[4], (unsigned long long)tot[5],
+                        (unsigned long long)tot[6], (unsigned long long)tot[7]);
+            }
+            e = sort_bins(d_blo, d_bln, nslots);
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort bin sort launch");
         }
+        if (d_prof) cudaFree(d_prof);
     }
     if (nleaf > 0) {
         uint64_t* d_lo = reinterpret_cast<uint64_t*>(qws);
@@ -800,25 +1353,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             e = cudaMemcpyAsync(d_lo, leaf_lo.data() + b0, 8 * cnt, cudaMemcpyHostToDevice, st);
             if (e == cudaSuccess) e = cudaMemcpyAsync(d_len, leaf_len.data() + b0, 4 * cnt, cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort leaves H2D");
-            if (P.leaf_algo == 1) {
-                const size_t smem = sizeof(K) * LC::LEAF;
-                cudaFuncSetAttribute(qs_leaf_kernel<K, LC::LEAF, LC::NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-                qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo, d_len);
-            } else if (LEAF <= (uint64_t)LC::LEAF / 2) {  // small leaves: half-size CTAs, more per SM
-                constexpr int HL = LC::LEAF / 2, HN = HL / LEAF_E;
-                const size_t smem = 2 * sizeof(K) * (HL + HL / 8);
-                cudaFuncSetAttribute(qs_leaf_merge_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-                qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, st>>>(keys, d_lo, d_len);
-            } else {
-                const size_t smem = 2 * sizeof(K) * (LC::LEAF + LC::LEAF / 8);
-                cudaFuncSetAttribute(qs_leaf_merge_kernel<K, LC::LEAF, LC::NT>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo, d_len);
-            }
-            note_launches(1);
-            e = cudaGetLastError();
+            e = sort_bins(d_lo, d_len, cnt);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort leaf launch");
         }
     }

@@ -76,11 +76,13 @@ def test_medium_sizes(pp, dt, mx):
 
 
 @pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
-@pytest.mark.parametrize("params", [{"leaf_algo": 1}, {"leaf_algo": 0, "leaf": 300}, {"qs_waves": 1},
-                                    {"qs_waves": 16, "leaf": 1000}])
+@pytest.mark.parametrize("params", [{"leaf_algo": 1}, {"leaf_algo": 3}, {"leaf_algo": 3, "leaf": 300},
+                                    {"leaf_algo": 2, "leaf": 300}, {"qs_waves": 1}, {"qs_waves": 16, "leaf": 1000},
+                                    {"qs_heavy": 1 << 17}, {"qs_heavy": 0}, {"qs_small": 0}, {"strided": 1}])
 def test_qs_parameters(pp, dt, mx, params):
-    """Leaf algorithms (merge / bitonic), leaf sizes and level balancing all
-    give the oracle's sorted output."""
+    """Bin sorts (radix / merge / bitonic), leaf sizes, level balancing, the
+    heavy-segment batched cleanup, the per-CTA recursion and the Strided
+    offsets all give the oracle's sorted output."""
     rng = np.random.default_rng(4)
     for n in (5000, 300_007):
         for a in list(_cases(dt, mx, n, rng))[:3]:
