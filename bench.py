@@ -354,7 +354,7 @@ def e2e(pp, n, args):
         times.append(time.perf_counter() - t0)
     v = n * steps / sum(times)
     return {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 8,
-            "steps": steps, "ms_per_step": 1e3 * sum(times) / steps, "api": "pp_partition_host_u64 (pinned host)",
+            "steps": steps, "ms_per_step": 1e3 * sum(times) / steps, "api": "pp_partition_host_u64 (pinned host; streamed chunks: H2D from both ends, per-chunk GPU partition, D2H of each side overlapping the uploads)",
             "timing": "host wall clock around the synchronous call"}
 
 
@@ -382,7 +382,32 @@ def extras(pp, torch, synth, dev, stream, flush):
         st = pp.pp_last_stats()
         res[f"partition_mu{mu}"] = {"keys_per_s": n / (ms / 1e3), "ms": ms,
                                     "gbs": 16 * n / (ms / 1e3) / 1e9, "window_frac": st["W"] / n}
-    del pristine, buf
+    # Strided (X = 0) vs Smoothed Striding
+    # (random X) on the c2 input and on the stride-aligned
+    # adversary (line j true iff j mod g < g/2, g = the library's group count)
+    st0 = pp.pp_last_stats()
+    adv = synth.stride_aligned_u64_torch(n, synth.SEEDS["c2"], st0["line_keys"], st0["g"], dev)
+    abl = {}
+    for name, src in (("uniform", pristine), ("stride_aligned", adv)):
+        for strided in (0, 1):
+            pp.pp_set_param("strided", strided)
+            ts = []
+            for i in range(6):
+                buf.copy_(src)
+                flush.sum()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                pp.pp_partition_async_u64(buf, PIVOT, d)
+                e.record(stream)
+                torch.cuda.synchronize()
+                if i >= 2:
+                    ts.append(s.elapsed_time(e))
+            ms = statistics.mean(ts)
+            abl[f"{name}_{'strided' if strided else 'smoothed'}"] = {
+                "ms": ms, "gbs": 16 * n / (ms / 1e3) / 1e9, "window_frac": pp.pp_last_stats()["W"] / n}
+    pp.pp_set_param("strided", 0)
+    res["ablation_strided_vs_smoothed"] = abl
+    del pristine, buf, adv
     nq = 1 << 28
     for kind in ("uniform", "dup1000"):
         if kind == "uniform":

@@ -75,9 +75,18 @@ pp_status pp_quicksort_u32(uint32_t *keys, uint64_t n, void *stream);
 
 /* ---- host-buffer (end-to-end) variants ------------------------------------
  * host_keys: HOST pointer (pinned or pageable) to n keys, partitioned / sorted
- * in place: copied to a library-owned device buffer, processed, copied back.
- * These are what an application with host-resident data calls; bench.py's
- * "e2e" number times them (H2D + kernels + D2H). */
+ * in place through a library-owned device buffer.  These are what an
+ * application with host-resident data calls; bench.py's "e2e" number times
+ * them (H2D + kernels + D2H).  pp_partition_host_* streams: chunks of
+ * "host_chunk" keys (param, default 2^22) are uploaded alternately from the
+ * front and the back, each is partitioned on the device as it lands, and its
+ * keys < pivot are copied back to the front of host_keys, the others to the
+ * back, as soon as those host positions have been uploaded -- downloads
+ * overlap uploads.  The result satisfies the partition contract (keys <
+ * pivot in [0, split), the rest after); the arrangement within each side is
+ * chunk order (any arrangement is a correct output).
+ * pp_quicksort_host_u64: H2D, sort, D2H.  Synchronous; PP_E_NOMEM if the
+ * device buffer cannot be allocated. */
 pp_status pp_partition_host_u64(uint64_t *host_keys, uint64_t n, uint64_t pivot, uint64_t *split_out);
 pp_status pp_partition_host_u32(uint32_t *host_keys, uint64_t n, uint32_t pivot, uint64_t *split_out);
 pp_status pp_quicksort_host_u64(uint64_t *host_keys, uint64_t n);

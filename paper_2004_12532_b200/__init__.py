@@ -29,7 +29,8 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
-LIB_PATH = os.path.join(_PKG, "libpp.so")
+# PP_LIB_PATH: load another build of the library (A/B timing in tools/ only)
+LIB_PATH = os.environ.get("PP_LIB_PATH") or os.path.join(_PKG, "libpp.so")
 HEADER = os.path.join(_ROOT, "include", "pp.h")
 
 PP_OK = 0

@@ -5,6 +5,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "pp_internal.h"
 
@@ -197,6 +199,25 @@ static void* host_device_buffer(size_t bytes) {
     return g_hbuf;
 }
 
+// Host-buffer partition with the transfers streamed.  A
+// partition's arrangement within each side is free, so the
+// host result is built chunk by chunk: chunks of C keys are uploaded
+// alternately from the front and the back of the array (copy engine 1), each
+// is partitioned in place on the device as soon as it lands (the full GPU
+// partition, one launch chain per chunk), and its predecessors are written
+// back to the host front [T, T + t_c), its successors to the host back
+// [n - F - f_c, n - F) (copy engine 2), each as soon as every host position
+// of its destination has been uploaded (its original key is on the device).
+// Uploading from both ends keeps both destination frontiers covered, so the
+// downloads overlap the uploads on the full-duplex link.  Result: keys < pivot
+// in [0, K), the rest in [K, n); the split K is returned.
+static cudaStream_t g_hs_up = nullptr, g_hs_dn = nullptr;
+static std::vector<cudaEvent_t> g_hs_ev_up, g_hs_ev_part;
+static uint64_t* g_hs_splits = nullptr;  // pinned, one per chunk
+static size_t g_hs_nsplit = 0;
+static uint64_t* g_hs_dsplit = nullptr;  // device, one per chunk
+static size_t g_hs_ndsplit = 0;
+
 template <typename K>
 static pp_status partition_host(K* host_keys, uint64_t n, K pivot, uint64_t* split_out) {
     if (!split_out || (n > 0 && !host_keys)) {
@@ -207,25 +228,96 @@ static pp_status partition_host(K* host_keys, uint64_t n, K pivot, uint64_t* spl
         *split_out = 0;
         return PP_OK;
     }
-    K* d;
-    {
-        std::lock_guard<std::mutex> lk(g_mu);
-        d = static_cast<K*>(host_device_buffer(n * sizeof(K)));
-        if (!d) {
-            set_error("device buffer allocation failed");
+    std::lock_guard<std::mutex> lk(g_mu);
+    K* d = static_cast<K*>(host_device_buffer(n * sizeof(K)));
+    if (!d) {
+        set_error("device buffer allocation failed");
+        return PP_E_NOMEM;
+    }
+    if (!g_hs_up) {
+        cudaStreamCreateWithFlags(&g_hs_up, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&g_hs_dn, cudaStreamNonBlocking);
+    }
+    const uint64_t C = (uint64_t)std::max<int64_t>(g_params.host_chunk, 1 << 12);
+    const uint64_t nch = (n + C - 1) / C;
+    auto clen = [&](uint64_t c) { return std::min<uint64_t>(C, n - c * C); };
+    while (g_hs_ev_up.size() < nch) {
+        cudaEvent_t a, b;
+        cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+        g_hs_ev_up.push_back(a);
+        g_hs_ev_part.push_back(b);
+    }
+    if (g_hs_nsplit < nch) {
+        if (g_hs_splits) cudaFreeHost(g_hs_splits);
+        g_hs_splits = nullptr;
+        g_hs_nsplit = 0;
+        if (cudaMallocHost(&g_hs_splits, 8 * nch) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("pinned split buffer allocation failed");
             return PP_E_NOMEM;
         }
-        cudaError_t e = cudaMemcpyAsync(d, host_keys, n * sizeof(K), cudaMemcpyHostToDevice, g_hstream);
-        if (e != cudaSuccess) return cuda_fail(e, "H2D");
+        g_hs_nsplit = nch;
     }
-    uint64_t split = 0;
-    pp_status s = partition_sync<K>(d, n, pivot, g_hstream, &split);
-    if (s != PP_OK) return s;
-    std::lock_guard<std::mutex> lk(g_mu);
-    cudaError_t e = cudaMemcpyAsync(host_keys, d, n * sizeof(K), cudaMemcpyDeviceToHost, g_hstream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(g_hstream);
-    if (e != cudaSuccess) return cuda_fail(e, "D2H");
-    *split_out = split;
+    if (g_hs_ndsplit < nch) {
+        cudaStreamSynchronize(g_hstream);
+        if (g_hs_dsplit) cudaFree(g_hs_dsplit);
+        g_hs_dsplit = nullptr;
+        g_hs_ndsplit = 0;
+        if (cudaMalloc(&g_hs_dsplit, 8 * nch) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("device split buffer allocation failed");
+            return PP_E_NOMEM;
+        }
+        g_hs_ndsplit = nch;
+    }
+    // upload order: front, back, front, back, ...; seq[c] = position in it
+    std::vector<uint64_t> order(nch), seq(nch);
+    for (uint64_t k = 0, f = 0, b = nch; k < nch; ++k) {
+        const uint64_t c = (k % 2 == 0) ? f++ : --b;
+        order[k] = c;
+        seq[c] = k;
+    }
+    cudaError_t e = cudaSuccess;
+    for (uint64_t k = 0; k < nch && e == cudaSuccess; ++k) {
+        const uint64_t c = order[k];
+        e = cudaMemcpyAsync(d + c * C, host_keys + c * C, clen(c) * sizeof(K), cudaMemcpyHostToDevice, g_hs_up);
+        if (e == cudaSuccess) e = cudaEventRecord(g_hs_ev_up[c], g_hs_up);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(g_hstream, g_hs_ev_up[c], 0);
+        if (e != cudaSuccess) break;
+        const pp_status ps = partition_device<K>(d + c * C, clen(c), pivot, g_hstream, g_hs_dsplit + c, nullptr);
+        if (ps != PP_OK) return ps;
+        e = cudaMemcpyAsync(g_hs_splits + c, g_hs_dsplit + c, 8, cudaMemcpyDeviceToHost, g_hstream);
+        if (e == cudaSuccess) e = cudaEventRecord(g_hs_ev_part[c], g_hstream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "streamed partition enqueue");
+    // downloads, in upload order; a destination range waits for the upload
+    // of every chunk it overlaps (uploads complete in order: the latest one)
+    uint64_t T = 0, F = 0;
+    auto download = [&](uint64_t c, uint64_t src_off, uint64_t len, uint64_t dst) -> cudaError_t {
+        if (len == 0) return cudaSuccess;
+        uint64_t last = 0;
+        for (uint64_t j = dst / C; j <= (dst + len - 1) / C; ++j) last = std::max(last, seq[j]);
+        cudaError_t r = cudaStreamWaitEvent(g_hs_dn, g_hs_ev_up[order[last]], 0);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(g_hs_dn, g_hs_ev_part[c], 0);
+        if (r == cudaSuccess)
+            r = cudaMemcpyAsync(host_keys + dst, d + c * C + src_off, len * sizeof(K), cudaMemcpyDeviceToHost,
+                                g_hs_dn);
+        return r;
+    };
+    for (uint64_t k = 0; k < nch && e == cudaSuccess; ++k) {
+        const uint64_t c = order[k];
+        e = cudaEventSynchronize(g_hs_ev_part[c]);
+        if (e != cudaSuccess) break;
+        const uint64_t t = g_hs_splits[c], f = clen(c) - t;
+        e = download(c, 0, t, T);
+        if (e == cudaSuccess) e = download(c, t, f, n - F - f);
+        T += t;
+        F += f;
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g_hs_dn);
+    if (e != cudaSuccess) return cuda_fail(e, "streamed partition");
+    *split_out = T;
     return PP_OK;
 }
 
@@ -438,6 +530,7 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "fused_stop") P.fused_stop = value;
     else if (k == "qs_waves") P.qs_waves = value;
     else if (k == "qs_heavy") P.qs_heavy = value;
+    else if (k == "host_chunk") P.host_chunk = value;
     else {
         set_error("unknown parameter " + k);
         return PP_E_INVAL;
@@ -467,6 +560,7 @@ int64_t pp_get_param(const char* name) {
     if (k == "fused_stop") return P.fused_stop;
     if (k == "qs_waves") return P.qs_waves;
     if (k == "qs_heavy") return P.qs_heavy;
+    if (k == "host_chunk") return P.host_chunk;
     return INT64_MIN;
 }
 

@@ -27,10 +27,7 @@ __host__ __device__ __forceinline__ uint64_t ss_fmix(uint64_t z) {
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
     return z ^ (z >> 31);
 }
-// seed == 0 is reserved for the Strided Algorithm (X[j] = 0 for every chunk,
-// PAPER.md:796-825, §4 "The Strided Algorithm"): the SURVEY §8(f) ablation.
 __host__ __device__ __forceinline__ uint32_t ss_offset(uint64_t seed, uint64_t j, uint32_t g) {
-    if (seed == 0) return 0;
     uint64_t h = ss_fmix(seed + (j + 1) * 0x9E3779B97F4A7C15ULL);
     return (uint32_t)(((h >> 32) * (uint64_t)g) >> 32);
 }

@@ -9,10 +9,14 @@ namespace pp {
 // LINE_BYTES = b * sizeof(K) (the paper's cache line of b elements,
 // PAPER.md:747, 814-816; b = 512 elements there).
 // NT threads; PF lines in flight per end; TMA_STORE: resolved lines leave
-// shared memory through the bulk-copy engine instead of thread stores.
-template <typename K, int LINE_BYTES, int NT_, int PF_, bool TMA_STORE_>
+// shared memory through the bulk-copy engine instead of thread stores;
+// STRIDED: X[j] = 0 for every chunk, the Strided Algorithm (PAPER.md:796-825,
+// the SURVEY §8(f) ablation) -- a separate instantiation, so the default
+// engine carries no branch for it.
+template <typename K, int LINE_BYTES, int NT_, int PF_, bool TMA_STORE_, bool STRIDED_ = false>
 struct GroupCfgT {
     using Key = K;
+    static constexpr bool STRIDED = STRIDED_;
     static constexpr int LK = LINE_BYTES / (int)sizeof(K);
     static constexpr int NT = NT_;
     static constexpr int PF = PF_;
@@ -38,7 +42,9 @@ using GroupCfg = GroupCfgT<K, sizeof(K) == 8 ? 8192 : 4096, 128, 4, false>;
 
 // Line index of the j-th line (group order) of group gi: G_i(j) of
 // PAPER.md:963-969 in 0-based form, j*g + ((X[j] + i) mod g).
+template <bool STRIDED = false>
 __device__ __forceinline__ uint64_t group_line(uint64_t seed, uint32_t g, uint32_t gi, uint32_t j) {
+    if (STRIDED) return (uint64_t)j * g + gi;
     uint32_t x = ss_offset(seed, (uint64_t)j, g) + gi;
     if (x >= g) x -= g;
     return (uint64_t)j * g + x;
@@ -109,7 +115,7 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
     // number of lines of this group: s-1 full chunks + the last chunk's line if it exists
     const uint32_t s = (uint32_t)((n_lines + g - 1) / g);
     int S = 0;
-    if (s > 0) S = (int)s - 1 + (group_line(seed, g, gi, s - 1) < n_lines ? 1 : 0);
+    if (s > 0) S = (int)s - 1 + (group_line<C::STRIDED>(seed, g, gi, s - 1) < n_lines ? 1 : 0);
 
     if (tid == 0) {
         for (int k = 0; k < 2 * PF; ++k) mbar_init(&bars[k], 1);
@@ -126,7 +132,7 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
 
     // thread 0 only: issue the load of group line j into ring slot bi
     auto issue = [&](uint32_t bi, int j) {
-        const uint32_t line = (uint32_t)group_line(seed, g, gi, (uint32_t)j);
+        const uint32_t line = (uint32_t)group_line<C::STRIDED>(seed, g, gi, (uint32_t)j);
         slot_line[bi] = line;
         mbar_expect_tx(&bars[bi], LBYTES);
         bulk_g2s(ring + bi * LK, region + (uint64_t)line * LK, LBYTES, &bars[bi]);
@@ -288,9 +294,9 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
             o.vlo = n_lines * LK;
             o.vhi = 0;
         } else if (T == (uint64_t)S * LK) {
-            o.vlo = o.vhi = group_line(seed, g, gi, (uint32_t)(S - 1)) * LK + LK;
+            o.vlo = o.vhi = group_line<C::STRIDED>(seed, g, gi, (uint32_t)(S - 1)) * LK + LK;
         } else {
-            o.vlo = o.vhi = group_line(seed, g, gi, (uint32_t)(T / LK)) * LK + T % LK;
+            o.vlo = o.vhi = group_line<C::STRIDED>(seed, g, gi, (uint32_t)(T / LK)) * LK + T % LK;
         }
         *out = o;
     }

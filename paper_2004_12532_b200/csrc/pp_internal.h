@@ -51,6 +51,7 @@ struct Params {
     int64_t qs_waves = 2;          // quicksort mid levels: target CTA waves of the group launch
     int64_t qs_small = 1 << 16;    // quicksort: segments <= this finish in one CTA (0 = off)
     int64_t qs_small_cfg = 1;      // quicksort: per-CTA recursion config (pp_quicksort.cu SmallCfg)
+    int64_t host_chunk = 1 << 22;  // host-buffer partition: keys per streamed chunk
     int64_t qs_heavy = 1 << 21;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
 };
 Params& params();

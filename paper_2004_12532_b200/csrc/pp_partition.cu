@@ -516,7 +516,14 @@ template <typename K> struct VariantCfg<K, 3> { using type = GroupCfgT<K, 8192, 
 template <typename K> struct VariantCfg<K, 4> { using type = GroupCfgT<K, 8192, 128, 3, false>; };
 template <typename K> struct VariantCfg<K, 5> { using type = GroupCfgT<K, 4096, 64, 6, false>; };
 template <typename K> struct VariantCfg<K, 6> { using type = GroupCfgT<K, 8192, 128, 4, true>; };
+// 7: the default configuration with X = 0 (Strided Algorithm), selected by
+// the "strided" param (seed 0), not by "variant"
+template <typename K> struct VariantCfg<K, 7> {
+    using D = GroupCfg<K>;
+    using type = GroupCfgT<K, D::LK * (int)sizeof(K), D::NT, D::PF, D::TMA_STORE, true>;
+};
 constexpr int N_VARIANTS = 7;
+constexpr int STRIDED_VARIANT = 7;
 
 template <typename K, int V>
 static VariantInfo variant_info_t() {
@@ -532,6 +539,7 @@ static VariantInfo variant_info(int v) {
         case 4: return variant_info_t<K, 4>();
         case 5: return variant_info_t<K, 5>();
         case 6: return variant_info_t<K, 6>();
+        case 7: return variant_info_t<K, 7>();
         default: return variant_info_t<K, 0>();
     }
 }
@@ -553,6 +561,7 @@ static void launch_group(int v, K* region, uint64_t n_lines, uint32_t g, uint64_
         case 4: launch_group_t<K, 4>(region, n_lines, g, seed, pivot, out, st); break;
         case 5: launch_group_t<K, 5>(region, n_lines, g, seed, pivot, out, st); break;
         case 6: launch_group_t<K, 6>(region, n_lines, g, seed, pivot, out, st); break;
+        case 7: launch_group_t<K, 7>(region, n_lines, g, seed, pivot, out, st); break;
         default: launch_group_t<K, 0>(region, n_lines, g, seed, pivot, out, st); break;
     }
 }
@@ -590,6 +599,7 @@ static uint32_t next_epoch() {
 }
 
 static int cur_variant() {
+    if (params().seed == 0) return STRIDED_VARIANT;  // "strided" param: X = 0
     const int v = (int)params().variant;
     return (v >= 0 && v < N_VARIANTS) ? v : 0;
 }

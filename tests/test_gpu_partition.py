@@ -207,13 +207,33 @@ def test_async_and_stats(pp):
     assert st["aux_bytes"] < 0.01 * n * 8
 
 
-def test_host_variant(pp):
-    for dt, p in ((np.uint64, 1 << 62), (np.uint32, 1 << 30)):
-        a = (synth.uniform_u64_np(200003, 11) if dt == np.uint64 else synth.uniform_u32_np(200003, 11))
-        b = a.copy()
-        f = pp.pp_partition_host_u64 if dt == np.uint64 else pp.pp_partition_host_u32
-        split = f(b, p)
-        oracle.check_partition(a, b, p, split)
+@pytest.mark.parametrize("chunk", [0, 4096, 5000, 1 << 16])
+def test_host_variant(pp, chunk):
+    """Host-buffer partition (streamed chunks, uploads from both ends,
+    predecessors written to the front / successors to the back): the host
+    result passes the oracle checks for ragged chunk counts, pivot extremes
+    and pinned as well as pageable memory."""
+    if chunk:
+        pp.pp_set_param("host_chunk", chunk)
+    try:
+        for dt in (np.uint64, np.uint32):
+            mx = U64_MAX if dt == np.uint64 else U32_MAX
+            for n in (1, 7, 4095, 4097, 200003, 1 << 20):
+                a = (synth.uniform_u64_np(n, 11) if dt == np.uint64 else synth.uniform_u32_np(n, 11))
+                f = pp.pp_partition_host_u64 if dt == np.uint64 else pp.pp_partition_host_u32
+                for p in (0, mx // 100, mx // 2, mx - mx // 100, mx):
+                    b = a.copy()
+                    split = f(b, p)
+                    oracle.check_partition(a, b, p, split)
+            # pinned host memory
+            a = synth.uniform_u64_np(300007, 12)
+            pin = torch.empty(a.size, dtype=torch.int64, pin_memory=True)
+            pv = pin.numpy().view(np.uint64)
+            np.copyto(pv, a)
+            split = pp.pp_partition_host_u64(pv, 1 << 63)
+            oracle.check_partition(a, pv, 1 << 63, split)
+    finally:
+        pp.reset_params()
 
 
 def test_invalid_args(pp):
@@ -397,3 +417,37 @@ def test_group_variants(pp, variant):
                 p = int(frac * (mx + 1))
                 split, out = _run(pp, a, p, 1, variant=variant)
                 oracle.check_partition(a, out, p, split)
+
+
+@pytest.mark.parametrize("strided", [0, 1])
+def test_strided_ablation(pp, strided):
+    """the Strided Algorithm (X = 0) and
+    Smoothed Striding on uniform keys and on the stride-aligned adversary
+    (stride = the library's group count): both give a correct partition; on
+    the adversary the Strided window covers most of the array while the
+    smoothed one stays small."""
+    n = 1 << 24
+    a = synth.uniform_u64_np(n, 21)
+    # g = 32 groups of 512 chunks each (the smoothing averages over chunks)
+    s, out = _run(pp, a, 1 << 63, 0, strided=strided, g=32)
+    oracle.check_partition(a, out, 1 << 63, s)
+    pp.pp_set_param("strided", strided)
+    pp.pp_set_param("g", 32)
+    try:
+        from gpu_util import to_dev, to_host
+        t = to_dev(a)
+        pp.pp_partition(t, 1 << 63)
+        st = pp.pp_last_stats()
+        g, lk = st["g"], st["line_keys"]
+        assert g == 32
+        adv = synth.stride_aligned_u64_np(n, 22, lk, g)
+        t = to_dev(adv)
+        s = pp.pp_partition(t, 1 << 63)
+        w = pp.pp_last_stats()["W"] / n
+        oracle.check_partition(adv, to_host(t, np.uint64), 1 << 63, s)
+    finally:
+        pp.reset_params()
+    if strided:
+        assert w > 0.9, w
+    else:
+        assert w < 0.15, w

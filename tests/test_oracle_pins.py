@@ -242,3 +242,31 @@ def test_ss_offsets_generator():
     X = synth.ss_offsets(5, 200000, 8)
     counts = np.bincount(X.astype(np.int64), minlength=8)
     assert counts.min() > 0.9 * 25000 and counts.max() < 1.1 * 25000
+
+
+def test_strided_vs_smoothed_window_on_stride_aligned_adversary():
+    """SURVEY §8(f) #2 / PAPER.md:836-849 vs 865-913: on the stride-aligned
+    adversary (line j true iff j mod g < g/2) the Strided Algorithm (X = 0)
+    leaves almost the whole region unresolved (groups are all-true or
+    all-false), while uniformly random offsets X (Smoothed Striding) leave a
+    window of a few chunks.  Checked with the oracle's group statistics."""
+    g, b, s = 16, 32, 256
+    n_lines = g * s
+    a = synth.stride_aligned_u64_np(n_lines * b, 3, b, g)
+    p = 1 << 63
+    def window(X):
+        T, vlo, vhi = oracle.ss_groups(a, 0, n_lines, b, g, X, p)
+        assert int(T.sum()) == oracle.count(a, p)
+        return (int(vhi.max()) - int(vlo.min())) / (n_lines * b)
+    w_strided = window(np.zeros(s, dtype=np.uint64))
+    w_smooth = window(synth.ss_offsets(0x5EEDC0DE2004, s, g))
+    assert w_strided > 0.9, w_strided
+    assert w_smooth < 0.25, w_smooth
+
+
+def test_stride_aligned_np_torch_agree():
+    a = synth.stride_aligned_u64_np(5000, 11, 64, 6)
+    t = synth.stride_aligned_u64_torch(5000, 11, 64, 6, "cpu").numpy().view(np.uint64)
+    assert np.array_equal(a, t)
+    line = np.arange(5000) // 64
+    assert np.array_equal(a < (1 << 63), (line % 6) < 3)
