@@ -407,6 +407,25 @@ def extras(pp, torch, synth, dev, stream, flush):
                 "ms": ms, "gbs": 16 * n / (ms / 1e3) / 1e9, "window_frac": pp.pp_last_stats()["W"] / n}
     pp.pp_set_param("strided", 0)
     res["ablation_strided_vs_smoothed"] = abl
+    # the paper's Standard Algorithm (stable, out of place,
+    # PAPER.md:284-311) on the same input: count pass + scatter pass = 3*n*w
+    # bytes of traffic and a second n-key array, vs the in-place 2*n*w
+    outb = torch.empty_like(pristine)
+    ts = []
+    for i in range(6):
+        flush.sum()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        pp.pp_partition_stable_async_u64(pristine, outb, PIVOT, d)
+        e.record(stream)
+        torch.cuda.synchronize()
+        if i >= 2:
+            ts.append(s.elapsed_time(e))
+    ms = statistics.mean(ts)
+    res["standard_algorithm_out_of_place"] = {
+        "ms": ms, "keys_per_s": n / (ms / 1e3), "gbs_2nw": 16 * n / (ms / 1e3) / 1e9,
+        "gbs_traffic_3nw": 24 * n / (ms / 1e3) / 1e9, "aux_bytes": 8 * n}
+    del outb
     del pristine, buf, adv
     nq = 1 << 28
     for kind in ("uniform", "dup1000"):

@@ -73,6 +73,24 @@ pp_status pp_partition_async_u32(uint32_t *keys, uint64_t n, uint32_t pivot, voi
 pp_status pp_quicksort_u64(uint64_t *keys, uint64_t n, void *stream);
 pp_status pp_quicksort_u32(uint32_t *keys, uint64_t n, void *stream);
 
+/* ---- the Standard Algorithm: stable, OUT-OF-PLACE partition ---------------
+ * PAPER.md:284-311 (§2): D[i] = [in[i] < pivot], S = prefix sums of D, t =
+ * S[n-1]; predecessor i -> out[S[i]-1], successor i -> out[t + i - S[i]]
+ * (0-based; reading R9 fixes the paper's index garbles).  The output is
+ * unique (stable on both sides).  in, out: DEVICE pointers to n keys each,
+ * non-overlapping (PP_E_INVAL otherwise); in is not modified.  Not in place:
+ * Theta(n) extra memory (out) and 3*n*w bytes of traffic (count pass +
+ * scatter pass), the paper's baseline that the in-place algorithms avoid;
+ * kept as the SURVEY §8(f) #4 comparison row.  Aux: 12 bytes per 4096 keys.
+ * split_out: HOST pointer (synchronous); the async variant writes the split
+ * to the DEVICE word d_split and does not synchronise. */
+pp_status pp_partition_stable_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t pivot, void *stream,
+                                  uint64_t *split_out);
+pp_status pp_partition_stable_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t pivot, void *stream,
+                                  uint64_t *split_out);
+pp_status pp_partition_stable_async_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t pivot,
+                                        void *stream, uint64_t *d_split);
+
 /* ---- host-buffer (end-to-end) variants ------------------------------------
  * host_keys: HOST pointer (pinned or pageable) to n keys, partitioned / sorted
  * in place through a library-owned device buffer.  These are what an

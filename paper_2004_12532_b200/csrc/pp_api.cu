@@ -168,6 +168,51 @@ static pp_status partition_async(K* keys, uint64_t n, K pivot, void* stream, uin
     return s;
 }
 
+// Standard Algorithm (stable, out-of-place; pp_stable.cu): in and out are
+// distinct device arrays of n keys; the split goes to split_out (host, sync)
+// or d_split (device, async).
+template <typename K>
+static pp_status partition_stable(const K* in, K* out, uint64_t n, K pivot, void* stream, uint64_t* split_out,
+                                  uint64_t* d_split) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!split_out && !d_split) {
+        set_error("split_out / d_split is NULL");
+        return PP_E_INVAL;
+    }
+    pp_status s = check_device_keys(in, n);
+    if (s == PP_OK) s = check_device_keys(out, n);
+    if (s != PP_OK) return s;
+    if (n > 0 && in < out + n && out < in + n) {
+        set_error("in and out overlap (the Standard Algorithm is out of place)");
+        return PP_E_INVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    g_last_ctl = nullptr;
+    if (n == 0) {
+        g_stats = LastStats();
+        if (split_out) *split_out = 0;
+        if (d_split) {
+            const cudaError_t e = cudaMemsetAsync(d_split, 0, sizeof(uint64_t), st);
+            if (e != cudaSuccess) return cuda_fail(e, "memset");
+        }
+        return PP_OK;
+    }
+    if (d_split) return partition_stable_device<K>(in, out, n, pivot, st, d_split, nullptr);
+    uint64_t* pw = pinned_word();
+    if (!pw) {
+        set_error("cudaMallocHost failed");
+        return PP_E_NOMEM;
+    }
+    uint64_t* total = nullptr;
+    s = partition_stable_device<K>(in, out, n, pivot, st, nullptr, &total);
+    if (s != PP_OK) return s;
+    cudaError_t e = cudaMemcpyAsync(pw, total, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "stable partition");
+    *split_out = *pw;
+    return PP_OK;
+}
+
 template <typename K>
 static pp_status quicksort_sync(K* keys, uint64_t n, void* stream) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -381,6 +426,18 @@ pp_status pp_partition_async_u32(uint32_t* keys, uint64_t n, uint32_t pivot, voi
 }
 pp_status pp_quicksort_u64(uint64_t* keys, uint64_t n, void* stream) {
     return quicksort_sync<uint64_t>(keys, n, stream);
+}
+pp_status pp_partition_stable_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t pivot, void* stream,
+                                  uint64_t* split_out) {
+    return partition_stable<uint64_t>(in, out, n, pivot, stream, split_out, nullptr);
+}
+pp_status pp_partition_stable_u32(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t pivot, void* stream,
+                                  uint64_t* split_out) {
+    return partition_stable<uint32_t>(in, out, n, pivot, stream, split_out, nullptr);
+}
+pp_status pp_partition_stable_async_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t pivot,
+                                        void* stream, uint64_t* d_split) {
+    return partition_stable<uint64_t>(in, out, n, pivot, stream, nullptr, d_split);
 }
 pp_status pp_quicksort_u32(uint32_t* keys, uint64_t n, void* stream) {
     return quicksort_sync<uint32_t>(keys, n, stream);

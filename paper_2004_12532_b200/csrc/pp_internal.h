@@ -85,6 +85,11 @@ pp_status ss_groups_device(K* keys, uint64_t n, K pivot, uint64_t g, cudaStream_
 template <typename K>
 pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st);
 
+// the Standard Algorithm, stable and out of place (pp_stable.cu)
+template <typename K>
+pp_status partition_stable_device(const K* in, K* out, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split,
+                                  uint64_t** total_out);
+
 // multi-GPU (pp_dist.cu)
 pp_status dist_unique_id(void* out128);
 pp_status dist_init(const void* id128, int nranks, int rank, int device);

@@ -451,3 +451,51 @@ def test_strided_ablation(pp, strided):
         assert w > 0.9, w
     else:
         assert w < 0.15, w
+
+
+@pytest.mark.parametrize("dt", [np.uint64, np.uint32])
+def test_standard_algorithm_bytewise(pp, dt):
+    """the GPU Standard Algorithm (stable, out of place,
+    PAPER.md:284-311) equals the oracle's Standard Algorithm byte for byte
+    (stability makes the output unique); edge sizes around the 4096-key tile,
+    duplicates, pivot extremes; the input is left untouched."""
+    from gpu_util import to_dev, to_host
+    rng = np.random.default_rng(31)
+    mx = U64_MAX if dt == np.uint64 else U32_MAX
+    sizes = [0, 1, 2, 31, 32, 33, 4095, 4096, 4097, 8191, 12289, 100003, 1 << 20]
+    for n in sizes:
+        for a in (rng.integers(0, mx, size=n, dtype=dt, endpoint=True), rng.integers(0, 5, size=n).astype(dt)):
+            for p in sorted({0, 1, 2, mx // 3, mx}):
+                ref = a.copy()
+                k_ref = oracle.partition_standard(ref, p)
+                t_in = to_dev(a)
+                t_out = torch.zeros_like(t_in)
+                k = pp.pp_partition_stable(t_in, t_out, p)
+                assert k == k_ref, (n, p)
+                assert np.array_equal(to_host(t_out, dt), ref), (n, p)
+                assert np.array_equal(to_host(t_in, dt), a)
+
+
+def test_standard_algorithm_config2(pp):
+    """Config 2 size (2^27 u64, three pivots): byte-exact against the oracle's
+    Standard Algorithm, async variant (split to device memory)."""
+    from gpu_util import to_host
+    n = 1 << 27
+    a = synth.uniform_u64_np(n, synth.SEEDS["c2"])
+    t_in = synth.uniform_u64_torch(n, synth.SEEDS["c2"], "cuda")
+    t_out = torch.empty_like(t_in)
+    d = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for mu, p in synth.PIVOT_MU.items():
+        pp.pp_partition_stable_async_u64(t_in, t_out, p, d)
+        ref = a.copy()
+        k_ref = oracle.partition_standard(ref, p)
+        assert int(d.item()) == k_ref
+        assert np.array_equal(to_host(t_out, np.uint64), ref), mu
+
+
+def test_standard_algorithm_rejects_overlap(pp):
+    import ctypes
+    L = pp.load()
+    t = torch.zeros(64, dtype=torch.int64, device="cuda")
+    out = ctypes.c_uint64(0)
+    assert L.pp_partition_stable_u64(t.data_ptr(), t.data_ptr() + 8 * 8, 32, 5, None, ctypes.byref(out)) == 1
