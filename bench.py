@@ -207,6 +207,9 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     pp.load(build_if_missing=False)
     pp.reset_params()
+    for kv in filter(None, os.environ.get("PP_BENCH_PARAMS", "").split(",")):  # A/B tuning (tools/ab_params.sh)
+        k, v = kv.split("=")
+        pp.pp_set_param(k, int(v))
     stream = torch.cuda.current_stream()
 
     n = N_KEYS

@@ -87,6 +87,7 @@ static __device__ void finish_ctl(Ctl* c, uint64_t n, uint64_t K, uint64_t a[3],
     const uint64_t cap = max_tiles ? max_tiles : cleanup_max_tiles(n);
     uint64_t tile = (side + cap - 1) / cap;
     if (tile < min_tile) tile = min_tile;
+    tile = (tile + min_tile - 1) / min_tile * min_tile;  // a multiple of the one-round-trip tile
     c->n = n;
     c->K = K;
     c->W = W;
@@ -223,23 +224,27 @@ __device__ void select_pair(const K* __restrict__ keys, const Dirty& d, K pivot,
 // predecessor of [uR, uRend), for i < npairs (ranges <= NT*EPT; all items
 // of both ranges belong to this CTA).  Values cross through shared memory
 // by rank; each thread writes back its own items' positions.
+// (ra, rb: the pairs are the items of ranks [ra, ra+npairs) on the left and
+// [rb, rb+npairs) on the right -- a task that starts inside its tiles.)
 template <typename K, int NT, int EPT>
 __device__ __forceinline__ void swap_pair(K* __restrict__ keys, const Dirty& d, K pivot, uint64_t uL,
                                           uint64_t uLend, uint64_t uR, uint64_t uRend, uint64_t npairs,
-                                          PairBuf<K, NT, EPT>& pb) {
+                                          PairBuf<K, NT, EPT>& pb, uint32_t ra = 0, uint32_t rb = 0) {
     PairScan<K, EPT> ps;
     scan_pair<K, NT, EPT>(keys, d, pivot, uL, uLend, uR, uRend, pb.sc, ps);
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
-        if (((ps.fl >> k) & 1u) && ps.rl[k] < npairs) pb.lval[ps.rl[k]] = ps.xl[k];
-        if (((ps.fr >> k) & 1u) && ps.rr[k] < npairs) pb.rval[ps.rr[k]] = ps.xr[k];
+        const uint32_t il = ps.rl[k] - ra, ir = ps.rr[k] - rb;  // wraps (large) below the window
+        if (((ps.fl >> k) & 1u) && il < npairs) pb.lval[il] = ps.xl[k];
+        if (((ps.fr >> k) & 1u) && ir < npairs) pb.rval[ir] = ps.xr[k];
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
         const uint64_t off = (uint64_t)k * NT + threadIdx.x;
-        if (((ps.fl >> k) & 1u) && ps.rl[k] < npairs) keys[vreal(d, uL + off)] = pb.rval[ps.rl[k]];
-        if (((ps.fr >> k) & 1u) && ps.rr[k] < npairs) keys[vreal(d, uR + off)] = pb.lval[ps.rr[k]];
+        const uint32_t il = ps.rl[k] - ra, ir = ps.rr[k] - rb;
+        if (((ps.fl >> k) & 1u) && il < npairs) keys[vreal(d, uL + off)] = pb.rval[il];
+        if (((ps.fr >> k) & 1u) && ir < npairs) keys[vreal(d, uR + off)] = pb.lval[ir];
     }
     __syncthreads();
 }
@@ -261,11 +266,14 @@ struct StreamBuf {
 
 template <typename K, int NT, int EPT>
 __device__ void walk_swap_stream(K* __restrict__ keys, const Dirty& d, K pivot, uint64_t uL0, uint64_t uLend,
-                                 uint64_t uR0, uint64_t uRend, StreamBuf<NT, EPT>& sb) {
+                                 uint64_t uR0, uint64_t uRend, StreamBuf<NT, EPT>& sb,
+                                 uint64_t max_pairs = ~0ull) {
     constexpr uint32_t RNG = NT * EPT, Q = StreamBuf<NT, EPT>::Q;
     uint64_t uL = uL0, uR = uR0;
     uint32_t hl = 0, tl = 0, hr = 0, tr = 0;  // ring head / tail counters
+    uint64_t done = 0;
     for (;;) {
+        if (done >= max_pairs) break;
         const bool scanL = (tl - hl) < RNG && uL < uLend;
         const bool scanR = (tr - hr) < RNG && uR < uRend;
         if (scanL || scanR) {
@@ -284,8 +292,10 @@ __device__ void walk_swap_stream(K* __restrict__ keys, const Dirty& d, K pivot, 
             if (scanR) uR = min(uR + RNG, uRend);
             __syncthreads();
         }
-        const uint32_t m = min(tl - hl, tr - hr);
+        uint32_t m = min(tl - hl, tr - hr);
+        if ((uint64_t)m > max_pairs - done) m = (uint32_t)(max_pairs - done);
         if (m == 0) {
+            if (done >= max_pairs) break;
             if (!(uL < uLend && (tl - hl) < RNG) && !(uR < uRend && (tr - hr) < RNG)) break;
             continue;
         }
@@ -298,6 +308,7 @@ __device__ void walk_swap_stream(K* __restrict__ keys, const Dirty& d, K pivot, 
         }
         hl += m;
         hr += m;
+        done += m;
         __syncthreads();
     }
 }
@@ -328,12 +339,18 @@ static_assert(SW_RNG == (int)CLEANUP_MIN_TILE, "tile = one round trip");
 // FROM_GROUPS: K = head_T + sum T_i + tail_T from the group outputs;
 // otherwise (cleanup-only path) K = sum of the count_kernel partials and
 // D = [0, n).  max_tiles: tiles per side (0 = cleanup_max_tiles(n)).
+// Misplaced-flag bitmap of the dirty set (fused cleanup tail): one bit per
+// dirty position, left side [0, Kv) then right side [Kv, W), each side
+// bm_side_words(cap) words; written only when W <= cap.
+__host__ __device__ __forceinline__ uint64_t bm_side_words(uint64_t cap) { return cap / 32 + 64; }
+
 template <typename K, bool FROM_GROUPS>
 __device__ void reduce_count_body(const K* __restrict__ keys, uint64_t n, uint64_t h, uint64_t n_lines, uint32_t LK,
                                   const GroupOut* __restrict__ go, uint32_t g, const uint64_t* __restrict__ partial,
                                   int np, K pivot, Ctl* __restrict__ ctl, uint64_t* __restrict__ d_split,
                                   uint32_t* __restrict__ cntL, uint32_t* __restrict__ cntR, uint64_t max_tiles,
-                                  uint32_t bx, uint32_t gx) {
+                                  uint32_t bx, uint32_t gx, uint32_t* __restrict__ flags = nullptr,
+                                  uint32_t nflags = 0, uint32_t* __restrict__ bm = nullptr, uint64_t bm_cap = 0) {
     __shared__ uint64_t sT[8], sMin[8], sMax[8], sHT[8];
     __shared__ Ctl sc;
     __shared__ uint32_t s[8];
@@ -401,6 +418,9 @@ __device__ void reduce_count_body(const K* __restrict__ keys, uint64_t n, uint64
             if (d_split) *d_split = Ksplit;
         }
     }
+    // the next kernel's grid barrier starts from zeroed flags
+    if (bx == 0)
+        for (uint32_t i = tid; i < nflags; i += 256) flags[i] = 0;
     __syncthreads();
     griddep_launch();
     Dirty d;
@@ -410,6 +430,7 @@ __device__ void reduce_count_body(const K* __restrict__ keys, uint64_t n, uint64
         d.l[k] = sc.dl[k];
     }
     const uint64_t Kv = sc.Kv, W = sc.W, TT = sc.tile, nL = sc.nL, nR = sc.nR;
+    const bool use_bm = bm != nullptr && W <= bm_cap;
     for (uint64_t t = bx; t < nL + nR; t += gx) {
         const bool left = t < nL;
         const uint64_t u0 = left ? t * TT : Kv + (t - nL) * TT;
@@ -426,7 +447,13 @@ __device__ void reduce_count_body(const K* __restrict__ keys, uint64_t n, uint64
             for (int k = 0; k < 8; ++k) {
                 const uint64_t u = ub + (uint64_t)k * 256 + tid;
                 const bool p = is_pred(x[k], pivot);
-                c += (u < u1 && (left ? !p : p)) ? 1u : 0u;
+                const bool f = u < u1 && (left ? !p : p);
+                c += f ? 1u : 0u;
+                if (use_bm) {  // misplaced-flag bitmap of the dirty set (tiles start at multiples of 32)
+                    const uint32_t b = __ballot_sync(0xffffffffu, f);
+                    const uint64_t w = (u - lane - (left ? 0 : Kv)) >> 5;
+                    if (lane == 0 && u - lane < u1) (left ? bm : bm + bm_side_words(bm_cap))[w] = b;
+                }
             }
         }
 #pragma unroll
@@ -598,6 +625,245 @@ __device__ void swap_body(K* __restrict__ keys, const Ctl* __restrict__ ctl, K p
             swap_pair<K, SW_NT, SW_EPT2>(keys, d, pivot, uL, eL, uR, eR, pairs, sm.pb);
         } else {
             walk_swap_stream<K, SW_NT, SW_EPT2>(keys, d, pivot, uL, eL, uR, eR, sm.sb);
+        }
+    }
+}
+
+
+// ===========================================================================
+// K2+K5 fused (the default cleanup tail): every CTA redundantly scans the
+// tile counts (<= FUSED_MAX_TILES per side) into shared memory, finds its
+// tasks -- the breakpoints U_j of the stable merge of the left and right tile
+// rank boundaries -- by a merge-path co-rank search, and swaps task j's pairs
+// (ranks [U_j, U_j+1)), which lie in ONE left and ONE right tile, in one
+// round trip over the two tiles (rank offsets instead of a separate locate
+// pass).  Tiles larger than one round trip (huge dirty sets) locate the
+// task's first items, then walk with a pair limit.  CTA bx == 0 publishes the
+// totals.  Dynamic shared memory: 2 * (FUSED_MAX_TILES + 1) u64.
+// ===========================================================================
+constexpr uint64_t FUSED_MAX_TILES = 2048;
+
+template <int NT>
+__device__ __forceinline__ uint64_t block_exscan(uint64_t v, uint64_t* sw, uint64_t& total) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sw[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t w = lane < NW ? sw[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < NW) sw[lane] = w;
+    }
+    __syncthreads();
+    total = sw[NW - 1];
+    const uint64_t wpre = warp > 0 ? sw[warp - 1] : 0;
+    __syncthreads();
+    return wpre + x - v;
+}
+
+// the j-th value of the sorted merge of a[0..na) and b[0..nb)
+__device__ __forceinline__ uint64_t merged_at(const uint64_t* a, uint64_t na, const uint64_t* b, uint64_t nb,
+                                             uint64_t j) {
+    uint64_t lo = j > nb ? j - nb : 0, hi = j < na ? j : na;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] <= b[j - 1 - mid]) lo = mid + 1; else hi = mid;
+    }
+    return (lo < na && (j - lo >= nb || a[lo] <= b[j - lo])) ? a[lo] : b[j - lo];
+}
+
+// Grid barrier over nb co-resident CTAs (cooperative launch): every CTA
+// release-stores 1 into its own flag (the flags were zeroed by the previous
+// kernel of the stream), then acquire-polls all flags.  No atomics.
+__device__ __forceinline__ void grid_barrier_flags(uint32_t* flags, uint32_t bx, uint32_t nb) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_gpu(flags + bx, 1u);
+    }
+    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
+        while (ld_acquire_gpu(flags + i) == 0u) __nanosleep(32);
+    __threadfence();
+    __syncthreads();
+}
+
+constexpr int FUSED_TASKS_PER_CTA = 32;  // task slots per CTA (grid >= 2*FUSED_MAX_TILES / 32)
+
+// position (0..31) of the k-th set bit of w (k < popc(w))
+__device__ __forceinline__ uint32_t select_bit(uint32_t w, uint32_t k) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) {
+        const uint32_t lo = w & ((1u << sh) - 1u);
+        const uint32_t c = __popc(lo);
+        if (k >= c) {
+            k -= c;
+            w >>= sh;
+            pos += sh;
+        } else {
+            w = lo;
+        }
+    }
+    return pos;
+}
+
+// bitmap path: tiles of <= FUSED_BM_TILE_WORDS * 32 keys (W <= the bitmap cap
+// <= FUSED_MAX_TILES * that, so the tile size stays within it)
+constexpr int FUSED_BM_TILE_WORDS = 512;
+__host__ __device__ __forceinline__ uint64_t fused_bm_cap(uint64_t n) {
+    const uint64_t c = n / 128, mx = FUSED_MAX_TILES * (uint64_t)FUSED_BM_TILE_WORDS * 32;
+    return c < mx ? c : mx;
+}
+
+template <typename K>
+__device__ void scan_swap_body(K* __restrict__ keys, Ctl* __restrict__ ctl, K pivot,
+                               const uint32_t* __restrict__ cntL, const uint32_t* __restrict__ cntR,
+                               uint32_t* __restrict__ flags, const uint32_t* __restrict__ bm, uint64_t bm_cap,
+                               uint64_t* sp, uint32_t bx, uint32_t gx) {
+    __shared__ uint64_t sw[32];
+    __shared__ uint64_t posLs[FUSED_TASKS_PER_CTA], posRs[FUSED_TASKS_PER_CTA];
+    __shared__ CleanupSmem<K, SW_NT, SW_EPT2> sm;
+    griddep_wait();
+    griddep_launch();
+    const int tid = threadIdx.x;
+    const Dirty d = load_dirty(ctl);
+    const uint64_t Kv = ctl->Kv, W = ctl->W, T = ctl->tile, nL = ctl->nL, nR = ctl->nR;
+    uint64_t* sPL = sp;
+    uint64_t* sPR = sp + nL + 1;
+    uint64_t carry = 0;
+    for (uint64_t b = 0; b < nL; b += SW_NT) {
+        const uint64_t i = b + tid;
+        uint64_t tot;
+        const uint64_t ex = block_exscan<SW_NT>(i < nL ? cntL[i] : 0, sw, tot);
+        if (i < nL) sPL[i] = carry + ex;
+        carry += tot;
+    }
+    const uint64_t ML = carry;
+    carry = 0;
+    for (uint64_t b = 0; b < nR; b += SW_NT) {
+        const uint64_t i = b + tid;
+        uint64_t tot;
+        const uint64_t ex = block_exscan<SW_NT>(i < nR ? cntR[i] : 0, sw, tot);
+        if (i < nR) sPR[i] = carry + ex;
+        carry += tot;
+    }
+    const uint64_t MR = carry;
+    __syncthreads();
+    const bool ok = ML == MR && ML > 0;  // identical in every CTA: all return or none
+    if (bx == 0 && tid == 0) {
+        ctl->ML = ML;
+        ctl->MR = MR;
+        if (ML != MR) ctl->err = 1;  // #misplaced successors must equal #misplaced predecessors
+        ctl->nTasks = ok ? nL + nR : 0;
+    }
+    if (!ok) return;
+    const uint64_t nT = nL + nR;
+    // task j covers ranks [U_j, U_j+1) of the stable merge of the tile rank
+    // boundaries; its items lie in left tile tl and right tile tr
+    struct Task {
+        uint64_t np, ra, rb, uL, uLe, uR, uRe;
+    };
+    auto task = [&](uint64_t j) {
+        Task t;
+        const uint64_t U = merged_at(sPL, nL, sPR, nR, j);
+        const uint64_t U1 = j + 1 < nT ? merged_at(sPL, nL, sPR, nR, j + 1) : ML;
+        t.np = U1 - U;
+        const uint64_t tl = upper_bound_u64(sPL, nL, U) - 1, tr = upper_bound_u64(sPR, nR, U) - 1;
+        t.ra = U - sPL[tl];
+        t.rb = U - sPR[tr];
+        t.uL = tl * T;
+        t.uLe = min(t.uL + T, Kv);
+        t.uR = Kv + tr * T;
+        t.uRe = min(t.uR + T, W);
+        return t;
+    };
+    if (bm != nullptr && W <= bm_cap) {
+        // bitmap path: the misplaced flags of the dirty set were recorded by
+        // the count kernel and are never changed by a swap, so every task
+        // locates its pairs from its two tiles' bitmap words (popcount
+        // prefix + bit select) and swaps them -- no key scan, no barrier
+        __shared__ uint32_t bwL[FUSED_BM_TILE_WORDS], bwR[FUSED_BM_TILE_WORDS];
+        __shared__ uint32_t bpL[FUSED_BM_TILE_WORDS], bpR[FUSED_BM_TILE_WORDS];
+        const uint32_t* bmL = bm;
+        const uint32_t* bmR = bm + bm_side_words(bm_cap);
+        for (uint64_t j = bx; j < nT; j += gx) {
+            const Task t = task(j);
+            if (t.np == 0) continue;  // uniform
+            const uint32_t nwL = (uint32_t)((t.uLe - t.uL + 31) / 32), nwR = (uint32_t)((t.uRe - t.uR + 31) / 32);
+            const uint64_t wL0 = t.uL / 32, wR0 = (t.uR - Kv) / 32;
+            const uint32_t nw = nwL > nwR ? nwL : nwR;
+            uint64_t cL = 0, cR = 0;
+            for (uint32_t b = 0; b < nw; b += SW_NT) {
+                const uint32_t i = b + tid;
+                const uint32_t wl = i < nwL ? bmL[wL0 + i] : 0u, wr = i < nwR ? bmR[wR0 + i] : 0u;
+                uint64_t tl, tr;
+                const uint64_t el = block_exscan<SW_NT>(__popc(wl), sw, tl);
+                const uint64_t er = block_exscan<SW_NT>(__popc(wr), sw, tr);
+                if (i < nwL) { bwL[i] = wl; bpL[i] = (uint32_t)(cL + el); }
+                if (i < nwR) { bwR[i] = wr; bpR[i] = (uint32_t)(cR + er); }
+                cL += tl;
+                cR += tr;
+            }
+            __syncthreads();
+            for (uint64_t i = tid; i < t.np; i += SW_NT) {
+                const uint32_t rl = (uint32_t)(t.ra + i), rr = (uint32_t)(t.rb + i);
+                uint32_t lo = 0, hi = nwL;  // last word with prefix <= rl
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (bpL[mid] <= rl) lo = mid; else hi = mid;
+                }
+                const uint64_t uL = t.uL + 32ull * lo + select_bit(bwL[lo], rl - bpL[lo]);
+                lo = 0;
+                hi = nwR;
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (bpR[mid] <= rr) lo = mid; else hi = mid;
+                }
+                const uint64_t uR = t.uR + 32ull * lo + select_bit(bwR[lo], rr - bpR[lo]);
+                const uint64_t pl = vreal(d, uL), pr = vreal(d, uR);
+                const K a = keys[pl], b = keys[pr];
+                keys[pl] = b;
+                keys[pr] = a;
+            }
+            __syncthreads();
+        }
+        return;
+    }
+    // barrier path (dirty set beyond the bitmap cap)
+    // phase 1 (read only): the positions of every task's first items
+    int k = 0;
+    for (uint64_t j = bx; j < nT; j += gx, ++k) {
+        const Task t = task(j);
+        if (t.np == 0) continue;  // uniform
+        uint64_t pl, pr;
+        select_pair<K, SW_NT, SW_EPT2>(keys, d, pivot, t.uL, t.uLe, t.ra, t.uR, t.uRe, t.rb, sm.pb, pl, pr);
+        if (tid == 0) {
+            posLs[k] = pl;
+            posRs[k] = pr;
+        }
+    }
+    // no swap may change a key another CTA is still classifying
+    grid_barrier_flags(flags, bx, gx);
+    // phase 2: swap each task's pairs, scanning from its first items
+    k = 0;
+    for (uint64_t j = bx; j < nT; j += gx, ++k) {
+        const Task t = task(j);
+        if (t.np == 0) continue;
+        const uint64_t pl = posLs[k], pr = posRs[k];
+        if (T == (uint64_t)SW_RNG) {
+            swap_pair<K, SW_NT, SW_EPT2>(keys, d, pivot, pl, t.uLe, pr, t.uRe, t.np, sm.pb);
+        } else {
+            walk_swap_stream<K, SW_NT, SW_EPT2>(keys, d, pivot, pl, t.uLe, pr, t.uRe, sm.sb, t.np);
         }
     }
 }

@@ -69,9 +69,25 @@ __global__ void __launch_bounds__(256) reduce_count_kernel(const K* __restrict__
                                                            const GroupOut* __restrict__ go, uint32_t g,
                                                            const uint64_t* __restrict__ partial, int np, K pivot,
                                                            Ctl* __restrict__ ctl, uint64_t* __restrict__ d_split,
-                                                           uint32_t* __restrict__ cntL, uint32_t* __restrict__ cntR) {
-    reduce_count_body<K, FROM_GROUPS>(keys, n, h, n_lines, LK, go, g, partial, np, pivot, ctl, d_split, cntL, cntR, 0,
-                                      blockIdx.x, gridDim.x);
+                                                           uint32_t* __restrict__ cntL, uint32_t* __restrict__ cntR,
+                                                           uint64_t max_tiles, uint32_t* __restrict__ flags,
+                                                           uint32_t nflags, uint32_t* __restrict__ bm,
+                                                           uint64_t bm_cap) {
+    reduce_count_body<K, FROM_GROUPS>(keys, n, h, n_lines, LK, go, g, partial, np, pivot, ctl, d_split, cntL, cntR,
+                                      max_tiles, blockIdx.x, gridDim.x, flags, nflags, bm, bm_cap);
+}
+
+// K2+K5 fused cleanup tail (pp_engine.cuh scan_swap_body).
+// Launched cooperatively (all CTAs co-resident: the grid barrier between
+// its locate and swap phases needs it).
+template <typename K>
+__global__ void __launch_bounds__(SW_NT, 2) scan_swap_kernel(K* __restrict__ keys, Ctl* __restrict__ ctl, K pivot,
+                                                          const uint32_t* __restrict__ cntL,
+                                                          const uint32_t* __restrict__ cntR,
+                                                          uint32_t* __restrict__ flags,
+                                                          const uint32_t* __restrict__ bm, uint64_t bm_cap) {
+    extern __shared__ uint64_t ssp[];
+    scan_swap_body<K>(keys, ctl, pivot, cntL, cntR, flags, bm, bm_cap, ssp, blockIdx.x, gridDim.x);
 }
 
 // ===========================================================================
@@ -154,30 +170,6 @@ __device__ __forceinline__ void grid_sync(uint32_t* flags, uint32_t nb, uint32_t
         while ((int32_t)(ld_acquire_gpu(flags + i) - epoch) < 0) __nanosleep(64);
     __threadfence();
     __syncthreads();
-}
-
-template <int NT>
-__device__ uint64_t block_exscan(uint64_t v, uint64_t* sw, uint64_t& total) {
-    constexpr int NW = NT / 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) sw[warp] = x;
-    __syncthreads();
-    uint64_t wpre = 0;
-    total = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        const uint64_t c = sw[w];
-        wpre += (w < warp) ? c : 0;
-        total += c;
-    }
-    __syncthreads();
-    return wpre + x - v;
 }
 
 template <typename C>
@@ -605,8 +597,9 @@ static int cur_variant() {
 }
 
 struct Layout {
-    size_t ctl, gout, cntL, cntR, PL, PR, posL, posR, rk, ttl, ttr, partial, total;
+    size_t ctl, gout, cntL, cntR, PL, PR, posL, posR, rk, ttl, ttr, partial, flags, bm, total;
 };
+constexpr uint64_t MAX_BARRIER_CTAS = 4096;  // grid-barrier flags of the fused cleanup tail
 
 // Workspace: fixed-size cleanup arrays (cleanup_max_tiles(n) per side, the
 // tile size adapts to the dirty set on the device) + one GroupOut per group:
@@ -634,6 +627,8 @@ static Layout make_layout(uint64_t n, uint64_t g, bool cleanup, uint64_t nPartia
     L.ttl = take(4 * (maxTasks + 1));
     L.ttr = take(4 * (maxTasks + 1));
     L.partial = take(8 * nPartial);
+    L.flags = take(4 * MAX_BARRIER_CTAS);
+    L.bm = take(cleanup ? 4 * 2 * bm_side_words(fused_bm_cap(n)) : 4);
     L.total = o;
     return L;
 }
@@ -645,6 +640,52 @@ static uint64_t choose_groups(uint64_t n_lines, int occ) {
     const uint64_t cap = (uint64_t)sm_count() * occ;
     uint64_t g = n_lines / (uint64_t)std::max<int64_t>(P.min_lines_per_group, 1);
     return std::max<uint64_t>(1, std::min(g, cap));
+}
+
+// The fused cleanup tail runs on a co-resident grid (cooperative launch):
+// #SM x its occupancy, capped so every CTA has <= FUSED_TASKS_PER_CTA tasks.
+static constexpr size_t SCAN_SWAP_SMEM = 2 * 8 * (FUSED_MAX_TILES + 1);
+static uint32_t fused_tail_grid() {
+    static uint32_t G = 0;
+    if (!G) {
+        int occ = 0;
+        cudaFuncSetAttribute(scan_swap_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)SCAN_SWAP_SMEM);
+        cudaFuncSetAttribute(scan_swap_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)SCAN_SWAP_SMEM);
+        int o64 = 0, o32 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o64, scan_swap_kernel<uint64_t>, SW_NT, SCAN_SWAP_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o32, scan_swap_kernel<uint32_t>, SW_NT, SCAN_SWAP_SMEM);
+        occ = std::max(1, std::min(o64, o32));
+        G = (uint32_t)std::min<uint64_t>((uint64_t)sm_count() * (uint64_t)occ, MAX_BARRIER_CTAS);
+        static_assert(2 * FUSED_MAX_TILES <= 148 * (uint64_t)FUSED_TASKS_PER_CTA, "task slots per CTA");
+    }
+    return G;
+}
+
+template <typename K>
+static cudaError_t launch_scan_swap(uint32_t G, cudaStream_t st, K* keys, Ctl* ctl, K pivot, const uint32_t* cntL,
+                                    const uint32_t* cntR, uint32_t* flags, const uint32_t* bm, uint64_t bm_cap) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(SW_NT);
+    cfg.dynamicSmemBytes = SCAN_SWAP_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    note_launches(1);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, scan_swap_kernel<K>, keys, ctl, pivot, cntL, cntR, flags, bm, bm_cap);
+    if (e != cudaSuccess) {  // cooperative + programmatic serialization refused: plain cooperative
+        cudaGetLastError();
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, scan_swap_kernel<K>, keys, ctl, pivot, cntL, cntR, flags, bm, bm_cap);
+    }
+    return e;
 }
 
 template <typename K>
@@ -744,30 +785,46 @@ pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64
             if (e != cudaSuccess) return cuda_fail(e, "fused partition launch");
             return PP_OK;
         }
+        // cleanup tail: fused scan+locate+barrier+swap (default) or the 3-kernel chain
+        // (the fused tail needs a grid with <= FUSED_TASKS_PER_CTA tasks per CTA)
+        const bool fused_tail = P.cleanup_chain == 0 &&
+                                (uint64_t)fused_tail_grid() * FUSED_TASKS_PER_CTA >= 2 * FUSED_MAX_TILES;
+        const uint64_t max_tiles = fused_tail ? std::min<uint64_t>(cleanup_max_tiles(n), FUSED_MAX_TILES) : 0;
+        const uint32_t nflags = fused_tail ? fused_tail_grid() : 0;
+        uint32_t* flags = reinterpret_cast<uint32_t*>(ws + L.flags);
+        uint32_t* bm = fused_tail && P.cleanup_bitmap ? reinterpret_cast<uint32_t*>(ws + L.bm) : nullptr;
+        const uint64_t bm_cap = fused_bm_cap(n);
         if (path == 2) {
             launch_group<K>(variant, keys + h, n_lines, (uint32_t)g, P.seed, pivot, gout, st);
             timing_mark(st);
             e = launch_pdl(reduce_count_kernel<K, true>, grid_cleanup, 256, st, keys, n, h, n_lines, (uint32_t)LK,
-                           gout, (uint32_t)g, partial, nPartial, pivot, ctl, d_split, cntL, cntR);
+                           gout, (uint32_t)g, partial, nPartial, pivot, ctl, d_split, cntL, cntR, max_tiles, flags,
+                           nflags, bm, bm_cap);
         } else {
             count_kernel<K><<<nPartial, 256, 0, st>>>(keys, n, pivot, partial);
             note_launches(1);
             timing_mark(st);
             e = launch_pdl(reduce_count_kernel<K, false>, grid_cleanup, 256, st, keys, n, (uint64_t)0, (uint64_t)0,
-                           (uint32_t)LK, gout, (uint32_t)0, partial, nPartial, pivot, ctl, d_split, cntL, cntR);
+                           (uint32_t)LK, gout, (uint32_t)0, partial, nPartial, pivot, ctl, d_split, cntL, cntR,
+                           max_tiles, flags, nflags, bm, bm_cap);
         }
-        const size_t scan_smem = 2 * 8 * (cleanup_max_tiles(n) + 1);
-        static size_t scan_smem_set = 0;
-        if (scan_smem > 48 * 1024 && scan_smem > scan_smem_set) {
-            cudaFuncSetAttribute(tile_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem);
-            scan_smem_set = scan_smem;
+        if (fused_tail) {
+            if (e == cudaSuccess) e = launch_scan_swap<K>(nflags, st, keys, ctl, pivot, cntL, cntR, flags, bm, bm_cap);
+        } else {
+            const size_t scan_smem = 2 * 8 * (cleanup_max_tiles(n) + 1);
+            static size_t scan_smem_set = 0;
+            if (scan_smem > 48 * 1024 && scan_smem > scan_smem_set) {
+                cudaFuncSetAttribute(tile_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem);
+                scan_smem_set = scan_smem;
+            }
+            if (e == cudaSuccess)
+                e = launch_pdl_smem(tile_scan_kernel, 1, 1024, scan_smem, st, ctl, cntL, cntR, PL, PR, rk, ttl, ttr);
+            if (e == cudaSuccess)
+                e = launch_pdl(locate_kernel<K>, grid_cleanup, SW_NT, st, keys, ctl, pivot, PL, PR, posL, posR, rk,
+                               ttl, ttr);
+            if (e == cudaSuccess)
+                e = launch_pdl(swap_kernel<K>, grid_cleanup, SW_NT, st, keys, ctl, pivot, posL, posR, rk);
         }
-        if (e == cudaSuccess)
-            e = launch_pdl_smem(tile_scan_kernel, 1, 1024, scan_smem, st, ctl, cntL, cntR, PL, PR, rk, ttl, ttr);
-        if (e == cudaSuccess)
-            e = launch_pdl(locate_kernel<K>, grid_cleanup, SW_NT, st, keys, ctl, pivot, PL, PR, posL, posR, rk, ttl,
-                           ttr);
-        if (e == cudaSuccess) e = launch_pdl(swap_kernel<K>, grid_cleanup, SW_NT, st, keys, ctl, pivot, posL, posR, rk);
     }
     timing_mark(st);
     if (e != cudaSuccess) return cuda_fail(e, "partition launch");
