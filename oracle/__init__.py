@@ -17,6 +17,12 @@ SPEC.md worked examples).  Functions and their pin status:
 - quicksort        : pinned (numpy.sort byte-for-byte)
 - ss_groups        : pinned (brute-force group enumeration in the test and
                      the window invariant PAPER.md:999-1001 on partitioned data)
+- bps_make_successor_heavy : pinned (Lemma 3.1: every t-prefix holds >= t/4
+                     successors, brute force over all small patterns; a
+                     permutation of the input)
+- partition_bps    : pinned ((1)-(3) by brute force over all small patterns
+                     and several block sizes; Lemma 3.4's conflict-freeness
+                     checked inside on every swap)
 """
 from __future__ import annotations
 
@@ -65,6 +71,10 @@ def lib():
             getattr(L, f"oracle_ss_groups_{sfx}").argtypes = [P, u64, u64, u64, u64, U64P, K,
                                                               U64P, U64P, U64P]
             getattr(L, f"oracle_ss_groups_{sfx}").restype = None
+            getattr(L, f"oracle_bps_make_successor_heavy_{sfx}").argtypes = [P, u64, K, ctypes.c_int]
+            getattr(L, f"oracle_bps_make_successor_heavy_{sfx}").restype = None
+            getattr(L, f"oracle_partition_bps_{sfx}").argtypes = [P, u64, K, u64, U64P]
+            getattr(L, f"oracle_partition_bps_{sfx}").restype = u64
         L.oracle_prefix_sum_recursive.argtypes = [U64P, u64]
         L.oracle_prefix_sum_recursive.restype = None
         _lib = L
@@ -107,6 +117,25 @@ def partition_standard(a: np.ndarray, pivot: int) -> int:
     C = np.empty(max(1, a.size), dtype=a.dtype)
     return int(getattr(lib(), f"oracle_partition_standard_{sfx}")(
         _ptr(a, P), a.size, K(pivot), _ptr(S, U64P), _ptr(C, P)))
+
+
+def bps_make_successor_heavy(a: np.ndarray, pivot: int, rev: bool = False) -> None:
+    """In place: the Preprocessing phase on the view
+    (reversed, with roles swapped, when rev)."""
+    sfx, P, K = _sfx(a)
+    getattr(lib(), f"oracle_bps_make_successor_heavy_{sfx}")(_ptr(a, P), a.size, K(pivot), int(rev))
+
+
+def partition_bps(a: np.ndarray, pivot: int, B: int = 4096) -> int:
+    """In place: the Blocked-Prefix-Sum partition, low-space form
+     with blocks of B keys; returns the split.
+    Raises if a Reorder swap broke Lemma 3.4."""
+    sfx, P, K = _sfx(a)
+    S = np.empty(a.size // B + 2, dtype=np.uint64)
+    k = int(getattr(lib(), f"oracle_partition_bps_{sfx}")(_ptr(a, P), a.size, K(pivot), B, _ptr(S, U64P)))
+    if k == (1 << 64) - 1:
+        raise AssertionError("BPS Reorder: a swap target was not a successor of the reordered prefix")
+    return k
 
 
 def quicksort(a: np.ndarray) -> None:

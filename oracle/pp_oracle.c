@@ -217,3 +217,110 @@ void oracle_prefix_sum_recursive(uint64_t *S, uint64_t n)
 
 DEFINE_ORACLE(uint64_t, u64)
 DEFINE_ORACLE(uint32_t, u32)
+
+/* ------------------------------------------------------------------------- */
+/* The Blocked-Prefix-Sum partition (§3, Figs. 1-2) in the  */
+/* form of the paper's "low-space implementation" (§5):   */
+/* the block prefix sums are kept in an explicit array of floor(n/B)+1 words  */
+/* (the implicit bit-pair codec of Lemma 3.2 is not used),    */
+/* the Preprocessing and Reordering phases are in place.  Serial.             */
+/*                                                                           */
+/* Role swap (Fig. 2): the phases need successors to be at  */
+/* least half of the array.  When fewer than half are successors, the         */
+/* algorithm runs on the logically reversed array V(i) = A[n-1-i] with the    */
+/* roles of predecessors and successors swapped; the reversed result read     */
+/* forwards is the partition.  pred_v(x) below is "predecessor in the view".  */
+/* ------------------------------------------------------------------------- */
+#define BPS_V(i) (rev ? n - 1 - (i) : (i))
+#define BPS_PRED(x) (rev ? !((x) < pivot) : ((x) < pivot))
+#define BPS_SWAP(T, a, b) do { T t_ = A[a]; A[a] = A[b]; A[b] = t_; } while (0)
+
+#define DEFINE_BPS_ORACLE(T, SFX)                                               \
+                                                                                \
+/* MakeSuccessorHeavy (Fig. 1; Lemma 3.1):*/ \
+/* for i < floor(m/2): if V[i] is a predecessor and V[m-1-i] a successor,    */ \
+/* swap them; then recurse on the first ceil(m/2) positions (stopping at     */ \
+/* m <= 1, reading R21).  Afterwards every t-prefix holds >= t/4 successors.  */ \
+void oracle_bps_make_successor_heavy_##SFX(T *A, uint64_t n, T pivot, int rev)  \
+{                                                                               \
+    uint64_t m = n;                                                             \
+    while (m > 1) {                                                             \
+        for (uint64_t i = 0; i < m / 2; i++) {                                  \
+            uint64_t a = BPS_V(i), b = BPS_V(m - 1 - i);                        \
+            if (BPS_PRED(A[a]) && !BPS_PRED(A[b])) BPS_SWAP(T, a, b);           \
+        }                                                                       \
+        m = (m + 1) / 2;                                                        \
+    }                                                                           \
+}                                                                               \
+                                                                                \
+/* Reorder (Fig. 2; Lemma 3.4) on the     */ \
+/* prefix of the first tb blocks (the whole view when tb == nb).  S[i] =     */ \
+/* predecessors in blocks 0..i-1.  m <= 5B: the serial base case (PAPER.md:  */ \
+/* 606-608; here the r-th successor in [0,K') is swapped with the r-th       */ \
+/* predecessor in [K',m), reading R22).  Otherwise recurse on the least t    */ \
+/* blocks with t*B > 4m/5, then swap the j-th predecessor of each later      */ \
+/* block i with position S[i] + j, which the lemma puts in the successor     */ \
+/* part of the reordered prefix: returns 1 if a target is not a successor    */ \
+/* inside the prefix (the conflict-freeness the lemma proves), else 0.       */ \
+static int bps_reorder_##SFX(T *A, uint64_t n, T pivot, int rev, uint64_t B,    \
+                             uint64_t nb, const uint64_t *S, uint64_t tb)       \
+{                                                                               \
+    uint64_t m = (tb == nb) ? n : tb * B;                                       \
+    uint64_t t = (4 * m) / (5 * B) + 1;  /* least t with t*B > 4m/5 */           \
+    if (m <= 5 * B || t >= tb) {  /* base case (also when the extended last */  \
+                                  /* block leaves no shorter prefix)        */  \
+        uint64_t Kp = S[tb], i = 0, j = Kp;                                     \
+        for (;;) {                                                              \
+            while (i < Kp && BPS_PRED(A[BPS_V(i)])) i++;                        \
+            while (j < m && !BPS_PRED(A[BPS_V(j)])) j++;                        \
+            if (i >= Kp || j >= m) break;                                       \
+            BPS_SWAP(T, BPS_V(i), BPS_V(j));                                    \
+            i++; j++;                                                           \
+        }                                                                       \
+        return 0;                                                               \
+    }                                                                           \
+    if (bps_reorder_##SFX(A, n, pivot, rev, B, nb, S, t)) return 1;             \
+    for (uint64_t i = t; i < tb; i++) {                                         \
+        uint64_t lo = i * B, hi = (i == nb - 1) ? n : (i + 1) * B, j = 0;       \
+        for (uint64_t q = lo; q < hi; q++) {                                    \
+            if (!BPS_PRED(A[BPS_V(q)])) continue;                               \
+            uint64_t target = S[i] + j++;                                       \
+            if (target >= t * B || BPS_PRED(A[BPS_V(target)])) return 1;        \
+            BPS_SWAP(T, BPS_V(q), BPS_V(target));                               \
+        }                                                                       \
+    }                                                                           \
+    return 0;                                                                   \
+}                                                                               \
+                                                                                \
+/* ParallelPartition (Fig. 2), low-space form: count,      */ \
+/* role swap, MakeSuccessorHeavy, explicit block prefix sums over blocks of  */ \
+/* B keys (the last block takes the remainder; the paper's  */ \
+/* own recursive scan), Reorder.  S: scratch of            */ \
+/* floor(n/B)+1 words.  Returns K, or UINT64_MAX if a Reorder swap target    */ \
+/* broke Lemma 3.4's guarantee.                                              */ \
+uint64_t oracle_partition_bps_##SFX(T *A, uint64_t n, T pivot, uint64_t B,     \
+                                    uint64_t *S)                               \
+{                                                                               \
+    uint64_t K = 0;                                                             \
+    for (uint64_t i = 0; i < n; i++) if (A[i] < pivot) K++;                     \
+    int rev = 2 * (n - K) < n;  /* fewer than half are successors */           \
+    oracle_bps_make_successor_heavy_##SFX(A, n, pivot, rev);                    \
+    uint64_t nb = n / B;                                                        \
+    if (nb == 0) {  /* a single short block: the base case */                   \
+        uint64_t S0[2] = {0, rev ? n - K : K};                                  \
+        bps_reorder_##SFX(A, n, pivot, rev, n > 0 ? n : 1, 1, S0, 1);           \
+        return K;                                                               \
+    }                                                                           \
+    S[0] = 0;                                                                   \
+    for (uint64_t i = 0; i < nb; i++) {                                         \
+        uint64_t lo = i * B, hi = (i == nb - 1) ? n : (i + 1) * B, c = 0;       \
+        for (uint64_t q = lo; q < hi; q++) c += BPS_PRED(A[BPS_V(q)]) ? 1 : 0;  \
+        S[i + 1] = c;                                                           \
+    }                                                                           \
+    oracle_prefix_sum_recursive(S + 1, nb);  /* S[i+1] = preds in blocks <= i */ \
+    if (bps_reorder_##SFX(A, n, pivot, rev, B, nb, S, nb)) return UINT64_MAX;   \
+    return K;                                                                   \
+}
+
+DEFINE_BPS_ORACLE(uint64_t, u64)
+DEFINE_BPS_ORACLE(uint32_t, u32)

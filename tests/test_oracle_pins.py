@@ -270,3 +270,66 @@ def test_stride_aligned_np_torch_agree():
     assert np.array_equal(a, t)
     line = np.arange(5000) // 64
     assert np.array_equal(a < (1 << 63), (line % 6) < 3)
+
+
+def _succ_heavy(pred: np.ndarray) -> bool:
+    """Lemma 3.1: every t-prefix holds >= t/4 successors."""
+    succ = np.cumsum(~pred)
+    t = np.arange(1, pred.size + 1)
+    return bool(np.all(4 * succ >= t))
+
+
+@pytest.mark.parametrize("rev", [False, True])
+def test_bps_make_successor_heavy_lemma(rev):
+    """MakeSuccessorHeavy: on every predecessor/successor
+    pattern with at least half successors (in the view), the result is a
+    permutation of the input whose every prefix is successor-heavy."""
+    for n in range(0, 13):
+        for mask in range(1 << n):
+            bits = np.array([(mask >> i) & 1 for i in range(n)], dtype=bool)  # True = view predecessor
+            if 2 * int(bits.sum()) > n:
+                continue  # the phase requires >= half successors (PAPER.md:326-332)
+            idx = np.arange(n, dtype=np.uint64)
+            # keys: view predecessor <=> key < 1000 (rev: view predecessor <=> key >= 1000)
+            pred_key = bits if not rev else ~bits
+            a = np.where(pred_key, idx, idx + 1000).astype(np.uint64)
+            if rev:
+                a = a[::-1].copy()
+            b = a.copy()
+            oracle.bps_make_successor_heavy(b, 1000, rev)
+            assert np.array_equal(np.sort(a), np.sort(b))
+            view = b[::-1] if rev else b
+            vpred = (view < 1000) if not rev else (view >= 1000)
+            assert _succ_heavy(vpred), (n, mask, rev)
+
+
+@pytest.mark.parametrize("B", [1, 2, 3, 4, 8])
+def test_bps_partition_bruteforce(B):
+    """The Blocked-Prefix-Sum partition (low-space form
+    PAPER.md:1466-1486): every 2^n pattern for n <= 12 (tagged keys, both
+    role-swap sides), block sizes 1..8 so the Reorder recursion runs several
+    levels; (1)-(3) hold and no Reorder swap broke Lemma 3.4 (the oracle
+    raises if one did)."""
+    for n in range(0, 13):
+        for mask in range(1 << n):
+            bits = np.array([(mask >> i) & 1 for i in range(n)], dtype=bool)
+            idx = np.arange(n, dtype=np.uint64)
+            a = np.where(bits, idx, idx + 1000).astype(np.uint64)
+            b = a.copy()
+            k = oracle.partition_bps(b, 1000, B)
+            oracle.check_partition(a, b, 1000, k)
+
+
+@pytest.mark.parametrize("dt", [np.uint64, np.uint32])
+def test_bps_partition_random(dt):
+    """Larger random and duplicate-heavy arrays, several pivots and block
+    sizes (deep Reorder recursions), ragged last blocks."""
+    rng = np.random.default_rng(77)
+    mx = (1 << 64) - 1 if dt == np.uint64 else (1 << 32) - 1
+    for n in (0, 1, 5, 97, 1000, 4096, 4097, 20001, 100003):
+        for a in (rng.integers(0, mx, size=n, dtype=dt, endpoint=True), rng.integers(0, 4, size=n).astype(dt)):
+            for p in (0, 1, 2, mx // 100, mx // 2, mx - mx // 100, mx):
+                for B in (4, 64, 4096):
+                    b = a.copy()
+                    k = oracle.partition_bps(b, p, B)
+                    oracle.check_partition(a, b, p, k)
