@@ -73,6 +73,23 @@ pp_status pp_partition_async_u32(uint32_t *keys, uint64_t n, uint32_t pivot, voi
 pp_status pp_quicksort_u64(uint64_t *keys, uint64_t n, void *stream);
 pp_status pp_quicksort_u32(uint32_t *keys, uint64_t n, void *stream);
 
+/* ---- the paper's Blocked-Prefix-Sum partition (low-space form) -----------
+ * PAPER.md:319-478 (§3, Figs. 1-2) as the paper's "low-space implementation"
+ * (PAPER.md:1466-1486): role swap when fewer than half of the keys are
+ * successors (the view is the reversed array),
+ * MakeSuccessorHeavy in place (Fig. 1), block prefix sums over blocks of 4096
+ * keys kept in an explicit array (the bit-pair codec of Lemma 3.2 is not
+ * used), the recursive in-place Reorder (Fig. 2).  keys: DEVICE pointer to n
+ * keys, partitioned in place by key < pivot; the arrangement is the
+ * algorithm's (deterministic; equals the CPU oracle's byte for byte).
+ * Several passes over the array (count, ~2n for MakeSuccessorHeavy, block
+ * counts, Reorder): the comparison row of SURVEY §8(f) #3, not the fast path.
+ * Aux: 12 bytes per 4096 keys + O(1).  split_out: HOST pointer (sync);
+ * d_split: DEVICE word (async, no host synchronisation). */
+pp_status pp_partition_bps_u64(uint64_t *keys, uint64_t n, uint64_t pivot, void *stream, uint64_t *split_out);
+pp_status pp_partition_bps_u32(uint32_t *keys, uint64_t n, uint32_t pivot, void *stream, uint64_t *split_out);
+pp_status pp_partition_bps_async_u64(uint64_t *keys, uint64_t n, uint64_t pivot, void *stream, uint64_t *d_split);
+
 /* ---- the Standard Algorithm: stable, OUT-OF-PLACE partition ---------------
  * PAPER.md:284-311 (§2): D[i] = [in[i] < pivot], S = prefix sums of D, t =
  * S[n-1]; predecessor i -> out[S[i]-1], successor i -> out[t + i - S[i]]

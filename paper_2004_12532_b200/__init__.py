@@ -15,6 +15,7 @@ Function names mirror the C ABI:
     pp_quicksort_host_u64(np_array)
     pp_partition(keys, pivot) / pp_quicksort(keys)         (dtype dispatch)
     pp_partition_stable(keys_in, keys_out, pivot) -> split (Standard Algorithm, out of place)
+    pp_partition_bps(keys, pivot) -> split           (Blocked-Prefix-Sum, low-space form)
     pp_ss_groups(keys, pivot, g=0) -> (T, vlo, vhi, info)
 
 int64/int32 tensors are treated as their unsigned bit patterns (torch lacks
@@ -75,6 +76,9 @@ def load(build_if_missing: bool = True):
         "pp_quicksort_u32": ([vp, u64, vp], st),
         "pp_partition_host_u64": ([vp, u64, u64, P64], st),
         "pp_partition_stable_u64": ([vp, vp, u64, u64, vp, P64], st),
+        "pp_partition_bps_u64": ([vp, u64, u64, vp, P64], st),
+        "pp_partition_bps_u32": ([vp, u64, u32, vp, P64], st),
+        "pp_partition_bps_async_u64": ([vp, u64, u64, vp, vp], st),
         "pp_partition_stable_u32": ([vp, vp, u64, u32, vp, P64], st),
         "pp_partition_stable_async_u64": ([vp, vp, u64, u64, vp, vp], st),
         "pp_partition_host_u32": ([vp, u64, u32, P64], st),
@@ -188,6 +192,23 @@ def pp_quicksort_u64(keys, stream=None) -> None:
 def pp_quicksort_u32(keys, stream=None) -> None:
     assert _key_kind(keys) == "u32"
     _check(load().pp_quicksort_u32(keys.data_ptr(), keys.numel(), _stream_ptr(stream)), "pp_quicksort_u32")
+
+
+def pp_partition_bps(keys, pivot: int, stream=None) -> int:
+    """The paper's Blocked-Prefix-Sum partition, low-space form
+    (PAPER.md:319-478, 1466-1486), in place; returns the split."""
+    kind = _key_kind(keys)
+    out = ctypes.c_uint64(0)
+    f = load().pp_partition_bps_u64 if kind == "u64" else load().pp_partition_bps_u32
+    _check(f(keys.data_ptr(), keys.numel(), _pivot(pivot, kind), _stream_ptr(stream), ctypes.byref(out)),
+           "pp_partition_bps")
+    return int(out.value)
+
+
+def pp_partition_bps_async_u64(keys, pivot: int, d_split, stream=None) -> None:
+    assert _key_kind(keys) == "u64" and d_split.is_cuda
+    _check(load().pp_partition_bps_async_u64(keys.data_ptr(), keys.numel(), _pivot(pivot, "u64"),
+                                             _stream_ptr(stream), d_split.data_ptr()), "pp_partition_bps_async_u64")
 
 
 def pp_partition_stable(keys_in, keys_out, pivot: int, stream=None) -> int:

@@ -82,6 +82,16 @@ void* workspace(size_t bytes, cudaStream_t st) {
     return g_ws;
 }
 
+// one device word for the split of synchronous calls that need it
+static void* host_split_slot() {
+    static void* p = nullptr;
+    if (!p && cudaMalloc(&p, 256) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+    }
+    return p;
+}
+
 // pinned host word for split readback
 static uint64_t* pinned_word() {
     static uint64_t* p = nullptr;
@@ -209,6 +219,44 @@ static pp_status partition_stable(const K* in, K* out, uint64_t n, K pivot, void
     cudaError_t e = cudaMemcpyAsync(pw, total, 8, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "stable partition");
+    *split_out = *pw;
+    return PP_OK;
+}
+
+// Blocked-Prefix-Sum partition (pp_bps.cu), in place; sync (split_out) or
+// async (d_split).
+template <typename K>
+static pp_status partition_bps(K* keys, uint64_t n, K pivot, void* stream, uint64_t* split_out, uint64_t* d_split) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!split_out && !d_split) {
+        set_error("split_out / d_split is NULL");
+        return PP_E_INVAL;
+    }
+    pp_status s = check_device_keys(keys, n);
+    if (s != PP_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    g_last_ctl = nullptr;
+    if (n == 0) {
+        g_stats = LastStats();
+        if (split_out) *split_out = 0;
+        if (d_split) {
+            const cudaError_t e = cudaMemsetAsync(d_split, 0, sizeof(uint64_t), st);
+            if (e != cudaSuccess) return cuda_fail(e, "memset");
+        }
+        return PP_OK;
+    }
+    if (d_split) return partition_bps_device<K>(keys, n, pivot, st, d_split);
+    uint64_t* pw = pinned_word();
+    uint64_t* dk = static_cast<uint64_t*>(host_split_slot());
+    if (!pw || !dk) {
+        set_error("split buffers unavailable");
+        return PP_E_NOMEM;
+    }
+    s = partition_bps_device<K>(keys, n, pivot, st, dk);
+    if (s != PP_OK) return s;
+    cudaError_t e = cudaMemcpyAsync(pw, dk, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "bps partition");
     *split_out = *pw;
     return PP_OK;
 }
@@ -434,6 +482,15 @@ pp_status pp_partition_stable_u64(const uint64_t* in, uint64_t* out, uint64_t n,
 pp_status pp_partition_stable_u32(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t pivot, void* stream,
                                   uint64_t* split_out) {
     return partition_stable<uint32_t>(in, out, n, pivot, stream, split_out, nullptr);
+}
+pp_status pp_partition_bps_u64(uint64_t* keys, uint64_t n, uint64_t pivot, void* stream, uint64_t* split_out) {
+    return partition_bps<uint64_t>(keys, n, pivot, stream, split_out, nullptr);
+}
+pp_status pp_partition_bps_u32(uint32_t* keys, uint64_t n, uint32_t pivot, void* stream, uint64_t* split_out) {
+    return partition_bps<uint32_t>(keys, n, pivot, stream, split_out, nullptr);
+}
+pp_status pp_partition_bps_async_u64(uint64_t* keys, uint64_t n, uint64_t pivot, void* stream, uint64_t* d_split) {
+    return partition_bps<uint64_t>(keys, n, pivot, stream, nullptr, d_split);
 }
 pp_status pp_partition_stable_async_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t pivot,
                                         void* stream, uint64_t* d_split) {

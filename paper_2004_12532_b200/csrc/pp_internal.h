@@ -87,6 +87,10 @@ pp_status ss_groups_device(K* keys, uint64_t n, K pivot, uint64_t g, cudaStream_
 template <typename K>
 pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st);
 
+// the paper's Blocked-Prefix-Sum partition, low-space form (pp_bps.cu)
+template <typename K>
+pp_status partition_bps_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split);
+
 // the Standard Algorithm, stable and out of place (pp_stable.cu)
 template <typename K>
 pp_status partition_stable_device(const K* in, K* out, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split,

@@ -499,3 +499,40 @@ def test_standard_algorithm_rejects_overlap(pp):
     t = torch.zeros(64, dtype=torch.int64, device="cuda")
     out = ctypes.c_uint64(0)
     assert L.pp_partition_stable_u64(t.data_ptr(), t.data_ptr() + 8 * 8, 32, 5, None, ctypes.byref(out)) == 1
+
+
+@pytest.mark.parametrize("dt", [np.uint64, np.uint32])
+def test_bps_bytewise(pp, dt):
+    """the GPU Blocked-Prefix-Sum partition (low-space form,
+    PAPER.md:319-478, 1466-1486) equals the CPU oracle's byte for byte (the
+    algorithm is deterministic): sizes around the 4096-key block and the
+    one-CTA MakeSuccessorHeavy threshold, both sides of the role swap,
+    duplicates, pivot extremes, unaligned bases."""
+    from gpu_util import to_dev, to_host
+    rng = np.random.default_rng(41)
+    mx = U64_MAX if dt == np.uint64 else U32_MAX
+    for n in (0, 1, 2, 3, 100, 4095, 4096, 4097, 8191, 20480, 20481, 40000, 100003, 1 << 20, 3_000_017):
+        for a in (rng.integers(0, mx, size=n, dtype=dt, endpoint=True), rng.integers(0, 4, size=n).astype(dt)):
+            for p in sorted({0, 1, 2, mx // 100, mx // 2, mx - mx // 100, mx}):
+                ref = a.copy()
+                k_ref = oracle.partition_bps(ref, p, 4096)
+                t = to_dev(a)
+                k = pp.pp_partition_bps(t, p)
+                assert k == k_ref, (n, p)
+                assert np.array_equal(to_host(t, dt), ref), (n, p)
+
+
+def test_bps_config2(pp):
+    """Config 2 (2^27 u64, the three pivots), async variant: byte for byte
+    against the oracle."""
+    from gpu_util import to_host
+    n = 1 << 27
+    a = synth.uniform_u64_np(n, synth.SEEDS["c2"])
+    d = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for mu, p in synth.PIVOT_MU.items():
+        t = synth.uniform_u64_torch(n, synth.SEEDS["c2"], "cuda")
+        pp.pp_partition_bps_async_u64(t, p, d)
+        ref = a.copy()
+        k_ref = oracle.partition_bps(ref, p, 4096)
+        assert int(d.item()) == k_ref
+        assert np.array_equal(to_host(t, np.uint64), ref), mu
