@@ -947,7 +947,7 @@ static QsGeom qs_geom() {
     QsGeom q;
     // leaf capacity: default LC::LEAF (8192 keys); "leaf" may lower it
     q.LEAF = (P.leaf > 0 && (uint64_t)P.leaf <= (uint64_t)LC::LEAF) ? (uint64_t)P.leaf : (uint64_t)LC::LEAF;
-    q.BIG = P.qs_cta_max > 0 ? (uint64_t)P.qs_cta_max : (uint64_t)1 << 25;
+    q.BIG = P.qs_cta_max > 0 ? (uint64_t)P.qs_cta_max : (uint64_t)1 << 27;
     q.SMALL = P.qs_small > 0 ? std::max<uint64_t>((uint64_t)P.qs_small, q.LEAF) : q.LEAF;
     q.HEAVY = P.qs_heavy > 0 ? std::max<uint64_t>((uint64_t)P.qs_heavy, q.SMALL + 1) : 0;
     int occ = 1;

@@ -1,10 +1,10 @@
 #!/usr/bin/env bash
 # One GPU session: tests, smoke, bench, launch list, one full ncu capture.
 #   gpurun --timeout 3000 -- 'bash tools/gpu_round.sh [tag] [what]'
-# what: any of tests,smoke,bench,launches,ncu (comma separated; default all)
+# what: any of tests,smoke,bench,launches,qs,ncu (comma separated; default all)
 set -u
 TAG=${1:-r01}
-WHAT=${2:-tests,smoke,bench,launches,ncu}
+WHAT=${2:-tests,smoke,bench,launches,qs,ncu}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > "$OUT/gpu.txt" 2>&1
@@ -29,6 +29,15 @@ if has launches; then
     --log-file "$OUT/launches.csv" python bench.py --steps 3 --warmup 3 --no-extras --no-cpu-baseline --no-e2e \
     > "$OUT/ncu_launches.log" 2>&1
   echo "launches exit $?" >> "$OUT/status.txt"
+fi
+if has qs; then
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+    --log-file "$OUT/launches_qs_uniform.csv" python tools/profile_quicksort.py --reps 1 --kind uniform \
+    > "$OUT/ncu_qs.log" 2>&1
+  echo "launches_qs exit $?" >> "$OUT/status.txt"
+  PP_QS_PROF=1 timeout 300 python tools/profile_quicksort.py --reps 2 --kind uniform > "$OUT/qs_levels_uniform.log" 2>&1
+  PP_QS_PROF=1 timeout 300 python tools/profile_quicksort.py --reps 2 --kind dup1000 > "$OUT/qs_levels_dup1000.log" 2>&1
+  echo "qs_levels exit $?" >> "$OUT/status.txt"
 fi
 if has ncu; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:ss_group -s 1 -c 1 \
