@@ -973,7 +973,8 @@ uint64_t quicksort_workspace_bound(uint64_t n) {
     const uint64_t cl = std::min<uint64_t>(n / 2 + 1, QS_LIST_CHUNK);
     const uint64_t cs = std::min<uint64_t>(n / (q.LEAF + 1) + 1, QS_LIST_CHUNK);
     // bin slots of one chunk of small segments: sum of qs_bin_cap <= 2 n / LEAF + 6 per segment
-    const uint64_t nslot = std::min<uint64_t>(2 * (n / q.LEAF) + 6 * cs, cs * qs_bin_cap(q.SMALL, q.LEAF));
+    // bin slots of all small segments: sum of qs_bin_cap <= 2 n / LEAF + 6 per segment
+    const uint64_t nslot = 2 * (n / q.LEAF) + 6 * (n / (q.LEAF + 1) + 1) + 6;
     const size_t lists = al256(8 * cl) + al256(4 * cl) + al256(8 * cs) + al256(4 * cs) + al256(8 * cs) +
                          al256(sizeof(GroupOut) * cs) + al256(8 * nslot) + al256(4 * nslot) + 256;
     return std::max(level, lists);
@@ -1242,17 +1243,12 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     //      uploaded in chunks of QS_LIST_CHUNK (stream order makes reuse safe) ----
     const uint64_t nleaf = leaf_lo.size(), nsmall = small_lo.size();
     const uint64_t cl = std::min<uint64_t>(nleaf, QS_LIST_CHUNK), cs = std::min<uint64_t>(nsmall, QS_LIST_CHUNK);
+    // bin slots of every small segment (global offsets: chunks of the
+    // per-CTA recursion and their bin sorts are pipelined on two streams, so
+    // no chunk reuses another's slots)
     std::vector<uint64_t> small_base(nsmall + 1, 0);
-    uint64_t max_slots = 0;
-    for (uint64_t b0 = 0; b0 < nsmall; b0 += QS_LIST_CHUNK) {
-        const uint64_t cnt = std::min<uint64_t>(nsmall - b0, QS_LIST_CHUNK);
-        uint64_t acc = 0;
-        for (uint64_t i = 0; i < cnt; ++i) {
-            small_base[b0 + i] = acc;
-            acc += qs_bin_cap(small_len[b0 + i], LEAF);
-        }
-        max_slots = std::max(max_slots, acc);
-    }
+    for (uint64_t i = 0; i < nsmall; ++i) small_base[i + 1] = small_base[i] + qs_bin_cap(small_len[i], LEAF);
+    const uint64_t max_slots = small_base[nsmall];
     const size_t loB = al256(8 * cl), lnB = al256(4 * cl), sloB = al256(8 * cs), slnB = al256(4 * cs);
     const size_t sbB = al256(8 * cs), scrB = al256(sizeof(GroupOut) * cs);
     const size_t bloB = al256(8 * max_slots), blnB = al256(4 * max_slots);
@@ -1260,35 +1256,35 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         static_cast<unsigned char*>(qs_workspace(loB + lnB + sloB + slnB + sbB + scrB + bloB + blnB + 256));
     if (!qws) return PP_E_NOMEM;
     // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot
-    auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt) -> cudaError_t {
+    auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
         const int64_t algo = P.leaf_algo == 0 ? 3 : P.leaf_algo;  // default: merge sort
         if (algo == 2) {
             constexpr int NW = LC::LEAF / 256;
             const size_t smem = sizeof(K) * LC::LEAF + 2 * 256 * NW;
             cudaFuncSetAttribute(qs_leaf_radix_kernel<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_radix_kernel<K, NW><<<(unsigned)cnt, NW * 32, smem, st>>>(keys, d_lo, d_len);
+            qs_leaf_radix_kernel<K, NW><<<(unsigned)cnt, NW * 32, smem, bst>>>(keys, d_lo, d_len);
         } else if (algo == 1) {
             const size_t smem = sizeof(K) * LC::LEAF;
             cudaFuncSetAttribute(qs_leaf_kernel<K, LC::LEAF, LC::NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo, d_len);
+            qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, bst>>>(keys, d_lo, d_len);
         } else if (LEAF <= (uint64_t)LC::LEAF / 4) {  // small bins: quarter-size CTAs, more per SM
             constexpr int QL = LC::LEAF / 4, QN = QL / LEAF_E;
             const size_t smem = sizeof(K) * (QL + QL / 8);
             cudaFuncSetAttribute(qs_leaf_merge_kernel<K, QL, QN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            qs_leaf_merge_kernel<K, QL, QN><<<(unsigned)cnt, QN, smem, st>>>(keys, d_lo, d_len);
+            qs_leaf_merge_kernel<K, QL, QN><<<(unsigned)cnt, QN, smem, bst>>>(keys, d_lo, d_len);
         } else if (LEAF <= (uint64_t)LC::LEAF / 2) {  // half-size CTAs
             constexpr int HL = LC::LEAF / 2, HN = HL / LEAF_E;
             const size_t smem = sizeof(K) * (HL + HL / 8);
             cudaFuncSetAttribute(qs_leaf_merge_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, st>>>(keys, d_lo, d_len);
+            qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, bst>>>(keys, d_lo, d_len);
         } else {
             const size_t smem = sizeof(K) * (LC::LEAF + LC::LEAF / 8);
             cudaFuncSetAttribute(qs_leaf_merge_kernel<K, LC::LEAF, LC::NT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, st>>>(keys, d_lo, d_len);
+            qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, bst>>>(keys, d_lo, d_len);
         }
         note_launches(1);
         return cudaGetLastError();
@@ -1304,9 +1300,22 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         uint64_t* d_prof = nullptr;  // debug phase profile (env PP_QS_PROF)
         static const bool qs_prof = getenv("PP_QS_PROF") != nullptr;
         if (qs_prof) cudaMalloc(&d_prof, 64 * cs);
-        for (uint64_t b0 = 0; b0 < nsmall; b0 += QS_LIST_CHUNK) {
-            const uint64_t cnt = std::min<uint64_t>(nsmall - b0, QS_LIST_CHUNK);
-            const uint64_t nslots = small_base[b0 + cnt - 1] + qs_bin_cap(small_len[b0 + cnt - 1], LEAF);
+        // pipeline: chunk c's bins are sorted on a second stream while the
+        // per-CTA recursion of chunk c+1 runs (disjoint segments)
+        static cudaStream_t st2 = nullptr;
+        static std::vector<cudaEvent_t> evs;
+        if (!st2) cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking);
+        const uint64_t pipe = (uint64_t)std::max<int64_t>(P.qs_pipe, 1);
+        const uint64_t chunk = std::min<uint64_t>(QS_LIST_CHUNK, std::max<uint64_t>(1, (nsmall + pipe - 1) / pipe));
+        const uint64_t nchunks = (nsmall + chunk - 1) / chunk;
+        while (evs.size() < nchunks + 1) {
+            cudaEvent_t ev;
+            cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            evs.push_back(ev);
+        }
+        for (uint64_t c = 0, b0 = 0; b0 < nsmall; ++c, b0 += chunk) {
+            const uint64_t cnt = std::min<uint64_t>(nsmall - b0, chunk);
+            const uint64_t slot0 = small_base[b0], nslots = small_base[b0 + cnt] - slot0;
             e = cudaMemcpyAsync(d_slo, small_lo.data() + b0, 8 * cnt, cudaMemcpyHostToDevice, st);
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(d_sln, small_len.data() + b0, 4 * cnt, cudaMemcpyHostToDevice, st);
@@ -1340,9 +1349,14 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                         (double)tot[3], (double)tot[2], (unsigned long long)tot[4], (unsigned long long)tot[5],
                         (unsigned long long)tot[6], (unsigned long long)tot[7]);
             }
-            e = sort_bins(d_blo, d_bln, nslots);
+            e = cudaEventRecord(evs[c], st);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(st2, evs[c], 0);
+            if (e == cudaSuccess) e = sort_bins(d_blo + slot0, d_bln + slot0, nslots, st2);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort bin sort launch");
         }
+        e = cudaEventRecord(evs[nchunks], st2);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, evs[nchunks], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort pipeline join");
         if (d_prof) cudaFree(d_prof);
     }
     if (nleaf > 0) {
@@ -1353,7 +1367,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             e = cudaMemcpyAsync(d_lo, leaf_lo.data() + b0, 8 * cnt, cudaMemcpyHostToDevice, st);
             if (e == cudaSuccess) e = cudaMemcpyAsync(d_len, leaf_len.data() + b0, 4 * cnt, cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort leaves H2D");
-            e = sort_bins(d_lo, d_len, cnt);
+            e = sort_bins(d_lo, d_len, cnt, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort leaf launch");
         }
     }
