@@ -512,7 +512,7 @@ template <typename K> struct VariantCfg<K, 6> { using type = GroupCfgT<K, 8192, 
 // the "strided" param (seed 0), not by "variant"
 template <typename K> struct VariantCfg<K, 7> {
     using D = GroupCfg<K>;
-    using type = GroupCfgT<K, D::LK * (int)sizeof(K), D::NT, D::PF, D::TMA_STORE, true>;
+    using type = GroupCfgT<K, D::LK * (int)sizeof(K), D::NT, D::PF, D::TMA_STORE, true, D::PAR_ISSUE>;
 };
 constexpr int N_VARIANTS = 7;
 constexpr int STRIDED_VARIANT = 7;

@@ -21,17 +21,21 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--n", type=int, default=27)
+    ap.add_argument("--dtype", default="u64")
     args = ap.parse_args()
     pp.load(build_if_missing=False)
     pp.reset_params()
     pp.pp_set_param("variant", args.variant)
     n = 1 << args.n
     dev = torch.device("cuda")
-    pristine = synth.uniform_u64_torch(n, synth.SEEDS["c2"], dev)
+    if args.dtype == "u64":
+        pristine, piv = synth.uniform_u64_torch(n, synth.SEEDS["c2"], dev), 1 << 63
+    else:
+        pristine, piv = synth.uniform_u32_torch(n, synth.SEEDS["c2"], dev), 1 << 31
     buf = torch.empty_like(pristine)
     for _ in range(args.reps):
         buf.copy_(pristine)
-        split = pp.pp_partition_u64(buf, 1 << 63)
+        split = pp.pp_partition(buf, piv)
     torch.cuda.synchronize()
     print("split", split, pp.pp_last_stats())
 
