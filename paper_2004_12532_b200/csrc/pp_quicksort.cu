@@ -267,6 +267,7 @@ __device__ __forceinline__ void cmpx(K& a, K& b) {
 // so that a warp whose lanes each own 8 consecutive keys hits distinct banks
 // (stride 9 words instead of 8).
 __device__ __forceinline__ uint32_t lpad(uint32_t i) { return i + (i >> 3); }
+static inline uint32_t lpad_host(uint32_t i) { return i + (i >> 3); }
 
 template <typename K>
 __device__ __forceinline__ void sort8(K (&v)[8]) {  // Batcher's 19-comparator network
@@ -372,6 +373,32 @@ __device__ __forceinline__ void warp_sort256(K (&v)[8]) {
     }
 }
 
+// Sorts the P (a multiple of 256) keys of a padded shared-memory buffer
+// (index lpad(i)) with nthr = P/8 threads: 8 consecutive keys per thread
+// sorted in registers, runs of 256 per warp by the shuffle bitonic merge,
+// then merge rounds in place (outputs staged in registers across a barrier).
+// Ends with a barrier: buf holds the sorted keys.
+template <typename K>
+__device__ __forceinline__ void smem_merge_sort(K* buf, uint32_t P, uint32_t nthr) {
+    const uint32_t base = threadIdx.x * LEAF_E;
+    K v[LEAF_E];
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) v[r] = buf[lpad(base + r)];
+    sort8(v);
+    warp_sort256(v);  // runs of 256 (one warp) sorted in registers
+    leaf_bar(nthr);
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) buf[lpad(base + r)] = v[r];
+    leaf_bar(nthr);
+    for (uint32_t L = 32 * LEAF_E; L < P; L <<= 1) {
+        merge_chunk_regs<K>(buf, base, L, P, v);
+        leaf_bar(nthr);
+#pragma unroll
+        for (int r = 0; r < LEAF_E; ++r) buf[lpad(base + r)] = v[r];
+        leaf_bar(nthr);
+    }
+}
+
 // Sort of one bin (a contiguous range of <= LEAF keys; len 0 = empty slot) by
 // merging in ONE padded shared-memory buffer: every thread loads its keys
 // (all loads in flight), sorts 8 consecutive keys in registers (Batcher's
@@ -406,27 +433,131 @@ __global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
         for (int r = 0; r < LEAF_E; ++r) buf[lpad((uint32_t)r * nthr + tid)] = v[r];
     }
     leaf_bar(nthr);
-    const uint32_t base = tid * LEAF_E;
-    K v[LEAF_E];
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) v[r] = buf[lpad(base + r)];
-    sort8(v);
-    warp_sort256(v);  // runs of 256 (one warp) sorted in registers
-    leaf_bar(nthr);
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) buf[lpad(base + r)] = v[r];
-    leaf_bar(nthr);
-    for (uint32_t L = 32 * LEAF_E; L < P; L <<= 1) {
-        merge_chunk_regs<K>(buf, base, L, P, v);
-        leaf_bar(nthr);
-#pragma unroll
-        for (int r = 0; r < LEAF_E; ++r) buf[lpad(base + r)] = v[r];
-        leaf_bar(nthr);
-    }
+    smem_merge_sort<K>(buf, P, nthr);
 #pragma unroll
     for (int r = 0; r < LEAF_E; ++r) {
         const uint32_t i = (uint32_t)r * nthr + tid;
         if (i < len) __stcs(keys + lo + i, buf[lpad(i)]);
+    }
+}
+
+// Bin sort for u64 keys through 32-bit packed values: p = (top << 13) | i,
+// top = the 19 high bits of (key - min) over the bin's range (all of it when
+// the range has <= 19 bits), i = the key's position in the bin (< 8192).
+// The packed values are sorted with the same machinery as the keys
+// (smem_merge_sort) at about half the instructions (32-bit compare-exchange
+// and shuffles); the keys are gathered by index; runs of equal `top` are
+// then put in key order by the thread owning the run's first slot (insertion
+// sort; runs of equal keys are already in order).  A run of > 64 distinct
+// keys sharing `top` (keys clustered inside a wide range) sends the whole bin
+// to the 64-bit merge sort instead.  Shared memory: the keys (64 KiB), the
+// packed buffer (36 KiB) and the output (72 KiB, also the fallback's buffer).
+constexpr int PK_LEAF = 8192, PK_NT = PK_LEAF / LEAF_E, PK_IDX_BITS = 13, PK_TOP_BITS = 32 - PK_IDX_BITS;
+constexpr uint32_t PK_MAX_RUN = 64;
+__global__ void __launch_bounds__(PK_NT) qs_leaf_packed_kernel(uint64_t* __restrict__ keys,
+                                                               const uint64_t* __restrict__ leaf_lo,
+                                                               const uint32_t* __restrict__ leaf_len) {
+    extern __shared__ __align__(16) unsigned char lsm[];
+    uint64_t* ks = reinterpret_cast<uint64_t*>(lsm);          // [PK_LEAF] original keys
+    uint64_t* ob = ks + PK_LEAF;                              // [lpad(PK_LEAF)] output / fallback buffer
+    uint32_t* pb = reinterpret_cast<uint32_t*>(ob + lpad(PK_LEAF));  // [lpad(PK_LEAF)] packed
+    __shared__ uint64_t rmn[32], rmx[32];
+    __shared__ int fallback;
+    const uint64_t lo = leaf_lo[blockIdx.x];
+    const uint32_t len = leaf_len[blockIdx.x];
+    const uint32_t P = (len + 32 * LEAF_E - 1) / (32 * LEAF_E) * (32 * LEAF_E);
+    const uint32_t nthr = P / LEAF_E;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid >= nthr) return;
+    uint64_t x[LEAF_E];
+    uint64_t mn = ~0ull, mx = 0;
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) {
+        const uint32_t i = (uint32_t)r * nthr + tid;
+        x[r] = i < len ? __ldcs(keys + lo + i) : 0ull;
+        if (i < len) {
+            ks[i] = x[r];
+            mn = x[r] < mn ? x[r] : mn;
+            mx = x[r] > mx ? x[r] : mx;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+    }
+    if (lane == 0) {
+        rmn[warp] = mn;
+        rmx[warp] = mx;
+    }
+    if (tid == 0) fallback = 0;
+    leaf_bar(nthr);
+    for (uint32_t w = 0; w < nthr / 32; ++w) {
+        mn = rmn[w] < mn ? rmn[w] : mn;
+        mx = rmx[w] > mx ? rmx[w] : mx;
+    }
+    if (mn == mx) return;  // all keys equal: sorted already (uniform over the CTA)
+    const int bits = 64 - __clzll((long long)(mx - mn));
+    const int sh = bits > PK_TOP_BITS ? bits - PK_TOP_BITS : 0;
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) {
+        const uint32_t i = (uint32_t)r * nthr + tid;
+        pb[lpad(i)] = i < len ? ((uint32_t)((x[r] - mn) >> sh) << PK_IDX_BITS) | i : 0xFFFFFFFFu;
+    }
+    leaf_bar(nthr);
+    smem_merge_sort<uint32_t>(pb, P, nthr);
+    // gather the keys in packed order
+    const uint32_t base = tid * LEAF_E;
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) {
+        const uint32_t j = base + r;
+        if (j < len) ob[lpad(j)] = ks[pb[lpad(j)] & ((1u << PK_IDX_BITS) - 1)];
+    }
+    leaf_bar(nthr);
+    // runs of equal top: the owner of the run's first slot orders it
+#pragma unroll 1
+    for (int r = 0; r < LEAF_E; ++r) {
+        const uint32_t j = base + r;
+        if (j + 1 >= len) break;
+        const uint32_t t = pb[lpad(j)] >> PK_IDX_BITS;
+        if ((pb[lpad(j + 1)] >> PK_IDX_BITS) != t) continue;
+        if (j > 0 && (pb[lpad(j - 1)] >> PK_IDX_BITS) == t) continue;  // not the first slot of its run
+        uint32_t e = j + 1;
+        bool sorted = true;
+        while (e < len && (pb[lpad(e)] >> PK_IDX_BITS) == t) {
+            if (ob[lpad(e)] < ob[lpad(e - 1)]) sorted = false;
+            ++e;
+        }
+        if (sorted) continue;
+        if (e - j > PK_MAX_RUN) {
+            fallback = 1;
+            continue;
+        }
+        for (uint32_t a = j + 1; a < e; ++a) {  // insertion sort of ob[j, e)
+            const uint64_t v = ob[lpad(a)];
+            uint32_t b = a;
+            while (b > j && ob[lpad(b - 1)] > v) {
+                ob[lpad(b)] = ob[lpad(b - 1)];
+                --b;
+            }
+            ob[lpad(b)] = v;
+        }
+    }
+    leaf_bar(nthr);
+    if (fallback) {  // uniform: sort the original keys with 64-bit compares
+#pragma unroll
+        for (int r = 0; r < LEAF_E; ++r) {
+            const uint32_t i = (uint32_t)r * nthr + tid;
+            ob[lpad(i)] = i < len ? ks[i] : ~0ull;
+        }
+        leaf_bar(nthr);
+        smem_merge_sort<uint64_t>(ob, P, nthr);
+    }
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) {
+        const uint32_t i = (uint32_t)r * nthr + tid;
+        if (i < len) __stcs(keys + lo + i, ob[lpad(i)]);
     }
 }
 
@@ -1257,8 +1388,13 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     if (!qws) return PP_E_NOMEM;
     // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot
     auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
-        const int64_t algo = P.leaf_algo == 0 ? 3 : P.leaf_algo;  // default: merge sort
-        if (algo == 2) {
+        // default: packed 32-bit sort for u64 bins of up to 8192 keys, else merge sort
+        const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : (sizeof(K) == 8 && LEAF > LC::LEAF / 2 ? 4 : 3);
+        if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF) {
+            const size_t smem = 8 * PK_LEAF + 8 * lpad_host(PK_LEAF) + 4 * lpad_host(PK_LEAF);
+            cudaFuncSetAttribute(qs_leaf_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_packed_kernel<<<(unsigned)cnt, PK_NT, smem, bst>>>(reinterpret_cast<uint64_t*>(keys), d_lo, d_len);
+        } else if (algo == 2) {
             constexpr int NW = LC::LEAF / 256;
             const size_t smem = sizeof(K) * LC::LEAF + 2 * 256 * NW;
             cudaFuncSetAttribute(qs_leaf_radix_kernel<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -126,3 +126,35 @@ def test_config5_full(pp, kind):
         lo = oracle.count(inp_host, v)
         hi = oracle.count(inp_host, v + 1) if v < U64_MAX else n
         assert lo <= r < hi, r
+
+
+@pytest.mark.parametrize("leaf_algo", [0, 2, 3, 4])
+def test_bin_sorts_clustered(pp, leaf_algo):
+    """Bins whose keys cluster inside a wide range: the packed 32-bit bin sort
+    (leaf_algo 4, the u64 default) sees runs of equal top bits -- short runs
+    are insertion-sorted, a run of > 64 distinct keys falls back to the
+    64-bit merge sort -- and every bin sort gives the oracle's order."""
+    rng = np.random.default_rng(9)
+    cases = []
+    # 100 clusters of 50 distinct keys each + the maximum: runs of 50 equal tops
+    cl = (np.arange(100, dtype=np.uint64)[:, None] << np.uint64(40)) + np.arange(50, dtype=np.uint64)[None, :]
+    cases.append(np.concatenate([cl.reshape(-1), np.array([U64_MAX], dtype=np.uint64)]))
+    # one cluster of 6000 distinct small keys + two huge ones: a run of 6000 -> fallback
+    cases.append(np.concatenate([np.arange(6000, dtype=np.uint64), np.array([1 << 63, U64_MAX], dtype=np.uint64)]))
+    # clusters of 80 (just above the run limit) and of 64 (at it)
+    for w in (80, 64, 65):
+        c = (np.arange(60, dtype=np.uint64)[:, None] << np.uint64(45)) + np.arange(w, dtype=np.uint64)[None, :]
+        cases.append(np.concatenate([c.reshape(-1), np.array([U64_MAX - 5], dtype=np.uint64)]))
+    # duplicates of few values spread over the whole range
+    cases.append(rng.choice(np.array([0, 5, 1 << 40, 1 << 63, U64_MAX], dtype=np.uint64), size=8000))
+    for a in cases:
+        a = a[rng.permutation(a.size)]
+        for n in (a.size, min(a.size, 8192), 300):
+            b = a[:n].copy()
+            out = _sort_gpu(pp, b, 1, leaf_algo=leaf_algo)
+            assert np.array_equal(out, _oracle_sorted(b)), (leaf_algo, n)
+    # the same clusters inside a large quicksort (bins from the per-CTA recursion)
+    big = np.concatenate([c.reshape(-1) for c in [cl] * 40] + [synth.uniform_u64_np(300000, 3)])
+    big = big[rng.permutation(big.size)]
+    out = _sort_gpu(pp, big, 0, leaf_algo=leaf_algo)
+    assert np.array_equal(out, _oracle_sorted(big))
