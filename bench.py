@@ -155,7 +155,8 @@ def run_reference(args):
         "config": {"workload": WORKLOAD, "n": N_KEYS, "pivot": PIVOT, "split": split},
         "gbs": 2 * 8 * N_KEYS * args.steps / tot / 1e9,
         "cpu_baseline": {"value": value, "unit": "keys/s", "cores": 1, "kind": "oracle",
-                         "sample": f"full c2 input (2^27 keys), {args.steps} timed steps, fresh copy each"},
+                         "sample": f"full c2 input (2^27 keys), {args.steps} timed steps, fresh copy each",
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -177,7 +178,45 @@ def cpu_baseline(budget_s: float = 12.0):
     v = N_KEYS * len(times) / sum(times)
     return {"value": v, "unit": "keys/s", "cores": 1, "kind": "oracle",
             "sample": f"full c2 input (2^27 keys), {len(times)} runs of the serial two-pointer oracle, "
-                      f"fresh copy each, 1 host thread"}
+                      f"fresh copy each, 1 host thread", "host": host_info()}
+
+
+def host_info():
+    """The box's host (nproc, CPU model, RAM)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu"] = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            info["ram_gb"] = round(int(f.readline().split()[1]) / 2**20, 1)
+    except OSError:
+        pass
+    return info
+
+
+def cpu_quicksort_baseline(budget_s: float = 8.0):
+    """Config 5's CPU rows on a bounded sample: the serial oracle quicksort
+    (median-of-3) and numpy.sort as a library reference,
+    1 host thread, on the first 2^24 keys of the c5 uniform input."""
+    import oracle
+    import synth
+    m = 1 << 24
+    a = synth.uniform_u64_np(m, synth.SEEDS["c5"])
+    res = {}
+    for name, fn in (("oracle_quicksort", oracle.quicksort), ("numpy_sort", lambda x: x.sort())):
+        times = []
+        t_start = time.perf_counter()
+        while len(times) < 1 or (time.perf_counter() - t_start < budget_s / 2 and len(times) < 5):
+            b = a.copy()
+            t0 = time.perf_counter()
+            fn(b)
+            times.append(time.perf_counter() - t0)
+        res[name] = {"keys_per_s": m / min(times), "ms": 1e3 * min(times)}
+    res["sample"] = "first 2^24 keys of the c5 uniform input, 1 host thread"
+    return res
 
 
 def main():
@@ -326,6 +365,8 @@ def main():
         if not args.no_cpu_baseline:
             cb = cpu_baseline()
             out["cpu_baseline"] = cb
+            if not args.no_extras:
+                out["extras"]["cpu_quicksort_sample"] = cpu_quicksort_baseline()
         # split sanity vs oracle count (oracle used only as a reported check)
         import oracle
         out["split_ok"] = (split == oracle.count(pristine.cpu().numpy().view(np.uint64), PIVOT))

@@ -221,6 +221,8 @@ pp_status pp_last_stats(uint64_t *out13);
  * name.  pp_get_param returns INT64_MIN for an unknown name. */
 pp_status pp_set_param(const char *name, int64_t value);
 int64_t pp_get_param(const char *name);
+/* Restores every tunable to the library's default. */
+void pp_reset_params(void);
 
 const char *pp_status_string(pp_status s);
 const char *pp_last_error(void);

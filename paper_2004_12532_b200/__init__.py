@@ -75,6 +75,7 @@ def load(build_if_missing: bool = True):
         "pp_quicksort_u64": ([vp, u64, vp], st),
         "pp_quicksort_u32": ([vp, u64, vp], st),
         "pp_partition_host_u64": ([vp, u64, u64, P64], st),
+        "pp_reset_params": ([], None),
         "pp_partition_stable_u64": ([vp, vp, u64, u64, vp, P64], st),
         "pp_partition_bps_u64": ([vp, u64, u64, vp, P64], st),
         "pp_partition_bps_u32": ([vp, u64, u32, vp, P64], st),
@@ -383,11 +384,6 @@ def pp_timing_read() -> dict:
     return {"calls": int(out[0]), "group_ms": out[1], "rest_ms": out[2], "total_ms": out[3]}
 
 
-DEFAULT_PARAMS = {"g": 0, "min_lines_per_group": 16, "small_n": 1 << 15, "path": 0, "tile": 0, "ranks": 0, "variant": 0,
-                  "leaf": 0, "qs_cta_max": 0, "leaf_algo": 0, "qs_waves": 2, "fused": 0,
-                  "fused_stop": 0, "qs_small": 1 << 16, "qs_small_cfg": 1}
-
-
 def reset_params() -> None:
-    for k, v in DEFAULT_PARAMS.items():
-        pp_set_param(k, v)
+    """Every tunable back to the library's default (C ABI pp_reset_params)."""
+    load().pp_reset_params()

@@ -621,6 +621,11 @@ pp_status pp_last_stats(uint64_t* out) {
     return PP_OK;
 }
 
+void pp_reset_params(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_params = Params();
+}
+
 pp_status pp_set_param(const char* name, int64_t value) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!name) return PP_E_INVAL;
