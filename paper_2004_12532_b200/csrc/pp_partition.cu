@@ -514,7 +514,11 @@ template <typename K> struct VariantCfg<K, 7> {
     using D = GroupCfg<K>;
     using type = GroupCfgT<K, D::LK * (int)sizeof(K), D::NT, D::PF, D::TMA_STORE, true, D::PAR_ISSUE>;
 };
-constexpr int N_VARIANTS = 7;
+// 8: 8 KiB lines, 128 threads, 4 in flight per end, parallel refill issue
+template <typename K> struct VariantCfg<K, 8> { using type = GroupCfgT<K, 8192, 128, 4, false, false, true>; };
+// 9: 4 KiB lines, 256 threads, parallel refill issue
+template <typename K> struct VariantCfg<K, 9> { using type = GroupCfgT<K, 4096, 256, 4, false, false, true>; };
+constexpr int N_VARIANTS = 10;
 constexpr int STRIDED_VARIANT = 7;
 
 template <typename K, int V>
@@ -532,6 +536,8 @@ static VariantInfo variant_info(int v) {
         case 5: return variant_info_t<K, 5>();
         case 6: return variant_info_t<K, 6>();
         case 7: return variant_info_t<K, 7>();
+        case 8: return variant_info_t<K, 8>();
+        case 9: return variant_info_t<K, 9>();
         default: return variant_info_t<K, 0>();
     }
 }
@@ -554,6 +560,8 @@ static void launch_group(int v, K* region, uint64_t n_lines, uint32_t g, uint64_
         case 5: launch_group_t<K, 5>(region, n_lines, g, seed, pivot, out, st); break;
         case 6: launch_group_t<K, 6>(region, n_lines, g, seed, pivot, out, st); break;
         case 7: launch_group_t<K, 7>(region, n_lines, g, seed, pivot, out, st); break;
+        case 8: launch_group_t<K, 8>(region, n_lines, g, seed, pivot, out, st); break;
+        case 9: launch_group_t<K, 9>(region, n_lines, g, seed, pivot, out, st); break;
         default: launch_group_t<K, 0>(region, n_lines, g, seed, pivot, out, st); break;
     }
 }

@@ -404,7 +404,7 @@ def test_config4_adversarial_full(pp, pat):
     _full_check(pp, t, synth.ADV_PIVOT_U32, K)
 
 
-@pytest.mark.parametrize("variant", list(range(7)))
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 8, 9])
 def test_group_variants(pp, variant):
     """Every group-kernel configuration (line size, threads, prefetch depth,
     store path) is parity-exact, including runs right after other kernels
