@@ -585,6 +585,14 @@ struct SmallCfg<K, 0> {
     static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
 };
 template <typename K>
+struct SmallCfg<K, 2> {  // V = 1 with the refills issued by one lane per line (PAR_ISSUE)
+    static constexpr int NT = 128, MINB = 4;
+    using GC = GroupCfgT<K, 4096, 128, 2, false, false, true>;
+    static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 2048 : 4096;
+    static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);
+    static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
+};
+template <typename K>
 struct SmallCfg<K, 1> {
     static constexpr int NT = 128, MINB = 4;
     using GC = GroupCfgT<K, 4096, 128, 2, false>;
@@ -1458,7 +1466,12 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(d_sbase, small_base.data() + b0, 8 * cnt, cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort small H2D");
-            if (P.qs_small_cfg == 0) {
+            if (P.qs_small_cfg == 2) {
+                using S = SmallCfg<K, 2>;
+                cudaFuncSetAttribute(qs_small_kernel<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+                qs_small_kernel<K, 2><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(
+                    keys, d_slo, d_sln, d_sbase, d_blo, d_bln, (uint32_t)LEAF, P.seed, d_scr, d_prof);
+            } else if (P.qs_small_cfg == 0) {
                 using S = SmallCfg<K, 0>;
                 cudaFuncSetAttribute(qs_small_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
                 qs_small_kernel<K, 0><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(
