@@ -228,6 +228,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the mu sweep and quicksort lines")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU code path (NCCL process group, pp_partition_dist) even at one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -240,9 +242,10 @@ def main():
     import synth
 
     ws, rank, local = dist_env()
+    dist_on = ws > 1 or args.force_dist
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    if dist_on:
         dist.init_process_group("nccl", device_id=dev)
     pp.load(build_if_missing=False)
     pp.reset_params()
@@ -261,7 +264,7 @@ def main():
     flush = torch.ones(L2_FLUSH_BYTES // 8, dtype=torch.int64, device=dev)
     d_split = torch.zeros(1, dtype=torch.int64, device=dev)
     last_split = [None]
-    if ws > 1:
+    if dist_on:
         # the library's own NCCL communicator (C ABI pp_dist_*): rank 0 makes
         # the unique id, the torch process group only carries its 128 bytes
         uid = [pp.pp_dist_unique_id() if rank == 0 else None]
@@ -269,7 +272,7 @@ def main():
         pp.pp_dist_init(uid[0], ws, rank, local)
 
     def step(buf):
-        if ws > 1:
+        if dist_on:
             last_split[0] = pp.pp_partition_dist(buf, PIVOT)
         else:
             pp.pp_partition_async_u64(buf, PIVOT, d_split)
@@ -295,7 +298,7 @@ def main():
     #      cleanup costs ~12 us per step (tools/timing_overhead.py) ----
     ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if ws > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     pp.pp_launch_count(reset=True)
@@ -305,7 +308,7 @@ def main():
         step(bufs[i])
         ev_e[i].record(stream)
     torch.cuda.synchronize()
-    if ws > 1:
+    if dist_on:
         dist.barrier()
     launches = pp.pp_launch_count()
     step_ms = [s.elapsed_time(e) for s, e in zip(ev_s, ev_e)]
@@ -316,7 +319,7 @@ def main():
     for b in bufs:
         b.copy_(pristine)
     torch.cuda.synchronize()
-    if ws > 1:
+    if dist_on:
         dist.barrier()
     pp.pp_timing(True)
     for i in range(args.steps):
@@ -326,14 +329,14 @@ def main():
     pp.pp_timing(False)
     clocks = sampler.stop()
     del bufs
-    if ws > 1:
+    if dist_on:
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
 
     # sanity: the split equals the oracle's count on this input (cheap check)
-    split = int(d_split.item()) if ws == 1 else last_split[0]
-    stats = pp.pp_last_stats() if ws == 1 else {}
+    split = int(d_split.item()) if not dist_on else last_split[0]
+    stats = pp.pp_last_stats() if not dist_on else {}
 
     value = ws * n * args.steps / (tot_ms / 1e3)
     ms_per_step = tot_ms / args.steps
@@ -352,7 +355,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "n_per_gpu": n, "pivot": PIVOT, "mu": 0.5,
-                   "parallelism": f"dp{ws}" if ws > 1 else "single",
+                   "parallelism": f"dp{ws}" if dist_on else "single",
                    "l2": "inputs larger than L2: each of the K back-to-back steps partitions its own fresh "
                          "1 GiB copy of the input (K GiB resident in HBM)"},
         "gbs": ws * bytes_step * args.steps / (tot_ms / 1e3) / 1e9,
@@ -373,7 +376,7 @@ def main():
         "aux_frac": (stats.get("aux_bytes", 0) / (8 * n)) if stats else None,
     }
 
-    if rank == 0 and ws == 1:
+    if rank == 0 and not dist_on:
         if not args.no_e2e:
             out["e2e"] = e2e(pp, n, args)
         if not args.no_extras:
@@ -388,7 +391,7 @@ def main():
         out["split_ok"] = (split == oracle.count(pristine.cpu().numpy().view(np.uint64), PIVOT))
     if rank == 0:
         print(json.dumps(out))
-    if ws > 1:
+    if dist_on:
         pp.pp_dist_finalize()
         dist.destroy_process_group()
     return 0
