@@ -158,3 +158,19 @@ def test_bin_sorts_clustered(pp, leaf_algo):
     big = big[rng.permutation(big.size)]
     out = _sort_gpu(pp, big, 0, leaf_algo=leaf_algo)
     assert np.array_equal(out, _oracle_sorted(big))
+
+
+@pytest.mark.parametrize("kind", ["uniform", "dup1000"])
+def test_quicksort_2pow30(pp, kind):
+    """4x config 5 (2^30 u64 = 8 GiB): beyond the benchmarked size (segment
+    lists, bin slots, heavy-segment batches all scale); the output equals the
+    library sort (torch.sort on the order-preserving image)."""
+    from gpu_util import order_key
+    n = 1 << 30
+    t = (synth.uniform_u64_torch(n, 77, "cuda") if kind == "uniform"
+         else synth.mod_range_u64_torch(n, 77, 1000, "cuda"))
+    ref = torch.sort(order_key(t)).values
+    pp.pp_quicksort(t)
+    assert torch.equal(order_key(t), ref)
+    del t, ref
+    torch.cuda.empty_cache()
