@@ -671,6 +671,43 @@ __device__ __forceinline__ uint64_t block_exscan(uint64_t v, uint64_t* sw, uint6
     return wpre + x - v;
 }
 
+// Two independent exclusive scans in one pass (the same barriers): the
+// left and right tile counts, or the left and right bitmap words.
+template <int NT>
+__device__ __forceinline__ void block_exscan2(uint64_t va, uint64_t vb, uint64_t* sw /* [64] */, uint64_t& exa,
+                                              uint64_t& exb, uint64_t& tota, uint64_t& totb) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t xa = va, xb = vb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
+        if (lane >= o) {
+            xa += ya;
+            xb += yb;
+        }
+    }
+    if (lane == 31) {
+        sw[warp] = xa;
+        sw[32 + warp] = xb;
+    }
+    __syncthreads();
+    uint64_t pa = 0, pb = 0;
+    tota = 0;
+    totb = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const uint64_t ca = sw[w], cb = sw[32 + w];
+        pa += w < warp ? ca : 0;
+        pb += w < warp ? cb : 0;
+        tota += ca;
+        totb += cb;
+    }
+    __syncthreads();
+    exa = pa + xa - va;
+    exb = pb + xb - vb;
+}
+
 // the j-th value of the sorted merge of a[0..na) and b[0..nb)
 __device__ __forceinline__ uint64_t merged_at(const uint64_t* a, uint64_t na, const uint64_t* b, uint64_t nb,
                                              uint64_t j) {
@@ -730,7 +767,7 @@ __device__ void scan_swap_body(K* __restrict__ keys, Ctl* __restrict__ ctl, K pi
                                const uint32_t* __restrict__ cntL, const uint32_t* __restrict__ cntR,
                                uint32_t* __restrict__ flags, const uint32_t* __restrict__ bm, uint64_t bm_cap,
                                uint64_t* sp, uint32_t bx, uint32_t gx) {
-    __shared__ uint64_t sw[32];
+    __shared__ uint64_t sw[64];
     __shared__ uint64_t posLs[FUSED_TASKS_PER_CTA], posRs[FUSED_TASKS_PER_CTA];
     __shared__ CleanupSmem<K, SW_NT, SW_EPT2> sm;
     griddep_wait();
@@ -740,24 +777,16 @@ __device__ void scan_swap_body(K* __restrict__ keys, Ctl* __restrict__ ctl, K pi
     const uint64_t Kv = ctl->Kv, W = ctl->W, T = ctl->tile, nL = ctl->nL, nR = ctl->nR;
     uint64_t* sPL = sp;
     uint64_t* sPR = sp + nL + 1;
-    uint64_t carry = 0;
-    for (uint64_t b = 0; b < nL; b += SW_NT) {
+    uint64_t ML = 0, MR = 0;  // both sides' counts scanned in one pass per chunk
+    for (uint64_t b = 0; b < nL || b < nR; b += SW_NT) {
         const uint64_t i = b + tid;
-        uint64_t tot;
-        const uint64_t ex = block_exscan<SW_NT>(i < nL ? cntL[i] : 0, sw, tot);
-        if (i < nL) sPL[i] = carry + ex;
-        carry += tot;
+        uint64_t exl, exr, tl, tr;
+        block_exscan2<SW_NT>(i < nL ? cntL[i] : 0, i < nR ? cntR[i] : 0, sw, exl, exr, tl, tr);
+        if (i < nL) sPL[i] = ML + exl;
+        if (i < nR) sPR[i] = MR + exr;
+        ML += tl;
+        MR += tr;
     }
-    const uint64_t ML = carry;
-    carry = 0;
-    for (uint64_t b = 0; b < nR; b += SW_NT) {
-        const uint64_t i = b + tid;
-        uint64_t tot;
-        const uint64_t ex = block_exscan<SW_NT>(i < nR ? cntR[i] : 0, sw, tot);
-        if (i < nR) sPR[i] = carry + ex;
-        carry += tot;
-    }
-    const uint64_t MR = carry;
     __syncthreads();
     const bool ok = ML == MR && ML > 0;  // identical in every CTA: all return or none
     if (bx == 0 && tid == 0) {
@@ -806,9 +835,8 @@ __device__ void scan_swap_body(K* __restrict__ keys, Ctl* __restrict__ ctl, K pi
             for (uint32_t b = 0; b < nw; b += SW_NT) {
                 const uint32_t i = b + tid;
                 const uint32_t wl = i < nwL ? bmL[wL0 + i] : 0u, wr = i < nwR ? bmR[wR0 + i] : 0u;
-                uint64_t tl, tr;
-                const uint64_t el = block_exscan<SW_NT>(__popc(wl), sw, tl);
-                const uint64_t er = block_exscan<SW_NT>(__popc(wr), sw, tr);
+                uint64_t tl, tr, el, er;
+                block_exscan2<SW_NT>(__popc(wl), __popc(wr), sw, el, er, tl, tr);
                 if (i < nwL) { bwL[i] = wl; bpL[i] = (uint32_t)(cL + el); }
                 if (i < nwR) { bwR[i] = wr; bpR[i] = (uint32_t)(cR + er); }
                 cL += tl;
