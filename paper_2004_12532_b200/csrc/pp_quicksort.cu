@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "pp_engine.cuh"
@@ -1070,6 +1071,25 @@ static void* qs_workspace(size_t bytes) {
     return g_qws;
 }
 
+// Pinned host staging for the level loop's small transfers (segment list
+// up, splits and device-computed pivots down): pageable copies are staged
+// synchronously by the driver and lengthen every level's host round trip.
+static unsigned char* g_qs_pin = nullptr;
+static size_t g_qs_pin_bytes = 0;
+static unsigned char* qs_pinned(size_t bytes) {
+    if (bytes <= g_qs_pin_bytes) return g_qs_pin;
+    if (g_qs_pin) cudaFreeHost(g_qs_pin);
+    g_qs_pin = nullptr;
+    g_qs_pin_bytes = 0;
+    const size_t want = std::max<size_t>(bytes + (bytes >> 1), 1 << 16);
+    if (cudaMallocHost(&g_qs_pin, want) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    g_qs_pin_bytes = want;
+    return g_qs_pin;
+}
+
 // Size thresholds of the quicksort driver (current params).
 struct QsGeom {
     uint64_t LEAF;      // segments <= LEAF: one smem sort
@@ -1271,6 +1291,16 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         uint64_t* d_splits = reinterpret_cast<uint64_t*>(ws + segB + goB);
         uint32_t* d_hidx = reinterpret_cast<uint32_t*>(ws + segB + goB + spB);
         unsigned char* d_hv = ws + segB + goB + spB + hiB;
+        // pinned staging: [segs][splits][heavy index]
+        const size_t pin_sB = al256(sizeof(QSeg) * std::max<uint64_t>(nmid, 1));
+        const size_t pin_spB = al256(8 * (nmid + nbig + 1));
+        unsigned char* pin = qs_pinned(pin_sB + pin_spB + al256(4 * std::max<uint64_t>(nh, 1)));
+        if (!pin) return PP_E_NOMEM;
+        QSeg* pin_segs = reinterpret_cast<QSeg*>(pin);
+        uint64_t* pin_splits = reinterpret_cast<uint64_t*>(pin + pin_sB);
+        uint32_t* pin_hidx = reinterpret_cast<uint32_t*>(pin + pin_sB + pin_spB);
+        if (nmid > 0) memcpy(pin_segs, mids.data(), sizeof(QSeg) * nmid);
+        if (nh > 0) memcpy(pin_hidx, hidx.data(), 4 * nh);
 
         // ---- big segments: full multi-CTA partition, one at a time ----
         pivots_h.assign(cur.size(), 0);
@@ -1298,14 +1328,14 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         }
         // ---- mid segments: one batched pass ----
         if (nmid > 0) {
-            e = cudaMemcpyAsync(d_segs, mids.data(), sizeof(QSeg) * nmid, cudaMemcpyHostToDevice, st);
+            e = cudaMemcpyAsync(d_segs, pin_segs, sizeof(QSeg) * nmid, cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort H2D");
             qs_pivot_kernel<K><<<(unsigned)((nmid + 255) / 256), 256, 0, st>>>(keys, d_segs, nmid);
             if (lvl_prof) cudaEventRecord(lev[0], st);
             qs_group_kernel<K><<<(unsigned)gtot, C::NT, C::SMEM, st>>>(keys, d_segs, nmid, P.seed, d_gout);
             if (lvl_prof) cudaEventRecord(lev[1], st);
             if (nh > 0) {
-                e = cudaMemcpyAsync(d_hidx, hidx.data(), 4 * nh, cudaMemcpyHostToDevice, st);
+                e = cudaMemcpyAsync(d_hidx, pin_hidx, 4 * nh, cudaMemcpyHostToDevice, st);
                 if (e != cudaSuccess) return cuda_fail(e, "quicksort H2D");
                 const unsigned X = (unsigned)std::min<uint64_t>(
                     2 * QS_HEAVY_TILES, std::max<uint64_t>(2, ((uint64_t)sm_count() * 4 + nh - 1) / nh));
@@ -1338,16 +1368,17 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         // ---- read back splits (and mid pivots) ----
         splits_h.assign(nmid + nbig, 0);
         if (nmid + nbig > 0) {
-            e = cudaMemcpyAsync(splits_h.data(), d_splits, 8 * (nmid + nbig), cudaMemcpyDeviceToHost, st);
+            e = cudaMemcpyAsync(pin_splits, d_splits, 8 * (nmid + nbig), cudaMemcpyDeviceToHost, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort D2H");
         }
         if (nmid > 0) {
-            e = cudaMemcpyAsync(mids.data(), d_segs, sizeof(QSeg) * nmid, cudaMemcpyDeviceToHost, st);
+            e = cudaMemcpyAsync(pin_segs, d_segs, sizeof(QSeg) * nmid, cudaMemcpyDeviceToHost, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort D2H");
         }
         e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return cuda_fail(e, "quicksort level");
-        for (size_t mi = 0; mi < nmid; ++mi) pivots_h[mid_idx[mi]] = mids[mi].pivot;
+        if (nmid + nbig > 0) memcpy(splits_h.data(), pin_splits, 8 * (nmid + nbig));
+        for (size_t mi = 0; mi < nmid; ++mi) pivots_h[mid_idx[mi]] = pin_segs[mi].pivot;
         if (lvl_prof && nmid > 0) {  // debug: per-level times of the batched mid pass
             float tg = 0, tc = 0;
             cudaEventElapsedTime(&tg, lev[0], lev[1]);
