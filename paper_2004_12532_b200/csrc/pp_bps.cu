@@ -224,52 +224,55 @@ __global__ void __launch_bounds__(1024) bps_base_kernel(K* __restrict__ keys, ui
 // One Reorder level: CTA per tail block i in [t, tb): its j-th view
 // predecessor (position order) is swapped with V[S[i] + j] (Lemma 3.4: a
 // successor of the already reordered prefix).  Blocks hold < 2B keys.
-template <typename K>
-__global__ void __launch_bounds__(1024) bps_tail_kernel(K* __restrict__ keys, uint64_t n, K pivot, uint64_t nb,
-                                                        uint64_t t0, const uint64_t* __restrict__ S,
-                                                        const uint64_t* __restrict__ dK) {
-    constexpr int NT = 1024, NW = NT / 32, EPT = 8;  // 8192 >= 2B - 1 positions
+template <typename K, int NT>
+__global__ void __launch_bounds__(NT) bps_tail_kernel(K* __restrict__ keys, uint64_t n, K pivot, uint64_t nb,
+                                                      uint64_t t0, const uint64_t* __restrict__ S,
+                                                      const uint64_t* __restrict__ dK) {
+    constexpr int NW = NT / 32, EPT = 8, CH = NT * EPT;  // positions per pass; blocks hold < 2B
     __shared__ uint32_t wc[EPT][NW];
     const BpsView v = bps_view(n, dK);
     const uint64_t i = t0 + blockIdx.x;
     const uint64_t lo = i * BPS_B, hi = (i == nb - 1) ? n : lo + BPS_B;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = lanemask_lt();
-    K x[EPT];
-    uint32_t ball[EPT];
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-        const uint64_t q = lo + (uint64_t)k * NT + tid;
-        x[k] = q < hi ? keys[v.at(q)] : (K)0;
-        ball[k] = __ballot_sync(0xffffffffu, q < hi && bps_pred(x[k], pivot, v.rev));
-        if (lane == 0) wc[k][warp] = __popc(ball[k]);
-    }
-    __syncthreads();
     const uint64_t base = S[i];
-    // all targets first, then all target loads (independent, in flight
-    // together), then the stores: no load waits behind another pair's store
-    uint64_t tgt[EPT];
-    uint32_t before = 0;
+    uint32_t before = 0;  // the block's predecessors at earlier positions (earlier passes)
+    for (uint64_t c0 = lo; c0 < hi; c0 += CH) {
+        K x[EPT];
+        uint32_t ball[EPT];
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-        uint32_t wpre = 0, row = 0;
-        for (int w = 0; w < NW; ++w) {
-            const uint32_t c = wc[k][w];
-            wpre += w < warp ? c : 0u;
-            row += c;
+        for (int k = 0; k < EPT; ++k) {
+            const uint64_t q = c0 + (uint64_t)k * NT + tid;
+            x[k] = q < hi ? keys[v.at(q)] : (K)0;
+            ball[k] = __ballot_sync(0xffffffffu, q < hi && bps_pred(x[k], pivot, v.rev));
+            if (lane == 0) wc[k][warp] = __popc(ball[k]);
         }
-        tgt[k] = v.at(base + before + wpre + __popc(ball[k] & lt));
-        before += row;
-    }
-    K y[EPT];
+        __syncthreads();
+        // all targets first, then all target loads (independent, in flight
+        // together), then the stores: no load waits behind another pair's store
+        uint64_t tgt[EPT];
 #pragma unroll
-    for (int k = 0; k < EPT; ++k)
-        if ((ball[k] >> lane) & 1u) y[k] = keys[tgt[k]];
+        for (int k = 0; k < EPT; ++k) {
+            uint32_t wpre = 0, row = 0;
+            for (int w = 0; w < NW; ++w) {
+                const uint32_t cc = wc[k][w];
+                wpre += w < warp ? cc : 0u;
+                row += cc;
+            }
+            tgt[k] = v.at(base + before + wpre + __popc(ball[k] & lt));
+            before += row;
+        }
+        __syncthreads();  // wc reusable by the next pass
+        K y[EPT];
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-        if ((ball[k] >> lane) & 1u) {
-            keys[tgt[k]] = x[k];
-            keys[v.at(lo + (uint64_t)k * NT + tid)] = y[k];
+        for (int k = 0; k < EPT; ++k)
+            if ((ball[k] >> lane) & 1u) y[k] = keys[tgt[k]];
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+            if ((ball[k] >> lane) & 1u) {
+                keys[tgt[k]] = x[k];
+                keys[v.at(c0 + (uint64_t)k * NT + tid)] = y[k];
+            }
         }
     }
 }
@@ -332,7 +335,14 @@ pp_status partition_bps_device(K* keys, uint64_t n, K pivot, cudaStream_t st, ui
         ++launches;
         for (size_t k = tbs.size() - 1; k-- > 0;) {
             const uint64_t t = tbs[k + 1], tb = tbs[k];
-            bps_tail_kernel<K><<<(unsigned)(tb - t), 1024, 0, st>>>(keys, n, pivot, nb, t, S, dK);
+            if (params().bps_nt == 1024)
+                bps_tail_kernel<K, 1024><<<(unsigned)(tb - t), 1024, 0, st>>>(keys, n, pivot, nb, t, S, dK);
+            else if (params().bps_nt == 512)
+                bps_tail_kernel<K, 512><<<(unsigned)(tb - t), 512, 0, st>>>(keys, n, pivot, nb, t, S, dK);
+            else if (params().bps_nt == 128)
+                bps_tail_kernel<K, 128><<<(unsigned)(tb - t), 128, 0, st>>>(keys, n, pivot, nb, t, S, dK);
+            else
+                bps_tail_kernel<K, 256><<<(unsigned)(tb - t), 256, 0, st>>>(keys, n, pivot, nb, t, S, dK);
             ++launches;
         }
     }

@@ -53,6 +53,7 @@ struct Params {
     int64_t qs_small_cfg = 2;      // quicksort: per-CTA recursion config (pp_quicksort.cu SmallCfg)
     int64_t cleanup_chain = 0;     // partition cleanup tail: 0 fused scan+swap, 1 scan / locate / swap kernels
     int64_t cleanup_bitmap = 1;    // fused tail: locate pairs from the dirty-set bitmap (0: locate + grid barrier)
+    int64_t bps_nt = 256;          // Blocked-Prefix-Sum Reorder level kernel: threads per CTA (256/512/1024)
     int64_t qs_pipe = 1;           // quicksort: chunks of the per-CTA recursion pipelined with their bin sorts (measured: no gain)
     int64_t host_chunk = 1 << 22;  // host-buffer partition: keys per streamed chunk
     int64_t qs_heavy = 1 << 23;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
