@@ -455,9 +455,13 @@ __global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
 // packed buffer (36 KiB) and the output (72 KiB, also the fallback's buffer).
 constexpr int PK_LEAF = 8192, PK_NT = PK_LEAF / LEAF_E, PK_IDX_BITS = 13, PK_TOP_BITS = 32 - PK_IDX_BITS;
 constexpr uint32_t PK_MAX_RUN = 64;
-__global__ void __launch_bounds__(PK_NT) qs_leaf_packed_kernel(uint64_t* __restrict__ keys,
-                                                               const uint64_t* __restrict__ leaf_lo,
-                                                               const uint32_t* __restrict__ leaf_len) {
+// PLEAF = the bin capacity (8192 with 1024 threads, or 4096 with 512 threads:
+// half the shared memory, two CTAs per SM); the index keeps 13 bits.
+template <int PLEAF>
+__global__ void __launch_bounds__(PLEAF / LEAF_E) qs_leaf_packed_kernel(uint64_t* __restrict__ keys,
+                                                                        const uint64_t* __restrict__ leaf_lo,
+                                                                        const uint32_t* __restrict__ leaf_len) {
+    constexpr int PK_LEAF = PLEAF;
     extern __shared__ __align__(16) unsigned char lsm[];
     uint64_t* ks = reinterpret_cast<uint64_t*>(lsm);          // [PK_LEAF] original keys
     uint64_t* ob = ks + PK_LEAF;                              // [lpad(PK_LEAF)] output / fallback buffer
@@ -1428,11 +1432,19 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot
     auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
         // default: packed 32-bit sort for u64 bins of up to 8192 keys, else merge sort
-        const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : (sizeof(K) == 8 && LEAF > LC::LEAF / 2 ? 4 : 3);
-        if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF) {
+        const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : (sizeof(K) == 8 ? 4 : 3);
+        if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF / 2) {
+            constexpr int PL = PK_LEAF / 2;
+            const size_t smem = 8 * PL + 8 * lpad_host(PL) + 4 * lpad_host(PL);
+            cudaFuncSetAttribute(qs_leaf_packed_kernel<PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_packed_kernel<PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(reinterpret_cast<uint64_t*>(keys),
+                                                                                d_lo, d_len);
+        } else if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF) {
             const size_t smem = 8 * PK_LEAF + 8 * lpad_host(PK_LEAF) + 4 * lpad_host(PK_LEAF);
-            cudaFuncSetAttribute(qs_leaf_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_packed_kernel<<<(unsigned)cnt, PK_NT, smem, bst>>>(reinterpret_cast<uint64_t*>(keys), d_lo, d_len);
+            cudaFuncSetAttribute(qs_leaf_packed_kernel<PK_LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            qs_leaf_packed_kernel<PK_LEAF><<<(unsigned)cnt, PK_NT, smem, bst>>>(reinterpret_cast<uint64_t*>(keys), d_lo,
+                                                                               d_len);
         } else if (algo == 2) {
             constexpr int NW = LC::LEAF / 256;
             const size_t smem = sizeof(K) * LC::LEAF + 2 * 256 * NW;
