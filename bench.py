@@ -545,6 +545,25 @@ def extras(pp, torch, synth, dev, stream, flush):
                 ts.append(s.elapsed_time(e))
         return statistics.mean(ts)
 
+    # BASELINE config 1: n = 2^20 u64 (8 MiB, L2-resident: launch-bound, reported not judged),
+    # back-to-back partitions of fresh copies
+    n1 = 1 << 20
+    c1src = synth.uniform_u64_torch(n1, synth.SEEDS["c1"], dev)
+    c1bufs = [c1src.clone() for _ in range(50)]
+    d1 = torch.zeros(1, dtype=torch.int64, device=dev)
+    for b in c1bufs[:5]:
+        pp.pp_partition_async_u64(b, PIVOT, d1)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for b in c1bufs[5:]:
+        pp.pp_partition_async_u64(b, PIVOT, d1)
+    e.record(stream)
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / 45
+    res["c1_u64_2^20"] = {"keys_per_s": n1 / (ms / 1e3), "ms": ms, "gbs": 16 * n1 / (ms / 1e3) / 1e9,
+                          "note": "8 MiB: L2-resident and launch-bound (SURVEY §8(d)); back-to-back calls"}
+    del c1src, c1bufs
     # BASELINE config 4: n = 1,000,000,007 u32 adversarial inputs, pivot 2^31
     n4 = 1_000_000_007
     for pat in ("partitioned", "reverse", "alternating", "all_false"):
