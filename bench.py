@@ -593,6 +593,28 @@ def extras(pp, torch, synth, dev, stream, flush):
         res[f"c4_u32_{pat}"] = {"keys_per_s": n4 / (m / 1e3), "ms": m, "gbs": 8 * n4 / (m / 1e3) / 1e9,
                                 "window_frac": st["W"] / n4}
         del a0, a
+    # BASELINE config 4, Zipf(1.1) keys (rank - 1 on [0, 2^32)), pivot = sample median
+    z0 = synth.zipf_u32_torch(n4, 1.1, synth.SEEDS["c4"], dev)
+    zp = int(torch.sort(z0.to(torch.int64) & 0xFFFFFFFF).values[n4 // 2])
+    z = torch.empty_like(z0)
+    dz = torch.zeros(1, dtype=torch.int64, device=dev)
+    ms = []
+    for i in range(4):
+        z.copy_(z0)
+        flush.sum()
+        torch.cuda.synchronize()
+        pp.pp_timing(True)
+        pp.pp_partition_async_u32(z, zp, dz)
+        torch.cuda.synchronize()
+        t = pp.pp_timing_read()
+        pp.pp_timing(False)
+        if i >= 1:
+            ms.append(t["total_ms"])
+    m = statistics.mean(ms)
+    st = pp.pp_last_stats()
+    res["c4_u32_zipf1.1_median"] = {"keys_per_s": n4 / (m / 1e3), "ms": m, "gbs": 8 * n4 / (m / 1e3) / 1e9,
+                                    "pivot": zp, "window_frac": st["W"] / n4}
+    del z0, z
     # BASELINE config 3 at P = 1: n = 2^33 u64 (64 GiB) in one GPU
     n3 = 1 << 33
     try:
