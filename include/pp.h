@@ -175,6 +175,18 @@ pp_status pp_dist_plan(const uint64_t *ns, const uint64_t *ts, int nranks, uint6
                        uint64_t out_cap, uint64_t *n_out, uint64_t *K_out);
 pp_status pp_dist_finalize(void);
 
+/* pp_swap_ranges_u64/u32: the staging-free exchange primitive (SURVEY §8(f)
+ * #1): for each of n_pieces HOST triples (a, b, len) -- a and b DEVICE
+ * addresses (a peer-mapped b is allowed), aligned to the key size -- swaps
+ * keys [a, a+len) with [b, b+len) elementwise, one thread per pair.  With
+ * the pieces of pp_dist_plan (a = the left rank's misplaced successors, b =
+ * the right rank's misplaced predecessors) it performs the partition's
+ * exchange one-sidedly with no staging buffer; on one GPU it executes the
+ * plan of emulated ranks.  Ranges must not overlap.  Synchronous on
+ * `stream`; PP_E_INVAL for misaligned ranges or NULL triples. */
+pp_status pp_swap_ranges_u64(const uint64_t *triples, uint64_t n_pieces, void *stream);
+pp_status pp_swap_ranges_u32(const uint64_t *triples, uint64_t n_pieces, void *stream);
+
 /* ---- Smoothed Striding partial partition step alone (parity of internals) --
  * Runs only the group kernel on the 16-B aligned region of `keys` with g
  * groups (g = 0: the library's automatic choice) and copies the per-group

@@ -76,6 +76,8 @@ def load(build_if_missing: bool = True):
         "pp_quicksort_u32": ([vp, u64, vp], st),
         "pp_partition_host_u64": ([vp, u64, u64, P64], st),
         "pp_reset_params": ([], None),
+        "pp_swap_ranges_u64": ([vp, u64, vp], st),
+        "pp_swap_ranges_u32": ([vp, u64, vp], st),
         "pp_partition_stable_u64": ([vp, vp, u64, u64, vp, P64], st),
         "pp_partition_bps_u64": ([vp, u64, u64, vp, P64], st),
         "pp_partition_bps_u32": ([vp, u64, u32, vp, P64], st),
@@ -372,6 +374,14 @@ def pp_dist_plan(ns, ts, cap: int):
                                rows.ctypes.data_as(P64), n_out.value, ctypes.byref(n_out), ctypes.byref(K)),
            "pp_dist_plan")
     return int(K.value), [tuple(int(x) for x in r) for r in rows[: n_out.value]]
+
+
+def pp_swap_ranges(pieces, key_bytes: int = 8, stream=None) -> None:
+    """Swap [a, a+len) <-> [b, b+len) for each (a, b, len) of device
+    addresses (the staging-free exchange primitive)."""
+    tri = np.ascontiguousarray(np.asarray(pieces, dtype=np.uint64).reshape(-1, 3))
+    f = load().pp_swap_ranges_u64 if key_bytes == 8 else load().pp_swap_ranges_u32
+    _check(f(tri.ctypes.data, tri.shape[0], _stream_ptr(stream)), "pp_swap_ranges")
 
 
 def pp_timing(enable: bool) -> None:

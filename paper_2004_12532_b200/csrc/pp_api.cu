@@ -492,6 +492,14 @@ pp_status pp_partition_bps_u32(uint32_t* keys, uint64_t n, uint32_t pivot, void*
 pp_status pp_partition_bps_async_u64(uint64_t* keys, uint64_t n, uint64_t pivot, void* stream, uint64_t* d_split) {
     return partition_bps<uint64_t>(keys, n, pivot, stream, nullptr, d_split);
 }
+pp_status pp_swap_ranges_u64(const uint64_t* triples, uint64_t n_pieces, void* stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return swap_ranges<uint64_t>(triples, n_pieces, (cudaStream_t)stream);
+}
+pp_status pp_swap_ranges_u32(const uint64_t* triples, uint64_t n_pieces, void* stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return swap_ranges<uint32_t>(triples, n_pieces, (cudaStream_t)stream);
+}
 pp_status pp_partition_stable_async_u64(const uint64_t* in, uint64_t* out, uint64_t n, uint64_t pivot,
                                         void* stream, uint64_t* d_split) {
     return partition_stable<uint64_t>(in, out, n, pivot, stream, nullptr, d_split);

@@ -18,6 +18,8 @@
 
 namespace pp {
 
+void note_launches(uint64_t k);
+
 // ---------------------------------------------------------------------------
 // The exchange plan (host arithmetic; mirrored independently in Python by
 // paper_2004_12532_b200/dist.py and cross-checked by tests/test_dist.py).
@@ -459,6 +461,82 @@ pp_status quicksort_dist(K* shard, uint64_t n_local, cudaStream_t st, uint64_t s
 
 template pp_status quicksort_dist<uint64_t>(uint64_t*, uint64_t, cudaStream_t, uint64_t);
 template pp_status quicksort_dist<uint32_t>(uint32_t*, uint64_t, cudaStream_t, uint64_t);
+
+// ---------------------------------------------------------------------------
+// Staging-free exchange primitive: swap ranges [a, a+len)
+// <-> [b, b+len) elementwise for every piece, one thread per element pair
+// (EREW), grid-stride over all pieces' elements; the piece of an element is
+// found by binary search over the length prefix.  a and b are device
+// pointers -- with peer-mapped b (CUDA IPC / symmetric memory) one rank
+// performs its exchange pieces one-sidedly over NVLink with no staging
+// buffer and no second copy; on one GPU it executes a whole plan of emulated
+// ranks (tests).  The caller guarantees that no two ranges overlap.
+// ---------------------------------------------------------------------------
+template <typename K>
+__global__ void __launch_bounds__(256) swap_ranges_kernel(const uint64_t* __restrict__ tri,
+                                                          const uint64_t* __restrict__ pre, uint64_t np,
+                                                          uint64_t total) {
+    for (uint64_t e = (uint64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (uint64_t)gridDim.x * 256) {
+        uint64_t lo = 0, hi = np;  // last piece with pre <= e
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (pre[mid] <= e) lo = mid; else hi = mid;
+        }
+        const uint64_t i = e - pre[lo];
+        K* a = reinterpret_cast<K*>(tri[3 * lo]) + i;
+        K* b = reinterpret_cast<K*>(tri[3 * lo + 1]) + i;
+        const K x = *a, y = *b;
+        *a = y;
+        *b = x;
+    }
+}
+
+static uint64_t* g_swap_buf = nullptr;
+static size_t g_swap_cap = 0;
+
+template <typename K>
+pp_status swap_ranges(const uint64_t* host_tri, uint64_t np, cudaStream_t st) {
+    if (np == 0) return PP_OK;
+    if (!host_tri) return PP_E_INVAL;
+    std::vector<uint64_t> buf(4 * np);  // [3 np triples][np prefix]
+    uint64_t total = 0;
+    for (uint64_t k = 0; k < np; ++k) {
+        buf[3 * k] = host_tri[3 * k];
+        buf[3 * k + 1] = host_tri[3 * k + 1];
+        buf[3 * k + 2] = host_tri[3 * k + 2];
+        if ((host_tri[3 * k] | host_tri[3 * k + 1]) % sizeof(K)) {
+            set_error("pp_swap_ranges: unaligned range");
+            return PP_E_INVAL;
+        }
+        buf[3 * np + k] = total;
+        total += host_tri[3 * k + 2];
+    }
+    if (total == 0) return PP_OK;
+    if (4 * np > g_swap_cap) {
+        cudaStreamSynchronize(st);
+        if (g_swap_buf) cudaFree(g_swap_buf);
+        g_swap_buf = nullptr;
+        g_swap_cap = 0;
+        if (cudaMalloc(&g_swap_buf, 8 * 4 * np) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("pp_swap_ranges: piece buffer allocation failed");
+            return PP_E_NOMEM;
+        }
+        g_swap_cap = 4 * np;
+    }
+    cudaError_t e = cudaMemcpyAsync(g_swap_buf, buf.data(), 8 * 4 * np, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "pp_swap_ranges H2D");
+    const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
+    swap_ranges_kernel<K><<<(unsigned)blocks, 256, 0, st>>>(g_swap_buf, g_swap_buf + 3 * np, np, total);
+    note_launches(1);
+    // the host triples were staged by the (pageable) copy; wait before the
+    // vector goes away only if the copy could still read it
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return e == cudaSuccess ? PP_OK : cuda_fail(e, "pp_swap_ranges");
+}
+template pp_status swap_ranges<uint64_t>(const uint64_t*, uint64_t, cudaStream_t);
+template pp_status swap_ranges<uint32_t>(const uint64_t*, uint64_t, cudaStream_t);
 
 pp_status dist_plan(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap, uint64_t* out, uint64_t out_cap,
                     uint64_t* n_out, uint64_t* K_out) {

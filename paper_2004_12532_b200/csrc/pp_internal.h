@@ -109,5 +109,7 @@ pp_status dist_plan(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap,
                     uint64_t* n_out, uint64_t* K_out);
 template <typename K>
 pp_status quicksort_dist(K* shard, uint64_t n_local, cudaStream_t st, uint64_t small);
+template <typename K>
+pp_status swap_ranges(const uint64_t* host_tri, uint64_t np, cudaStream_t st);
 
 }  // namespace pp

@@ -54,3 +54,36 @@ def test_dist_finalize_and_reinit(pp):
     pp.pp_dist_init(uid, 1, 0, torch.cuda.current_device())
     with pytest.raises(pp.PPError):
         pp.pp_dist_init(uid, 1, 0, torch.cuda.current_device())  # already initialised
+
+
+@pytest.mark.parametrize("P,dt", [(2, np.uint64), (3, np.uint64), (4, np.uint32), (8, np.uint64)])
+def test_emulated_ranks_staging_free_exchange(pp, P, dt):
+    """SURVEY §8(f) #1 core, emulated on one GPU (the profiling guide's advice
+    for multi-rank logic with fewer GPUs than ranks): P "ranks" are
+    contiguous, uneven shards of one device array; each partitions its shard
+    with the library, the exchange plan pairs the misplaced ranges
+    (pp_dist_plan, the same host arithmetic as the NCCL path), and the
+    staging-free primitive pp_swap_ranges swaps each piece one-sidedly.  The
+    whole array must then be a partition (oracle checks) with K = sum t_r."""
+    from gpu_util import to_dev, to_host
+    rng = np.random.default_rng(P * 7 + (dt == np.uint64))
+    mx = (1 << 64) - 1 if dt == np.uint64 else (1 << 32) - 1
+    w = np.dtype(dt).itemsize
+    for total in (1000, 300_007, 1 << 22):
+        cuts = np.sort(rng.integers(0, total, size=P - 1))
+        ns = np.diff(np.concatenate([[0], cuts, [total]])).astype(np.uint64)
+        a = rng.integers(0, mx, size=total, dtype=dt, endpoint=True)
+        for p in (int(mx // 3), int(mx // 2), int(mx - mx // 10), 0):
+            t = to_dev(a)
+            ts, base = [], 0
+            for r in range(P):
+                view = t[base:base + int(ns[r])]
+                ts.append(pp.pp_partition(view, p) if ns[r] else 0)
+                base += int(ns[r])
+            K, rows = pp.pp_dist_plan(ns, ts, 1 << 40)
+            assert K == sum(ts)
+            ptr = t.data_ptr()
+            pieces = [(ptr + w * f, ptr + w * tt, ln) for (_, rf, f, rt, tt, ln) in rows]
+            if pieces:
+                pp.pp_swap_ranges(pieces, w)
+            oracle.check_partition(a, to_host(t, dt), p, K)
