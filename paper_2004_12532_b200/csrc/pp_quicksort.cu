@@ -566,6 +566,190 @@ __global__ void __launch_bounds__(PLEAF / LEAF_E) qs_leaf_packed_kernel(uint64_t
     }
 }
 
+// Bin sort by one counting pass (leaf_algo 5).  Bucket d = (key - min) >> sh
+// with sh the smallest shift that maps the bin's range below NB = 2 PLEAF
+// buckets: one shared-memory atomic per key yields both its bucket's count
+// and its rank inside the bucket, an exclusive scan of the counts gives the
+// bucket starts, every key is written to start + rank, and then every key
+// finds its final slot inside its bucket by counting the bucket's smaller
+// keys (ties by scatter slot; uniform keys: ~1-2 keys per bucket), all keys
+// in parallel.  With sh = 0 a bucket holds one key value, so the scatter
+// alone sorts.  A bin whose keys crowd into few buckets (a bucket of more
+// than BK_MAX_RUN keys while sh > 0: clusters inside a wide range) is sorted
+// by the 64-bit merge sort instead.  The atomics' order inside a bucket
+// never shows: the output is the sorted bin.  Far fewer instructions per key
+// than the merge sorts above (the bin sort is issue-bound, not HBM-bound).
+constexpr uint32_t BK_MAX_RUN = 48;
+template <typename K>
+__device__ __forceinline__ int key_bits(K v) {
+    return sizeof(K) == 8 ? 64 - __clzll((long long)v) : 32 - __clz((int)v);
+}
+template <typename K, int PLEAF>
+__global__ void __launch_bounds__(PLEAF / LEAF_E, 8192 / PLEAF) qs_leaf_bucket_kernel(K* __restrict__ keys,
+                                                                       const uint64_t* __restrict__ leaf_lo,
+                                                                       const uint32_t* __restrict__ leaf_len) {
+    // NB = 2 * PLEAF buckets (about 0.5 keys per bucket), their 16-bit counts
+    // packed two per 32-bit word (counts and starts are <= PLEAF < 2^16)
+    constexpr int NT = PLEAF / LEAF_E, NW = NT / 32, NB = 2 * PLEAF, NWD = NB / 2;
+    constexpr int NBITS = PLEAF == 8192 ? 14 : PLEAF == 4096 ? 13 : PLEAF == 2048 ? 12 : 11;
+    static_assert((1 << NBITS) == NB, "power-of-two bin capacity");
+    static_assert(NWD == NT * LEAF_E, "8 count words per thread");
+    extern __shared__ __align__(16) unsigned char lsm[];
+    K* ob = reinterpret_cast<K*>(lsm);                                    // [lpad(PLEAF)] output
+    uint32_t* cw = reinterpret_cast<uint32_t*>(ob + lpad(PLEAF));  // [NWD + 1] packed counts, then starts
+    __shared__ K rmn[NW], rmx[NW];
+    __shared__ uint64_t sw[32];
+    __shared__ int fallback;
+    const K KMAX = (K)~(K)0;
+    const uint64_t lo = leaf_lo[blockIdx.x];
+    const uint32_t len = leaf_len[blockIdx.x];
+    if (len < 2) return;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    K x[LEAF_E];
+    K mn = KMAX, mx = 0;
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) {
+        const uint32_t i = (uint32_t)r * NT + tid;
+        x[r] = i < len ? __ldcs(keys + lo + i) : KMAX;
+        if (i < len) {
+            mn = x[r] < mn ? x[r] : mn;
+            mx = x[r] > mx ? x[r] : mx;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) cw[r * NT + tid] = 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const K a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+    }
+    if (lane == 0) {
+        rmn[warp] = mn;
+        rmx[warp] = mx;
+    }
+    if (tid == 0) {
+        fallback = 0;
+        cw[NWD] = len;  // the end of the last bucket
+    }
+    __syncthreads();
+    if (warp == 0) {  // warp 0 combines the per-warp extremes
+        mn = lane < NW ? rmn[lane] : KMAX;
+        mx = lane < NW ? rmx[lane] : (K)0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const K a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+        }
+        if (lane == 0) {
+            rmn[0] = mn;
+            rmx[0] = mx;
+        }
+    }
+    __syncthreads();
+    mn = rmn[0];
+    mx = rmx[0];
+    if (mn == mx) return;  // all keys equal (uniform over the CTA)
+    const int bits = key_bits<K>(mx - mn);
+    const int sh = bits > NBITS ? bits - NBITS : 0;
+    uint32_t rk[LEAF_E];
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) {
+        const uint32_t i = (uint32_t)r * NT + tid;
+        const uint32_t d = (uint32_t)((x[r] - mn) >> sh), hs = (d & 1u) * 16u;
+        rk[r] = i < len ? (atomicAdd(&cw[d >> 1], 1u << hs) >> hs) & 0xFFFFu : 0u;
+    }
+    __syncthreads();
+    // bucket starts: thread t owns words [8t, 8t + 8) = buckets [16t, 16t + 16)
+    uint32_t c[LEAF_E], s = 0;
+#pragma unroll
+    for (int j = 0; j < LEAF_E; ++j) {
+        c[j] = cw[tid * LEAF_E + j];
+        s += (c[j] & 0xFFFFu) + (c[j] >> 16);
+    }
+    uint64_t tot;
+    const uint32_t start = (uint32_t)block_exscan<NT>(s, sw, tot);
+    if (sh > 0) {
+#pragma unroll
+        for (int j = 0; j < LEAF_E; ++j)
+            if ((c[j] & 0xFFFFu) > BK_MAX_RUN || (c[j] >> 16) > BK_MAX_RUN) fallback = 1;
+    }
+    {
+        uint32_t e = start;
+#pragma unroll
+        for (int j = 0; j < LEAF_E; ++j) {
+            const uint32_t e1 = e + (c[j] & 0xFFFFu);
+            cw[tid * LEAF_E + j] = e | (e1 << 16);
+            e = e1 + (c[j] >> 16);
+        }
+    }
+    __syncthreads();
+    if (fallback) {  // crowded buckets: 64-bit merge sort of the whole bin
+        const uint32_t P = (len + 32 * LEAF_E - 1) / (32 * LEAF_E) * (32 * LEAF_E);
+        const uint32_t nthr = P / LEAF_E;
+#pragma unroll
+        for (int r = 0; r < LEAF_E; ++r) {
+            const uint32_t i = (uint32_t)r * NT + tid;
+            if (i < P) ob[lpad(i)] = x[r];  // x = KMAX past len
+        }
+        __syncthreads();
+        if (tid < nthr) smem_merge_sort<K>(ob, P, nthr);
+        __syncthreads();
+    } else {
+        // (unpadded layout: every access below is either random or warp-contiguous)
+#pragma unroll
+        for (int r = 0; r < LEAF_E; ++r) {
+            const uint32_t i = (uint32_t)r * NT + tid;
+            const uint32_t d = (uint32_t)((x[r] - mn) >> sh);
+            if (i < len) ob[((cw[d >> 1] >> ((d & 1u) * 16u)) & 0xFFFFu) + rk[r]] = x[r];
+        }
+        __syncthreads();
+        if (sh > 0) {  // final place inside the bucket: smaller keys, ties by scatter slot
+            uint32_t (&dst)[LEAF_E] = rk;  // rank -> destination, in place
+#pragma unroll
+            for (int r = 0; r < LEAF_E; ++r) {
+                const uint32_t i = (uint32_t)r * NT + tid;
+                if (i < len) {
+                    const uint32_t d = (uint32_t)((x[r] - mn) >> sh);
+                    const uint32_t w = cw[d >> 1];
+                    const uint32_t b0 = (d & 1u) ? w >> 16 : w & 0xFFFFu;
+                    const uint32_t b1 = (d & 1u) ? cw[(d >> 1) + 1] & 0xFFFFu : w >> 16;  // cw[NWD] = len
+                    const uint32_t p = b0 + rk[r];
+                    uint32_t q = 0xFFFFFFFFu;  // a bucket of one key: already in place
+                    if (b1 - b0 > 1) {
+                        q = b0;
+#pragma unroll 1
+                        for (uint32_t j = b0; j < b1; ++j) {
+                            const K y = ob[j];
+                            q += (y < x[r]) | ((y == x[r]) & (j < p));
+                        }
+                    }
+                    dst[r] = q;
+                } else {
+                    dst[r] = 0xFFFFFFFFu;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < LEAF_E; ++r)
+                if (dst[r] != 0xFFFFFFFFu) ob[dst[r]] = x[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < LEAF_E; ++r) {
+            const uint32_t i = (uint32_t)r * NT + tid;
+            if (i < len) __stcs(keys + lo + i, ob[i]);
+        }
+        return;
+    }
+#pragma unroll
+    for (int r = 0; r < LEAF_E; ++r) {
+        const uint32_t i = (uint32_t)r * NT + tid;
+        if (i < len) __stcs(keys + lo + i, ob[lpad(i)]);
+    }
+}
+
 // ===========================================================================
 // CTA-level quicksort of small segments (LEAF < len <= qs_small keys): one
 // CTA runs the whole remaining recursion of its segment -- partitions with
@@ -1431,9 +1615,19 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     if (!qws) return PP_E_NOMEM;
     // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot
     auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
-        // default: packed 32-bit sort for u64 bins of up to 8192 keys, else merge sort
-        const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : (sizeof(K) == 8 ? 4 : 3);
-        if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF / 2) {
+        // default: the counting bin sort (5); 4 = packed 32-bit merge (u64 only), 3 = merge
+        const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : 5;
+        if (algo == 5 && LEAF <= (uint64_t)LC::LEAF / 2) {
+            constexpr int PL = LC::LEAF / 2;
+            const size_t smem = sizeof(K) * lpad_host(PL) + 4 * PL + 16;
+            cudaFuncSetAttribute(qs_leaf_bucket_kernel<K, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_bucket_kernel<K, PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(keys, d_lo, d_len);
+        } else if (algo == 5) {
+            constexpr int PL = LC::LEAF;
+            const size_t smem = sizeof(K) * lpad_host(PL) + 4 * PL + 16;
+            cudaFuncSetAttribute(qs_leaf_bucket_kernel<K, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_bucket_kernel<K, PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(keys, d_lo, d_len);
+        } else if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF / 2) {
             constexpr int PL = PK_LEAF / 2;
             const size_t smem = 8 * PL + 8 * lpad_host(PL) + 4 * lpad_host(PL);
             cudaFuncSetAttribute(qs_leaf_packed_kernel<PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -79,7 +79,8 @@ def test_medium_sizes(pp, dt, mx):
 @pytest.mark.parametrize("params", [{"leaf_algo": 1}, {"leaf_algo": 3}, {"leaf_algo": 3, "leaf": 300},
                                     {"leaf_algo": 2, "leaf": 300}, {"qs_waves": 1}, {"qs_waves": 16, "leaf": 1000},
                                     {"qs_heavy": 1 << 17}, {"qs_heavy": 0}, {"qs_small": 0}, {"strided": 1},
-                                    {"qs_pipe": 1}, {"qs_pipe": 16}, {"qs_small_cfg": 0}, {"qs_small_cfg": 1}])
+                                    {"qs_pipe": 1}, {"qs_pipe": 16}, {"qs_small_cfg": 0}, {"qs_small_cfg": 1},
+                                    {"leaf_algo": 5}, {"leaf_algo": 5, "leaf": 4096}, {"leaf_algo": 5, "leaf": 300}])
 def test_qs_parameters(pp, dt, mx, params):
     """Bin sorts (radix / merge / bitonic), leaf sizes, level balancing, the
     heavy-segment batched cleanup, the per-CTA recursion and the Strided
@@ -128,12 +129,14 @@ def test_config5_full(pp, kind):
         assert lo <= r < hi, r
 
 
-@pytest.mark.parametrize("leaf_algo", [0, 2, 3, 4])
-def test_bin_sorts_clustered(pp, leaf_algo):
+@pytest.mark.parametrize("leaf_algo,leaf", [(0, 0), (2, 0), (3, 0), (4, 0), (5, 0), (5, 4096)])
+def test_bin_sorts_clustered(pp, leaf_algo, leaf):
     """Bins whose keys cluster inside a wide range: the packed 32-bit bin sort
-    (leaf_algo 4, the u64 default) sees runs of equal top bits -- short runs
-    are insertion-sorted, a run of > 64 distinct keys falls back to the
-    64-bit merge sort -- and every bin sort gives the oracle's order."""
+    (leaf_algo 4) sees runs of equal top bits -- short runs are
+    insertion-sorted, a run of > 64 distinct keys falls back to the 64-bit
+    merge sort; the counting bin sort (leaf_algo 5) sees crowded buckets --
+    up to 48 keys per thread's 8 buckets are insertion-sorted, more fall back
+    to the merge sort -- and every bin sort gives the oracle's order."""
     rng = np.random.default_rng(9)
     cases = []
     # 100 clusters of 50 distinct keys each + the maximum: runs of 50 equal tops
@@ -142,7 +145,7 @@ def test_bin_sorts_clustered(pp, leaf_algo):
     # one cluster of 6000 distinct small keys + two huge ones: a run of 6000 -> fallback
     cases.append(np.concatenate([np.arange(6000, dtype=np.uint64), np.array([1 << 63, U64_MAX], dtype=np.uint64)]))
     # clusters of 80 (just above the run limit) and of 64 (at it)
-    for w in (80, 64, 65):
+    for w in (80, 64, 65, 47, 48, 49, 20):
         c = (np.arange(60, dtype=np.uint64)[:, None] << np.uint64(45)) + np.arange(w, dtype=np.uint64)[None, :]
         cases.append(np.concatenate([c.reshape(-1), np.array([U64_MAX - 5], dtype=np.uint64)]))
     # duplicates of few values spread over the whole range
@@ -151,12 +154,12 @@ def test_bin_sorts_clustered(pp, leaf_algo):
         a = a[rng.permutation(a.size)]
         for n in (a.size, min(a.size, 8192), 300):
             b = a[:n].copy()
-            out = _sort_gpu(pp, b, 1, leaf_algo=leaf_algo)
+            out = _sort_gpu(pp, b, 1, leaf_algo=leaf_algo, leaf=leaf)
             assert np.array_equal(out, _oracle_sorted(b)), (leaf_algo, n)
     # the same clusters inside a large quicksort (bins from the per-CTA recursion)
     big = np.concatenate([c.reshape(-1) for c in [cl] * 40] + [synth.uniform_u64_np(300000, 3)])
     big = big[rng.permutation(big.size)]
-    out = _sort_gpu(pp, big, 0, leaf_algo=leaf_algo)
+    out = _sort_gpu(pp, big, 0, leaf_algo=leaf_algo, leaf=leaf)
     assert np.array_equal(out, _oracle_sorted(big))
 
 

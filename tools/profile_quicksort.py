@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Driver for quicksort profiling: sorts n = 2^k u64 keys (uniform or [0,1000)).
 
-    python tools/profile_quicksort.py [--n 28] [--kind uniform|dup1000] [--reps 2]
+    python tools/profile_quicksort.py [--n 28] [--kind uniform|dup1000] [--reps 2] [--params k=v,...]
 """
 import argparse
 import os
@@ -22,8 +22,12 @@ def main():
     ap.add_argument("--n", type=int, default=28)
     ap.add_argument("--kind", default="uniform")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--params", default="", help="k=v,k=v library params")
     args = ap.parse_args()
     pp.load(build_if_missing=False)
+    for kv in filter(None, args.params.split(",")):
+        k, v = kv.split("=")
+        pp.pp_set_param(k, int(v))
     n = 1 << args.n
     if args.kind == "uniform":
         q0 = synth.uniform_u64_torch(n, synth.SEEDS["c5"], "cuda")
