@@ -29,7 +29,9 @@
  * PP_E_INTERNAL: a device-side invariant check failed (never expected).
  *
  * Determinism: output bytes are a pure function of (input bytes, n, pivot,
- * library build): no atomics, fixed thread mappings, a fixed offset seed.
+ * library build): no atomics on the partition paths, fixed thread mappings,
+ * a fixed offset seed.  (The quicksort's bin sort counts with shared-memory
+ * atomics; its output, a sorted array, is unique.)
  */
 #ifndef PP_H_
 #define PP_H_
