@@ -45,7 +45,7 @@ struct Params {
     int64_t leaf = 0;              // quicksort: 0 = auto smem leaf size
     int64_t qs_cta_max = 0;        // quicksort: 0 = auto segment size handled by one CTA
     int64_t variant = 0;           // group-kernel configuration (pp_partition.cu VariantCfg)
-    int64_t leaf_algo = 0;         // quicksort bins: 0 auto (= 5), 1 bitonic, 2 LSD radix, 3 merge, 4 packed 32-bit merge (u64), 5 counting
+    int64_t leaf_algo = 0;         // quicksort bins: 0 auto (= 6), 1 bitonic, 2 LSD radix, 3 merge, 4 packed 32-bit merge (u64), 5 counting, 6 counting (index-staged)
     int64_t fused = 0;             // path 2: one cooperative kernel (1) or the kernel chain (0, faster)
     int64_t fused_stop = 0;        // debug/profiling: stop the fused kernel after this phase
     int64_t qs_waves = 2;          // quicksort mid levels: target CTA waves of the group launch

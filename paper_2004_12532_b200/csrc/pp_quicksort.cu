@@ -442,6 +442,55 @@ __global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
     }
 }
 
+// The bins another bin sort handed over (length word tagged BIN_HANDOFF):
+// a persistent grid walks all slots and merge-sorts the tagged ones (rare:
+// keys clustered inside a wide range), so the untagged majority costs one
+// load each instead of one CTA launch each.
+constexpr uint32_t BIN_HANDOFF = 0x80000000u;
+template <typename K, int LEAF, int NT>
+__global__ void __launch_bounds__(NT) qs_leaf_handoff_kernel(K* __restrict__ keys,
+                                                             const uint64_t* __restrict__ leaf_lo,
+                                                             const uint32_t* __restrict__ leaf_len, uint64_t cnt) {
+    static_assert(LEAF == NT * LEAF_E, "one block holds LEAF keys");
+    extern __shared__ __align__(16) unsigned char lsm[];
+    K* buf = reinterpret_cast<K*>(lsm);
+    const K KMAX = (K)~(K)0;
+    __shared__ uint32_t tags[NT];
+    const uint32_t tid = threadIdx.x;
+    for (uint64_t base = (uint64_t)blockIdx.x * NT; base < cnt; base += (uint64_t)gridDim.x * NT) {
+        const uint32_t t = base + tid < cnt ? leaf_len[base + tid] : 0u;  // one slot per thread
+        tags[tid] = t;
+        if (!__syncthreads_or((t & BIN_HANDOFF) != 0u)) continue;
+        for (uint32_t k = 0; k < (uint32_t)NT; ++k) {
+            const uint32_t tagged = tags[k];
+            if (!(tagged & BIN_HANDOFF)) continue;  // uniform over the CTA
+            const uint32_t len = tagged & ~BIN_HANDOFF;
+            const uint64_t lo = leaf_lo[base + k];
+            const uint32_t P = (len + 32 * LEAF_E - 1) / (32 * LEAF_E) * (32 * LEAF_E);
+            const uint32_t nthr = P / LEAF_E;
+            if (tid < nthr) {
+                K v[LEAF_E];
+#pragma unroll
+                for (int r = 0; r < LEAF_E; ++r) {
+                    const uint32_t i = (uint32_t)r * nthr + tid;
+                    v[r] = i < len ? __ldcs(keys + lo + i) : KMAX;
+                }
+#pragma unroll
+                for (int r = 0; r < LEAF_E; ++r) buf[lpad((uint32_t)r * nthr + tid)] = v[r];
+                leaf_bar(nthr);
+                smem_merge_sort<K>(buf, P, nthr);
+#pragma unroll
+                for (int r = 0; r < LEAF_E; ++r) {
+                    const uint32_t i = (uint32_t)r * nthr + tid;
+                    if (i < len) __stcs(keys + lo + i, buf[lpad(i)]);
+                }
+            }
+            __syncthreads();  // buf is reused by the next tagged bin
+        }
+        __syncthreads();  // tags[] is rewritten by the next chunk
+    }
+}
+
 // Bin sort for u64 keys through 32-bit packed values: p = (top << 13) | i,
 // top = the 19 high bits of (key - min) over the bin's range (all of it when
 // the range has <= 19 bits), i = the key's position in the bin (< 8192).
@@ -747,6 +796,175 @@ __global__ void __launch_bounds__(PLEAF / LEAF_E, 8192 / PLEAF) qs_leaf_bucket_k
     for (int r = 0; r < LEAF_E; ++r) {
         const uint32_t i = (uint32_t)r * NT + tid;
         if (i < len) __stcs(keys + lo + i, ob[lpad(i)]);
+    }
+}
+
+// Bin sort leaf_algo 6: the counting sort of qs_leaf_bucket_kernel with the
+// keys staged in shared memory (input order) and 16-bit key INDICES
+// scattered and ranked instead of the keys: NT = 512 threads x 16 keys,
+// 2 PLEAF buckets (16-bit counts packed two per word).  After the scan every
+// key keeps (its position, its slot in the bucket, the bucket's size) packed
+// in one register, so the index array can then reuse the counters' memory:
+// 96 KiB of shared memory and <= 64 registers -- two CTAs share an SM and
+// one's HBM loads, barriers and scans overlap the other's work (the
+// 1024-thread kernel holds its keys in registers: one CTA per SM).  A bin
+// with a crowded bucket is left untouched and tagged (BIN_HANDOFF in its
+// length word) for qs_leaf_handoff_kernel, launched right after.
+template <typename K, int PLEAF, int NT>
+__global__ void __launch_bounds__(NT, 2) qs_leaf_bidx_kernel(K* __restrict__ keys,
+                                                            const uint64_t* __restrict__ leaf_lo,
+                                                            uint32_t* __restrict__ leaf_len) {
+    constexpr int E = PLEAF / NT, NW = NT / 32, NB = 2 * PLEAF, NWD = NB / 2, WPT = NWD / NT;
+    constexpr int NBITS = PLEAF == 8192 ? 14 : PLEAF == 4096 ? 13 : PLEAF == 2048 ? 12 : 11;
+    static_assert((1 << NBITS) == NB && WPT >= 1 && PLEAF <= (1 << 14), "bin geometry");
+    static_assert(BK_MAX_RUN < 64, "bucket size fits the 6-bit field");
+    extern __shared__ __align__(16) unsigned char lsm[];
+    K* ks = reinterpret_cast<K*>(lsm);                          // [PLEAF] keys, input order
+    uint32_t* cw = reinterpret_cast<uint32_t*>(ks + PLEAF);     // [NWD + 1] packed counts, then starts
+    uint16_t* ix = reinterpret_cast<uint16_t*>(cw);             // [PLEAF] key indices (after the starts are read)
+    __shared__ K rmn[NW], rmx[NW];
+    __shared__ uint64_t sw[32];
+    __shared__ int handoff;
+    const K KMAX = (K)~(K)0;
+    const uint64_t lo = leaf_lo[blockIdx.x];
+    const uint32_t len = leaf_len[blockIdx.x];
+    if (len < 2) return;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    K mn = KMAX, mx = 0;
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const uint32_t i = (uint32_t)r * NT + tid;
+        if (i < len) {
+            const K v = __ldcs(keys + lo + i);
+            ks[i] = v;
+            mn = v < mn ? v : mn;
+            mx = v > mx ? v : mx;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) cw[j * NT + tid] = 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const K a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+    }
+    if (lane == 0) {
+        rmn[warp] = mn;
+        rmx[warp] = mx;
+    }
+    if (tid == 0) {
+        handoff = 0;
+        cw[NWD] = len;  // the end of the last bucket
+    }
+    __syncthreads();
+    if (warp == 0) {
+        mn = lane < NW ? rmn[lane] : KMAX;
+        mx = lane < NW ? rmx[lane] : (K)0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const K a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+        }
+        if (lane == 0) {
+            rmn[0] = mn;
+            rmx[0] = mx;
+        }
+    }
+    __syncthreads();
+    mn = rmn[0];
+    mx = rmx[0];
+    if (mn == mx) return;
+    const int bits = key_bits<K>(mx - mn);
+    const int sh = bits > NBITS ? bits - NBITS : 0;
+    // per key: pos (14 bits) | slot in its bucket (6 bits) << 14 | min(bucket size, 63) << 20
+    uint32_t meta[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const uint32_t i = (uint32_t)r * NT + tid;
+        meta[r] = 0u;
+        if (i < len) {
+            const uint32_t d = (uint32_t)((ks[i] - mn) >> sh), hs = (d & 1u) * 16u;
+            meta[r] = (atomicAdd(&cw[d >> 1], 1u << hs) >> hs) & 0xFFFFu;  // the slot (for now)
+        }
+    }
+    __syncthreads();
+    {  // bucket starts: thread t owns words [WPT t, WPT t + WPT)
+        uint32_t c[WPT], s = 0;
+#pragma unroll
+        for (int j = 0; j < WPT; ++j) {
+            c[j] = cw[tid * WPT + j];
+            s += (c[j] & 0xFFFFu) + (c[j] >> 16);
+        }
+        uint64_t tot;
+        uint32_t e = (uint32_t)block_exscan<NT>(s, sw, tot);
+        if (sh > 0) {
+#pragma unroll
+            for (int j = 0; j < WPT; ++j)
+                if ((c[j] & 0xFFFFu) > BK_MAX_RUN || (c[j] >> 16) > BK_MAX_RUN) handoff = 1;
+        }
+#pragma unroll
+        for (int j = 0; j < WPT; ++j) {
+            const uint32_t e1 = e + (c[j] & 0xFFFFu);
+            cw[tid * WPT + j] = e | (e1 << 16);
+            e = e1 + (c[j] >> 16);
+        }
+    }
+    __syncthreads();
+    if (handoff) {  // crowded buckets: the handoff merge sort takes this bin (keys untouched)
+        if (tid == 0) leaf_len[blockIdx.x] = len | BIN_HANDOFF;
+        return;
+    }
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const uint32_t i = (uint32_t)r * NT + tid;
+        if (i < len) {
+            const uint32_t d = (uint32_t)((ks[i] - mn) >> sh);
+            const uint32_t w = cw[d >> 1];
+            const uint32_t b0 = (d & 1u) ? w >> 16 : w & 0xFFFFu;
+            const uint32_t b1 = (d & 1u) ? cw[(d >> 1) + 1] & 0xFFFFu : w >> 16;
+            const uint32_t slot = meta[r];
+            meta[r] = (b0 + slot) | ((slot & 63u) << 14) | (min(b1 - b0, 63u) << 20);
+        }
+    }
+    __syncthreads();  // the counters are dead: ix takes their memory
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const uint32_t i = (uint32_t)r * NT + tid;
+        if (i < len) ix[meta[r] & 0x3FFFu] = (uint16_t)i;
+    }
+    __syncthreads();
+    if (sh > 0) {  // final place inside the bucket: smaller keys, ties by scatter slot
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const uint32_t i = (uint32_t)r * NT + tid;
+            const uint32_t c = meta[r] >> 20;
+            if (i < len && c > 1) {
+                const K x = ks[i];
+                const uint32_t p = meta[r] & 0x3FFFu, slot = (meta[r] >> 14) & 63u, b0 = p - slot;
+                uint32_t q = b0;
+#pragma unroll 1
+                for (uint32_t k = 0; k + 1 < c; ++k) {  // the bucket's other keys (skip its own slot)
+                    const uint32_t m = b0 + k + (k >= slot);
+                    const K y = ks[ix[m]];
+                    q += (y < x) | ((y == x) & (m < p));
+                }
+                meta[r] = (meta[r] & ~0x3FFFu) | q | 0x80000000u;  // moved
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const uint32_t i = (uint32_t)r * NT + tid;
+            if (i < len && (meta[r] & 0x80000000u)) ix[meta[r] & 0x3FFFu] = (uint16_t)i;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const uint32_t j = (uint32_t)r * NT + tid;
+        if (j < len) __stcs(keys + lo + j, ks[ix[j]]);
     }
 }
 
@@ -1615,9 +1833,25 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     if (!qws) return PP_E_NOMEM;
     // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot
     auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
-        // default: the counting bin sort (5); 4 = packed 32-bit merge (u64 only), 3 = merge
-        const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : 5;
-        if (algo == 5 && LEAF <= (uint64_t)LC::LEAF / 2) {
+        if (cnt == 0) return cudaSuccess;
+        // default: the index-staged counting bin sort (6); 5 = counting with keys in registers,
+        // 4 = packed 32-bit merge (u64 only), 3 = merge
+        const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : 6;
+        if (algo == 6) {
+            constexpr int PL = LC::LEAF, BNT = 512;
+            const size_t smem = sizeof(K) * PL + 4 * PL + 16;
+            cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
+                                                                              const_cast<uint32_t*>(d_len));
+            const size_t msmem = sizeof(K) * (PL + PL / 8);
+            cudaFuncSetAttribute(qs_leaf_handoff_kernel<K, PL, PL / LEAF_E>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
+            const unsigned hg = (unsigned)std::min<uint64_t>((cnt + PL / LEAF_E - 1) / (PL / LEAF_E),
+                                                             2 * (uint64_t)sm_count());
+            qs_leaf_handoff_kernel<K, PL, PL / LEAF_E><<<hg, PL / LEAF_E, msmem, bst>>>(keys, d_lo, d_len, cnt);
+            note_launches(1);
+        } else if (algo == 5 && LEAF <= (uint64_t)LC::LEAF / 2) {
             constexpr int PL = LC::LEAF / 2;
             const size_t smem = sizeof(K) * lpad_host(PL) + 4 * PL + 16;
             cudaFuncSetAttribute(qs_leaf_bucket_kernel<K, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

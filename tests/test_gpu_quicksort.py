@@ -80,7 +80,8 @@ def test_medium_sizes(pp, dt, mx):
                                     {"leaf_algo": 2, "leaf": 300}, {"qs_waves": 1}, {"qs_waves": 16, "leaf": 1000},
                                     {"qs_heavy": 1 << 17}, {"qs_heavy": 0}, {"qs_small": 0}, {"strided": 1},
                                     {"qs_pipe": 1}, {"qs_pipe": 16}, {"qs_small_cfg": 0}, {"qs_small_cfg": 1},
-                                    {"leaf_algo": 5}, {"leaf_algo": 5, "leaf": 4096}, {"leaf_algo": 5, "leaf": 300}])
+                                    {"leaf_algo": 5}, {"leaf_algo": 5, "leaf": 4096}, {"leaf_algo": 5, "leaf": 300},
+                                    {"leaf_algo": 6}, {"leaf_algo": 6, "leaf": 300}])
 def test_qs_parameters(pp, dt, mx, params):
     """Bin sorts (radix / merge / bitonic), leaf sizes, level balancing, the
     heavy-segment batched cleanup, the per-CTA recursion and the Strided
@@ -129,7 +130,7 @@ def test_config5_full(pp, kind):
         assert lo <= r < hi, r
 
 
-@pytest.mark.parametrize("leaf_algo,leaf", [(0, 0), (2, 0), (3, 0), (4, 0), (5, 0), (5, 4096)])
+@pytest.mark.parametrize("leaf_algo,leaf", [(0, 0), (2, 0), (3, 0), (4, 0), (5, 0), (5, 4096), (6, 0), (6, 1000)])
 def test_bin_sorts_clustered(pp, leaf_algo, leaf):
     """Bins whose keys cluster inside a wide range: the packed 32-bit bin sort
     (leaf_algo 4) sees runs of equal top bits -- short runs are
