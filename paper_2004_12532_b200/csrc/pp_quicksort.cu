@@ -443,17 +443,20 @@ __global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
 }
 
 // The bins another bin sort handed over (length word tagged BIN_HANDOFF):
-// a persistent grid walks all slots and merge-sorts the tagged ones (rare:
-// keys clustered inside a wide range), so the untagged majority costs one
-// load each instead of one CTA launch each.
+// a persistent grid walks all slots (one per thread) and merge-sorts the
+// tagged ones (rare: keys clustered inside a wide range), so the untagged
+// majority costs one load each instead of one CTA launch each.  Bins of up
+// to 2 LEAF keys: each half is merge-sorted in its part of one padded buffer
+// (the second half right after the first, so the pair is laid out as two
+// adjacent runs) and one merge-path round writes the result to global memory.
 constexpr uint32_t BIN_HANDOFF = 0x80000000u;
 template <typename K, int LEAF, int NT>
 __global__ void __launch_bounds__(NT) qs_leaf_handoff_kernel(K* __restrict__ keys,
                                                              const uint64_t* __restrict__ leaf_lo,
                                                              const uint32_t* __restrict__ leaf_len, uint64_t cnt) {
-    static_assert(LEAF == NT * LEAF_E, "one block holds LEAF keys");
+    static_assert(LEAF == NT * LEAF_E, "one block holds LEAF keys per half");
     extern __shared__ __align__(16) unsigned char lsm[];
-    K* buf = reinterpret_cast<K*>(lsm);
+    K* buf = reinterpret_cast<K*>(lsm);  // [lpad(2 LEAF)]
     const K KMAX = (K)~(K)0;
     __shared__ uint32_t tags[NT];
     const uint32_t tid = threadIdx.x;
@@ -466,23 +469,35 @@ __global__ void __launch_bounds__(NT) qs_leaf_handoff_kernel(K* __restrict__ key
             if (!(tagged & BIN_HANDOFF)) continue;  // uniform over the CTA
             const uint32_t len = tagged & ~BIN_HANDOFF;
             const uint64_t lo = leaf_lo[base + k];
-            const uint32_t P = (len + 32 * LEAF_E - 1) / (32 * LEAF_E) * (32 * LEAF_E);
-            const uint32_t nthr = P / LEAF_E;
-            if (tid < nthr) {
-                K v[LEAF_E];
+            const uint32_t h1 = len < (uint32_t)LEAF ? len : (uint32_t)LEAF, h2 = len - h1;
+            const uint32_t P1 = (h1 + 32 * LEAF_E - 1) / (32 * LEAF_E) * (32 * LEAF_E);
+            const uint32_t P2 = (h2 + 32 * LEAF_E - 1) / (32 * LEAF_E) * (32 * LEAF_E);
+            K* buf2 = buf + lpad(LEAF);
+#pragma unroll
+            for (int r = 0; r < LEAF_E; ++r) {
+                const uint32_t i = (uint32_t)r * NT + tid;
+                if (i < P1) buf[lpad(i)] = i < h1 ? __ldcs(keys + lo + i) : KMAX;
+                if (i < P2) buf2[lpad(i)] = i < h2 ? __ldcs(keys + lo + LEAF + i) : KMAX;
+            }
+            __syncthreads();
+            if (tid < P1 / LEAF_E) smem_merge_sort<K>(buf, P1, P1 / LEAF_E);
+            __syncthreads();
+            if (h2 == 0) {
 #pragma unroll
                 for (int r = 0; r < LEAF_E; ++r) {
-                    const uint32_t i = (uint32_t)r * nthr + tid;
-                    v[r] = i < len ? __ldcs(keys + lo + i) : KMAX;
-                }
-#pragma unroll
-                for (int r = 0; r < LEAF_E; ++r) buf[lpad((uint32_t)r * nthr + tid)] = v[r];
-                leaf_bar(nthr);
-                smem_merge_sort<K>(buf, P, nthr);
-#pragma unroll
-                for (int r = 0; r < LEAF_E; ++r) {
-                    const uint32_t i = (uint32_t)r * nthr + tid;
+                    const uint32_t i = (uint32_t)r * NT + tid;
                     if (i < len) __stcs(keys + lo + i, buf[lpad(i)]);
+                }
+            } else {
+                if (tid < P2 / LEAF_E) smem_merge_sort<K>(buf2, P2, P2 / LEAF_E);
+                __syncthreads();
+                // runs [0, LEAF) and [LEAF, LEAF + P2): 8 outputs per chunk, two chunks per thread
+                for (uint32_t c = tid; c < (LEAF + P2) / LEAF_E; c += NT) {
+                    K v[LEAF_E];
+                    merge_chunk_regs<K>(buf, c * LEAF_E, LEAF, LEAF + P2, v);
+#pragma unroll
+                    for (int r = 0; r < LEAF_E; ++r)
+                        if (c * LEAF_E + r < len) __stcs(keys + lo + c * LEAF_E + r, v[r]);
                 }
             }
             __syncthreads();  // buf is reused by the next tagged bin
@@ -811,11 +826,11 @@ __global__ void __launch_bounds__(PLEAF / LEAF_E, 8192 / PLEAF) qs_leaf_bucket_k
 // with a crowded bucket is left untouched and tagged (BIN_HANDOFF in its
 // length word) for qs_leaf_handoff_kernel, launched right after.
 template <typename K, int PLEAF, int NT>
-__global__ void __launch_bounds__(NT, 2) qs_leaf_bidx_kernel(K* __restrict__ keys,
+__global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kernel(K* __restrict__ keys,
                                                             const uint64_t* __restrict__ leaf_lo,
                                                             uint32_t* __restrict__ leaf_len) {
     constexpr int E = PLEAF / NT, NW = NT / 32, NB = 2 * PLEAF, NWD = NB / 2, WPT = NWD / NT;
-    constexpr int NBITS = PLEAF == 8192 ? 14 : PLEAF == 4096 ? 13 : PLEAF == 2048 ? 12 : 11;
+    constexpr int NBITS = PLEAF == 16384 ? 15 : PLEAF == 8192 ? 14 : PLEAF == 4096 ? 13 : PLEAF == 2048 ? 12 : 11;
     static_assert((1 << NBITS) == NB && WPT >= 1 && PLEAF <= (1 << 14), "bin geometry");
     static_assert(BK_MAX_RUN < 64, "bucket size fits the 6-bit field");
     extern __shared__ __align__(16) unsigned char lsm[];
@@ -1510,8 +1525,11 @@ static QsGeom qs_geom() {
     using LC = LeafCfg<K>;
     const Params& P = params();
     QsGeom q;
-    // leaf capacity: default LC::LEAF (8192 keys); "leaf" may lower it
-    q.LEAF = (P.leaf > 0 && (uint64_t)P.leaf <= (uint64_t)LC::LEAF) ? (uint64_t)P.leaf : (uint64_t)LC::LEAF;
+    // leaf capacity: LC::LEAF (8192 keys) for the bin sorts 1-5; the default
+    // bin sort (6) takes bins of up to 2 LC::LEAF and defaults to that;
+    // "leaf" may lower it
+    const uint64_t lmax = (P.leaf_algo == 0 || P.leaf_algo == 6) ? 2 * (uint64_t)LC::LEAF : (uint64_t)LC::LEAF;
+    q.LEAF = (P.leaf > 0 && (uint64_t)P.leaf <= lmax) ? (uint64_t)P.leaf : lmax;
     q.BIG = P.qs_cta_max > 0 ? (uint64_t)P.qs_cta_max : (uint64_t)1 << 27;
     q.SMALL = P.qs_small > 0 ? std::max<uint64_t>((uint64_t)P.qs_small, q.LEAF) : q.LEAF;
     q.HEAVY = P.qs_heavy > 0 ? std::max<uint64_t>((uint64_t)P.qs_heavy, q.SMALL + 1) : 0;
@@ -1837,19 +1855,28 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         // default: the index-staged counting bin sort (6); 5 = counting with keys in registers,
         // 4 = packed 32-bit merge (u64 only), 3 = merge
         const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : 6;
-        if (algo == 6) {
-            constexpr int PL = LC::LEAF, BNT = 512;
-            const size_t smem = sizeof(K) * PL + 4 * PL + 16;
-            cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
-                                                                              const_cast<uint32_t*>(d_len));
-            const size_t msmem = sizeof(K) * (PL + PL / 8);
-            cudaFuncSetAttribute(qs_leaf_handoff_kernel<K, PL, PL / LEAF_E>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
-            const unsigned hg = (unsigned)std::min<uint64_t>((cnt + PL / LEAF_E - 1) / (PL / LEAF_E),
-                                                             2 * (uint64_t)sm_count());
-            qs_leaf_handoff_kernel<K, PL, PL / LEAF_E><<<hg, PL / LEAF_E, msmem, bst>>>(keys, d_lo, d_len, cnt);
+        if (algo == 6) {  // bins of <= 2 LC::LEAF keys (1024 threads) or <= LC::LEAF (512 threads, 2 CTAs/SM)
+            constexpr int HL = LC::LEAF, HN = HL / LEAF_E;
+            if (LEAF > (uint64_t)HL) {
+                constexpr int PL = 2 * HL, BNT = 1024;
+                const size_t smem = sizeof(K) * PL + 4 * PL + 16;
+                cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+                qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
+                                                                                  const_cast<uint32_t*>(d_len));
+            } else {
+                constexpr int PL = HL, BNT = 512;
+                const size_t smem = sizeof(K) * PL + 4 * PL + 16;
+                cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+                qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
+                                                                                  const_cast<uint32_t*>(d_len));
+            }
+            const size_t msmem = sizeof(K) * lpad_host(2 * HL);
+            cudaFuncSetAttribute(qs_leaf_handoff_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)msmem);
+            const unsigned hg = (unsigned)std::min<uint64_t>((cnt + HN - 1) / HN, 2 * (uint64_t)sm_count());
+            qs_leaf_handoff_kernel<K, HL, HN><<<hg, HN, msmem, bst>>>(keys, d_lo, d_len, cnt);
             note_launches(1);
         } else if (algo == 5 && LEAF <= (uint64_t)LC::LEAF / 2) {
             constexpr int PL = LC::LEAF / 2;

@@ -130,7 +130,8 @@ def test_config5_full(pp, kind):
         assert lo <= r < hi, r
 
 
-@pytest.mark.parametrize("leaf_algo,leaf", [(0, 0), (2, 0), (3, 0), (4, 0), (5, 0), (5, 4096), (6, 0), (6, 1000)])
+@pytest.mark.parametrize("leaf_algo,leaf", [(0, 0), (2, 0), (3, 0), (4, 0), (5, 0), (5, 4096), (6, 0), (6, 1000),
+                                            (6, 8192), (6, 12000)])
 def test_bin_sorts_clustered(pp, leaf_algo, leaf):
     """Bins whose keys cluster inside a wide range: the packed 32-bit bin sort
     (leaf_algo 4) sees runs of equal top bits -- short runs are
@@ -146,14 +147,14 @@ def test_bin_sorts_clustered(pp, leaf_algo, leaf):
     # one cluster of 6000 distinct small keys + two huge ones: a run of 6000 -> fallback
     cases.append(np.concatenate([np.arange(6000, dtype=np.uint64), np.array([1 << 63, U64_MAX], dtype=np.uint64)]))
     # clusters of 80 (just above the run limit) and of 64 (at it)
-    for w in (80, 64, 65, 47, 48, 49, 20):
+    for w in (80, 64, 65, 47, 48, 49, 20, 300):
         c = (np.arange(60, dtype=np.uint64)[:, None] << np.uint64(45)) + np.arange(w, dtype=np.uint64)[None, :]
         cases.append(np.concatenate([c.reshape(-1), np.array([U64_MAX - 5], dtype=np.uint64)]))
     # duplicates of few values spread over the whole range
     cases.append(rng.choice(np.array([0, 5, 1 << 40, 1 << 63, U64_MAX], dtype=np.uint64), size=8000))
     for a in cases:
         a = a[rng.permutation(a.size)]
-        for n in (a.size, min(a.size, 8192), 300):
+        for n in (a.size, min(a.size, 8192), min(a.size, 16384), min(a.size, 12345), 300):
             b = a[:n].copy()
             out = _sort_gpu(pp, b, 1, leaf_algo=leaf_algo, leaf=leaf)
             assert np.array_equal(out, _oracle_sorted(b)), (leaf_algo, n)
