@@ -189,6 +189,31 @@ pp_status pp_dist_finalize(void);
 pp_status pp_swap_ranges_u64(const uint64_t *triples, uint64_t n_pieces, void *stream);
 pp_status pp_swap_ranges_u32(const uint64_t *triples, uint64_t n_pieces, void *stream);
 
+/* One-sided (staging-free) exchange of pp_partition_dist_* (
+ * param "dist_p2p" = 1, default 0): every rank maps every other rank's shard
+ * through CUDA IPC and swaps its share of the misplaced pairs directly with
+ * pp_swap_ranges' kernel; a closing collective keeps ranks from returning
+ * while a peer still writes into their shard.  Needs peer access between the
+ * GPUs (NVLink/NVSwitch).
+ * pp_dist_p2p_pieces: the share of rank `rank` (host arithmetic, no GPU): for
+ *   shard sizes ns[P] and local splits ts[P], writes *n_out rows of 5 uint64
+ *   {rank_a, a, rank_b, b, len} -- swap GLOBAL positions [a, a+len) (on
+ *   rank_a, misplaced successors) with [b, b+len) (on rank_b, misplaced
+ *   predecessors) -- into out[5*out_cap].  Every matched run of the plan is
+ *   split: the left rank takes the first ceil(len/2) pairs, the right rank the
+ *   rest, so each pair is swapped by exactly one rank.  PP_E_INVAL if out_cap
+ *   is too small (n_out still set), ts[r] > ns[r], or rank is out of range.
+ * pp_ipc_export: (64-byte CUDA IPC handle of the allocation holding d_ptr,
+ *   byte offset of d_ptr in it) -> handle_out[64], *offset_out.
+ * pp_ipc_import: maps an exported range in this process (cached per handle;
+ *   peer access enabled lazily) -> *d_ptr_out = mapped base + offset.
+ * pp_ipc_close_all: unmaps every imported range (pp_dist_finalize does too). */
+pp_status pp_dist_p2p_pieces(const uint64_t *ns, const uint64_t *ts, int nranks, int rank, uint64_t *out,
+                             uint64_t out_cap, uint64_t *n_out);
+pp_status pp_ipc_export(const void *d_ptr, void *handle_out, uint64_t *offset_out);
+pp_status pp_ipc_import(const void *handle, uint64_t offset, void **d_ptr_out);
+pp_status pp_ipc_close_all(void);
+
 /* ---- Smoothed Striding partial partition step alone (parity of internals) --
  * Runs only the group kernel on the 16-B aligned region of `keys` with g
  * groups (g = 0: the library's automatic choice) and copies the per-group
@@ -231,7 +256,7 @@ pp_status pp_last_stats(uint64_t *out13);
  * "path" (0 auto, 1 single-CTA, 2 smoothed striding, 3 cleanup only), "tile",
  * "ranks", "seed", "strided" (1: X = 0, the Strided Algorithm PAPER.md:796-825,
  * i.e. seed 0; 0: back to the default seed), "leaf", "qs_cta_max", "variant",
- * "leaf_algo", "fused", "qs_small", "qs_small_cfg", "qs_waves".  Returns PP_E_INVAL for an unknown
+ * "leaf_algo", "fused", "qs_small", "qs_small_cfg", "qs_waves", "dist_p2p".  Returns PP_E_INVAL for an unknown
  * name.  pp_get_param returns INT64_MIN for an unknown name. */
 pp_status pp_set_param(const char *name, int64_t value);
 int64_t pp_get_param(const char *name);

@@ -111,6 +111,10 @@ def load(build_if_missing: bool = True):
         "pp_quicksort_dist_u32": ([vp, u64, vp], st),
         "pp_dist_plan": ([P64, P64, ctypes.c_int, u64, P64, u64, P64, P64], st),
         "pp_dist_finalize": ([], st),
+        "pp_dist_p2p_pieces": ([P64, P64, ctypes.c_int, ctypes.c_int, P64, u64, P64], st),
+        "pp_ipc_export": ([vp, vp, P64], st),
+        "pp_ipc_import": ([vp, u64, ctypes.POINTER(ctypes.c_void_p)], st),
+        "pp_ipc_close_all": ([], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -374,6 +378,43 @@ def pp_dist_plan(ns, ts, cap: int):
                                rows.ctypes.data_as(P64), n_out.value, ctypes.byref(n_out), ctypes.byref(K)),
            "pp_dist_plan")
     return int(K.value), [tuple(int(x) for x in r) for r in rows[: n_out.value]]
+
+
+def pp_dist_p2p_pieces(ns, ts, rank: int):
+    """The share of `rank` in the one-sided exchange (host arithmetic): rows
+    of (rank_a, a, rank_b, b, len), global positions."""
+    P = len(ns)
+    a = np.ascontiguousarray(np.asarray(ns, dtype=np.uint64))
+    b = np.ascontiguousarray(np.asarray(ts, dtype=np.uint64))
+    P64 = ctypes.POINTER(ctypes.c_uint64)
+    n_out = ctypes.c_uint64(0)
+    _check(load().pp_dist_p2p_pieces(a.ctypes.data_as(P64), b.ctypes.data_as(P64), P, int(rank), None, 0,
+                                     ctypes.byref(n_out)), "pp_dist_p2p_pieces")
+    rows = np.zeros((max(1, n_out.value), 5), dtype=np.uint64)
+    _check(load().pp_dist_p2p_pieces(a.ctypes.data_as(P64), b.ctypes.data_as(P64), P, int(rank),
+                                     rows.ctypes.data_as(P64), n_out.value, ctypes.byref(n_out)),
+           "pp_dist_p2p_pieces")
+    return [tuple(int(x) for x in r) for r in rows[: n_out.value]]
+
+
+def pp_ipc_export(t) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding t, byte offset)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64(0)
+    _check(load().pp_ipc_export(t.data_ptr(), h, ctypes.byref(off)), "pp_ipc_export")
+    return h.raw, int(off.value)
+
+
+def pp_ipc_import(handle: bytes, offset: int) -> int:
+    """Maps an exported range in this process; returns its device address."""
+    h = ctypes.create_string_buffer(bytes(handle), 64)
+    out = ctypes.c_void_p(0)
+    _check(load().pp_ipc_import(h, int(offset), ctypes.byref(out)), "pp_ipc_import")
+    return int(out.value or 0)
+
+
+def pp_ipc_close_all() -> None:
+    _check(load().pp_ipc_close_all(), "pp_ipc_close_all")
 
 
 def pp_swap_ranges(pieces, key_bytes: int = 8, stream=None) -> None:

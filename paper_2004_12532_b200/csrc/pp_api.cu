@@ -578,6 +578,22 @@ pp_status pp_dist_plan(const uint64_t* ns, const uint64_t* ts, int nranks, uint6
                        uint64_t out_cap, uint64_t* n_out, uint64_t* K_out) {
     return dist_plan(ns, ts, nranks, cap, out, out_cap, n_out, K_out);
 }
+pp_status pp_dist_p2p_pieces(const uint64_t* ns, const uint64_t* ts, int nranks, int rank, uint64_t* out,
+                             uint64_t out_cap, uint64_t* n_out) {
+    return dist_p2p_pieces(ns, ts, nranks, rank, out, out_cap, n_out);
+}
+pp_status pp_ipc_export(const void* d_ptr, void* handle_out, uint64_t* offset_out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return ipc_export(d_ptr, handle_out, offset_out);
+}
+pp_status pp_ipc_import(const void* handle, uint64_t offset, void** d_ptr_out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return ipc_import(handle, offset, d_ptr_out);
+}
+pp_status pp_ipc_close_all(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return ipc_close_all();
+}
 
 uint64_t pp_workspace_bytes(uint64_t n, int key_bytes, int op) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -659,6 +675,7 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "qs_heavy") P.qs_heavy = value;
     else if (k == "host_chunk") P.host_chunk = value;
     else if (k == "qs_pipe") P.qs_pipe = value;
+    else if (k == "dist_p2p") P.dist_p2p = value ? 1 : 0;
     else if (k == "bps_nt") P.bps_nt = value;
     else if (k == "cleanup_chain") P.cleanup_chain = value;
     else if (k == "cleanup_bitmap") P.cleanup_bitmap = value;
@@ -693,6 +710,7 @@ int64_t pp_get_param(const char* name) {
     if (k == "qs_heavy") return P.qs_heavy;
     if (k == "host_chunk") return P.host_chunk;
     if (k == "qs_pipe") return P.qs_pipe;
+    if (k == "dist_p2p") return P.dist_p2p;
     if (k == "bps_nt") return P.bps_nt;
     if (k == "cleanup_chain") return P.cleanup_chain;
     if (k == "cleanup_bitmap") return P.cleanup_bitmap;

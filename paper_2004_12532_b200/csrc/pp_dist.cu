@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>  // driver types only (cuMemGetAddressRange is fetched through the runtime)
 #include <nccl.h>
 
 #include "pp_internal.h"
@@ -73,6 +74,105 @@ static uint64_t plan_pieces(const uint64_t* ns, const uint64_t* ts, int P, uint6
         if (T[j].s == T[j].e) ++j;
     }
     return K;
+}
+
+// One-sided (staging-free) exchange: who executes which pairs.  The plan
+// with no staging cap has one piece per matched run (the left rank's
+// misplaced successors [f, f+len) against the right rank's misplaced
+// predecessors [t, t+len); the two ranks always differ, because a shard's
+// misplaced keys are all successors (shard ends left of K) or all
+// predecessors).  The left rank swaps the first ceil(len/2) pairs, the right
+// rank the rest, each reading and writing its partner's keys through the
+// peer mapping, so both directions of every NVLink pair carry traffic.
+// Mirrored by paper_2004_12532_b200/dist.py p2p_pieces (tests/test_dist.py).
+struct P2PPiece {
+    uint64_t rank_a, a, rank_b, b, len;
+};
+static uint64_t p2p_pieces(const uint64_t* ns, const uint64_t* ts, int P, int me, std::vector<P2PPiece>& out) {
+    std::vector<Piece> pcs;
+    const uint64_t K = plan_pieces(ns, ts, P, ~0ull, pcs);
+    out.clear();
+    for (const Piece& p : pcs) {
+        const uint64_t h = (p.len + 1) / 2;
+        if ((int)p.rank_f == me) out.push_back({p.rank_f, p.f, p.rank_t, p.t, h});
+        if ((int)p.rank_t == me && p.len > h) out.push_back({p.rank_f, p.f + h, p.rank_t, p.t + h, p.len - h});
+    }
+    return K;
+}
+
+// ---------------------------------------------------------------------------
+// CUDA IPC: a device range exported as (allocation handle, offset) and
+// mapped in another process (peer access enabled lazily).  Mappings are
+// cached by handle and released by ipc_close_all / dist_finalize.
+// ---------------------------------------------------------------------------
+struct IpcMap {
+    cudaIpcMemHandle_t h;
+    void* base;
+};
+static std::vector<IpcMap> g_ipc;
+
+static pp_status alloc_base(const void* p, void** base) {
+    using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !f) {
+            set_error("cuMemGetAddressRange unavailable");
+            return PP_E_CUDA;
+        }
+        fn = reinterpret_cast<Fn>(f);
+    }
+    CUdeviceptr b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, (CUdeviceptr)p) != CUDA_SUCCESS) {
+        set_error("cuMemGetAddressRange failed (not a device allocation?)");
+        return PP_E_INVAL;
+    }
+    *base = reinterpret_cast<void*>(b);
+    return PP_OK;
+}
+
+pp_status ipc_export(const void* d_ptr, void* handle_out, uint64_t* offset_out) {
+    if (!d_ptr || !handle_out || !offset_out) return PP_E_INVAL;
+    void* base = nullptr;
+    pp_status s = alloc_base(d_ptr, &base);
+    if (s != PP_OK) return s;
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, base);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "64-byte IPC handle");
+    memcpy(handle_out, &h, 64);
+    *offset_out = (uint64_t)(static_cast<const char*>(d_ptr) - static_cast<const char*>(base));
+    return PP_OK;
+}
+
+pp_status ipc_import(const void* handle, uint64_t offset, void** d_ptr_out) {
+    if (!handle || !d_ptr_out) return PP_E_INVAL;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    for (const IpcMap& m : g_ipc)
+        if (memcmp(&m.h, &h, 64) == 0) {
+            *d_ptr_out = static_cast<char*>(m.base) + offset;
+            return PP_OK;
+        }
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    g_ipc.push_back({h, base});
+    *d_ptr_out = static_cast<char*>(base) + offset;
+    return PP_OK;
+}
+
+pp_status ipc_close_all() {
+    cudaError_t first = cudaSuccess;
+    for (const IpcMap& m : g_ipc) {
+        cudaError_t e = cudaIpcCloseMemHandle(m.base);
+        if (first == cudaSuccess) first = e;
+    }
+    g_ipc.clear();
+    return first == cudaSuccess ? PP_OK : cuda_fail(first, "cudaIpcCloseMemHandle");
 }
 
 // ---------------------------------------------------------------------------
@@ -179,6 +279,7 @@ pp_status dist_init(const void* id128, int nranks, int rank, int device) {
 }
 
 pp_status dist_finalize() {
+    ipc_close_all();
     if (g_dist.comm) g_nccl.CommDestroy(g_dist.comm);
     g_dist.comm = nullptr;
     if (g_dist.staging) cudaFree(g_dist.staging);
@@ -190,6 +291,60 @@ pp_status dist_finalize() {
 }
 
 void dist_set_staging(uint64_t bytes) { g_dist.staging_cap_bytes = bytes < 16 ? 16 : bytes; }
+
+static pp_status allgather_u64(const uint64_t* host_in, uint64_t count, std::vector<uint64_t>& host_out,
+                               cudaStream_t st);
+template <typename K>
+static pp_status swap_ranges_impl(const uint64_t* host_tri, uint64_t np, cudaStream_t st, bool sys_fence);
+
+// The exchange one-sidedly over CUDA-IPC peer mappings (param dist_p2p):
+// every rank's shard is mapped on every rank (handles + offsets gathered
+// once per call, mappings cached), each rank swaps its share of the pairs
+// (p2p_pieces) with swap_ranges_kernel directly between its shard and the
+// peers' -- no staging buffer, no second copy -- and a final collective keeps
+// any rank from returning while a peer may still be writing into its shard.
+// Ordering: a rank's swaps are enqueued after the (n_r, t_r) all-gather, which
+// completes only once every rank has contributed, i.e. after every rank's
+// local partition finished (stream order).  Needs peer access between the
+// GPUs (NVLink / NVSwitch); untested here beyond one GPU.
+template <typename K>
+static pp_status exchange_p2p(K* shard, uint64_t n_local, const std::vector<uint64_t>& ns,
+                              const std::vector<uint64_t>& ts, cudaStream_t st) {
+    const int P = g_dist.nranks, me = g_dist.rank;
+    std::vector<uint64_t> mine(9, 0), all;
+    if (n_local > 0) {
+        pp_status s = ipc_export(shard, mine.data(), &mine[8]);
+        if (s != PP_OK) return s;
+    }
+    pp_status s = allgather_u64(mine.data(), 9, all, st);
+    if (s != PP_OK) return s;
+    std::vector<P2PPiece> pcs;
+    p2p_pieces(ns.data(), ts.data(), P, me, pcs);
+    std::vector<uint64_t> bases(P, 0);
+    for (int q = 1; q < P; ++q) bases[q] = bases[q - 1] + ns[q - 1];
+    std::vector<K*> ptr(P, nullptr);
+    ptr[me] = shard;
+    for (const P2PPiece& p : pcs) {
+        for (uint64_t q : {p.rank_a, p.rank_b}) {
+            if (ptr[q]) continue;
+            void* d = nullptr;
+            s = ipc_import(&all[9 * q], all[9 * q + 8], &d);
+            if (s != PP_OK) return s;
+            ptr[q] = static_cast<K*>(d);
+        }
+    }
+    std::vector<uint64_t> tri;
+    for (const P2PPiece& p : pcs) {
+        tri.push_back(reinterpret_cast<uint64_t>(ptr[p.rank_a] + (p.a - bases[p.rank_a])));
+        tri.push_back(reinterpret_cast<uint64_t>(ptr[p.rank_b] + (p.b - bases[p.rank_b])));
+        tri.push_back(p.len);
+    }
+    s = swap_ranges_impl<K>(tri.data(), pcs.size(), st, true);
+    if (s != PP_OK) return s;
+    std::vector<uint64_t> done;
+    const uint64_t one = 1;
+    return allgather_u64(&one, 1, done, st);  // no rank leaves before every peer's swaps finished
+}
 
 template <typename K>
 pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, uint64_t* global_split) {
@@ -226,6 +381,14 @@ pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, u
             set_error("pp_partition_dist: ranks passed different pivots or key types");
             return PP_E_INVAL;
         }
+    }
+    if (params().dist_p2p && P > 1) {  // one-sided over peer mappings, no staging
+        uint64_t Kg = 0;
+        for (int q = 0; q < P; ++q) Kg += ts[q];
+        pp_status s2 = exchange_p2p<K>(shard, n_local, ns, ts, st);
+        if (s2 != PP_OK) return s2;
+        if (global_split) *global_split = Kg;
+        return PP_OK;
     }
     // 3. the same plan on every rank
     const uint64_t cap = std::max<uint64_t>(1, g_dist.staging_cap_bytes / sizeof(K));
@@ -475,7 +638,7 @@ template pp_status quicksort_dist<uint32_t>(uint32_t*, uint64_t, cudaStream_t, u
 template <typename K>
 __global__ void __launch_bounds__(256) swap_ranges_kernel(const uint64_t* __restrict__ tri,
                                                           const uint64_t* __restrict__ pre, uint64_t np,
-                                                          uint64_t total) {
+                                                          uint64_t total, int sys_fence) {
     for (uint64_t e = (uint64_t)blockIdx.x * 256 + threadIdx.x; e < total; e += (uint64_t)gridDim.x * 256) {
         uint64_t lo = 0, hi = np;  // last piece with pre <= e
         while (hi - lo > 1) {
@@ -489,13 +652,14 @@ __global__ void __launch_bounds__(256) swap_ranges_kernel(const uint64_t* __rest
         *a = y;
         *b = x;
     }
+    if (sys_fence) __threadfence_system();  // peer writes ordered before the closing collective
 }
 
 static uint64_t* g_swap_buf = nullptr;
 static size_t g_swap_cap = 0;
 
 template <typename K>
-pp_status swap_ranges(const uint64_t* host_tri, uint64_t np, cudaStream_t st) {
+static pp_status swap_ranges_impl(const uint64_t* host_tri, uint64_t np, cudaStream_t st, bool sys_fence) {
     if (np == 0) return PP_OK;
     if (!host_tri) return PP_E_INVAL;
     std::vector<uint64_t> buf(4 * np);  // [3 np triples][np prefix]
@@ -527,7 +691,8 @@ pp_status swap_ranges(const uint64_t* host_tri, uint64_t np, cudaStream_t st) {
     cudaError_t e = cudaMemcpyAsync(g_swap_buf, buf.data(), 8 * 4 * np, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "pp_swap_ranges H2D");
     const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
-    swap_ranges_kernel<K><<<(unsigned)blocks, 256, 0, st>>>(g_swap_buf, g_swap_buf + 3 * np, np, total);
+    swap_ranges_kernel<K><<<(unsigned)blocks, 256, 0, st>>>(g_swap_buf, g_swap_buf + 3 * np, np, total,
+                                                            sys_fence ? 1 : 0);
     note_launches(1);
     // the host triples were staged by the (pageable) copy; wait before the
     // vector goes away only if the copy could still read it
@@ -535,8 +700,33 @@ pp_status swap_ranges(const uint64_t* host_tri, uint64_t np, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     return e == cudaSuccess ? PP_OK : cuda_fail(e, "pp_swap_ranges");
 }
+template <typename K>
+pp_status swap_ranges(const uint64_t* host_tri, uint64_t np, cudaStream_t st) {
+    return swap_ranges_impl<K>(host_tri, np, st, false);
+}
 template pp_status swap_ranges<uint64_t>(const uint64_t*, uint64_t, cudaStream_t);
 template pp_status swap_ranges<uint32_t>(const uint64_t*, uint64_t, cudaStream_t);
+
+pp_status dist_p2p_pieces(const uint64_t* ns, const uint64_t* ts, int P, int rank, uint64_t* out, uint64_t out_cap,
+                          uint64_t* n_out) {
+    if (!ns || !ts || P < 1 || rank < 0 || rank >= P || !n_out) return PP_E_INVAL;
+    for (int r = 0; r < P; ++r)
+        if (ts[r] > ns[r]) return PP_E_INVAL;
+    std::vector<P2PPiece> pcs;
+    p2p_pieces(ns, ts, P, rank, pcs);
+    *n_out = pcs.size();
+    if (out) {
+        for (size_t k = 0; k < pcs.size() && k < out_cap; ++k) {
+            uint64_t* o = out + 5 * k;
+            o[0] = pcs[k].rank_a;
+            o[1] = pcs[k].a;
+            o[2] = pcs[k].rank_b;
+            o[3] = pcs[k].b;
+            o[4] = pcs[k].len;
+        }
+    }
+    return pcs.size() <= out_cap || !out ? PP_OK : PP_E_INVAL;
+}
 
 pp_status dist_plan(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap, uint64_t* out, uint64_t out_cap,
                     uint64_t* n_out, uint64_t* K_out) {

@@ -55,6 +55,7 @@ struct Params {
     int64_t cleanup_bitmap = 1;    // fused tail: locate pairs from the dirty-set bitmap (0: locate + grid barrier)
     int64_t bps_nt = 256;          // Blocked-Prefix-Sum Reorder level kernel: threads per CTA (256/512/1024)
     int64_t qs_pipe = 1;           // quicksort: chunks of the per-CTA recursion pipelined with their bin sorts (measured: no gain)
+    int64_t dist_p2p = 0;          // pp_partition_dist: 1 = one-sided exchange over CUDA-IPC peer mappings (no staging)
     int64_t host_chunk = 1 << 22;  // host-buffer partition: keys per streamed chunk
     int64_t qs_heavy = 1 << 23;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
 };
@@ -111,5 +112,10 @@ template <typename K>
 pp_status quicksort_dist(K* shard, uint64_t n_local, cudaStream_t st, uint64_t small);
 template <typename K>
 pp_status swap_ranges(const uint64_t* host_tri, uint64_t np, cudaStream_t st);
+pp_status dist_p2p_pieces(const uint64_t* ns, const uint64_t* ts, int P, int rank, uint64_t* out, uint64_t out_cap,
+                          uint64_t* n_out);
+pp_status ipc_export(const void* d_ptr, void* handle_out, uint64_t* offset_out);
+pp_status ipc_import(const void* handle, uint64_t offset, void** d_ptr_out);
+pp_status ipc_close_all();
 
 }  // namespace pp

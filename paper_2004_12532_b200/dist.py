@@ -95,6 +95,23 @@ def schedule_rounds(transfers: List[Transfer], world: int, cap: int):
     return [r for r in rounds if r]
 
 
+def p2p_pieces(ns: List[int], ts: List[int], rank: int):
+    """The one-sided exchange share of `rank` (mirror of the C
+    pp_dist_p2p_pieces): every matched run of the plan is swapped in place
+    by the two ranks holding it -- the left rank (misplaced successors)
+    takes the first ceil(len/2) pairs, the right rank the rest.  Rows of
+    (rank_a, a, rank_b, b, len) in global positions."""
+    _, plan = exchange_plan(ns, ts)
+    out = []
+    for tr in plan:
+        h = (tr.length + 1) // 2
+        if tr.rank_f == rank:
+            out.append((tr.rank_f, tr.f, tr.rank_t, tr.t, h))
+        if tr.rank_t == rank and tr.length > h:
+            out.append((tr.rank_f, tr.f + h, tr.rank_t, tr.t + h, tr.length - h))
+    return out
+
+
 def my_ops(pieces: List[Transfer], rank: int, base: int):
     """The (peer, local_offset, length) swaps this rank takes part in."""
     ops = []

@@ -107,6 +107,40 @@ def test_c_plan_matches_python_plan():
         assert rows == py
 
 
+def test_p2p_shares_cover_the_plan_once():
+    """One-sided exchange: the C share rule (pp_dist_p2p_pieces) equals the
+    Python mirror for every rank, the shares of all ranks cover every pair of
+    the plan exactly once, each rank's rows involve itself, and executing all
+    shares (in any rank order) partitions the global array."""
+    import paper_2004_12532_b200 as pp
+    from paper_2004_12532_b200.dist import p2p_pieces
+    rng = np.random.default_rng(2026)
+    for trial in range(150):
+        P = int(rng.integers(1, 10))
+        ns = [int(x) for x in rng.integers(0, 200, size=P)]
+        glob = rng.integers(0, 50, size=sum(ns)).astype(np.uint64)
+        pivot = int(rng.integers(0, 51))
+        shards = np.split(glob.copy(), np.cumsum(ns)[:-1]) if P > 1 else [glob.copy()]
+        ts = []
+        for sh in shards:  # local partition (any correct one)
+            ts.append(oracle.partition_two_pointer(sh, pivot))
+        K, plan = exchange_plan(ns, ts)
+        pairs = {(tr.f + i, tr.t + i) for tr in plan for i in range(tr.length)}
+        seen = []
+        arr = np.concatenate(shards) if P > 1 else shards[0]
+        for rank in rng.permutation(P):
+            rows = pp.pp_dist_p2p_pieces(ns, ts, int(rank))
+            assert rows == p2p_pieces(ns, ts, int(rank))
+            for ra, a, rb, b, ln in rows:
+                assert rank in (ra, rb) and ra != rb and ln > 0
+                seen += [(a + i, b + i) for i in range(ln)]
+                x = arr[a:a + ln].copy()
+                arr[a:a + ln] = arr[b:b + ln]
+                arr[b:b + ln] = x
+        assert len(seen) == len(set(seen)) and set(seen) == pairs
+        oracle.check_partition(glob, arr, pivot, K)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))

@@ -87,3 +87,100 @@ def test_emulated_ranks_staging_free_exchange(pp, P, dt):
             if pieces:
                 pp.pp_swap_ranges(pieces, w)
             oracle.check_partition(a, to_host(t, dt), p, K)
+
+
+@pytest.mark.parametrize("P,dt", [(2, np.uint64), (5, np.uint32), (8, np.uint64)])
+def test_emulated_ranks_p2p_shares(pp, P, dt):
+    """The one-sided exchange as pp_partition_dist runs it with dist_p2p=1,
+    emulated on one GPU: every emulated rank executes only ITS share
+    (pp_dist_p2p_pieces: half of each matched run, addresses of its own shard
+    and of the partner's) with pp_swap_ranges, ranks one after another; the
+    union of the shares partitions the whole array."""
+    from gpu_util import to_dev, to_host
+    rng = np.random.default_rng(P * 11 + (dt == np.uint64))
+    mx = (1 << 64) - 1 if dt == np.uint64 else (1 << 32) - 1
+    w = np.dtype(dt).itemsize
+    for total in (999, 500_001, 1 << 21):
+        cuts = np.sort(rng.integers(0, total, size=P - 1))
+        ns = [int(x) for x in np.diff(np.concatenate([[0], cuts, [total]]))]
+        a = rng.integers(0, mx, size=total, dtype=dt, endpoint=True)
+        for p in (int(mx // 2), int(mx // 7), int(mx - mx // 5)):
+            t = to_dev(a)
+            ts, base = [], 0
+            for r in range(P):
+                ts.append(pp.pp_partition(t[base:base + ns[r]], p) if ns[r] else 0)
+                base += ns[r]
+            ptr = t.data_ptr()
+            for r in rng.permutation(P):
+                rows = pp.pp_dist_p2p_pieces(ns, ts, int(r))
+                if rows:
+                    pp.pp_swap_ranges([(ptr + w * ga, ptr + w * gb, ln) for (_, ga, _, gb, ln) in rows], w)
+            oracle.check_partition(a, to_host(t, dt), p, sum(ts))
+
+
+_IPC_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2004_12532_b200 as pp
+pp.load(build_if_missing=False)
+handle, off, n = bytes.fromhex(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+remote = pp.pp_ipc_import(handle, off)
+assert pp.pp_ipc_import(handle, off) == remote  # cached mapping
+mine = torch.arange(n, dtype=torch.int64, device="cuda") + 1_000_000
+# swap the parent's [n/4, n/4 + n/2) with my [0, n/2), half the range per piece
+h = n // 2
+pieces = [(remote + 8 * (n // 4), mine.data_ptr(), h // 2),
+          (remote + 8 * (n // 4 + h // 2), mine.data_ptr() + 8 * (h // 2), h - h // 2)]
+pp.pp_swap_ranges(pieces, 8)
+torch.cuda.synchronize()
+got = mine[:h].cpu().numpy()
+assert np.array_equal(got, np.arange(n // 4, n // 4 + h) * 3), got[:4]
+pp.pp_ipc_close_all()
+print("child ok")
+"""
+
+
+def test_ipc_export_import_two_processes(pp, tmp_path):
+    """CUDA IPC path of the one-sided exchange on one GPU with two processes
+    (no kernel waits on another): the parent exports a range inside a larger
+    allocation (handle + offset), a child process maps it, swaps half of it
+    with its own buffer through pp_swap_ranges, and both sides see the
+    exchanged keys."""
+    import os
+    import subprocess
+    import sys
+    n = 1 << 20
+    big = torch.zeros(n + 4096, dtype=torch.int64, device="cuda")
+    t = big[1000:1000 + n]  # an interior range: the offset matters
+    t.copy_(torch.arange(n, dtype=torch.int64, device="cuda") * 3)
+    torch.cuda.synchronize()
+    handle, off = pp.pp_ipc_export(t)
+    assert len(handle) == 64 and off >= 8000 and off % 8 == 0  # allocation base <= big's start
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "ipc_child.py"
+    script.write_text(_IPC_CHILD)
+    r = subprocess.run([sys.executable, str(script), root, handle.hex(), str(off), str(n)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "child ok" in r.stdout, r.stderr[-2000:]
+    out = t.cpu().numpy()
+    h = n // 2
+    assert np.array_equal(out[n // 4:n // 4 + h], np.arange(h) + 1_000_000)
+    assert np.array_equal(out[:n // 4], np.arange(n // 4) * 3)
+    assert np.array_equal(out[n // 4 + h:], np.arange(n // 4 + h, n) * 3)
+    assert int(big[:1000].abs().sum()) == 0 and int(big[1000 + n:].abs().sum()) == 0
+
+
+def test_partition_dist_p2p_param_single_rank(pp):
+    """dist_p2p=1 on a one-rank communicator: the local partition alone (no
+    peers to map); the parameter round-trips and resets."""
+    from gpu_util import to_dev, to_host
+    a = synth.uniform_u64_np(1 << 18, 5)
+    pp.pp_set_param("dist_p2p", 1)
+    try:
+        assert pp.pp_get_param("dist_p2p") == 1
+        t = to_dev(a)
+        K = pp.pp_partition_dist(t, 1 << 63)
+        oracle.check_partition(a, to_host(t, np.uint64), 1 << 63, K)
+    finally:
+        pp.reset_params()
+    assert pp.pp_get_param("dist_p2p") == 0
