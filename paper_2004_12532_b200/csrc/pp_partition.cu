@@ -647,6 +647,9 @@ static uint64_t choose_groups(uint64_t n_lines, int occ) {
     if (P.g > 0) return std::min<uint64_t>((uint64_t)P.g, std::max<uint64_t>(n_lines, 1));
     const uint64_t cap = (uint64_t)sm_count() * occ;
     uint64_t g = n_lines / (uint64_t)std::max<int64_t>(P.min_lines_per_group, 1);
+    // small arrays are latency-bound: at least one group per SM while every
+    // group keeps >= 2 lines (measured at 2^18-2^20 keys: 10-15% faster)
+    g = std::max<uint64_t>(g, std::min<uint64_t>((uint64_t)sm_count(), n_lines / 2));
     return std::max<uint64_t>(1, std::min(g, cap));
 }
 
@@ -795,8 +798,12 @@ pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64
         }
         // cleanup tail: fused scan+locate+barrier+swap (default) or the 3-kernel chain
         // (the fused tail needs a grid with <= FUSED_TASKS_PER_CTA tasks per CTA)
-        const bool fused_tail = P.cleanup_chain == 0 &&
-                                (uint64_t)fused_tail_grid() * FUSED_TASKS_PER_CTA >= 2 * FUSED_MAX_TILES;
+        // auto: the 3-kernel chain below 1 GiB of keys, the fused tail from
+        // 1 GiB (measured crossover between 2^26 and 2^27 u64 keys)
+        const bool want_fused =
+            P.cleanup_chain == 0 || (P.cleanup_chain < 0 && n * sizeof(K) >= (uint64_t(1) << 30));
+        const bool fused_tail =
+            want_fused && (uint64_t)fused_tail_grid() * FUSED_TASKS_PER_CTA >= 2 * FUSED_MAX_TILES;
         const uint64_t max_tiles = fused_tail ? std::min<uint64_t>(cleanup_max_tiles(n), FUSED_MAX_TILES) : 0;
         const uint32_t nflags = fused_tail ? fused_tail_grid() : 0;
         uint32_t* flags = reinterpret_cast<uint32_t*>(ws + L.flags);
