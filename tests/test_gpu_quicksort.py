@@ -59,7 +59,8 @@ def _cases(dt, mx, n, rng):
 @pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
 def test_small_sizes(pp, dt, mx):
     rng = np.random.default_rng(1)
-    for n in list(range(0, 40)) + [255, 256, 257, 4095, 4096, 4097, 8191, 8192, 8193, 20000]:
+    for n in list(range(0, 40)) + [255, 256, 257, 4095, 4096, 4097, 8191, 8192, 8193, 12289, 16383, 16384,
+                                   16385, 20000, 32769]:
         for a in _cases(dt, mx, n, rng):
             for off in (0, 1):
                 out = _sort_gpu(pp, a, off)
