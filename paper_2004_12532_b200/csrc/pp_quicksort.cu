@@ -15,6 +15,8 @@
 // split is empty (p is the segment minimum) the next level splits by x <= p
 // and the left part (all == p) is final (reading R14).
 #include <algorithm>
+#include <chrono>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1613,6 +1615,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     cudaEvent_t lev[3];
     if (lvl_prof)
         for (auto& x : lev) cudaEventCreate(&x);
+    auto t_sync = std::chrono::steady_clock::now();  // debug (PP_QS_PROF): host time between levels
     while (!cur.empty()) {
         // ---- classify ----
         mids.clear();
@@ -1661,9 +1664,14 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             const uint64_t slots = G_TARGET / (uint64_t)std::max<int64_t>(P.qs_waves, 1);
             uint64_t excess = gtot > slots ? gtot % slots : 0;
             if (excess > 0 && excess <= slots / 16) {
+                // segments by group count, descending (ties: segment order): counting sort
+                uint64_t gmax = 0;
+                for (const QSeg& q : mids) gmax = std::max<uint64_t>(gmax, q.g);
+                std::vector<uint32_t> gc(gmax + 2, 0);
+                for (const QSeg& q : mids) ++gc[gmax - q.g + 1];
+                for (uint64_t b = 0; b <= gmax; ++b) gc[b + 1] += gc[b];
                 std::vector<size_t> byg(mids.size());
-                for (size_t i = 0; i < byg.size(); ++i) byg[i] = i;
-                std::stable_sort(byg.begin(), byg.end(), [&](size_t x, size_t y) { return mids[x].g > mids[y].g; });
+                for (size_t i = 0; i < mids.size(); ++i) byg[gc[gmax - mids[i].g]++] = i;
                 for (bool any = true; excess > 0 && any;) {  // round robin, most groups first
                     any = false;
                     for (size_t k : byg) {
@@ -1676,16 +1684,29 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                     }
                 }
             }
-            gtot = 0;
-            std::vector<size_t> ord(mids.size());
-            for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
-            std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) {
-                return seg_nl[x] * mids[y].g > seg_nl[y] * mids[x].g;  // lines per group, descending
-            });
+                gtot = 0;
+            // lines per group, descending, to 1/8 of an octave (ties: segment
+            // order) -- the order only steers the LPT dispatch, so a counting
+            // sort over 8 x 64 log-scale buckets replaces a comparison sort
+            // (O(segments); the host sits on the critical path between levels)
+            constexpr int NBK = 8 * 64;
+            std::vector<uint32_t> bk(mids.size());
+            std::vector<uint32_t> cnt(NBK + 1, 0);
+            for (size_t i = 0; i < mids.size(); ++i) {
+                const uint64_t lpg = std::max<uint64_t>(1, (seg_nl[i] << 10) / mids[i].g);
+                const int oct = 63 - __builtin_clzll(lpg);
+                const int sub = oct >= 3 ? (int)((lpg >> (oct - 3)) & 7) : (int)((lpg << (3 - oct)) & 7);
+                bk[i] = (uint32_t)(NBK - 1 - (oct * 8 + sub));  // descending
+                ++cnt[bk[i] + 1];
+            }
+            for (int b = 0; b < NBK; ++b) cnt[b + 1] += cnt[b];
+            std::vector<size_t> ordi(mids.size());
+            for (size_t i = 0; i < mids.size(); ++i) ordi[cnt[bk[i]]++] = i;
             std::vector<QSeg> m2;
             std::vector<size_t> i2;
             m2.reserve(mids.size());
-            for (size_t k : ord) {
+            i2.reserve(mids.size());
+            for (size_t k : ordi) {
                 m2.push_back(mids[k]);
                 i2.push_back(mid_idx[k]);
             }
@@ -1726,6 +1747,10 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         if (nmid > 0) memcpy(pin_segs, mids.data(), sizeof(QSeg) * nmid);
         if (nh > 0) memcpy(pin_hidx, hidx.data(), 4 * nh);
 
+        if (lvl_prof)
+            fprintf(stderr, "qs host: %.1f us from the previous level's sync to this level's launches (%zu segments)\n",
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_sync).count(),
+                    cur.size());
         // ---- big segments: full multi-CTA partition, one at a time ----
         pivots_h.assign(cur.size(), 0);
         for (size_t bi = 0; bi < nbig; ++bi) {
@@ -1801,6 +1826,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         }
         e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return cuda_fail(e, "quicksort level");
+        t_sync = std::chrono::steady_clock::now();
         if (nmid + nbig > 0) memcpy(splits_h.data(), pin_splits, 8 * (nmid + nbig));
         for (size_t mi = 0; mi < nmid; ++mi) pivots_h[mid_idx[mi]] = pin_segs[mi].pivot;
         if (lvl_prof && nmid > 0) {  // debug: per-level times of the batched mid pass
