@@ -322,17 +322,33 @@ def main():
     if dist_on:
         dist.barrier()
     pp.pp_timing(True)
+    phases = []
     for i in range(args.steps):
         step(bufs[i])
+        if dist_on:
+            phases.append(pp.pp_dist_last_timing())
     torch.cuda.synchronize()
     tim = pp.pp_timing_read()
     pp.pp_timing(False)
     clocks = sampler.stop()
     del bufs
+    exchange = None
     if dist_on:
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
+        # exchange phase: NVLink GB/s = bytes a GPU moved / exchange time,
+        # max over ranks of the per-step averages (library events, second pass)
+        k = max(len(phases), 1)
+        loc = [sum(p[f] for p in phases) / k for f in ("local_ms", "gather_ms", "exchange_ms", "bytes")]
+        tt = torch.tensor(loc, dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        lm, gm, xm, xb = (float(x) for x in tt.tolist())
+        exchange = {"path": "one-sided CUDA IPC" if pp.pp_get_param("dist_p2p") else "NCCL send/recv via staging",
+                    "local_partition_ms": lm, "allgather_ms": gm, "exchange_ms": xm, "bytes_per_gpu": xb,
+                    "nvlink_gbs": (xb / (xm / 1e3) / 1e9) if xm > 0 else None,
+                    "frac_of_900_gbs": (xb / (xm / 1e3) / 1e9 / 900.0) if xm > 0 else None,
+                    "timing": "library CUDA events on the call's stream (second pass), max over ranks"}
 
     # sanity: the split equals the oracle's count on this input (cheap check)
     split = int(d_split.item()) if not dist_on else last_split[0]
@@ -370,6 +386,7 @@ def main():
                                "the same K steps (fresh copies); the K timed steps run without these events"},
         "gpu_launches": launches,
         "clocks": clocks,
+        **({"exchange": exchange} if exchange else {}),
         "split": split,
         "window_frac": (stats.get("W", 0) / n) if stats else None,
         "aux_bytes": stats.get("aux_bytes"),

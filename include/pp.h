@@ -164,6 +164,12 @@ pp_status pp_partition_dist_u64(uint64_t *shard, uint64_t n_local, uint64_t pivo
 pp_status pp_partition_dist_u32(uint32_t *shard, uint64_t n_local, uint32_t pivot, void *stream,
                                 uint64_t *global_split_out);
 pp_status pp_dist_set_staging(uint64_t bytes);
+/* pp_dist_last_timing: phases of this rank's last pp_partition_dist_* call,
+ * from CUDA events on its stream: out4[0] = local partition ms, out4[1] =
+ * (n_r, t_r) all-gather ms, out4[2] = exchange ms, out4[3] = bytes this rank
+ * moved between GPUs in the exchange (staged path: bytes sent, as many are
+ * received; one-sided path: remote bytes read + written by its swaps). */
+pp_status pp_dist_last_timing(double *out4);
 /* pp_quicksort_dist_u64/u32: sorts the GLOBAL array (shards in rank order)
  * ascending, unsigned, in place (collective).  Segments spanning ranks are
  * split by pp_partition_dist_* with a median-of-3 pivot gathered from the

@@ -115,6 +115,7 @@ def load(build_if_missing: bool = True):
         "pp_ipc_export": ([vp, vp, P64], st),
         "pp_ipc_import": ([vp, u64, ctypes.POINTER(ctypes.c_void_p)], st),
         "pp_ipc_close_all": ([], st),
+        "pp_dist_last_timing": ([ctypes.POINTER(ctypes.c_double)], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -411,6 +412,13 @@ def pp_ipc_import(handle: bytes, offset: int) -> int:
     out = ctypes.c_void_p(0)
     _check(load().pp_ipc_import(h, int(offset), ctypes.byref(out)), "pp_ipc_import")
     return int(out.value or 0)
+
+
+def pp_dist_last_timing() -> dict:
+    """Phases of this rank's last pp_partition_dist call (device events)."""
+    a = (ctypes.c_double * 4)()
+    _check(load().pp_dist_last_timing(a), "pp_dist_last_timing")
+    return {"local_ms": a[0], "gather_ms": a[1], "exchange_ms": a[2], "bytes": int(a[3])}
 
 
 def pp_ipc_close_all() -> None:

@@ -590,6 +590,10 @@ pp_status pp_ipc_import(const void* handle, uint64_t offset, void** d_ptr_out) {
     std::lock_guard<std::mutex> lk(g_mu);
     return ipc_import(handle, offset, d_ptr_out);
 }
+pp_status pp_dist_last_timing(double* out4) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return dist_last_timing(out4);
+}
 pp_status pp_ipc_close_all(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     return ipc_close_all();

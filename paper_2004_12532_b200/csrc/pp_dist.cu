@@ -231,6 +231,9 @@ static pp_status nccl_fail(ncclResult_t r, const char* what) {
 }
 
 struct DistState {
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, local done, gathered, exchanged
+    double last_local_ms = 0, last_gather_ms = 0, last_exchange_ms = 0;
+    uint64_t last_bytes = 0;  // bytes this rank moved between GPUs in the last exchange
     ncclComm_t comm = nullptr;
     int nranks = 0, rank = 0, device = 0;
     void* staging = nullptr;
@@ -275,11 +278,39 @@ pp_status dist_init(const void* id128, int nranks, int rank, int device) {
     g_dist.device = device;
     e = cudaMalloc(&g_dist.d_info, sizeof(uint64_t) * 4 * (nranks + 1));
     if (e != cudaSuccess) return cuda_fail(e, "dist info alloc");
+    for (auto& ev : g_dist.ev)
+        if (!ev) cudaEventCreate(&ev);
     return PP_OK;
+}
+
+pp_status dist_last_timing(double* out4) {
+    if (!out4) return PP_E_INVAL;
+    out4[0] = g_dist.last_local_ms;
+    out4[1] = g_dist.last_gather_ms;
+    out4[2] = g_dist.last_exchange_ms;
+    out4[3] = (double)g_dist.last_bytes;
+    return PP_OK;
+}
+
+// phase times of the call that just synchronised (events on its stream)
+static void dist_read_timing(uint64_t bytes) {
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, g_dist.ev[0], g_dist.ev[1]);
+    cudaEventElapsedTime(&b, g_dist.ev[1], g_dist.ev[2]);
+    cudaEventElapsedTime(&c, g_dist.ev[2], g_dist.ev[3]);
+    g_dist.last_local_ms = a;
+    g_dist.last_gather_ms = b;
+    g_dist.last_exchange_ms = c;
+    g_dist.last_bytes = bytes;
 }
 
 pp_status dist_finalize() {
     ipc_close_all();
+    for (auto& ev : g_dist.ev)
+        if (ev) {
+            cudaEventDestroy(ev);
+            ev = nullptr;
+        }
     if (g_dist.comm) g_nccl.CommDestroy(g_dist.comm);
     g_dist.comm = nullptr;
     if (g_dist.staging) cudaFree(g_dist.staging);
@@ -309,7 +340,7 @@ static pp_status swap_ranges_impl(const uint64_t* host_tri, uint64_t np, cudaStr
 // GPUs (NVLink / NVSwitch); untested here beyond one GPU.
 template <typename K>
 static pp_status exchange_p2p(K* shard, uint64_t n_local, const std::vector<uint64_t>& ns,
-                              const std::vector<uint64_t>& ts, cudaStream_t st) {
+                              const std::vector<uint64_t>& ts, cudaStream_t st, uint64_t* moved) {
     const int P = g_dist.nranks, me = g_dist.rank;
     std::vector<uint64_t> mine(9, 0), all;
     if (n_local > 0) {
@@ -334,7 +365,9 @@ static pp_status exchange_p2p(K* shard, uint64_t n_local, const std::vector<uint
         }
     }
     std::vector<uint64_t> tri;
+    *moved = 0;  // remote bytes read + written by this rank's swaps
     for (const P2PPiece& p : pcs) {
+        *moved += 2 * p.len * sizeof(K);
         tri.push_back(reinterpret_cast<uint64_t>(ptr[p.rank_a] + (p.a - bases[p.rank_a])));
         tri.push_back(reinterpret_cast<uint64_t>(ptr[p.rank_b] + (p.b - bases[p.rank_b])));
         tri.push_back(p.len);
@@ -353,6 +386,7 @@ pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, u
         return PP_E_INVAL;
     }
     const int P = g_dist.nranks, me = g_dist.rank;
+    cudaEventRecord(g_dist.ev[0], st);
     // 1. local partition (library kernels), split left in device memory
     uint64_t* d_mine = g_dist.d_info + 4 * P;
     pp_status s = PP_OK;
@@ -362,6 +396,7 @@ pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, u
         cudaMemsetAsync(d_mine + 1, 0, 8, st);
     }
     if (s != PP_OK) return s;
+    cudaEventRecord(g_dist.ev[1], st);
     uint64_t info[3] = {n_local, (uint64_t)pivot, (uint64_t)sizeof(K)};
     cudaError_t e = cudaMemcpyAsync(d_mine, &info[0], 8, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_mine + 2, &info[1], 16, cudaMemcpyHostToDevice, st);
@@ -369,6 +404,7 @@ pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, u
     // 2. allgather (n_r, t_r, pivot, key bytes)
     ncclResult_t r = g_nccl.AllGather(d_mine, g_dist.d_info, 4, ncclUint64, g_dist.comm, st);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+    cudaEventRecord(g_dist.ev[2], st);
     std::vector<uint64_t> all(4 * P);
     e = cudaMemcpyAsync(all.data(), g_dist.d_info, 8 * 4 * P, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -385,8 +421,12 @@ pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, u
     if (params().dist_p2p && P > 1) {  // one-sided over peer mappings, no staging
         uint64_t Kg = 0;
         for (int q = 0; q < P; ++q) Kg += ts[q];
-        pp_status s2 = exchange_p2p<K>(shard, n_local, ns, ts, st);
+        uint64_t moved = 0;
+        pp_status s2 = exchange_p2p<K>(shard, n_local, ns, ts, st, &moved);
         if (s2 != PP_OK) return s2;
+        cudaEventRecord(g_dist.ev[3], st);
+        cudaEventSynchronize(g_dist.ev[3]);
+        dist_read_timing(moved);
         if (global_split) *global_split = Kg;
         return PP_OK;
     }
@@ -458,8 +498,13 @@ pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, u
         }
         i = j;
     }
+    cudaEventRecord(g_dist.ev[3], st);
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "dist exchange");
+    uint64_t sent = 0;  // keys this rank sent (it receives as many)
+    for (const Piece& p : pcs)
+        if ((int)p.rank_f == me || (int)p.rank_t == me) sent += p.len;
+    dist_read_timing(sent * sizeof(K));
     if (global_split) *global_split = K_global;
     return PP_OK;
 }

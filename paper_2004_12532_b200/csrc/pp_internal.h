@@ -118,5 +118,6 @@ pp_status dist_p2p_pieces(const uint64_t* ns, const uint64_t* ts, int P, int ran
 pp_status ipc_export(const void* d_ptr, void* handle_out, uint64_t* offset_out);
 pp_status ipc_import(const void* handle, uint64_t offset, void** d_ptr_out);
 pp_status ipc_close_all();
+pp_status dist_last_timing(double* out4);
 
 }  // namespace pp
