@@ -239,6 +239,8 @@ struct DistState {
     void* staging = nullptr;
     size_t staging_bytes = 0;
     uint64_t* d_info = nullptr;  // [P][4] gathered (n, t, pivot, key_bytes)
+    uint64_t* d_ag = nullptr;    // all-gather scratch (grown on demand, freed at finalize)
+    size_t d_ag_words = 0;
     uint64_t staging_cap_bytes = 256ull << 20;
 };
 static DistState g_dist;
@@ -315,8 +317,11 @@ pp_status dist_finalize() {
     g_dist.comm = nullptr;
     if (g_dist.staging) cudaFree(g_dist.staging);
     if (g_dist.d_info) cudaFree(g_dist.d_info);
+    if (g_dist.d_ag) cudaFree(g_dist.d_ag);
     g_dist.staging = nullptr;
     g_dist.d_info = nullptr;
+    g_dist.d_ag = nullptr;
+    g_dist.d_ag_words = 0;
     g_dist.staging_bytes = 0;
     return PP_OK;
 }
@@ -525,23 +530,24 @@ template pp_status partition_dist<uint32_t>(uint32_t*, uint64_t, uint32_t, cudaS
 static pp_status allgather_u64(const uint64_t* host_in, uint64_t count, std::vector<uint64_t>& host_out,
                                cudaStream_t st) {
     const int P = g_dist.nranks;
-    uint64_t* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, 8 * count * (P + 1));
-    if (e != cudaSuccess) return cuda_fail(e, "allgather buffer");
+    const size_t words = count * (P + 1);
+    cudaError_t e = cudaSuccess;
+    if (words > g_dist.d_ag_words) {  // grow (the previous user synchronised its stream)
+        if (g_dist.d_ag) cudaFree(g_dist.d_ag);
+        g_dist.d_ag = nullptr;
+        g_dist.d_ag_words = 0;
+        e = cudaMalloc(&g_dist.d_ag, 8 * words);
+        if (e != cudaSuccess) return cuda_fail(e, "allgather buffer");
+        g_dist.d_ag_words = words;
+    }
+    uint64_t* d = g_dist.d_ag;
     e = cudaMemcpyAsync(d + count * P, host_in, 8 * count, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) {
-        cudaFree(d);
-        return cuda_fail(e, "allgather H2D");
-    }
+    if (e != cudaSuccess) return cuda_fail(e, "allgather H2D");
     ncclResult_t r = g_nccl.AllGather(d + count * P, d, count, ncclUint64, g_dist.comm, st);
-    if (r != ncclSuccess) {
-        cudaFree(d);
-        return nccl_fail(r, "ncclAllGather");
-    }
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
     host_out.assign(count * P, 0);
     e = cudaMemcpyAsync(host_out.data(), d, 8 * count * P, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    cudaFree(d);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // also: the buffer is free for the next call
     return e == cudaSuccess ? PP_OK : cuda_fail(e, "allgather D2H");
 }
 
