@@ -132,7 +132,7 @@ def test_config5_full(pp, kind):
 
 
 @pytest.mark.parametrize("leaf_algo,leaf", [(0, 0), (2, 0), (3, 0), (4, 0), (5, 0), (5, 4096), (6, 0), (6, 1000),
-                                            (6, 8192), (6, 12000)])
+                                            (6, 8192), (6, 12000), (6, 10240)])
 def test_bin_sorts_clustered(pp, leaf_algo, leaf):
     """Bins whose keys cluster inside a wide range: the packed 32-bit bin sort
     (leaf_algo 4) sees runs of equal top bits -- short runs are
