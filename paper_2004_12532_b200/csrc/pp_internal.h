@@ -50,7 +50,7 @@ struct Params {
     int64_t fused_stop = 0;        // debug/profiling: stop the fused kernel after this phase
     int64_t qs_waves = 2;          // quicksort mid levels: target CTA waves of the group launch
     int64_t qs_small = 1 << 16;    // quicksort: segments <= this finish in one CTA (0 = off)
-    int64_t qs_small_cfg = 2;      // quicksort: per-CTA recursion config (pp_quicksort.cu SmallCfg)
+    int64_t qs_small_cfg = 3;      // quicksort: per-CTA recursion config (pp_quicksort.cu SmallCfg; 3 = 4 lines in flight)
     int64_t cleanup_chain = -1;    // partition cleanup tail: 0 fused scan+swap, 1 scan / locate / swap kernels,
                                    // -1 auto (chain below 1 GiB of keys, fused from 1 GiB: measured crossover)
     int64_t cleanup_bitmap = 1;    // fused tail: locate pairs from the dirty-set bitmap (0: locate + grid barrier)

@@ -1017,6 +1017,14 @@ struct SmallCfg<K, 2> {  // V = 1 with the refills issued by one lane per line (
     static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
 };
 template <typename K>
+struct SmallCfg<K, 3> {  // V = 2 with 4 lines in flight per end
+    static constexpr int NT = 128, MINB = 4;
+    using GC = GroupCfgT<K, 4096, 128, 4, false, false, true>;
+    static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 2048 : 4096;
+    static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);
+    static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
+};
+template <typename K>
 struct SmallCfg<K, 1> {
     static constexpr int NT = 128, MINB = 4;
     using GC = GroupCfgT<K, 4096, 128, 2, false>;
@@ -1994,6 +2002,11 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                 using S = SmallCfg<K, 2>;
                 cudaFuncSetAttribute(qs_small_kernel<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
                 qs_small_kernel<K, 2><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(
+                    keys, d_slo, d_sln, d_sbase, d_blo, d_bln, (uint32_t)LEAF, P.seed, d_scr, d_prof);
+            } else if (P.qs_small_cfg == 3) {
+                using S = SmallCfg<K, 3>;
+                cudaFuncSetAttribute(qs_small_kernel<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+                qs_small_kernel<K, 3><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(
                     keys, d_slo, d_sln, d_sbase, d_blo, d_bln, (uint32_t)LEAF, P.seed, d_scr, d_prof);
             } else if (P.qs_small_cfg == 0) {
                 using S = SmallCfg<K, 0>;

@@ -80,7 +80,7 @@ def test_medium_sizes(pp, dt, mx):
 @pytest.mark.parametrize("params", [{"leaf_algo": 1}, {"leaf_algo": 3}, {"leaf_algo": 3, "leaf": 300},
                                     {"leaf_algo": 2, "leaf": 300}, {"qs_waves": 1}, {"qs_waves": 16, "leaf": 1000},
                                     {"qs_heavy": 1 << 17}, {"qs_heavy": 0}, {"qs_small": 0}, {"strided": 1},
-                                    {"qs_pipe": 1}, {"qs_pipe": 16}, {"qs_small_cfg": 0}, {"qs_small_cfg": 1},
+                                    {"qs_pipe": 1}, {"qs_pipe": 16}, {"qs_small_cfg": 0}, {"qs_small_cfg": 1}, {"qs_small_cfg": 2},
                                     {"leaf_algo": 5}, {"leaf_algo": 5, "leaf": 4096}, {"leaf_algo": 5, "leaf": 300},
                                     {"leaf_algo": 6}, {"leaf_algo": 6, "leaf": 300}])
 def test_qs_parameters(pp, dt, mx, params):
