@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(GroupCfg<K>::NT) qs_group_kernel(K* __restrict
                                                                    uint64_t seed, GroupOut* __restrict__ gout) {
     extern __shared__ __align__(128) unsigned char smem[];
     using C = GroupCfg<K>;
+    griddep_wait();  // PDL launch: the pivots come from qs_pivot_kernel
     const uint64_t task = blockIdx.x;
     // segment of this task: last s with gbase <= task
     uint64_t lo = 0, hi = nseg;
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(NT) qs_cleanup_kernel(K* __restrict__ keys, co
                                                          uint64_t* __restrict__ splits, uint64_t heavy) {
     using C = GroupCfg<K>;
     extern __shared__ __align__(16) unsigned char csm[];
+    griddep_wait();  // PDL launch: gout comes from qs_group_kernel
     if (heavy && segs[blockIdx.x].hi - segs[blockIdx.x].lo >= heavy) return;  // batched multi-CTA cleanup
     StreamBuf<NT, EPT>& sb = *reinterpret_cast<StreamBuf<NT, EPT>*>(csm);
     __shared__ uint64_t red[4][NT / 32];
@@ -1465,6 +1467,25 @@ struct LeafCfg {
     static constexpr int NT = LEAF / LEAF_E;
 };
 
+// Launch with programmatic stream serialization: the launch overlaps the
+// previous kernel's tail; the kernel calls griddep_wait() before reading
+// what its predecessor wrote (the shared cleanup bodies do so themselves).
+template <typename... KArgs, typename... Args>
+static cudaError_t qs_launch_pdl(void (*kern)(KArgs...), dim3 grid, unsigned block, size_t smem, cudaStream_t st,
+                                 Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // quicksort workspace (separate from the partition workspace)
 static void* g_qws = nullptr;
 static size_t g_qws_bytes = 0;
@@ -1785,22 +1806,33 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         }
         // ---- mid segments: one batched pass ----
         if (nmid > 0) {
+            // host lists up first, then the level's kernels back to back (PDL-chained;
+            // with the profiling events in between they run plainly serialized)
             e = cudaMemcpyAsync(d_segs, pin_segs, sizeof(QSeg) * nmid, cudaMemcpyHostToDevice, st);
+            if (e == cudaSuccess && nh > 0) e = cudaMemcpyAsync(d_hidx, pin_hidx, 4 * nh, cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort H2D");
             qs_pivot_kernel<K><<<(unsigned)((nmid + 255) / 256), 256, 0, st>>>(keys, d_segs, nmid);
             if (lvl_prof) cudaEventRecord(lev[0], st);
-            qs_group_kernel<K><<<(unsigned)gtot, C::NT, C::SMEM, st>>>(keys, d_segs, nmid, P.seed, d_gout);
+            e = qs_launch_pdl(qs_group_kernel<K>, dim3((unsigned)gtot), C::NT, C::SMEM, st, keys, d_segs, nmid,
+                              P.seed, d_gout);
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort group launch");
             if (lvl_prof) cudaEventRecord(lev[1], st);
             if (nh > 0) {
-                e = cudaMemcpyAsync(d_hidx, pin_hidx, 4 * nh, cudaMemcpyHostToDevice, st);
-                if (e != cudaSuccess) return cuda_fail(e, "quicksort H2D");
                 const unsigned X = (unsigned)std::min<uint64_t>(
                     2 * QS_HEAVY_TILES, std::max<uint64_t>(2, ((uint64_t)sm_count() * 4 + nh - 1) / nh));
                 const dim3 grid(X, (unsigned)nh);
-                qs_hv_reduce_kernel<K><<<grid, 256, 0, st>>>(keys, d_segs, d_hidx, d_gout, d_splits, d_hv, HVL);
-                qs_hv_scan_kernel<<<(unsigned)nh, 1024, 2 * 8 * (QS_HEAVY_TILES + 1), st>>>(d_hv, HVL);
-                qs_hv_locate_kernel<K><<<grid, SW_NT, 0, st>>>(keys, d_segs, d_hidx, d_hv, HVL);
-                qs_hv_swap_kernel<K><<<grid, SW_NT, 0, st>>>(keys, d_segs, d_hidx, d_hv, HVL);
+                e = qs_launch_pdl(qs_hv_reduce_kernel<K>, grid, 256, 0, st, keys, (const QSeg*)d_segs,
+                                  (const uint32_t*)d_hidx, (const GroupOut*)d_gout, d_splits, d_hv, HVL);
+                if (e == cudaSuccess)
+                    e = qs_launch_pdl(qs_hv_scan_kernel, dim3((unsigned)nh), 1024, 2 * 8 * (QS_HEAVY_TILES + 1), st,
+                                      d_hv, HVL);
+                if (e == cudaSuccess)
+                    e = qs_launch_pdl(qs_hv_locate_kernel<K>, grid, SW_NT, 0, st, keys, (const QSeg*)d_segs,
+                                      (const uint32_t*)d_hidx, d_hv, HVL);
+                if (e == cudaSuccess)
+                    e = qs_launch_pdl(qs_hv_swap_kernel<K>, grid, SW_NT, 0, st, keys, (const QSeg*)d_segs,
+                                      (const uint32_t*)d_hidx, d_hv, HVL);
+                if (e != cudaSuccess) return cuda_fail(e, "quicksort heavy cleanup launch");
                 note_launches(4);
             }
             if (nh == nmid) {
@@ -1811,12 +1843,14 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                 const size_t sm = sizeof(StreamBuf<NT, EPT>);
                 cudaFuncSetAttribute(qs_cleanup_kernel<K, NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sm);
-                qs_cleanup_kernel<K, NT, EPT><<<(unsigned)nmid, NT, sm, st>>>(keys, d_segs, d_gout, d_splits, HEAVY);
+                e = qs_launch_pdl(qs_cleanup_kernel<K, NT, EPT>, dim3((unsigned)nmid), NT, sm, st, keys,
+                                  (const QSeg*)d_segs, (const GroupOut*)d_gout, d_splits, HEAVY);
             } else {
                 const size_t sm = sizeof(StreamBuf<SW_NT, SW_EPT2>);
-                qs_cleanup_kernel<K, SW_NT, SW_EPT2><<<(unsigned)nmid, SW_NT, sm, st>>>(keys, d_segs, d_gout,
-                                                                                         d_splits, HEAVY);
+                e = qs_launch_pdl(qs_cleanup_kernel<K, SW_NT, SW_EPT2>, dim3((unsigned)nmid), SW_NT, sm, st, keys,
+                                  (const QSeg*)d_segs, (const GroupOut*)d_gout, d_splits, HEAVY);
             }
+            if (e != cudaSuccess) return cuda_fail(e, "quicksort cleanup launch");
             if (lvl_prof) cudaEventRecord(lev[2], st);
             note_launches(3);
             e = cudaGetLastError();
