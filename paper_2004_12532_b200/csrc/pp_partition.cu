@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(C::NT) ss_group_kernel(typename C::Key* __rest
                                                          uint32_t g, uint64_t seed, typename C::Key pivot,
                                                          GroupOut* __restrict__ out) {
     extern __shared__ __align__(128) unsigned char smem[];
+    griddep_wait();  // PDL launch: the previous kernel on the stream may still be finishing
     ss_group_engine<C>(region, n_lines, g, blockIdx.x, seed, pivot, out + blockIdx.x, smem);
 }
 
@@ -546,8 +547,10 @@ static void launch_group_t(K* region, uint64_t n_lines, uint32_t g, uint64_t see
                            cudaStream_t st) {
     using C = typename VariantCfg<K, V>::type;
     occupancy_of<C>();
-    ss_group_kernel<C><<<g, C::NT, C::SMEM, st>>>(region, n_lines, g, seed, pivot, out);
-    note_launches(1);
+    // programmatic dependent launch: launch and CTA setup overlap the tail of
+    // the previous kernel on the stream (e.g. the previous call's cleanup);
+    // the kernel waits for it before touching memory
+    launch_pdl_smem(ss_group_kernel<C>, g, C::NT, C::SMEM, st, region, n_lines, g, seed, pivot, out);
 }
 template <typename K>
 static void launch_group(int v, K* region, uint64_t n_lines, uint32_t g, uint64_t seed, K pivot, GroupOut* out,
