@@ -1638,6 +1638,12 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     std::vector<QSeg> mids;
     std::vector<uint64_t> splits_h, pivots_h;
     std::vector<size_t> order;  // cur index -> splits index
+    // per-level scratch, hoisted so its capacity survives the levels (the
+    // host work between levels sits on the critical path)
+    std::vector<size_t> big_idx, mid_idx, ordi, i2;
+    std::vector<uint64_t> seg_nl;
+    std::vector<uint32_t> bk, cnt, hidx;
+    std::vector<QSeg> m2;
     cudaError_t e;
     cudaFuncSetAttribute(qs_group_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     static const bool lvl_prof = getenv("PP_QS_PROF") != nullptr;
@@ -1648,7 +1654,8 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     while (!cur.empty()) {
         // ---- classify ----
         mids.clear();
-        std::vector<size_t> big_idx, mid_idx;
+        big_idx.clear();
+        mid_idx.clear();
         uint64_t gtot = 0;
         // mid segments share one launch.  Every CTA should carry about the
         // same number of lines: L* = (lines of all mid segments) / G_TARGET,
@@ -1656,7 +1663,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         // the tasks are then ordered by lines per group, longest first, so the
         // in-order CTA dispatch approximates longest-processing-time-first
         // scheduling over the SMs' slots (balanced waves, no straggler wave).
-        std::vector<uint64_t> seg_nl;
+        seg_nl.clear();
         uint64_t mid_lines = 0;
         for (size_t i = 0; i < cur.size(); ++i) {
             const uint64_t len = cur[i].hi - cur[i].lo;
@@ -1719,8 +1726,8 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             // sort over 8 x 64 log-scale buckets replaces a comparison sort
             // (O(segments); the host sits on the critical path between levels)
             constexpr int NBK = 8 * 64;
-            std::vector<uint32_t> bk(mids.size());
-            std::vector<uint32_t> cnt(NBK + 1, 0);
+            bk.resize(mids.size());
+            cnt.assign(NBK + 1, 0);
             for (size_t i = 0; i < mids.size(); ++i) {
                 const uint64_t lpg = std::max<uint64_t>(1, (seg_nl[i] << 10) / mids[i].g);
                 const int oct = 63 - __builtin_clzll(lpg);
@@ -1729,10 +1736,10 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                 ++cnt[bk[i] + 1];
             }
             for (int b = 0; b < NBK; ++b) cnt[b + 1] += cnt[b];
-            std::vector<size_t> ordi(mids.size());
+            ordi.resize(mids.size());
             for (size_t i = 0; i < mids.size(); ++i) ordi[cnt[bk[i]]++] = i;
-            std::vector<QSeg> m2;
-            std::vector<size_t> i2;
+            m2.clear();
+            i2.clear();
             m2.reserve(mids.size());
             i2.reserve(mids.size());
             for (size_t k : ordi) {
@@ -1748,7 +1755,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         }
         const uint64_t nmid = mids.size(), nbig = big_idx.size();
         // heavy mid segments: batched multi-CTA cleanup
-        std::vector<uint32_t> hidx;
+        hidx.clear();
         for (size_t mi = 0; mi < mids.size(); ++mi)
             if (HEAVY && mids[mi].hi - mids[mi].lo >= HEAVY) hidx.push_back((uint32_t)mi);
         const uint64_t nh = hidx.size();
