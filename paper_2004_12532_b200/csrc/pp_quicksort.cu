@@ -1577,13 +1577,18 @@ static QsGeom qs_geom() {
 // <= its proportional share of G_TARGET groups + 1 (rounding, the max(1,.)
 // floor), big ones number <= n/BIG + 1.  The final lists are chunked.
 template <typename K>
-uint64_t quicksort_workspace_bound(uint64_t n) {
+static size_t qs_level_bound(uint64_t n) {  // one level's region (any level, any lane)
     const QsGeom q = qs_geom<K>();
     const uint64_t nmid = n / (q.SMALL + 1) + 1, nbig = n / q.BIG + 1;
     const uint64_t gtot = q.G_TARGET + 2 * nmid + 1;
     const uint64_t nh = q.HEAVY ? n / q.HEAVY + 1 : 0;
-    const size_t level = al256(sizeof(QSeg) * nmid) + al256(sizeof(GroupOut) * gtot) + al256(8 * (nmid + nbig + 1)) +
-                         al256(4 * (nh + 1)) + hv_layout().stride * nh;
+    return al256(al256(sizeof(QSeg) * nmid) + al256(sizeof(GroupOut) * gtot) + al256(8 * (nmid + nbig + 1)) +
+                 al256(4 * (nh + 1)) + hv_layout().stride * nh);
+}
+template <typename K>
+uint64_t quicksort_workspace_bound(uint64_t n) {
+    const QsGeom q = qs_geom<K>();
+    const size_t level = qs_level_bound<K>(n);
     const uint64_t cl = std::min<uint64_t>(n / 2 + 1, QS_LIST_CHUNK);
     const uint64_t cs = std::min<uint64_t>(n / (q.LEAF + 1) + 1, QS_LIST_CHUNK);
     // bin slots of one chunk of small segments: sum of qs_bin_cap <= 2 n / LEAF + 6 per segment
@@ -1591,7 +1596,7 @@ uint64_t quicksort_workspace_bound(uint64_t n) {
     const uint64_t nslot = 2 * (n / q.LEAF) + 6 * (n / (q.LEAF + 1) + 1) + 6;
     const size_t lists = al256(8 * cl) + al256(4 * cl) + al256(8 * cs) + al256(4 * cs) + al256(8 * cs) +
                          al256(sizeof(GroupOut) * cs) + al256(8 * nslot) + al256(4 * nslot) + 256;
-    return std::max(level, lists);
+    return std::max(2 * level, lists);  // two level lanes (quicksort_device) or the final lists
 }
 template uint64_t quicksort_workspace_bound<uint64_t>(uint64_t);
 template uint64_t quicksort_workspace_bound<uint32_t>(uint64_t);
@@ -1613,12 +1618,11 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         uint64_t lo, hi, pivot;
         uint32_t mode;
     };
-    std::vector<HSeg> cur{{0, n, 0, 0}}, next;
     std::vector<uint64_t> leaf_lo, small_lo;
     std::vector<uint32_t> leaf_len, small_len;
     // segments in (LEAF, SMALL] finish in one CTA each (qs_small_kernel)
     const uint64_t SMALL = geom.SMALL;
-    auto add_child = [&](uint64_t lo, uint64_t hi) {
+    auto add_child = [&](std::vector<HSeg>& next, uint64_t lo, uint64_t hi) {
         const uint64_t len = hi - lo;
         if (len <= 1) return;
         if (len <= LEAF) {
@@ -1631,67 +1635,106 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             next.push_back({lo, hi, 0, 0});
         }
     };
-    if (n <= SMALL) {
-        cur.clear();
-        add_child(0, n);
+    // The level loop runs in up to two LANES: while some segment takes the
+    // big-segment path (or fewer than two segments exist) one lane runs on
+    // the caller's stream; then the segment list is split in two array-disjoint
+    // halves, each recursing independently on its own stream with its own
+    // workspace and pinned regions.  While the host waits on one lane's
+    // level and builds its next list, the other lane's kernels keep the GPU
+    // busy, and each lane's kernel tails overlap the other's work.
+    struct Lane {
+        std::vector<HSeg> cur, next;
+        std::vector<QSeg> mids, m2;
+        std::vector<uint64_t> splits_h, pivots_h, seg_nl;
+        std::vector<size_t> big_idx, mid_idx, ordi, i2;
+        std::vector<uint32_t> bk, cnt, hidx;
+        cudaStream_t st = nullptr;
+        cudaEvent_t done = nullptr;
+        cudaEvent_t lev[3] = {nullptr, nullptr, nullptr};
+        unsigned char* pin = nullptr;
+        uint64_t nmid = 0, nbig = 0, gtot = 0;
+        bool inflight = false;
+        int id = 0;
+    };
+    static cudaStream_t lane_st1 = nullptr;
+    static cudaEvent_t lane_ev[3] = {nullptr, nullptr, nullptr};
+    if (!lane_st1) {
+        cudaStreamCreateWithFlags(&lane_st1, cudaStreamNonBlocking);
+        for (auto& x : lane_ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
     }
-    std::vector<QSeg> mids;
-    std::vector<uint64_t> splits_h, pivots_h;
-    std::vector<size_t> order;  // cur index -> splits index
-    // per-level scratch, hoisted so its capacity survives the levels (the
-    // host work between levels sits on the critical path)
-    std::vector<size_t> big_idx, mid_idx, ordi, i2;
-    std::vector<uint64_t> seg_nl;
-    std::vector<uint32_t> bk, cnt, hidx;
-    std::vector<QSeg> m2;
+    Lane lanes[2];
+    lanes[0].st = st;
+    lanes[0].done = lane_ev[0];
+    lanes[1].st = lane_st1;
+    lanes[1].done = lane_ev[1];
+    lanes[1].id = 1;
+    lanes[0].cur.push_back({0, n, 0, 0});
+    if (n <= SMALL) {
+        lanes[0].cur.clear();
+        add_child(lanes[0].cur, 0, n);
+    }
     cudaError_t e;
     cudaFuncSetAttribute(qs_group_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     static const bool lvl_prof = getenv("PP_QS_PROF") != nullptr;
-    cudaEvent_t lev[3];
     if (lvl_prof)
-        for (auto& x : lev) cudaEventCreate(&x);
-    auto t_sync = std::chrono::steady_clock::now();  // debug (PP_QS_PROF): host time between levels
-    while (!cur.empty()) {
-        // ---- classify ----
-        mids.clear();
-        big_idx.clear();
-        mid_idx.clear();
-        uint64_t gtot = 0;
+        for (Lane& L : lanes)
+            for (auto& x : L.lev) cudaEventCreate(&x);
+    // pinned staging per lane, sized once from the level bound (a lane's
+    // readback may be in flight while the other lane builds its level)
+    const uint64_t nmid_max = n / (SMALL + 1) + 1, nbig_max = n / BIG + 1;
+    const uint64_t nh_max = HEAVY ? n / HEAVY + 1 : 1;
+    const size_t pin_sB = al256(sizeof(QSeg) * nmid_max), pin_spB = al256(8 * (nmid_max + nbig_max + 1));
+    const size_t pin_lane = pin_sB + pin_spB + al256(4 * nh_max);
+    unsigned char* pin_all = qs_pinned(2 * pin_lane);
+    if (!pin_all) return PP_E_NOMEM;
+    lanes[0].pin = pin_all;
+    lanes[1].pin = pin_all + pin_lane;
+    size_t lane_half = 0;  // bytes of each lane's device region (monotone within a sort)
+
+    // classify a lane's segments, upload its level, launch its kernels and
+    // the readback; records L.done (L.inflight = false if nothing to do)
+    auto launch_level = [&](Lane& L) -> pp_status {
+        L.inflight = false;
+        if (L.cur.empty()) return PP_OK;
+        L.mids.clear();
+        L.big_idx.clear();
+        L.mid_idx.clear();
+        L.seg_nl.clear();
+        uint64_t gtot = 0, mid_lines = 0;
         // mid segments share one launch.  Every CTA should carry about the
         // same number of lines: L* = (lines of all mid segments) / G_TARGET,
         // a segment gets round(lines / L*) groups (>= 1, <= lines / MINL);
         // the tasks are then ordered by lines per group, longest first, so the
         // in-order CTA dispatch approximates longest-processing-time-first
         // scheduling over the SMs' slots (balanced waves, no straggler wave).
-        seg_nl.clear();
-        uint64_t mid_lines = 0;
-        for (size_t i = 0; i < cur.size(); ++i) {
-            const uint64_t len = cur[i].hi - cur[i].lo;
+        for (size_t i = 0; i < L.cur.size(); ++i) {
+            const uint64_t len = L.cur[i].hi - L.cur[i].lo;
             if (len >= BIG) {
-                big_idx.push_back(i);
+                L.big_idx.push_back(i);
                 continue;
             }
-            mid_idx.push_back(i);
+            L.mid_idx.push_back(i);
             QSeg q;
-            q.lo = cur[i].lo;
-            q.hi = cur[i].hi;
-            q.pivot = cur[i].pivot;
-            q.mode = cur[i].mode;
+            q.lo = L.cur[i].lo;
+            q.hi = L.cur[i].hi;
+            q.pivot = L.cur[i].pivot;
+            q.mode = L.cur[i].mode;
             q.pad = 0;
             // lines of the aligned region (host mirror of seg_head)
             const uint64_t addr = (uint64_t)(uintptr_t)(keys + q.lo);
             uint64_t h = ((16 - (addr & 15)) & 15) / sizeof(K);
             if (h > len) h = len;
             const uint64_t nl = (len - h) / C::LK;
-            seg_nl.push_back(nl);
+            L.seg_nl.push_back(nl);
             mid_lines += nl;
-            mids.push_back(q);
+            L.mids.push_back(q);
         }
+        std::vector<QSeg>& mids = L.mids;
         {
             const double Lstar = std::max(1.0, (double)mid_lines / (double)G_TARGET);
             for (size_t i = 0; i < mids.size(); ++i) {
-                const uint64_t cap = std::max<uint64_t>(1, seg_nl[i] / MINL);
-                const uint64_t want = (uint64_t)((double)seg_nl[i] / Lstar + 0.5);
+                const uint64_t cap = std::max<uint64_t>(1, L.seg_nl[i] / MINL);
+                const uint64_t want = (uint64_t)((double)L.seg_nl[i] / Lstar + 0.5);
                 mids[i].g = std::max<uint64_t>(1, std::min<uint64_t>(cap, want));
                 gtot += mids[i].g;
             }
@@ -1720,124 +1763,131 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                     }
                 }
             }
-                gtot = 0;
+            gtot = 0;
             // lines per group, descending, to 1/8 of an octave (ties: segment
             // order) -- the order only steers the LPT dispatch, so a counting
             // sort over 8 x 64 log-scale buckets replaces a comparison sort
             // (O(segments); the host sits on the critical path between levels)
             constexpr int NBK = 8 * 64;
-            bk.resize(mids.size());
-            cnt.assign(NBK + 1, 0);
+            L.bk.resize(mids.size());
+            L.cnt.assign(NBK + 1, 0);
             for (size_t i = 0; i < mids.size(); ++i) {
-                const uint64_t lpg = std::max<uint64_t>(1, (seg_nl[i] << 10) / mids[i].g);
+                const uint64_t lpg = std::max<uint64_t>(1, (L.seg_nl[i] << 10) / mids[i].g);
                 const int oct = 63 - __builtin_clzll(lpg);
                 const int sub = oct >= 3 ? (int)((lpg >> (oct - 3)) & 7) : (int)((lpg << (3 - oct)) & 7);
-                bk[i] = (uint32_t)(NBK - 1 - (oct * 8 + sub));  // descending
-                ++cnt[bk[i] + 1];
+                L.bk[i] = (uint32_t)(NBK - 1 - (oct * 8 + sub));  // descending
+                ++L.cnt[L.bk[i] + 1];
             }
-            for (int b = 0; b < NBK; ++b) cnt[b + 1] += cnt[b];
-            ordi.resize(mids.size());
-            for (size_t i = 0; i < mids.size(); ++i) ordi[cnt[bk[i]]++] = i;
-            m2.clear();
-            i2.clear();
-            m2.reserve(mids.size());
-            i2.reserve(mids.size());
-            for (size_t k : ordi) {
-                m2.push_back(mids[k]);
-                i2.push_back(mid_idx[k]);
+            for (int b = 0; b < NBK; ++b) L.cnt[b + 1] += L.cnt[b];
+            L.ordi.resize(mids.size());
+            for (size_t i = 0; i < mids.size(); ++i) L.ordi[L.cnt[L.bk[i]]++] = i;
+            L.m2.clear();
+            L.i2.clear();
+            for (size_t k : L.ordi) {
+                L.m2.push_back(mids[k]);
+                L.i2.push_back(L.mid_idx[k]);
             }
-            mids.swap(m2);
-            mid_idx.swap(i2);
+            mids.swap(L.m2);
+            L.mid_idx.swap(L.i2);
             for (QSeg& q : mids) {
                 q.gbase = gtot;
                 gtot += q.g;
             }
         }
-        const uint64_t nmid = mids.size(), nbig = big_idx.size();
+        const uint64_t nmid = mids.size(), nbig = L.big_idx.size();
+        L.nmid = nmid;
+        L.nbig = nbig;
+        L.gtot = gtot;
         // heavy mid segments: batched multi-CTA cleanup
-        hidx.clear();
+        L.hidx.clear();
         for (size_t mi = 0; mi < mids.size(); ++mi)
-            if (HEAVY && mids[mi].hi - mids[mi].lo >= HEAVY) hidx.push_back((uint32_t)mi);
-        const uint64_t nh = hidx.size();
-        // ---- workspace: [segs][gout][splits][heavy index][heavy blocks] ----
+            if (HEAVY && mids[mi].hi - mids[mi].lo >= HEAVY) L.hidx.push_back((uint32_t)mi);
+        const uint64_t nh = L.hidx.size();
+        // ---- workspace: this lane's region [segs][gout][splits][heavy index][heavy blocks] ----
         const size_t segB = al256(sizeof(QSeg) * std::max<uint64_t>(nmid, 1));
         const size_t goB = al256(sizeof(GroupOut) * std::max<uint64_t>(gtot, 1));
         const size_t spB = al256(8 * (nmid + nbig + 1));
         const size_t hiB = al256(4 * std::max<uint64_t>(nh, 1));
         const size_t hvB = HVL.stride * nh;
-        unsigned char* ws = static_cast<unsigned char*>(qs_workspace(segB + goB + spB + hiB + hvB));
-        if (!ws) return PP_E_NOMEM;
+        const size_t need = al256(segB + goB + spB + hiB + hvB);
+        if (need > lane_half) {
+            // a new layout [lane 0 | lane 1] would overlap the other lane's
+            // in-flight region: drain that lane first (a few times per sort,
+            // while the levels grow); reallocation itself synchronises too
+            Lane& O = lanes[1 - L.id];
+            if (O.inflight) {
+                e = cudaStreamSynchronize(O.st);
+                if (e != cudaSuccess) return cuda_fail(e, "quicksort lane drain");
+            }
+            lane_half = std::max(need, std::min<size_t>(al256(need + need / 4), qs_level_bound<K>(n)));
+        }
+        unsigned char* wsb = static_cast<unsigned char*>(qs_workspace(2 * lane_half));
+        if (!wsb) return PP_E_NOMEM;
+        unsigned char* ws = wsb + (size_t)L.id * lane_half;
         QSeg* d_segs = reinterpret_cast<QSeg*>(ws);
         GroupOut* d_gout = reinterpret_cast<GroupOut*>(ws + segB);
         uint64_t* d_splits = reinterpret_cast<uint64_t*>(ws + segB + goB);
         uint32_t* d_hidx = reinterpret_cast<uint32_t*>(ws + segB + goB + spB);
         unsigned char* d_hv = ws + segB + goB + spB + hiB;
         // pinned staging: [segs][splits][heavy index]
-        const size_t pin_sB = al256(sizeof(QSeg) * std::max<uint64_t>(nmid, 1));
-        const size_t pin_spB = al256(8 * (nmid + nbig + 1));
-        unsigned char* pin = qs_pinned(pin_sB + pin_spB + al256(4 * std::max<uint64_t>(nh, 1)));
-        if (!pin) return PP_E_NOMEM;
-        QSeg* pin_segs = reinterpret_cast<QSeg*>(pin);
-        uint64_t* pin_splits = reinterpret_cast<uint64_t*>(pin + pin_sB);
-        uint32_t* pin_hidx = reinterpret_cast<uint32_t*>(pin + pin_sB + pin_spB);
+        QSeg* pin_segs = reinterpret_cast<QSeg*>(L.pin);
+        uint64_t* pin_splits = reinterpret_cast<uint64_t*>(L.pin + pin_sB);
+        uint32_t* pin_hidx = reinterpret_cast<uint32_t*>(L.pin + pin_sB + pin_spB);
         if (nmid > 0) memcpy(pin_segs, mids.data(), sizeof(QSeg) * nmid);
-        if (nh > 0) memcpy(pin_hidx, hidx.data(), 4 * nh);
-
-        if (lvl_prof)
-            fprintf(stderr, "qs host: %.1f us from the previous level's sync to this level's launches (%zu segments)\n",
-                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_sync).count(),
-                    cur.size());
-        // ---- big segments: full multi-CTA partition, one at a time ----
-        pivots_h.assign(cur.size(), 0);
+        if (nh > 0) memcpy(pin_hidx, L.hidx.data(), 4 * nh);
+        cudaStream_t lst = L.st;
+        // ---- big segments: full multi-CTA partition, one at a time (lane 0 only) ----
+        L.pivots_h.assign(L.cur.size(), 0);
         for (size_t bi = 0; bi < nbig; ++bi) {
-            HSeg& s = cur[big_idx[bi]];
-            uint64_t p = s.pivot;
-            if (s.mode == 0) {
+            HSeg& sg = L.cur[L.big_idx[bi]];
+            uint64_t p = sg.pivot;
+            if (sg.mode == 0) {
                 K three[3];
-                const uint64_t len = s.hi - s.lo;
-                e = cudaMemcpyAsync(&three[0], keys + s.lo, sizeof(K), cudaMemcpyDeviceToHost, st);
+                const uint64_t len = sg.hi - sg.lo;
+                e = cudaMemcpyAsync(&three[0], keys + sg.lo, sizeof(K), cudaMemcpyDeviceToHost, lst);
                 if (e == cudaSuccess)
-                    e = cudaMemcpyAsync(&three[1], keys + s.lo + (len - 1) / 2, sizeof(K), cudaMemcpyDeviceToHost, st);
+                    e = cudaMemcpyAsync(&three[1], keys + sg.lo + (len - 1) / 2, sizeof(K), cudaMemcpyDeviceToHost,
+                                        lst);
                 if (e == cudaSuccess)
-                    e = cudaMemcpyAsync(&three[2], keys + s.hi - 1, sizeof(K), cudaMemcpyDeviceToHost, st);
-                if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+                    e = cudaMemcpyAsync(&three[2], keys + sg.hi - 1, sizeof(K), cudaMemcpyDeviceToHost, lst);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(lst);
                 if (e != cudaSuccess) return cuda_fail(e, "quicksort pivot");
                 K a = three[0], b = three[1], c = three[2];
                 if (a > b) std::swap(a, b);
                 if (b > c) b = c;
                 p = (uint64_t)(a > b ? a : b);
             }
-            pivots_h[big_idx[bi]] = p;
-            pp_status ps = partition_device<K>(keys + s.lo, s.hi - s.lo, (K)p, st, d_splits + nmid + bi, nullptr);
+            L.pivots_h[L.big_idx[bi]] = p;
+            pp_status ps = partition_device<K>(keys + sg.lo, sg.hi - sg.lo, (K)p, lst, d_splits + nmid + bi, nullptr);
             if (ps != PP_OK) return ps;
         }
         // ---- mid segments: one batched pass ----
         if (nmid > 0) {
             // host lists up first, then the level's kernels back to back (PDL-chained;
             // with the profiling events in between they run plainly serialized)
-            e = cudaMemcpyAsync(d_segs, pin_segs, sizeof(QSeg) * nmid, cudaMemcpyHostToDevice, st);
-            if (e == cudaSuccess && nh > 0) e = cudaMemcpyAsync(d_hidx, pin_hidx, 4 * nh, cudaMemcpyHostToDevice, st);
+            e = cudaMemcpyAsync(d_segs, pin_segs, sizeof(QSeg) * nmid, cudaMemcpyHostToDevice, lst);
+            if (e == cudaSuccess && nh > 0) e = cudaMemcpyAsync(d_hidx, pin_hidx, 4 * nh, cudaMemcpyHostToDevice, lst);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort H2D");
-            qs_pivot_kernel<K><<<(unsigned)((nmid + 255) / 256), 256, 0, st>>>(keys, d_segs, nmid);
-            if (lvl_prof) cudaEventRecord(lev[0], st);
-            e = qs_launch_pdl(qs_group_kernel<K>, dim3((unsigned)gtot), C::NT, C::SMEM, st, keys, d_segs, nmid,
+            qs_pivot_kernel<K><<<(unsigned)((nmid + 255) / 256), 256, 0, lst>>>(keys, d_segs, nmid);
+            if (lvl_prof) cudaEventRecord(L.lev[0], lst);
+            e = qs_launch_pdl(qs_group_kernel<K>, dim3((unsigned)gtot), C::NT, C::SMEM, lst, keys, d_segs, nmid,
                               P.seed, d_gout);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort group launch");
-            if (lvl_prof) cudaEventRecord(lev[1], st);
+            if (lvl_prof) cudaEventRecord(L.lev[1], lst);
             if (nh > 0) {
                 const unsigned X = (unsigned)std::min<uint64_t>(
                     2 * QS_HEAVY_TILES, std::max<uint64_t>(2, ((uint64_t)sm_count() * 4 + nh - 1) / nh));
                 const dim3 grid(X, (unsigned)nh);
-                e = qs_launch_pdl(qs_hv_reduce_kernel<K>, grid, 256, 0, st, keys, (const QSeg*)d_segs,
+                e = qs_launch_pdl(qs_hv_reduce_kernel<K>, grid, 256, 0, lst, keys, (const QSeg*)d_segs,
                                   (const uint32_t*)d_hidx, (const GroupOut*)d_gout, d_splits, d_hv, HVL);
                 if (e == cudaSuccess)
-                    e = qs_launch_pdl(qs_hv_scan_kernel, dim3((unsigned)nh), 1024, 2 * 8 * (QS_HEAVY_TILES + 1), st,
+                    e = qs_launch_pdl(qs_hv_scan_kernel, dim3((unsigned)nh), 1024, 2 * 8 * (QS_HEAVY_TILES + 1), lst,
                                       d_hv, HVL);
                 if (e == cudaSuccess)
-                    e = qs_launch_pdl(qs_hv_locate_kernel<K>, grid, SW_NT, 0, st, keys, (const QSeg*)d_segs,
+                    e = qs_launch_pdl(qs_hv_locate_kernel<K>, grid, SW_NT, 0, lst, keys, (const QSeg*)d_segs,
                                       (const uint32_t*)d_hidx, d_hv, HVL);
                 if (e == cudaSuccess)
-                    e = qs_launch_pdl(qs_hv_swap_kernel<K>, grid, SW_NT, 0, st, keys, (const QSeg*)d_segs,
+                    e = qs_launch_pdl(qs_hv_swap_kernel<K>, grid, SW_NT, 0, lst, keys, (const QSeg*)d_segs,
                                       (const uint32_t*)d_hidx, d_hv, HVL);
                 if (e != cudaSuccess) return cuda_fail(e, "quicksort heavy cleanup launch");
                 note_launches(4);
@@ -1850,62 +1900,119 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                 const size_t sm = sizeof(StreamBuf<NT, EPT>);
                 cudaFuncSetAttribute(qs_cleanup_kernel<K, NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sm);
-                e = qs_launch_pdl(qs_cleanup_kernel<K, NT, EPT>, dim3((unsigned)nmid), NT, sm, st, keys,
+                e = qs_launch_pdl(qs_cleanup_kernel<K, NT, EPT>, dim3((unsigned)nmid), NT, sm, lst, keys,
                                   (const QSeg*)d_segs, (const GroupOut*)d_gout, d_splits, HEAVY);
             } else {
                 const size_t sm = sizeof(StreamBuf<SW_NT, SW_EPT2>);
-                e = qs_launch_pdl(qs_cleanup_kernel<K, SW_NT, SW_EPT2>, dim3((unsigned)nmid), SW_NT, sm, st, keys,
+                e = qs_launch_pdl(qs_cleanup_kernel<K, SW_NT, SW_EPT2>, dim3((unsigned)nmid), SW_NT, sm, lst, keys,
                                   (const QSeg*)d_segs, (const GroupOut*)d_gout, d_splits, HEAVY);
             }
             if (e != cudaSuccess) return cuda_fail(e, "quicksort cleanup launch");
-            if (lvl_prof) cudaEventRecord(lev[2], st);
+            if (lvl_prof) cudaEventRecord(L.lev[2], lst);
             note_launches(3);
             e = cudaGetLastError();
             if (e != cudaSuccess) return cuda_fail(e, "quicksort mid launch");
         }
         // ---- read back splits (and mid pivots) ----
-        splits_h.assign(nmid + nbig, 0);
         if (nmid + nbig > 0) {
-            e = cudaMemcpyAsync(pin_splits, d_splits, 8 * (nmid + nbig), cudaMemcpyDeviceToHost, st);
+            e = cudaMemcpyAsync(pin_splits, d_splits, 8 * (nmid + nbig), cudaMemcpyDeviceToHost, lst);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort D2H");
         }
         if (nmid > 0) {
-            e = cudaMemcpyAsync(pin_segs, d_segs, sizeof(QSeg) * nmid, cudaMemcpyDeviceToHost, st);
+            e = cudaMemcpyAsync(pin_segs, d_segs, sizeof(QSeg) * nmid, cudaMemcpyDeviceToHost, lst);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort D2H");
         }
-        e = cudaStreamSynchronize(st);
+        e = cudaEventRecord(L.done, lst);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort level event");
+        L.inflight = true;
+        return PP_OK;
+    };
+
+    // wait for a lane's level, read its splits and build its next segment list
+    auto finish_level = [&](Lane& L) -> pp_status {
+        e = cudaEventSynchronize(L.done);
         if (e != cudaSuccess) return cuda_fail(e, "quicksort level");
-        t_sync = std::chrono::steady_clock::now();
-        if (nmid + nbig > 0) memcpy(splits_h.data(), pin_splits, 8 * (nmid + nbig));
-        for (size_t mi = 0; mi < nmid; ++mi) pivots_h[mid_idx[mi]] = pin_segs[mi].pivot;
+        L.inflight = false;
+        const uint64_t nmid = L.nmid, nbig = L.nbig;
+        const QSeg* pin_segs = reinterpret_cast<const QSeg*>(L.pin);
+        const uint64_t* pin_splits = reinterpret_cast<const uint64_t*>(L.pin + pin_sB);
+        L.splits_h.assign(pin_splits, pin_splits + nmid + nbig);
+        for (size_t mi = 0; mi < nmid; ++mi) L.pivots_h[L.mid_idx[mi]] = pin_segs[mi].pivot;
         if (lvl_prof && nmid > 0) {  // debug: per-level times of the batched mid pass
             float tg = 0, tc = 0;
-            cudaEventElapsedTime(&tg, lev[0], lev[1]);
-            cudaEventElapsedTime(&tc, lev[1], lev[2]);
+            cudaEventElapsedTime(&tg, L.lev[0], L.lev[1]);
+            cudaEventElapsedTime(&tc, L.lev[1], L.lev[2]);
             uint64_t mk = 0, mx = 0;
-            for (const QSeg& q : mids) { mk += q.hi - q.lo; mx = std::max<uint64_t>(mx, q.hi - q.lo); }
-            fprintf(stderr, "qs level: nmid=%llu nbig=%llu gtot=%llu keys=%llu maxseg=%llu group=%.3f ms (%.2f TB/s) cleanup=%.3f ms\n",
-                    (unsigned long long)nmid, (unsigned long long)nbig, (unsigned long long)gtot,
-                    (unsigned long long)mk, (unsigned long long)mx, tg, 16.0 * mk / (tg * 1e9), tc);
+            for (const QSeg& q : L.mids) { mk += q.hi - q.lo; mx = std::max<uint64_t>(mx, q.hi - q.lo); }
+            fprintf(stderr, "qs level: lane=%d nmid=%llu nbig=%llu gtot=%llu keys=%llu maxseg=%llu group=%.3f ms "
+                    "(%.2f TB/s) cleanup=%.3f ms\n", L.id, (unsigned long long)nmid, (unsigned long long)nbig,
+                    (unsigned long long)L.gtot, (unsigned long long)mk, (unsigned long long)mx, tg,
+                    16.0 * mk / (tg * 1e9), tc);
         }
         // ---- next level ----
-        next.clear();
-        auto visit = [&](const HSeg& s, uint64_t p, uint64_t k) {
-            if (s.mode == 0) {
+        L.next.clear();
+        auto visit = [&](const HSeg& sg, uint64_t p, uint64_t k) {
+            if (sg.mode == 0) {
                 if (k == 0) {
                     // p is the segment minimum; split by x <= p next (unless all == MAX)
-                    if ((K)p != KMAX) next.push_back({s.lo, s.hi, (uint64_t)(K)(p + 1), 1});
+                    if ((K)p != KMAX) L.next.push_back({sg.lo, sg.hi, (uint64_t)(K)(p + 1), 1});
                 } else {
-                    add_child(s.lo, s.lo + k);
-                    add_child(s.lo + k, s.hi);
+                    add_child(L.next, sg.lo, sg.lo + k);
+                    add_child(L.next, sg.lo + k, sg.hi);
                 }
             } else {
-                add_child(s.lo + k, s.hi);  // [lo, lo+k) is all equal: final
+                add_child(L.next, sg.lo + k, sg.hi);  // [lo, lo+k) is all equal: final
             }
         };
-        for (size_t mi = 0; mi < nmid; ++mi) visit(cur[mid_idx[mi]], pivots_h[mid_idx[mi]], splits_h[mi]);
-        for (size_t bi = 0; bi < nbig; ++bi) visit(cur[big_idx[bi]], pivots_h[big_idx[bi]], splits_h[nmid + bi]);
-        cur.swap(next);
+        for (size_t mi = 0; mi < nmid; ++mi) visit(L.cur[L.mid_idx[mi]], L.pivots_h[L.mid_idx[mi]], L.splits_h[mi]);
+        for (size_t bi = 0; bi < nbig; ++bi)
+            visit(L.cur[L.big_idx[bi]], L.pivots_h[L.big_idx[bi]], L.splits_h[nmid + bi]);
+        L.cur.swap(L.next);
+        return PP_OK;
+    };
+
+    // phase 1: one lane while big segments exist (or fewer than two segments)
+    auto needs_one_lane = [&](const Lane& L) {
+        const int64_t nl = P.qs_lanes > 0 ? P.qs_lanes : (sizeof(K) == 8 ? 2 : 1);
+        if (nl < 2 || L.cur.size() < 2) return true;
+        for (const HSeg& sg : L.cur)
+            if (sg.hi - sg.lo >= BIG) return true;
+        return false;
+    };
+    pp_status ps = PP_OK;
+    while (!lanes[0].cur.empty() && needs_one_lane(lanes[0])) {
+        if ((ps = launch_level(lanes[0])) != PP_OK) return ps;
+        if ((ps = finish_level(lanes[0])) != PP_OK) return ps;
+    }
+    if (!lanes[0].cur.empty()) {
+        // phase 2: split by keys (array order), lane 1 starts after the work so far on `st`
+        std::vector<HSeg>& c0 = lanes[0].cur;
+        uint64_t total = 0, acc = 0;
+        for (const HSeg& sg : c0) total += sg.hi - sg.lo;
+        size_t cut = 0;
+        while (cut + 1 < c0.size() && acc + (c0[cut].hi - c0[cut].lo) <= total / 2) {
+            acc += c0[cut].hi - c0[cut].lo;
+            ++cut;
+        }
+        if (cut == 0) cut = 1;
+        lanes[1].cur.assign(c0.begin() + cut, c0.end());
+        c0.resize(cut);
+        e = cudaEventRecord(lane_ev[2], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(lane_st1, lane_ev[2], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort lanes");
+        if ((ps = launch_level(lanes[0])) != PP_OK) return ps;
+        if ((ps = launch_level(lanes[1])) != PP_OK) return ps;
+        while (lanes[0].inflight || lanes[1].inflight) {
+            for (Lane& L : lanes) {
+                if (!L.inflight) continue;
+                if ((ps = finish_level(L)) != PP_OK) return ps;
+                if ((ps = launch_level(L)) != PP_OK) return ps;
+            }
+        }
+        // lane 1's last work precedes whatever follows on `st`
+        e = cudaEventRecord(lane_ev[2], lane_st1);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, lane_ev[2], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort lanes");
     }
     // ---- small segments (one CTA each: recursion down to leaves, packed into
     //      bins) and leaves (sorted in shared memory, one CTA per bin); lists
