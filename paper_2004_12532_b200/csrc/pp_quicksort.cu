@@ -1689,7 +1689,9 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     if (!pin_all) return PP_E_NOMEM;
     lanes[0].pin = pin_all;
     lanes[1].pin = pin_all + pin_lane;
-    size_t lane_half = 0;  // bytes of each lane's device region (monotone within a sort)
+    // bytes of each lane's device region: the level bound up front (a few MB
+    // at 2^28 keys), so a growing level never has to drain the other lane
+    size_t lane_half = qs_level_bound<K>(n);
 
     // classify a lane's segments, upload its level, launch its kernels and
     // the readback; records L.done (L.inflight = false if nothing to do)
