@@ -681,6 +681,7 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "qs_pipe") P.qs_pipe = value;
     else if (k == "dist_p2p") P.dist_p2p = value ? 1 : 0;
     else if (k == "qs_lanes") P.qs_lanes = value;
+    else if (k == "qs_early") P.qs_early = value;
     else if (k == "bps_nt") P.bps_nt = value;
     else if (k == "cleanup_chain") P.cleanup_chain = value;
     else if (k == "cleanup_bitmap") P.cleanup_bitmap = value;
@@ -717,6 +718,7 @@ int64_t pp_get_param(const char* name) {
     if (k == "qs_pipe") return P.qs_pipe;
     if (k == "dist_p2p") return P.dist_p2p;
     if (k == "qs_lanes") return P.qs_lanes;
+    if (k == "qs_early") return P.qs_early;
     if (k == "bps_nt") return P.bps_nt;
     if (k == "cleanup_chain") return P.cleanup_chain;
     if (k == "cleanup_bitmap") return P.cleanup_bitmap;

@@ -1596,7 +1596,11 @@ uint64_t quicksort_workspace_bound(uint64_t n) {
     const uint64_t nslot = 2 * (n / q.LEAF) + 6 * (n / (q.LEAF + 1) + 1) + 6;
     const size_t lists = al256(8 * cl) + al256(4 * cl) + al256(8 * cs) + al256(4 * cs) + al256(8 * cs) +
                          al256(sizeof(GroupOut) * cs) + al256(8 * nslot) + al256(4 * nslot) + 256;
-    return std::max(2 * level, lists);  // two level lanes (quicksort_device) or the final lists
+    // early per-CTA recursion lists (every small segment, all bin slots), beside the lanes
+    const uint64_t s_max = n / (q.LEAF + 1) + 1, slot_max = 2 * (n / q.LEAF) + 6 * s_max + 6;
+    const size_t early = al256(8 * s_max) + al256(4 * s_max) + al256(8 * s_max) + al256(sizeof(GroupOut) * s_max) +
+                         al256(8 * slot_max) + al256(4 * slot_max);
+    return std::max(2 * level + early, lists);  // two level lanes + early lists (quicksort_device), or the final lists
 }
 template uint64_t quicksort_workspace_bound<uint64_t>(uint64_t);
 template uint64_t quicksort_workspace_bound<uint32_t>(uint64_t);
@@ -1620,6 +1624,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     };
     std::vector<uint64_t> leaf_lo, small_lo;
     std::vector<uint32_t> leaf_len, small_len;
+    std::vector<uint64_t> small_base_v{0};  // bin-slot offset of each small segment (prefix of qs_bin_cap)
     // segments in (LEAF, SMALL] finish in one CTA each (qs_small_kernel)
     const uint64_t SMALL = geom.SMALL;
     auto add_child = [&](std::vector<HSeg>& next, uint64_t lo, uint64_t hi) {
@@ -1631,6 +1636,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         } else if (len <= SMALL) {
             small_lo.push_back(lo);
             small_len.push_back((uint32_t)len);
+            small_base_v.push_back(small_base_v.back() + qs_bin_cap(len, LEAF));
         } else {
             next.push_back({lo, hi, 0, 0});
         }
@@ -1679,6 +1685,115 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     if (lvl_prof)
         for (Lane& L : lanes)
             for (auto& x : L.lev) cudaEventCreate(&x);
+    // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot
+    auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
+        if (cnt == 0) return cudaSuccess;
+        // default: the index-staged counting bin sort (6); 5 = counting with keys in registers,
+        // 4 = packed 32-bit merge (u64 only), 3 = merge
+        const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : 6;
+        if (algo == 6) {  // bins of <= 2 LC::LEAF keys (1024 threads) or <= LC::LEAF (512 threads, 2 CTAs/SM)
+            constexpr int HL = LC::LEAF, HN = HL / LEAF_E;
+            if (LEAF > (uint64_t)HL) {
+                constexpr int PL = 2 * HL, BNT = 1024;
+                const size_t smem = sizeof(K) * PL + 4 * PL + 16;
+                cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+                qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
+                                                                                  const_cast<uint32_t*>(d_len));
+            } else {
+                constexpr int PL = HL, BNT = 512;
+                const size_t smem = sizeof(K) * PL + 4 * PL + 16;
+                cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+                qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
+                                                                                  const_cast<uint32_t*>(d_len));
+            }
+            const size_t msmem = sizeof(K) * lpad_host(2 * HL);
+            cudaFuncSetAttribute(qs_leaf_handoff_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)msmem);
+            const unsigned hg = (unsigned)std::min<uint64_t>((cnt + HN - 1) / HN, 2 * (uint64_t)sm_count());
+            qs_leaf_handoff_kernel<K, HL, HN><<<hg, HN, msmem, bst>>>(keys, d_lo, d_len, cnt);
+            note_launches(1);
+        } else if (algo == 5 && LEAF <= (uint64_t)LC::LEAF / 2) {
+            constexpr int PL = LC::LEAF / 2;
+            const size_t smem = sizeof(K) * lpad_host(PL) + 4 * PL + 16;
+            cudaFuncSetAttribute(qs_leaf_bucket_kernel<K, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_bucket_kernel<K, PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(keys, d_lo, d_len);
+        } else if (algo == 5) {
+            constexpr int PL = LC::LEAF;
+            const size_t smem = sizeof(K) * lpad_host(PL) + 4 * PL + 16;
+            cudaFuncSetAttribute(qs_leaf_bucket_kernel<K, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_bucket_kernel<K, PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(keys, d_lo, d_len);
+        } else if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF / 2) {
+            constexpr int PL = PK_LEAF / 2;
+            const size_t smem = 8 * PL + 8 * lpad_host(PL) + 4 * lpad_host(PL);
+            cudaFuncSetAttribute(qs_leaf_packed_kernel<PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_packed_kernel<PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(reinterpret_cast<uint64_t*>(keys),
+                                                                                d_lo, d_len);
+        } else if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF) {
+            const size_t smem = 8 * PK_LEAF + 8 * lpad_host(PK_LEAF) + 4 * lpad_host(PK_LEAF);
+            cudaFuncSetAttribute(qs_leaf_packed_kernel<PK_LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            qs_leaf_packed_kernel<PK_LEAF><<<(unsigned)cnt, PK_NT, smem, bst>>>(reinterpret_cast<uint64_t*>(keys), d_lo,
+                                                                               d_len);
+        } else if (algo == 2) {
+            constexpr int NW = LC::LEAF / 256;
+            const size_t smem = sizeof(K) * LC::LEAF + 2 * 256 * NW;
+            cudaFuncSetAttribute(qs_leaf_radix_kernel<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_radix_kernel<K, NW><<<(unsigned)cnt, NW * 32, smem, bst>>>(keys, d_lo, d_len);
+        } else if (algo == 1) {
+            const size_t smem = sizeof(K) * LC::LEAF;
+            cudaFuncSetAttribute(qs_leaf_kernel<K, LC::LEAF, LC::NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, bst>>>(keys, d_lo, d_len);
+        } else if (LEAF <= (uint64_t)LC::LEAF / 4) {  // small bins: quarter-size CTAs, more per SM
+            constexpr int QL = LC::LEAF / 4, QN = QL / LEAF_E;
+            const size_t smem = sizeof(K) * (QL + QL / 8);
+            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, QL, QN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            qs_leaf_merge_kernel<K, QL, QN><<<(unsigned)cnt, QN, smem, bst>>>(keys, d_lo, d_len);
+        } else if (LEAF <= (uint64_t)LC::LEAF / 2) {  // half-size CTAs
+            constexpr int HL = LC::LEAF / 2, HN = HL / LEAF_E;
+            const size_t smem = sizeof(K) * (HL + HL / 8);
+            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, bst>>>(keys, d_lo, d_len);
+        } else {
+            const size_t smem = sizeof(K) * (LC::LEAF + LC::LEAF / 8);
+            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, LC::LEAF, LC::NT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, bst>>>(keys, d_lo, d_len);
+        }
+        note_launches(1);
+        return cudaGetLastError();
+    };
+    // the per-CTA recursion over `cnt` small segments (lists on the device)
+    auto launch_small = [&](uint64_t cnt, const uint64_t* slo, const uint32_t* sln, const uint64_t* sbase,
+                            uint64_t* blo, uint32_t* bln, GroupOut* scr, uint64_t* prof, cudaStream_t s3) {
+        if (P.qs_small_cfg == 2) {
+            using S = SmallCfg<K, 2>;
+            cudaFuncSetAttribute(qs_small_kernel<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+            qs_small_kernel<K, 2><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln,
+                                                                         (uint32_t)LEAF, P.seed, scr, prof);
+        } else if (P.qs_small_cfg == 3) {
+            using S = SmallCfg<K, 3>;
+            cudaFuncSetAttribute(qs_small_kernel<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+            qs_small_kernel<K, 3><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln,
+                                                                         (uint32_t)LEAF, P.seed, scr, prof);
+        } else if (P.qs_small_cfg == 0) {
+            using S = SmallCfg<K, 0>;
+            cudaFuncSetAttribute(qs_small_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+            qs_small_kernel<K, 0><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln,
+                                                                         (uint32_t)LEAF, P.seed, scr, prof);
+        } else {
+            using S = SmallCfg<K, 1>;
+            cudaFuncSetAttribute(qs_small_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+            qs_small_kernel<K, 1><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln,
+                                                                         (uint32_t)LEAF, P.seed, scr, prof);
+        }
+        note_launches(1);
+        return cudaGetLastError();
+    };
     // pinned staging per lane, sized once from the level bound (a lane's
     // readback may be in flight while the other lane builds its level)
     const uint64_t nmid_max = n / (SMALL + 1) + 1, nbig_max = n / BIG + 1;
@@ -1692,6 +1807,51 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     // bytes of each lane's device region: the level bound up front (a few MB
     // at 2^28 keys), so a growing level never has to drain the other lane
     size_t lane_half = qs_level_bound<K>(n);
+    // early per-CTA recursion (param qs_early): the lists of every small
+    // segment and all bin slots, indexed globally, after the two lane regions;
+    // a batch runs on a third stream as soon as its segments are final
+    const bool early = P.qs_early > 0 || (P.qs_early < 0 && sizeof(K) == 8);
+    const uint64_t s_max = n / (LEAF + 1) + 1, slot_max = 2 * (n / LEAF) + 6 * s_max + 6;
+    const size_t e_sloB = al256(8 * s_max), e_slnB = al256(4 * s_max), e_sbB = al256(8 * s_max);
+    const size_t e_scrB = al256(sizeof(GroupOut) * s_max), e_bloB = al256(8 * slot_max);
+    const size_t earlyB = early ? e_sloB + e_slnB + e_sbB + e_scrB + e_bloB + al256(4 * slot_max) : 0;
+    unsigned char* ws_all = static_cast<unsigned char*>(qs_workspace(2 * lane_half + earlyB));
+    if (!ws_all) return PP_E_NOMEM;
+    unsigned char* ew = ws_all + 2 * lane_half;
+    uint64_t* d_eslo = reinterpret_cast<uint64_t*>(ew);
+    uint32_t* d_esln = reinterpret_cast<uint32_t*>(ew + e_sloB);
+    uint64_t* d_esbase = reinterpret_cast<uint64_t*>(ew + e_sloB + e_slnB);
+    GroupOut* d_escr = reinterpret_cast<GroupOut*>(ew + e_sloB + e_slnB + e_sbB);
+    uint64_t* d_eblo = reinterpret_cast<uint64_t*>(ew + e_sloB + e_slnB + e_sbB + e_scrB);
+    uint32_t* d_ebln = reinterpret_cast<uint32_t*>(ew + e_sloB + e_slnB + e_sbB + e_scrB + e_bloB);
+    static cudaStream_t early_st = nullptr, early_bst = nullptr;  // recursion; bin sorts
+    static cudaEvent_t early_ev[64];
+    if (!early_st) {
+        cudaStreamCreateWithFlags(&early_st, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&early_bst, cudaStreamNonBlocking);
+        for (auto& x : early_ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    }
+    uint64_t early_nb = 0;  // batches so far (events recycled: a batch's bins wait on its recursion)
+    uint64_t small_done = 0;
+    // small segments [b, en) (their levels have completed: the host synchronised on them)
+    auto small_batch = [&](uint64_t b, uint64_t en) -> pp_status {
+        if (en <= b) return PP_OK;
+        const uint64_t cnt = en - b;
+        e = cudaMemcpyAsync(d_eslo + b, small_lo.data() + b, 8 * cnt, cudaMemcpyHostToDevice, early_st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d_esln + b, small_len.data() + b, 4 * cnt, cudaMemcpyHostToDevice, early_st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d_esbase + b, small_base_v.data() + b, 8 * cnt, cudaMemcpyHostToDevice, early_st);
+        if (e == cudaSuccess)
+            e = launch_small(cnt, d_eslo + b, d_esln + b, d_esbase + b, d_eblo, d_ebln, d_escr + b, nullptr, early_st);
+        cudaEvent_t ev = early_ev[early_nb++ % 64];
+        if (e == cudaSuccess) e = cudaEventRecord(ev, early_st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(early_bst, ev, 0);
+        if (e == cudaSuccess)
+            e = sort_bins(d_eblo + small_base_v[b], d_ebln + small_base_v[b], small_base_v[en] - small_base_v[b],
+                          early_bst);
+        return e == cudaSuccess ? PP_OK : cuda_fail(e, "quicksort early small batch");
+    };
 
     // classify a lane's segments, upload its level, launch its kernels and
     // the readback; records L.done (L.inflight = false if nothing to do)
@@ -2009,6 +2169,10 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                 if (!L.inflight) continue;
                 if ((ps = finish_level(L)) != PP_OK) return ps;
                 if ((ps = launch_level(L)) != PP_OK) return ps;
+                if (early && small_lo.size() - small_done >= 4 * (uint64_t)sm_count()) {
+                    if ((ps = small_batch(small_done, small_lo.size())) != PP_OK) return ps;
+                    small_done = small_lo.size();
+                }
             }
         }
         // lane 1's last work precedes whatever follows on `st`
@@ -2016,10 +2180,17 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, lane_ev[2], 0);
         if (e != cudaSuccess) return cuda_fail(e, "quicksort lanes");
     }
+    if (early) {  // the rest of the small segments, then `st` waits for the early stream
+        if ((ps = small_batch(small_done, small_lo.size())) != PP_OK) return ps;
+        small_done = small_lo.size();
+        e = cudaEventRecord(lane_ev[2], early_bst);  // the bin sorts follow their recursions
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, lane_ev[2], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort early join");
+    }
     // ---- small segments (one CTA each: recursion down to leaves, packed into
     //      bins) and leaves (sorted in shared memory, one CTA per bin); lists
     //      uploaded in chunks of QS_LIST_CHUNK (stream order makes reuse safe) ----
-    const uint64_t nleaf = leaf_lo.size(), nsmall = small_lo.size();
+    const uint64_t nleaf = leaf_lo.size(), nsmall = early ? 0 : small_lo.size();
     const uint64_t cl = std::min<uint64_t>(nleaf, QS_LIST_CHUNK), cs = std::min<uint64_t>(nsmall, QS_LIST_CHUNK);
     // bin slots of every small segment (global offsets: chunks of the
     // per-CTA recursion and their bin sorts are pipelined on two streams, so
@@ -2033,88 +2204,6 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     unsigned char* qws =
         static_cast<unsigned char*>(qs_workspace(loB + lnB + sloB + slnB + sbB + scrB + bloB + blnB + 256));
     if (!qws) return PP_E_NOMEM;
-    // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot
-    auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
-        if (cnt == 0) return cudaSuccess;
-        // default: the index-staged counting bin sort (6); 5 = counting with keys in registers,
-        // 4 = packed 32-bit merge (u64 only), 3 = merge
-        const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : 6;
-        if (algo == 6) {  // bins of <= 2 LC::LEAF keys (1024 threads) or <= LC::LEAF (512 threads, 2 CTAs/SM)
-            constexpr int HL = LC::LEAF, HN = HL / LEAF_E;
-            if (LEAF > (uint64_t)HL) {
-                constexpr int PL = 2 * HL, BNT = 1024;
-                const size_t smem = sizeof(K) * PL + 4 * PL + 16;
-                cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-                qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
-                                                                                  const_cast<uint32_t*>(d_len));
-            } else {
-                constexpr int PL = HL, BNT = 512;
-                const size_t smem = sizeof(K) * PL + 4 * PL + 16;
-                cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-                qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
-                                                                                  const_cast<uint32_t*>(d_len));
-            }
-            const size_t msmem = sizeof(K) * lpad_host(2 * HL);
-            cudaFuncSetAttribute(qs_leaf_handoff_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)msmem);
-            const unsigned hg = (unsigned)std::min<uint64_t>((cnt + HN - 1) / HN, 2 * (uint64_t)sm_count());
-            qs_leaf_handoff_kernel<K, HL, HN><<<hg, HN, msmem, bst>>>(keys, d_lo, d_len, cnt);
-            note_launches(1);
-        } else if (algo == 5 && LEAF <= (uint64_t)LC::LEAF / 2) {
-            constexpr int PL = LC::LEAF / 2;
-            const size_t smem = sizeof(K) * lpad_host(PL) + 4 * PL + 16;
-            cudaFuncSetAttribute(qs_leaf_bucket_kernel<K, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_bucket_kernel<K, PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(keys, d_lo, d_len);
-        } else if (algo == 5) {
-            constexpr int PL = LC::LEAF;
-            const size_t smem = sizeof(K) * lpad_host(PL) + 4 * PL + 16;
-            cudaFuncSetAttribute(qs_leaf_bucket_kernel<K, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_bucket_kernel<K, PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(keys, d_lo, d_len);
-        } else if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF / 2) {
-            constexpr int PL = PK_LEAF / 2;
-            const size_t smem = 8 * PL + 8 * lpad_host(PL) + 4 * lpad_host(PL);
-            cudaFuncSetAttribute(qs_leaf_packed_kernel<PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_packed_kernel<PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(reinterpret_cast<uint64_t*>(keys),
-                                                                                d_lo, d_len);
-        } else if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF) {
-            const size_t smem = 8 * PK_LEAF + 8 * lpad_host(PK_LEAF) + 4 * lpad_host(PK_LEAF);
-            cudaFuncSetAttribute(qs_leaf_packed_kernel<PK_LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            qs_leaf_packed_kernel<PK_LEAF><<<(unsigned)cnt, PK_NT, smem, bst>>>(reinterpret_cast<uint64_t*>(keys), d_lo,
-                                                                               d_len);
-        } else if (algo == 2) {
-            constexpr int NW = LC::LEAF / 256;
-            const size_t smem = sizeof(K) * LC::LEAF + 2 * 256 * NW;
-            cudaFuncSetAttribute(qs_leaf_radix_kernel<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_radix_kernel<K, NW><<<(unsigned)cnt, NW * 32, smem, bst>>>(keys, d_lo, d_len);
-        } else if (algo == 1) {
-            const size_t smem = sizeof(K) * LC::LEAF;
-            cudaFuncSetAttribute(qs_leaf_kernel<K, LC::LEAF, LC::NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, bst>>>(keys, d_lo, d_len);
-        } else if (LEAF <= (uint64_t)LC::LEAF / 4) {  // small bins: quarter-size CTAs, more per SM
-            constexpr int QL = LC::LEAF / 4, QN = QL / LEAF_E;
-            const size_t smem = sizeof(K) * (QL + QL / 8);
-            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, QL, QN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            qs_leaf_merge_kernel<K, QL, QN><<<(unsigned)cnt, QN, smem, bst>>>(keys, d_lo, d_len);
-        } else if (LEAF <= (uint64_t)LC::LEAF / 2) {  // half-size CTAs
-            constexpr int HL = LC::LEAF / 2, HN = HL / LEAF_E;
-            const size_t smem = sizeof(K) * (HL + HL / 8);
-            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, bst>>>(keys, d_lo, d_len);
-        } else {
-            const size_t smem = sizeof(K) * (LC::LEAF + LC::LEAF / 8);
-            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, LC::LEAF, LC::NT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, bst>>>(keys, d_lo, d_len);
-        }
-        note_launches(1);
-        return cudaGetLastError();
-    };
     if (nsmall > 0) {
         unsigned char* w = qws + loB + lnB;
         uint64_t* d_slo = reinterpret_cast<uint64_t*>(w);

@@ -111,6 +111,7 @@ QUICKSORT_PARAMS = [
     {"qs_heavy": 0}, {"qs_waves": 1}, {"qs_small_cfg": 0}, {"qs_pipe": 3},
     {"leaf_algo": 5}, {"leaf_algo": 5, "leaf": 4096}, {"leaf_algo": 4}, {"leaf_algo": 3, "leaf": 4096},
     {"leaf_algo": 6}, {"leaf_algo": 6, "leaf": 2000}, {"qs_lanes": 1}, {"qs_lanes": 2, "qs_cta_max": 1 << 18},
+    {"qs_early": 1}, {"qs_early": 1, "qs_small": 1 << 17, "qs_cta_max": 1 << 19},
 ]
 
 

@@ -83,7 +83,8 @@ def test_medium_sizes(pp, dt, mx):
                                     {"qs_pipe": 1}, {"qs_pipe": 16}, {"qs_small_cfg": 0}, {"qs_small_cfg": 1}, {"qs_small_cfg": 2},
                                     {"leaf_algo": 5}, {"leaf_algo": 5, "leaf": 4096}, {"leaf_algo": 5, "leaf": 300},
                                     {"leaf_algo": 6}, {"leaf_algo": 6, "leaf": 300}, {"qs_lanes": 1},
-                                    {"qs_lanes": 2}, {"qs_lanes": 2, "qs_small": 1 << 17}])
+                                    {"qs_lanes": 2}, {"qs_lanes": 2, "qs_small": 1 << 17}, {"qs_early": 1},
+                                    {"qs_early": 1, "qs_lanes": 1}, {"qs_early": 0}])
 def test_qs_parameters(pp, dt, mx, params):
     """Bin sorts (radix / merge / bitonic), leaf sizes, level balancing, the
     heavy-segment batched cleanup, the per-CTA recursion and the Strided
