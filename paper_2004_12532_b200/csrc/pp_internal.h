@@ -63,7 +63,7 @@ struct Params {
                                    // -1 auto (u64: on, u32: off -- measured), 0 off, 1 on
     int64_t dist_p2p = 0;          // pp_partition_dist: 1 = one-sided exchange over CUDA-IPC peer mappings (no staging)
     int64_t host_chunk = 1 << 22;  // host-buffer partition: keys per streamed chunk
-    int64_t qs_heavy = 1 << 23;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
+    int64_t qs_heavy = 1 << 22;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
 };
 Params& params();
 
