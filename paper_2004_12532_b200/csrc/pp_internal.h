@@ -57,10 +57,10 @@ struct Params {
     int64_t bps_nt = 256;          // Blocked-Prefix-Sum Reorder level kernel: threads per CTA (256/512/1024)
     int64_t qs_pipe = 1;           // quicksort: chunks of the per-CTA recursion pipelined with their bin sorts (measured: no gain)
     int64_t qs_lanes = 0;          // quicksort level loop: 1 = one stream, 2 = two array-disjoint lanes on two
-                                   // streams, 0 = auto (u64: 2, u32: 1 -- measured)
+                                   // streams, 0 = auto (= 2)
     int64_t qs_early = -1;         // quicksort: run the per-CTA recursion + bin sort of small segments on two more
                                    // streams as soon as their levels complete (overlapping the remaining levels);
-                                   // -1 auto (u64: on, u32: off -- measured), 0 off, 1 on
+                                   // -1 auto (= on), 0 off, 1 on
     int64_t dist_p2p = 0;          // pp_partition_dist: 1 = one-sided exchange over CUDA-IPC peer mappings (no staging)
     int64_t host_chunk = 1 << 22;  // host-buffer partition: keys per streamed chunk
     int64_t qs_heavy = 1 << 22;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)

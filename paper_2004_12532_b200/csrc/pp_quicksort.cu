@@ -1810,7 +1810,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     // early per-CTA recursion (param qs_early): the lists of every small
     // segment and all bin slots, indexed globally, after the two lane regions;
     // a batch runs on a third stream as soon as its segments are final
-    const bool early = P.qs_early > 0 || (P.qs_early < 0 && sizeof(K) == 8);
+    const bool early = P.qs_early != 0;  // -1 auto = on
     const uint64_t s_max = n / (LEAF + 1) + 1, slot_max = 2 * (n / LEAF) + 6 * s_max + 6;
     const size_t e_sloB = al256(8 * s_max), e_slnB = al256(4 * s_max), e_sbB = al256(8 * s_max);
     const size_t e_scrB = al256(sizeof(GroupOut) * s_max), e_bloB = al256(8 * slot_max);
@@ -2135,7 +2135,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
 
     // phase 1: one lane while big segments exist (or fewer than two segments)
     auto needs_one_lane = [&](const Lane& L) {
-        const int64_t nl = P.qs_lanes > 0 ? P.qs_lanes : (sizeof(K) == 8 ? 2 : 1);
+        const int64_t nl = P.qs_lanes > 0 ? P.qs_lanes : 2;
         if (nl < 2 || L.cur.size() < 2) return true;
         for (const HSeg& sg : L.cur)
             if (sg.hi - sg.lo >= BIG) return true;
