@@ -547,10 +547,12 @@ static void launch_group_t(K* region, uint64_t n_lines, uint32_t g, uint64_t see
                            cudaStream_t st) {
     using C = typename VariantCfg<K, V>::type;
     occupancy_of<C>();
-    // programmatic dependent launch: launch and CTA setup overlap the tail of
-    // the previous kernel on the stream (e.g. the previous call's cleanup);
-    // the kernel waits for it before touching memory
-    launch_pdl_smem(ss_group_kernel<C>, g, C::NT, C::SMEM, st, region, n_lines, g, seed, pivot, out);
+    // plain launch: with programmatic dependent launch the group CTAs became
+    // resident while the previous call's cooperative cleanup still held SMs,
+    // placing them unevenly -- the group kernel ran ~4% slower at 2^27 keys
+    // (measured; its griddep_wait() is then a no-op)
+    ss_group_kernel<C><<<g, C::NT, C::SMEM, st>>>(region, n_lines, g, seed, pivot, out);
+    note_launches(1);
 }
 template <typename K>
 static void launch_group(int v, K* region, uint64_t n_lines, uint32_t g, uint64_t seed, K pivot, GroupOut* out,
