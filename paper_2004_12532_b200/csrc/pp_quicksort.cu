@@ -1811,6 +1811,9 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     // segment and all bin slots, indexed globally, after the two lane regions;
     // a batch runs on a third stream as soon as its segments are final
     const bool early = P.qs_early != 0;  // -1 auto = on
+    // batch size of the early recursion: x #SM segments (auto: 4 for u64, 2 for u32 -- measured)
+    const uint64_t early_min =
+        (uint64_t)(P.qs_early_min > 0 ? P.qs_early_min : (sizeof(K) == 8 ? 4 : 2)) * (uint64_t)sm_count();
     const uint64_t s_max = n / (LEAF + 1) + 1, slot_max = 2 * (n / LEAF) + 6 * s_max + 6;
     const size_t e_sloB = al256(8 * s_max), e_slnB = al256(4 * s_max), e_sbB = al256(8 * s_max);
     const size_t e_scrB = al256(sizeof(GroupOut) * s_max), e_bloB = al256(8 * slot_max);
@@ -2169,7 +2172,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                 if (!L.inflight) continue;
                 if ((ps = finish_level(L)) != PP_OK) return ps;
                 if ((ps = launch_level(L)) != PP_OK) return ps;
-                if (early && small_lo.size() - small_done >= 4 * (uint64_t)sm_count()) {
+                if (early && small_lo.size() - small_done >= early_min) {
                     if ((ps = small_batch(small_done, small_lo.size())) != PP_OK) return ps;
                     small_done = small_lo.size();
                 }
