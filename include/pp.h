@@ -269,7 +269,8 @@ pp_status pp_last_stats(uint64_t *out13);
  * (-1 auto: 3-kernel chain below 1 GiB of keys, fused tail above; 0 fused;
  * 1 chain), "cleanup_bitmap", "qs_small", "qs_small_cfg", "qs_waves",
  * "qs_heavy", "qs_pipe", "qs_lanes" (0 auto = 2 lanes), "qs_early" (-1 auto
- * = on), "qs_early_min" (0 auto), "host_chunk", "bps_nt", "dist_p2p".
+ * = on), "qs_early_min" (0 auto), "qs_minl" (0 auto: 128 KiB per group), "host_chunk",
+ * "bps_nt", "dist_p2p".
  * Returns PP_E_INVAL for an unknown name.  pp_get_param returns INT64_MIN
  * for an unknown name. */
 pp_status pp_set_param(const char *name, int64_t value);

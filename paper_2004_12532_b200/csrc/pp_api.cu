@@ -683,6 +683,7 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "qs_lanes") P.qs_lanes = value;
     else if (k == "qs_early") P.qs_early = value;
     else if (k == "qs_early_min") P.qs_early_min = value;
+    else if (k == "qs_minl") P.qs_minl = value;
     else if (k == "bps_nt") P.bps_nt = value;
     else if (k == "cleanup_chain") P.cleanup_chain = value;
     else if (k == "cleanup_bitmap") P.cleanup_bitmap = value;
@@ -721,6 +722,7 @@ int64_t pp_get_param(const char* name) {
     if (k == "qs_lanes") return P.qs_lanes;
     if (k == "qs_early") return P.qs_early;
     if (k == "qs_early_min") return P.qs_early_min;
+    if (k == "qs_minl") return P.qs_minl;
     if (k == "bps_nt") return P.bps_nt;
     if (k == "cleanup_chain") return P.cleanup_chain;
     if (k == "cleanup_bitmap") return P.cleanup_bitmap;

@@ -63,6 +63,7 @@ struct Params {
                                    // -1 auto (= on), 0 off, 1 on
     int64_t qs_early_min = 0;      // quicksort early recursion: batch when >= this x #SM small segments are final
                                    // (0 auto: 4 for u64, 2 for u32 -- measured)
+    int64_t qs_minl = 0;           // quicksort: at least this many lines per group for mid segments (0 auto: 128 KiB)
     int64_t dist_p2p = 0;          // pp_partition_dist: 1 = one-sided exchange over CUDA-IPC peer mappings (no staging)
     int64_t host_chunk = 1 << 22;  // host-buffer partition: keys per streamed chunk
     int64_t qs_heavy = 1 << 22;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)

@@ -1613,7 +1613,9 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     const QsGeom geom = qs_geom<K>();
     const uint64_t LEAF = geom.LEAF, BIG = geom.BIG, G_TARGET = geom.G_TARGET, HEAVY = geom.HEAVY;
     const HvLayout HVL = hv_layout();
-    const uint64_t MINL = 16;  // at least this many lines per group for mid segments
+    // at least this many lines per group (mid segments); auto: 128 KiB of keys
+    // per group (16 lines u64, 32 lines u32 -- the best of a same-box sweep for each)
+    const uint64_t MINL = P.qs_minl > 0 ? (uint64_t)P.qs_minl : std::max<uint64_t>(1, (128u << 10) / (C::LK * sizeof(K)));
     const K KMAX = (K)~(K)0;
     g_qs_user_base = al256(partition_workspace_bound(n));
     g_qs_peak = 0;
