@@ -64,6 +64,7 @@ def _pivot(rng, a, mx):
 PARTITION_PARAMS = [
     {}, {"path": 1}, {"path": 3}, {"small_n": 0}, {"small_n": 0, "min_lines_per_group": 1},
     {"g": 3}, {"g": 64}, {"variant": 1}, {"variant": 4}, {"variant": 8}, {"cleanup_chain": 1},
+    {"cleanup_chain": 0}, {"cleanup_chain": 0, "small_n": 0},
     {"cleanup_bitmap": 0}, {"strided": 1}, {"strided": 1, "small_n": 0}, {"fused": 1},
 ]
 
