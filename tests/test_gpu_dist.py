@@ -184,3 +184,16 @@ def test_partition_dist_p2p_param_single_rank(pp):
     finally:
         pp.reset_params()
     assert pp.pp_get_param("dist_p2p") == 0
+
+
+def test_dist_last_timing_single_rank(pp):
+    """pp_dist_last_timing after a one-rank pp_partition_dist: the three
+    phase times are set (non-negative, local partition > 0) and no bytes
+    moved between GPUs."""
+    from gpu_util import to_dev
+    a = synth.uniform_u64_np(1 << 20, 17)
+    t = to_dev(a)
+    pp.pp_partition_dist(t, 1 << 63)
+    tm = pp.pp_dist_last_timing()
+    assert tm["local_ms"] > 0 and tm["gather_ms"] >= 0 and tm["exchange_ms"] >= 0
+    assert tm["bytes"] == 0
