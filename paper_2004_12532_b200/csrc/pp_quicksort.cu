@@ -1808,7 +1808,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     lanes[1].pin = pin_all + pin_lane;
     // bytes of each lane's device region: the level bound up front (a few MB
     // at 2^28 keys), so a growing level never has to drain the other lane
-    size_t lane_half = qs_level_bound<K>(n);
+    const size_t lane_half = qs_level_bound<K>(n);
     // early per-CTA recursion (param qs_early): the lists of every small
     // segment and all bin slots, indexed globally, after the two lane regions;
     // a batch runs on a third stream as soon as its segments are final
@@ -1978,15 +1978,11 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         const size_t hvB = HVL.stride * nh;
         const size_t need = al256(segB + goB + spB + hiB + hvB);
         if (need > lane_half) {
-            // a new layout [lane 0 | lane 1] would overlap the other lane's
-            // in-flight region: drain that lane first (a few times per sort,
-            // while the levels grow); reallocation itself synchronises too
-            Lane& O = lanes[1 - L.id];
-            if (O.inflight) {
-                e = cudaStreamSynchronize(O.st);
-                if (e != cudaSuccess) return cuda_fail(e, "quicksort lane drain");
-            }
-            lane_half = std::max(need, std::min<size_t>(al256(need + need / 4), qs_level_bound<K>(n)));
+            // impossible by construction (lane_half is the level bound: gtot <=
+            // G_TARGET + nmid, nmid <= n / (SMALL + 1) + 1, nh <= n / HEAVY + 1);
+            // growing the lanes would overlap the early-recursion lists in flight
+            set_error("quicksort: a level exceeds its workspace bound");
+            return PP_E_INVAL;
         }
         unsigned char* wsb = static_cast<unsigned char*>(qs_workspace(2 * lane_half));
         if (!wsb) return PP_E_NOMEM;
