@@ -71,8 +71,9 @@ PARTITION_PARAMS = [
 
 def test_fuzz_partition(pp):
     from gpu_util import to_dev, to_host
-    rng = np.random.default_rng(2004_12532)
-    for it in range(160):
+    import os
+    rng = np.random.default_rng(int(os.environ.get("PP_FUZZ_SEED", 2004_12532)))
+    for it in range(int(os.environ.get("PP_FUZZ_ITERS", 160))):
         dt, mx = ((np.uint64, U64_MAX) if rng.integers(0, 2) else (np.uint32, U32_MAX))
         n = int(rng.choice([rng.integers(0, 100), rng.integers(100, 70000), rng.integers(70000, 3_000_000)]))
         a, kind = _keys(rng, n, dt, mx)
