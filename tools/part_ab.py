@@ -39,10 +39,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c4", default="partitioned,all_false,all_true,reverse")
     ap.add_argument("--reps", type=int, default=15)
+    ap.add_argument("--params", default="", help="k=v,k=v library params")
     args = ap.parse_args()
     pp.load(build_if_missing=False)
+    for kv in filter(None, args.params.split(",")):
+        k, v = kv.split("=")
+        pp.pp_set_param(k, int(v))
     d = torch.zeros(1, dtype=torch.int64, device="cuda")
-    res = {"lib": os.environ.get("PP_LIB_PATH", "default")}
+    res = {"lib": os.environ.get("PP_LIB_PATH", "default"), "params": args.params}
     c2 = synth.uniform_u64_torch(1 << 27, synth.SEEDS["c2"], "cuda")
     res["c2"] = timed(lambda w: pp.pp_partition_async_u64(w, 1 << 63, d), c2, args.reps)
     del c2
