@@ -148,10 +148,16 @@ pp_status pp_quicksort(uint64_t *keys, uint64_t n);
  *   by key < pivot, then exchanges misplaced ranges so that the GLOBAL array
  *   is partitioned; *global_split_out = K = #keys < pivot over all ranks
  *   (HOST pointer).  The local step is pp_partition_*; then ncclAllGather of
- *   (n_r, t_r, pivot), a plan computed identically on every rank, and
+ *   (status, n_r, t_r, pivot), a plan computed identically on every rank, and
  *   ncclSend/ncclRecv rounds through a staging buffer of <= the staging size
  *   (default 256 MiB, pp_dist_set_staging).  Mismatched pivots or key types
  *   across ranks -> PP_E_INVAL on every rank.  Synchronises `stream`.
+ *   Failure handling: every rank agrees on the status before returning (a
+ *   local failure is reported by all ranks); the communicator is
+ *   non-blocking and every wait polls ncclCommGetAsyncError with a timeout
+ *   (param "dist_timeout_ms", default 600000): a dead or hung peer aborts the
+ *   communicator and returns PP_E_NCCL (pp_dist_finalize + pp_dist_init to
+ *   recover).
  * pp_dist_plan: the exchange plan alone (host arithmetic, no GPU): for shard
  *   sizes ns[P] and local splits ts[P], writes *n_out pieces of 6 uint64
  *   {round, rank_f, f, rank_t, t, len} (swap global [f, f+len) on rank_f with
@@ -179,6 +185,25 @@ pp_status pp_dist_last_timing(double *out4);
  * may differ.  Synchronises `stream`. */
 pp_status pp_quicksort_dist_u64(uint64_t *shard, uint64_t n_local, void *stream);
 pp_status pp_quicksort_dist_u32(uint32_t *shard, uint64_t n_local, void *stream);
+/* ---- loopback: the distributed calls with P emulated ranks on ONE GPU --------
+ * The multi-GPU algorithm above (local partition, record all-gather with
+ * status agreement, the same plan, staged send/recv rounds or the one-sided
+ * share rule with param "dist_p2p", the batched distributed quicksort) run
+ * by P host threads of this process, rank r owning the DEVICE slice
+ * keys[sum(ns[0..r-1]), + ns[r]) on its own stream.  Collectives rendezvous
+ * on a host barrier; every received piece is one cudaMemcpyAsync from the
+ * sender's range; local library calls are serialised (one workspace).  This
+ * is how the P > 1 code path is tested on a single GPU (PAPER.md:272-281:
+ * the global result must be a partition / the sort).  1 <= nranks <= 64;
+ * shards may be empty.  Synchronous.  Errors: the lowest-ranked failure is
+ * returned (every rank agrees); a rank that never arrives (test param
+ * "dist_fault" = 2) makes the others fail after "dist_timeout_ms". */
+pp_status pp_partition_dist_loopback_u64(uint64_t *keys, const uint64_t *ns, int nranks, uint64_t pivot,
+                                         uint64_t *global_split_out);
+pp_status pp_partition_dist_loopback_u32(uint32_t *keys, const uint64_t *ns, int nranks, uint32_t pivot,
+                                         uint64_t *global_split_out);
+pp_status pp_quicksort_dist_loopback_u64(uint64_t *keys, const uint64_t *ns, int nranks);
+pp_status pp_quicksort_dist_loopback_u32(uint32_t *keys, const uint64_t *ns, int nranks);
 pp_status pp_dist_plan(const uint64_t *ns, const uint64_t *ts, int nranks, uint64_t cap, uint64_t *out,
                        uint64_t out_cap, uint64_t *n_out, uint64_t *K_out);
 pp_status pp_dist_finalize(void);
@@ -270,7 +295,9 @@ pp_status pp_last_stats(uint64_t *out13);
  * 1 chain), "cleanup_bitmap", "qs_small", "qs_small_cfg", "qs_waves",
  * "qs_heavy", "qs_pipe", "qs_lanes" (0 auto = 2 lanes), "qs_early" (-1 auto
  * = on), "qs_early_min" (0 auto), "qs_minl" (0 auto: 128 KiB per group), "host_chunk",
- * "bps_nt", "dist_p2p".
+ * "bps_nt", "dist_p2p", "dist_timeout_ms", "dist_small" (distributed quicksort:
+ * spanning segments of <= this many keys are gathered and sorted locally),
+ * "dist_fault", "dist_fault_rank" (loopback test hooks).
  * Returns PP_E_INVAL for an unknown name.  pp_get_param returns INT64_MIN
  * for an unknown name. */
 pp_status pp_set_param(const char *name, int64_t value);

@@ -116,6 +116,10 @@ def load(build_if_missing: bool = True):
         "pp_ipc_import": ([vp, u64, ctypes.POINTER(ctypes.c_void_p)], st),
         "pp_ipc_close_all": ([], st),
         "pp_dist_last_timing": ([ctypes.POINTER(ctypes.c_double)], st),
+        "pp_partition_dist_loopback_u64": ([vp, P64, ctypes.c_int, u64, P64], st),
+        "pp_partition_dist_loopback_u32": ([vp, P64, ctypes.c_int, u32, P64], st),
+        "pp_quicksort_dist_loopback_u64": ([vp, P64, ctypes.c_int], st),
+        "pp_quicksort_dist_loopback_u32": ([vp, P64, ctypes.c_int], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -353,6 +357,35 @@ def pp_quicksort_dist(shard, stream=None) -> None:
     kind = _key_kind(shard)
     f = load().pp_quicksort_dist_u64 if kind == "u64" else load().pp_quicksort_dist_u32
     _check(f(shard.data_ptr(), shard.numel(), _stream_ptr(stream)), "pp_quicksort_dist")
+
+
+def _shard_sizes(keys, ns):
+    a = np.ascontiguousarray(np.asarray(ns, dtype=np.uint64))
+    if int(a.sum()) != keys.numel():
+        raise ValueError(f"shard sizes sum to {int(a.sum())}, keys has {keys.numel()}")
+    return a
+
+
+def pp_partition_dist_loopback(keys, ns, pivot: int) -> int:
+    """The distributed partition with len(ns) emulated ranks on this GPU
+    (rank r owns keys[sum(ns[:r]) : + ns[r]]); returns the global split."""
+    kind = _key_kind(keys)
+    a = _shard_sizes(keys, ns)
+    out = ctypes.c_uint64(0)
+    P64 = ctypes.POINTER(ctypes.c_uint64)
+    f = load().pp_partition_dist_loopback_u64 if kind == "u64" else load().pp_partition_dist_loopback_u32
+    _check(f(keys.data_ptr(), a.ctypes.data_as(P64), len(a), _pivot(pivot, kind), ctypes.byref(out)),
+           "pp_partition_dist_loopback")
+    return int(out.value)
+
+
+def pp_quicksort_dist_loopback(keys, ns) -> None:
+    """The distributed quicksort with len(ns) emulated ranks on this GPU."""
+    kind = _key_kind(keys)
+    a = _shard_sizes(keys, ns)
+    P64 = ctypes.POINTER(ctypes.c_uint64)
+    f = load().pp_quicksort_dist_loopback_u64 if kind == "u64" else load().pp_quicksort_dist_loopback_u32
+    _check(f(keys.data_ptr(), a.ctypes.data_as(P64), len(a)), "pp_quicksort_dist_loopback")
 
 
 def pp_dist_set_staging(nbytes: int) -> None:

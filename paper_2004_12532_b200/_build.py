@@ -5,6 +5,7 @@ from __future__ import annotations
 import glob
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -50,15 +51,31 @@ def nccl_paths():
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every .cu to an object in parallel (one nvcc per source; no
+    device code crosses translation units), then link libpp.so."""
     if not force and up_to_date():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
     nccl_inc, nccl_lib = nccl_paths()
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", nccl_inc,
-           f'-DPP_NCCL_LIB="{nccl_lib}"', "-o", LIB + ".tmp", *sources(), "-ldl"]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    common = [nvcc, *NVCC_FLAGS[:-1], "-I", os.path.join(ROOT, "include"), "-I", nccl_inc,
+              f'-DPP_NCCL_LIB="{nccl_lib}"']
+    jobs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        jobs.append((obj, common + ["-c", "-o", obj, src]))
+
+    def run(cmd):
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        list(ex.map(run, [c for _, c in jobs]))
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp",
+            *[o for o, _ in jobs], "-ldl"]
+    run(link)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

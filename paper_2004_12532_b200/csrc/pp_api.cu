@@ -18,6 +18,7 @@ void timing_enable(int on);
 int timing_read(double* out);
 
 static std::mutex g_mu;
+static std::mutex g_err_mu;  // set_error may run on the loopback's rank threads
 static std::string g_err;
 static Params g_params;
 static LastStats g_stats;
@@ -26,7 +27,10 @@ static Ctl* g_last_ctl = nullptr;
 Params& params() { return g_params; }
 LastStats& last_stats() { return g_stats; }
 
-void set_error(const std::string& msg) { g_err = msg; }
+void set_error(const std::string& msg) {
+    std::lock_guard<std::mutex> lk(g_err_mu);
+    g_err = msg;
+}
 pp_status cuda_fail(cudaError_t e, const char* what) {
     set_error(std::string(what) + ": " + cudaGetErrorString(e));
     return PP_E_CUDA;
@@ -566,13 +570,47 @@ pp_status pp_quicksort_dist_u64(uint64_t* shard, uint64_t n_local, void* stream)
     std::lock_guard<std::mutex> lk(g_mu);
     pp_status s = check_device_keys(shard, n_local);
     if (s != PP_OK) return s;
-    return quicksort_dist<uint64_t>(shard, n_local, (cudaStream_t)stream, 1u << 16);
+    return quicksort_dist<uint64_t>(shard, n_local, (cudaStream_t)stream, (uint64_t)g_params.dist_small);
 }
 pp_status pp_quicksort_dist_u32(uint32_t* shard, uint64_t n_local, void* stream) {
     std::lock_guard<std::mutex> lk(g_mu);
     pp_status s = check_device_keys(shard, n_local);
     if (s != PP_OK) return s;
-    return quicksort_dist<uint32_t>(shard, n_local, (cudaStream_t)stream, 1u << 16);
+    return quicksort_dist<uint32_t>(shard, n_local, (cudaStream_t)stream, (uint64_t)g_params.dist_small);
+}
+pp_status pp_partition_dist_loopback_u64(uint64_t* keys, const uint64_t* ns, int nranks, uint64_t pivot,
+                                         uint64_t* global_split_out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    uint64_t n = 0;
+    for (int r = 0; ns && r < nranks; ++r) n += ns[r];
+    pp_status s = check_device_keys(keys, n);
+    if (s != PP_OK) return s;
+    return partition_dist_loopback<uint64_t>(keys, ns, nranks, pivot, global_split_out);
+}
+pp_status pp_partition_dist_loopback_u32(uint32_t* keys, const uint64_t* ns, int nranks, uint32_t pivot,
+                                         uint64_t* global_split_out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    uint64_t n = 0;
+    for (int r = 0; ns && r < nranks; ++r) n += ns[r];
+    pp_status s = check_device_keys(keys, n);
+    if (s != PP_OK) return s;
+    return partition_dist_loopback<uint32_t>(keys, ns, nranks, pivot, global_split_out);
+}
+pp_status pp_quicksort_dist_loopback_u64(uint64_t* keys, const uint64_t* ns, int nranks) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    uint64_t n = 0;
+    for (int r = 0; ns && r < nranks; ++r) n += ns[r];
+    pp_status s = check_device_keys(keys, n);
+    if (s != PP_OK) return s;
+    return quicksort_dist_loopback<uint64_t>(keys, ns, nranks, (uint64_t)g_params.dist_small);
+}
+pp_status pp_quicksort_dist_loopback_u32(uint32_t* keys, const uint64_t* ns, int nranks) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    uint64_t n = 0;
+    for (int r = 0; ns && r < nranks; ++r) n += ns[r];
+    pp_status s = check_device_keys(keys, n);
+    if (s != PP_OK) return s;
+    return quicksort_dist_loopback<uint32_t>(keys, ns, nranks, (uint64_t)g_params.dist_small);
 }
 pp_status pp_dist_plan(const uint64_t* ns, const uint64_t* ts, int nranks, uint64_t cap, uint64_t* out,
                        uint64_t out_cap, uint64_t* n_out, uint64_t* K_out) {
@@ -680,6 +718,10 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "host_chunk") P.host_chunk = value;
     else if (k == "qs_pipe") P.qs_pipe = value;
     else if (k == "dist_p2p") P.dist_p2p = value ? 1 : 0;
+    else if (k == "dist_timeout_ms") P.dist_timeout_ms = value < 1 ? 1 : value;
+    else if (k == "dist_fault") P.dist_fault = value;
+    else if (k == "dist_fault_rank") P.dist_fault_rank = value;
+    else if (k == "dist_small") P.dist_small = value < 1 ? 1 : value;
     else if (k == "qs_lanes") P.qs_lanes = value;
     else if (k == "qs_early") P.qs_early = value;
     else if (k == "qs_early_min") P.qs_early_min = value;
@@ -719,6 +761,10 @@ int64_t pp_get_param(const char* name) {
     if (k == "host_chunk") return P.host_chunk;
     if (k == "qs_pipe") return P.qs_pipe;
     if (k == "dist_p2p") return P.dist_p2p;
+    if (k == "dist_timeout_ms") return P.dist_timeout_ms;
+    if (k == "dist_fault") return P.dist_fault;
+    if (k == "dist_fault_rank") return P.dist_fault_rank;
+    if (k == "dist_small") return P.dist_small;
     if (k == "qs_lanes") return P.qs_lanes;
     if (k == "qs_early") return P.qs_early;
     if (k == "qs_early_min") return P.qs_early_min;

@@ -1,15 +1,37 @@
-// pp_dist.cu -- multi-GPU partition of one array sharded contiguously over
-// ranks (BASELINE config 3): local partition on every
-// rank, ncclAllGather of (n_r, t_r, pivot), identical exchange plan on every
-// rank, and ncclSend/ncclRecv of matched misplaced ranges through a bounded
-// staging buffer.  NCCL is loaded at run time (dlopen) -- preferably the copy
-// already loaded by PyTorch in this process -- so libpp.so has no link-time
-// NCCL dependency and two NCCLs never end up in one process.
+// pp_dist.cu -- multi-GPU partition and quicksort of one array sharded
+// contiguously over ranks (BASELINE config 3 / config 5 at P GPUs; SURVEY
+// §8(a) a8, §8(e)).  A rank partitions its shard(s) locally with the
+// single-GPU kernels, all-gathers (status, n_r, t_r, pivot) once, computes the
+// exchange plan identically on every rank (a merge of the misplaced-successor
+// ranges left of K with the misplaced-predecessor ranges right of K), and
+// moves the matched ranges either through bounded staging (grouped
+// send/recv rounds) or one-sidedly through peer mappings (param dist_p2p).
+//
+// The algorithm is written once against a Transport:
+//   * NcclTransport -- the product path: NCCL (loaded at run time, the copy
+//     PyTorch already loaded) with a NON-BLOCKING communicator; every wait
+//     polls the stream and ncclCommGetAsyncError with a timeout and aborts the
+//     communicator on failure, so a dead peer turns into PP_E_NCCL instead of
+//     a hang.  Peer mappings through CUDA IPC.
+//   * LoopTransport -- P emulated ranks as host threads of one process on one
+//     GPU (disjoint slices of one device array): collectives rendezvous on a
+//     host barrier and every received piece is ONE plain cudaMemcpyAsync from
+//     the sender's range.  This runs the same plan -> rounds -> staging ->
+//     place code (and the one-sided share rule) at P > 1 on a single GPU
+//     (pp_*_dist_loopback_*; tests/test_gpu_dist.py).
+// Every collective call agrees on a status before it returns: a rank that
+// fails locally still takes part in the next all-gather with its status set,
+// and every rank returns the same error.
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda.h>  // driver types only (cuMemGetAddressRange is fetched through the runtime)
@@ -23,17 +45,19 @@ void note_launches(uint64_t k);
 
 // ---------------------------------------------------------------------------
 // The exchange plan (host arithmetic; mirrored independently in Python by
-// paper_2004_12532_b200/dist.py and cross-checked by tests/test_dist.py).
+// tests/dist_mirror.py and cross-checked by tests/test_dist.py).
 // ---------------------------------------------------------------------------
+struct Run {  // swap [a, a+len) on rank ra (misplaced successors) with [b, b+len) on rank rb (predecessors)
+    uint64_t ra, a, rb, b, len;
+};
 struct Piece {
     uint64_t round, rank_f, f, rank_t, t, len;
 };
 
 // Pairs the i-th misplaced successor (global order, left of K) with the i-th
-// misplaced predecessor (right of K); splits transfers into pieces <= cap and
-// groups them into rounds where no rank moves more than cap keys.
-static uint64_t plan_pieces(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap,
-                            std::vector<Piece>& out) {
+// misplaced predecessor (right of K): one run per maximal matched stretch.
+// Positions are global (shard base of rank r = sum of ns[<r]).
+static uint64_t match_runs(const uint64_t* ns, const uint64_t* ts, int P, std::vector<Run>& out) {
     uint64_t K = 0;
     for (int r = 0; r < P; ++r) K += ts[r];
     struct Iv {
@@ -50,24 +74,10 @@ static uint64_t plan_pieces(const uint64_t* ns, const uint64_t* ts, int P, uint6
         base += n;
     }
     out.clear();
-    std::vector<uint64_t> used(P, 0);
-    uint64_t round = 0;
     size_t i = 0, j = 0;
     while (i < F.size() && j < T.size()) {
         const uint64_t m = std::min(F[i].e - F[i].s, T[j].e - T[j].s);
-        // split into pieces of <= cap, each placed in the current or a new round
-        uint64_t s = 0;
-        while (s < m) {
-            const uint64_t len = std::min(cap, m - s);
-            if (used[F[i].rank] + len > cap || used[T[j].rank] + len > cap) {
-                ++round;
-                std::fill(used.begin(), used.end(), 0);
-            }
-            out.push_back({round, F[i].rank, F[i].s + s, T[j].rank, T[j].s + s, len});
-            used[F[i].rank] += len;
-            used[T[j].rank] += len;
-            s += len;
-        }
+        out.push_back({F[i].rank, F[i].s, T[j].rank, T[j].s, m});
         F[i].s += m;
         T[j].s += m;
         if (F[i].s == F[i].e) ++i;
@@ -76,28 +86,48 @@ static uint64_t plan_pieces(const uint64_t* ns, const uint64_t* ts, int P, uint6
     return K;
 }
 
-// One-sided (staging-free) exchange: who executes which pairs.  The plan
-// with no staging cap has one piece per matched run (the left rank's
-// misplaced successors [f, f+len) against the right rank's misplaced
-// predecessors [t, t+len); the two ranks always differ, because a shard's
-// misplaced keys are all successors (shard ends left of K) or all
-// predecessors).  The left rank swaps the first ceil(len/2) pairs, the right
-// rank the rest, each reading and writing its partner's keys through the
-// peer mapping, so both directions of every NVLink pair carry traffic.
-// Mirrored by paper_2004_12532_b200/dist.py p2p_pieces (tests/test_dist.py).
-struct P2PPiece {
-    uint64_t rank_a, a, rank_b, b, len;
-};
-static uint64_t p2p_pieces(const uint64_t* ns, const uint64_t* ts, int P, int me, std::vector<P2PPiece>& out) {
-    std::vector<Piece> pcs;
-    const uint64_t K = plan_pieces(ns, ts, P, ~0ull, pcs);
+// Splits runs into pieces of <= cap keys and groups them into rounds in which
+// no rank moves more than cap keys (a piece opens a new round when either of
+// its ranks would exceed cap).  Identical on every rank.
+static void schedule_rounds(const std::vector<Run>& runs, int P, uint64_t cap, std::vector<Piece>& out) {
     out.clear();
-    for (const Piece& p : pcs) {
-        const uint64_t h = (p.len + 1) / 2;
-        if ((int)p.rank_f == me) out.push_back({p.rank_f, p.f, p.rank_t, p.t, h});
-        if ((int)p.rank_t == me && p.len > h) out.push_back({p.rank_f, p.f + h, p.rank_t, p.t + h, p.len - h});
+    std::vector<uint64_t> used(P, 0);
+    uint64_t round = 0;
+    for (const Run& r : runs) {
+        for (uint64_t s = 0; s < r.len;) {
+            const uint64_t len = std::min(cap, r.len - s);
+            if (used[r.ra] + len > cap || used[r.rb] + len > cap) {
+                ++round;
+                std::fill(used.begin(), used.end(), 0);
+            }
+            out.push_back({round, r.ra, r.a + s, r.rb, r.b + s, len});
+            used[r.ra] += len;
+            used[r.rb] += len;
+            s += len;
+        }
     }
+}
+
+static uint64_t plan_pieces(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap, std::vector<Piece>& out) {
+    std::vector<Run> runs;
+    const uint64_t K = match_runs(ns, ts, P, runs);
+    schedule_rounds(runs, P, cap, out);
     return K;
+}
+
+// One-sided (staging-free) exchange: who executes which pairs.  Every run
+// has its two ranks distinct (a shard's misplaced keys are all successors --
+// it ends left of K -- or all predecessors).  The left rank swaps the first
+// ceil(len/2) pairs, the right rank the rest, each reading and writing its
+// partner's keys through the peer mapping, so both directions of every link
+// carry traffic.  Mirrored by tests/dist_mirror.py p2p_pieces.
+static void p2p_share(const std::vector<Run>& runs, int me, std::vector<Run>& out) {
+    out.clear();
+    for (const Run& p : runs) {
+        const uint64_t h = (p.len + 1) / 2;
+        if ((int)p.ra == me) out.push_back({p.ra, p.a, p.rb, p.b, h});
+        if ((int)p.rb == me && p.len > h) out.push_back({p.ra, p.a + h, p.rb, p.b + h, p.len - h});
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -176,13 +206,42 @@ pp_status ipc_close_all() {
 }
 
 // ---------------------------------------------------------------------------
+// Transport interface.
+// ---------------------------------------------------------------------------
+static constexpr int kPeerWords = 9;  // exported peer record (after the status word)
+
+struct Transport {
+    int P = 1, me = 0;
+    virtual ~Transport() = default;
+    // all-gather `bytes` per rank: device d_send -> device d_recv[P * bytes]
+    virtual pp_status allgather(const void* d_send, void* d_recv, size_t bytes, cudaStream_t st) = 0;
+    // grouped point-to-point; matched per (src, dst) pair in issue order
+    virtual pp_status group_start() = 0;
+    virtual pp_status send(const void* d, size_t bytes, int peer, cudaStream_t st) = 0;
+    virtual pp_status recv(void* d, size_t bytes, int peer, cudaStream_t st) = 0;
+    virtual pp_status group_end(cudaStream_t st) = 0;
+    // wait for everything enqueued on st, detecting peer failures
+    virtual pp_status wait(cudaStream_t st) = 0;
+    // one-sided exchange: describe a local device range / map a peer's
+    virtual pp_status export_range(void* d, uint64_t* rec) = 0;
+    virtual pp_status import_range(const uint64_t* rec, void** d) = 0;
+    // local library calls (the loopback serialises them: one process-wide workspace)
+    virtual void local_begin() {}
+    virtual pp_status local_end(cudaStream_t) { return PP_OK; }
+    // test hooks (loopback only): a rank that never arrives
+    virtual bool absent() const { return false; }
+};
+
+// ---------------------------------------------------------------------------
 // NCCL, loaded at run time.
 // ---------------------------------------------------------------------------
 struct NcclApi {
     void* lib = nullptr;
     decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
-    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommInitRankConfig) CommInitRankConfig = nullptr;
     decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclCommAbort) CommAbort = nullptr;
+    decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
     decltype(&ncclAllGather) AllGather = nullptr;
     decltype(&ncclSend) Send = nullptr;
     decltype(&ncclRecv) Recv = nullptr;
@@ -212,8 +271,10 @@ static bool nccl_load() {
         return false;                                                    \
     }
     PP_SYM(GetUniqueId, "ncclGetUniqueId")
-    PP_SYM(CommInitRank, "ncclCommInitRank")
+    PP_SYM(CommInitRankConfig, "ncclCommInitRankConfig")
     PP_SYM(CommDestroy, "ncclCommDestroy")
+    PP_SYM(CommAbort, "ncclCommAbort")
+    PP_SYM(CommGetAsyncError, "ncclCommGetAsyncError")
     PP_SYM(AllGather, "ncclAllGather")
     PP_SYM(Send, "ncclSend")
     PP_SYM(Recv, "ncclRecv")
@@ -225,32 +286,257 @@ static bool nccl_load() {
     return true;
 }
 
-static pp_status nccl_fail(ncclResult_t r, const char* what) {
-    set_error(std::string(what) + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error"));
-    return PP_E_NCCL;
+static double now_ms() {
+    using namespace std::chrono;
+    return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
 
-struct DistState {
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, local done, gathered, exchanged
-    double last_local_ms = 0, last_gather_ms = 0, last_exchange_ms = 0;
-    uint64_t last_bytes = 0;  // bytes this rank moved between GPUs in the last exchange
+struct NcclTransport : Transport {
     ncclComm_t comm = nullptr;
-    int nranks = 0, rank = 0, device = 0;
+    bool dead = false;
+
+    pp_status fail(const std::string& what) {
+        if (comm && !dead) g_nccl.CommAbort(comm);  // unblocks kernels waiting on a dead peer
+        dead = true;
+        set_error(what);
+        return PP_E_NCCL;
+    }
+    // Non-blocking communicator: a call may return ncclInProgress; poll the
+    // communicator's async state until it settles, with a timeout.
+    pp_status settle(ncclResult_t r, const char* what) {
+        if (dead) return fail(std::string(what) + ": communicator aborted earlier");
+        const double t0 = now_ms(), lim = (double)params().dist_timeout_ms;
+        while (r == ncclInProgress) {
+            if (now_ms() - t0 > lim) return fail(std::string(what) + ": timed out (dist_timeout_ms)");
+            std::this_thread::yield();
+            ncclResult_t a = ncclSuccess;
+            g_nccl.CommGetAsyncError(comm, &a);
+            r = a;
+        }
+        if (r != ncclSuccess) return fail(std::string(what) + ": " + g_nccl.GetErrorString(r));
+        return PP_OK;
+    }
+    pp_status allgather(const void* d_send, void* d_recv, size_t bytes, cudaStream_t st) override {
+        return settle(g_nccl.AllGather(d_send, d_recv, bytes, ncclUint8, comm, st), "ncclAllGather");
+    }
+    pp_status group_start() override { return settle(g_nccl.GroupStart(), "ncclGroupStart"); }
+    pp_status send(const void* d, size_t bytes, int peer, cudaStream_t st) override {
+        return settle(g_nccl.Send(d, bytes, ncclUint8, peer, comm, st), "ncclSend");
+    }
+    pp_status recv(void* d, size_t bytes, int peer, cudaStream_t st) override {
+        return settle(g_nccl.Recv(d, bytes, ncclUint8, peer, comm, st), "ncclRecv");
+    }
+    pp_status group_end(cudaStream_t) override { return settle(g_nccl.GroupEnd(), "ncclGroupEnd"); }
+    // stream completion polled together with the communicator's async error
+    // (a failed or vanished peer), bounded by dist_timeout_ms
+    pp_status wait(cudaStream_t st) override {
+        if (dead) return fail("communicator aborted earlier");
+        const double t0 = now_ms(), lim = (double)params().dist_timeout_ms;
+        for (;;) {
+            cudaError_t e = cudaStreamQuery(st);
+            if (e == cudaSuccess) return PP_OK;
+            if (e != cudaErrorNotReady) return cuda_fail(e, "dist stream");
+            ncclResult_t a = ncclSuccess;
+            g_nccl.CommGetAsyncError(comm, &a);
+            if (a != ncclSuccess && a != ncclInProgress)
+                return fail(std::string("NCCL async error: ") + g_nccl.GetErrorString(a));
+            if (now_ms() - t0 > lim) return fail("dist wait timed out (dist_timeout_ms); communicator aborted");
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+    }
+    pp_status export_range(void* d, uint64_t* rec) override {
+        std::memset(rec, 0, 8 * kPeerWords);
+        return d ? ipc_export(d, rec, &rec[8]) : PP_OK;
+    }
+    pp_status import_range(const uint64_t* rec, void** d) override { return ipc_import(rec, rec[8], d); }
+};
+
+// ---------------------------------------------------------------------------
+// Loopback: P emulated ranks = P host threads of this process, one GPU.
+// ---------------------------------------------------------------------------
+struct LoopHub {
+    int P = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    bool broken = false;
+    std::vector<const void*> slot;                               // per rank: all-gather source
+    std::vector<std::deque<std::pair<const void*, size_t>>> box;  // [src * P + dst]: posted sends, FIFO
+    std::mutex local_mu;                                         // serialises local library calls
+
+    explicit LoopHub(int p) : P(p), slot(p, nullptr), box((size_t)p * p) {}
+
+    pp_status barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (broken) return PP_E_NCCL;
+        const uint64_t g = gen;
+        if (++arrived == P) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+            return PP_OK;
+        }
+        const auto lim = std::chrono::milliseconds(params().dist_timeout_ms);
+        if (!cv.wait_for(lk, lim, [&] { return gen != g || broken; })) {
+            broken = true;  // a rank never arrived: every waiting and later rank fails
+            cv.notify_all();
+        }
+        if (gen != g) return PP_OK;
+        set_error("loopback rendezvous timed out (a rank did not arrive; dist_timeout_ms)");
+        return PP_E_NCCL;
+    }
+};
+
+struct LoopTransport : Transport {
+    LoopHub* hub = nullptr;
+    bool absent_ = false;
+    struct Pend {
+        int peer;
+        const void* src;
+        void* dst;
+        size_t bytes;
+    };
+    std::vector<Pend> sends, recvs;
+
+    pp_status allgather(const void* d_send, void* d_recv, size_t bytes, cudaStream_t st) override {
+        pp_status s = wait(st);  // the source is ready
+        if (s != PP_OK) return s;
+        {
+            std::lock_guard<std::mutex> lk(hub->mu);
+            hub->slot[me] = d_send;
+        }
+        if ((s = hub->barrier()) != PP_OK) return s;
+        for (int q = 0; q < P; ++q) {
+            const void* src;
+            {
+                std::lock_guard<std::mutex> lk(hub->mu);
+                src = hub->slot[q];
+            }
+            cudaError_t e = cudaMemcpyAsync(static_cast<char*>(d_recv) + bytes * q, src, bytes,
+                                            cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "loopback all-gather copy");
+        }
+        if ((s = wait(st)) != PP_OK) return s;
+        return hub->barrier();  // no rank reuses its source before every peer copied it
+    }
+    pp_status group_start() override {
+        sends.clear();
+        recvs.clear();
+        return PP_OK;
+    }
+    pp_status send(const void* d, size_t bytes, int peer, cudaStream_t) override {
+        sends.push_back({peer, d, nullptr, bytes});
+        return PP_OK;
+    }
+    pp_status recv(void* d, size_t bytes, int peer, cudaStream_t) override {
+        recvs.push_back({peer, nullptr, d, bytes});
+        return PP_OK;
+    }
+    pp_status group_end(cudaStream_t st) override {
+        pp_status s = wait(st);
+        if (s != PP_OK) return s;
+        {
+            std::lock_guard<std::mutex> lk(hub->mu);
+            for (const Pend& p : sends) hub->box[(size_t)me * P + p.peer].push_back({p.src, p.bytes});
+        }
+        if ((s = hub->barrier()) != PP_OK) return s;
+        for (const Pend& p : recvs) {  // one plain copy per received piece, from the sender's range
+            std::pair<const void*, size_t> m{nullptr, 0};
+            {
+                std::lock_guard<std::mutex> lk(hub->mu);
+                auto& q = hub->box[(size_t)p.peer * P + me];
+                if (!q.empty()) {
+                    m = q.front();
+                    q.pop_front();
+                }
+            }
+            if (!m.first || m.second != p.bytes) {
+                set_error("loopback: unmatched send/recv (plan differs between ranks)");
+                return PP_E_INTERNAL;
+            }
+            cudaError_t e = cudaMemcpyAsync(p.dst, m.first, p.bytes, cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "loopback piece copy");
+        }
+        sends.clear();
+        recvs.clear();
+        if ((s = wait(st)) != PP_OK) return s;
+        return hub->barrier();  // senders keep their ranges until every receiver copied them
+    }
+    pp_status wait(cudaStream_t st) override {
+        cudaError_t e = cudaStreamSynchronize(st);
+        return e == cudaSuccess ? PP_OK : cuda_fail(e, "loopback stream");
+    }
+    pp_status export_range(void* d, uint64_t* rec) override {
+        std::memset(rec, 0, 8 * kPeerWords);
+        rec[0] = reinterpret_cast<uint64_t>(d);  // same process: the address itself
+        return PP_OK;
+    }
+    pp_status import_range(const uint64_t* rec, void** d) override {
+        *d = reinterpret_cast<void*>(rec[0]);
+        return PP_OK;
+    }
+    void local_begin() override { hub->local_mu.lock(); }
+    pp_status local_end(cudaStream_t st) override {
+        pp_status s = wait(st);  // the shared workspace is free for the next emulated rank
+        hub->local_mu.unlock();
+        return s;
+    }
+    bool absent() const override { return absent_; }
+};
+
+// ---------------------------------------------------------------------------
+// Per-rank context (one in the NCCL process; one per thread in the loopback).
+// ---------------------------------------------------------------------------
+struct DistCtx {
+    Transport* tp = nullptr;
+    int P = 1, me = 0, device = 0;
     void* staging = nullptr;
     size_t staging_bytes = 0;
-    uint64_t* d_info = nullptr;  // [P][4] gathered (n, t, pivot, key_bytes)
-    uint64_t* d_ag = nullptr;    // all-gather scratch (grown on demand, freed at finalize)
+    uint64_t* d_ag = nullptr;  // all-gather scratch (words)
     size_t d_ag_words = 0;
-    uint64_t staging_cap_bytes = 256ull << 20;
+    void* gs = nullptr;  // gather-sort scratch
+    size_t gs_bytes = 0;
+    uint64_t* d_swap = nullptr;  // one-sided swap piece table
+    size_t d_swap_words = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, local done, gathered, exchanged
+    double last_local_ms = 0, last_gather_ms = 0, last_exchange_ms = 0;
+    uint64_t last_bytes = 0;
+
+    pp_status init_events() {
+        for (auto& e : ev)
+            if (!e && cudaEventCreate(&e) != cudaSuccess) return cuda_fail(cudaGetLastError(), "event");
+        return PP_OK;
+    }
+    void release() {
+        for (auto& e : ev)
+            if (e) {
+                cudaEventDestroy(e);
+                e = nullptr;
+            }
+        if (staging) cudaFree(staging);
+        if (d_ag) cudaFree(d_ag);
+        if (gs) cudaFree(gs);
+        if (d_swap) cudaFree(d_swap);
+        staging = gs = nullptr;
+        d_ag = d_swap = nullptr;
+        staging_bytes = gs_bytes = d_ag_words = d_swap_words = 0;
+    }
 };
-static DistState g_dist;
+
+static NcclTransport g_nccl_tp;
+static DistCtx g_ctx;
+static uint64_t g_staging_cap_bytes = 256ull << 20;
 
 pp_status dist_unique_id(void* out128) {
     if (!out128) return PP_E_INVAL;
     if (!nccl_load()) return PP_E_NCCL;
     ncclUniqueId id;
     ncclResult_t r = g_nccl.GetUniqueId(&id);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    if (r != ncclSuccess) {
+        set_error(std::string("ncclGetUniqueId: ") + g_nccl.GetErrorString(r));
+        return PP_E_NCCL;
+    }
     static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
     memcpy(out128, &id, 128);
     return PP_OK;
@@ -262,7 +548,7 @@ pp_status dist_init(const void* id128, int nranks, int rank, int device) {
         return PP_E_INVAL;
     }
     if (!nccl_load()) return PP_E_NCCL;
-    if (g_dist.comm) {
+    if (g_ctx.tp) {
         set_error("pp_dist_init: already initialised (call pp_dist_finalize first)");
         return PP_E_INVAL;
     }
@@ -270,421 +556,124 @@ pp_status dist_init(const void* id128, int nranks, int rank, int device) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
     ncclUniqueId id;
     memcpy(&id, id128, 128);
-    ncclResult_t r = g_nccl.CommInitRank(&g_dist.comm, nranks, id, rank);
-    if (r != ncclSuccess) {
-        g_dist.comm = nullptr;
-        return nccl_fail(r, "ncclCommInitRank");
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;  // every call returns; waits poll with a timeout (NcclTransport::settle / wait)
+    g_nccl_tp = NcclTransport();
+    ncclResult_t r = g_nccl.CommInitRankConfig(&g_nccl_tp.comm, nranks, id, rank, &cfg);
+    if (r != ncclSuccess && r != ncclInProgress) {
+        g_nccl_tp.comm = nullptr;
+        set_error(std::string("ncclCommInitRankConfig: ") + g_nccl.GetErrorString(r));
+        return PP_E_NCCL;
     }
-    g_dist.nranks = nranks;
-    g_dist.rank = rank;
-    g_dist.device = device;
-    e = cudaMalloc(&g_dist.d_info, sizeof(uint64_t) * 4 * (nranks + 1));
-    if (e != cudaSuccess) return cuda_fail(e, "dist info alloc");
-    for (auto& ev : g_dist.ev)
-        if (!ev) cudaEventCreate(&ev);
-    return PP_OK;
+    if (g_nccl_tp.settle(r, "ncclCommInitRankConfig") != PP_OK) {
+        g_nccl_tp.comm = nullptr;
+        return PP_E_NCCL;
+    }
+    g_nccl_tp.P = nranks;
+    g_nccl_tp.me = rank;
+    g_ctx = DistCtx();
+    g_ctx.tp = &g_nccl_tp;
+    g_ctx.P = nranks;
+    g_ctx.me = rank;
+    g_ctx.device = device;
+    return g_ctx.init_events();
 }
 
 pp_status dist_last_timing(double* out4) {
     if (!out4) return PP_E_INVAL;
-    out4[0] = g_dist.last_local_ms;
-    out4[1] = g_dist.last_gather_ms;
-    out4[2] = g_dist.last_exchange_ms;
-    out4[3] = (double)g_dist.last_bytes;
+    out4[0] = g_ctx.last_local_ms;
+    out4[1] = g_ctx.last_gather_ms;
+    out4[2] = g_ctx.last_exchange_ms;
+    out4[3] = (double)g_ctx.last_bytes;
     return PP_OK;
-}
-
-// phase times of the call that just synchronised (events on its stream)
-static void dist_read_timing(uint64_t bytes) {
-    float a = 0, b = 0, c = 0;
-    cudaEventElapsedTime(&a, g_dist.ev[0], g_dist.ev[1]);
-    cudaEventElapsedTime(&b, g_dist.ev[1], g_dist.ev[2]);
-    cudaEventElapsedTime(&c, g_dist.ev[2], g_dist.ev[3]);
-    g_dist.last_local_ms = a;
-    g_dist.last_gather_ms = b;
-    g_dist.last_exchange_ms = c;
-    g_dist.last_bytes = bytes;
 }
 
 pp_status dist_finalize() {
     ipc_close_all();
-    for (auto& ev : g_dist.ev)
-        if (ev) {
-            cudaEventDestroy(ev);
-            ev = nullptr;
-        }
-    if (g_dist.comm) g_nccl.CommDestroy(g_dist.comm);
-    g_dist.comm = nullptr;
-    if (g_dist.staging) cudaFree(g_dist.staging);
-    if (g_dist.d_info) cudaFree(g_dist.d_info);
-    if (g_dist.d_ag) cudaFree(g_dist.d_ag);
-    g_dist.staging = nullptr;
-    g_dist.d_info = nullptr;
-    g_dist.d_ag = nullptr;
-    g_dist.d_ag_words = 0;
-    g_dist.staging_bytes = 0;
+    g_ctx.release();
+    if (g_nccl_tp.comm) {
+        if (g_nccl_tp.dead)
+            ;  // aborted already (CommAbort frees it)
+        else
+            g_nccl.CommDestroy(g_nccl_tp.comm);
+    }
+    g_nccl_tp = NcclTransport();
+    g_ctx = DistCtx();
     return PP_OK;
 }
 
-void dist_set_staging(uint64_t bytes) { g_dist.staging_cap_bytes = bytes < 16 ? 16 : bytes; }
+void dist_set_staging(uint64_t bytes) { g_staging_cap_bytes = bytes < 16 ? 16 : bytes; }
 
-static pp_status allgather_u64(const uint64_t* host_in, uint64_t count, std::vector<uint64_t>& host_out,
-                               cudaStream_t st);
-template <typename K>
-static pp_status swap_ranges_impl(const uint64_t* host_tri, uint64_t np, cudaStream_t st, bool sys_fence);
-
-// The exchange one-sidedly over CUDA-IPC peer mappings (param dist_p2p):
-// every rank's shard is mapped on every rank (handles + offsets gathered
-// once per call, mappings cached), each rank swaps its share of the pairs
-// (p2p_pieces) with swap_ranges_kernel directly between its shard and the
-// peers' -- no staging buffer, no second copy -- and a final collective keeps
-// any rank from returning while a peer may still be writing into its shard.
-// Ordering: a rank's swaps are enqueued after the (n_r, t_r) all-gather, which
-// completes only once every rank has contributed, i.e. after every rank's
-// local partition finished (stream order).  Needs peer access between the
-// GPUs (NVLink / NVSwitch); untested here beyond one GPU.
-template <typename K>
-static pp_status exchange_p2p(K* shard, uint64_t n_local, const std::vector<uint64_t>& ns,
-                              const std::vector<uint64_t>& ts, cudaStream_t st, uint64_t* moved) {
-    const int P = g_dist.nranks, me = g_dist.rank;
-    std::vector<uint64_t> mine(9, 0), all;
-    if (n_local > 0) {
-        pp_status s = ipc_export(shard, mine.data(), &mine[8]);
-        if (s != PP_OK) return s;
-    }
-    pp_status s = allgather_u64(mine.data(), 9, all, st);
-    if (s != PP_OK) return s;
-    std::vector<P2PPiece> pcs;
-    p2p_pieces(ns.data(), ts.data(), P, me, pcs);
-    std::vector<uint64_t> bases(P, 0);
-    for (int q = 1; q < P; ++q) bases[q] = bases[q - 1] + ns[q - 1];
-    std::vector<K*> ptr(P, nullptr);
-    ptr[me] = shard;
-    for (const P2PPiece& p : pcs) {
-        for (uint64_t q : {p.rank_a, p.rank_b}) {
-            if (ptr[q]) continue;
-            void* d = nullptr;
-            s = ipc_import(&all[9 * q], all[9 * q + 8], &d);
-            if (s != PP_OK) return s;
-            ptr[q] = static_cast<K*>(d);
-        }
-    }
-    std::vector<uint64_t> tri;
-    *moved = 0;  // remote bytes read + written by this rank's swaps
-    for (const P2PPiece& p : pcs) {
-        *moved += 2 * p.len * sizeof(K);
-        tri.push_back(reinterpret_cast<uint64_t>(ptr[p.rank_a] + (p.a - bases[p.rank_a])));
-        tri.push_back(reinterpret_cast<uint64_t>(ptr[p.rank_b] + (p.b - bases[p.rank_b])));
-        tri.push_back(p.len);
-    }
-    s = swap_ranges_impl<K>(tri.data(), pcs.size(), st, true);
-    if (s != PP_OK) return s;
-    std::vector<uint64_t> done;
-    const uint64_t one = 1;
-    return allgather_u64(&one, 1, done, st);  // no rank leaves before every peer's swaps finished
-}
-
-template <typename K>
-pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, uint64_t* global_split) {
-    if (!g_dist.comm) {
-        set_error("pp_partition_dist: call pp_dist_init first");
-        return PP_E_INVAL;
-    }
-    const int P = g_dist.nranks, me = g_dist.rank;
-    cudaEventRecord(g_dist.ev[0], st);
-    // 1. local partition (library kernels), split left in device memory
-    uint64_t* d_mine = g_dist.d_info + 4 * P;
-    pp_status s = PP_OK;
-    if (n_local > 0) {
-        s = partition_device<K>(shard, n_local, pivot, st, d_mine + 1, nullptr);
-    } else {
-        cudaMemsetAsync(d_mine + 1, 0, 8, st);
-    }
-    if (s != PP_OK) return s;
-    cudaEventRecord(g_dist.ev[1], st);
-    uint64_t info[3] = {n_local, (uint64_t)pivot, (uint64_t)sizeof(K)};
-    cudaError_t e = cudaMemcpyAsync(d_mine, &info[0], 8, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_mine + 2, &info[1], 16, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "dist info H2D");
-    // 2. allgather (n_r, t_r, pivot, key bytes)
-    ncclResult_t r = g_nccl.AllGather(d_mine, g_dist.d_info, 4, ncclUint64, g_dist.comm, st);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
-    cudaEventRecord(g_dist.ev[2], st);
-    std::vector<uint64_t> all(4 * P);
-    e = cudaMemcpyAsync(all.data(), g_dist.d_info, 8 * 4 * P, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(e, "dist gather");
-    std::vector<uint64_t> ns(P), ts(P);
-    for (int q = 0; q < P; ++q) {
-        ns[q] = all[4 * q];
-        ts[q] = all[4 * q + 1];
-        if (all[4 * q + 2] != (uint64_t)pivot || all[4 * q + 3] != sizeof(K)) {
-            set_error("pp_partition_dist: ranks passed different pivots or key types");
-            return PP_E_INVAL;
-        }
-    }
-    if (params().dist_p2p && P > 1) {  // one-sided over peer mappings, no staging
-        uint64_t Kg = 0;
-        for (int q = 0; q < P; ++q) Kg += ts[q];
-        uint64_t moved = 0;
-        pp_status s2 = exchange_p2p<K>(shard, n_local, ns, ts, st, &moved);
-        if (s2 != PP_OK) return s2;
-        cudaEventRecord(g_dist.ev[3], st);
-        cudaEventSynchronize(g_dist.ev[3]);
-        dist_read_timing(moved);
-        if (global_split) *global_split = Kg;
-        return PP_OK;
-    }
-    // 3. the same plan on every rank
-    const uint64_t cap = std::max<uint64_t>(1, g_dist.staging_cap_bytes / sizeof(K));
-    std::vector<Piece> pcs;
-    const uint64_t K_global = plan_pieces(ns.data(), ts.data(), P, cap, pcs);
-    uint64_t base = 0;
-    for (int q = 0; q < me; ++q) base += ns[q];
-    // staging: the most this rank receives in one round
-    uint64_t need = 0, cur = 0, rnd = ~0ull;
-    for (const Piece& p : pcs) {
-        if (p.round != rnd) {
-            rnd = p.round;
-            cur = 0;
-        }
-        if ((int)p.rank_f == me || (int)p.rank_t == me) cur += p.len;
-        need = std::max(need, cur);
-    }
-    if (need * sizeof(K) > g_dist.staging_bytes) {
-        if (g_dist.staging) cudaFree(g_dist.staging);
-        g_dist.staging = nullptr;
-        g_dist.staging_bytes = 0;
-        e = cudaMalloc(&g_dist.staging, need * sizeof(K));
-        if (e != cudaSuccess) return cuda_fail(e, "dist staging alloc");
-        g_dist.staging_bytes = need * sizeof(K);
-    }
-    K* staging = static_cast<K*>(g_dist.staging);
-    const ncclDataType_t dt = sizeof(K) == 8 ? ncclUint64 : ncclUint32;
-    // 4. rounds: send my range, receive the partner's into staging, copy back
-    size_t i = 0;
-    while (i < pcs.size()) {
-        const uint64_t round = pcs[i].round;
-        size_t j = i;
-        while (j < pcs.size() && pcs[j].round == round) ++j;
-        std::vector<uint64_t> offs, soffs, lens;
-        uint64_t soff = 0;
-        r = g_nccl.GroupStart();
-        if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
-        for (size_t k = i; k < j; ++k) {
-            const Piece& p = pcs[k];
-            int peer = -1;
-            uint64_t off = 0;
-            if ((int)p.rank_f == me) {
-                peer = (int)p.rank_t;
-                off = p.f - base;
-            } else if ((int)p.rank_t == me) {
-                peer = (int)p.rank_f;
-                off = p.t - base;
-            }
-            if (peer < 0) continue;
-            r = g_nccl.Send(shard + off, p.len, dt, peer, g_dist.comm, st);
-            if (r == ncclSuccess) r = g_nccl.Recv(staging + soff, p.len, dt, peer, g_dist.comm, st);
-            if (r != ncclSuccess) {
-                g_nccl.GroupEnd();
-                return nccl_fail(r, "ncclSend/Recv");
-            }
-            offs.push_back(off);
-            soffs.push_back(soff);
-            lens.push_back(p.len);
-            soff += p.len;
-        }
-        r = g_nccl.GroupEnd();
-        if (r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
-        for (size_t k = 0; k < offs.size(); ++k) {
-            e = cudaMemcpyAsync(shard + offs[k], staging + soffs[k], lens[k] * sizeof(K), cudaMemcpyDeviceToDevice,
-                                st);
-            if (e != cudaSuccess) return cuda_fail(e, "dist place");
-        }
-        i = j;
-    }
-    cudaEventRecord(g_dist.ev[3], st);
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(e, "dist exchange");
-    uint64_t sent = 0;  // keys this rank sent (it receives as many)
-    for (const Piece& p : pcs)
-        if ((int)p.rank_f == me || (int)p.rank_t == me) sent += p.len;
-    dist_read_timing(sent * sizeof(K));
-    if (global_split) *global_split = K_global;
+// ---------------------------------------------------------------------------
+// Collective helpers on a context.
+// ---------------------------------------------------------------------------
+// all-gather scratch of >= words (grown identically on every rank: same call
+// sequence; every collective call ends with a wait, so nothing uses it)
+static pp_status ensure_ag(DistCtx& c, size_t words) {
+    if (words <= c.d_ag_words) return PP_OK;
+    if (c.d_ag) cudaFree(c.d_ag);
+    c.d_ag = nullptr;
+    c.d_ag_words = 0;
+    words = std::max<size_t>(words, 256);
+    cudaError_t e = cudaMalloc(&c.d_ag, 8 * words);
+    if (e != cudaSuccess) return cuda_fail(e, "all-gather scratch");
+    c.d_ag_words = words;
     return PP_OK;
 }
 
-template pp_status partition_dist<uint64_t>(uint64_t*, uint64_t, uint64_t, cudaStream_t, uint64_t*);
-template pp_status partition_dist<uint32_t>(uint32_t*, uint64_t, uint32_t, cudaStream_t, uint64_t*);
-
-// ---------------------------------------------------------------------------
-// Distributed quicksort (BASELINE config 5 at P GPUs): segments spanning
-// several ranks are split by partition_dist (median-of-3 pivot gathered from
-// the owning ranks; "x <= p" step when the pivot is the minimum -- DESIGN.md
-// R14); spanning segments of <= `small` keys are all-gathered, sorted on
-// every participating rank, and each keeps its part.  When no segment spans
-// two ranks each shard is a concatenation of whole segments in key order:
-// one local quicksort per rank finishes.  Mirrors Partitioner.sort in
-// paper_2004_12532_b200/dist.py (tested there over gloo with P = 2..4).
-// ---------------------------------------------------------------------------
-static pp_status allgather_u64(const uint64_t* host_in, uint64_t count, std::vector<uint64_t>& host_out,
-                               cudaStream_t st) {
-    const int P = g_dist.nranks;
-    const size_t words = count * (P + 1);
-    cudaError_t e = cudaSuccess;
-    if (words > g_dist.d_ag_words) {  // grow (the previous user synchronised its stream)
-        if (g_dist.d_ag) cudaFree(g_dist.d_ag);
-        g_dist.d_ag = nullptr;
-        g_dist.d_ag_words = 0;
-        e = cudaMalloc(&g_dist.d_ag, 8 * words);
-        if (e != cudaSuccess) return cuda_fail(e, "allgather buffer");
-        g_dist.d_ag_words = words;
-    }
-    uint64_t* d = g_dist.d_ag;
-    e = cudaMemcpyAsync(d + count * P, host_in, 8 * count, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "allgather H2D");
-    ncclResult_t r = g_nccl.AllGather(d + count * P, d, count, ncclUint64, g_dist.comm, st);
-    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
-    host_out.assign(count * P, 0);
-    e = cudaMemcpyAsync(host_out.data(), d, 8 * count * P, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // also: the buffer is free for the next call
-    return e == cudaSuccess ? PP_OK : cuda_fail(e, "allgather D2H");
+// host words -> all ranks' words (count per rank), through the device scratch
+static pp_status ag_host(DistCtx& c, const uint64_t* in, uint64_t count, std::vector<uint64_t>& out, cudaStream_t st) {
+    pp_status s = ensure_ag(c, count * (c.P + 1));
+    if (s != PP_OK) return s;
+    uint64_t* d = c.d_ag;
+    cudaError_t e = cudaMemcpyAsync(d + count * c.P, in, 8 * count, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "all-gather H2D");
+    s = c.tp->allgather(d + count * c.P, d, 8 * count, st);
+    if (s != PP_OK) return s;
+    out.assign(count * c.P, 0);
+    e = cudaMemcpyAsync(out.data(), d, 8 * count * c.P, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "all-gather D2H");
+    return c.tp->wait(st);
 }
 
-template <typename K>
-pp_status quicksort_dist(K* shard, uint64_t n_local, cudaStream_t st, uint64_t small) {
-    if (!g_dist.comm) {
-        set_error("pp_quicksort_dist: call pp_dist_init first");
-        return PP_E_INVAL;
-    }
-    const int P = g_dist.nranks, me = g_dist.rank;
-    const uint64_t KMAXU = (uint64_t)(K)~(K)0;
+// Every rank contributes its status; all return the lowest-ranked failure.
+static pp_status agree(DistCtx& c, pp_status mine, cudaStream_t st) {
+    const uint64_t w = (uint64_t)mine;
     std::vector<uint64_t> all;
-    pp_status s = allgather_u64(&n_local, 1, all, st);
+    pp_status s = ag_host(c, &w, 1, all, st);
     if (s != PP_OK) return s;
-    std::vector<uint64_t> ns(all), base(P, 0);
-    for (int r = 1; r < P; ++r) base[r] = base[r - 1] + ns[r - 1];
-    const uint64_t N = base[P - 1] + ns[P - 1], b0 = base[me];
-    auto owner = [&](uint64_t x) {
-        int r = 0;
-        while (r + 1 < P && base[r + 1] <= x) ++r;
-        return r;
-    };
-    auto piece = [&](uint64_t lo, uint64_t hi, uint64_t& pa, uint64_t& pb) {
-        const uint64_t a = std::max(lo, b0), b = std::min(hi, b0 + ns[me]);
-        if (a < b) { pa = a - b0; pb = b - b0; } else { pa = pb = 0; }
-    };
-    struct Seg {
-        uint64_t lo, hi;
-    };
-    std::vector<Seg> segs;
-    if (N > 1) segs.push_back({0, N});
-    cudaError_t e;
-    for (;;) {
-        std::vector<Seg> span, nxt;
-        for (const Seg& sg : segs)
-            if (sg.hi - sg.lo > 1 && owner(sg.lo) != owner(sg.hi - 1)) span.push_back(sg);
-        if (span.empty()) break;
-        for (const Seg& sg : span) {
-            const uint64_t lo = sg.lo, hi = sg.hi;
-            uint64_t pa, pb;
-            piece(lo, hi, pa, pb);
-            if (hi - lo <= small) {
-                // all-gather the segment, sort it everywhere, keep my part
-                std::vector<uint64_t> lens(P);
-                uint64_t mx = 0, off = 0;
-                for (int r = 0; r < P; ++r) {
-                    const uint64_t a = std::max(lo, base[r]), b = std::min(hi, base[r] + ns[r]);
-                    lens[r] = a < b ? b - a : 0;
-                    mx = std::max(mx, lens[r]);
-                    if (r < me) off += lens[r];
-                }
-                K* d = nullptr;
-                e = cudaMalloc(&d, sizeof(K) * (mx * (P + 1) + (hi - lo)));
-                if (e != cudaSuccess) return cuda_fail(e, "gather-sort buffer");
-                K* mine = d + mx * P;
-                K* full = mine + mx;
-                if (pb > pa) e = cudaMemcpyAsync(mine, shard + pa, sizeof(K) * (pb - pa), cudaMemcpyDeviceToDevice, st);
-                ncclResult_t r = g_nccl.AllGather(mine, d, mx, sizeof(K) == 8 ? ncclUint64 : ncclUint32, g_dist.comm,
-                                                  st);
-                if (r != ncclSuccess) {
-                    cudaFree(d);
-                    return nccl_fail(r, "ncclAllGather");
-                }
-                uint64_t at = 0;
-                for (int q = 0; q < P; ++q) {
-                    if (lens[q]) cudaMemcpyAsync(full + at, d + mx * q, sizeof(K) * lens[q], cudaMemcpyDeviceToDevice, st);
-                    at += lens[q];
-                }
-                s = quicksort_device<K>(full, hi - lo, st);
-                if (s == PP_OK && pb > pa)
-                    e = cudaMemcpyAsync(shard + pa, full + off, sizeof(K) * (pb - pa), cudaMemcpyDeviceToDevice, st);
-                if (s == PP_OK) e = cudaStreamSynchronize(st);
-                cudaFree(d);
-                if (s != PP_OK) return s;
-                if (e != cudaSuccess) return cuda_fail(e, "gather-sort");
-                continue;
-            }
-            // median of 3 from the owning ranks
-            const uint64_t pos[3] = {lo, lo + (hi - lo - 1) / 2, hi - 1};
-            uint64_t mv[6] = {0, 0, 0, 0, 0, 0};
-            for (int i = 0; i < 3; ++i) {
-                if (pos[i] >= b0 && pos[i] < b0 + ns[me]) {
-                    K v;
-                    e = cudaMemcpy(&v, shard + (pos[i] - b0), sizeof(K), cudaMemcpyDeviceToHost);
-                    if (e != cudaSuccess) return cuda_fail(e, "pivot read");
-                    mv[2 * i] = 1;
-                    mv[2 * i + 1] = (uint64_t)v;
-                }
-            }
-            s = allgather_u64(mv, 6, all, st);
-            if (s != PP_OK) return s;
-            uint64_t v3[3] = {0, 0, 0};
-            for (int i = 0; i < 3; ++i)
-                for (int q = 0; q < P; ++q)
-                    if (all[6 * q + 2 * i]) {
-                        v3[i] = all[6 * q + 2 * i + 1];
-                        break;
-                    }
-            std::sort(v3, v3 + 3);
-            const uint64_t p = v3[1];
-            uint64_t k = 0;
-            s = partition_dist<K>(shard + pa, pb - pa, (K)p, st, &k);
-            if (s != PP_OK) return s;
-            if (k == 0) {
-                if (p == KMAXU) continue;  // all keys equal the maximum
-                s = partition_dist<K>(shard + pa, pb - pa, (K)(p + 1), st, &k);
-                if (s != PP_OK) return s;
-                nxt.push_back({lo + k, hi});  // [lo, lo+k) all equal p
-            } else {
-                nxt.push_back({lo, lo + k});
-                nxt.push_back({lo + k, hi});
-            }
+    for (int q = 0; q < c.P; ++q)
+        if (all[q] != PP_OK) {
+            if (q != c.me) set_error("peer rank " + std::to_string(q) + " failed with status " + std::to_string(all[q]));
+            return (pp_status)all[q];
         }
-        segs.clear();
-        for (const Seg& sg : nxt)
-            if (sg.hi - sg.lo > 1) segs.push_back(sg);
-    }
-    if (n_local > 1) {
-        s = quicksort_device<K>(shard, n_local, st);
-        if (s != PP_OK) return s;
-    }
-    e = cudaStreamSynchronize(st);
-    return e == cudaSuccess ? PP_OK : cuda_fail(e, "quicksort_dist");
+    return PP_OK;
 }
 
-template pp_status quicksort_dist<uint64_t>(uint64_t*, uint64_t, cudaStream_t, uint64_t);
-template pp_status quicksort_dist<uint32_t>(uint32_t*, uint64_t, cudaStream_t, uint64_t);
+static pp_status grow(void** p, size_t* have, size_t want) {
+    if (want <= *have) return PP_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    cudaError_t e = cudaMalloc(p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        set_error("dist buffer cudaMalloc of " + std::to_string(want) + " bytes failed");
+        return PP_E_NOMEM;
+    }
+    *have = want;
+    return PP_OK;
+}
 
 // ---------------------------------------------------------------------------
 // Staging-free exchange primitive: swap ranges [a, a+len)
 // <-> [b, b+len) elementwise for every piece, one thread per element pair
 // (EREW), grid-stride over all pieces' elements; the piece of an element is
 // found by binary search over the length prefix.  a and b are device
-// pointers -- with peer-mapped b (CUDA IPC / symmetric memory) one rank
-// performs its exchange pieces one-sidedly over NVLink with no staging
-// buffer and no second copy; on one GPU it executes a whole plan of emulated
-// ranks (tests).  The caller guarantees that no two ranges overlap.
+// pointers -- with peer-mapped b (CUDA IPC) one rank performs its exchange
+// pieces one-sidedly with no staging buffer and no second copy.  The caller
+// guarantees that no two ranges overlap.
 // ---------------------------------------------------------------------------
 template <typename K>
 __global__ void __launch_bounds__(256) swap_ranges_kernel(const uint64_t* __restrict__ tri,
@@ -706,72 +695,583 @@ __global__ void __launch_bounds__(256) swap_ranges_kernel(const uint64_t* __rest
     if (sys_fence) __threadfence_system();  // peer writes ordered before the closing collective
 }
 
-static uint64_t* g_swap_buf = nullptr;
-static size_t g_swap_cap = 0;
-
+// Enqueues the swaps on st; the piece table is copied into *buf (grown; the
+// previous user synchronised) from host memory that the call keeps alive
+// until the copy is done (it waits for st before returning).
 template <typename K>
-static pp_status swap_ranges_impl(const uint64_t* host_tri, uint64_t np, cudaStream_t st, bool sys_fence) {
+static pp_status swap_ranges_impl(const uint64_t* host_tri, uint64_t np, cudaStream_t st, bool sys_fence,
+                                  uint64_t** buf, size_t* cap_words) {
     if (np == 0) return PP_OK;
     if (!host_tri) return PP_E_INVAL;
-    std::vector<uint64_t> buf(4 * np);  // [3 np triples][np prefix]
+    std::vector<uint64_t> tab(4 * np);  // [3 np triples][np prefix]
     uint64_t total = 0;
     for (uint64_t k = 0; k < np; ++k) {
-        buf[3 * k] = host_tri[3 * k];
-        buf[3 * k + 1] = host_tri[3 * k + 1];
-        buf[3 * k + 2] = host_tri[3 * k + 2];
+        tab[3 * k] = host_tri[3 * k];
+        tab[3 * k + 1] = host_tri[3 * k + 1];
+        tab[3 * k + 2] = host_tri[3 * k + 2];
         if ((host_tri[3 * k] | host_tri[3 * k + 1]) % sizeof(K)) {
             set_error("pp_swap_ranges: unaligned range");
             return PP_E_INVAL;
         }
-        buf[3 * np + k] = total;
+        tab[3 * np + k] = total;
         total += host_tri[3 * k + 2];
     }
     if (total == 0) return PP_OK;
-    if (4 * np > g_swap_cap) {
+    if (4 * np > *cap_words) {
         cudaStreamSynchronize(st);
-        if (g_swap_buf) cudaFree(g_swap_buf);
-        g_swap_buf = nullptr;
-        g_swap_cap = 0;
-        if (cudaMalloc(&g_swap_buf, 8 * 4 * np) != cudaSuccess) {
-            cudaGetLastError();
-            set_error("pp_swap_ranges: piece buffer allocation failed");
-            return PP_E_NOMEM;
-        }
-        g_swap_cap = 4 * np;
+        size_t have = *cap_words * 8;
+        void* p = *buf;
+        pp_status s = grow(&p, &have, 8 * 4 * np);
+        *buf = static_cast<uint64_t*>(p);
+        *cap_words = have / 8;
+        if (s != PP_OK) return s;
     }
-    cudaError_t e = cudaMemcpyAsync(g_swap_buf, buf.data(), 8 * 4 * np, cudaMemcpyHostToDevice, st);
+    cudaError_t e = cudaMemcpyAsync(*buf, tab.data(), 8 * 4 * np, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "pp_swap_ranges H2D");
     const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
-    swap_ranges_kernel<K><<<(unsigned)blocks, 256, 0, st>>>(g_swap_buf, g_swap_buf + 3 * np, np, total,
-                                                            sys_fence ? 1 : 0);
+    swap_ranges_kernel<K><<<(unsigned)blocks, 256, 0, st>>>(*buf, *buf + 3 * np, np, total, sys_fence ? 1 : 0);
     note_launches(1);
-    // the host triples were staged by the (pageable) copy; wait before the
-    // vector goes away only if the copy could still read it
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host table stays alive until the copy ran
     return e == cudaSuccess ? PP_OK : cuda_fail(e, "pp_swap_ranges");
 }
+
+static uint64_t* g_swap_buf = nullptr;
+static size_t g_swap_cap = 0;
 template <typename K>
 pp_status swap_ranges(const uint64_t* host_tri, uint64_t np, cudaStream_t st) {
-    return swap_ranges_impl<K>(host_tri, np, st, false);
+    return swap_ranges_impl<K>(host_tri, np, st, false, &g_swap_buf, &g_swap_cap);
 }
 template pp_status swap_ranges<uint64_t>(const uint64_t*, uint64_t, cudaStream_t);
 template pp_status swap_ranges<uint32_t>(const uint64_t*, uint64_t, cudaStream_t);
 
+// ---------------------------------------------------------------------------
+// Batched distributed partition: S segments, each a contiguous range of the
+// global array cut into per-rank pieces (a piece may be empty); every
+// segment is partitioned by its own pivot.  One record all-gather for all
+// segments, one exchange (all segments' runs in one round schedule).
+// ---------------------------------------------------------------------------
+struct SegPiece {
+    uint64_t off, len;  // this rank's piece: shard[off, off + len)
+    uint64_t pivot;
+};
+
+template <typename K>
+static pp_status partition_multi(DistCtx& c, K* shard, const std::vector<SegPiece>& mine, cudaStream_t st,
+                                 std::vector<uint64_t>& K_out, bool timing) {
+    Transport& tp = *c.tp;
+    const int P = c.P, me = c.me;
+    const size_t S = mine.size();
+    if (tp.absent()) {  // test hook: this rank never takes part
+        set_error("rank absent (dist_fault = 2)");
+        return PP_E_INTERNAL;
+    }
+    const size_t RW = 2 + 4 * S;  // record: [status, key bytes, n[S], pivot[S], off[S], t[S]]
+    if (timing) cudaEventRecord(c.ev[0], st);
+    pp_status s = PP_OK;
+    uint64_t my_total = 0;
+    for (const SegPiece& p : mine) my_total += p.len;
+    // staging: a rank moves <= min(cap, its misplaced keys) per round
+    const uint64_t cap = std::max<uint64_t>(1, g_staging_cap_bytes / sizeof(K));
+    if (!params().dist_p2p && P > 1)
+        s = grow(&c.staging, &c.staging_bytes, sizeof(K) * std::max<uint64_t>(1, std::min(cap, my_total)));
+    {  // record scratch: [P gathered records][my record]; without it this rank cannot take part
+        const pp_status sa = ensure_ag(c, RW * (P + 1));
+        if (sa != PP_OK) return sa;
+    }
+    if (s == PP_OK && params().dist_fault == 1 && params().dist_fault_rank == me) {
+        set_error("injected local failure (dist_fault = 1)");
+        s = PP_E_INTERNAL;
+    }
+    uint64_t* rec = c.d_ag + RW * P;  // my record (device); t[] is written by the local partitions
+    // 1. local partitions (library kernels)
+    if (s == PP_OK) {
+        tp.local_begin();
+        for (size_t k = 0; k < S && s == PP_OK; ++k) {
+            uint64_t* t_slot = rec + 2 + 3 * S + k;
+            if (mine[k].len > 0)
+                s = partition_device<K>(shard + mine[k].off, mine[k].len, (K)mine[k].pivot, st, t_slot, nullptr);
+            else if (cudaMemsetAsync(t_slot, 0, 8, st) != cudaSuccess)
+                s = cuda_fail(cudaGetLastError(), "memset");
+        }
+        const pp_status s2 = tp.local_end(st);
+        if (s == PP_OK) s = s2;
+    }
+    if (timing) cudaEventRecord(c.ev[1], st);
+    std::vector<uint64_t> head(2 + 3 * S);
+    head[0] = (uint64_t)s;
+    head[1] = sizeof(K);
+    for (size_t k = 0; k < S; ++k) {
+        head[2 + k] = mine[k].len;
+        head[2 + S + k] = mine[k].pivot;
+        head[2 + 2 * S + k] = mine[k].off;
+    }
+    cudaError_t e = cudaMemcpyAsync(rec, head.data(), 8 * head.size(), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "dist record H2D");
+    // 2. all-gather the records (status agreement included)
+    pp_status sg = tp.allgather(rec, c.d_ag, 8 * RW, st);
+    if (sg != PP_OK) return sg;
+    if (timing) cudaEventRecord(c.ev[2], st);
+    std::vector<uint64_t> all(RW * P);
+    e = cudaMemcpyAsync(all.data(), c.d_ag, 8 * RW * P, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "dist record D2H");
+    if ((sg = tp.wait(st)) != PP_OK) return sg;
+    for (int q = 0; q < P; ++q)
+        if (all[RW * q] != PP_OK) {
+            if (q != me) set_error("peer rank " + std::to_string(q) + " failed with status " + std::to_string(all[RW * q]));
+            return (pp_status)all[RW * q];
+        }
+    for (int q = 0; q < P; ++q) {
+        bool bad = all[RW * q + 1] != sizeof(K);
+        for (size_t k = 0; k < S; ++k) bad |= all[RW * q + 2 + S + k] != mine[k].pivot;
+        if (bad) {
+            set_error("pp_partition_dist: ranks passed different pivots or key types");
+            return PP_E_INVAL;
+        }
+    }
+    // 3. the same plan on every rank: runs per segment in shard-local offsets
+    std::vector<Run> runs;
+    K_out.assign(S, 0);
+    {
+        std::vector<uint64_t> ns(P), ts(P), base(P);
+        std::vector<Run> rs;
+        for (size_t k = 0; k < S; ++k) {
+            uint64_t b = 0;
+            for (int q = 0; q < P; ++q) {
+                ns[q] = all[RW * q + 2 + k];
+                ts[q] = all[RW * q + 2 + 3 * S + k];
+                base[q] = b;
+                b += ns[q];
+                if (ts[q] > ns[q]) {
+                    set_error("pp_partition_dist: corrupt local split");
+                    return PP_E_INTERNAL;
+                }
+            }
+            K_out[k] = match_runs(ns.data(), ts.data(), P, rs);
+            for (const Run& r : rs)
+                runs.push_back({r.ra, all[RW * r.ra + 2 + 2 * S + k] + (r.a - base[r.ra]), r.rb,
+                                all[RW * r.rb + 2 + 2 * S + k] + (r.b - base[r.rb]), r.len});
+        }
+    }
+    uint64_t moved = 0;
+    if (params().dist_p2p && P > 1) {
+        // 4a. one-sided: map the peers' shards, swap my share, then agree
+        std::vector<uint64_t> prec(1 + kPeerWords), allp;
+        pp_status se = tp.export_range(shard, prec.data() + 1);
+        prec[0] = (uint64_t)se;
+        pp_status sa = ag_host(c, prec.data(), 1 + kPeerWords, allp, st);
+        if (sa != PP_OK) return sa;
+        for (int q = 0; q < P; ++q)
+            if (allp[(1 + kPeerWords) * q] != PP_OK) return agree(c, (pp_status)allp[(1 + kPeerWords) * q], st);
+        std::vector<Run> share;
+        p2p_share(runs, me, share);
+        std::vector<K*> ptr(P, nullptr);
+        ptr[me] = shard;
+        pp_status sl = PP_OK;
+        for (const Run& p : share)
+            for (uint64_t q : {p.ra, p.rb}) {
+                if (ptr[q] || sl != PP_OK) continue;
+                void* d = nullptr;
+                sl = tp.import_range(&allp[(1 + kPeerWords) * q + 1], &d);
+                ptr[q] = static_cast<K*>(d);
+            }
+        if (sl == PP_OK && !share.empty()) {
+            std::vector<uint64_t> tri;
+            for (const Run& p : share) {
+                moved += 2 * p.len * sizeof(K);
+                tri.push_back(reinterpret_cast<uint64_t>(ptr[p.ra] + p.a));
+                tri.push_back(reinterpret_cast<uint64_t>(ptr[p.rb] + p.b));
+                tri.push_back(p.len);
+            }
+            tp.local_begin();
+            sl = swap_ranges_impl<K>(tri.data(), share.size(), st, true, &c.d_swap, &c.d_swap_words);
+            const pp_status s2 = tp.local_end(st);
+            if (sl == PP_OK) sl = s2;
+        }
+        // no rank leaves (or reads its shard) before every peer's swaps finished
+        if ((sl = agree(c, sl, st)) != PP_OK) return sl;
+    } else if (P > 1) {
+        // 4b. staged rounds: send my range, receive the partner's into staging, place
+        std::vector<Piece> pcs;
+        schedule_rounds(runs, P, cap, pcs);
+        K* staging = static_cast<K*>(c.staging);
+        size_t i = 0;
+        while (i < pcs.size()) {
+            const uint64_t round = pcs[i].round;
+            size_t j = i;
+            while (j < pcs.size() && pcs[j].round == round) ++j;
+            std::vector<uint64_t> offs, soffs, lens;
+            uint64_t soff = 0;
+            pp_status sr = tp.group_start();
+            for (size_t k = i; k < j && sr == PP_OK; ++k) {
+                const Piece& p = pcs[k];
+                int peer = -1;
+                uint64_t off = 0;
+                if ((int)p.rank_f == me) {
+                    peer = (int)p.rank_t;
+                    off = p.f;
+                } else if ((int)p.rank_t == me) {
+                    peer = (int)p.rank_f;
+                    off = p.t;
+                }
+                if (peer < 0) continue;
+                sr = tp.send(shard + off, p.len * sizeof(K), peer, st);
+                if (sr == PP_OK) sr = tp.recv(staging + soff, p.len * sizeof(K), peer, st);
+                offs.push_back(off);
+                soffs.push_back(soff);
+                lens.push_back(p.len);
+                soff += p.len;
+                moved += p.len * sizeof(K);
+            }
+            const pp_status se = tp.group_end(st);
+            if (sr == PP_OK) sr = se;
+            if (sr != PP_OK) return sr;
+            for (size_t k = 0; k < offs.size(); ++k) {
+                e = cudaMemcpyAsync(shard + offs[k], staging + soffs[k], lens[k] * sizeof(K),
+                                    cudaMemcpyDeviceToDevice, st);
+                if (e != cudaSuccess) return cuda_fail(e, "dist place");
+            }
+            i = j;
+        }
+    }
+    if (timing) cudaEventRecord(c.ev[3], st);
+    if ((s = tp.wait(st)) != PP_OK) return s;
+    if (timing) {
+        float a = 0, b = 0, d = 0;
+        cudaEventElapsedTime(&a, c.ev[0], c.ev[1]);
+        cudaEventElapsedTime(&b, c.ev[1], c.ev[2]);
+        cudaEventElapsedTime(&d, c.ev[2], c.ev[3]);
+        c.last_local_ms = a;
+        c.last_gather_ms = b;
+        c.last_exchange_ms = d;
+        c.last_bytes = moved;
+    }
+    return PP_OK;
+}
+
+template <typename K>
+static pp_status partition_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, K pivot, cudaStream_t st,
+                                    uint64_t* global_split) {
+    std::vector<uint64_t> Ks;
+    pp_status s = partition_multi<K>(c, shard, {SegPiece{0, n_local, (uint64_t)pivot}}, st, Ks, true);
+    if (s == PP_OK && global_split) *global_split = Ks[0];
+    return s;
+}
+
+template <typename K>
+pp_status partition_dist(K* shard, uint64_t n_local, K pivot, cudaStream_t st, uint64_t* global_split) {
+    if (!g_ctx.tp) {
+        set_error("pp_partition_dist: call pp_dist_init first");
+        return PP_E_INVAL;
+    }
+    return partition_dist_ctx<K>(g_ctx, shard, n_local, pivot, st, global_split);
+}
+template pp_status partition_dist<uint64_t>(uint64_t*, uint64_t, uint64_t, cudaStream_t, uint64_t*);
+template pp_status partition_dist<uint32_t>(uint32_t*, uint64_t, uint32_t, cudaStream_t, uint64_t*);
+
+// ---------------------------------------------------------------------------
+// Distributed quicksort (BASELINE config 5 at P GPUs; PAPER.md:1701-1732 with
+// the parallel partition at the top levels).  Level by level over the
+// segments that span ranks, all identical on every rank:
+//   * pivots: the median-of-3 sample keys (R14) of every spanning
+//     segment are copied device-to-device into one sample array, ONE
+//     all-gather per level, each taken from its owner's slot;
+//   * segments > `small` keys: ONE batched partition_multi for all of them
+//     (one record all-gather, one exchange); a segment whose pivot is its
+//     minimum (split 0) is re-partitioned next level by "x <= p" (pivot p+1),
+//     whose left part (all == p) is final;
+//   * segments <= `small`: ONE all-gather of every rank's pieces of all of
+//     them; each participating rank sorts the whole segment locally and keeps
+//     its part.
+// When no segment spans ranks each shard is a concatenation of whole
+// segments in key order: one local quicksort per rank finishes.
+// ---------------------------------------------------------------------------
+template <typename K>
+static pp_status quicksort_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, cudaStream_t st, uint64_t small) {
+    Transport& tp = *c.tp;
+    const int P = c.P, me = c.me;
+    const uint64_t KMAXU = (uint64_t)(K)~(K)0;
+    if (tp.absent()) {
+        set_error("rank absent (dist_fault = 2)");
+        return PP_E_INTERNAL;
+    }
+    std::vector<uint64_t> all;
+    const uint64_t hdr[2] = {PP_OK, n_local};
+    pp_status s = ag_host(c, hdr, 2, all, st);
+    if (s != PP_OK) return s;
+    std::vector<uint64_t> ns(P), base(P, 0);
+    for (int r = 0; r < P; ++r) ns[r] = all[2 * r + 1];
+    for (int r = 1; r < P; ++r) base[r] = base[r - 1] + ns[r - 1];
+    const uint64_t N = base[P - 1] + ns[P - 1], b0 = base[me];
+    auto owner = [&](uint64_t x) {
+        int r = 0;
+        while (r + 1 < P && base[r + 1] <= x) ++r;
+        return r;
+    };
+    auto inter = [&](uint64_t lo, uint64_t hi, int r, uint64_t& a, uint64_t& b) {  // piece of rank r (global)
+        a = std::max(lo, base[r]);
+        b = std::min(hi, base[r] + ns[r]);
+        if (a >= b) a = b = 0;
+    };
+    struct Seg {
+        uint64_t lo, hi;
+        bool leq;  // re-partition by x <= pivot (the pivot was the minimum)
+        uint64_t pivot;
+    };
+    std::vector<Seg> segs;
+    if (N > 1) segs.push_back({0, N, false, 0});
+    cudaError_t e;
+    while (true) {
+        std::vector<Seg> big, sm, nxt;
+        for (const Seg& sg : segs)
+            if (sg.hi - sg.lo > 1 && owner(sg.lo) != owner(sg.hi - 1)) (sg.hi - sg.lo <= small ? sm : big).push_back(sg);
+        if (big.empty() && sm.empty()) break;
+        // ---- pivots: one all-gather of the sample keys of this level ----
+        std::vector<uint64_t> spos;  // 3 per segment needing a sample
+        for (const Seg& sg : big)
+            if (!sg.leq) {
+                spos.push_back(sg.lo);
+                spos.push_back(sg.lo + (sg.hi - sg.lo - 1) / 2);
+                spos.push_back(sg.hi - 1);
+            }
+        std::vector<uint64_t> sval;
+        if (!spos.empty()) {
+            const size_t m = spos.size();
+            if ((s = grow(&c.gs, &c.gs_bytes, 8 * m * (P + 1))) != PP_OK) return agree(c, s, st);
+            uint64_t* d_samp = static_cast<uint64_t*>(c.gs) + m * P;
+            e = cudaMemsetAsync(d_samp, 0, 8 * m, st);
+            for (size_t i = 0; i < m && e == cudaSuccess; ++i)
+                if (owner(spos[i]) == me)  // little-endian: a u32 key lands in the low half of its word
+                    e = cudaMemcpyAsync(d_samp + i, shard + (spos[i] - b0), sizeof(K), cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "pivot samples");
+            if ((s = tp.allgather(d_samp, c.gs, 8 * m, st)) != PP_OK) return s;
+            std::vector<uint64_t> got(m * P);
+            e = cudaMemcpyAsync(got.data(), c.gs, 8 * m * P, cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) return cuda_fail(e, "pivot samples D2H");
+            if ((s = tp.wait(st)) != PP_OK) return s;
+            for (size_t i = 0; i < m; ++i) sval.push_back(got[m * owner(spos[i]) + i]);
+        }
+        // ---- big spanning segments: one batched distributed partition ----
+        if (!big.empty()) {
+            std::vector<SegPiece> mine;
+            std::vector<uint64_t> piv(big.size());
+            for (size_t k = 0, si = 0; k < big.size(); ++k) {
+                const Seg& sg = big[k];
+                uint64_t p = sg.pivot;
+                if (!sg.leq) {
+                    uint64_t v3[3] = {sval[si], sval[si + 1], sval[si + 2]};
+                    si += 3;
+                    std::sort(v3, v3 + 3);
+                    p = v3[1];
+                }
+                piv[k] = p;
+                uint64_t a, b;
+                inter(sg.lo, sg.hi, me, a, b);
+                // x <= p is x < p + 1 (p < KMAX here: see below)
+                mine.push_back({a < b ? a - b0 : 0, b - a, sg.leq ? p + 1 : p});
+            }
+            std::vector<uint64_t> Ks;
+            if ((s = partition_multi<K>(c, shard, mine, st, Ks, false)) != PP_OK) return s;
+            for (size_t k = 0; k < big.size(); ++k) {
+                const Seg& sg = big[k];
+                const uint64_t kk = Ks[k], p = piv[k];
+                if (sg.leq) {
+                    nxt.push_back({sg.lo + kk, sg.hi, false, 0});  // [lo, lo+kk) all == p: final
+                } else if (kk == 0) {
+                    if (p != KMAXU) nxt.push_back({sg.lo, sg.hi, true, p});  // else: all keys equal the maximum
+                } else {
+                    nxt.push_back({sg.lo, sg.lo + kk, false, 0});
+                    nxt.push_back({sg.lo + kk, sg.hi, false, 0});
+                }
+            }
+        }
+        // ---- small spanning segments: one gather, sort locally, keep my part ----
+        if (!sm.empty()) {
+            std::vector<uint64_t> contrib(P, 0);
+            uint64_t tot = 0;
+            for (const Seg& sg : sm) {
+                tot += sg.hi - sg.lo;
+                for (int r = 0; r < P; ++r) {
+                    uint64_t a, b;
+                    inter(sg.lo, sg.hi, r, a, b);
+                    contrib[r] += b - a;
+                }
+            }
+            const uint64_t mx = *std::max_element(contrib.begin(), contrib.end());
+            // layout: gathered [P][mx] | mine [mx] | assembled segments [tot]
+            s = grow(&c.gs, &c.gs_bytes, sizeof(K) * (mx * (P + 1) + tot));
+            if ((s = agree(c, s, st)) != PP_OK) return s;
+            K* g = static_cast<K*>(c.gs);
+            K* snd = g + mx * P;
+            K* asm_ = snd + mx;
+            uint64_t at = 0;
+            e = cudaSuccess;
+            for (const Seg& sg : sm) {
+                uint64_t a, b;
+                inter(sg.lo, sg.hi, me, a, b);
+                if (b > a) e = cudaMemcpyAsync(snd + at, shard + (a - b0), sizeof(K) * (b - a), cudaMemcpyDeviceToDevice, st);
+                at += b - a;
+                if (e != cudaSuccess) return cuda_fail(e, "gather-sort pack");
+            }
+            if ((s = tp.allgather(snd, g, sizeof(K) * mx, st)) != PP_OK) return s;
+            std::vector<uint64_t> rat(P, 0);  // read cursor per rank in the gathered rows
+            uint64_t seg_at = 0;
+            pp_status sl = PP_OK;
+            tp.local_begin();
+            for (const Seg& sg : sm) {
+                const uint64_t len = sg.hi - sg.lo;
+                K* full = asm_ + seg_at;
+                uint64_t w = 0, my_off = 0, my_len = 0;
+                for (int r = 0; r < P && e == cudaSuccess; ++r) {
+                    uint64_t a, b;
+                    inter(sg.lo, sg.hi, r, a, b);
+                    if (r == me) {
+                        my_off = w;
+                        my_len = b - a;
+                    }
+                    if (b > a) e = cudaMemcpyAsync(full + w, g + mx * r + rat[r], sizeof(K) * (b - a), cudaMemcpyDeviceToDevice, st);
+                    rat[r] += b - a;
+                    w += b - a;
+                }
+                if (e != cudaSuccess) break;
+                if (my_len > 0 && sl == PP_OK) {  // only participating ranks sort
+                    sl = quicksort_device<K>(full, len, st);
+                    if (sl == PP_OK)
+                        e = cudaMemcpyAsync(shard + (std::max(sg.lo, b0) - b0), full + my_off, sizeof(K) * my_len,
+                                            cudaMemcpyDeviceToDevice, st);
+                }
+                seg_at += len;
+            }
+            const pp_status s2 = tp.local_end(st);
+            if (sl == PP_OK && e != cudaSuccess) sl = cuda_fail(e, "gather-sort");
+            if (sl == PP_OK) sl = s2;
+            if ((s = agree(c, sl, st)) != PP_OK) return s;  // also: every rank read the gather before reuse
+        }
+        segs.clear();
+        for (const Seg& sg : nxt)
+            if (sg.hi - sg.lo > 1) segs.push_back(sg);
+    }
+    pp_status sl = PP_OK;
+    if (n_local > 1) {
+        tp.local_begin();
+        sl = quicksort_device<K>(shard, n_local, st);
+        const pp_status s2 = tp.local_end(st);
+        if (sl == PP_OK) sl = s2;
+    }
+    if (sl == PP_OK) sl = tp.wait(st);
+    return agree(c, sl, st);
+}
+
+template <typename K>
+pp_status quicksort_dist(K* shard, uint64_t n_local, cudaStream_t st, uint64_t small) {
+    if (!g_ctx.tp) {
+        set_error("pp_quicksort_dist: call pp_dist_init first");
+        return PP_E_INVAL;
+    }
+    return quicksort_dist_ctx<K>(g_ctx, shard, n_local, st, small);
+}
+template pp_status quicksort_dist<uint64_t>(uint64_t*, uint64_t, cudaStream_t, uint64_t);
+template pp_status quicksort_dist<uint32_t>(uint32_t*, uint64_t, cudaStream_t, uint64_t);
+
+// ---------------------------------------------------------------------------
+// Loopback drivers: P emulated ranks on this GPU, rank r = keys[sum ns[<r],
+// + ns[r]); each runs the collective call on its own thread and stream.
+// ---------------------------------------------------------------------------
+template <typename K, typename F>
+static pp_status loopback_run(K* keys, const uint64_t* ns, int P, F&& body) {
+    if (P < 1 || P > 64 || !ns) {
+        set_error("loopback: 1 <= nranks <= 64 and ns != NULL required");
+        return PP_E_INVAL;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    LoopHub hub(P);
+    std::vector<LoopTransport> tps(P);
+    std::vector<DistCtx> ctx(P);
+    std::vector<cudaStream_t> sts(P, nullptr);
+    std::vector<pp_status> res(P, PP_OK);
+    std::vector<std::string> errs(P);
+    std::vector<uint64_t> off(P, 0);
+    for (int r = 1; r < P; ++r) off[r] = off[r - 1] + ns[r - 1];
+    for (int r = 0; r < P; ++r) {
+        tps[r].P = P;
+        tps[r].me = r;
+        tps[r].hub = &hub;
+        tps[r].absent_ = params().dist_fault == 2 && params().dist_fault_rank == r;
+        ctx[r].tp = &tps[r];
+        ctx[r].P = P;
+        ctx[r].me = r;
+        ctx[r].device = dev;
+        if (ctx[r].init_events() != PP_OK || cudaStreamCreateWithFlags(&sts[r], cudaStreamNonBlocking) != cudaSuccess) {
+            for (int q = 0; q <= r; ++q) {
+                ctx[q].release();
+                if (sts[q]) cudaStreamDestroy(sts[q]);
+            }
+            return cuda_fail(cudaGetLastError(), "loopback setup");
+        }
+    }
+    cudaDeviceSynchronize();  // the caller's prior work on keys is complete
+    std::vector<std::thread> th;
+    for (int r = 0; r < P; ++r)
+        th.emplace_back([&, r] {
+            cudaSetDevice(dev);
+            res[r] = body(ctx[r], keys + off[r], ns[r], sts[r], r);
+        });
+    for (auto& t : th) t.join();
+    for (int r = 0; r < P; ++r) {
+        ctx[r].release();
+        cudaStreamDestroy(sts[r]);
+    }
+    for (int r = 0; r < P; ++r)
+        if (res[r] != PP_OK) return res[r];
+    return PP_OK;
+}
+
+template <typename K>
+pp_status partition_dist_loopback(K* keys, const uint64_t* ns, int P, K pivot, uint64_t* split_out) {
+    std::vector<uint64_t> Ks(P > 0 ? P : 1, 0);
+    pp_status s = loopback_run<K>(keys, ns, P, [&](DistCtx& c, K* shard, uint64_t n, cudaStream_t st, int r) {
+        return partition_dist_ctx<K>(c, shard, n, pivot, st, &Ks[r]);
+    });
+    if (s != PP_OK) return s;
+    for (int r = 1; r < P; ++r)
+        if (Ks[r] != Ks[0]) {
+            set_error("loopback: ranks disagree on the global split");
+            return PP_E_INTERNAL;
+        }
+    if (split_out) *split_out = Ks[0];
+    return PP_OK;
+}
+template pp_status partition_dist_loopback<uint64_t>(uint64_t*, const uint64_t*, int, uint64_t, uint64_t*);
+template pp_status partition_dist_loopback<uint32_t>(uint32_t*, const uint64_t*, int, uint32_t, uint64_t*);
+
+template <typename K>
+pp_status quicksort_dist_loopback(K* keys, const uint64_t* ns, int P, uint64_t small) {
+    return loopback_run<K>(keys, ns, P, [&](DistCtx& c, K* shard, uint64_t n, cudaStream_t st, int) {
+        return quicksort_dist_ctx<K>(c, shard, n, st, small);
+    });
+}
+template pp_status quicksort_dist_loopback<uint64_t>(uint64_t*, const uint64_t*, int, uint64_t);
+template pp_status quicksort_dist_loopback<uint32_t>(uint32_t*, const uint64_t*, int, uint64_t);
+
+// ---------------------------------------------------------------------------
+// Host arithmetic exported for tests.
+// ---------------------------------------------------------------------------
 pp_status dist_p2p_pieces(const uint64_t* ns, const uint64_t* ts, int P, int rank, uint64_t* out, uint64_t out_cap,
                           uint64_t* n_out) {
     if (!ns || !ts || P < 1 || rank < 0 || rank >= P || !n_out) return PP_E_INVAL;
     for (int r = 0; r < P; ++r)
         if (ts[r] > ns[r]) return PP_E_INVAL;
-    std::vector<P2PPiece> pcs;
-    p2p_pieces(ns, ts, P, rank, pcs);
+    std::vector<Run> runs, pcs;
+    match_runs(ns, ts, P, runs);
+    p2p_share(runs, rank, pcs);
     *n_out = pcs.size();
     if (out) {
         for (size_t k = 0; k < pcs.size() && k < out_cap; ++k) {
             uint64_t* o = out + 5 * k;
-            o[0] = pcs[k].rank_a;
+            o[0] = pcs[k].ra;
             o[1] = pcs[k].a;
-            o[2] = pcs[k].rank_b;
+            o[2] = pcs[k].rb;
             o[3] = pcs[k].b;
             o[4] = pcs[k].len;
         }

@@ -65,6 +65,10 @@ struct Params {
                                    // (0 auto: 4 for u64, 2 for u32 -- measured)
     int64_t qs_minl = 0;           // quicksort: at least this many lines per group for mid segments (0 auto: 128 KiB)
     int64_t dist_p2p = 0;          // pp_partition_dist: 1 = one-sided exchange over CUDA-IPC peer mappings (no staging)
+    int64_t dist_timeout_ms = 600000;  // distributed calls: a wait longer than this aborts (PP_E_NCCL on every rank)
+    int64_t dist_fault = 0;        // test hook (loopback): 1 = rank dist_fault_rank fails its local step, 2 = it never arrives
+    int64_t dist_fault_rank = -1;
+    int64_t dist_small = 1 << 16;  // distributed quicksort: spanning segments <= this are gathered and sorted locally
     int64_t host_chunk = 1 << 22;  // host-buffer partition: keys per streamed chunk
     int64_t qs_heavy = 1 << 22;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
 };
@@ -119,6 +123,10 @@ pp_status dist_plan(const uint64_t* ns, const uint64_t* ts, int P, uint64_t cap,
                     uint64_t* n_out, uint64_t* K_out);
 template <typename K>
 pp_status quicksort_dist(K* shard, uint64_t n_local, cudaStream_t st, uint64_t small);
+template <typename K>
+pp_status partition_dist_loopback(K* keys, const uint64_t* ns, int P, K pivot, uint64_t* split_out);
+template <typename K>
+pp_status quicksort_dist_loopback(K* keys, const uint64_t* ns, int P, uint64_t small);
 template <typename K>
 pp_status swap_ranges(const uint64_t* host_tri, uint64_t np, cudaStream_t st);
 pp_status dist_p2p_pieces(const uint64_t* ns, const uint64_t* ts, int P, int rank, uint64_t* out, uint64_t out_cap,

@@ -20,6 +20,7 @@
 //                        exactly one CTA (EREW).
 // No atomics anywhere; all reductions are fixed-order.  The cleanup kernels
 // are chained with programmatic dependent launch (griddepcontrol).
+#include <atomic>
 #include <algorithm>
 #include <cstdio>
 #include <vector>
@@ -409,11 +410,9 @@ __global__ void __launch_bounds__(SW_NT) small_partition_kernel(K* __restrict__ 
 // ===========================================================================
 // Host driver.
 // ===========================================================================
-static uint64_t g_launches = 0;
+static std::atomic<uint64_t> g_launches{0};
 uint64_t launch_count(int reset) {
-    uint64_t v = g_launches;
-    if (reset) g_launches = 0;
-    return v;
+    return reset ? g_launches.exchange(0) : g_launches.load();
 }
 void note_launches(uint64_t k) { g_launches += k; }
 

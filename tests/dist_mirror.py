@@ -1,5 +1,10 @@
-"""Multi-GPU in-place partition of one array sharded contiguously over ranks
-(BASELINE config 3).
+"""TEST MIRROR (test infrastructure, not the product path) of the multi-GPU
+in-place partition of one array sharded contiguously over ranks (BASELINE
+config 3).  The product path is the C ABI
+(pp_partition_dist_* / pp_quicksort_dist_*, csrc/pp_dist.cu); this is an
+independent Python re-statement of its exchange plan and round schedule,
+cross-checked against the C plan and run over torch.distributed (gloo) with
+oracle local steps in tests/test_dist.py.
 
 One process per GPU.  Rank r holds the contiguous shard A[β_r, β_r + n_r) of
 the global array.  A global partition needs exactly one exchange step:
@@ -142,8 +147,7 @@ class Partitioner:
         self.world = dist.get_world_size(group)
         self.staging_bytes = staging_bytes
         if local_partition is None:
-            from . import pp_partition
-            local_partition = pp_partition
+            raise ValueError("the mirror needs an injected local_partition (tests use the oracle)")
         self.local_partition = local_partition
         self.last_global_split = None
         self.last_plan = None
@@ -212,8 +216,7 @@ class Partitioner:
         segments in key order, so one local sort per rank finishes the job."""
         torch, dist = self.torch, self.dist
         if local_sort is None:
-            from . import pp_quicksort
-            local_sort = pp_quicksort
+            raise ValueError("the mirror needs an injected local_sort (tests use the oracle)")
         bits = 64 if shard.element_size() == 8 else 32
         umask = (1 << bits) - 1
         n_me = torch.tensor([shard.numel()], dtype=torch.int64, device=self.device)

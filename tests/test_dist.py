@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_2004_12532_b200.dist import Partitioner, exchange_plan, my_ops, schedule_rounds
+from dist_mirror import Partitioner, exchange_plan, my_ops, schedule_rounds
 
 
 def _simulate(shards, pivot):
@@ -113,7 +113,7 @@ def test_p2p_shares_cover_the_plan_once():
     the plan exactly once, each rank's rows involve itself, and executing all
     shares (in any rank order) partitions the global array."""
     import paper_2004_12532_b200 as pp
-    from paper_2004_12532_b200.dist import p2p_pieces
+    from dist_mirror import p2p_pieces
     rng = np.random.default_rng(2026)
     for trial in range(150):
         P = int(rng.integers(1, 10))

@@ -1,6 +1,10 @@
-"""GPU: the C-ABI multi-GPU partition (pp_dist_*) on a single-rank NCCL
-communicator (only one GPU is available to the tests; the exchange logic
-with several ranks is covered on CPU by tests/test_dist.py)."""
+"""GPU: the C-ABI multi-GPU partition and quicksort (pp_dist_*).
+
+* The product code path at P > 1 on one GPU: the loopback transport runs P
+  emulated ranks (host threads, disjoint slices of one device array) through
+  the SAME plan -> rounds -> staging -> place code and the one-sided share
+  rule as the NCCL path (pp_*_dist_loopback_*), checked against the oracle.
+* The NCCL transport itself on a single-rank communicator (one GPU)."""
 import numpy as np
 import pytest
 
@@ -197,3 +201,159 @@ def test_dist_last_timing_single_rank(pp):
     tm = pp.pp_dist_last_timing()
     assert tm["local_ms"] > 0 and tm["gather_ms"] >= 0 and tm["exchange_ms"] >= 0
     assert tm["bytes"] == 0
+
+
+# ---------------------------------------------------------------------------
+# P > 1 through the product code (loopback transport)
+# ---------------------------------------------------------------------------
+def _shards(rng, total, P, kind):
+    """Shard sizes summing to total: ragged, with empty shards (kind 'empty'),
+    or equal."""
+    if kind == "equal":
+        ns = [total // P] * P
+        ns[-1] += total - sum(ns)
+        return ns
+    cuts = np.sort(rng.integers(0, total + 1, size=P - 1))
+    ns = [int(x) for x in np.diff(np.concatenate([[0], cuts, [total]]))]
+    if kind == "empty" and P > 2:
+        ns[1] += ns[0]
+        ns[0] = 0  # an empty first shard
+        ns[-2] += ns[-1]
+        ns[-1] = 0  # and an empty last one
+    return ns
+
+
+def _keys(rng, total, dt, dist_kind):
+    mx = (1 << 64) - 1 if dt == np.uint64 else (1 << 32) - 1
+    if dist_kind == "uniform":
+        return rng.integers(0, mx, size=total, dtype=dt, endpoint=True)
+    if dist_kind == "dup":
+        return rng.integers(0, 1000, size=total).astype(dt)
+    if dist_kind == "equal":
+        return np.full(total, 12345, dtype=dt)
+    if dist_kind == "max":
+        return np.full(total, mx, dtype=dt)
+    raise ValueError(dist_kind)
+
+
+@pytest.mark.parametrize("P", [2, 3, 5, 8])
+@pytest.mark.parametrize("dt", [np.uint64, np.uint32])
+@pytest.mark.parametrize("p2p", [0, 1])
+def test_loopback_partition(pp, P, dt, p2p):
+    """Global partition of P contiguous shards (ragged, empty, equal) by the
+    product exchange: oracle checks (1)-(3) on the whole array, K = oracle
+    count; pivots 0, MAX, mid and skewed; staging caps 4 KiB .. 256 MiB (the
+    staged path runs hundreds of rounds at 4 KiB)."""
+    from gpu_util import to_dev, to_host
+    rng = np.random.default_rng(1000 * P + 10 * (dt == np.uint64) + p2p)
+    mx = (1 << 64) - 1 if dt == np.uint64 else (1 << 32) - 1
+    pp.pp_set_param("dist_p2p", p2p)
+    try:
+        for total, kind, cap in ((1, "ragged", 1 << 12), (977, "empty", 1 << 12), (300_007, "ragged", 1 << 12),
+                                 (1_000_003, "empty", 1 << 16), (1 << 22, "equal", 256 << 20)):
+            ns = _shards(rng, total, P, kind)
+            a = _keys(rng, total, dt, "uniform")
+            pp.pp_dist_set_staging(cap)
+            for pivot in (0, mx, (mx + 1) // 2, int(mx // 100), int(rng.integers(0, mx, dtype=dt))):
+                t = to_dev(a)
+                K = pp.pp_partition_dist_loopback(t, ns, pivot)
+                assert K == oracle.count(a, pivot)
+                oracle.check_partition(a, to_host(t, dt), pivot, K)
+    finally:
+        pp.pp_dist_set_staging(256 << 20)
+        pp.reset_params()
+
+
+def test_loopback_partition_deterministic(pp):
+    """Two runs of the loopback exchange give identical bytes (EREW
+    determinism): the plan and the pieces are a pure function
+    of the input."""
+    from gpu_util import to_dev
+    a = synth.uniform_u64_np(2_000_003, 91)
+    ns = [300_000, 0, 700_000, 1_000_003]
+    outs = []
+    for _ in range(2):
+        t = to_dev(a)
+        pp.pp_dist_set_staging(1 << 16)
+        pp.pp_partition_dist_loopback(t, ns, 1 << 63)
+        outs.append(t.cpu().numpy())
+    pp.pp_dist_set_staging(256 << 20)
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("P", [2, 3, 5, 8])
+@pytest.mark.parametrize("dt", [np.uint64, np.uint32])
+def test_loopback_quicksort(pp, P, dt):
+    """Distributed quicksort through the product code (batched pivot gather,
+    batched partition of the spanning segments, gather-sort of small spanning
+    segments, local sorts), byte for byte against oracle.quicksort; small
+    dist_small forces several distributed levels, the default takes the
+    gather-sort path."""
+    from gpu_util import to_dev, to_host
+    rng = np.random.default_rng(77 * P + (dt == np.uint64))
+    try:
+        for total, kind, dk, small in ((2, "ragged", "uniform", 1 << 16), (1000, "empty", "uniform", 1 << 16),
+                                       (200_003, "ragged", "uniform", 1000), (300_001, "empty", "dup", 1000),
+                                       (100_000, "equal", "equal", 1000), (50_001, "ragged", "max", 1000),
+                                       (1 << 20, "equal", "uniform", 1 << 16)):
+            pp.pp_set_param("dist_small", small)
+            ns = _shards(rng, total, P, kind)
+            a = _keys(rng, total, dt, dk)
+            t = to_dev(a)
+            pp.pp_quicksort_dist_loopback(t, ns)
+            ref = a.copy()
+            oracle.quicksort(ref)
+            assert np.array_equal(to_host(t, dt), ref), (total, kind, dk, small)
+    finally:
+        pp.reset_params()
+
+
+def test_loopback_quicksort_p2p(pp):
+    """The distributed quicksort with the one-sided exchange."""
+    from gpu_util import to_dev, to_host
+    a = synth.uniform_u64_np(400_009, 5)
+    ns = [100_000, 0, 150_000, 150_009]
+    pp.pp_set_param("dist_p2p", 1)
+    pp.pp_set_param("dist_small", 2000)
+    try:
+        t = to_dev(a)
+        pp.pp_quicksort_dist_loopback(t, ns)
+    finally:
+        pp.reset_params()
+    ref = a.copy()
+    oracle.quicksort(ref)
+    assert np.array_equal(to_host(t, np.uint64), ref)
+
+
+@pytest.mark.parametrize("fault", [1, 2])
+@pytest.mark.parametrize("rank", [0, 2])
+def test_loopback_failure_agreement(pp, fault, rank):
+    """A rank that fails its local step (fault 1) is reported by EVERY rank
+    (status agreement; no hang); a rank that never arrives (fault 2) makes
+    the others time out (dist_timeout_ms) instead of hanging.  The array stays
+    a permutation of the input."""
+    import time
+    from gpu_util import to_dev, to_host
+    a = synth.uniform_u64_np(500_000, 8)
+    ns = [100_000, 150_000, 200_000, 50_000]
+    pp.pp_set_param("dist_fault", fault)
+    pp.pp_set_param("dist_fault_rank", rank)
+    pp.pp_set_param("dist_timeout_ms", 3000)
+    try:
+        for call in ("partition", "quicksort"):
+            t = to_dev(a)
+            t0 = time.time()
+            with pytest.raises(pp.PPError) as ei:
+                if call == "partition":
+                    pp.pp_partition_dist_loopback(t, ns, 1 << 63)
+                else:
+                    pp.pp_quicksort_dist_loopback(t, ns)
+            assert time.time() - t0 < 60
+            assert ei.value.status in (4, 5)  # PP_E_NCCL (timeout) / PP_E_INTERNAL (injected)
+            assert np.array_equal(np.sort(to_host(t, np.uint64)), np.sort(a))
+    finally:
+        pp.reset_params()
+    # the library still works afterwards
+    t = to_dev(a)
+    K = pp.pp_partition_dist_loopback(t, ns, 1 << 63)
+    oracle.check_partition(a, to_host(t, np.uint64), 1 << 63, K)
