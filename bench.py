@@ -1,26 +1,30 @@
 #!/usr/bin/env python
 """bench.py -- BASELINE metric: partition keys/s and GB/s (fraction of the HBM
-read+write roofline) on B200; quicksort keys/s.
+read+write roofline) at 1/2/4/8 B200; quicksort keys/s.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (BASELINE.json configs[1]): in-place
-partition of n = 2^27 uint64 keys, i.i.d. uniform from the splitmix64 stream
-(seed c2), pivot 2^63 (mu = 0.5).  One step = one full pp_partition (all
-kernels of the hot path) over a fresh copy of the input resident in HBM.
-Every timed step partitions its own fresh copy of the input (K copies made
-before the timed region; inputs are larger than L2, so no flush is needed)
-and the K steps run back to back between two CUDA events on the launching
-stream (per-step events are recorded too).
+Headline workload (BASELINE.json configs[2], the configuration the metric is
+quoted on "at 1/2/4/8 B200"): in-place partition of the GLOBAL
+array of n = 2^33 uint64 keys (64 GiB), i.i.d. uniform from the splitmix64
+stream (seed c3; key_i depends only on the global index i), pivot 2^63
+(mu = 0.5), sharded contiguously over the N ranks (2^33/N keys per GPU:
+64 GiB at N = 1, 8 GiB at N = 8) -- strong scaling.  One step = one full
+partition of the whole array: at N = 1 pp_partition_async_u64 (all kernels
+of the hot path); at N > 1 (torchrun) pp_partition_dist_u64 on every rank
+(local partition, ncclAllGather of (status, n_r, t_r, pivot), the exchange of
+misplaced ranges over NCCL/NVLink).  Before every timed step the shard is
+restored from a pristine device copy (or regenerated when two copies do not
+fit), untimed; each step is bracketed by a barrier + synchronize and CUDA
+events on the launching stream; the step time is the max over ranks.  The
+inputs (>= 8 GiB per GPU) are far larger than L2.
 
-N > 1 (torchrun): each rank partitions its own contiguous 2^27-key shard of
-one global array (weak scaling) and the ranks exchange misplaced ranges over
-NCCL to complete the GLOBAL partition (C ABI pp_partition_dist_u64: local
-partition, ncclAllGather of the counts, ncclSend/ncclRecv of misplaced
-ranges); the step time is the max over ranks.
+The c2 line (2^27 keys, mu = 0.01 / 0.5 / 0.99, aux memory), config 1, 4 and
+5 and the comparison rows go to "extras" (rank 0, N = 1).
 
 --impl reference: the CPU oracle (oracle/, serial two-pointer partition,
-PAPER.md:1433-1436) on the host cores, same workload and metric.
+PAPER.md:1433-1436) on the host cores, on a bounded sample of the same
+workload (the first 2^27 keys of the c3 array per step).
 """
 from __future__ import annotations
 
@@ -38,11 +42,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_KEYS = 1 << 27
+N_TOTAL = 1 << 33  # BASELINE config 3: the global array
+N_C2 = 1 << 27     # BASELINE config 2
+N_REF_SAMPLE = 1 << 27  # CPU oracle sample per step (the reference arm / cpu_baseline)
+E2E_SAMPLE = 1 << 30    # per-rank host-buffer sample for the end-to-end number
 PIVOT = 1 << 63
 L2_FLUSH_BYTES = 512 << 20
 METRIC = "partition keys/s and GB/s (fraction of HBM roofline) at 1/2/4/8 B200; quicksort keys/s"
-WORKLOAD = "c2: in-place partition, n=2^27 uint64 uniform keys (1 GiB), pivot 2^63 (mu=0.5), 1 GPU per rank"
+WORKLOAD = ("c3: in-place partition of the global array, n=2^33 uint64 uniform keys (64 GiB), pivot 2^63 "
+            "(mu=0.5), sharded contiguously over the GPUs (strong scaling)")
 
 
 def peaks():
@@ -129,13 +137,15 @@ def dist_env():
 
 
 def run_reference(args):
-    """CPU oracle arm: serial two-pointer partition on the host."""
+    """CPU oracle arm: the serial two-pointer partition on the host, each step
+    a bounded sample of the headline workload (the first 2^27 keys of the c3
+    array, fresh copy each step); rank 0 only."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
     import oracle
     import synth
-    pristine = synth.uniform_u64_np(N_KEYS, synth.SEEDS["c2"])
+    pristine = synth.uniform_u64_np(N_REF_SAMPLE, synth.SEEDS["c3"])
     work = np.empty_like(pristine)
     for _ in range(args.warmup):
         np.copyto(work, pristine)
@@ -147,15 +157,17 @@ def run_reference(args):
         split = oracle.partition_two_pointer(work, PIVOT)
         times.append(time.perf_counter() - t0)
     tot = sum(times)
-    value = N_KEYS * args.steps / tot
+    value = N_REF_SAMPLE * args.steps / tot
+    sample = (f"first 2^27 keys of the c3 array (global indices 0..2^27-1) per step, {args.steps} timed steps, "
+              f"fresh copy each, serial oracle on 1 host thread")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n": N_KEYS, "pivot": PIVOT, "split": split},
-        "gbs": 2 * 8 * N_KEYS * args.steps / tot / 1e9,
-        "cpu_baseline": {"value": value, "unit": "keys/s", "cores": 1, "kind": "oracle",
-                         "sample": f"full c2 input (2^27 keys), {args.steps} timed steps, fresh copy each",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n": N_TOTAL, "sample_keys_per_step": N_REF_SAMPLE, "pivot": PIVOT,
+                   "split_of_sample": split},
+        "gbs": 2 * 8 * N_REF_SAMPLE * args.steps / tot / 1e9,
+        "cpu_baseline": {"value": value, "unit": "keys/s", "cores": 1, "kind": "oracle", "sample": sample,
                          "host": host_info()},
         "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -164,9 +176,11 @@ def run_reference(args):
 
 
 def cpu_baseline(budget_s: float = 12.0):
+    """The oracle as it stands on a bounded sample of the headline workload
+    (the first 2^27 keys of the c3 array), 1 host thread."""
     import oracle
     import synth
-    pristine = synth.uniform_u64_np(N_KEYS, synth.SEEDS["c2"])
+    pristine = synth.uniform_u64_np(N_REF_SAMPLE, synth.SEEDS["c3"])
     work = np.empty_like(pristine)
     times = []
     t_start = time.perf_counter()
@@ -175,9 +189,9 @@ def cpu_baseline(budget_s: float = 12.0):
         t0 = time.perf_counter()
         oracle.partition_two_pointer(work, PIVOT)
         times.append(time.perf_counter() - t0)
-    v = N_KEYS * len(times) / sum(times)
+    v = N_REF_SAMPLE * len(times) / sum(times)
     return {"value": v, "unit": "keys/s", "cores": 1, "kind": "oracle",
-            "sample": f"full c2 input (2^27 keys), {len(times)} runs of the serial two-pointer oracle, "
+            "sample": f"first 2^27 keys of the c3 array, {len(times)} runs of the serial two-pointer oracle, "
                       f"fresh copy each, 1 host thread", "host": host_info()}
 
 
@@ -219,6 +233,14 @@ def cpu_quicksort_baseline(budget_s: float = 8.0):
     return res
 
 
+def shard_range(rank: int, ws: int, n_total: int):
+    """Contiguous shards of the global array in rank order (the last rank takes
+    the remainder)."""
+    per = n_total // ws
+    off = rank * per
+    return off, (n_total - off if rank == ws - 1 else per)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -227,7 +249,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip the mu sweep and quicksort lines")
+    ap.add_argument("--no-extras", action="store_true", help="skip the c1/c2/c4/c5 and comparison lines")
+    ap.add_argument("--n-total", type=int, default=N_TOTAL,
+                    help="global keys (default 2^33 = BASELINE config 3; smaller only for quick checks)")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU code path (NCCL process group, pp_partition_dist) even at one rank")
     args = ap.parse_args()
@@ -254,14 +278,22 @@ def main():
         pp.pp_set_param(k, int(v))
     stream = torch.cuda.current_stream()
 
-    n = N_KEYS
-    pristine = synth.uniform_u64_torch(n, synth.SEEDS["c2"], dev, offset=rank * n)
-    # one fresh 1 GiB input per timed step (K GiB of HBM): the K steps run
-    # back to back with no restore traffic in between; each input is larger
-    # than L2 and untouched since its copy, so no L2 flush is needed
-    bufs = [pristine.clone() for _ in range(args.steps)]
-    work = torch.empty_like(pristine)
-    flush = torch.ones(L2_FLUSH_BYTES // 8, dtype=torch.int64, device=dev)
+    n_total = args.n_total
+    off, n = shard_range(rank, ws, n_total)
+    seed = synth.SEEDS["c3"]
+    work = torch.empty(n, dtype=torch.int64, device=dev)
+    synth.uniform_u64_torch(n, seed, dev, offset=off, out=work, chunk=1 << 27)
+    free, _ = torch.cuda.mem_get_info(dev)
+    pristine = None
+    if free > 8 * n + (6 << 30):  # a pristine copy fits: restore by D2D copy (else regenerate)
+        pristine = work.clone()
+
+    def restore():
+        if pristine is not None:
+            work.copy_(pristine)
+        else:
+            synth.uniform_u64_torch(n, seed, dev, offset=off, out=work, chunk=1 << 27)
+
     d_split = torch.zeros(1, dtype=torch.int64, device=dev)
     last_split = [None]
     if dist_on:
@@ -271,74 +303,67 @@ def main():
         dist.broadcast_object_list(uid, src=0)
         pp.pp_dist_init(uid[0], ws, rank, local)
 
-    def step(buf):
+    def step():
         if dist_on:
-            last_split[0] = pp.pp_partition_dist(buf, PIVOT)
+            last_split[0] = pp.pp_partition_dist(work, PIVOT)
         else:
-            pp.pp_partition_async_u64(buf, PIVOT, d_split)
+            pp.pp_partition_async_u64(work, PIVOT, d_split)
 
-    # warm-up (W steps on restored input), then ~0.5 s of back-to-back
-    # partitions of the warm-up buffer so the clock sampler sees the GPU in
-    # this load's steady state before and during the timed region
+    def sync_all():
+        torch.cuda.synchronize()
+        if dist_on:
+            dist.barrier()
+        torch.cuda.synchronize()
+
     sampler = ClockSampler(local)
     sampler.start()
     for _ in range(args.warmup):
-        work.copy_(pristine)
-        step(work)
+        restore()
+        step()
     torch.cuda.synchronize()
-    t_end = time.perf_counter() + 0.5
-    while time.perf_counter() < t_end:
-        for _ in range(8):
-            step(work)
-        torch.cuda.synchronize()
-    flush.sum()  # evict the warm-up buffer from L2
 
-    # ---- timed region: K steps back to back.  No library-internal events
-    #      here: an event between the group kernel and its PDL-launched
-    #      cleanup costs ~12 us per step (tools/timing_overhead.py) ----
-    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if dist_on:
-        dist.barrier()
-    torch.cuda.synchronize()
-    pp.pp_launch_count(reset=True)
+    # ---- timed region: K steps; each restored untimed, then bracketed by a
+    #      barrier + synchronize and CUDA events on the launching stream.  No
+    #      library-internal events here (an event between the group kernel and
+    #      its PDL-launched cleanup costs ~12 us; tools/timing_overhead.py) ----
     pp.pp_timing(False)
-    for i in range(args.steps):
-        ev_s[i].record(stream)
-        step(bufs[i])
-        ev_e[i].record(stream)
-    torch.cuda.synchronize()
-    if dist_on:
-        dist.barrier()
-    launches = pp.pp_launch_count()
-    step_ms = [s.elapsed_time(e) for s, e in zip(ev_s, ev_e)]
-    tot_ms = ev_s[0].elapsed_time(ev_e[-1])  # the whole back-to-back region
-    # ---- the same K steps again on fresh copies (restored untimed), with the
-    #      library's CUDA events around the group kernel on the launching
-    #      stream: its live duration for the roofline ----
-    for b in bufs:
-        b.copy_(pristine)
-    torch.cuda.synchronize()
-    if dist_on:
-        dist.barrier()
-    pp.pp_timing(True)
+    step_ms, launches = [], 0
     phases = []
     for i in range(args.steps):
-        step(bufs[i])
+        restore()
+        sync_all()
+        pp.pp_launch_count(reset=True)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        step()
+        e.record(stream)
+        sync_all()
+        launches += pp.pp_launch_count()
+        step_ms.append(s.elapsed_time(e))
         if dist_on:
             phases.append(pp.pp_dist_last_timing())
+    # ---- a second pass with the library's CUDA events around the group
+    #      kernel on the launching stream: its live duration for the roofline ----
+    reps2 = min(args.steps, 5)
+    pp.pp_timing(True)
+    for i in range(reps2):
+        restore()
+        torch.cuda.synchronize()
+        step()
     torch.cuda.synchronize()
     tim = pp.pp_timing_read()
     pp.pp_timing(False)
     clocks = sampler.stop()
-    del bufs
+    split = int(d_split.item()) if not dist_on else last_split[0]
+    stats = pp.pp_last_stats() if not dist_on else {}
+
     exchange = None
+    tot_ms = sum(step_ms)
     if dist_on:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
-        # exchange phase: NVLink GB/s = bytes a GPU moved / exchange time,
-        # max over ranks of the per-step averages (library events, second pass)
+        t = torch.tensor(step_ms, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # per step: max over ranks
+        step_ms = [float(x) for x in t.tolist()]
+        tot_ms = sum(step_ms)
         k = max(len(phases), 1)
         loc = [sum(p[f] for p in phases) / k for f in ("local_ms", "gather_ms", "exchange_ms", "bytes")]
         tt = torch.tensor(loc, dtype=torch.float64, device=dev)
@@ -348,42 +373,42 @@ def main():
                     "local_partition_ms": lm, "allgather_ms": gm, "exchange_ms": xm, "bytes_per_gpu": xb,
                     "nvlink_gbs": (xb / (xm / 1e3) / 1e9) if xm > 0 else None,
                     "frac_of_900_gbs": (xb / (xm / 1e3) / 1e9 / 900.0) if xm > 0 else None,
-                    "timing": "library CUDA events on the call's stream (second pass), max over ranks"}
+                    "local_hbm_gbs": (16 * n / (lm / 1e3) / 1e9) if lm > 0 else None,
+                    "timing": "library CUDA events on the call's stream (timed steps), per-rank means, max over ranks"}
 
-    # sanity: the split equals the oracle's count on this input (cheap check)
-    split = int(d_split.item()) if not dist_on else last_split[0]
-    stats = pp.pp_last_stats() if not dist_on else {}
-
-    value = ws * n * args.steps / (tot_ms / 1e3)
+    value = n_total * args.steps / (tot_ms / 1e3)
     ms_per_step = tot_ms / args.steps
-    bytes_step = 2 * 8 * n
+    bytes_step = 2 * 8 * n_total
     peak, peak_kind = peaks()
-    # dominant kernel: the Smoothed Striding group kernel (every full line
-    # read once + written once): algorithmic bytes per launch
+    # dominant kernel: the Smoothed Striding group kernel (every full line read
+    # once + written once): algorithmic bytes per launch
     line_keys = stats.get("line_keys", 1024)
     grp_bytes = 2 * 8 * stats.get("n_lines", n // 1024) * line_keys
     grp_ms = tim["group_ms"] / max(tim["calls"], 1)
     achieved = grp_bytes / (grp_ms / 1e3) / 1e9 if grp_ms > 0 else None
     traffic = ncu_traffic()
+    gbs = bytes_step / (ms_per_step / 1e3) / 1e9
 
     out = {
         "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n_per_gpu": n, "pivot": PIVOT, "mu": 0.5,
-                   "parallelism": f"dp{ws}" if dist_on else "single",
-                   "l2": "inputs larger than L2: each of the K back-to-back steps partitions its own fresh "
-                         "1 GiB copy of the input (K GiB resident in HBM)"},
-        "gbs": ws * bytes_step * args.steps / (tot_ms / 1e3) / 1e9,
-        "frac_of_8tbs": (bytes_step / (ms_per_step / 1e3) / 1e9) / 8000.0,
-        "frac_of_measured_hbm": (bytes_step / (ms_per_step / 1e3) / 1e9) / peak,
+        "config": {"workload": WORKLOAD if n_total == N_TOTAL else f"{WORKLOAD} [reduced: n={n_total}]",
+                   "n": n_total, "n_per_gpu": n, "pivot": PIVOT, "mu": 0.5,
+                   "parallelism": f"dp{ws} (contiguous shards + NCCL exchange)" if dist_on else "single",
+                   "l2": "inputs larger than L2 (>= 8 GiB per GPU); every step restores its shard untimed "
+                         + ("(D2D copy from a pristine copy)" if pristine is not None else "(regenerated)")},
+        "gbs": gbs,
+        "frac_of_8tbs": gbs / ws / 8000.0,
+        "frac_of_measured_hbm": gbs / ws / peak,
+        "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "ss_group_kernel", "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": grp_bytes, "avg_launch_ms": grp_ms,
                      "kernel_share_of_step": (tim["group_ms"] / tim["total_ms"]) if tim["total_ms"] else None,
-                     "timing": "group kernel bracketed by CUDA events on the launching stream in a second pass of "
-                               "the same K steps (fresh copies); the K timed steps run without these events"},
+                     "timing": f"group kernel bracketed by CUDA events on the launching stream in a second pass "
+                               f"of {reps2} steps (restored untimed); the timed steps run without these events"},
         "gpu_launches": launches,
         "clocks": clocks,
         **({"exchange": exchange} if exchange else {}),
@@ -392,20 +417,26 @@ def main():
         "aux_bytes": stats.get("aux_bytes"),
         "aux_frac": (stats.get("aux_bytes", 0) / (8 * n)) if stats else None,
     }
+    if not dist_on:
+        # split sanity vs the closed form: a device compare-and-count (torch)
+        # of the restored input -- the oracle's exact check runs in the tests
+        restore()
+        C = 1 << 28
+        out["split_ok"] = split == sum(int(((work[s:s + C] ^ (-(1 << 63))) < 0).sum().item())
+                                       for s in range(0, n, C))
+    del work, pristine
+    torch.cuda.empty_cache()
 
+    if not args.no_e2e:
+        out["e2e"] = e2e(pp, torch, dist if dist_on else None, rank, ws, off, n, args)
     if rank == 0 and not dist_on:
-        if not args.no_e2e:
-            out["e2e"] = e2e(pp, n, args)
+        flush = torch.ones(L2_FLUSH_BYTES // 8, dtype=torch.int64, device=dev)
         if not args.no_extras:
-            out["extras"] = extras(pp, torch, synth, dev, stream, flush)
+            out["extras"] = extras(pp, torch, synth, dev, stream, flush, args)
         if not args.no_cpu_baseline:
-            cb = cpu_baseline()
-            out["cpu_baseline"] = cb
+            out["cpu_baseline"] = cpu_baseline()
             if not args.no_extras:
                 out["extras"]["cpu_quicksort_sample"] = cpu_quicksort_baseline()
-        # split sanity vs oracle count (oracle used only as a reported check)
-        import oracle
-        out["split_ok"] = (split == oracle.count(pristine.cpu().numpy().view(np.uint64), PIVOT))
     if rank == 0:
         print(json.dumps(out))
     if dist_on:
@@ -414,37 +445,77 @@ def main():
     return 0
 
 
-def e2e(pp, n, args):
-    """End to end through the public host API: pinned host buffer -> H2D ->
-    partition -> D2H of the whole array and the split, every step
-    (wall clock around the synchronous call)."""
-    import torch
+def e2e(pp, torch, dist, rank, ws, off, n, args):
+    """End to end through the public host-buffer API on every rank: a sample
+    of min(n_per_gpu, 2^30) keys of the rank's c3 shard in pinned host
+    memory; every step copies it in (H2D), partitions it on the GPU and
+    copies the whole partitioned sample and the split back (D2H) --
+    pp_partition_host_u64 (the streamed host partition),
+    host wall clock around the synchronous call.  At N > 1 the ranks run
+    concurrently (barrier around each step) and the value is the sum over
+    ranks; the NCCL exchange is not part of this number (it is in the
+    device-timed value)."""
     import synth
-    pristine = synth.uniform_u64_np(n, synth.SEEDS["c2"])
-    host = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    m = min(n, E2E_SAMPLE)
+    pristine = synth.uniform_u64_np(m, synth.SEEDS["c3"], offset=off)
+    host = torch.empty(m, dtype=torch.int64, pin_memory=True)
     hv = host.numpy().view(np.uint64)
-    steps = max(3, min(args.steps, 8))
+    steps = max(3, min(args.steps, 5))
     np.copyto(hv, pristine)
     pp.pp_partition_host_u64(hv, PIVOT)  # warm
     times = []
     for _ in range(steps):
         np.copyto(hv, pristine)
+        if dist:
+            dist.barrier()
         t0 = time.perf_counter()
         pp.pp_partition_host_u64(hv, PIVOT)
         times.append(time.perf_counter() - t0)
-    v = n * steps / sum(times)
-    return {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 8,
-            "steps": steps, "ms_per_step": 1e3 * sum(times) / steps, "api": "pp_partition_host_u64 (pinned host; streamed chunks: H2D from both ends, per-chunk GPU partition, D2H of each side overlapping the uploads)",
-            "timing": "host wall clock around the synchronous call"}
+    v = m * steps / sum(times)
+    if dist:
+        t = torch.tensor([v], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(t)
+        v = float(t.item())
+    return {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 8 * m * ws, "d2h_bytes_per_step": (8 * m + 8) * ws,
+            "steps": steps, "ms_per_step": 1e3 * sum(times) / steps, "sample_keys_per_gpu": m,
+            "api": "pp_partition_host_u64 (pinned host; streamed chunks: H2D from both ends, per-chunk GPU "
+                   "partition, D2H of each side overlapping the uploads)",
+            "timing": "host wall clock around the synchronous call; sample = the first min(n_per_gpu, 2^30) keys "
+                      "of each rank's c3 shard (PCIe-bound, size-independent beyond a few GiB)"}
 
 
-def extras(pp, torch, synth, dev, stream, flush):
-    """Secondary numbers: mu = 0.01 / 0.99 partition and the config-5 quicksort."""
+def extras(pp, torch, synth, dev, stream, flush, args):
+    """Secondary numbers (rank 0, N = 1): BASELINE config 2 (mu = 0.5, 0.01,
+    0.99, aux memory), the comparison rows, configs 5, 1 and 4."""
     res = {}
-    n = N_KEYS
+    n = N_C2
     pristine = synth.uniform_u64_torch(n, synth.SEEDS["c2"], dev)
-    buf = torch.empty_like(pristine)
     d = torch.zeros(1, dtype=torch.int64, device=dev)
+    # config 2 at mu = 0.5: K fresh 1 GiB copies partitioned back to back
+    # between two events (no restore traffic between steps; each copy is
+    # larger than L2 and untouched since its copy)
+    K = max(5, min(args.steps, 20))
+    bufs = [pristine.clone() for _ in range(K)]
+    for b in bufs[:3]:
+        pp.pp_partition_async_u64(b, PIVOT, d)
+    for b in bufs[:3]:
+        b.copy_(pristine)
+    flush.sum()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for b in bufs:
+        pp.pp_partition_async_u64(b, PIVOT, d)
+    e.record(stream)
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / K
+    st = pp.pp_last_stats()
+    res["c2_u64_2^27_mu0.5"] = {"keys_per_s": n / (ms / 1e3), "ms": ms, "gbs": 16 * n / (ms / 1e3) / 1e9,
+                                "window_frac": st["W"] / n, "aux_bytes": st["aux_bytes"],
+                                "aux_frac": st["aux_bytes"] / (8 * n), "split": int(d.item()),
+                                "timing": f"{K} fresh copies back to back between two events"}
+    del bufs
+    buf = torch.empty_like(pristine)
     for mu in (0.01, 0.99):
         p = synth.PIVOT_MU[mu]
         ts = []
@@ -460,8 +531,8 @@ def extras(pp, torch, synth, dev, stream, flush):
                 ts.append(s.elapsed_time(e))
         ms = statistics.mean(ts)
         st = pp.pp_last_stats()
-        res[f"partition_mu{mu}"] = {"keys_per_s": n / (ms / 1e3), "ms": ms,
-                                    "gbs": 16 * n / (ms / 1e3) / 1e9, "window_frac": st["W"] / n}
+        res[f"c2_u64_2^27_mu{mu}"] = {"keys_per_s": n / (ms / 1e3), "ms": ms, "gbs": 16 * n / (ms / 1e3) / 1e9,
+                                      "window_frac": st["W"] / n, "aux_frac": st["aux_bytes"] / (8 * n)}
     # Strided (X = 0) vs Smoothed Striding
     # (random X) on the c2 input and on the stride-aligned
     # adversary (line j true iff j mod g < g/2, g = the library's group count)
@@ -583,7 +654,7 @@ def extras(pp, torch, synth, dev, stream, flush):
     del c1src, c1bufs
     # BASELINE config 4: n = 1,000,000,007 u32 adversarial inputs, pivot 2^31
     n4 = 1_000_000_007
-    for pat in ("partitioned", "reverse", "alternating", "all_false"):
+    for pat in ("partitioned", "reverse", "alternating", "all_false", "all_true"):
         a0 = synth.adversarial_u32_torch(n4, pat, synth.SEEDS["c4"], dev)
         a = torch.empty_like(a0)
         d4 = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -632,30 +703,6 @@ def extras(pp, torch, synth, dev, stream, flush):
     res["c4_u32_zipf1.1_median"] = {"keys_per_s": n4 / (m / 1e3), "ms": m, "gbs": 8 * n4 / (m / 1e3) / 1e9,
                                     "pivot": zp, "window_frac": st["W"] / n4}
     del z0, z
-    # BASELINE config 3 at P = 1: n = 2^33 u64 (64 GiB) in one GPU
-    n3 = 1 << 33
-    try:
-        big = torch.empty(n3, dtype=torch.int64, device=dev)
-        synth.uniform_u64_torch(n3, synth.SEEDS["c3"], dev, out=big, chunk=1 << 27)
-        d3 = torch.zeros(1, dtype=torch.int64, device=dev)
-        ms = []
-        for i in range(2):
-            if i:
-                synth.uniform_u64_torch(n3, synth.SEEDS["c3"], dev, out=big, chunk=1 << 27)
-            torch.cuda.synchronize()
-            pp.pp_timing(True)
-            pp.pp_partition_async_u64(big, PIVOT, d3)
-            torch.cuda.synchronize()
-            t = pp.pp_timing_read()
-            pp.pp_timing(False)
-            ms.append(t["total_ms"])
-        m = min(ms)
-        st = pp.pp_last_stats()
-        res["c3_u64_2^33_1gpu"] = {"keys_per_s": n3 / (m / 1e3), "ms": m, "gbs": 16 * n3 / (m / 1e3) / 1e9,
-                                   "window_frac": st["W"] / n3}
-        del big
-    except RuntimeError as ex:  # not enough memory on this device
-        res["c3_u64_2^33_1gpu"] = {"skipped": str(ex)[:120]}
     return res
 
 

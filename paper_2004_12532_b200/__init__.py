@@ -141,10 +141,23 @@ def _check(status: int, where: str):
         raise PPError(status, where, load().pp_last_error().decode())
 
 
-def _stream_ptr(stream=None) -> int:
+def _stream_ptr(stream=None, device=None) -> int:
+    """The stream the call is enqueued on: the given one, else the current
+    stream of the keys' device (not of the current device)."""
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _split_word(d_split, keys) -> int:
+    """Device address of the 8-byte split word of the async variants."""
+    import torch
+    if not d_split.is_cuda or d_split.device != keys.device:
+        raise ValueError("d_split must be a CUDA tensor on the keys' device")
+    if d_split.dtype not in (torch.int64, torch.uint64) or d_split.numel() < 1:
+        raise TypeError("d_split must hold at least one int64/uint64 word")
+    return d_split.data_ptr()
 
 
 def _key_kind(t) -> str:
@@ -171,7 +184,7 @@ def _pivot(p: int, kind: str) -> int:
 def pp_partition_u64(keys, pivot: int, stream=None) -> int:
     assert _key_kind(keys) == "u64"
     out = ctypes.c_uint64(0)
-    _check(load().pp_partition_u64(keys.data_ptr(), keys.numel(), _pivot(pivot, "u64"), _stream_ptr(stream),
+    _check(load().pp_partition_u64(keys.data_ptr(), keys.numel(), _pivot(pivot, "u64"), _stream_ptr(stream, keys.device),
                                    ctypes.byref(out)), "pp_partition_u64")
     return int(out.value)
 
@@ -179,31 +192,33 @@ def pp_partition_u64(keys, pivot: int, stream=None) -> int:
 def pp_partition_u32(keys, pivot: int, stream=None) -> int:
     assert _key_kind(keys) == "u32"
     out = ctypes.c_uint64(0)
-    _check(load().pp_partition_u32(keys.data_ptr(), keys.numel(), _pivot(pivot, "u32"), _stream_ptr(stream),
+    _check(load().pp_partition_u32(keys.data_ptr(), keys.numel(), _pivot(pivot, "u32"), _stream_ptr(stream, keys.device),
                                    ctypes.byref(out)), "pp_partition_u32")
     return int(out.value)
 
 
 def pp_partition_async_u64(keys, pivot: int, d_split, stream=None) -> None:
-    assert _key_kind(keys) == "u64" and d_split.is_cuda and d_split.numel() >= 1
-    _check(load().pp_partition_async_u64(keys.data_ptr(), keys.numel(), _pivot(pivot, "u64"), _stream_ptr(stream),
-                                         d_split.data_ptr()), "pp_partition_async_u64")
+    assert _key_kind(keys) == "u64"
+    _check(load().pp_partition_async_u64(keys.data_ptr(), keys.numel(), _pivot(pivot, "u64"),
+                                         _stream_ptr(stream, keys.device), _split_word(d_split, keys)),
+           "pp_partition_async_u64")
 
 
 def pp_partition_async_u32(keys, pivot: int, d_split, stream=None) -> None:
-    assert _key_kind(keys) == "u32" and d_split.is_cuda and d_split.numel() >= 1
-    _check(load().pp_partition_async_u32(keys.data_ptr(), keys.numel(), _pivot(pivot, "u32"), _stream_ptr(stream),
-                                         d_split.data_ptr()), "pp_partition_async_u32")
+    assert _key_kind(keys) == "u32"
+    _check(load().pp_partition_async_u32(keys.data_ptr(), keys.numel(), _pivot(pivot, "u32"),
+                                         _stream_ptr(stream, keys.device), _split_word(d_split, keys)),
+           "pp_partition_async_u32")
 
 
 def pp_quicksort_u64(keys, stream=None) -> None:
     assert _key_kind(keys) == "u64"
-    _check(load().pp_quicksort_u64(keys.data_ptr(), keys.numel(), _stream_ptr(stream)), "pp_quicksort_u64")
+    _check(load().pp_quicksort_u64(keys.data_ptr(), keys.numel(), _stream_ptr(stream, keys.device)), "pp_quicksort_u64")
 
 
 def pp_quicksort_u32(keys, stream=None) -> None:
     assert _key_kind(keys) == "u32"
-    _check(load().pp_quicksort_u32(keys.data_ptr(), keys.numel(), _stream_ptr(stream)), "pp_quicksort_u32")
+    _check(load().pp_quicksort_u32(keys.data_ptr(), keys.numel(), _stream_ptr(stream, keys.device)), "pp_quicksort_u32")
 
 
 def pp_partition_bps(keys, pivot: int, stream=None) -> int:
@@ -212,15 +227,16 @@ def pp_partition_bps(keys, pivot: int, stream=None) -> int:
     kind = _key_kind(keys)
     out = ctypes.c_uint64(0)
     f = load().pp_partition_bps_u64 if kind == "u64" else load().pp_partition_bps_u32
-    _check(f(keys.data_ptr(), keys.numel(), _pivot(pivot, kind), _stream_ptr(stream), ctypes.byref(out)),
+    _check(f(keys.data_ptr(), keys.numel(), _pivot(pivot, kind), _stream_ptr(stream, keys.device), ctypes.byref(out)),
            "pp_partition_bps")
     return int(out.value)
 
 
 def pp_partition_bps_async_u64(keys, pivot: int, d_split, stream=None) -> None:
-    assert _key_kind(keys) == "u64" and d_split.is_cuda
+    assert _key_kind(keys) == "u64"
     _check(load().pp_partition_bps_async_u64(keys.data_ptr(), keys.numel(), _pivot(pivot, "u64"),
-                                             _stream_ptr(stream), d_split.data_ptr()), "pp_partition_bps_async_u64")
+                                             _stream_ptr(stream, keys.device), _split_word(d_split, keys)),
+           "pp_partition_bps_async_u64")
 
 
 def pp_partition_stable(keys_in, keys_out, pivot: int, stream=None) -> int:
@@ -230,15 +246,16 @@ def pp_partition_stable(keys_in, keys_out, pivot: int, stream=None) -> int:
     assert _key_kind(keys_out) == kind and keys_out.numel() == keys_in.numel()
     out = ctypes.c_uint64(0)
     f = load().pp_partition_stable_u64 if kind == "u64" else load().pp_partition_stable_u32
-    _check(f(keys_in.data_ptr(), keys_out.data_ptr(), keys_in.numel(), _pivot(pivot, kind), _stream_ptr(stream),
+    _check(f(keys_in.data_ptr(), keys_out.data_ptr(), keys_in.numel(), _pivot(pivot, kind), _stream_ptr(stream, keys_in.device),
              ctypes.byref(out)), "pp_partition_stable")
     return int(out.value)
 
 
 def pp_partition_stable_async_u64(keys_in, keys_out, pivot: int, d_split, stream=None) -> None:
-    assert _key_kind(keys_in) == "u64" and _key_kind(keys_out) == "u64" and d_split.is_cuda
+    assert _key_kind(keys_in) == "u64" and _key_kind(keys_out) == "u64"
     _check(load().pp_partition_stable_async_u64(keys_in.data_ptr(), keys_out.data_ptr(), keys_in.numel(),
-                                                _pivot(pivot, "u64"), _stream_ptr(stream), d_split.data_ptr()),
+                                                _pivot(pivot, "u64"), _stream_ptr(stream, keys_in.device),
+                                                _split_word(d_split, keys_in)),
            "pp_partition_stable_async_u64")
 
 
@@ -283,7 +300,7 @@ def pp_ss_groups(keys, pivot: int, g: int = 0, stream=None):
     info = np.zeros(6, dtype=np.uint64)
     P = ctypes.POINTER(ctypes.c_uint64)
     f = L.pp_ss_groups_u64 if kind == "u64" else L.pp_ss_groups_u32
-    _check(f(keys.data_ptr(), keys.numel(), _pivot(pivot, kind), int(g), _stream_ptr(stream),
+    _check(f(keys.data_ptr(), keys.numel(), _pivot(pivot, kind), int(g), _stream_ptr(stream, keys.device),
              T.ctypes.data_as(P), vlo.ctypes.data_as(P), vhi.ctypes.data_as(P), info.ctypes.data_as(P)),
            "pp_ss_groups")
     gg = int(info[0])
@@ -347,7 +364,7 @@ def pp_partition_dist(shard, pivot: int, stream=None) -> int:
     kind = _key_kind(shard)
     out = ctypes.c_uint64(0)
     f = load().pp_partition_dist_u64 if kind == "u64" else load().pp_partition_dist_u32
-    _check(f(shard.data_ptr(), shard.numel(), _pivot(pivot, kind), _stream_ptr(stream), ctypes.byref(out)),
+    _check(f(shard.data_ptr(), shard.numel(), _pivot(pivot, kind), _stream_ptr(stream, shard.device), ctypes.byref(out)),
            "pp_partition_dist")
     return int(out.value)
 
@@ -356,7 +373,7 @@ def pp_quicksort_dist(shard, stream=None) -> None:
     """Global sort of a sharded array (collective; see include/pp.h)."""
     kind = _key_kind(shard)
     f = load().pp_quicksort_dist_u64 if kind == "u64" else load().pp_quicksort_dist_u32
-    _check(f(shard.data_ptr(), shard.numel(), _stream_ptr(stream)), "pp_quicksort_dist")
+    _check(f(shard.data_ptr(), shard.numel(), _stream_ptr(stream, shard.device)), "pp_quicksort_dist")
 
 
 def _shard_sizes(keys, ns):
@@ -463,7 +480,7 @@ def pp_swap_ranges(pieces, key_bytes: int = 8, stream=None) -> None:
     addresses (the staging-free exchange primitive)."""
     tri = np.ascontiguousarray(np.asarray(pieces, dtype=np.uint64).reshape(-1, 3))
     f = load().pp_swap_ranges_u64 if key_bytes == 8 else load().pp_swap_ranges_u32
-    _check(f(tri.ctypes.data, tri.shape[0], _stream_ptr(stream)), "pp_swap_ranges")
+    _check(f(tri.ctypes.data, tri.shape[0], _stream_ptr(stream, None)), "pp_swap_ranges")
 
 
 def pp_timing(enable: bool) -> None:

@@ -22,7 +22,8 @@ static std::mutex g_err_mu;  // set_error may run on the loopback's rank threads
 static std::string g_err;
 static Params g_params;
 static LastStats g_stats;
-static Ctl* g_last_ctl = nullptr;
+static Ctl* g_last_ctl = nullptr;          // Ctl of the last partition (in the workspace), for pp_last_stats
+static cudaStream_t g_last_ctl_st = nullptr; // the stream that call ran on
 
 Params& params() { return g_params; }
 LastStats& last_stats() { return g_stats; }
@@ -72,6 +73,7 @@ void* workspace(size_t bytes, cudaStream_t st) {
     if (g_ws) {
         cudaStreamSynchronize(st);
         cudaDeviceSynchronize();
+        g_last_ctl = nullptr;  // pointed into the old workspace
         cudaFree(g_ws);
         g_ws = nullptr;
         g_ws_bytes = 0;
@@ -106,6 +108,39 @@ static uint64_t* pinned_word() {
     return p;
 }
 
+// Ordering of the shared workspace across streams: every call
+// that may use it waits for the last such call when that one ran on another
+// stream (an event recorded on its stream once it had enqueued its work),
+// and records the event on its own stream when it has enqueued its work.
+// Async calls stay async; calls on one stream pay nothing but the record.
+static cudaEvent_t g_ws_ev = nullptr;
+static cudaStream_t g_ws_st = nullptr;
+static bool g_ws_pending = false;
+struct WsOrder {
+    cudaStream_t st;
+    explicit WsOrder(cudaStream_t s) : st(s) {
+        if (!g_ws_ev && cudaEventCreateWithFlags(&g_ws_ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            g_ws_ev = nullptr;
+        }
+        if (g_ws_ev && g_ws_pending && g_ws_st != st) cudaStreamWaitEvent(st, g_ws_ev, 0);
+    }
+    ~WsOrder() {
+        if (!g_ws_ev) return;
+        if (cudaEventRecord(g_ws_ev, st) == cudaSuccess) {
+            g_ws_st = st;
+            g_ws_pending = true;
+        } else {
+            cudaGetLastError();
+        }
+    }
+};
+
+// The library binds to the device of its first call (workspace, streams,
+// pinned buffers and the SM count are per device); keys on another device,
+// or a current device that is not the keys' device, are rejected.
+static int g_dev = -1;
+
 template <typename K>
 static pp_status check_device_keys(const K* keys, uint64_t n) {
     if (n == 0) return PP_OK;
@@ -126,6 +161,19 @@ static pp_status check_device_keys(const K* keys, uint64_t n) {
     }
     if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) {
         set_error("keys must be a device pointer (use the *_host variants for host memory)");
+        return PP_E_INVAL;
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (a.type == cudaMemoryTypeDevice && a.device != cur) {
+        set_error("keys are on device " + std::to_string(a.device) + " but the current device is " +
+                  std::to_string(cur));
+        return PP_E_INVAL;
+    }
+    if (g_dev < 0) g_dev = cur;
+    if (cur != g_dev) {
+        set_error("the library is bound to device " + std::to_string(g_dev) + " (its first call); got device " +
+                  std::to_string(cur));
         return PP_E_INVAL;
     }
     return PP_OK;
@@ -152,9 +200,13 @@ static pp_status partition_sync(K* keys, uint64_t n, K pivot, void* stream, uint
         return PP_E_NOMEM;
     }
     Ctl* ctl = nullptr;
-    s = partition_device<K>(keys, n, pivot, st, nullptr, &ctl);
+    {
+        WsOrder ws_order(st);
+        s = partition_device<K>(keys, n, pivot, st, nullptr, &ctl);
+    }
     if (s != PP_OK) return s;
     g_last_ctl = ctl;
+    g_last_ctl_st = st;
     cudaError_t e = cudaMemcpyAsync(pw, &ctl->K, sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "partition");
@@ -177,8 +229,12 @@ static pp_status partition_async(K* keys, uint64_t n, K pivot, void* stream, uin
         return e == cudaSuccess ? PP_OK : cuda_fail(e, "memset");
     }
     Ctl* ctl = nullptr;
-    s = partition_device<K>(keys, n, pivot, st, d_split, &ctl);
-    g_last_ctl = ctl;
+    {
+        WsOrder ws_order(st);
+        s = partition_device<K>(keys, n, pivot, st, d_split, &ctl);
+    }
+    g_last_ctl = s == PP_OK ? ctl : nullptr;
+    g_last_ctl_st = st;
     return s;
 }
 
@@ -211,6 +267,7 @@ static pp_status partition_stable(const K* in, K* out, uint64_t n, K pivot, void
         }
         return PP_OK;
     }
+    WsOrder ws_order(st);
     if (d_split) return partition_stable_device<K>(in, out, n, pivot, st, d_split, nullptr);
     uint64_t* pw = pinned_word();
     if (!pw) {
@@ -249,6 +306,7 @@ static pp_status partition_bps(K* keys, uint64_t n, K pivot, void* stream, uint6
         }
         return PP_OK;
     }
+    WsOrder ws_order(st);
     if (d_split) return partition_bps_device<K>(keys, n, pivot, st, d_split);
     uint64_t* pw = pinned_word();
     uint64_t* dk = static_cast<uint64_t*>(host_split_slot());
@@ -272,7 +330,11 @@ static pp_status quicksort_sync(K* keys, uint64_t n, void* stream) {
     if (s != PP_OK) return s;
     if (n <= 1) return PP_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    s = quicksort_device<K>(keys, n, st);
+    g_last_ctl = nullptr;
+    {
+        WsOrder ws_order(st);
+        s = quicksort_device<K>(keys, n, st);
+    }
     if (s != PP_OK) return s;
     cudaError_t e = cudaStreamSynchronize(st);
     return e == cudaSuccess ? PP_OK : cuda_fail(e, "quicksort");
@@ -331,6 +393,8 @@ static pp_status partition_host(K* host_keys, uint64_t n, K pivot, uint64_t* spl
         set_error("device buffer allocation failed");
         return PP_E_NOMEM;
     }
+    g_last_ctl = nullptr;
+    WsOrder ws_order(g_hstream);
     if (!g_hs_up) {
         cudaStreamCreateWithFlags(&g_hs_up, cudaStreamNonBlocking);
         cudaStreamCreateWithFlags(&g_hs_dn, cudaStreamNonBlocking);
@@ -455,6 +519,7 @@ static pp_status ss_groups(K* keys, uint64_t n, K pivot, uint64_t g, void* strea
         set_error("NULL output array");
         return PP_E_INVAL;
     }
+    WsOrder ws_order((cudaStream_t)stream);
     return ss_groups_device<K>(keys, n, pivot, g, (cudaStream_t)stream, T, vlo, vhi, info);
 }
 
@@ -557,6 +622,7 @@ pp_status pp_partition_dist_u64(uint64_t* shard, uint64_t n_local, uint64_t pivo
     std::lock_guard<std::mutex> lk(g_mu);
     pp_status s = check_device_keys(shard, n_local);
     if (s != PP_OK) return s;
+    WsOrder ws_order((cudaStream_t)stream);
     return partition_dist<uint64_t>(shard, n_local, pivot, (cudaStream_t)stream, global_split_out);
 }
 pp_status pp_partition_dist_u32(uint32_t* shard, uint64_t n_local, uint32_t pivot, void* stream,
@@ -564,18 +630,21 @@ pp_status pp_partition_dist_u32(uint32_t* shard, uint64_t n_local, uint32_t pivo
     std::lock_guard<std::mutex> lk(g_mu);
     pp_status s = check_device_keys(shard, n_local);
     if (s != PP_OK) return s;
+    WsOrder ws_order((cudaStream_t)stream);
     return partition_dist<uint32_t>(shard, n_local, pivot, (cudaStream_t)stream, global_split_out);
 }
 pp_status pp_quicksort_dist_u64(uint64_t* shard, uint64_t n_local, void* stream) {
     std::lock_guard<std::mutex> lk(g_mu);
     pp_status s = check_device_keys(shard, n_local);
     if (s != PP_OK) return s;
+    WsOrder ws_order((cudaStream_t)stream);
     return quicksort_dist<uint64_t>(shard, n_local, (cudaStream_t)stream, (uint64_t)g_params.dist_small);
 }
 pp_status pp_quicksort_dist_u32(uint32_t* shard, uint64_t n_local, void* stream) {
     std::lock_guard<std::mutex> lk(g_mu);
     pp_status s = check_device_keys(shard, n_local);
     if (s != PP_OK) return s;
+    WsOrder ws_order((cudaStream_t)stream);
     return quicksort_dist<uint32_t>(shard, n_local, (cudaStream_t)stream, (uint64_t)g_params.dist_small);
 }
 pp_status pp_partition_dist_loopback_u64(uint64_t* keys, const uint64_t* ns, int nranks, uint64_t pivot,
@@ -672,8 +741,9 @@ pp_status pp_last_stats(uint64_t* out) {
     if (!out) return PP_E_INVAL;
     Ctl c;
     memset(&c, 0, sizeof(c));
-    if (g_last_ctl) {
-        cudaError_t e = cudaMemcpy(&c, g_last_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost);
+    if (g_last_ctl) {  // read on the stream of the call that wrote it
+        cudaError_t e = cudaMemcpyAsync(&c, g_last_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g_last_ctl_st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(g_last_ctl_st);
         if (e != cudaSuccess) return cuda_fail(e, "stats");
     }
     const LastStats& S = g_stats;

@@ -1,4 +1,6 @@
 """GPU parity: the CUDA partition (through the C ABI) against the CPU oracle."""
+import os
+
 import numpy as np
 import pytest
 
@@ -326,50 +328,63 @@ def test_config2_full(pp, mu):
     assert st["aux_bytes"] < 0.001 * n * 8
 
 
+def _oracle_count_c3(n: int, p: int, chunk: int = 1 << 27) -> int:
+    """K = #keys < p over the seed-regenerated c3 input, computed by the
+    oracle chunk by chunk on the host (threads: numpy and the ctypes oracle
+    release the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(s):
+        return oracle.count(synth.uniform_u64_np(min(chunk, n - s), synth.SEEDS["c3"], offset=s), p)
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        return sum(ex.map(one, range(0, n, chunk)))
+
+
 def test_config3_single_gpu_full(pp):
-    """n = 2^33 u64 (64 GiB, BASELINE config 3 at P = 1), pivot 2^63.
-    Checks at full size: split = count of keys < pivot (device compare, and
-    the oracle's count on a 2^24-key sample of the input); the predicate on
-    every position; per-side multiset fingerprints (count, sum, xor, sum of
-    a mixed image) equal the input's -- a full sort of 2^33 keys does not fit
-    beside the array."""
+    """n = 2^33 u64 (64 GiB, BASELINE config 3 at P = 1), pivot 2^63, exact:
+    (1) split == the oracle's count over the whole seed-regenerated input
+    (host, chunkwise); (2) the predicate on every position (device);
+    (3) exact multiset equality by value-range bucketing: the
+    key space is cut into 64 equal ranges, and for each range the output's
+    keys and the regenerated input's keys in it are gathered and sorted with
+    the library sort and compared element by element.  Given (1) and (2),
+    whole-array multiset equality is equivalent to the per-side check (3)."""
     from gpu_util import order_key, order_pivot
     n = 1 << 33
     p = 1 << 63
+    K_oracle = _oracle_count_c3(n, p)
     t = torch.empty(n, dtype=torch.int64, device="cuda")
     synth.uniform_u64_torch(n, synth.SEEDS["c3"], "cuda", out=t, chunk=1 << 27)
-    sample = t[: 1 << 24].cpu().numpy().view(np.uint64)
-    assert oracle.count(sample, p) == int((order_key(t[: 1 << 24]) < order_pivot(p, torch.int64)).sum())
-
+    split = pp.pp_partition(t, p)
+    assert split == K_oracle
     pv = order_pivot(p, torch.int64)
     C = 1 << 28
-
-    def side_prints(by_value: bool, split: int = 0):
-        """(count, sum, sum of x*odd) of the true side and of the false side
-        (wrapping int64 arithmetic), chunk by chunk."""
-        acc = [[0, 0, 0], [0, 0, 0]]
-        for s in range(0, n, C):
-            x = t[s:s + C]
-            if by_value:
-                m = order_key(x) < pv
-            else:
-                m = torch.arange(s, s + x.numel(), device="cuda") < split
-            for side, sel in ((0, m), (1, ~m)):
-                v = x[sel]
-                acc[side][0] += v.numel()
-                acc[side][1] = (acc[side][1] + int(v.sum())) % (1 << 64)
-                acc[side][2] = (acc[side][2] + int((v * -7046029254386353131).sum())) % (1 << 64)
-        return acc
-
-    before = side_prints(True)
-    K = before[0][0]
-    split = pp.pp_partition(t, p)
-    assert split == K
     for s in range(0, n, C):
         ko = order_key(t[s:s + C])
         idx = torch.arange(s, s + ko.numel(), device="cuda")
         assert bool(((ko < pv) == (idx < split)).all())
-    assert side_prints(False, split) == before
+    del ko, idx
+    B = 64  # ranges of 2^58 keys: the top 6 bits of the unsigned key
+    Ci = 1 << 27
+    chunk_in = torch.empty(Ci, dtype=torch.int64, device="cuda")
+    for b in range(B):
+        outs, ins = [], []
+        for s in range(0, n, C):
+            x = t[s:s + C]
+            outs.append(x[((x >> 58) & 63) == b])
+        for s in range(0, n, Ci):
+            m = min(Ci, n - s)
+            synth.uniform_u64_torch(m, synth.SEEDS["c3"], "cuda", offset=s, out=chunk_in[:m], chunk=Ci)
+            x = chunk_in[:m]
+            ins.append(x[((x >> 58) & 63) == b])
+        o = torch.sort(order_key(torch.cat(outs))).values
+        del outs
+        i = torch.sort(order_key(torch.cat(ins))).values
+        del ins
+        assert o.numel() == i.numel() and torch.equal(o, i), f"multiset differs in key range {b}"
+        del o, i
+    torch.cuda.empty_cache()
 
 
 def test_config4_zipf_full(pp):
@@ -520,6 +535,24 @@ def test_bps_bytewise(pp, dt):
                 k = pp.pp_partition_bps(t, p)
                 assert k == k_ref, (n, p)
                 assert np.array_equal(to_host(t, dt), ref), (n, p)
+
+
+def test_bps_golden_make_successor_heavy(pp, golden):
+    """The SPEC.md:344 MakeSuccessorHeavy example (Fig. 1)
+    through the GPU Blocked-Prefix-Sum partition: byte for byte equal to the
+    oracle's BPS, whose MakeSuccessorHeavy stage the golden value pins."""
+    from gpu_util import to_dev, to_host
+    for ex in golden["make_successor_heavy"]:
+        for dt in (np.uint64, np.uint32):
+            a = np.array(ex["keys"], dtype=dt)
+            msh = a.copy()
+            oracle.bps_make_successor_heavy(msh, ex["pivot"], False)
+            assert msh.tolist() == ex["output"]
+            ref = a.copy()
+            k_ref = oracle.partition_bps(ref, ex["pivot"], 4096)
+            t = to_dev(a)
+            assert pp.pp_partition_bps(t, ex["pivot"]) == k_ref
+            assert np.array_equal(to_host(t, dt), ref), ex["cite"]
 
 
 def test_bps_config2(pp):

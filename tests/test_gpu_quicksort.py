@@ -107,30 +107,20 @@ def test_big_path_forced(pp):
 
 @pytest.mark.parametrize("kind", ["uniform", "dup1000"])
 def test_config5_full(pp, kind):
-    """n = 2^28 u64 (BASELINE config 5).  Checks: ascending order on every
-    adjacent pair; multiset equal to the input (library sort); sampled ranks
-    r: out[r] is the r-th smallest by the oracle's count
-    (count(in < out[r]) <= r < count(in <= out[r]))."""
-    from gpu_util import order_key
+    """n = 2^28 u64 (BASELINE config 5), byte for byte against the oracle's
+    serial quicksort of the same seed-regenerated input (north_star (4);
+    ~25 s of host time per input)."""
     n = 1 << 28
     if kind == "uniform":
         t = synth.uniform_u64_torch(n, synth.SEEDS["c5"], "cuda")
+        ref = synth.uniform_u64_np(n, synth.SEEDS["c5"])
     else:
         t = synth.mod_range_u64_torch(n, synth.SEEDS["c5"], 1000, "cuda")
-    inp_host = t.cpu().numpy().view(np.uint64).copy()
+        ref = synth.mod_range_u64_np(n, synth.SEEDS["c5"], 1000)
     pp.pp_quicksort(t)
-    ko = order_key(t)
-    assert bool((ko[1:] >= ko[:-1]).all()), "not sorted"
-    ref = torch.sort(order_key(torch.from_numpy(inp_host.view(np.int64)).to("cuda"))).values
-    assert torch.equal(ref, ko), "multiset differs"
-    del ref
+    oracle.quicksort(ref)
     out = t.cpu().numpy().view(np.uint64)
-    rng = np.random.default_rng(0)
-    for r in list(rng.integers(0, n, size=6)) + [0, n - 1]:
-        v = int(out[r])
-        lo = oracle.count(inp_host, v)
-        hi = oracle.count(inp_host, v + 1) if v < U64_MAX else n
-        assert lo <= r < hi, r
+    assert np.array_equal(out, ref)
 
 
 @pytest.mark.parametrize("leaf_algo,leaf", [(0, 0), (2, 0), (3, 0), (4, 0), (5, 0), (5, 4096), (6, 0), (6, 1000),
@@ -182,3 +172,4 @@ def test_quicksort_2pow30(pp, kind):
     assert torch.equal(order_key(t), ref)
     del t, ref
     torch.cuda.empty_cache()
+

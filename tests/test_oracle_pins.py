@@ -44,6 +44,17 @@ def test_golden_partition(golden):
             assert oracle.count(a, ex["pivot"]) == ex["split"]
 
 
+def test_golden_make_successor_heavy(golden):
+    """SPEC.md:344 worked example of Fig. 1 MakeSuccessorHeavy
+    pins the oracle's ARRANGEMENT (swap order and recursion split), not only
+    Lemma 3.1's prefix property; both key widths."""
+    for ex in golden["make_successor_heavy"]:
+        for dt in (np.uint64, np.uint32):
+            a = np.array(ex["keys"], dtype=dt)
+            oracle.bps_make_successor_heavy(a, ex["pivot"], False)
+            assert a.tolist() == ex["output"], ex["cite"]
+
+
 def test_golden_is_partitioned(golden):
     for ex in golden["is_partitioned"]:
         a = np.array(ex["keys"], dtype=np.uint64)
