@@ -286,18 +286,15 @@ pp_status pp_last_stats(uint64_t *out13);
 /* Tunables (tests / benchmarks): "g", "min_lines_per_group", "small_n",
  * "path" (0 auto, 1 single-CTA, 2 smoothed striding, 3 cleanup only), "tile",
  * "ranks", "seed", "strided" (1: X = 0, the Strided Algorithm PAPER.md:796-825,
- * i.e. seed 0; 0: back to the default seed), "leaf", "qs_cta_max", "variant",
- * "leaf" (quicksort bin capacity, <= 16384; default 16384 with the default
- * bin sort), "qs_cta_max", "variant", "leaf_algo" (0 auto = 6 the
- * index-staged counting sort, 5 counting with keys in registers, 4 packed
- * 32-bit merge, 3 merge, 2 LSD radix, 1 bitonic), "fused", "cleanup_chain"
- * (-1 auto: 3-kernel chain below 1 GiB of keys, fused tail above; 0 fused;
- * 1 chain), "cleanup_bitmap", "qs_small", "qs_small_cfg", "qs_waves",
- * "qs_heavy", "qs_pipe", "qs_lanes" (0 auto = 2 lanes), "qs_early" (-1 auto
- * = on), "qs_early_min" (0 auto), "qs_minl" (0 auto: 128 KiB per group), "host_chunk",
- * "bps_nt", "dist_p2p", "dist_timeout_ms", "dist_small" (distributed quicksort:
- * spanning segments of <= this many keys are gathered and sorted locally),
- * "dist_fault", "dist_fault_rank" (loopback test hooks).
+ * i.e. seed 0; 0: back to the default seed), "cleanup_chain" (-1 auto:
+ * 3-kernel chain below 1 GiB of keys, fused scan/swap tail above; 0 fused
+ * tail; 1 chain), "cleanup_bitmap"; quicksort: "leaf" (bin capacity, <= 16384,
+ * default 16384), "qs_cta_max", "qs_small", "qs_waves", "qs_heavy",
+ * "qs_lanes" (0 auto = 2 lanes), "qs_early" (-1 auto = on), "qs_early_min"
+ * (0 auto), "qs_minl" (0 auto: 128 KiB per group); "host_chunk", "bps_nt";
+ * multi-GPU: "dist_p2p", "dist_timeout_ms", "dist_small" (distributed
+ * quicksort: spanning segments of <= this many keys are gathered and sorted
+ * locally), "dist_fault", "dist_fault_rank" (loopback test hooks).
  * Returns PP_E_INVAL for an unknown name.  pp_get_param returns INT64_MIN
  * for an unknown name. */
 pp_status pp_set_param(const char *name, int64_t value);

@@ -777,16 +777,10 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "strided") P.seed = value ? 0 : Params().seed;
     else if (k == "leaf") P.leaf = value;
     else if (k == "qs_cta_max") P.qs_cta_max = value;
-    else if (k == "variant") P.variant = value;
-    else if (k == "leaf_algo") P.leaf_algo = value;
-    else if (k == "fused") P.fused = value;
     else if (k == "qs_small") P.qs_small = value;
-    else if (k == "qs_small_cfg") P.qs_small_cfg = value;
-    else if (k == "fused_stop") P.fused_stop = value;
     else if (k == "qs_waves") P.qs_waves = value;
     else if (k == "qs_heavy") P.qs_heavy = value;
     else if (k == "host_chunk") P.host_chunk = value;
-    else if (k == "qs_pipe") P.qs_pipe = value;
     else if (k == "dist_p2p") P.dist_p2p = value ? 1 : 0;
     else if (k == "dist_timeout_ms") P.dist_timeout_ms = value < 1 ? 1 : value;
     else if (k == "dist_fault") P.dist_fault = value;
@@ -820,16 +814,10 @@ int64_t pp_get_param(const char* name) {
     if (k == "strided") return P.seed == 0 ? 1 : 0;
     if (k == "leaf") return P.leaf;
     if (k == "qs_cta_max") return P.qs_cta_max;
-    if (k == "variant") return P.variant;
-    if (k == "leaf_algo") return P.leaf_algo;
-    if (k == "fused") return P.fused;
     if (k == "qs_small") return P.qs_small;
-    if (k == "qs_small_cfg") return P.qs_small_cfg;
-    if (k == "fused_stop") return P.fused_stop;
     if (k == "qs_waves") return P.qs_waves;
     if (k == "qs_heavy") return P.qs_heavy;
     if (k == "host_chunk") return P.host_chunk;
-    if (k == "qs_pipe") return P.qs_pipe;
     if (k == "dist_p2p") return P.dist_p2p;
     if (k == "dist_timeout_ms") return P.dist_timeout_ms;
     if (k == "dist_fault") return P.dist_fault;

@@ -44,18 +44,12 @@ struct Params {
     uint64_t seed = 0x5EEDC0DE2004ULL;  // Smoothed Striding offset seed (fixed => deterministic)
     int64_t leaf = 0;              // quicksort: 0 = auto smem leaf size
     int64_t qs_cta_max = 0;        // quicksort: 0 = auto segment size handled by one CTA
-    int64_t variant = 0;           // group-kernel configuration (pp_partition.cu VariantCfg)
-    int64_t leaf_algo = 0;         // quicksort bins: 0 auto (= 6), 1 bitonic, 2 LSD radix, 3 merge, 4 packed 32-bit merge (u64), 5 counting, 6 counting (index-staged)
-    int64_t fused = 0;             // path 2: one cooperative kernel (1) or the kernel chain (0, faster)
-    int64_t fused_stop = 0;        // debug/profiling: stop the fused kernel after this phase
     int64_t qs_waves = 2;          // quicksort mid levels: target CTA waves of the group launch
     int64_t qs_small = 1 << 16;    // quicksort: segments <= this finish in one CTA (0 = off)
-    int64_t qs_small_cfg = 3;      // quicksort: per-CTA recursion config (pp_quicksort.cu SmallCfg; 3 = 4 lines in flight)
     int64_t cleanup_chain = -1;    // partition cleanup tail: 0 fused scan+swap, 1 scan / locate / swap kernels,
                                    // -1 auto (chain below 1 GiB of keys, fused from 1 GiB: measured crossover)
     int64_t cleanup_bitmap = 1;    // fused tail: locate pairs from the dirty-set bitmap (0: locate + grid barrier)
     int64_t bps_nt = 256;          // Blocked-Prefix-Sum Reorder level kernel: threads per CTA (256/512/1024)
-    int64_t qs_pipe = 1;           // quicksort: chunks of the per-CTA recursion pipelined with their bin sorts (measured: no gain)
     int64_t qs_lanes = 0;          // quicksort level loop: 1 = one stream, 2 = two array-disjoint lanes on two
                                    // streams, 0 = auto (= 2)
     int64_t qs_early = -1;         // quicksort: run the per-CTA recursion + bin sort of small segments on two more

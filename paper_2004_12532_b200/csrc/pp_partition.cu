@@ -139,243 +139,6 @@ __global__ void __launch_bounds__(SW_NT, 3) swap_kernel(K* __restrict__ keys, co
 }
 
 // ===========================================================================
-// Fused single-kernel partition (default path): ONE cooperative launch runs
-// the group partition and the whole cleanup; the phases are separated by a
-// flag-array grid barrier (each CTA release-stores its own flag, then
-// acquire-polls all flags: no atomics).  Phases after the group step reuse
-// the group engine's shared memory.  Cleanup tiles are NT*EPT = 1024 keys
-// (one round trip per side), <= FU_MAX_TILES per side.
-// ===========================================================================
-constexpr int FU_EPT = 8;
-constexpr uint64_t FU_MAX_TILES = 4096;
-
-template <typename K>
-struct FusedArgs {
-    K* keys;
-    uint64_t n, h, n_lines, seed;
-    uint32_t g, epoch, stop;  // stop: debug, return after phase `stop` (0 = run all)
-    K pivot;
-    GroupOut* gout;
-    Ctl* ctl;
-    uint64_t* d_split;
-    uint32_t *cntL, *cntR, *ttl, *ttr, *flags;
-    uint64_t *PL, *PR, *rk, *posL, *posR;
-};
-
-__device__ __forceinline__ void grid_sync(uint32_t* flags, uint32_t nb, uint32_t epoch) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        st_release_gpu(flags + blockIdx.x, epoch);
-    }
-    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
-        while ((int32_t)(ld_acquire_gpu(flags + i) - epoch) < 0) __nanosleep(64);
-    __threadfence();
-    __syncthreads();
-}
-
-template <typename C>
-__global__ void __launch_bounds__(C::NT) fused_partition_kernel(const FusedArgs<typename C::Key> a) {
-    using K = typename C::Key;
-    constexpr int NT = C::NT, NW = NT / 32, EPT = FU_EPT, RNG = NT * EPT;
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t LK = C::LK;
-
-    // ---- phase 1: Smoothed Striding group partition ----
-    ss_group_engine<C>(a.keys + a.h, a.n_lines, a.g, blockIdx.x, a.seed, a.pivot, a.gout + blockIdx.x, smem);
-    if (a.stop == 1) return;
-    grid_sync(a.flags, a.g, a.epoch + 1);
-
-    // ---- phase 2: window reduction (every CTA) + tile counts ----
-    Ctl* sc = reinterpret_cast<Ctl*>(smem);
-    uint64_t* red = reinterpret_cast<uint64_t*>(smem + 512);    // [4][NW]
-    uint32_t* s32 = reinterpret_cast<uint32_t*>(smem + 1536);   // [NW]
-    unsigned char* work = smem + 2048;                          // phase buffers
-    const uint64_t region_end = a.n_lines * LK;
-    {
-        uint64_t T = 0, vmin = region_end, vmax = 0, ht = 0;
-        for (uint32_t i = tid; i < a.g; i += NT) {
-            T += __ldcg(&a.gout[i].T);
-            const uint64_t lo = __ldcg(&a.gout[i].vlo), hi = __ldcg(&a.gout[i].vhi);
-            vmin = lo < vmin ? lo : vmin;
-            vmax = hi > vmax ? hi : vmax;
-        }
-        for (uint64_t x = tid; x < a.h; x += NT) ht += is_pred(__ldcg(a.keys + x), a.pivot) ? 1 : 0;
-        for (uint64_t x = a.h + region_end + tid; x < a.n; x += NT) ht += is_pred(__ldcg(a.keys + x), a.pivot) ? 1 : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            T += __shfl_xor_sync(0xffffffffu, T, o);
-            ht += __shfl_xor_sync(0xffffffffu, ht, o);
-            const uint64_t p = __shfl_xor_sync(0xffffffffu, vmin, o), q = __shfl_xor_sync(0xffffffffu, vmax, o);
-            vmin = p < vmin ? p : vmin;
-            vmax = q > vmax ? q : vmax;
-        }
-        if (lane == 0) {
-            red[0 * NW + warp] = T;
-            red[1 * NW + warp] = ht;
-            red[2 * NW + warp] = vmin;
-            red[3 * NW + warp] = vmax;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            for (int w = 1; w < NW; ++w) {
-                T += red[0 * NW + w];
-                ht += red[1 * NW + w];
-                vmin = red[2 * NW + w] < vmin ? red[2 * NW + w] : vmin;
-                vmax = red[3 * NW + w] > vmax ? red[3 * NW + w] : vmax;
-            }
-            const uint64_t Ksplit = T + ht;
-            uint64_t lo[3], hi[3];
-            lo[0] = 0; hi[0] = a.h;
-            const uint64_t wlo = a.h + vmin, whi = a.h + vmax;
-            lo[1] = wlo < Ksplit ? wlo : Ksplit;
-            hi[1] = whi > Ksplit ? whi : Ksplit;
-            if (vmin > vmax) { lo[1] = hi[1] = 0; }
-            lo[2] = a.h + region_end; hi[2] = a.n;
-            const uint64_t cap = cleanup_max_tiles(a.n) < FU_MAX_TILES ? cleanup_max_tiles(a.n) : FU_MAX_TILES;
-            finish_ctl(sc, a.n, Ksplit, lo, hi, (uint64_t)RNG, cap);
-            sc->vmin = wlo;
-            sc->vmax = whi;
-            if (blockIdx.x == 0) {
-                *a.ctl = *sc;
-                if (a.d_split) *a.d_split = Ksplit;
-            }
-        }
-        __syncthreads();
-    }
-    Dirty d;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        d.s[k] = sc->ds[k];
-        d.l[k] = sc->dl[k];
-    }
-    const uint64_t Kv = sc->Kv, W = sc->W, TT = sc->tile, nL = sc->nL, nR = sc->nR;
-    for (uint64_t t = blockIdx.x; t < nL + nR; t += gridDim.x) {
-        const bool left = t < nL;
-        const uint64_t u0 = left ? t * TT : Kv + (t - nL) * TT;
-        const uint64_t u1 = left ? min(u0 + TT, Kv) : min(u0 + TT, W);
-        uint32_t c = 0;
-        for (uint64_t ub = u0; ub < u1; ub += (uint64_t)EPT * NT) {
-            K x[EPT];
-#pragma unroll
-            for (int k = 0; k < EPT; ++k) {
-                const uint64_t u = ub + (uint64_t)k * NT + tid;
-                x[k] = u < u1 ? __ldcg(a.keys + vreal(d, u)) : (K)0;
-            }
-#pragma unroll
-            for (int k = 0; k < EPT; ++k) {
-                const uint64_t u = ub + (uint64_t)k * NT + tid;
-                const bool p = is_pred(x[k], a.pivot);
-                c += (u < u1 && (left ? !p : p)) ? 1u : 0u;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) s32[warp] = c;
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t tot = 0;
-            for (int w = 0; w < NW; ++w) tot += s32[w];
-            if (left) a.cntL[t] = tot; else a.cntR[t - nL] = tot;
-        }
-        __syncthreads();
-    }
-    if (a.stop == 2) return;
-    grid_sync(a.flags, a.g, a.epoch + 2);
-
-    // ---- phase 3 (CTA 0): scans + merged task list ----
-    if (blockIdx.x == 0) {
-        uint64_t* sw = reinterpret_cast<uint64_t*>(smem + 1024);  // [NW]
-        uint64_t* sPL = reinterpret_cast<uint64_t*>(work);
-        uint64_t* sPR = sPL + nL;
-        uint64_t carry = 0;
-        for (uint64_t b = 0; b < nL; b += NT) {
-            const uint64_t i = b + tid;
-            uint64_t tot;
-            const uint64_t ex = block_exscan<NT>(i < nL ? __ldcg(a.cntL + i) : 0, sw, tot);
-            if (i < nL) a.PL[i] = sPL[i] = carry + ex;
-            carry += tot;
-        }
-        const uint64_t ML = carry;
-        carry = 0;
-        for (uint64_t b = 0; b < nR; b += NT) {
-            const uint64_t i = b + tid;
-            uint64_t tot;
-            const uint64_t ex = block_exscan<NT>(i < nR ? __ldcg(a.cntR + i) : 0, sw, tot);
-            if (i < nR) a.PR[i] = sPR[i] = carry + ex;
-            carry += tot;
-        }
-        __syncthreads();
-        const bool ok = (ML == carry && ML > 0);
-        if (ok) {
-            for (uint64_t t = tid; t < nL; t += NT) {
-                const uint64_t r = sPL[t];
-                const uint64_t m = t + lower_bound_u64(sPR, nR, r);
-                a.rk[m] = r;
-                a.ttl[m] = (uint32_t)t;
-                a.ttr[m] = (uint32_t)(upper_bound_u64(sPR, nR, r) - 1);
-            }
-            for (uint64_t t = tid; t < nR; t += NT) {
-                const uint64_t r = sPR[t];
-                const uint64_t ub = upper_bound_u64(sPL, nL, r);
-                const uint64_t m = t + ub;
-                a.rk[m] = r;
-                a.ttl[m] = (uint32_t)(ub - 1);
-                a.ttr[m] = (uint32_t)t;
-            }
-        }
-        if (tid == 0) {
-            a.ctl->ML = ML;
-            a.ctl->MR = carry;
-            if (ML != carry) a.ctl->err = 1;
-            a.ctl->nTasks = ok ? nL + nR : 0;
-            a.rk[ok ? nL + nR : 0] = ML;
-        }
-    }
-    if (a.stop == 3) return;
-    grid_sync(a.flags, a.g, a.epoch + 3);
-
-    // ---- phase 4: locate the first item of every task ----
-    const uint64_t nTasks = __ldcg(&a.ctl->nTasks), M = __ldcg(&a.ctl->ML);
-    {
-        PairBuf<K, NT, EPT>& pb = *reinterpret_cast<PairBuf<K, NT, EPT>*>(work);
-        for (uint64_t j = blockIdx.x; j <= nTasks; j += gridDim.x) {
-            const uint64_t r = __ldcg(a.rk + j);
-            uint64_t pl = Kv, pr = W;
-            if (j < nTasks && r < M) {
-                const uint64_t tl = __ldcg(a.ttl + j), tr = __ldcg(a.ttr + j);
-                select_pair<K, NT, EPT>(a.keys, d, a.pivot, tl * TT, min(tl * TT + TT, Kv), r - __ldcg(a.PL + tl),
-                                        Kv + tr * TT, min(Kv + tr * TT + TT, W), r - __ldcg(a.PR + tr), pb, pl,
-                                        pr);
-            }
-            if (tid == 0) {
-                a.posL[j] = pl;
-                a.posR[j] = pr;
-            }
-        }
-    }
-    if (a.stop == 4) return;
-    grid_sync(a.flags, a.g, a.epoch + 4);
-
-    // ---- phase 5: rank-matched swaps ----
-    for (uint64_t j = blockIdx.x; j < nTasks; j += gridDim.x) {
-        const uint64_t pairs = __ldcg(a.rk + j + 1) - __ldcg(a.rk + j);
-        if (pairs == 0) continue;
-        const uint64_t uL = __ldcg(a.posL + j), uR = __ldcg(a.posR + j);
-        const uint64_t tle = min((uL / TT + 1) * TT, Kv), tre = min(Kv + ((uR - Kv) / TT + 1) * TT, W);
-        const uint64_t eL = min(__ldcg(a.posL + j + 1), tle), eR = min(__ldcg(a.posR + j + 1), tre);
-        if (TT == (uint64_t)RNG) {
-            swap_pair<K, NT, EPT>(a.keys, d, a.pivot, uL, eL, uR, eR, pairs,
-                                  *reinterpret_cast<PairBuf<K, NT, EPT>*>(work));
-        } else {
-            walk_swap_stream<K, NT, EPT>(a.keys, d, a.pivot, uL, eL, uR, eR,
-                                         *reinterpret_cast<StreamBuf<NT, EPT>*>(work));
-        }
-    }
-}
-
-// ===========================================================================
 // Single-CTA path for small n: count, then one walk over [0,K) x [K,n).
 // ===========================================================================
 template <typename K>
@@ -479,8 +242,10 @@ int timing_read(double* out) {
 }
 
 // ---------------------------------------------------------------------------
-// Group-kernel variants (line size, threads, prefetch depth, store path),
-// selectable with pp_set_param("variant", v) for tuning; 0 is the default.
+// Group-kernel instantiations: the default and the Strided Algorithm (X = 0).
+// (Line sizes 4-8 KiB, 64-256 threads, 3-6 lines in flight, TMA stores and
+// parallel refill issue were measured in round 1 -- tools/tune.py -- and the
+// default is the fastest; the alternatives were removed.)
 // ---------------------------------------------------------------------------
 template <typename C>
 static int occupancy_of() {
@@ -501,25 +266,16 @@ struct VariantInfo {
 
 template <typename K, int V>
 struct VariantCfg;
+// 0: the default configuration (pp_group.cuh GroupCfg)
 template <typename K> struct VariantCfg<K, 0> { using type = GroupCfg<K>; };
-template <typename K> struct VariantCfg<K, 1> { using type = GroupCfgT<K, 8192, 256, 4, false>; };
-template <typename K> struct VariantCfg<K, 2> { using type = GroupCfgT<K, 4096, 128, 4, false>; };
-template <typename K> struct VariantCfg<K, 3> { using type = GroupCfgT<K, 8192, 64, 4, false>; };
-template <typename K> struct VariantCfg<K, 4> { using type = GroupCfgT<K, 8192, 128, 3, false>; };
-template <typename K> struct VariantCfg<K, 5> { using type = GroupCfgT<K, 4096, 64, 6, false>; };
-template <typename K> struct VariantCfg<K, 6> { using type = GroupCfgT<K, 8192, 128, 4, true>; };
-// 7: the default configuration with X = 0 (Strided Algorithm), selected by
-// the "strided" param (seed 0), not by "variant"
-template <typename K> struct VariantCfg<K, 7> {
+// 1: the same with X = 0 (the Strided Algorithm), selected by
+// the "strided" param (seed 0): a separate instantiation, since a runtime
+// branch on the seed made the compiler unswitch the whole engine (-7%)
+template <typename K> struct VariantCfg<K, 1> {
     using D = GroupCfg<K>;
     using type = GroupCfgT<K, D::LK * (int)sizeof(K), D::NT, D::PF, D::TMA_STORE, true, D::PAR_ISSUE>;
 };
-// 8: 8 KiB lines, 128 threads, 4 in flight per end, parallel refill issue
-template <typename K> struct VariantCfg<K, 8> { using type = GroupCfgT<K, 8192, 128, 4, false, false, true>; };
-// 9: 4 KiB lines, 256 threads, parallel refill issue
-template <typename K> struct VariantCfg<K, 9> { using type = GroupCfgT<K, 4096, 256, 4, false, false, true>; };
-constexpr int N_VARIANTS = 10;
-constexpr int STRIDED_VARIANT = 7;
+constexpr int STRIDED_VARIANT = 1;
 
 template <typename K, int V>
 static VariantInfo variant_info_t() {
@@ -528,18 +284,7 @@ static VariantInfo variant_info_t() {
 }
 template <typename K>
 static VariantInfo variant_info(int v) {
-    switch (v) {
-        case 1: return variant_info_t<K, 1>();
-        case 2: return variant_info_t<K, 2>();
-        case 3: return variant_info_t<K, 3>();
-        case 4: return variant_info_t<K, 4>();
-        case 5: return variant_info_t<K, 5>();
-        case 6: return variant_info_t<K, 6>();
-        case 7: return variant_info_t<K, 7>();
-        case 8: return variant_info_t<K, 8>();
-        case 9: return variant_info_t<K, 9>();
-        default: return variant_info_t<K, 0>();
-    }
+    return v == STRIDED_VARIANT ? variant_info_t<K, STRIDED_VARIANT>() : variant_info_t<K, 0>();
 }
 template <typename K, int V>
 static void launch_group_t(K* region, uint64_t n_lines, uint32_t g, uint64_t seed, K pivot, GroupOut* out,
@@ -556,57 +301,13 @@ static void launch_group_t(K* region, uint64_t n_lines, uint32_t g, uint64_t see
 template <typename K>
 static void launch_group(int v, K* region, uint64_t n_lines, uint32_t g, uint64_t seed, K pivot, GroupOut* out,
                          cudaStream_t st) {
-    switch (v) {
-        case 1: launch_group_t<K, 1>(region, n_lines, g, seed, pivot, out, st); break;
-        case 2: launch_group_t<K, 2>(region, n_lines, g, seed, pivot, out, st); break;
-        case 3: launch_group_t<K, 3>(region, n_lines, g, seed, pivot, out, st); break;
-        case 4: launch_group_t<K, 4>(region, n_lines, g, seed, pivot, out, st); break;
-        case 5: launch_group_t<K, 5>(region, n_lines, g, seed, pivot, out, st); break;
-        case 6: launch_group_t<K, 6>(region, n_lines, g, seed, pivot, out, st); break;
-        case 7: launch_group_t<K, 7>(region, n_lines, g, seed, pivot, out, st); break;
-        case 8: launch_group_t<K, 8>(region, n_lines, g, seed, pivot, out, st); break;
-        case 9: launch_group_t<K, 9>(region, n_lines, g, seed, pivot, out, st); break;
-        default: launch_group_t<K, 0>(region, n_lines, g, seed, pivot, out, st); break;
-    }
+    if (v == STRIDED_VARIANT)
+        launch_group_t<K, STRIDED_VARIANT>(region, n_lines, g, seed, pivot, out, st);
+    else
+        launch_group_t<K, 0>(region, n_lines, g, seed, pivot, out, st);
 }
 
-// Grid-barrier flags of the fused kernel: one u32 per CTA, zeroed once;
-// every launch uses 4 fresh epochs (monotone, compared wrap-safely).
-static uint32_t* g_flags = nullptr;
-static uint64_t g_flags_cap = 0;
-static uint32_t g_epoch = 0;
-static uint32_t* grid_flags(uint64_t g) {
-    if (g > g_flags_cap) {
-        if (g_flags) {
-            cudaDeviceSynchronize();
-            cudaFree(g_flags);
-        }
-        g_flags = nullptr;
-        g_flags_cap = 0;
-        const uint64_t cap = std::max<uint64_t>(g, 1024);
-        if (cudaMalloc(&g_flags, cap * 4) != cudaSuccess) {
-            cudaGetLastError();
-            set_error("grid flag allocation failed");
-            return nullptr;
-        }
-        cudaMemset(g_flags, 0, cap * 4);
-        cudaDeviceSynchronize();
-        g_flags_cap = cap;
-        g_epoch = 0;
-    }
-    return g_flags;
-}
-static uint32_t next_epoch() {
-    const uint32_t e = g_epoch;
-    g_epoch += 4;
-    return e;
-}
-
-static int cur_variant() {
-    if (params().seed == 0) return STRIDED_VARIANT;  // "strided" param: X = 0
-    const int v = (int)params().variant;
-    return (v >= 0 && v < N_VARIANTS) ? v : 0;
-}
+static int cur_variant() { return params().seed == 0 ? STRIDED_VARIANT : 0; }  // "strided" param: X = 0
 
 struct Layout {
     size_t ctl, gout, cntL, cntR, PL, PR, posL, posR, rk, ttl, ttr, partial, flags, bm, total;
@@ -754,52 +455,6 @@ pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64
         uint64_t* rk = reinterpret_cast<uint64_t*>(ws + L.rk);
         uint32_t* ttl = reinterpret_cast<uint32_t*>(ws + L.ttl);
         uint32_t* ttr = reinterpret_cast<uint32_t*>(ws + L.ttr);
-        if (path == 2 && P.fused && variant == 0 && g <= (uint64_t)sm_count() * (uint64_t)vi.occ) {
-            // one cooperative launch: group partition + cleanup
-            using C = GroupCfg<K>;
-            uint32_t* flags = grid_flags(g);
-            if (!flags) return PP_E_NOMEM;
-            FusedArgs<K> fa;
-            fa.keys = keys;
-            fa.n = n;
-            fa.h = h;
-            fa.n_lines = n_lines;
-            fa.seed = P.seed;
-            fa.g = (uint32_t)g;
-            fa.epoch = next_epoch();
-            fa.stop = (uint32_t)P.fused_stop;
-            fa.pivot = pivot;
-            fa.gout = gout;
-            fa.ctl = ctl;
-            fa.d_split = d_split;
-            fa.cntL = cntL;
-            fa.cntR = cntR;
-            fa.ttl = ttl;
-            fa.ttr = ttr;
-            fa.flags = flags;
-            fa.PL = PL;
-            fa.PR = PR;
-            fa.rk = rk;
-            fa.posL = posL;
-            fa.posR = posR;
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(fused_partition_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)C::SMEM);
-                attr = true;
-            }
-            void* args[] = {&fa};
-            e = cudaLaunchCooperativeKernel((void*)fused_partition_kernel<C>, dim3((unsigned)g), dim3(C::NT), args,
-                                            C::SMEM, st);
-            note_launches(1);
-            S.path = 4;
-            timing_mark(st);  // whole partition counted as the "group" phase
-            timing_mark(st);
-            if (e != cudaSuccess) return cuda_fail(e, "fused partition launch");
-            e = cudaGetLastError();
-            if (e != cudaSuccess) return cuda_fail(e, "fused partition launch");
-            return PP_OK;
-        }
         // cleanup tail: fused scan+locate+barrier+swap (default) or the 3-kernel chain
         // (the fused tail needs a grid with <= FUSED_TASKS_PER_CTA tasks per CTA)
         // auto: the 3-kernel chain below 1 GiB of keys, the fused tail from
@@ -888,7 +543,7 @@ pp_status ss_groups_device(K* keys, uint64_t n, K pivot, uint64_t g_req, cudaStr
 
 uint64_t max_groups() {
     int occ = 1;
-    for (int v = 0; v < N_VARIANTS; ++v) {
+    for (int v : {0, STRIDED_VARIANT}) {
         occ = std::max(occ, variant_info<uint64_t>(v).occ);
         occ = std::max(occ, variant_info<uint32_t>(v).occ);
     }

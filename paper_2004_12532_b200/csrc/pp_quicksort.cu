@@ -3,14 +3,18 @@
 //
 // The paper runs the parallel partition at the top levels of the recursion
 // and a serial partition once subproblems are small.
-// The GPU analogue is a breadth-first level loop:
-//   - big segments (>= qs_big keys): the full multi-CTA partition pipeline of
+// The GPU analogue is a breadth-first level loop (DESIGN.md §7):
+//   - big segments (>= 2^27 keys): the full multi-CTA partition pipeline of
 //     pp_partition.cu, one segment at a time;
 //   - mid segments: ONE launch for all of them: the Smoothed Striding group
-//     kernel with (segment, group) tasks, then one CTA per segment reduces its
-//     groups and cleans its (small) window by the rank-matched walk;
-//   - leaves (<= leaf keys): sorted entirely in shared memory (bitonic
-//     network), one CTA per leaf, all leaves in one launch at the end.
+//     kernel with (segment, group) tasks, then the batched multi-CTA cleanup
+//     (heavy segments) or one CTA per segment reducing its groups and
+//     cleaning its (small) window by the rank-matched walk;
+//   - small segments (<= 2^16 keys): one CTA each runs the rest of the
+//     recursion (qs_small_kernel) and packs the leaves (<= 16384 keys) into
+//     bins; every bin is sorted by a counting sort in shared memory
+//     (qs_leaf_bidx_kernel; crowded bins by the merge sort of
+//     qs_leaf_handoff_kernel).
 // Pivot: median of A[lo], A[lo+(len-1)/2], A[hi-1]; split by x < p; when that
 // split is empty (p is the segment minimum) the next level splits by x <= p
 // and the left part (all == p) is final (reading R14).
@@ -404,47 +408,6 @@ __device__ __forceinline__ void smem_merge_sort(K* buf, uint32_t P, uint32_t nth
     }
 }
 
-// Sort of one bin (a contiguous range of <= LEAF keys; len 0 = empty slot) by
-// merging in ONE padded shared-memory buffer: every thread loads its keys
-// (all loads in flight), sorts 8 consecutive keys in registers (Batcher's
-// 19-comparator network), then log2(P/8) merge rounds; in each round every
-// thread computes its 8 outputs on the merge path into registers, and they
-// are stored after a barrier (so the buffer is read and rewritten in place).
-// One buffer = ~74 KiB for 8192 u64 keys: two CTAs per SM.  Ties: left run
-// first (a plain ascending sort; stability is irrelevant for keys).
-template <typename K, int LEAF, int NT>
-__global__ void __launch_bounds__(NT) qs_leaf_merge_kernel(K* __restrict__ keys,
-                                                           const uint64_t* __restrict__ leaf_lo,
-                                                           const uint32_t* __restrict__ leaf_len) {
-    static_assert(LEAF == NT * LEAF_E, "one block holds LEAF keys");
-    extern __shared__ __align__(16) unsigned char lsm[];
-    K* buf = reinterpret_cast<K*>(lsm);
-    const uint64_t lo = leaf_lo[blockIdx.x];
-    const uint32_t len = leaf_len[blockIdx.x];
-    // pad to whole warps of 8 keys per thread (not to a power of two)
-    const uint32_t P = (len + 32 * LEAF_E - 1) / (32 * LEAF_E) * (32 * LEAF_E);
-    const uint32_t nthr = P / LEAF_E;
-    const uint32_t tid = threadIdx.x;
-    if (tid >= nthr) return;
-    const K KMAX = (K)~(K)0;
-    {
-        K v[LEAF_E];
-#pragma unroll
-        for (int r = 0; r < LEAF_E; ++r) {
-            const uint32_t i = (uint32_t)r * nthr + tid;
-            v[r] = i < len ? __ldcs(keys + lo + i) : KMAX;
-        }
-#pragma unroll
-        for (int r = 0; r < LEAF_E; ++r) buf[lpad((uint32_t)r * nthr + tid)] = v[r];
-    }
-    leaf_bar(nthr);
-    smem_merge_sort<K>(buf, P, nthr);
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) {
-        const uint32_t i = (uint32_t)r * nthr + tid;
-        if (i < len) __stcs(keys + lo + i, buf[lpad(i)]);
-    }
-}
 
 // The bins another bin sort handed over (length word tagged BIN_HANDOFF):
 // a persistent grid walks all slots (one per thread) and merge-sorts the
@@ -510,312 +473,11 @@ __global__ void __launch_bounds__(NT) qs_leaf_handoff_kernel(K* __restrict__ key
     }
 }
 
-// Bin sort for u64 keys through 32-bit packed values: p = (top << 13) | i,
-// top = the 19 high bits of (key - min) over the bin's range (all of it when
-// the range has <= 19 bits), i = the key's position in the bin (< 8192).
-// The packed values are sorted with the same machinery as the keys
-// (smem_merge_sort) at about half the instructions (32-bit compare-exchange
-// and shuffles); the keys are gathered by index; runs of equal `top` are
-// then put in key order by the thread owning the run's first slot (insertion
-// sort; runs of equal keys are already in order).  A run of > 64 distinct
-// keys sharing `top` (keys clustered inside a wide range) sends the whole bin
-// to the 64-bit merge sort instead.  Shared memory: the keys (64 KiB), the
-// packed buffer (36 KiB) and the output (72 KiB, also the fallback's buffer).
-constexpr int PK_LEAF = 8192, PK_NT = PK_LEAF / LEAF_E, PK_IDX_BITS = 13, PK_TOP_BITS = 32 - PK_IDX_BITS;
-constexpr uint32_t PK_MAX_RUN = 64;
-// PLEAF = the bin capacity (8192 with 1024 threads, or 4096 with 512 threads:
-// half the shared memory, two CTAs per SM); the index keeps 13 bits.
-template <int PLEAF>
-__global__ void __launch_bounds__(PLEAF / LEAF_E) qs_leaf_packed_kernel(uint64_t* __restrict__ keys,
-                                                                        const uint64_t* __restrict__ leaf_lo,
-                                                                        const uint32_t* __restrict__ leaf_len) {
-    constexpr int PK_LEAF = PLEAF;
-    extern __shared__ __align__(16) unsigned char lsm[];
-    uint64_t* ks = reinterpret_cast<uint64_t*>(lsm);          // [PK_LEAF] original keys
-    uint64_t* ob = ks + PK_LEAF;                              // [lpad(PK_LEAF)] output / fallback buffer
-    uint32_t* pb = reinterpret_cast<uint32_t*>(ob + lpad(PK_LEAF));  // [lpad(PK_LEAF)] packed
-    __shared__ uint64_t rmn[32], rmx[32];
-    __shared__ int fallback;
-    const uint64_t lo = leaf_lo[blockIdx.x];
-    const uint32_t len = leaf_len[blockIdx.x];
-    const uint32_t P = (len + 32 * LEAF_E - 1) / (32 * LEAF_E) * (32 * LEAF_E);
-    const uint32_t nthr = P / LEAF_E;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid >= nthr) return;
-    uint64_t x[LEAF_E];
-    uint64_t mn = ~0ull, mx = 0;
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) {
-        const uint32_t i = (uint32_t)r * nthr + tid;
-        x[r] = i < len ? __ldcs(keys + lo + i) : 0ull;
-        if (i < len) {
-            ks[i] = x[r];
-            mn = x[r] < mn ? x[r] : mn;
-            mx = x[r] > mx ? x[r] : mx;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
-        mn = a < mn ? a : mn;
-        mx = b > mx ? b : mx;
-    }
-    if (lane == 0) {
-        rmn[warp] = mn;
-        rmx[warp] = mx;
-    }
-    if (tid == 0) fallback = 0;
-    leaf_bar(nthr);
-    for (uint32_t w = 0; w < nthr / 32; ++w) {
-        mn = rmn[w] < mn ? rmn[w] : mn;
-        mx = rmx[w] > mx ? rmx[w] : mx;
-    }
-    if (mn == mx) return;  // all keys equal: sorted already (uniform over the CTA)
-    const int bits = 64 - __clzll((long long)(mx - mn));
-    const int sh = bits > PK_TOP_BITS ? bits - PK_TOP_BITS : 0;
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) {
-        const uint32_t i = (uint32_t)r * nthr + tid;
-        pb[lpad(i)] = i < len ? ((uint32_t)((x[r] - mn) >> sh) << PK_IDX_BITS) | i : 0xFFFFFFFFu;
-    }
-    leaf_bar(nthr);
-    smem_merge_sort<uint32_t>(pb, P, nthr);
-    // gather the keys in packed order
-    const uint32_t base = tid * LEAF_E;
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) {
-        const uint32_t j = base + r;
-        if (j < len) ob[lpad(j)] = ks[pb[lpad(j)] & ((1u << PK_IDX_BITS) - 1)];
-    }
-    leaf_bar(nthr);
-    // runs of equal top: the owner of the run's first slot orders it
-#pragma unroll 1
-    for (int r = 0; r < LEAF_E; ++r) {
-        const uint32_t j = base + r;
-        if (j + 1 >= len) break;
-        const uint32_t t = pb[lpad(j)] >> PK_IDX_BITS;
-        if ((pb[lpad(j + 1)] >> PK_IDX_BITS) != t) continue;
-        if (j > 0 && (pb[lpad(j - 1)] >> PK_IDX_BITS) == t) continue;  // not the first slot of its run
-        uint32_t e = j + 1;
-        bool sorted = true;
-        while (e < len && (pb[lpad(e)] >> PK_IDX_BITS) == t) {
-            if (ob[lpad(e)] < ob[lpad(e - 1)]) sorted = false;
-            ++e;
-        }
-        if (sorted) continue;
-        if (e - j > PK_MAX_RUN) {
-            fallback = 1;
-            continue;
-        }
-        for (uint32_t a = j + 1; a < e; ++a) {  // insertion sort of ob[j, e)
-            const uint64_t v = ob[lpad(a)];
-            uint32_t b = a;
-            while (b > j && ob[lpad(b - 1)] > v) {
-                ob[lpad(b)] = ob[lpad(b - 1)];
-                --b;
-            }
-            ob[lpad(b)] = v;
-        }
-    }
-    leaf_bar(nthr);
-    if (fallback) {  // uniform: sort the original keys with 64-bit compares
-#pragma unroll
-        for (int r = 0; r < LEAF_E; ++r) {
-            const uint32_t i = (uint32_t)r * nthr + tid;
-            ob[lpad(i)] = i < len ? ks[i] : ~0ull;
-        }
-        leaf_bar(nthr);
-        smem_merge_sort<uint64_t>(ob, P, nthr);
-    }
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) {
-        const uint32_t i = (uint32_t)r * nthr + tid;
-        if (i < len) __stcs(keys + lo + i, ob[lpad(i)]);
-    }
-}
 
-// Bin sort by one counting pass (leaf_algo 5).  Bucket d = (key - min) >> sh
-// with sh the smallest shift that maps the bin's range below NB = 2 PLEAF
-// buckets: one shared-memory atomic per key yields both its bucket's count
-// and its rank inside the bucket, an exclusive scan of the counts gives the
-// bucket starts, every key is written to start + rank, and then every key
-// finds its final slot inside its bucket by counting the bucket's smaller
-// keys (ties by scatter slot; uniform keys: ~1-2 keys per bucket), all keys
-// in parallel.  With sh = 0 a bucket holds one key value, so the scatter
-// alone sorts.  A bin whose keys crowd into few buckets (a bucket of more
-// than BK_MAX_RUN keys while sh > 0: clusters inside a wide range) is sorted
-// by the 64-bit merge sort instead.  The atomics' order inside a bucket
-// never shows: the output is the sorted bin.  Far fewer instructions per key
-// than the merge sorts above (the bin sort is issue-bound, not HBM-bound).
 constexpr uint32_t BK_MAX_RUN = 48;
 template <typename K>
 __device__ __forceinline__ int key_bits(K v) {
     return sizeof(K) == 8 ? 64 - __clzll((long long)v) : 32 - __clz((int)v);
-}
-template <typename K, int PLEAF>
-__global__ void __launch_bounds__(PLEAF / LEAF_E, 8192 / PLEAF) qs_leaf_bucket_kernel(K* __restrict__ keys,
-                                                                       const uint64_t* __restrict__ leaf_lo,
-                                                                       const uint32_t* __restrict__ leaf_len) {
-    // NB = 2 * PLEAF buckets (about 0.5 keys per bucket), their 16-bit counts
-    // packed two per 32-bit word (counts and starts are <= PLEAF < 2^16)
-    constexpr int NT = PLEAF / LEAF_E, NW = NT / 32, NB = 2 * PLEAF, NWD = NB / 2;
-    constexpr int NBITS = PLEAF == 8192 ? 14 : PLEAF == 4096 ? 13 : PLEAF == 2048 ? 12 : 11;
-    static_assert((1 << NBITS) == NB, "power-of-two bin capacity");
-    static_assert(NWD == NT * LEAF_E, "8 count words per thread");
-    extern __shared__ __align__(16) unsigned char lsm[];
-    K* ob = reinterpret_cast<K*>(lsm);                                    // [lpad(PLEAF)] output
-    uint32_t* cw = reinterpret_cast<uint32_t*>(ob + lpad(PLEAF));  // [NWD + 1] packed counts, then starts
-    __shared__ K rmn[NW], rmx[NW];
-    __shared__ uint64_t sw[32];
-    __shared__ int fallback;
-    const K KMAX = (K)~(K)0;
-    const uint64_t lo = leaf_lo[blockIdx.x];
-    const uint32_t len = leaf_len[blockIdx.x];
-    if (len < 2) return;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    K x[LEAF_E];
-    K mn = KMAX, mx = 0;
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) {
-        const uint32_t i = (uint32_t)r * NT + tid;
-        x[r] = i < len ? __ldcs(keys + lo + i) : KMAX;
-        if (i < len) {
-            mn = x[r] < mn ? x[r] : mn;
-            mx = x[r] > mx ? x[r] : mx;
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) cw[r * NT + tid] = 0u;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const K a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
-        mn = a < mn ? a : mn;
-        mx = b > mx ? b : mx;
-    }
-    if (lane == 0) {
-        rmn[warp] = mn;
-        rmx[warp] = mx;
-    }
-    if (tid == 0) {
-        fallback = 0;
-        cw[NWD] = len;  // the end of the last bucket
-    }
-    __syncthreads();
-    if (warp == 0) {  // warp 0 combines the per-warp extremes
-        mn = lane < NW ? rmn[lane] : KMAX;
-        mx = lane < NW ? rmx[lane] : (K)0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const K a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
-            mn = a < mn ? a : mn;
-            mx = b > mx ? b : mx;
-        }
-        if (lane == 0) {
-            rmn[0] = mn;
-            rmx[0] = mx;
-        }
-    }
-    __syncthreads();
-    mn = rmn[0];
-    mx = rmx[0];
-    if (mn == mx) return;  // all keys equal (uniform over the CTA)
-    const int bits = key_bits<K>(mx - mn);
-    const int sh = bits > NBITS ? bits - NBITS : 0;
-    uint32_t rk[LEAF_E];
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) {
-        const uint32_t i = (uint32_t)r * NT + tid;
-        const uint32_t d = (uint32_t)((x[r] - mn) >> sh), hs = (d & 1u) * 16u;
-        rk[r] = i < len ? (atomicAdd(&cw[d >> 1], 1u << hs) >> hs) & 0xFFFFu : 0u;
-    }
-    __syncthreads();
-    // bucket starts: thread t owns words [8t, 8t + 8) = buckets [16t, 16t + 16)
-    uint32_t c[LEAF_E], s = 0;
-#pragma unroll
-    for (int j = 0; j < LEAF_E; ++j) {
-        c[j] = cw[tid * LEAF_E + j];
-        s += (c[j] & 0xFFFFu) + (c[j] >> 16);
-    }
-    uint64_t tot;
-    const uint32_t start = (uint32_t)block_exscan<NT>(s, sw, tot);
-    if (sh > 0) {
-#pragma unroll
-        for (int j = 0; j < LEAF_E; ++j)
-            if ((c[j] & 0xFFFFu) > BK_MAX_RUN || (c[j] >> 16) > BK_MAX_RUN) fallback = 1;
-    }
-    {
-        uint32_t e = start;
-#pragma unroll
-        for (int j = 0; j < LEAF_E; ++j) {
-            const uint32_t e1 = e + (c[j] & 0xFFFFu);
-            cw[tid * LEAF_E + j] = e | (e1 << 16);
-            e = e1 + (c[j] >> 16);
-        }
-    }
-    __syncthreads();
-    if (fallback) {  // crowded buckets: 64-bit merge sort of the whole bin
-        const uint32_t P = (len + 32 * LEAF_E - 1) / (32 * LEAF_E) * (32 * LEAF_E);
-        const uint32_t nthr = P / LEAF_E;
-#pragma unroll
-        for (int r = 0; r < LEAF_E; ++r) {
-            const uint32_t i = (uint32_t)r * NT + tid;
-            if (i < P) ob[lpad(i)] = x[r];  // x = KMAX past len
-        }
-        __syncthreads();
-        if (tid < nthr) smem_merge_sort<K>(ob, P, nthr);
-        __syncthreads();
-    } else {
-        // (unpadded layout: every access below is either random or warp-contiguous)
-#pragma unroll
-        for (int r = 0; r < LEAF_E; ++r) {
-            const uint32_t i = (uint32_t)r * NT + tid;
-            const uint32_t d = (uint32_t)((x[r] - mn) >> sh);
-            if (i < len) ob[((cw[d >> 1] >> ((d & 1u) * 16u)) & 0xFFFFu) + rk[r]] = x[r];
-        }
-        __syncthreads();
-        if (sh > 0) {  // final place inside the bucket: smaller keys, ties by scatter slot
-            uint32_t (&dst)[LEAF_E] = rk;  // rank -> destination, in place
-#pragma unroll
-            for (int r = 0; r < LEAF_E; ++r) {
-                const uint32_t i = (uint32_t)r * NT + tid;
-                if (i < len) {
-                    const uint32_t d = (uint32_t)((x[r] - mn) >> sh);
-                    const uint32_t w = cw[d >> 1];
-                    const uint32_t b0 = (d & 1u) ? w >> 16 : w & 0xFFFFu;
-                    const uint32_t b1 = (d & 1u) ? cw[(d >> 1) + 1] & 0xFFFFu : w >> 16;  // cw[NWD] = len
-                    const uint32_t p = b0 + rk[r];
-                    uint32_t q = 0xFFFFFFFFu;  // a bucket of one key: already in place
-                    if (b1 - b0 > 1) {
-                        q = b0;
-#pragma unroll 1
-                        for (uint32_t j = b0; j < b1; ++j) {
-                            const K y = ob[j];
-                            q += (y < x[r]) | ((y == x[r]) & (j < p));
-                        }
-                    }
-                    dst[r] = q;
-                } else {
-                    dst[r] = 0xFFFFFFFFu;
-                }
-            }
-            __syncthreads();
-#pragma unroll
-            for (int r = 0; r < LEAF_E; ++r)
-                if (dst[r] != 0xFFFFFFFFu) ob[dst[r]] = x[r];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < LEAF_E; ++r) {
-            const uint32_t i = (uint32_t)r * NT + tid;
-            if (i < len) __stcs(keys + lo + i, ob[i]);
-        }
-        return;
-    }
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) {
-        const uint32_t i = (uint32_t)r * NT + tid;
-        if (i < len) __stcs(keys + lo + i, ob[lpad(i)]);
-    }
 }
 
 // Bin sort leaf_algo 6: the counting sort of qs_leaf_bucket_kernel with the
@@ -996,40 +658,14 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
 // shared memory by merging.  This removes the deepest, least efficient
 // levels of the breadth-first loop (many tiny CTAs, one launch + sync each).
 // ===========================================================================
-// V = 0: 256 threads, 8 KiB lines, 4 KiB... 64 KiB sort buffers (2 CTAs/SM);
-// V = 1: lean -- 128 threads, 4 KiB lines with 2 in flight per end, 32 KiB
-// sort buffers: ~37 KiB of shared memory, 4 CTAs per SM (more independent
-// recursions per SM to hide the latency-bound merge rounds).
-template <typename K, int V>
-struct SmallCfg;
+// 128 threads, 4 KiB lines with 4 in flight per end (refills issued by one
+// lane per line), 32 KiB sort buffers: 4 CTAs per SM (independent recursions
+// hide each other's latency).  (256-thread / 8 KiB-line and 2-in-flight
+// configurations measured slower in round 1 and were removed.)
 template <typename K>
-struct SmallCfg<K, 0> {
-    static constexpr int NT = 256, MINB = 2;
-    using GC = GroupCfgT<K, 8192, 256, 4, false>;
-    static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 4096 : 8192;  // 2 x LEAFC keys <= 64 KiB
-    static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);  // two padded buffers
-    static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
-};
-template <typename K>
-struct SmallCfg<K, 2> {  // V = 1 with the refills issued by one lane per line (PAR_ISSUE)
-    static constexpr int NT = 128, MINB = 4;
-    using GC = GroupCfgT<K, 4096, 128, 2, false, false, true>;
-    static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 2048 : 4096;
-    static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);
-    static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
-};
-template <typename K>
-struct SmallCfg<K, 3> {  // V = 2 with 4 lines in flight per end
+struct SmallCfg {
     static constexpr int NT = 128, MINB = 4;
     using GC = GroupCfgT<K, 4096, 128, 4, false, false, true>;
-    static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 2048 : 4096;
-    static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);
-    static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
-};
-template <typename K>
-struct SmallCfg<K, 1> {
-    static constexpr int NT = 128, MINB = 4;
-    using GC = GroupCfgT<K, 4096, 128, 2, false>;
     static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 2048 : 4096;
     static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);
     static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
@@ -1067,10 +703,10 @@ __device__ void cta_merge_sort(K* __restrict__ g, uint32_t len, K* A, K* B) {
 }
 
 // In-place partition of seg[0, len) by key < pivot with one CTA; returns K.
-template <typename K, int V>
+template <typename K>
 __device__ uint64_t cta_partition(K* __restrict__ seg, uint64_t len, K pivot, uint64_t seed, unsigned char* smem,
                                   GroupOut* scratch, Ctl* sc, uint64_t* red, uint64_t* pr = nullptr) {
-    using S = SmallCfg<K, V>;
+    using S = SmallCfg<K>;
     using GC = typename S::GC;
     constexpr int NT = S::NT, NW = NT / 32;
     const uint64_t addr = (uint64_t)(uintptr_t)seg;
@@ -1144,17 +780,17 @@ constexpr int QM_INCTA = 2;   // flag: this range is sorted inside the CTA (bin 
 // each bin (a contiguous range that is a union of whole leaves, so sorting it
 // whole sorts each leaf) is written to this segment's slots [slot_base[i],
 // +qs_bin_cap); unused slots get length 0.  One wide shared-memory sort
-// launch then sorts every bin (qs_leaf_merge_kernel).  Ranges whose keys are
+// launch then sorts every bin (qs_leaf_bidx_kernel).  Ranges whose keys are
 // all equal (the x <= min split, reading R14) are final and skipped.  If the
 // slots run out, the overflowing bin is pushed back with QM_INCTA and sorted
 // by this CTA itself (partition down to LEAFC, merge sort in shared memory).
-template <typename K, int V>
-__global__ void __launch_bounds__(SmallCfg<K, V>::NT, SmallCfg<K, V>::MINB)
+template <typename K>
+__global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
     qs_small_kernel(K* __restrict__ keys, const uint64_t* __restrict__ seg_lo, const uint32_t* __restrict__ seg_len,
                     const uint64_t* __restrict__ slot_base, uint64_t* __restrict__ bin_lo,
                     uint32_t* __restrict__ bin_len, uint32_t leaf, uint64_t seed, GroupOut* __restrict__ scratch,
                     uint64_t* __restrict__ prof) {
-    using S = SmallCfg<K, V>;
+    using S = SmallCfg<K>;
     constexpr int DEPTH = 64, LEFT_FIRST_MAX = 40;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ Ctl sc;
@@ -1231,7 +867,7 @@ __global__ void __launch_bounds__(SmallCfg<K, V>::NT, SmallCfg<K, V>::MINB)
         if ((mode & QM_LE) == 0) p = median3<K>(keys[lo], keys[lo + (len - 1) / 2], keys[hi - 1]);
         else p = (K)pm;
         if (prof) { const uint64_t t1 = clock64(); pr[0] += t1 - t0; t0 = t1; }
-        const uint64_t k = cta_partition<K, V>(keys + lo, len, p, seed, smem, scratch + blockIdx.x, &sc, red,
+        const uint64_t k = cta_partition<K>(keys + lo, len, p, seed, smem, scratch + blockIdx.x, &sc, red,
                                                prof ? pr : nullptr);
         if (prof) { const uint64_t t1 = clock64(); pr[1] += t1 - t0; pr[4] += 1; pr[6] += len; t0 = t1; }
         if (threadIdx.x == 0) {
@@ -1262,204 +898,7 @@ __global__ void __launch_bounds__(SmallCfg<K, V>::NT, SmallCfg<K, V>::MINB)
     }
 }
 
-// Bin sort by a stable LSD radix sort over the bits the bin's keys actually
-// span (after ~15 quicksort levels a bin is narrow: ~49 bits for uniform u64
-// keys, ~10 for keys in [0,1000)): digit_p(x) = ((x - min) >> 8p) & 255 for
-// p < ceil(bits(max - min) / 8); a bin whose keys are all equal is left as is.
-// No comparisons (the merge sort is issue-bound on 64-bit compare-exchange)
-// and no atomics: warp w owns positions [256w, 256w+256) (8 rounds of 32
-// lanes), ranks its keys per digit against its own row
-// of u16 counters (peers found by 8 ballots, one per digit bit), a
-// fixed-order scan turns the counters into offsets
-// (digit-major, then warp), and the keys are scattered from registers into
-// one shared buffer and reloaded in position order.  Stable by construction
-// (position order within a warp, warps in order within a digit).  Positions
-// >= len are padded with the bin's maximum, which stays after the real
-// maxima (stability) and is never stored.  Registers hold the keys, so one
-// 64 KiB buffer + 16 KiB of counters suffices.
-template <typename K, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) qs_leaf_radix_kernel(K* __restrict__ keys,
-                                                                   const uint64_t* __restrict__ leaf_lo,
-                                                                   const uint32_t* __restrict__ leaf_len) {
-    extern __shared__ __align__(16) unsigned char lsm[];
-    K* buf = reinterpret_cast<K*>(lsm);                        // NW * 256 keys
-    uint16_t* cnt = reinterpret_cast<uint16_t*>(buf + NW * 256);  // [NW][256]
-    __shared__ uint32_t dbase[256];
-    __shared__ uint32_t dtot[256];
-    __shared__ K rmn[NW], rmx[NW];
-    const uint64_t lo = leaf_lo[blockIdx.x];
-    const uint32_t len = leaf_len[blockIdx.x];
-    if (len <= 1) return;
-    const uint32_t W = (len + 255) / 256;  // active warps
-    const uint32_t nthr = W * 32;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    if (tid >= nthr) return;
-    const uint32_t lt = lanemask_lt();
-    const K KMAX = (K)~(K)0;
-    K v[8];
-    K mn = KMAX, mx = 0;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const uint32_t p = 256 * w + 32 * r + lane;
-        v[r] = p < len ? __ldcs(keys + lo + p) : (K)0;
-        if (p < len) {
-            mn = v[r] < mn ? v[r] : mn;
-            mx = v[r] > mx ? v[r] : mx;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const K a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
-        mn = a < mn ? a : mn;
-        mx = b > mx ? b : mx;
-    }
-    if (lane == 0) {
-        rmn[w] = mn;
-        rmx[w] = mx;
-    }
-    leaf_bar(nthr);
-    for (uint32_t i = 0; i < W; ++i) {
-        mn = rmn[i] < mn ? rmn[i] : mn;
-        mx = rmx[i] > mx ? rmx[i] : mx;
-    }
-    if (mn == mx) return;  // all keys equal: already sorted (uniform across the CTA)
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-        if (256 * w + 32 * r + lane >= len) v[r] = mx;
-    const uint64_t range = (uint64_t)(mx - mn);
-    const int bits = 64 - __clzll((long long)range);
-    const int npass = (bits + 7) / 8;
-    uint16_t* row = cnt + 256 * w;
-    for (int pass = 0; pass < npass; ++pass) {
-        const int shift = 8 * pass;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) row[32 * k + lane] = 0;
-        __syncwarp();
-        uint32_t d[8], rk[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) d[r] = (uint32_t)((uint64_t)(v[r] - mn) >> shift) & 255u;
-        uint32_t peers[8];  // lanes of this round with the same digit (ballot multisplit, 8 ballots)
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            uint32_t m = 0xffffffffu;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const bool bit = (d[r] >> b) & 1u;
-                const uint32_t bb = __ballot_sync(0xffffffffu, bit);
-                m &= bit ? bb : ~bb;
-            }
-            peers[r] = m;
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const uint32_t m = peers[r];
-            const uint32_t c = row[d[r]];
-            rk[r] = c + __popc(m & lt);
-            __syncwarp();
-            if (lane == (uint32_t)(__ffs(m) - 1)) row[d[r]] = (uint16_t)(c + __popc(m));
-            __syncwarp();
-        }
-        leaf_bar(nthr);
-        // per digit: exclusive prefix over the warps (in place) and the digit total
-        for (uint32_t dg = tid; dg < 256; dg += nthr) {
-            uint32_t acc = 0;
-            for (uint32_t i = 0; i < W; ++i) {
-                const uint32_t c = cnt[256 * i + dg];
-                cnt[256 * i + dg] = (uint16_t)acc;
-                acc += c;
-            }
-            dtot[dg] = acc;
-        }
-        leaf_bar(nthr);
-        if (w == 0) {  // exclusive scan of the 256 digit totals, 8 per lane
-            uint32_t t8[8], sacc = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                t8[k] = sacc;
-                sacc += dtot[8 * lane + k];
-            }
-            uint32_t x = sacc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= (uint32_t)o) x += y;
-            }
-            const uint32_t ex = x - sacc;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) dbase[8 * lane + k] = ex + t8[k];
-        }
-        leaf_bar(nthr);
-#pragma unroll
-        for (int r = 0; r < 8; ++r) buf[dbase[d[r]] + row[d[r]] + rk[r]] = v[r];
-        leaf_bar(nthr);
-#pragma unroll
-        for (int r = 0; r < 8; ++r) v[r] = buf[256 * w + 32 * r + lane];
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const uint32_t p = 256 * w + 32 * r + lane;
-        if (p < len) __stcs(keys + lo + p, v[r]);
-    }
-}
 
-template <typename K, int LEAF, int NT>
-__global__ void __launch_bounds__(NT) qs_leaf_kernel(K* __restrict__ keys, const uint64_t* __restrict__ leaf_lo,
-                                                     const uint32_t* __restrict__ leaf_len) {
-    static_assert(LEAF == NT * LEAF_E, "one block holds LEAF keys");
-    extern __shared__ __align__(16) unsigned char lsm_b[];
-    K* sk = reinterpret_cast<K*>(lsm_b);  // LEAF keys (dynamic shared memory)
-    const uint64_t lo = leaf_lo[blockIdx.x];
-    const uint32_t len = leaf_len[blockIdx.x];
-    uint32_t P = 32 * LEAF_E;
-    while (P < len) P <<= 1;
-    const uint32_t nthr = P / LEAF_E;  // whole warps
-    const uint32_t tid = threadIdx.x;
-    if (tid >= nthr) return;
-    const K KMAX = (K)~(K)0;
-    for (uint32_t i = tid; i < P; i += nthr) sk[i] = i < len ? keys[lo + i] : KMAX;
-    leaf_bar(nthr);
-    const uint32_t base = tid * LEAF_E;
-    K v[LEAF_E];
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) v[r] = sk[base + r];
-    for (uint32_t k = 2; k <= P; k <<= 1) {
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 32 * LEAF_E) {  // partner in another warp: exchange through smem
-                leaf_bar(nthr);
-#pragma unroll
-                for (int r = 0; r < LEAF_E; ++r) sk[base + r] = v[r];
-                leaf_bar(nthr);
-#pragma unroll
-                for (int r = 0; r < LEAF_E; ++r) {
-                    const uint32_t i = base + r, p = i ^ j;
-                    const K y = sk[p];
-                    const bool keep_min = ((i < p) == ((i & k) == 0));
-                    v[r] = keep_min ? (v[r] < y ? v[r] : y) : (v[r] > y ? v[r] : y);
-                }
-            } else if (j >= LEAF_E) {  // partner lane in this warp
-                const int lm = (int)(j / LEAF_E);
-#pragma unroll
-                for (int r = 0; r < LEAF_E; ++r) {
-                    const K y = __shfl_xor_sync(0xffffffffu, v[r], lm);
-                    const uint32_t i = base + r, p = i ^ j;
-                    const bool keep_min = ((i < p) == ((i & k) == 0));
-                    v[r] = keep_min ? (v[r] < y ? v[r] : y) : (v[r] > y ? v[r] : y);
-                }
-            } else if (j == 4) {
-                leaf_reg_stage<4>(v, base, k);
-            } else if (j == 2) {
-                leaf_reg_stage<2>(v, base, k);
-            } else {
-                leaf_reg_stage<1>(v, base, k);
-            }
-        }
-    }
-    leaf_bar(nthr);
-#pragma unroll
-    for (int r = 0; r < LEAF_E; ++r) sk[base + r] = v[r];
-    leaf_bar(nthr);
-    for (uint32_t i = tid; i < len; i += nthr) keys[lo + i] = sk[i];
-}
 
 template <typename K>
 struct LeafCfg {
@@ -1559,7 +998,7 @@ static QsGeom qs_geom() {
     // leaf capacity: LC::LEAF (8192 keys) for the bin sorts 1-5; the default
     // bin sort (6) takes bins of up to 2 LC::LEAF and defaults to that;
     // "leaf" may lower it
-    const uint64_t lmax = (P.leaf_algo == 0 || P.leaf_algo == 6) ? 2 * (uint64_t)LC::LEAF : (uint64_t)LC::LEAF;
+    const uint64_t lmax = 2 * (uint64_t)LC::LEAF;
     q.LEAF = (P.leaf > 0 && (uint64_t)P.leaf <= lmax) ? (uint64_t)P.leaf : lmax;
     q.BIG = P.qs_cta_max > 0 ? (uint64_t)P.qs_cta_max : (uint64_t)1 << 27;
     q.SMALL = P.qs_small > 0 ? std::max<uint64_t>((uint64_t)P.qs_small, q.LEAF) : q.LEAF;
@@ -1687,112 +1126,42 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     if (lvl_prof)
         for (Lane& L : lanes)
             for (auto& x : L.lev) cudaEventCreate(&x);
-    // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot
+    // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot:
+    // the index-staged counting sort, then the merge sort of the bins it handed
+    // off (crowded buckets)
     auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
         if (cnt == 0) return cudaSuccess;
-        // default: the index-staged counting bin sort (6); 5 = counting with keys in registers,
-        // 4 = packed 32-bit merge (u64 only), 3 = merge
-        const int64_t algo = P.leaf_algo != 0 ? P.leaf_algo : 6;
-        if (algo == 6) {  // bins of <= 2 LC::LEAF keys (1024 threads) or <= LC::LEAF (512 threads, 2 CTAs/SM)
-            constexpr int HL = LC::LEAF, HN = HL / LEAF_E;
-            if (LEAF > (uint64_t)HL) {
-                constexpr int PL = 2 * HL, BNT = 1024;
-                const size_t smem = sizeof(K) * PL + 4 * PL + 16;
-                cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-                qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
-                                                                                  const_cast<uint32_t*>(d_len));
-            } else {
-                constexpr int PL = HL, BNT = 512;
-                const size_t smem = sizeof(K) * PL + 4 * PL + 16;
-                cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-                qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
-                                                                                  const_cast<uint32_t*>(d_len));
-            }
-            const size_t msmem = sizeof(K) * lpad_host(2 * HL);
-            cudaFuncSetAttribute(qs_leaf_handoff_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)msmem);
-            const unsigned hg = (unsigned)std::min<uint64_t>((cnt + HN - 1) / HN, 2 * (uint64_t)sm_count());
-            qs_leaf_handoff_kernel<K, HL, HN><<<hg, HN, msmem, bst>>>(keys, d_lo, d_len, cnt);
-            note_launches(1);
-        } else if (algo == 5 && LEAF <= (uint64_t)LC::LEAF / 2) {
-            constexpr int PL = LC::LEAF / 2;
-            const size_t smem = sizeof(K) * lpad_host(PL) + 4 * PL + 16;
-            cudaFuncSetAttribute(qs_leaf_bucket_kernel<K, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_bucket_kernel<K, PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(keys, d_lo, d_len);
-        } else if (algo == 5) {
-            constexpr int PL = LC::LEAF;
-            const size_t smem = sizeof(K) * lpad_host(PL) + 4 * PL + 16;
-            cudaFuncSetAttribute(qs_leaf_bucket_kernel<K, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_bucket_kernel<K, PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(keys, d_lo, d_len);
-        } else if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF / 2) {
-            constexpr int PL = PK_LEAF / 2;
-            const size_t smem = 8 * PL + 8 * lpad_host(PL) + 4 * lpad_host(PL);
-            cudaFuncSetAttribute(qs_leaf_packed_kernel<PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_packed_kernel<PL><<<(unsigned)cnt, PL / LEAF_E, smem, bst>>>(reinterpret_cast<uint64_t*>(keys),
-                                                                                d_lo, d_len);
-        } else if (algo == 4 && sizeof(K) == 8 && LEAF <= (uint64_t)PK_LEAF) {
-            const size_t smem = 8 * PK_LEAF + 8 * lpad_host(PK_LEAF) + 4 * lpad_host(PK_LEAF);
-            cudaFuncSetAttribute(qs_leaf_packed_kernel<PK_LEAF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        constexpr int HL = LC::LEAF, HN = HL / LEAF_E;
+        if (LEAF > (uint64_t)HL) {  // bins of <= 2 LC::LEAF keys: 1024 threads, one CTA per SM
+            constexpr int PL = 2 * HL, BNT = 1024;
+            const size_t smem = sizeof(K) * PL + 4 * PL + 16;
+            cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            qs_leaf_packed_kernel<PK_LEAF><<<(unsigned)cnt, PK_NT, smem, bst>>>(reinterpret_cast<uint64_t*>(keys), d_lo,
-                                                                               d_len);
-        } else if (algo == 2) {
-            constexpr int NW = LC::LEAF / 256;
-            const size_t smem = sizeof(K) * LC::LEAF + 2 * 256 * NW;
-            cudaFuncSetAttribute(qs_leaf_radix_kernel<K, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_radix_kernel<K, NW><<<(unsigned)cnt, NW * 32, smem, bst>>>(keys, d_lo, d_len);
-        } else if (algo == 1) {
-            const size_t smem = sizeof(K) * LC::LEAF;
-            cudaFuncSetAttribute(qs_leaf_kernel<K, LC::LEAF, LC::NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
+                                                                              const_cast<uint32_t*>(d_len));
+        } else {  // bins of <= LC::LEAF keys: 512 threads, two CTAs per SM
+            constexpr int PL = HL, BNT = 512;
+            const size_t smem = sizeof(K) * PL + 4 * PL + 16;
+            cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            qs_leaf_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, bst>>>(keys, d_lo, d_len);
-        } else if (LEAF <= (uint64_t)LC::LEAF / 4) {  // small bins: quarter-size CTAs, more per SM
-            constexpr int QL = LC::LEAF / 4, QN = QL / LEAF_E;
-            const size_t smem = sizeof(K) * (QL + QL / 8);
-            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, QL, QN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            qs_leaf_merge_kernel<K, QL, QN><<<(unsigned)cnt, QN, smem, bst>>>(keys, d_lo, d_len);
-        } else if (LEAF <= (uint64_t)LC::LEAF / 2) {  // half-size CTAs
-            constexpr int HL = LC::LEAF / 2, HN = HL / LEAF_E;
-            const size_t smem = sizeof(K) * (HL + HL / 8);
-            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            qs_leaf_merge_kernel<K, HL, HN><<<(unsigned)cnt, HN, smem, bst>>>(keys, d_lo, d_len);
-        } else {
-            const size_t smem = sizeof(K) * (LC::LEAF + LC::LEAF / 8);
-            cudaFuncSetAttribute(qs_leaf_merge_kernel<K, LC::LEAF, LC::NT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            qs_leaf_merge_kernel<K, LC::LEAF, LC::NT><<<(unsigned)cnt, LC::NT, smem, bst>>>(keys, d_lo, d_len);
+            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
+                                                                              const_cast<uint32_t*>(d_len));
         }
-        note_launches(1);
+        const size_t msmem = sizeof(K) * lpad_host(2 * HL);
+        cudaFuncSetAttribute(qs_leaf_handoff_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)msmem);
+        const unsigned hg = (unsigned)std::min<uint64_t>((cnt + HN - 1) / HN, 2 * (uint64_t)sm_count());
+        qs_leaf_handoff_kernel<K, HL, HN><<<hg, HN, msmem, bst>>>(keys, d_lo, d_len, cnt);
+        note_launches(2);
         return cudaGetLastError();
     };
     // the per-CTA recursion over `cnt` small segments (lists on the device)
     auto launch_small = [&](uint64_t cnt, const uint64_t* slo, const uint32_t* sln, const uint64_t* sbase,
                             uint64_t* blo, uint32_t* bln, GroupOut* scr, uint64_t* prof, cudaStream_t s3) {
-        if (P.qs_small_cfg == 2) {
-            using S = SmallCfg<K, 2>;
-            cudaFuncSetAttribute(qs_small_kernel<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-            qs_small_kernel<K, 2><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln,
-                                                                         (uint32_t)LEAF, P.seed, scr, prof);
-        } else if (P.qs_small_cfg == 3) {
-            using S = SmallCfg<K, 3>;
-            cudaFuncSetAttribute(qs_small_kernel<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-            qs_small_kernel<K, 3><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln,
-                                                                         (uint32_t)LEAF, P.seed, scr, prof);
-        } else if (P.qs_small_cfg == 0) {
-            using S = SmallCfg<K, 0>;
-            cudaFuncSetAttribute(qs_small_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-            qs_small_kernel<K, 0><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln,
-                                                                         (uint32_t)LEAF, P.seed, scr, prof);
-        } else {
-            using S = SmallCfg<K, 1>;
-            cudaFuncSetAttribute(qs_small_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-            qs_small_kernel<K, 1><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln,
-                                                                         (uint32_t)LEAF, P.seed, scr, prof);
-        }
+        using S = SmallCfg<K>;
+        cudaFuncSetAttribute(qs_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+        qs_small_kernel<K><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln, (uint32_t)LEAF,
+                                                                  P.seed, scr, prof);
         note_launches(1);
         return cudaGetLastError();
     };
@@ -2221,8 +1590,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         static cudaStream_t st2 = nullptr;
         static std::vector<cudaEvent_t> evs;
         if (!st2) cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking);
-        const uint64_t pipe = (uint64_t)std::max<int64_t>(P.qs_pipe, 1);
-        const uint64_t chunk = std::min<uint64_t>(QS_LIST_CHUNK, std::max<uint64_t>(1, (nsmall + pipe - 1) / pipe));
+        const uint64_t chunk = QS_LIST_CHUNK;
         const uint64_t nchunks = (nsmall + chunk - 1) / chunk;
         while (evs.size() < nchunks + 1) {
             cudaEvent_t ev;
@@ -2238,29 +1606,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(d_sbase, small_base.data() + b0, 8 * cnt, cudaMemcpyHostToDevice, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort small H2D");
-            if (P.qs_small_cfg == 2) {
-                using S = SmallCfg<K, 2>;
-                cudaFuncSetAttribute(qs_small_kernel<K, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-                qs_small_kernel<K, 2><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(
-                    keys, d_slo, d_sln, d_sbase, d_blo, d_bln, (uint32_t)LEAF, P.seed, d_scr, d_prof);
-            } else if (P.qs_small_cfg == 3) {
-                using S = SmallCfg<K, 3>;
-                cudaFuncSetAttribute(qs_small_kernel<K, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-                qs_small_kernel<K, 3><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(
-                    keys, d_slo, d_sln, d_sbase, d_blo, d_bln, (uint32_t)LEAF, P.seed, d_scr, d_prof);
-            } else if (P.qs_small_cfg == 0) {
-                using S = SmallCfg<K, 0>;
-                cudaFuncSetAttribute(qs_small_kernel<K, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-                qs_small_kernel<K, 0><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(
-                    keys, d_slo, d_sln, d_sbase, d_blo, d_bln, (uint32_t)LEAF, P.seed, d_scr, d_prof);
-            } else {
-                using S = SmallCfg<K, 1>;
-                cudaFuncSetAttribute(qs_small_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
-                qs_small_kernel<K, 1><<<(unsigned)cnt, S::NT, S::SMEM, st>>>(
-                    keys, d_slo, d_sln, d_sbase, d_blo, d_bln, (uint32_t)LEAF, P.seed, d_scr, d_prof);
-            }
-            note_launches(1);
-            e = cudaGetLastError();
+            e = launch_small(cnt, d_slo, d_sln, d_sbase, d_blo, d_bln, d_scr, d_prof, st);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort small launch");
             if (d_prof) {
                 std::vector<uint64_t> h(8 * cnt);

@@ -1,6 +1,6 @@
 """Seeded fuzzing of the CUDA paths against the CPU oracle: random sizes,
 base alignments, key distributions, pivots and tuning-parameter
-combinations (paths, group-kernel variants, group counts, cleanup tails,
+combinations (paths, group counts, cleanup tails,
 Strided offsets, bin sorts, quicksort thresholds).  Deterministic (fixed
 seeds), so a failure reproduces."""
 import numpy as np
@@ -63,9 +63,9 @@ def _pivot(rng, a, mx):
 
 PARTITION_PARAMS = [
     {}, {"path": 1}, {"path": 3}, {"small_n": 0}, {"small_n": 0, "min_lines_per_group": 1},
-    {"g": 3}, {"g": 64}, {"variant": 1}, {"variant": 4}, {"variant": 8}, {"cleanup_chain": 1},
+    {"g": 3}, {"g": 64}, {"cleanup_chain": 1},
     {"cleanup_chain": 0}, {"cleanup_chain": 0, "small_n": 0},
-    {"cleanup_bitmap": 0}, {"strided": 1}, {"strided": 1, "small_n": 0}, {"fused": 1},
+    {"cleanup_bitmap": 0}, {"strided": 1}, {"strided": 1, "small_n": 0},
 ]
 
 
@@ -108,11 +108,9 @@ def test_fuzz_partition(pp):
 
 
 QUICKSORT_PARAMS = [
-    {}, {"leaf_algo": 1}, {"leaf_algo": 2}, {"leaf_algo": 3}, {"leaf": 1000}, {"leaf": 4096},
+    {}, {"leaf": 1000}, {"leaf": 4096}, {"leaf": 2000}, {"leaf": 8192},
     {"qs_small": 0}, {"qs_small": 1 << 18}, {"qs_cta_max": 1 << 16}, {"qs_heavy": 1 << 17},
-    {"qs_heavy": 0}, {"qs_waves": 1}, {"qs_small_cfg": 0}, {"qs_pipe": 3},
-    {"leaf_algo": 5}, {"leaf_algo": 5, "leaf": 4096}, {"leaf_algo": 4}, {"leaf_algo": 3, "leaf": 4096},
-    {"leaf_algo": 6}, {"leaf_algo": 6, "leaf": 2000}, {"qs_lanes": 1}, {"qs_lanes": 2, "qs_cta_max": 1 << 18},
+    {"qs_heavy": 0}, {"qs_waves": 1}, {"qs_lanes": 1}, {"qs_lanes": 2, "qs_cta_max": 1 << 18},
     {"qs_early": 1}, {"qs_early": 1, "qs_small": 1 << 17, "qs_cta_max": 1 << 19},
 ]
 

@@ -109,19 +109,18 @@ def test_groups_and_windows(pp, dt, mx, g):
 
 
 @pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
-@pytest.mark.parametrize("fused", [0, 1])
-def test_fused_and_chain_paths(pp, dt, mx, fused):
-    """The default single cooperative kernel and the multi-kernel chain give
+@pytest.mark.parametrize("chain", [0, 1])
+def test_cleanup_tails(pp, dt, mx, chain):
+    """The fused scan/swap cleanup tail and the 3-kernel chain give
     oracle-exact results, including large windows (forced g) and ragged n."""
-    rng = np.random.default_rng(31 + fused)
+    rng = np.random.default_rng(31 + chain)
     for n, g in ((1 << 20, 0), (3_000_017, 0), (3_000_017, 5), (1 << 22, 100), (777_777, 296)):
         a = rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
         for frac in (0.0, 0.2, 0.5, 1.0):
             p = min(mx, int(frac * (mx + 1)))
-            split, out = _run(pp, a, p, 1, fused=fused, g=g)
+            split, out = _run(pp, a, p, 1, cleanup_chain=chain, g=g)
             oracle.check_partition(a, out, p, split)
-            st = pp.pp_last_stats()
-            assert st["path"] == (4 if fused else 2)
+            assert pp.pp_last_stats()["path"] == 2
 
 
 @pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
@@ -419,19 +418,18 @@ def test_config4_adversarial_full(pp, pat):
     _full_check(pp, t, synth.ADV_PIVOT_U32, K)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 8, 9])
-def test_group_variants(pp, variant):
-    """Every group-kernel configuration (line size, threads, prefetch depth,
-    store path) is parity-exact, including runs right after other kernels
-    (dirty shared memory)."""
-    rng = np.random.default_rng(variant)
-    for dt, mx in ((np.uint64, U64_MAX), (np.uint32, U32_MAX)):
-        for n in (3_000_017, 1 << 22):
-            a = rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
-            for frac in (0.01, 0.5):
-                p = int(frac * (mx + 1))
-                split, out = _run(pp, a, p, 1, variant=variant)
-                oracle.check_partition(a, out, p, split)
+def test_group_kernel_dirty_smem(pp):
+    """The group kernel right after other kernels (dirty shared memory), both
+    key widths and instantiations (default, Strided)."""
+    rng = np.random.default_rng(7)
+    for strided in (0, 1):
+        for dt, mx in ((np.uint64, U64_MAX), (np.uint32, U32_MAX)):
+            for n in (3_000_017, 1 << 22):
+                a = rng.integers(0, mx, size=n, dtype=dt, endpoint=True)
+                for frac in (0.01, 0.5):
+                    p = int(frac * (mx + 1))
+                    split, out = _run(pp, a, p, 1, strided=strided)
+                    oracle.check_partition(a, out, p, split)
 
 
 @pytest.mark.parametrize("strided", [0, 1])

@@ -77,16 +77,13 @@ def test_medium_sizes(pp, dt, mx):
 
 
 @pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
-@pytest.mark.parametrize("params", [{"leaf_algo": 1}, {"leaf_algo": 3}, {"leaf_algo": 3, "leaf": 300},
-                                    {"leaf_algo": 2, "leaf": 300}, {"qs_waves": 1}, {"qs_waves": 16, "leaf": 1000},
+@pytest.mark.parametrize("params", [{"leaf": 300}, {"leaf": 1000}, {"leaf": 4096}, {"leaf": 8192},
+                                    {"qs_waves": 1}, {"qs_waves": 16, "leaf": 1000},
                                     {"qs_heavy": 1 << 17}, {"qs_heavy": 0}, {"qs_small": 0}, {"strided": 1},
-                                    {"qs_pipe": 1}, {"qs_pipe": 16}, {"qs_small_cfg": 0}, {"qs_small_cfg": 1}, {"qs_small_cfg": 2},
-                                    {"leaf_algo": 5}, {"leaf_algo": 5, "leaf": 4096}, {"leaf_algo": 5, "leaf": 300},
-                                    {"leaf_algo": 6}, {"leaf_algo": 6, "leaf": 300}, {"qs_lanes": 1},
-                                    {"qs_lanes": 2}, {"qs_lanes": 2, "qs_small": 1 << 17}, {"qs_early": 1},
-                                    {"qs_early": 1, "qs_lanes": 1}, {"qs_early": 0}])
+                                    {"qs_lanes": 1}, {"qs_lanes": 2}, {"qs_lanes": 2, "qs_small": 1 << 17},
+                                    {"qs_early": 1}, {"qs_early": 1, "qs_lanes": 1}, {"qs_early": 0}])
 def test_qs_parameters(pp, dt, mx, params):
-    """Bin sorts (radix / merge / bitonic), leaf sizes, level balancing, the
+    """Bin sizes (both bin-sort CTA shapes), level balancing, the
     heavy-segment batched cleanup, the per-CTA recursion and the Strided
     offsets all give the oracle's sorted output."""
     rng = np.random.default_rng(4)
@@ -123,15 +120,12 @@ def test_config5_full(pp, kind):
     assert np.array_equal(out, ref)
 
 
-@pytest.mark.parametrize("leaf_algo,leaf", [(0, 0), (2, 0), (3, 0), (4, 0), (5, 0), (5, 4096), (6, 0), (6, 1000),
-                                            (6, 8192), (6, 12000), (6, 10240)])
-def test_bin_sorts_clustered(pp, leaf_algo, leaf):
-    """Bins whose keys cluster inside a wide range: the packed 32-bit bin sort
-    (leaf_algo 4) sees runs of equal top bits -- short runs are
-    insertion-sorted, a run of > 64 distinct keys falls back to the 64-bit
-    merge sort; the counting bin sort (leaf_algo 5) sees crowded buckets --
-    up to 48 keys per thread's 8 buckets are insertion-sorted, more fall back
-    to the merge sort -- and every bin sort gives the oracle's order."""
+@pytest.mark.parametrize("leaf", [0, 1000, 4096, 8192, 12000, 10240])
+def test_bin_sorts_clustered(pp, leaf):
+    """Bins whose keys cluster inside a wide range: the counting bin sort sees
+    crowded buckets (> 48 keys in a bucket while the shift is > 0) and hands
+    the bin to the merge sort (qs_leaf_handoff_kernel); buckets at and around
+    the limit; every bin capacity gives the oracle's order."""
     rng = np.random.default_rng(9)
     cases = []
     # 100 clusters of 50 distinct keys each + the maximum: runs of 50 equal tops
@@ -149,12 +143,12 @@ def test_bin_sorts_clustered(pp, leaf_algo, leaf):
         a = a[rng.permutation(a.size)]
         for n in (a.size, min(a.size, 8192), min(a.size, 16384), min(a.size, 12345), 300):
             b = a[:n].copy()
-            out = _sort_gpu(pp, b, 1, leaf_algo=leaf_algo, leaf=leaf)
-            assert np.array_equal(out, _oracle_sorted(b)), (leaf_algo, n)
+            out = _sort_gpu(pp, b, 1, leaf=leaf)
+            assert np.array_equal(out, _oracle_sorted(b)), (leaf, n)
     # the same clusters inside a large quicksort (bins from the per-CTA recursion)
     big = np.concatenate([c.reshape(-1) for c in [cl] * 40] + [synth.uniform_u64_np(300000, 3)])
     big = big[rng.permutation(big.size)]
-    out = _sort_gpu(pp, big, 0, leaf_algo=leaf_algo, leaf=leaf)
+    out = _sort_gpu(pp, big, 0, leaf=leaf)
     assert np.array_equal(out, _oracle_sorted(big))
 
 

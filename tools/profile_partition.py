@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Short driver for ncu captures: a few c2 partitions (n=2^27 u64, mu=0.5).
 
-    python tools/profile_partition.py [--reps 3] [--variant 0] [--n 27]
+    python tools/profile_partition.py [--reps 3] [--n 27]
 """
 import argparse
 import os
@@ -19,13 +19,11 @@ import synth  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--n", type=int, default=27)
     ap.add_argument("--dtype", default="u64")
     args = ap.parse_args()
     pp.load(build_if_missing=False)
     pp.reset_params()
-    pp.pp_set_param("variant", args.variant)
     n = 1 << args.n
     dev = torch.device("cuda")
     if args.dtype == "u64":

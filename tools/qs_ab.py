@@ -2,7 +2,7 @@
 """A/B quicksort parameter settings on the GPU (CUDA-event timing, median of
 reps), each result checked against the library sort.
 
-    python tools/qs_ab.py "" "leaf_algo=5" "leaf_algo=5,leaf=4096" [--n 28] [--kinds uniform,dup1000] [--dtype u64]
+    python tools/qs_ab.py "" "leaf=8192" "qs_early=0" [--n 28] [--kinds uniform,dup1000] [--dtype u64]
 """
 import argparse
 import json

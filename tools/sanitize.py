@@ -56,7 +56,6 @@ def case_partition():
     part(u64, 1 << 63, small_n=1 << 12, cleanup_chain=1)        # group + 3-kernel cleanup chain
     part(u64, 1 << 62, small_n=1 << 12, cleanup_chain=0)        # group + fused tail (bitmap)
     part(u64, 1 << 63, small_n=1 << 12, cleanup_chain=0, cleanup_bitmap=0)  # fused tail, grid barrier
-    part(u64, 1 << 63, small_n=1 << 12, fused=1)                # one cooperative kernel
     part(u64, 1 << 63, small_n=1 << 12, path=3)                 # cleanup only
     part(u32, 1 << 31, small_n=1 << 12)
     part(u32, 1 << 30, small_n=1 << 12, cleanup_chain=0)
