@@ -617,7 +617,18 @@ def extras(pp, torch, synth, dev, stream, flush, args):
             if i >= 1:
                 ts.append(s.elapsed_time(e))
         ms = statistics.mean(ts)
-        res[f"quicksort_{kind}_2^28"] = {"keys_per_s": nq / (ms / 1e3), "ms": ms}
+        qs = pp.pp_quicksort_last_stats()
+        # pass model: every level reads + writes the keys of the
+        # segments it partitions (level_keys), the per-CTA recursion makes at
+        # least one pass over the small segments, the bin sort one over all n
+        model = 16 * (qs["level_keys"] + qs["small_keys"] + nq)
+        peak, _ = peaks()
+        res[f"quicksort_{kind}_2^28"] = {
+            "keys_per_s": nq / (ms / 1e3), "ms": ms, "stats": qs,
+            "roofline": {"bound": "hbm", "model_bytes": model, "achieved": model / (ms / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": model / (ms / 1e3) / 1e9 / peak,
+                         "model": "2*w*(level_keys + small_keys + n): levels + one per-CTA recursion pass + one bin "
+                                  "pass (a lower bound on the bytes moved)"}}
         del q0, q
 
     def timed(fn, reps=3):

@@ -283,6 +283,15 @@ uint64_t pp_last_aux_bytes(void);
  * size), v_min, v_max, M (misplaced pairs in the cleanup), g, line_keys,
  * n_lines, head, aux_bytes, path, nTasks}.  Reads device memory: synchronous. */
 pp_status pp_last_stats(uint64_t *out13);
+/* Work statistics of the last single-GPU quicksort (host counters, no device
+ * access): out6 = {n, levels (depth of the breadth-first level loop),
+ * level_keys (sum over levels of the keys in the segments partitioned there:
+ * each is read and written once by that level's kernels), small_keys (keys in
+ * segments of (leaf, qs_small] keys, finished by the per-CTA recursion),
+ * leaf_keys (keys in segments of <= leaf keys, sorted by the bin sort
+ * directly), nsmall (number of such small segments)}.  bench.py derives the
+ * quicksort's algorithmic bytes from these. */
+pp_status pp_quicksort_last_stats(uint64_t *out6);
 /* Tunables (tests / benchmarks): "g", "min_lines_per_group", "small_n",
  * "path" (0 auto, 1 single-CTA, 2 smoothed striding, 3 cleanup only), "tile",
  * "ranks", "seed", "strided" (1: X = 0, the Strided Algorithm PAPER.md:796-825,

@@ -116,6 +116,7 @@ def load(build_if_missing: bool = True):
         "pp_ipc_import": ([vp, u64, ctypes.POINTER(ctypes.c_void_p)], st),
         "pp_ipc_close_all": ([], st),
         "pp_dist_last_timing": ([ctypes.POINTER(ctypes.c_double)], st),
+        "pp_quicksort_last_stats": ([P64], st),
         "pp_partition_dist_loopback_u64": ([vp, P64, ctypes.c_int, u64, P64], st),
         "pp_partition_dist_loopback_u32": ([vp, P64, ctypes.c_int, u32, P64], st),
         "pp_quicksort_dist_loopback_u64": ([vp, P64, ctypes.c_int], st),
@@ -316,6 +317,16 @@ def pp_last_stats() -> dict:
     out = (ctypes.c_uint64 * 13)()
     _check(load().pp_last_stats(out), "pp_last_stats")
     return dict(zip(STAT_KEYS, [int(v) for v in out]))
+
+
+QS_STAT_KEYS = ("n", "levels", "level_keys", "small_keys", "leaf_keys", "nsmall")
+
+
+def pp_quicksort_last_stats() -> dict:
+    """Work statistics of the last quicksort (include/pp.h)."""
+    out = (ctypes.c_uint64 * 6)()
+    _check(load().pp_quicksort_last_stats(out), "pp_quicksort_last_stats")
+    return dict(zip(QS_STAT_KEYS, [int(v) for v in out]))
 
 
 def pp_set_param(name: str, value: int) -> None:

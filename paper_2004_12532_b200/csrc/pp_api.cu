@@ -757,6 +757,11 @@ pp_status pp_last_stats(uint64_t* out) {
     return PP_OK;
 }
 
+pp_status pp_quicksort_last_stats(uint64_t* out6) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return quicksort_last_stats(out6);
+}
+
 void pp_reset_params(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     g_params = Params();

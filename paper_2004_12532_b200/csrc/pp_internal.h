@@ -96,6 +96,7 @@ pp_status ss_groups_device(K* keys, uint64_t n, K pivot, uint64_t g, cudaStream_
 
 template <typename K>
 pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st);
+pp_status quicksort_last_stats(uint64_t* out6);
 
 // the paper's Blocked-Prefix-Sum partition, low-space form (pp_bps.cu)
 template <typename K>

@@ -932,6 +932,18 @@ static size_t g_qws_bytes = 0;
 // after the partition region of the top-level call: [partition | quicksort].
 static size_t g_qs_user_base = 0;
 static size_t g_qs_peak = 0;
+// work statistics of the last quicksort (pp_quicksort_last_stats)
+struct QsStats {
+    uint64_t n = 0, levels = 0, level_keys = 0, small_keys = 0, leaf_keys = 0, nsmall = 0;
+};
+static QsStats g_qs_stats;
+pp_status quicksort_last_stats(uint64_t* out6) {
+    if (!out6) return PP_E_INVAL;
+    const QsStats& q = g_qs_stats;
+    const uint64_t v[6] = {q.n, q.levels, q.level_keys, q.small_keys, q.leaf_keys, q.nsmall};
+    for (int i = 0; i < 6; ++i) out6[i] = v[i];
+    return PP_OK;
+}
 static inline size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
 // leaf / small-segment descriptor lists are uploaded in chunks of this many
 // entries, so the quicksort workspace stays o(n) however many leaves there are
@@ -1058,6 +1070,8 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     const K KMAX = (K)~(K)0;
     g_qs_user_base = al256(partition_workspace_bound(n));
     g_qs_peak = 0;
+    g_qs_stats = QsStats();
+    g_qs_stats.n = n;
 
     struct HSeg {
         uint64_t lo, hi, pivot;
@@ -1074,7 +1088,10 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         if (len <= LEAF) {
             leaf_lo.push_back(lo);
             leaf_len.push_back((uint32_t)len);
+            g_qs_stats.leaf_keys += len;
         } else if (len <= SMALL) {
+            g_qs_stats.small_keys += len;
+            ++g_qs_stats.nsmall;
             small_lo.push_back(lo);
             small_len.push_back((uint32_t)len);
             small_base_v.push_back(small_base_v.back() + qs_bin_cap(len, LEAF));
@@ -1099,7 +1116,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         cudaEvent_t done = nullptr;
         cudaEvent_t lev[3] = {nullptr, nullptr, nullptr};
         unsigned char* pin = nullptr;
-        uint64_t nmid = 0, nbig = 0, gtot = 0;
+        uint64_t nmid = 0, nbig = 0, gtot = 0, depth = 0;
         bool inflight = false;
         int id = 0;
     };
@@ -1137,15 +1154,13 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             const size_t smem = sizeof(K) * PL + 4 * PL + 16;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
-                                                                              const_cast<uint32_t*>(d_len));
+            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
         } else {  // bins of <= LC::LEAF keys: 512 threads, two CTAs per SM
             constexpr int PL = HL, BNT = 512;
             const size_t smem = sizeof(K) * PL + 4 * PL + 16;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo,
-                                                                              const_cast<uint32_t*>(d_len));
+            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
         }
         const size_t msmem = sizeof(K) * lpad_host(2 * HL);
         cudaFuncSetAttribute(qs_leaf_handoff_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1232,6 +1247,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     auto launch_level = [&](Lane& L) -> pp_status {
         L.inflight = false;
         if (L.cur.empty()) return PP_OK;
+        g_qs_stats.levels = std::max<uint64_t>(g_qs_stats.levels, ++L.depth);
         L.mids.clear();
         L.big_idx.clear();
         L.mid_idx.clear();
@@ -1332,6 +1348,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         }
         const uint64_t nmid = mids.size(), nbig = L.big_idx.size();
         L.nmid = nmid;
+        for (const HSeg& sg : L.cur) g_qs_stats.level_keys += sg.hi - sg.lo;  // every key of the level is partitioned
         L.nbig = nbig;
         L.gtot = gtot;
         // heavy mid segments: batched multi-CTA cleanup
@@ -1528,6 +1545,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         }
         if (cut == 0) cut = 1;
         lanes[1].cur.assign(c0.begin() + cut, c0.end());
+        lanes[1].depth = lanes[0].depth;
         c0.resize(cut);
         e = cudaEventRecord(lane_ev[2], st);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(lane_st1, lane_ev[2], 0);

@@ -167,3 +167,22 @@ def test_quicksort_2pow30(pp, kind):
     del t, ref
     torch.cuda.empty_cache()
 
+
+
+def test_quicksort_last_stats(pp):
+    """pp_quicksort_last_stats: the level loop partitions every key once per
+    level while its segment is above qs_small (level_keys >= n for n above it),
+    and every key ends in a small segment or a leaf list (or an all-equal
+    range, which no list holds): small_keys + leaf_keys <= n."""
+    from gpu_util import to_dev
+    n = 1 << 22
+    a = synth.uniform_u64_np(n, 4)
+    t = to_dev(a)
+    pp.pp_quicksort(t)
+    st = pp.pp_quicksort_last_stats()
+    assert st["n"] == n and st["levels"] >= 5 and st["level_keys"] >= 5 * n
+    assert 0 < st["small_keys"] + st["leaf_keys"] <= n and st["nsmall"] > 0
+    t = to_dev(np.full(1000, 5, dtype=np.uint64))
+    pp.pp_quicksort(t)
+    st = pp.pp_quicksort_last_stats()
+    assert st["n"] == 1000 and st["levels"] == 0 and st["leaf_keys"] == 1000
