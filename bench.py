@@ -329,9 +329,14 @@ def main():
     pp.pp_timing(False)
     step_ms, launches = [], 0
     phases = []
+    copy_ms = []  # the untimed restores: a D2D copy of the shard, the sustained copy rate at this size
     for i in range(args.steps):
+        cs, ce = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cs.record(stream)
         restore()
+        ce.record(stream)
         sync_all()
+        copy_ms.append(cs.elapsed_time(ce))
         pp.pp_launch_count(reset=True)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
@@ -407,6 +412,10 @@ def main():
                      "kernel": "ss_group_kernel", "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": grp_bytes, "avg_launch_ms": grp_ms,
                      "kernel_share_of_step": (tim["group_ms"] / tim["total_ms"]) if tim["total_ms"] else None,
+                     "sustained_copy_gbs_same_size": (16 * n / (statistics.median(copy_ms) / 1e3) / 1e9)
+                     if pristine is not None else None,
+                     "frac_of_sustained_copy": (achieved / (16 * n / (statistics.median(copy_ms) / 1e3) / 1e9))
+                     if (pristine is not None and achieved) else None,
                      "timing": f"group kernel bracketed by CUDA events on the launching stream in a second pass "
                                f"of {reps2} steps (restored untimed); the timed steps run without these events"},
         "gpu_launches": launches,

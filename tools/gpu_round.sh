@@ -43,5 +43,8 @@ if has ncu; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:ss_group -s 1 -c 1 \
     -o "$OUT/group_full" -f python tools/profile_partition.py > "$OUT/ncu_full.log" 2>&1
   echo "ncu_full exit $?" >> "$OUT/status.txt"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:ss_group -s 1 -c 1 \
+    -o "$OUT/group_full_u32" -f python tools/profile_partition.py --dtype u32 > "$OUT/ncu_full_u32.log" 2>&1
+  echo "ncu_full_u32 exit $?" >> "$OUT/status.txt"
 fi
 cat "$OUT/status.txt"
