@@ -26,6 +26,7 @@ if has bench; then
 fi
 if has launches; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    -k regex:"ss_group|reduce_count|scan_swap|tile_scan|locate_kernel|swap_kernel|small_partition|count_kernel" \
     --log-file "$OUT/launches.csv" python bench.py --steps 3 --warmup 3 --no-extras --no-cpu-baseline --no-e2e \
     > "$OUT/ncu_launches.log" 2>&1
   echo "launches exit $?" >> "$OUT/status.txt"
