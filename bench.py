@@ -265,6 +265,10 @@ def main():
     import paper_2004_12532_b200 as pp
     import synth
 
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep rank 0's stdout to the one JSON line
+    if args.force_dist and "RANK" not in os.environ:  # one process without torchrun
+        os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0", "MASTER_ADDR": "127.0.0.1",
+                           "MASTER_PORT": os.environ.get("MASTER_PORT", "29533")})
     ws, rank, local = dist_env()
     dist_on = ws > 1 or args.force_dist
     torch.cuda.set_device(local)
