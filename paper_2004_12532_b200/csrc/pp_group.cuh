@@ -43,8 +43,18 @@ struct GroupCfgT {
 // the default configuration (used by quicksort and by variant 0), measured
 // fastest on B200 (tools/tune.py): 8 KiB lines for u64 (b = 1024 keys),
 // 4 KiB lines for u32 (b = 1024 keys, 4 CTAs per SM); 128 threads.
+#ifndef PP_U32_LINE  // A/B builds only (tools/)
+#define PP_U32_LINE 4096
+#endif
+#ifndef PP_U32_NT
+#define PP_U32_NT 128
+#endif
+#ifndef PP_U32_PF
+#define PP_U32_PF 4
+#endif
 template <typename K>
-using GroupCfg = GroupCfgT<K, sizeof(K) == 8 ? 8192 : 4096, 128, 4, false, false, sizeof(K) == 4>;
+using GroupCfg = GroupCfgT<K, sizeof(K) == 8 ? 8192 : PP_U32_LINE, sizeof(K) == 8 ? 128 : PP_U32_NT,
+                           sizeof(K) == 8 ? 4 : PP_U32_PF, false, false, sizeof(K) == 4>;
 
 // Line index of the j-th line (group order) of group gi: G_i(j) of
 // PAPER.md:963-969 in 0-based form, j*g + ((X[j] + i) mod g).

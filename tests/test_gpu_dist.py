@@ -357,3 +357,46 @@ def test_loopback_failure_agreement(pp, fault, rank):
     t = to_dev(a)
     K = pp.pp_partition_dist_loopback(t, ns, 1 << 63)
     oracle.check_partition(a, to_host(t, np.uint64), 1 << 63, K)
+
+
+def test_loopback_fuzz(pp):
+    """Seeded fuzz of the product exchange at P > 1 (loopback): random rank
+    counts, shard sizes (empty ones included), key widths, key alphabets,
+    pivots, staging caps and exchange paths; partition against the oracle's
+    checks, quicksort byte for byte against oracle.quicksort."""
+    import os
+    from gpu_util import to_dev, to_host
+    rng = np.random.default_rng(int(os.environ.get("PP_FUZZ_SEED", 20_0412_532)))
+    try:
+        for trial in range(40):
+            P = int(rng.integers(2, 9))
+            dt = np.uint64 if rng.random() < 0.6 else np.uint32
+            mx = (1 << 64) - 1 if dt == np.uint64 else (1 << 32) - 1
+            total = int(rng.choice([0, 1, 7, 1000, 65_537, 333_333, 1 << 20]))
+            ns = _shards(rng, total, P, str(rng.choice(["ragged", "empty", "equal"])))
+            alpha = int(rng.choice([2, 1000, 0]))
+            a = (rng.integers(0, alpha, size=total).astype(dt) if alpha
+                 else rng.integers(0, mx, size=total, dtype=dt, endpoint=True))
+            pp.reset_params()
+            pp.pp_set_param("dist_p2p", int(rng.integers(0, 2)))
+            pp.pp_set_param("dist_small", int(rng.choice([64, 5000, 1 << 16])))
+            pp.pp_dist_set_staging(int(rng.choice([16, 4096, 1 << 20, 256 << 20])))
+            ctx = (trial, P, dt, total, ns, alpha)
+            if rng.random() < 0.5:
+                pivot = int(rng.choice([0, mx, int(a[rng.integers(0, total)]) if total else 1,
+                                        int(rng.integers(0, mx, dtype=dt))]))
+                t = to_dev(a) if total else torch.empty(0, dtype=torch.int64 if dt == np.uint64 else torch.int32,
+                                                       device="cuda")
+                K = pp.pp_partition_dist_loopback(t, ns, pivot)
+                assert K == oracle.count(a, pivot), ctx
+                if total:
+                    oracle.check_partition(a, to_host(t, dt), pivot, K)
+            elif total:
+                t = to_dev(a)
+                pp.pp_quicksort_dist_loopback(t, ns)
+                ref = a.copy()
+                oracle.quicksort(ref)
+                assert np.array_equal(to_host(t, dt), ref), ctx
+    finally:
+        pp.pp_dist_set_staging(256 << 20)
+        pp.reset_params()
