@@ -372,7 +372,7 @@ def test_loopback_fuzz(pp):
             P = int(rng.integers(2, 9))
             dt = np.uint64 if rng.random() < 0.6 else np.uint32
             mx = (1 << 64) - 1 if dt == np.uint64 else (1 << 32) - 1
-            total = int(rng.choice([0, 1, 7, 1000, 65_537, 333_333, 1 << 20]))
+            total = [0, 1, 7, 1000, 65_537, 333_333, 1 << 20][int(rng.integers(0, 7))]
             ns = _shards(rng, total, P, str(rng.choice(["ragged", "empty", "equal"])))
             alpha = int(rng.choice([2, 1000, 0]))
             a = (rng.integers(0, alpha, size=total).astype(dt) if alpha
@@ -383,8 +383,8 @@ def test_loopback_fuzz(pp):
             pp.pp_dist_set_staging(int(rng.choice([16, 4096, 1 << 20, 256 << 20])))
             ctx = (trial, P, dt, total, ns, alpha)
             if rng.random() < 0.5:
-                pivot = int(rng.choice([0, mx, int(a[rng.integers(0, total)]) if total else 1,
-                                        int(rng.integers(0, mx, dtype=dt))]))
+                cands = [0, mx, int(a[rng.integers(0, total)]) if total else 1, int(rng.integers(0, mx, dtype=dt))]
+                pivot = cands[int(rng.integers(0, len(cands)))]  # (rng.choice would round through float64)
                 t = to_dev(a) if total else torch.empty(0, dtype=torch.int64 if dt == np.uint64 else torch.int32,
                                                        device="cuda")
                 K = pp.pp_partition_dist_loopback(t, ns, pivot)
