@@ -115,7 +115,7 @@ pp_status pp_partition_stable_async_u64(const uint64_t *in, uint64_t *out, uint6
  * in place through a library-owned device buffer.  These are what an
  * application with host-resident data calls; bench.py's "e2e" number times
  * them (H2D + kernels + D2H).  pp_partition_host_* streams: chunks of
- * "host_chunk" keys (param, default 2^22) are uploaded alternately from the
+ * "host_chunk" keys (param, default 2^23) are uploaded alternately from the
  * front and the back, each is partitioned on the device as it lands, and its
  * keys < pivot are copied back to the front of host_keys, the others to the
  * back, as soon as those host positions have been uploaded -- downloads

@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""e2e host-buffer partition (pinned host memory, 2^27 u64) for several
-streamed chunk sizes: python tools/e2e_sweep.py [chunk ...]"""
+"""e2e host-buffer partition (pinned host memory, 2^EXP u64; env E2E_EXP,
+default 27) for several streamed chunk sizes: python tools/e2e_sweep.py [chunk ...]"""
 import json
 import os
 import sys
@@ -17,15 +17,15 @@ import synth  # noqa: E402
 
 def main():
     pp.load(build_if_missing=False)
-    n = 1 << 27
-    a = synth.uniform_u64_np(n, synth.SEEDS["c2"])
+    n = 1 << int(os.environ.get("E2E_EXP", "27"))
+    a = synth.uniform_u64_np(n, synth.SEEDS["c3"])
     pin = torch.empty(n, dtype=torch.int64, pin_memory=True)
     hv = pin.numpy().view(np.uint64)
     for c in [int(x) for x in sys.argv[1:]] or [1 << 20, 1 << 22, 1 << 24]:
         pp.reset_params()
         pp.pp_set_param("host_chunk", c)
         ts = []
-        for i in range(5):
+        for i in range(4):
             np.copyto(hv, a)
             t0 = time.perf_counter()
             pp.pp_partition_host_u64(hv, 1 << 63)
