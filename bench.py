@@ -62,15 +62,23 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the group kernel from the committed ncu capture."""
+def ncu_traffic(n: int, alg_bytes: int):
+    """DRAM bytes per launch of the group kernel from the committed ncu
+    captures (profiles/ncu_summary.json): the capture of this very size when
+    there is one (2^33 keys: one-pass dram metrics, no replay), else the c2
+    capture's traffic per algorithmic byte times this launch's algorithmic
+    bytes (said so in the line)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("ss_group_kernel", {}).get("dram_bytes_per_launch")
+        exact = {(1 << 33): "ss_group_kernel_2^33", (1 << 27): "ss_group_kernel"}.get(n)
+        if exact and exact in d:
+            return d[exact]["dram_bytes_per_launch"], d[exact]["source"]
+        e = d["ss_group_kernel"]
+        return e["dram_bytes_per_launch"] / e["algorithmic_bytes"] * alg_bytes, "scaled from " + e["source"]
     except Exception:
-        return None
+        return None, None
 
 
 class ClockSampler:
@@ -395,7 +403,7 @@ def main():
     grp_bytes = 2 * 8 * stats.get("n_lines", n // 1024) * line_keys
     grp_ms = tim["group_ms"] / max(tim["calls"], 1)
     achieved = grp_bytes / (grp_ms / 1e3) / 1e9 if grp_ms > 0 else None
-    traffic = ncu_traffic()
+    traffic, traffic_src = ncu_traffic(n, grp_bytes)
     gbs = bytes_step / (ms_per_step / 1e3) / 1e9
 
     out = {
@@ -413,7 +421,7 @@ def main():
         "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "ss_group_kernel", "peak_source": peak_kind,
+                     "kernel": "ss_group_kernel", "peak_source": peak_kind, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": grp_bytes, "avg_launch_ms": grp_ms,
                      "kernel_share_of_step": (tim["group_ms"] / tim["total_ms"]) if tim["total_ms"] else None,
                      "sustained_copy_gbs_same_size": (16 * n / (statistics.median(copy_ms) / 1e3) / 1e9)

@@ -47,5 +47,10 @@ if has ncu; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:ss_group -s 1 -c 1 \
     -o "$OUT/group_full_u32" -f python tools/profile_partition.py --dtype u32 > "$OUT/ncu_full_u32.log" 2>&1
   echo "ncu_full_u32 exit $?" >> "$OUT/status.txt"
+  # the headline launch (2^33 u64): one-pass DRAM metrics, no replay of the 64 GiB kernel
+  timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:ss_group -c 1 --csv --log-file "$OUT/c3_traffic.csv" python tools/size_sweep.py --exps 33 --reps 1 \
+    > "$OUT/ncu_c3.log" 2>&1
+  echo "ncu_c3_traffic exit $?" >> "$OUT/status.txt"
 fi
 cat "$OUT/status.txt"
