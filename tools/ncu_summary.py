@@ -46,7 +46,9 @@ def launches(path):
         us = v / 1e3 if unit in ("ns", "nsecond") else (v * 1e3 if unit in ("ms", "msecond") else v)
         c, t = agg.get(k, (0, 0.0))
         agg[k] = (c + 1, t + us)
-    ours = {k: v for k, v in agg.items() if "pp::" in k or k.startswith("void pp") or "ss_group" in k}
+    OURS = ("pp::", "ss_group", "reduce_count", "scan_swap", "tile_scan", "locate_kernel", "swap_kernel",
+            "small_partition", "count_kernel", "qs_", "bps_", "stable_", "swap_ranges")
+    ours = {k: v for k, v in agg.items() if k.startswith("void pp") or any(t in k for t in OURS)}
     tot = sum(t for _, t in ours.values()) or 1.0
     print(f"{'kernel':72s} {'launches':>8s} {'total_us':>10s} {'avg_us':>9s} {'share_of_pp':>11s}")
     for k, (c, t) in agg.items():
