@@ -468,7 +468,7 @@ def main():
 
 def e2e(pp, torch, dist, rank, ws, off, n, args):
     """End to end through the public host-buffer API on every rank: a sample
-    of min(n_per_gpu, 2^30) keys of the rank's c3 shard in pinned host
+    of min(n_per_gpu, 2^30 / N) keys of the rank's c3 shard in pinned host
     memory; every step copies it in (H2D), partitions it on the GPU and
     copies the whole partitioned sample and the split back (D2H) --
     pp_partition_host_u64 (the streamed host partition),
@@ -477,7 +477,7 @@ def e2e(pp, torch, dist, rank, ws, off, n, args):
     ranks; the NCCL exchange is not part of this number (it is in the
     device-timed value)."""
     import synth
-    m = min(n, E2E_SAMPLE)
+    m = min(n, max(1 << 20, E2E_SAMPLE // ws))  # the whole job samples ~2^30 keys: host memory stays bounded at N = 8
     pristine = synth.uniform_u64_np(m, synth.SEEDS["c3"], offset=off)
     host = torch.empty(m, dtype=torch.int64, pin_memory=True)
     hv = host.numpy().view(np.uint64)
@@ -501,8 +501,8 @@ def e2e(pp, torch, dist, rank, ws, off, n, args):
             "steps": steps, "ms_per_step": 1e3 * sum(times) / steps, "sample_keys_per_gpu": m,
             "api": "pp_partition_host_u64 (pinned host; streamed chunks: H2D from both ends, per-chunk GPU "
                    "partition, D2H of each side overlapping the uploads)",
-            "timing": "host wall clock around the synchronous call; sample = the first min(n_per_gpu, 2^30) keys "
-                      "of each rank's c3 shard (PCIe-bound, size-independent beyond a few GiB)"}
+            "timing": "host wall clock around the synchronous call; sample = the first min(n_per_gpu, 2^30 / N) "
+                      "keys of each rank's c3 shard (PCIe-bound, size-independent beyond a few GiB)"}
 
 
 def extras(pp, torch, synth, dev, stream, flush, args):
