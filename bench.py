@@ -598,6 +598,25 @@ def extras(pp, torch, synth, dev, stream, flush, args):
         "ms": ms, "keys_per_s": n / (ms / 1e3), "gbs_2nw": 16 * n / (ms / 1e3) / 1e9,
         "gbs_traffic_3nw": 24 * n / (ms / 1e3) / 1e9, "aux_bytes": 8 * n}
     del outb
+    # SURVEY §8(f) #4, in place: the stable partition by tile partitions +
+    # rotation merges (O(n log n) work), the price of stability in place
+    wb = torch.empty_like(pristine)
+    ts = []
+    for i in range(4):
+        wb.copy_(pristine)
+        flush.sum()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        pp.pp_partition_stable_inplace(wb, PIVOT)
+        e.record(stream)
+        torch.cuda.synchronize()
+        if i >= 1:
+            ts.append(s.elapsed_time(e))
+    ms = statistics.mean(ts)
+    res["stable_in_place"] = {"ms": ms, "keys_per_s": n / (ms / 1e3), "gbs_2nw": 16 * n / (ms / 1e3) / 1e9,
+                              "aux_bytes": pp.pp_last_stats()["aux_bytes"],
+                              "note": "synchronous call (includes the split readback)"}
+    del wb
     # the paper's Blocked-Prefix-Sum partition (low-space form,
     # PAPER.md:319-478, 1466-1486), in place, on the same input
     wb = torch.empty_like(pristine)

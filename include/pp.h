@@ -110,6 +110,21 @@ pp_status pp_partition_stable_u32(const uint32_t *in, uint32_t *out, uint64_t n,
 pp_status pp_partition_stable_async_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t pivot,
                                         void *stream, uint64_t *d_split);
 
+/* ---- stable IN-PLACE partition (comparison row) ----------
+ * The Standard Algorithm's output (stable on both sides)
+ * produced in place: every tile of 4096 keys is stable-partitioned in
+ * registers, then adjacent partitioned segments [P1 S1][P2 S2] are merged
+ * into [P1 P2 S1 S2] by rotating [S1 P2] with three in-place reversals,
+ * level by level (PAPER.md:309-311 notes that only the out-of-place
+ * Standard Algorithm is stable).  O(n log(n / 4096)) work (about two passes
+ * over the array per level), O(n / 4096) aux words, deterministic, no
+ * atomics; equals pp_partition_stable_* byte for byte.  keys: DEVICE
+ * pointer to n keys (in place); split_out: HOST pointer; synchronous. */
+pp_status pp_partition_stable_inplace_u64(uint64_t *keys, uint64_t n, uint64_t pivot, void *stream,
+                                          uint64_t *split_out);
+pp_status pp_partition_stable_inplace_u32(uint32_t *keys, uint64_t n, uint32_t pivot, void *stream,
+                                          uint64_t *split_out);
+
 /* ---- host-buffer (end-to-end) variants ------------------------------------
  * host_keys: HOST pointer (pinned or pageable) to n keys, partitioned / sorted
  * in place through a library-owned device buffer.  These are what an

@@ -83,6 +83,8 @@ def load(build_if_missing: bool = True):
         "pp_partition_bps_u32": ([vp, u64, u32, vp, P64], st),
         "pp_partition_bps_async_u64": ([vp, u64, u64, vp, vp], st),
         "pp_partition_stable_u32": ([vp, vp, u64, u32, vp, P64], st),
+        "pp_partition_stable_inplace_u64": ([vp, u64, u64, vp, P64], st),
+        "pp_partition_stable_inplace_u32": ([vp, u64, u32, vp, P64], st),
         "pp_partition_stable_async_u64": ([vp, vp, u64, u64, vp, vp], st),
         "pp_partition_host_u32": ([vp, u64, u32, P64], st),
         "pp_quicksort_host_u64": ([vp, u64], st),
@@ -249,6 +251,17 @@ def pp_partition_stable(keys_in, keys_out, pivot: int, stream=None) -> int:
     f = load().pp_partition_stable_u64 if kind == "u64" else load().pp_partition_stable_u32
     _check(f(keys_in.data_ptr(), keys_out.data_ptr(), keys_in.numel(), _pivot(pivot, kind), _stream_ptr(stream, keys_in.device),
              ctypes.byref(out)), "pp_partition_stable")
+    return int(out.value)
+
+
+def pp_partition_stable_inplace(keys, pivot: int, stream=None) -> int:
+    """Stable partition IN PLACE (tile partitions + rotation merges,
+    O(n log n) work): the Standard Algorithm's output; returns the split."""
+    kind = _key_kind(keys)
+    out = ctypes.c_uint64(0)
+    f = load().pp_partition_stable_inplace_u64 if kind == "u64" else load().pp_partition_stable_inplace_u32
+    _check(f(keys.data_ptr(), keys.numel(), _pivot(pivot, kind), _stream_ptr(stream, keys.device), ctypes.byref(out)),
+           "pp_partition_stable_inplace")
     return int(out.value)
 
 

@@ -323,6 +323,41 @@ static pp_status partition_bps(K* keys, uint64_t n, K pivot, void* stream, uint6
     return PP_OK;
 }
 
+// In-place stable partition (pp_stable.cu): synchronous, split to the host.
+template <typename K>
+static pp_status partition_stable_inplace(K* keys, uint64_t n, K pivot, void* stream, uint64_t* split_out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!split_out) {
+        set_error("split_out is NULL");
+        return PP_E_INVAL;
+    }
+    pp_status s = check_device_keys(keys, n);
+    if (s != PP_OK) return s;
+    g_last_ctl = nullptr;
+    if (n == 0) {
+        g_stats = LastStats();
+        *split_out = 0;
+        return PP_OK;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    uint64_t* pw = pinned_word();
+    uint64_t* dk = static_cast<uint64_t*>(host_split_slot());
+    if (!pw || !dk) {
+        set_error("split buffers unavailable");
+        return PP_E_NOMEM;
+    }
+    {
+        WsOrder ws_order(st);
+        s = partition_stable_inplace_device<K>(keys, n, pivot, st, dk);
+    }
+    if (s != PP_OK) return s;
+    cudaError_t e = cudaMemcpyAsync(pw, dk, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "stable in-place partition");
+    *split_out = *pw;
+    return PP_OK;
+}
+
 template <typename K>
 static pp_status quicksort_sync(K* keys, uint64_t n, void* stream) {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -551,6 +586,14 @@ pp_status pp_partition_stable_u64(const uint64_t* in, uint64_t* out, uint64_t n,
 pp_status pp_partition_stable_u32(const uint32_t* in, uint32_t* out, uint64_t n, uint32_t pivot, void* stream,
                                   uint64_t* split_out) {
     return partition_stable<uint32_t>(in, out, n, pivot, stream, split_out, nullptr);
+}
+pp_status pp_partition_stable_inplace_u64(uint64_t* keys, uint64_t n, uint64_t pivot, void* stream,
+                                          uint64_t* split_out) {
+    return partition_stable_inplace<uint64_t>(keys, n, pivot, stream, split_out);
+}
+pp_status pp_partition_stable_inplace_u32(uint32_t* keys, uint64_t n, uint32_t pivot, void* stream,
+                                          uint64_t* split_out) {
+    return partition_stable_inplace<uint32_t>(keys, n, pivot, stream, split_out);
 }
 pp_status pp_partition_bps_u64(uint64_t* keys, uint64_t n, uint64_t pivot, void* stream, uint64_t* split_out) {
     return partition_bps<uint64_t>(keys, n, pivot, stream, split_out, nullptr);

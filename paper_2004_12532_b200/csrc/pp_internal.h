@@ -107,6 +107,10 @@ template <typename K>
 pp_status partition_stable_device(const K* in, K* out, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split,
                                   uint64_t** total_out);
 
+// the in-place stable variant (pp_stable.cu): O(n log n) work, split to a device word
+template <typename K>
+pp_status partition_stable_inplace_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split);
+
 // multi-GPU (pp_dist.cu)
 pp_status dist_unique_id(void* out128);
 pp_status dist_init(const void* id128, int nranks, int rank, int device);

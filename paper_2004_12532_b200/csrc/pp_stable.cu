@@ -15,6 +15,24 @@
 //                     destinations above -- every output written once.
 // No atomics; the output is unique (stability), so it is compared byte for
 // byte with the oracle's Standard Algorithm.
+//
+// The in-place STABLE variant (SURVEY §8(f) #4 "stable in-place variants";
+// of the algorithms there only the out-of-place Standard
+// Algorithm is stable): O(n log n) work, O(n / 4096) aux words.
+//   sti_leaf_kernel      every tile of ST_TILE keys stable-partitioned in
+//                        place (the tile is held in registers, then the
+//                        Standard Algorithm's placement inside the tile);
+//   merge levels         adjacent stable-partitioned segments [P1 S1][P2 S2]
+//                        become [P1 P2 S1 S2] by rotating the middle
+//                        [S1 P2] with three in-place reversals (reverse S1
+//                        and P2: sti_reverse2_kernel; reverse the whole
+//                        middle: sti_reverse_mid_kernel), one swap per
+//                        thread; segment sizes double each level.
+// Relative order is kept by every step, so the result is the Standard
+// Algorithm's output, byte for byte.  The price of stability in place: about
+// 2 passes over the array per level, log2(n / 4096) levels.
+#include <algorithm>
+
 #include "pp_engine.cuh"
 
 namespace pp {
@@ -115,6 +133,146 @@ __global__ void __launch_bounds__(ST_NT) st_scatter_kernel(const K* __restrict__
         before += rowtot;
     }
 }
+
+// ---- in-place stable variant ----
+template <typename K>
+__global__ void __launch_bounds__(ST_NT) sti_leaf_kernel(K* __restrict__ keys, uint64_t n, K pivot,
+                                                         uint64_t* __restrict__ cnt) {
+    constexpr int NW = ST_NT / 32;
+    __shared__ uint32_t wc[ST_EPT][NW];
+    const uint64_t t = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t lt = lanemask_lt();
+    K x[ST_EPT];
+    uint32_t ball[ST_EPT];
+#pragma unroll
+    for (int k = 0; k < ST_EPT; ++k) {
+        const uint64_t p = st_pos(t, k, tid);
+        x[k] = p < n ? keys[p] : (K)0;
+    }
+#pragma unroll
+    for (int k = 0; k < ST_EPT; ++k) {
+        ball[k] = __ballot_sync(0xffffffffu, st_pos(t, k, tid) < n && is_pred(x[k], pivot));
+        if (lane == 0) wc[k][warp] = __popc(ball[k]);
+    }
+    __syncthreads();  // every key of the tile is in registers: the tile may be overwritten
+    uint32_t tt = 0;  // predecessors in the tile
+#pragma unroll
+    for (int k = 0; k < ST_EPT; ++k)
+#pragma unroll
+        for (int w = 0; w < NW; ++w) tt += wc[k][w];
+    const uint64_t base = t * ST_TILE;
+    uint32_t before = 0;
+#pragma unroll
+    for (int k = 0; k < ST_EPT; ++k) {
+        uint32_t wpre = 0, rowtot = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const uint32_t c = wc[k][w];
+            wpre += (w < warp) ? c : 0u;
+            rowtot += c;
+        }
+        const uint64_t p = st_pos(t, k, tid);
+        if (p < n) {
+            const uint32_t rt = before + wpre + __popc(ball[k] & lt);
+            const uint32_t off = (uint32_t)k * ST_NT + tid;
+            keys[base + (((ball[k] >> lane) & 1u) ? rt : tt + (off - rt))] = x[k];
+        }
+        before += rowtot;
+    }
+    if (tid == 0) cnt[t] = tt;
+}
+
+// Pair i of level with segment size seg: left [2i seg, +len1), right after it
+// (+len2); t1, t2 their predecessor counts.  x = pair-local thread index.
+template <typename K>
+__global__ void __launch_bounds__(256) sti_reverse2_kernel(K* __restrict__ keys, uint64_t n, uint64_t seg,
+                                                           uint64_t npairs, const uint64_t* __restrict__ cnt) {
+    const uint64_t total = npairs * seg;
+    for (uint64_t g = (uint64_t)blockIdx.x * 256 + threadIdx.x; g < total; g += (uint64_t)gridDim.x * 256) {
+        const uint64_t i = g / seg, x = g - i * seg;
+        const uint64_t s0 = 2 * i * seg, len1 = seg, len2 = min(seg, n - s0 - len1);
+        const uint64_t t1 = cnt[2 * i], t2 = cnt[2 * i + 1];
+        const uint64_t a = len1 - t1;  // |S1|
+        if (x < a / 2) {               // reverse S1 = [s0 + t1, s0 + len1)
+            K* p = keys + s0 + t1 + x;
+            K* q = keys + s0 + len1 - 1 - x;
+            const K u = *p, v = *q;
+            *p = v;
+            *q = u;
+        }
+        if (x < t2 / 2) {  // reverse P2 = [s0 + len1, s0 + len1 + t2)
+            K* p = keys + s0 + len1 + x;
+            K* q = keys + s0 + len1 + t2 - 1 - x;
+            const K u = *p, v = *q;
+            *p = v;
+            *q = u;
+        }
+        (void)len2;
+    }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) sti_reverse_mid_kernel(K* __restrict__ keys, uint64_t seg, uint64_t npairs,
+                                                              const uint64_t* __restrict__ cnt,
+                                                              uint64_t* __restrict__ cnt_next) {
+    const uint64_t total = npairs * seg;
+    for (uint64_t g = (uint64_t)blockIdx.x * 256 + threadIdx.x; g < total; g += (uint64_t)gridDim.x * 256) {
+        const uint64_t i = g / seg, x = g - i * seg;
+        const uint64_t s0 = 2 * i * seg, len1 = seg;
+        const uint64_t t1 = cnt[2 * i], t2 = cnt[2 * i + 1];
+        const uint64_t m = len1 - t1 + t2;  // the middle [S1 P2] (both reversed): reverse it whole
+        if (x < m / 2) {
+            K* p = keys + s0 + t1 + x;
+            K* q = keys + s0 + t1 + m - 1 - x;
+            const K u = *p, v = *q;
+            *p = v;
+            *q = u;
+        }
+        if (x == 0) cnt_next[i] = t1 + t2;
+    }
+}
+
+// the unpaired last segment of a level keeps its count
+__global__ void sti_carry_kernel(const uint64_t* __restrict__ cnt, uint64_t* __restrict__ cnt_next, uint64_t nseg) {
+    if (threadIdx.x == 0 && (nseg & 1)) cnt_next[nseg / 2] = cnt[nseg - 1];
+}
+
+template <typename K>
+pp_status partition_stable_inplace_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split) {
+    const uint64_t ntiles = (n + ST_TILE - 1) / ST_TILE;
+    const size_t cB = (8 * (ntiles + 1) + 255) & ~size_t(255);
+    unsigned char* ws = static_cast<unsigned char*>(workspace(2 * cB, st));
+    if (!ws) return PP_E_NOMEM;
+    uint64_t* ca = reinterpret_cast<uint64_t*>(ws);
+    uint64_t* cb = reinterpret_cast<uint64_t*>(ws + cB);
+    LastStats& S = last_stats();
+    S = LastStats();
+    S.n = n;
+    S.aux_bytes = 2 * cB;
+    S.path = 6;
+    sti_leaf_kernel<K><<<(unsigned)ntiles, ST_NT, 0, st>>>(keys, n, pivot, ca);
+    uint64_t launches = 1;
+    uint64_t nseg = ntiles, seg = ST_TILE;
+    const unsigned grid_cap = (unsigned)sm_count() * 16;
+    while (nseg > 1) {
+        const uint64_t npairs = nseg / 2;
+        const unsigned grid = (unsigned)std::min<uint64_t>((npairs * seg + 255) / 256, grid_cap);
+        sti_reverse2_kernel<K><<<grid, 256, 0, st>>>(keys, n, seg, npairs, ca);
+        sti_reverse_mid_kernel<K><<<grid, 256, 0, st>>>(keys, seg, npairs, ca, cb);
+        sti_carry_kernel<<<1, 32, 0, st>>>(ca, cb, nseg);
+        launches += 3;
+        std::swap(ca, cb);
+        nseg = (nseg + 1) / 2;
+        seg *= 2;
+    }
+    note_launches(launches + 1);
+    cudaError_t e = cudaMemcpyAsync(d_split, ca, 8, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e == cudaSuccess ? PP_OK : cuda_fail(e, "stable in-place partition launch");
+}
+template pp_status partition_stable_inplace_device<uint64_t>(uint64_t*, uint64_t, uint64_t, cudaStream_t, uint64_t*);
+template pp_status partition_stable_inplace_device<uint32_t>(uint32_t*, uint64_t, uint32_t, cudaStream_t, uint64_t*);
 
 template <typename K>
 pp_status partition_stable_device(const K* in, K* out, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split,

@@ -137,6 +137,10 @@ def test_bps_stable_dist_guards(pp):
     ref = a.copy()
     assert oracle.partition_standard(ref, 1 << 63) == K and np.array_equal(out, ref)
     buf, view = _guarded(a)
+    K = pp.pp_partition_stable_inplace(view, 1 << 63)
+    ok, out = _guards_ok(buf, a.size, np.uint64)
+    assert ok and K == oracle.partition_standard(ref.copy(), 1 << 63) and np.array_equal(out, ref)
+    buf, view = _guarded(a)
     ns = [100_000, 0, 150_000, 50_007]
     pp.pp_dist_set_staging(1 << 14)
     try:
