@@ -52,9 +52,18 @@ struct GroupCfgT {
 #ifndef PP_U32_PF
 #define PP_U32_PF 4
 #endif
+#ifndef PP_U64_LINE
+#define PP_U64_LINE 8192
+#endif
+#ifndef PP_U64_NT
+#define PP_U64_NT 128
+#endif
+#ifndef PP_U64_PF
+#define PP_U64_PF 4
+#endif
 template <typename K>
-using GroupCfg = GroupCfgT<K, sizeof(K) == 8 ? 8192 : PP_U32_LINE, sizeof(K) == 8 ? 128 : PP_U32_NT,
-                           sizeof(K) == 8 ? 4 : PP_U32_PF, false, false, sizeof(K) == 4>;
+using GroupCfg = GroupCfgT<K, sizeof(K) == 8 ? PP_U64_LINE : PP_U32_LINE, sizeof(K) == 8 ? PP_U64_NT : PP_U32_NT,
+                           sizeof(K) == 8 ? PP_U64_PF : PP_U32_PF, false, false, sizeof(K) == 4>;
 
 // Line index of the j-th line (group order) of group gi: G_i(j) of
 // PAPER.md:963-969 in 0-based form, j*g + ((X[j] + i) mod g).
