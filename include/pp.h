@@ -164,8 +164,10 @@ pp_status pp_quicksort(uint64_t *keys, uint64_t n);
  *   is partitioned; *global_split_out = K = #keys < pivot over all ranks
  *   (HOST pointer).  The local step is pp_partition_*; then ncclAllGather of
  *   (status, n_r, t_r, pivot), a plan computed identically on every rank, and
- *   ncclSend/ncclRecv rounds through a staging buffer of <= the staging size
- *   (default 256 MiB, pp_dist_set_staging).  Mismatched pivots or key types
+ *   ncclSend/ncclRecv rounds through two staging halves of <= the staging size
+ *   each (default 256 MiB, pp_dist_set_staging): a round's copies from
+ *   staging into place run on a side stream while the next round transfers
+ *   into the other half.  Mismatched pivots or key types
  *   across ranks -> PP_E_INVAL on every rank.  Synchronises `stream`.
  *   Failure handling: every rank agrees on the status before returning (a
  *   local failure is reported by all ranks); the communicator is

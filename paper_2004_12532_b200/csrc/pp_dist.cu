@@ -500,20 +500,40 @@ struct DistCtx {
     uint64_t* d_swap = nullptr;  // one-sided swap piece table
     size_t d_swap_words = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, local done, gathered, exchanged
+    // staged exchange: the copies staging -> shard of round r run on pst while
+    // round r+1 transfers into the other staging half
+    cudaStream_t pst = nullptr;
+    cudaEvent_t ev_recv[2] = {nullptr, nullptr}, ev_place[2] = {nullptr, nullptr};
     double last_local_ms = 0, last_gather_ms = 0, last_exchange_ms = 0;
     uint64_t last_bytes = 0;
 
     pp_status init_events() {
         for (auto& e : ev)
             if (!e && cudaEventCreate(&e) != cudaSuccess) return cuda_fail(cudaGetLastError(), "event");
+        for (int h = 0; h < 2; ++h) {
+            if (!ev_recv[h] && cudaEventCreateWithFlags(&ev_recv[h], cudaEventDisableTiming) != cudaSuccess)
+                return cuda_fail(cudaGetLastError(), "event");
+            if (!ev_place[h] && cudaEventCreateWithFlags(&ev_place[h], cudaEventDisableTiming) != cudaSuccess)
+                return cuda_fail(cudaGetLastError(), "event");
+        }
+        if (!pst && cudaStreamCreateWithFlags(&pst, cudaStreamNonBlocking) != cudaSuccess)
+            return cuda_fail(cudaGetLastError(), "stream");
         return PP_OK;
     }
     void release() {
+        if (pst) cudaStreamSynchronize(pst);
         for (auto& e : ev)
             if (e) {
                 cudaEventDestroy(e);
                 e = nullptr;
             }
+        for (int h = 0; h < 2; ++h) {
+            if (ev_recv[h]) cudaEventDestroy(ev_recv[h]);
+            if (ev_place[h]) cudaEventDestroy(ev_place[h]);
+            ev_recv[h] = ev_place[h] = nullptr;
+        }
+        if (pst) cudaStreamDestroy(pst);
+        pst = nullptr;
         if (staging) cudaFree(staging);
         if (d_ag) cudaFree(d_ag);
         if (gs) cudaFree(gs);
@@ -773,8 +793,9 @@ static pp_status partition_multi(DistCtx& c, K* shard, const std::vector<SegPiec
     for (const SegPiece& p : mine) my_total += p.len;
     // staging: a rank moves <= min(cap, its misplaced keys) per round
     const uint64_t cap = std::max<uint64_t>(1, g_staging_cap_bytes / sizeof(K));
-    if (!params().dist_p2p && P > 1)
-        s = grow(&c.staging, &c.staging_bytes, sizeof(K) * std::max<uint64_t>(1, std::min(cap, my_total)));
+    // two staging halves of min(cap, my misplaced keys) each (double-buffered rounds)
+    const uint64_t half = std::max<uint64_t>(1, std::min(cap, my_total));
+    if (!params().dist_p2p && P > 1) s = grow(&c.staging, &c.staging_bytes, 2 * sizeof(K) * half);
     {  // record scratch: [P gathered records][my record]; without it this rank cannot take part
         const pp_status sa = ensure_ag(c, RW * (P + 1));
         if (sa != PP_OK) return sa;
@@ -891,13 +912,22 @@ static pp_status partition_multi(DistCtx& c, K* shard, const std::vector<SegPiec
         // no rank leaves (or reads its shard) before every peer's swaps finished
         if ((sl = agree(c, sl, st)) != PP_OK) return sl;
     } else if (P > 1) {
-        // 4b. staged rounds: send my range, receive the partner's into staging, place
+        // 4b. staged rounds: send my range, receive the partner's into a staging
+        //     half, place it (on the side stream pst, overlapping the next
+        //     round's transfer into the other half).  Round r+1's sends read
+        //     ranges disjoint from round r's place targets; a half is reused
+        //     only after its previous place copies (ev_place).
         std::vector<Piece> pcs;
         schedule_rounds(runs, P, cap, pcs);
-        K* staging = static_cast<K*>(c.staging);
         size_t i = 0;
+        uint64_t rno = 0;
+        bool placed[2] = {false, false};
         while (i < pcs.size()) {
             const uint64_t round = pcs[i].round;
+            const int hf = (int)(rno++ & 1);
+            K* staging = static_cast<K*>(c.staging) + (size_t)hf * half;
+            if (placed[hf] && cudaStreamWaitEvent(st, c.ev_place[hf], 0) != cudaSuccess)
+                return cuda_fail(cudaGetLastError(), "dist staging order");
             size_t j = i;
             while (j < pcs.size() && pcs[j].round == round) ++j;
             std::vector<uint64_t> offs, soffs, lens;
@@ -926,13 +956,21 @@ static pp_status partition_multi(DistCtx& c, K* shard, const std::vector<SegPiec
             const pp_status se = tp.group_end(st);
             if (sr == PP_OK) sr = se;
             if (sr != PP_OK) return sr;
-            for (size_t k = 0; k < offs.size(); ++k) {
-                e = cudaMemcpyAsync(shard + offs[k], staging + soffs[k], lens[k] * sizeof(K),
-                                    cudaMemcpyDeviceToDevice, st);
+            if (!offs.empty()) {
+                e = cudaEventRecord(c.ev_recv[hf], st);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(c.pst, c.ev_recv[hf], 0);
+                for (size_t k = 0; k < offs.size() && e == cudaSuccess; ++k)
+                    e = cudaMemcpyAsync(shard + offs[k], staging + soffs[k], lens[k] * sizeof(K),
+                                        cudaMemcpyDeviceToDevice, c.pst);
+                if (e == cudaSuccess) e = cudaEventRecord(c.ev_place[hf], c.pst);
                 if (e != cudaSuccess) return cuda_fail(e, "dist place");
+                placed[hf] = true;
             }
             i = j;
         }
+        for (int h = 0; h < 2; ++h)  // the exchange ends when every place copy has
+            if (placed[h] && cudaStreamWaitEvent(st, c.ev_place[h], 0) != cudaSuccess)
+                return cuda_fail(cudaGetLastError(), "dist place join");
     }
     if (timing) cudaEventRecord(c.ev[3], st);
     if ((s = tp.wait(st)) != PP_OK) return s;
