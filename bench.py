@@ -554,6 +554,25 @@ def extras(pp, torch, synth, dev, stream, flush, args):
         st = pp.pp_last_stats()
         res[f"c2_u64_2^27_mu{mu}"] = {"keys_per_s": n / (ms / 1e3), "ms": ms, "gbs": 16 * n / (ms / 1e3) / 1e9,
                                       "window_frac": st["W"] / n, "aux_frac": st["aux_bytes"] / (8 * n)}
+    # duplicate-heavy u64 keys (uniform, skewed and duplicate-heavy
+    # inputs): c2 size, keys uniform on [0, 1000), pivot 500 (mu = 0.5)
+    dup = synth.mod_range_u64_torch(n, synth.SEEDS["c2"], 1000, dev)
+    ts = []
+    for i in range(8):
+        buf.copy_(dup)
+        flush.sum()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        pp.pp_partition_async_u64(buf, 500, d)
+        e.record(stream)
+        torch.cuda.synchronize()
+        if i >= 3:
+            ts.append(s.elapsed_time(e))
+    ms = statistics.mean(ts)
+    st = pp.pp_last_stats()
+    res["c2_u64_2^27_dup1000_pivot500"] = {"keys_per_s": n / (ms / 1e3), "ms": ms, "gbs": 16 * n / (ms / 1e3) / 1e9,
+                                           "window_frac": st["W"] / n, "split": int(d.item())}
+    del dup
     # Strided (X = 0) vs Smoothed Striding
     # (random X) on the c2 input and on the stride-aligned
     # adversary (line j true iff j mod g < g/2, g = the library's group count)
