@@ -125,6 +125,8 @@ def load(build_if_missing: bool = True):
         "pp_quicksort_dist_loopback_u32": ([vp, P64, ctypes.c_int], st),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("PP_LIB_PATH") and not hasattr(L, name):
+            continue  # an older build loaded for an A/B comparison (tools/ only)
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res

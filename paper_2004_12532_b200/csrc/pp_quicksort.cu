@@ -1186,15 +1186,8 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     const uint64_t nh_max = HEAVY ? n / HEAVY + 1 : 1;
     const size_t pin_sB = al256(sizeof(QSeg) * nmid_max), pin_spB = al256(8 * (nmid_max + nbig_max + 1));
     const size_t pin_lane = pin_sB + pin_spB + al256(4 * nh_max);
-    // pinned mirror of the early batches' lists (indexed globally like the
-    // device lists: a batch's range is never rewritten while its copy runs)
-    const uint64_t es_max = n / (LEAF + 1) + 1;
-    const size_t epin_lo = al256(8 * es_max), epin_ln = al256(4 * es_max), epin_sb = al256(8 * (es_max + 1));
-    unsigned char* pin_all = qs_pinned(2 * pin_lane + epin_lo + epin_ln + epin_sb);
+    unsigned char* pin_all = qs_pinned(2 * pin_lane);
     if (!pin_all) return PP_E_NOMEM;
-    uint64_t* pin_eslo = reinterpret_cast<uint64_t*>(pin_all + 2 * pin_lane);
-    uint32_t* pin_esln = reinterpret_cast<uint32_t*>(pin_all + 2 * pin_lane + epin_lo);
-    uint64_t* pin_esbase = reinterpret_cast<uint64_t*>(pin_all + 2 * pin_lane + epin_lo + epin_ln);
     lanes[0].pin = pin_all;
     lanes[1].pin = pin_all + pin_lane;
     // bytes of each lane's device region: the level bound up front (a few MB
@@ -1233,15 +1226,11 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     auto small_batch = [&](uint64_t b, uint64_t en) -> pp_status {
         if (en <= b) return PP_OK;
         const uint64_t cnt = en - b;
-        // staged through the pinned mirror: a pageable copy could wait for the
-        // previous batch's kernels on early_st and stall the level loop
-        memcpy(pin_eslo + b, small_lo.data() + b, 8 * cnt);
-        memcpy(pin_esln + b, small_len.data() + b, 4 * cnt);
-        memcpy(pin_esbase + b, small_base_v.data() + b, 8 * cnt);
-        e = cudaMemcpyAsync(d_eslo + b, pin_eslo + b, 8 * cnt, cudaMemcpyHostToDevice, early_st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(d_esln + b, pin_esln + b, 4 * cnt, cudaMemcpyHostToDevice, early_st);
+        e = cudaMemcpyAsync(d_eslo + b, small_lo.data() + b, 8 * cnt, cudaMemcpyHostToDevice, early_st);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(d_esbase + b, pin_esbase + b, 8 * cnt, cudaMemcpyHostToDevice, early_st);
+            e = cudaMemcpyAsync(d_esln + b, small_len.data() + b, 4 * cnt, cudaMemcpyHostToDevice, early_st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(d_esbase + b, small_base_v.data() + b, 8 * cnt, cudaMemcpyHostToDevice, early_st);
         if (e == cudaSuccess)
             e = launch_small(cnt, d_eslo + b, d_esln + b, d_esbase + b, d_eblo, d_ebln, d_escr + b, nullptr, early_st);
         cudaEvent_t ev = early_ev[early_nb++ % 64];
