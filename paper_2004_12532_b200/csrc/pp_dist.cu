@@ -1075,7 +1075,9 @@ static pp_status quicksort_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, cuda
         std::vector<uint64_t> sval;
         if (!spos.empty()) {
             const size_t m = spos.size();
-            if ((s = grow(&c.gs, &c.gs_bytes, 8 * m * (P + 1))) != PP_OK) return agree(c, s, st);
+            // every rank takes part in the agreement (a failed allocation on one rank must not
+            // leave the others in a different collective)
+            if ((s = agree(c, grow(&c.gs, &c.gs_bytes, 8 * m * (P + 1)), st)) != PP_OK) return s;
             uint64_t* d_samp = static_cast<uint64_t*>(c.gs) + m * P;
             e = cudaMemsetAsync(d_samp, 0, 8 * m, st);
             for (size_t i = 0; i < m && e == cudaSuccess; ++i)
