@@ -24,11 +24,18 @@ def main():
     ap.add_argument("specs", nargs="+")
     ap.add_argument("--exp", type=int, default=33)
     ap.add_argument("--rounds", type=int, default=4)
+    ap.add_argument("--dtype", default="u64")
+    ap.add_argument("--n", type=int, default=0, help="key count (overrides --exp)")
     args = ap.parse_args()
     pp.load(build_if_missing=False)
-    n = 1 << args.exp
-    work = torch.empty(n, dtype=torch.int64, device="cuda")
-    synth.uniform_u64_torch(n, synth.SEEDS["c3"], "cuda", out=work, chunk=1 << 27)
+    n = args.n or (1 << args.exp)
+    if args.dtype == "u64":
+        work = torch.empty(n, dtype=torch.int64, device="cuda")
+        synth.uniform_u64_torch(n, synth.SEEDS["c3"], "cuda", out=work, chunk=1 << 27)
+        part, pivot, w = pp.pp_partition_async_u64, 1 << 63, 8
+    else:
+        work = synth.uniform_u32_torch(n, synth.SEEDS["c4"], "cuda")
+        part, pivot, w = pp.pp_partition_async_u32, 1 << 31, 4
     pristine = work.clone()
     d = torch.zeros(1, dtype=torch.int64, device="cuda")
     res = {sp: {"group": [], "total": [], "copy": []} for sp in args.specs}
@@ -44,7 +51,7 @@ def main():
             e.record()
             torch.cuda.synchronize()
             pp.pp_timing(True)
-            pp.pp_partition_async_u64(work, 1 << 63, d)
+            part(work, pivot, d)
             torch.cuda.synchronize()
             t = pp.pp_timing_read()
             pp.pp_timing(False)
@@ -55,10 +62,10 @@ def main():
     pp.reset_params()
     for sp, v in res.items():
         st = pp.pp_last_stats()
-        print(json.dumps({"spec": sp, "n": f"2^{args.exp}", "group_ms_med": statistics.median(v["group"]),
+        print(json.dumps({"spec": sp, "n": n, "dtype": args.dtype, "group_ms_med": statistics.median(v["group"]),
                           "total_ms_med": statistics.median(v["total"]), "total_ms_all": v["total"],
-                          "copy_gbs_med": 16 * n / (statistics.median(v["copy"]) / 1e3) / 1e9,
-                          "total_gbs_med": 16 * n / (statistics.median(v["total"]) / 1e3) / 1e9}), flush=True)
+                          "copy_gbs_med": 2 * w * n / (statistics.median(v["copy"]) / 1e3) / 1e9,
+                          "total_gbs_med": 2 * w * n / (statistics.median(v["total"]) / 1e3) / 1e9}), flush=True)
 
 
 if __name__ == "__main__":
