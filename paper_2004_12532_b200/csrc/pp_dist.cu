@@ -340,8 +340,10 @@ struct NcclTransport : Transport {
             g_nccl.CommGetAsyncError(comm, &a);
             if (a != ncclSuccess && a != ncclInProgress)
                 return fail(std::string("NCCL async error: ") + g_nccl.GetErrorString(a));
-            if (now_ms() - t0 > lim) return fail("dist wait timed out (dist_timeout_ms); communicator aborted");
-            std::this_thread::sleep_for(std::chrono::microseconds(20));
+            const double el = now_ms() - t0;
+            if (el > lim) return fail("dist wait timed out (dist_timeout_ms); communicator aborted");
+            if (el > 1.0) std::this_thread::sleep_for(std::chrono::microseconds(20));  // spin the first ms
+            else std::this_thread::yield();
         }
     }
     pp_status export_range(void* d, uint64_t* rec) override {
