@@ -657,37 +657,44 @@ def extras(pp, torch, synth, dev, stream, flush, args):
     del wb
     del pristine, buf, adv
     nq = 1 << 28
+    # BASELINE config 5 (median-of-3 pivots, the config's rule), and the same
+    # sorts with Tukey's ninther pivots (qs_deep = 0; same input, same output)
     for kind in ("uniform", "dup1000"):
         if kind == "uniform":
             q0 = synth.uniform_u64_torch(nq, synth.SEEDS["c5"], dev)
         else:
             q0 = synth.mod_range_u64_torch(nq, synth.SEEDS["c5"], 1000, dev)
         q = torch.empty_like(q0)
-        ts = []
-        for i in range(3):
-            q.copy_(q0)
-            flush.sum()
-            torch.cuda.synchronize()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(stream)
-            pp.pp_quicksort_u64(q)
-            e.record(stream)
-            torch.cuda.synchronize()
-            if i >= 1:
-                ts.append(s.elapsed_time(e))
-        ms = statistics.mean(ts)
-        qs = pp.pp_quicksort_last_stats()
-        # pass model: every level reads + writes the keys of the
-        # segments it partitions (level_keys), the per-CTA recursion makes at
-        # least one pass over the small segments, the bin sort one over all n
-        model = 16 * (qs["level_keys"] + qs["small_keys"] + nq)
-        peak, _ = peaks()
-        res[f"quicksort_{kind}_2^28"] = {
-            "keys_per_s": nq / (ms / 1e3), "ms": ms, "stats": qs,
-            "roofline": {"bound": "hbm", "model_bytes": model, "achieved": model / (ms / 1e3) / 1e9, "peak": peak,
-                         "unit": "GB/s", "frac": model / (ms / 1e3) / 1e9 / peak,
-                         "model": "2*w*(level_keys + small_keys + n): levels + one per-CTA recursion pass + one bin "
-                                  "pass (a lower bound on the bytes moved)"}}
+        for rule in ("median3", "ninther"):
+            pp.reset_params()
+            if rule == "ninther":
+                pp.pp_set_param("qs_deep", 0)
+            ts = []
+            for i in range(3):
+                q.copy_(q0)
+                flush.sum()
+                torch.cuda.synchronize()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                pp.pp_quicksort_u64(q)
+                e.record(stream)
+                torch.cuda.synchronize()
+                if i >= 1:
+                    ts.append(s.elapsed_time(e))
+            ms = statistics.mean(ts)
+            qs = pp.pp_quicksort_last_stats()
+            # pass model: every level reads + writes the keys of the
+            # segments it partitions (level_keys), the per-CTA recursion makes at
+            # least one pass over the small segments, the bin sort one over all n
+            model = 16 * (qs["level_keys"] + qs["small_keys"] + nq)
+            peak, _ = peaks()
+            res[f"quicksort_{kind}_2^28" + ("" if rule == "median3" else "_ninther")] = {
+                "keys_per_s": nq / (ms / 1e3), "ms": ms, "pivot": rule, "stats": qs,
+                "roofline": {"bound": "hbm", "model_bytes": model, "achieved": model / (ms / 1e3) / 1e9,
+                             "peak": peak, "unit": "GB/s", "frac": model / (ms / 1e3) / 1e9 / peak,
+                             "model": "2*w*(level_keys + small_keys + n): levels + one per-CTA recursion pass + "
+                                      "one bin pass (a lower bound on the bytes moved)"}}
+        pp.reset_params()
         del q0, q
 
     def timed(fn, reps=3):

@@ -37,7 +37,8 @@ struct QSeg {
     uint64_t pivot;    // effective strict pivot (key < pivot goes left)
     uint64_t gbase;    // first task (CTA) of this segment in the group launch
     uint64_t g;        // groups of this segment
-    uint32_t mode;     // 0: pivot = median-of-3 (computed on device); 1: pivot given
+    uint32_t mode;     // 0: pivot = median-of-3 (computed on device); 1: pivot given (x <= p step);
+                       // 2: pivot = ninther (computed on device; segments deeper than QS_DEEP)
     uint32_t pad;
 };
 
@@ -48,13 +49,27 @@ __device__ __forceinline__ K median3(K a, K b, K c) {
     return a > b ? a : b;
 }
 
+// Tukey's ninther: the median of the medians of three triples at the nine
+// positions lo + j (len - 1) / 8, j = 0..8 (deep segments, see QS_DEEP)
+template <typename K>
+__host__ __device__ __forceinline__ uint64_t ninther_pos(uint64_t lo, uint64_t len, int j) {
+    return lo + (len - 1) / 8 * (uint64_t)j + ((len - 1) % 8) * (uint64_t)j / 8;
+}
+
 template <typename K>
 __global__ void qs_pivot_kernel(const K* __restrict__ keys, QSeg* __restrict__ segs, uint64_t nseg) {
     for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += (uint64_t)gridDim.x * blockDim.x) {
         QSeg q = segs[s];
+        const uint64_t len = q.hi - q.lo;
         if (q.mode == 0) {
-            const uint64_t len = q.hi - q.lo;
             segs[s].pivot = (uint64_t)median3<K>(keys[q.lo], keys[q.lo + (len - 1) / 2], keys[q.hi - 1]);
+        } else if (q.mode == 2) {
+            K m[3];
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+                m[t] = median3<K>(keys[ninther_pos<K>(q.lo, len, 3 * t)], keys[ninther_pos<K>(q.lo, len, 3 * t + 1)],
+                                  keys[ninther_pos<K>(q.lo, len, 3 * t + 2)]);
+            segs[s].pivot = (uint64_t)median3<K>(m[0], m[1], m[2]);
         }
     }
 }
@@ -789,7 +804,7 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
     qs_small_kernel(K* __restrict__ keys, const uint64_t* __restrict__ seg_lo, const uint32_t* __restrict__ seg_len,
                     const uint64_t* __restrict__ slot_base, uint64_t* __restrict__ bin_lo,
                     uint32_t* __restrict__ bin_len, uint32_t leaf, uint64_t seed, GroupOut* __restrict__ scratch,
-                    uint64_t* __restrict__ prof) {
+                    uint64_t* __restrict__ prof, int ninther) {
     using S = SmallCfg<K>;
     constexpr int DEPTH = 64, LEFT_FIRST_MAX = 40;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -864,7 +879,19 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
             continue;
         }
         K p;
-        if ((mode & QM_LE) == 0) p = median3<K>(keys[lo], keys[lo + (len - 1) / 2], keys[hi - 1]);
+        if ((mode & QM_LE) == 0) {
+            if (ninther) {  // Tukey's ninther (param qs_deep = 0)
+                const K m0 = median3<K>(keys[ninther_pos<K>(lo, len, 0)], keys[ninther_pos<K>(lo, len, 1)],
+                                        keys[ninther_pos<K>(lo, len, 2)]);
+                const K m1 = median3<K>(keys[ninther_pos<K>(lo, len, 3)], keys[ninther_pos<K>(lo, len, 4)],
+                                        keys[ninther_pos<K>(lo, len, 5)]);
+                const K m2 = median3<K>(keys[ninther_pos<K>(lo, len, 6)], keys[ninther_pos<K>(lo, len, 7)],
+                                        keys[ninther_pos<K>(lo, len, 8)]);
+                p = median3<K>(m0, m1, m2);
+            } else {
+                p = median3<K>(keys[lo], keys[lo + (len - 1) / 2], keys[hi - 1]);
+            }
+        }
         else p = (K)pm;
         if (prof) { const uint64_t t1 = clock64(); pr[0] += t1 - t0; t0 = t1; }
         const uint64_t k = cta_partition<K>(keys + lo, len, p, seed, smem, scratch + blockIdx.x, &sc, red,
@@ -1075,14 +1102,21 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
 
     struct HSeg {
         uint64_t lo, hi, pivot;
-        uint32_t mode;
+        uint32_t mode, depth;
     };
+    // Deep segments (an adversarial order can make median-of-3 peel off a few
+    // keys per level) take the ninther instead (R14 fixes only the default
+    // rule; the sorted output is unique, so parity is unaffected).  Uniform
+    // and structured inputs never get this deep.
+    uint32_t lg = 0;
+    while ((1ull << lg) < n) ++lg;
+    const uint32_t QS_DEEP = P.qs_deep >= 0 ? (uint32_t)P.qs_deep : 2 * lg + 16;
     std::vector<uint64_t> leaf_lo, small_lo;
     std::vector<uint32_t> leaf_len, small_len;
     std::vector<uint64_t> small_base_v{0};  // bin-slot offset of each small segment (prefix of qs_bin_cap)
     // segments in (LEAF, SMALL] finish in one CTA each (qs_small_kernel)
     const uint64_t SMALL = geom.SMALL;
-    auto add_child = [&](std::vector<HSeg>& next, uint64_t lo, uint64_t hi) {
+    auto add_child = [&](std::vector<HSeg>& next, uint64_t lo, uint64_t hi, uint32_t depth) {
         const uint64_t len = hi - lo;
         if (len <= 1) return;
         if (len <= LEAF) {
@@ -1096,7 +1130,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             small_len.push_back((uint32_t)len);
             small_base_v.push_back(small_base_v.back() + qs_bin_cap(len, LEAF));
         } else {
-            next.push_back({lo, hi, 0, 0});
+            next.push_back({lo, hi, 0, depth > QS_DEEP ? 2u : 0u, depth});
         }
     };
     // The level loop runs in up to two LANES: while some segment takes the
@@ -1132,10 +1166,10 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     lanes[1].st = lane_st1;
     lanes[1].done = lane_ev[1];
     lanes[1].id = 1;
-    lanes[0].cur.push_back({0, n, 0, 0});
+    lanes[0].cur.push_back({0, n, 0, QS_DEEP == 0 ? 2u : 0u, 0});
     if (n <= SMALL) {
         lanes[0].cur.clear();
-        add_child(lanes[0].cur, 0, n);
+        add_child(lanes[0].cur, 0, n, 0);
     }
     cudaError_t e;
     cudaFuncSetAttribute(qs_group_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -1176,7 +1210,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         using S = SmallCfg<K>;
         cudaFuncSetAttribute(qs_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
         qs_small_kernel<K><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln, (uint32_t)LEAF,
-                                                                  P.seed, scr, prof);
+                                                                  P.seed, scr, prof, P.qs_deep == 0 ? 1 : 0);
         note_launches(1);
         return cudaGetLastError();
     };
@@ -1390,21 +1424,30 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         for (size_t bi = 0; bi < nbig; ++bi) {
             HSeg& sg = L.cur[L.big_idx[bi]];
             uint64_t p = sg.pivot;
-            if (sg.mode == 0) {
-                K three[3];
+            if (sg.mode != 1) {  // median-of-3 (mode 0) or the ninther (mode 2) of host-read samples
                 const uint64_t len = sg.hi - sg.lo;
-                e = cudaMemcpyAsync(&three[0], keys + sg.lo, sizeof(K), cudaMemcpyDeviceToHost, lst);
-                if (e == cudaSuccess)
-                    e = cudaMemcpyAsync(&three[1], keys + sg.lo + (len - 1) / 2, sizeof(K), cudaMemcpyDeviceToHost,
-                                        lst);
-                if (e == cudaSuccess)
-                    e = cudaMemcpyAsync(&three[2], keys + sg.hi - 1, sizeof(K), cudaMemcpyDeviceToHost, lst);
+                const int ns = sg.mode == 2 ? 9 : 3;
+                uint64_t pos[9];
+                if (ns == 3) {
+                    pos[0] = sg.lo;
+                    pos[1] = sg.lo + (len - 1) / 2;
+                    pos[2] = sg.hi - 1;
+                } else {
+                    for (int j = 0; j < 9; ++j) pos[j] = ninther_pos<K>(sg.lo, len, j);
+                }
+                K v[9];
+                e = cudaSuccess;
+                for (int j = 0; j < ns && e == cudaSuccess; ++j)
+                    e = cudaMemcpyAsync(&v[j], keys + pos[j], sizeof(K), cudaMemcpyDeviceToHost, lst);
                 if (e == cudaSuccess) e = cudaStreamSynchronize(lst);
                 if (e != cudaSuccess) return cuda_fail(e, "quicksort pivot");
-                K a = three[0], b = three[1], c = three[2];
-                if (a > b) std::swap(a, b);
-                if (b > c) b = c;
-                p = (uint64_t)(a > b ? a : b);
+                auto med3 = [](K a, K b, K c) {
+                    if (a > b) std::swap(a, b);
+                    if (b > c) b = c;
+                    return a > b ? a : b;
+                };
+                p = (uint64_t)(ns == 3 ? med3(v[0], v[1], v[2])
+                                       : med3(med3(v[0], v[1], v[2]), med3(v[3], v[4], v[5]), med3(v[6], v[7], v[8])));
             }
             L.pivots_h[L.big_idx[bi]] = p;
             pp_status ps = partition_device<K>(keys + sg.lo, sg.hi - sg.lo, (K)p, lst, d_splits + nmid + bi, nullptr);
@@ -1501,16 +1544,17 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         // ---- next level ----
         L.next.clear();
         auto visit = [&](const HSeg& sg, uint64_t p, uint64_t k) {
-            if (sg.mode == 0) {
+            const uint32_t d = sg.depth + 1;
+            if (sg.mode != 1) {
                 if (k == 0) {
                     // p is the segment minimum; split by x <= p next (unless all == MAX)
-                    if ((K)p != KMAX) L.next.push_back({sg.lo, sg.hi, (uint64_t)(K)(p + 1), 1});
+                    if ((K)p != KMAX) L.next.push_back({sg.lo, sg.hi, (uint64_t)(K)(p + 1), 1, d});
                 } else {
-                    add_child(L.next, sg.lo, sg.lo + k);
-                    add_child(L.next, sg.lo + k, sg.hi);
+                    add_child(L.next, sg.lo, sg.lo + k, d);
+                    add_child(L.next, sg.lo + k, sg.hi, d);
                 }
             } else {
-                add_child(L.next, sg.lo + k, sg.hi);  // [lo, lo+k) is all equal: final
+                add_child(L.next, sg.lo + k, sg.hi, d);  // [lo, lo+k) is all equal: final
             }
         };
         for (size_t mi = 0; mi < nmid; ++mi) visit(L.cur[L.mid_idx[mi]], L.pivots_h[L.mid_idx[mi]], L.splits_h[mi]);

@@ -81,7 +81,8 @@ def test_medium_sizes(pp, dt, mx):
                                     {"qs_waves": 1}, {"qs_waves": 16, "leaf": 1000},
                                     {"qs_heavy": 1 << 17}, {"qs_heavy": 0}, {"qs_small": 0}, {"strided": 1},
                                     {"qs_lanes": 1}, {"qs_lanes": 2}, {"qs_lanes": 2, "qs_small": 1 << 17},
-                                    {"qs_early": 1}, {"qs_early": 1, "qs_lanes": 1}, {"qs_early": 0}])
+                                    {"qs_early": 1}, {"qs_early": 1, "qs_lanes": 1}, {"qs_early": 0},
+                                    {"qs_deep": 0}, {"qs_deep": 3}, {"qs_deep": 0, "qs_cta_max": 1 << 12}])
 def test_qs_parameters(pp, dt, mx, params):
     """Bin sizes (both bin-sort CTA shapes), level balancing, the
     heavy-segment batched cleanup, the per-CTA recursion and the Strided
@@ -186,3 +187,27 @@ def test_quicksort_last_stats(pp):
     pp.pp_quicksort(t)
     st = pp.pp_quicksort_last_stats()
     assert st["n"] == 1000 and st["levels"] == 0 and st["leaf_keys"] == 1000
+
+
+def test_deep_segments_take_the_ninther(pp):
+    """Segments deeper than qs_deep switch from the median of 3 to Tukey's
+    ninther (the guard against inputs that make the median of 3 peel off a
+    few keys per level): with qs_deep = 0 every level segment (device-side
+    pivots) and every big segment (host-read pivots, qs_cta_max small) uses
+    it; the result is still the oracle's sort, in a similar number of levels."""
+    from gpu_util import to_dev, to_host
+    for a in (synth.uniform_u64_np(3_000_017, 7), synth.mod_range_u64_np(2_000_003, 8, 1000),
+              np.concatenate([np.arange(1 << 20, dtype=np.uint64), np.arange(1 << 20, dtype=np.uint64)[::-1]])):
+        ref = _oracle_sorted(a)
+        levels = []
+        for params in ({}, {"qs_deep": 0}, {"qs_deep": 0, "qs_cta_max": 1 << 16}):
+            for k, v in params.items():
+                pp.pp_set_param(k, v)
+            try:
+                t = to_dev(a)
+                pp.pp_quicksort(t)
+                levels.append(pp.pp_quicksort_last_stats()["levels"])
+            finally:
+                pp.reset_params()
+            assert np.array_equal(to_host(t, np.uint64), ref), params
+        assert max(levels) <= 2 * min(levels) + 4, levels
