@@ -658,17 +658,18 @@ def extras(pp, torch, synth, dev, stream, flush, args):
     del pristine, buf, adv
     nq = 1 << 28
     # BASELINE config 5 (median-of-3 pivots, the config's rule), and the same
-    # sorts with Tukey's ninther pivots (qs_deep = 0; same input, same output)
+    # sorts with the median of 31 sampled keys as pivot (qs_pivot = 2; same
+    # input, same output)
     for kind in ("uniform", "dup1000"):
         if kind == "uniform":
             q0 = synth.uniform_u64_torch(nq, synth.SEEDS["c5"], dev)
         else:
             q0 = synth.mod_range_u64_torch(nq, synth.SEEDS["c5"], 1000, dev)
         q = torch.empty_like(q0)
-        for rule in ("median3", "ninther"):
+        for rule in ("median3", "median31"):
             pp.reset_params()
-            if rule == "ninther":
-                pp.pp_set_param("qs_deep", 0)
+            if rule == "median31":
+                pp.pp_set_param("qs_pivot", 2)
             ts = []
             for i in range(3):
                 q.copy_(q0)
@@ -688,7 +689,7 @@ def extras(pp, torch, synth, dev, stream, flush, args):
             # least one pass over the small segments, the bin sort one over all n
             model = 16 * (qs["level_keys"] + qs["small_keys"] + nq)
             peak, _ = peaks()
-            res[f"quicksort_{kind}_2^28" + ("" if rule == "median3" else "_ninther")] = {
+            res[f"quicksort_{kind}_2^28" + ("" if rule == "median3" else "_median31")] = {
                 "keys_per_s": nq / (ms / 1e3), "ms": ms, "pivot": rule, "stats": qs,
                 "roofline": {"bound": "hbm", "model_bytes": model, "achieved": model / (ms / 1e3) / 1e9,
                              "peak": peak, "unit": "GB/s", "frac": model / (ms / 1e3) / 1e9 / peak,

@@ -836,6 +836,7 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "dist_small") P.dist_small = value < 1 ? 1 : value;
     else if (k == "qs_lanes") P.qs_lanes = value;
     else if (k == "qs_deep") P.qs_deep = value;
+    else if (k == "qs_pivot") P.qs_pivot = value < 0 || value > 2 ? 0 : value;
     else if (k == "qs_early") P.qs_early = value;
     else if (k == "qs_early_min") P.qs_early_min = value;
     else if (k == "qs_minl") P.qs_minl = value;
@@ -874,6 +875,7 @@ int64_t pp_get_param(const char* name) {
     if (k == "dist_small") return P.dist_small;
     if (k == "qs_lanes") return P.qs_lanes;
     if (k == "qs_deep") return P.qs_deep;
+    if (k == "qs_pivot") return P.qs_pivot;
     if (k == "qs_early") return P.qs_early;
     if (k == "qs_early_min") return P.qs_early_min;
     if (k == "qs_minl") return P.qs_minl;

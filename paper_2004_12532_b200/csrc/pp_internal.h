@@ -64,6 +64,8 @@ struct Params {
     int64_t dist_fault_rank = -1;
     int64_t dist_small = 1 << 16;  // distributed quicksort: spanning segments <= this are gathered and sorted locally
     int64_t host_chunk = 1 << 23;  // host-buffer partition: keys per streamed chunk (measured best at 1-8 GiB)
+    int64_t qs_pivot = 0;          // quicksort level-loop pivot: 0 median of 3 (BJ config 5), 1 Tukey's ninther,
+                                   // 2 median of 31 samples (the per-CTA recursion takes the ninther for 1, 2)
     int64_t qs_deep = -1;          // quicksort levels: segments deeper than this use the ninther pivot (-1 auto:
                                    // 2 log2(n) + 16; 0: always)
     int64_t qs_heavy = 1 << 22;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)

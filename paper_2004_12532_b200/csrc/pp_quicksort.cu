@@ -38,7 +38,8 @@ struct QSeg {
     uint64_t gbase;    // first task (CTA) of this segment in the group launch
     uint64_t g;        // groups of this segment
     uint32_t mode;     // 0: pivot = median-of-3 (computed on device); 1: pivot given (x <= p step);
-                       // 2: pivot = ninther (computed on device; segments deeper than QS_DEEP)
+                       // 2: pivot = ninther; 3: median of 31 samples (computed on device; param
+                       // qs_pivot, and segments deeper than QS_DEEP take at least the ninther)
     uint32_t pad;
 };
 
@@ -56,14 +57,38 @@ __host__ __device__ __forceinline__ uint64_t ninther_pos(uint64_t lo, uint64_t l
     return lo + (len - 1) / 8 * (uint64_t)j + ((len - 1) % 8) * (uint64_t)j / 8;
 }
 
+// One warp per segment: mode 0 median of 3, 2 ninther, 3 the median of 31
+// evenly spaced samples (warp bitonic sort of 31 samples + one +inf pad).
+// the median of 31 evenly spaced keys (sample j at lo + j (len - 1) / 30)
 template <typename K>
-__global__ void qs_pivot_kernel(const K* __restrict__ keys, QSeg* __restrict__ segs, uint64_t nseg) {
-    for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += (uint64_t)gridDim.x * blockDim.x) {
-        QSeg q = segs[s];
+__device__ __forceinline__ K warp_median31(const K* keys, uint64_t lo, uint64_t len, int lane) {
+    const K KMAX = (K)~(K)0;
+    K v = lane < 31 ? keys[lo + (len - 1) / 30 * (uint64_t)lane + ((len - 1) % 30) * (uint64_t)lane / 30] : KMAX;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const K o = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool up = ((lane & k) == 0), lower = ((lane & j) == 0);
+            v = (lower == up) ? (v < o ? v : o) : (v < o ? o : v);
+        }
+    return __shfl_sync(0xffffffffu, v, 15);  // the 16th smallest of the 31 samples
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) qs_pivot_kernel(const K* __restrict__ keys, QSeg* __restrict__ segs,
+                                                       uint64_t nseg) {
+    const int lane = threadIdx.x & 31;
+    for (uint64_t s = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nseg;
+         s += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const QSeg q = segs[s];  // uniform over the warp
         const uint64_t len = q.hi - q.lo;
-        if (q.mode == 0) {
+        if (q.mode == 3) {
+            const K p = warp_median31<K>(keys, q.lo, len, lane);
+            if (lane == 0) segs[s].pivot = (uint64_t)p;
+        } else if (lane == 0 && q.mode == 0) {
             segs[s].pivot = (uint64_t)median3<K>(keys[q.lo], keys[q.lo + (len - 1) / 2], keys[q.hi - 1]);
-        } else if (q.mode == 2) {
+        } else if (lane == 0 && q.mode == 2) {
             K m[3];
 #pragma unroll
             for (int t = 0; t < 3; ++t)
@@ -879,8 +904,17 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
             continue;
         }
         K p;
-        if ((mode & QM_LE) == 0) {
-            if (ninther) {  // Tukey's ninther (param qs_deep = 0)
+        if ((mode & QM_LE) == 0 && ninther == 2) {  // median of 31 samples (param qs_pivot = 2): warp 0
+            __shared__ K p31;
+            if (threadIdx.x < 32) {
+                const K v = warp_median31<K>(keys, lo, len, (int)threadIdx.x);
+                if (threadIdx.x == 0) p31 = v;
+            }
+            __syncthreads();
+            p = p31;
+            __syncthreads();  // p31 is rewritten by the next partition
+        } else if ((mode & QM_LE) == 0) {
+            if (ninther) {  // Tukey's ninther (param qs_deep = 0, qs_pivot = 1)
                 const K m0 = median3<K>(keys[ninther_pos<K>(lo, len, 0)], keys[ninther_pos<K>(lo, len, 1)],
                                         keys[ninther_pos<K>(lo, len, 2)]);
                 const K m1 = median3<K>(keys[ninther_pos<K>(lo, len, 3)], keys[ninther_pos<K>(lo, len, 4)],
@@ -1111,6 +1145,9 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     uint32_t lg = 0;
     while ((1ull << lg) < n) ++lg;
     const uint32_t QS_DEEP = P.qs_deep >= 0 ? (uint32_t)P.qs_deep : 2 * lg + 16;
+    // pivot rule of the level loop: param qs_pivot 0 median of 3 (BJ config 5), 1 ninther, 2 median of 31
+    const uint32_t RULE = P.qs_pivot == 2 ? 3u : P.qs_pivot == 1 ? 2u : 0u;
+    auto rule_at = [&](uint32_t depth) -> uint32_t { return depth > QS_DEEP && RULE == 0 ? 2u : RULE; };
     std::vector<uint64_t> leaf_lo, small_lo;
     std::vector<uint32_t> leaf_len, small_len;
     std::vector<uint64_t> small_base_v{0};  // bin-slot offset of each small segment (prefix of qs_bin_cap)
@@ -1130,7 +1167,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             small_len.push_back((uint32_t)len);
             small_base_v.push_back(small_base_v.back() + qs_bin_cap(len, LEAF));
         } else {
-            next.push_back({lo, hi, 0, depth > QS_DEEP ? 2u : 0u, depth});
+            next.push_back({lo, hi, 0, rule_at(depth), depth});
         }
     };
     // The level loop runs in up to two LANES: while some segment takes the
@@ -1166,7 +1203,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
     lanes[1].st = lane_st1;
     lanes[1].done = lane_ev[1];
     lanes[1].id = 1;
-    lanes[0].cur.push_back({0, n, 0, QS_DEEP == 0 ? 2u : 0u, 0});
+    lanes[0].cur.push_back({0, n, 0, rule_at(0), 0});
     if (n <= SMALL) {
         lanes[0].cur.clear();
         add_child(lanes[0].cur, 0, n, 0);
@@ -1210,7 +1247,8 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         using S = SmallCfg<K>;
         cudaFuncSetAttribute(qs_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
         qs_small_kernel<K><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln, (uint32_t)LEAF,
-                                                                  P.seed, scr, prof, P.qs_deep == 0 ? 1 : 0);
+                                                                  P.seed, scr, prof,
+                                                                  P.qs_pivot == 2 ? 2 : (P.qs_deep == 0 || P.qs_pivot == 1) ? 1 : 0);
         note_launches(1);
         return cudaGetLastError();
     };
@@ -1424,18 +1462,21 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         for (size_t bi = 0; bi < nbig; ++bi) {
             HSeg& sg = L.cur[L.big_idx[bi]];
             uint64_t p = sg.pivot;
-            if (sg.mode != 1) {  // median-of-3 (mode 0) or the ninther (mode 2) of host-read samples
+            if (sg.mode != 1) {  // median of 3 (mode 0), ninther (2) or median of 31 (3) of host-read samples
                 const uint64_t len = sg.hi - sg.lo;
-                const int ns = sg.mode == 2 ? 9 : 3;
-                uint64_t pos[9];
+                const int ns = sg.mode == 3 ? 31 : sg.mode == 2 ? 9 : 3;
+                uint64_t pos[31];
                 if (ns == 3) {
                     pos[0] = sg.lo;
                     pos[1] = sg.lo + (len - 1) / 2;
                     pos[2] = sg.hi - 1;
-                } else {
+                } else if (ns == 9) {
                     for (int j = 0; j < 9; ++j) pos[j] = ninther_pos<K>(sg.lo, len, j);
+                } else {
+                    for (int j = 0; j < 31; ++j)
+                        pos[j] = sg.lo + (len - 1) / 30 * (uint64_t)j + ((len - 1) % 30) * (uint64_t)j / 30;
                 }
-                K v[9];
+                K v[31];
                 e = cudaSuccess;
                 for (int j = 0; j < ns && e == cudaSuccess; ++j)
                     e = cudaMemcpyAsync(&v[j], keys + pos[j], sizeof(K), cudaMemcpyDeviceToHost, lst);
@@ -1446,8 +1487,14 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                     if (b > c) b = c;
                     return a > b ? a : b;
                 };
-                p = (uint64_t)(ns == 3 ? med3(v[0], v[1], v[2])
-                                       : med3(med3(v[0], v[1], v[2]), med3(v[3], v[4], v[5]), med3(v[6], v[7], v[8])));
+                if (ns == 3) {
+                    p = (uint64_t)med3(v[0], v[1], v[2]);
+                } else if (ns == 9) {
+                    p = (uint64_t)med3(med3(v[0], v[1], v[2]), med3(v[3], v[4], v[5]), med3(v[6], v[7], v[8]));
+                } else {
+                    std::sort(v, v + 31);
+                    p = (uint64_t)v[15];
+                }
             }
             L.pivots_h[L.big_idx[bi]] = p;
             pp_status ps = partition_device<K>(keys + sg.lo, sg.hi - sg.lo, (K)p, lst, d_splits + nmid + bi, nullptr);
@@ -1460,7 +1507,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             e = cudaMemcpyAsync(d_segs, pin_segs, sizeof(QSeg) * nmid, cudaMemcpyHostToDevice, lst);
             if (e == cudaSuccess && nh > 0) e = cudaMemcpyAsync(d_hidx, pin_hidx, 4 * nh, cudaMemcpyHostToDevice, lst);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort H2D");
-            qs_pivot_kernel<K><<<(unsigned)((nmid + 255) / 256), 256, 0, lst>>>(keys, d_segs, nmid);
+            qs_pivot_kernel<K><<<(unsigned)((nmid + 7) / 8), 256, 0, lst>>>(keys, d_segs, nmid);
             if (lvl_prof) cudaEventRecord(L.lev[0], lst);
             e = qs_launch_pdl(qs_group_kernel<K>, dim3((unsigned)gtot), C::NT, C::SMEM, lst, keys, d_segs, nmid,
                               P.seed, d_gout);

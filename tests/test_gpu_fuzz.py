@@ -111,6 +111,7 @@ QUICKSORT_PARAMS = [
     {}, {"leaf": 1000}, {"leaf": 4096}, {"leaf": 2000}, {"leaf": 8192},
     {"qs_small": 0}, {"qs_small": 1 << 18}, {"qs_cta_max": 1 << 16}, {"qs_heavy": 1 << 17},
     {"qs_heavy": 0}, {"qs_waves": 1}, {"qs_lanes": 1}, {"qs_lanes": 2, "qs_cta_max": 1 << 18},
+    {"qs_pivot": 1}, {"qs_pivot": 2}, {"qs_deep": 0},
     {"qs_early": 1}, {"qs_early": 1, "qs_small": 1 << 17, "qs_cta_max": 1 << 19},
 ]
 

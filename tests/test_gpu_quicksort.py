@@ -82,7 +82,8 @@ def test_medium_sizes(pp, dt, mx):
                                     {"qs_heavy": 1 << 17}, {"qs_heavy": 0}, {"qs_small": 0}, {"strided": 1},
                                     {"qs_lanes": 1}, {"qs_lanes": 2}, {"qs_lanes": 2, "qs_small": 1 << 17},
                                     {"qs_early": 1}, {"qs_early": 1, "qs_lanes": 1}, {"qs_early": 0},
-                                    {"qs_deep": 0}, {"qs_deep": 3}, {"qs_deep": 0, "qs_cta_max": 1 << 12}])
+                                    {"qs_deep": 0}, {"qs_deep": 3}, {"qs_deep": 0, "qs_cta_max": 1 << 12},
+                                    {"qs_pivot": 1}, {"qs_pivot": 2}, {"qs_pivot": 2, "qs_cta_max": 1 << 16}])
 def test_qs_parameters(pp, dt, mx, params):
     """Bin sizes (both bin-sort CTA shapes), level balancing, the
     heavy-segment batched cleanup, the per-CTA recursion and the Strided
@@ -200,7 +201,8 @@ def test_deep_segments_take_the_ninther(pp):
               np.concatenate([np.arange(1 << 20, dtype=np.uint64), np.arange(1 << 20, dtype=np.uint64)[::-1]])):
         ref = _oracle_sorted(a)
         levels = []
-        for params in ({}, {"qs_deep": 0}, {"qs_deep": 0, "qs_cta_max": 1 << 16}):
+        for params in ({}, {"qs_deep": 0}, {"qs_deep": 0, "qs_cta_max": 1 << 16}, {"qs_pivot": 2},
+                       {"qs_pivot": 2, "qs_cta_max": 1 << 16}):
             for k, v in params.items():
                 pp.pp_set_param(k, v)
             try:
