@@ -319,7 +319,8 @@ pp_status pp_quicksort_last_stats(uint64_t *out6);
  * "qs_lanes" (0 auto = 2 lanes), "qs_early" (-1 auto = on), "qs_early_min"
  * (0 auto), "qs_minl" (0 auto: 128 KiB per group), "qs_pivot" (0 median of 3
  * -- BASELINE config 5's rule, the default --, 1 Tukey's ninther, 2 the median
- * of 31 evenly spaced keys: better balanced splits, fewer levels), "qs_deep" (segments deeper
+ * of 31 evenly spaced keys: better balanced splits, fewer levels; also the
+ * distributed quicksort's rule for segments spanning ranks), "qs_deep" (segments deeper
  * than this take Tukey's ninther instead of the median of 3; -1 auto =
  * 2 log2(n) + 16, 0 = always); "host_chunk", "bps_nt";
  * multi-GPU: "dist_p2p", "dist_timeout_ms", "dist_small" (distributed

@@ -1067,12 +1067,20 @@ static pp_status quicksort_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, cuda
             if (sg.hi - sg.lo > 1 && owner(sg.lo) != owner(sg.hi - 1)) (sg.hi - sg.lo <= small ? sm : big).push_back(sg);
         if (big.empty() && sm.empty()) break;
         // ---- pivots: one all-gather of the sample keys of this level ----
-        std::vector<uint64_t> spos;  // 3 per segment needing a sample
+        // median of 3 (A[lo], A[mid], A[hi-1]; R14), or of 31 evenly spaced keys
+        // with qs_pivot = 2 (the single-GPU level loop's rule)
+        const int NSMP = params().qs_pivot == 2 ? 31 : 3;
+        std::vector<uint64_t> spos;  // NSMP per segment needing a sample
         for (const Seg& sg : big)
             if (!sg.leq) {
-                spos.push_back(sg.lo);
-                spos.push_back(sg.lo + (sg.hi - sg.lo - 1) / 2);
-                spos.push_back(sg.hi - 1);
+                const uint64_t len = sg.hi - sg.lo;
+                if (NSMP == 3) {
+                    spos.push_back(sg.lo);
+                    spos.push_back(sg.lo + (len - 1) / 2);
+                    spos.push_back(sg.hi - 1);
+                } else {
+                    for (uint64_t j = 0; j < 31; ++j) spos.push_back(sg.lo + (len - 1) / 30 * j + ((len - 1) % 30) * j / 30);
+                }
             }
         std::vector<uint64_t> sval;
         if (!spos.empty()) {
@@ -1101,10 +1109,10 @@ static pp_status quicksort_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, cuda
                 const Seg& sg = big[k];
                 uint64_t p = sg.pivot;
                 if (!sg.leq) {
-                    uint64_t v3[3] = {sval[si], sval[si + 1], sval[si + 2]};
-                    si += 3;
-                    std::sort(v3, v3 + 3);
-                    p = v3[1];
+                    std::vector<uint64_t> v(sval.begin() + si, sval.begin() + si + NSMP);
+                    si += NSMP;
+                    std::sort(v.begin(), v.end());
+                    p = v[NSMP / 2];
                 }
                 piv[k] = p;
                 uint64_t a, b;

@@ -380,6 +380,7 @@ def test_loopback_fuzz(pp):
             pp.reset_params()
             pp.pp_set_param("dist_p2p", int(rng.integers(0, 2)))
             pp.pp_set_param("dist_small", int(rng.choice([64, 5000, 1 << 16])))
+            pp.pp_set_param("qs_pivot", int(rng.integers(0, 3)))
             pp.pp_dist_set_staging(int(rng.choice([16, 4096, 1 << 20, 256 << 20])))
             ctx = (trial, P, dt, total, ns, alpha)
             if rng.random() < 0.5:
