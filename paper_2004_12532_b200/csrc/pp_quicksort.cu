@@ -75,6 +75,16 @@ __device__ __forceinline__ K warp_median31(const K* keys, uint64_t lo, uint64_t 
     return __shfl_sync(0xffffffffu, v, 15);  // the 16th smallest of the 31 samples
 }
 
+// Sample keys of a big segment (host-computed pivot): one launch writing into
+// pinned host memory (mapped, UVA) instead of one pageable 8-byte copy each.
+struct QsSamplePos {
+    uint64_t p[31];
+};
+template <typename K>
+__global__ void qs_sample_kernel(const K* __restrict__ keys, QsSamplePos pos, int ns, uint64_t* out) {
+    if ((int)threadIdx.x < ns) out[threadIdx.x] = (uint64_t)keys[pos.p[threadIdx.x]];
+}
+
 template <typename K>
 __global__ void __launch_bounds__(256) qs_pivot_kernel(const K* __restrict__ keys, QSeg* __restrict__ segs,
                                                        uint64_t nseg) {
@@ -1465,7 +1475,8 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             if (sg.mode != 1) {  // median of 3 (mode 0), ninther (2) or median of 31 (3) of host-read samples
                 const uint64_t len = sg.hi - sg.lo;
                 const int ns = sg.mode == 3 ? 31 : sg.mode == 2 ? 9 : 3;
-                uint64_t pos[31];
+                QsSamplePos sp;
+                uint64_t* pos = sp.p;
                 if (ns == 3) {
                     pos[0] = sg.lo;
                     pos[1] = sg.lo + (len - 1) / 2;
@@ -1476,12 +1487,15 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
                     for (int j = 0; j < 31; ++j)
                         pos[j] = sg.lo + (len - 1) / 30 * (uint64_t)j + ((len - 1) % 30) * (uint64_t)j / 30;
                 }
-                K v[31];
-                e = cudaSuccess;
-                for (int j = 0; j < ns && e == cudaSuccess; ++j)
-                    e = cudaMemcpyAsync(&v[j], keys + pos[j], sizeof(K), cudaMemcpyDeviceToHost, lst);
+                // the lane's pinned split area is idle until this level's splits come down
+                volatile uint64_t* hs = reinterpret_cast<uint64_t*>(L.pin + pin_sB);
+                qs_sample_kernel<K><<<1, 32, 0, lst>>>(keys, sp, ns, const_cast<uint64_t*>(hs));
+                note_launches(1);
+                e = cudaGetLastError();
                 if (e == cudaSuccess) e = cudaStreamSynchronize(lst);
                 if (e != cudaSuccess) return cuda_fail(e, "quicksort pivot");
+                K v[31];
+                for (int j = 0; j < ns; ++j) v[j] = (K)hs[j];
                 auto med3 = [](K a, K b, K c) {
                     if (a > b) std::swap(a, b);
                     if (b > c) b = c;
