@@ -393,6 +393,38 @@ def main():
                     "local_hbm_gbs": (16 * n / (lm / 1e3) / 1e9) if lm > 0 else None,
                     "timing": "library CUDA events on the call's stream (timed steps), per-rank means, max over ranks"}
 
+    overlap = None
+    if dist_on:
+        # the count-first overlapped exchange (param dist_overlap, SURVEY
+        # §8(f) #1): same input, same step bracket, a few steps, max over ranks
+        pp.pp_set_param("dist_overlap", 1)
+        ov_ms, ov_ph, ov_split = [], [], None
+        for i in range(min(args.steps, 5) + 1):
+            restore()
+            sync_all()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            step()
+            e.record(stream)
+            sync_all()
+            if i:  # the first one warms the path up
+                ov_ms.append(s.elapsed_time(e))
+                ov_ph.append(pp.pp_dist_last_timing())
+            ov_split = last_split[0]
+        pp.pp_set_param("dist_overlap", 0)
+        t = torch.tensor(ov_ms, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ov_ms = [float(x) for x in t.tolist()]
+        loc = [sum(p[f] for p in ov_ph) / len(ov_ph) for f in ("local_ms", "gather_ms", "exchange_ms", "bytes")]
+        tt = torch.tensor(loc, dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        cm, gm2, pxm, xb2 = (float(x) for x in tt.tolist())
+        overlap = {"ms_per_step": sum(ov_ms) / len(ov_ms), "steps": len(ov_ms),
+                   "keys_per_s": n_total / (sum(ov_ms) / len(ov_ms) / 1e3),
+                   "count_ms": cm, "allgather_ms": gm2, "partition_and_exchange_ms": pxm, "bytes_per_gpu": xb2,
+                   "chunks": pp.pp_get_param("dist_chunks"), "split_matches_default": ov_split == last_split[0],
+                   "timing": "same bracket as the timed steps (barrier + synchronize, CUDA events, max over ranks)"}
+
     value = n_total * args.steps / (tot_ms / 1e3)
     ms_per_step = tot_ms / args.steps
     bytes_step = 2 * 8 * n_total
@@ -433,6 +465,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
         **({"exchange": exchange} if exchange else {}),
+        **({"exchange_overlap": overlap} if overlap else {}),
         "split": split,
         "window_frac": (stats.get("W", 0) / n) if stats else None,
         "aux_bytes": stats.get("aux_bytes"),

@@ -325,7 +325,12 @@ pp_status pp_quicksort_last_stats(uint64_t *out6);
  * 2 log2(n) + 16, 0 = always); "host_chunk", "bps_nt";
  * multi-GPU: "dist_p2p", "dist_timeout_ms", "dist_small" (distributed
  * quicksort: spanning segments of <= this many keys are gathered and sorted
- * locally), "dist_fault", "dist_fault_rank" (loopback test hooks).
+ * locally), "dist_overlap" (1: pp_partition_dist counts every chunk of the
+ * shard first, all-gathers the counts, then partitions the "dist_chunks"
+ * chunks in order while the exchange of each finished chunk runs on a second
+ * stream -- SURVEY §8(f) #1; same result contract), "dist_chunks" (default
+ * 8, must be equal on every rank), "dist_fault", "dist_fault_rank" (loopback
+ * test hooks).
  * Returns PP_E_INVAL for an unknown name.  pp_get_param returns INT64_MIN
  * for an unknown name. */
 pp_status pp_set_param(const char *name, int64_t value);

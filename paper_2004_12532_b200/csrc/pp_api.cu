@@ -834,6 +834,8 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "dist_fault") P.dist_fault = value;
     else if (k == "dist_fault_rank") P.dist_fault_rank = value;
     else if (k == "dist_small") P.dist_small = value < 1 ? 1 : value;
+    else if (k == "dist_overlap") P.dist_overlap = value ? 1 : 0;
+    else if (k == "dist_chunks") P.dist_chunks = value < 1 ? 1 : value > 1024 ? 1024 : value;
     else if (k == "qs_lanes") P.qs_lanes = value;
     else if (k == "qs_deep") P.qs_deep = value;
     else if (k == "qs_pivot") P.qs_pivot = value < 0 || value > 2 ? 0 : value;
@@ -873,6 +875,8 @@ int64_t pp_get_param(const char* name) {
     if (k == "dist_fault") return P.dist_fault;
     if (k == "dist_fault_rank") return P.dist_fault_rank;
     if (k == "dist_small") return P.dist_small;
+    if (k == "dist_overlap") return P.dist_overlap;
+    if (k == "dist_chunks") return P.dist_chunks;
     if (k == "qs_lanes") return P.qs_lanes;
     if (k == "qs_deep") return P.qs_deep;
     if (k == "qs_pivot") return P.qs_pivot;

@@ -37,6 +37,7 @@
 #include <cuda.h>  // driver types only (cuMemGetAddressRange is fetched through the runtime)
 #include <nccl.h>
 
+#include "pp_device.cuh"
 #include "pp_internal.h"
 
 namespace pp {
@@ -501,13 +502,42 @@ struct DistCtx {
     size_t gs_bytes = 0;
     uint64_t* d_swap = nullptr;  // one-sided swap piece table
     size_t d_swap_words = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // start, local done, gathered, exchanged
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // start, local done, gathered, exchanged, join
     // staged exchange: the copies staging -> shard of round r run on pst while
     // round r+1 transfers into the other staging half
     cudaStream_t pst = nullptr;
     cudaEvent_t ev_recv[2] = {nullptr, nullptr}, ev_place[2] = {nullptr, nullptr};
+    // count-first overlapped exchange (dist_overlap): exchange stream, one
+    // event per chunk, per-chunk count partials + the local splits' check words
+    cudaStream_t xst = nullptr;
+    std::vector<cudaEvent_t> ev_chunk;
+    uint64_t* d_cnt = nullptr;
+    size_t d_cnt_words = 0;
     double last_local_ms = 0, last_gather_ms = 0, last_exchange_ms = 0;
     uint64_t last_bytes = 0;
+
+    pp_status init_overlap(size_t chunks, size_t cnt_words) {
+        if (!xst && cudaStreamCreateWithFlags(&xst, cudaStreamNonBlocking) != cudaSuccess)
+            return cuda_fail(cudaGetLastError(), "stream");
+        while (ev_chunk.size() < chunks) {
+            cudaEvent_t e = nullptr;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                return cuda_fail(cudaGetLastError(), "event");
+            ev_chunk.push_back(e);
+        }
+        if (cnt_words > d_cnt_words) {
+            if (d_cnt) cudaFree(d_cnt);
+            d_cnt = nullptr;
+            d_cnt_words = 0;
+            if (cudaMalloc(&d_cnt, 8 * cnt_words) != cudaSuccess) {
+                cudaGetLastError();
+                set_error("dist overlap scratch cudaMalloc failed");
+                return PP_E_NOMEM;
+            }
+            d_cnt_words = cnt_words;
+        }
+        return PP_OK;
+    }
 
     pp_status init_events() {
         for (auto& e : ev)
@@ -524,6 +554,14 @@ struct DistCtx {
     }
     void release() {
         if (pst) cudaStreamSynchronize(pst);
+        if (xst) cudaStreamSynchronize(xst);
+        for (cudaEvent_t e : ev_chunk) cudaEventDestroy(e);
+        ev_chunk.clear();
+        if (xst) cudaStreamDestroy(xst);
+        xst = nullptr;
+        if (d_cnt) cudaFree(d_cnt);
+        d_cnt = nullptr;
+        d_cnt_words = 0;
         for (auto& e : ev)
             if (e) {
                 cudaEventDestroy(e);
@@ -768,6 +806,82 @@ template pp_status swap_ranges<uint64_t>(const uint64_t*, uint64_t, cudaStream_t
 template pp_status swap_ranges<uint32_t>(const uint64_t*, uint64_t, cudaStream_t);
 
 // ---------------------------------------------------------------------------
+// Staged exchange: rounds of grouped send/recv into one half of a
+// double-buffered staging buffer, then a copy into place on the side stream
+// pst, which overlaps the next round's transfer into the other half.  Round
+// r+1's sends read ranges disjoint from round r's place targets; a half is
+// reused only after its previous place copies (ev_place).  The state carries
+// across calls (the overlapped exchange runs one call per chunk step).
+// ---------------------------------------------------------------------------
+struct StagedState {
+    uint64_t rno = 0;
+    bool placed[2] = {false, false};
+};
+
+template <typename K>
+static pp_status staged_rounds(DistCtx& c, K* shard, const std::vector<Piece>& pcs, uint64_t half, cudaStream_t xs,
+                               StagedState& ss, uint64_t& moved) {
+    Transport& tp = *c.tp;
+    const int me = c.me;
+    size_t i = 0;
+    while (i < pcs.size()) {
+        const uint64_t round = pcs[i].round;
+        const int hf = (int)(ss.rno++ & 1);
+        K* staging = static_cast<K*>(c.staging) + (size_t)hf * half;
+        if (ss.placed[hf] && cudaStreamWaitEvent(xs, c.ev_place[hf], 0) != cudaSuccess)
+            return cuda_fail(cudaGetLastError(), "dist staging order");
+        size_t j = i;
+        while (j < pcs.size() && pcs[j].round == round) ++j;
+        std::vector<uint64_t> offs, soffs, lens;
+        uint64_t soff = 0;
+        pp_status sr = tp.group_start();
+        for (size_t k = i; k < j && sr == PP_OK; ++k) {
+            const Piece& p = pcs[k];
+            int peer = -1;
+            uint64_t off = 0;
+            if ((int)p.rank_f == me) {
+                peer = (int)p.rank_t;
+                off = p.f;
+            } else if ((int)p.rank_t == me) {
+                peer = (int)p.rank_f;
+                off = p.t;
+            }
+            if (peer < 0) continue;
+            sr = tp.send(shard + off, p.len * sizeof(K), peer, xs);
+            if (sr == PP_OK) sr = tp.recv(staging + soff, p.len * sizeof(K), peer, xs);
+            offs.push_back(off);
+            soffs.push_back(soff);
+            lens.push_back(p.len);
+            soff += p.len;
+            moved += p.len * sizeof(K);
+        }
+        const pp_status se = tp.group_end(xs);
+        if (sr == PP_OK) sr = se;
+        if (sr != PP_OK) return sr;
+        if (!offs.empty()) {
+            cudaError_t e = cudaEventRecord(c.ev_recv[hf], xs);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(c.pst, c.ev_recv[hf], 0);
+            for (size_t k = 0; k < offs.size() && e == cudaSuccess; ++k)
+                e = cudaMemcpyAsync(shard + offs[k], staging + soffs[k], lens[k] * sizeof(K), cudaMemcpyDeviceToDevice,
+                                    c.pst);
+            if (e == cudaSuccess) e = cudaEventRecord(c.ev_place[hf], c.pst);
+            if (e != cudaSuccess) return cuda_fail(e, "dist place");
+            ss.placed[hf] = true;
+        }
+        i = j;
+    }
+    return PP_OK;
+}
+
+// the exchange on xs ends when every place copy has
+static pp_status staged_join(DistCtx& c, cudaStream_t xs, const StagedState& ss) {
+    for (int h = 0; h < 2; ++h)
+        if (ss.placed[h] && cudaStreamWaitEvent(xs, c.ev_place[h], 0) != cudaSuccess)
+            return cuda_fail(cudaGetLastError(), "dist place join");
+    return PP_OK;
+}
+
+// ---------------------------------------------------------------------------
 // Batched distributed partition: S segments, each a contiguous range of the
 // global array cut into per-rank pieces (a piece may be empty); every
 // segment is partitioned by its own pivot.  One record all-gather for all
@@ -914,65 +1028,13 @@ static pp_status partition_multi(DistCtx& c, K* shard, const std::vector<SegPiec
         // no rank leaves (or reads its shard) before every peer's swaps finished
         if ((sl = agree(c, sl, st)) != PP_OK) return sl;
     } else if (P > 1) {
-        // 4b. staged rounds: send my range, receive the partner's into a staging
-        //     half, place it (on the side stream pst, overlapping the next
-        //     round's transfer into the other half).  Round r+1's sends read
-        //     ranges disjoint from round r's place targets; a half is reused
-        //     only after its previous place copies (ev_place).
+        // 4b. staged rounds (double-buffered staging halves, place copies on pst)
         std::vector<Piece> pcs;
         schedule_rounds(runs, P, cap, pcs);
-        size_t i = 0;
-        uint64_t rno = 0;
-        bool placed[2] = {false, false};
-        while (i < pcs.size()) {
-            const uint64_t round = pcs[i].round;
-            const int hf = (int)(rno++ & 1);
-            K* staging = static_cast<K*>(c.staging) + (size_t)hf * half;
-            if (placed[hf] && cudaStreamWaitEvent(st, c.ev_place[hf], 0) != cudaSuccess)
-                return cuda_fail(cudaGetLastError(), "dist staging order");
-            size_t j = i;
-            while (j < pcs.size() && pcs[j].round == round) ++j;
-            std::vector<uint64_t> offs, soffs, lens;
-            uint64_t soff = 0;
-            pp_status sr = tp.group_start();
-            for (size_t k = i; k < j && sr == PP_OK; ++k) {
-                const Piece& p = pcs[k];
-                int peer = -1;
-                uint64_t off = 0;
-                if ((int)p.rank_f == me) {
-                    peer = (int)p.rank_t;
-                    off = p.f;
-                } else if ((int)p.rank_t == me) {
-                    peer = (int)p.rank_f;
-                    off = p.t;
-                }
-                if (peer < 0) continue;
-                sr = tp.send(shard + off, p.len * sizeof(K), peer, st);
-                if (sr == PP_OK) sr = tp.recv(staging + soff, p.len * sizeof(K), peer, st);
-                offs.push_back(off);
-                soffs.push_back(soff);
-                lens.push_back(p.len);
-                soff += p.len;
-                moved += p.len * sizeof(K);
-            }
-            const pp_status se = tp.group_end(st);
-            if (sr == PP_OK) sr = se;
-            if (sr != PP_OK) return sr;
-            if (!offs.empty()) {
-                e = cudaEventRecord(c.ev_recv[hf], st);
-                if (e == cudaSuccess) e = cudaStreamWaitEvent(c.pst, c.ev_recv[hf], 0);
-                for (size_t k = 0; k < offs.size() && e == cudaSuccess; ++k)
-                    e = cudaMemcpyAsync(shard + offs[k], staging + soffs[k], lens[k] * sizeof(K),
-                                        cudaMemcpyDeviceToDevice, c.pst);
-                if (e == cudaSuccess) e = cudaEventRecord(c.ev_place[hf], c.pst);
-                if (e != cudaSuccess) return cuda_fail(e, "dist place");
-                placed[hf] = true;
-            }
-            i = j;
-        }
-        for (int h = 0; h < 2; ++h)  // the exchange ends when every place copy has
-            if (placed[h] && cudaStreamWaitEvent(st, c.ev_place[h], 0) != cudaSuccess)
-                return cuda_fail(cudaGetLastError(), "dist place join");
+        StagedState ss;
+        pp_status sr = staged_rounds<K>(c, shard, pcs, half, st, ss, moved);
+        if (sr == PP_OK) sr = staged_join(c, st, ss);
+        if (sr != PP_OK) return sr;
     }
     if (timing) cudaEventRecord(c.ev[3], st);
     if ((s = tp.wait(st)) != PP_OK) return s;
@@ -989,9 +1051,284 @@ static pp_status partition_multi(DistCtx& c, K* shard, const std::vector<SegPiec
     return PP_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Count-first overlapped exchange (param dist_overlap = 1).
+// The shard is cut into C chunks (the same C on every rank).  (1) One read
+// pass counts the predecessors of every chunk (chunk_count_kernel, fixed-order
+// sums: no atomics).  (2) ONE all-gather of (status, key bytes, pivot, C, n,
+// n_c[C], t_c[C]) fixes K and the plan BEFORE any key moves: every chunk
+// acts as a unit of the same interval merge as the ranks of match_runs (a
+// chunk partitioned in place holds its predecessors first, so its misplaced
+// range is [β_u + t_u, min(K, β_u + n_u)) or [max(K, β_u), β_u + t_u) exactly
+// as for a shard).  A matched run between chunk c of one rank and chunk c' of
+// another can move once both are partitioned: it belongs to step max(c, c').
+// (3) All C local partitions are enqueued on the caller's stream, an event
+// after each; (4) the exchange of step k waits on chunk k's event on a second
+// stream, so it overlaps the partition of chunks k+1.. (staged rounds through
+// NCCL, or one-sided peer swaps after a per-step status barrier).  The local
+// splits are checked against the counts at the end (PP_E_INTERNAL on every
+// rank on a mismatch).  Unlike whole shards, two chunks of the rank holding K
+// can be matched with each other: those runs are local swaps.  Cost: one extra read of the shard; gain: the
+// NVLink-bound exchange runs under the local partition (§9).
+// ---------------------------------------------------------------------------
+template <typename K>
+__global__ void __launch_bounds__(256) chunk_count_kernel(const K* __restrict__ keys, uint64_t n, uint64_t L,
+                                                          K pivot, uint64_t* __restrict__ partial) {
+    __shared__ uint64_t ws[8];
+    const uint64_t lo = (uint64_t)blockIdx.y * L, hi = lo + L < n ? lo + L : n;
+    const uint64_t S = (uint64_t)gridDim.x * 256;
+    uint64_t cnt = 0;
+    uint64_t x = lo + (uint64_t)blockIdx.x * 256 + threadIdx.x;
+    for (; x + 3 * S < hi; x += 4 * S) {  // four independent loads in flight per thread
+        const K a = keys[x], b = keys[x + S], d = keys[x + 2 * S], e = keys[x + 3 * S];
+        cnt += (uint64_t)is_pred(a, pivot) + is_pred(b, pivot) + is_pred(d, pivot) + is_pred(e, pivot);
+    }
+    for (; x < hi; x += S) cnt += is_pred(keys[x], pivot) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) cnt += ws[w];
+        partial[(uint64_t)blockIdx.y * gridDim.x + blockIdx.x] = cnt;
+    }
+}
+
+// out[c] = sum of chunk c's B partials, in index order (thread c)
+__global__ void chunk_count_reduce_kernel(const uint64_t* __restrict__ partial, uint32_t B, uint32_t C,
+                                          uint64_t* __restrict__ out) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < C; c += gridDim.x * blockDim.x) {
+        uint64_t t = 0;
+        for (uint32_t b = 0; b < B; ++b) t += partial[(uint64_t)c * B + b];
+        out[c] = t;
+    }
+}
+
+template <typename K>
+static pp_status partition_overlap(DistCtx& c, K* shard, uint64_t n_local, K pivot, cudaStream_t st,
+                                   uint64_t* K_out) {
+    Transport& tp = *c.tp;
+    const int P = c.P, me = c.me;
+    if (tp.absent()) {  // test hook: this rank never takes part
+        set_error("rank absent (dist_fault = 2)");
+        return PP_E_INTERNAL;
+    }
+    const uint64_t C = (uint64_t)std::max<int64_t>(1, params().dist_chunks);
+    uint64_t L = (n_local + C - 1) / C;
+    L = std::max<uint64_t>(64, (L + 63) / 64 * 64);  // chunk length (the last chunks may be short or empty)
+    auto clo = [&](uint64_t k) { return std::min(n_local, k * L); };
+    auto chi = [&](uint64_t k) { return std::min(n_local, (k + 1) * L); };
+    const size_t RW = 5 + 2 * C;  // record: [status, key bytes, pivot, C, n, n_c[C], t_c[C]]
+    const uint32_t B = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(1024, (uint64_t)sm_count() * 8 / C));
+    cudaEventRecord(c.ev[0], st);
+    pp_status s = PP_OK;
+    const uint64_t cap = std::max<uint64_t>(1, g_staging_cap_bytes / sizeof(K));
+    const uint64_t half = std::max<uint64_t>(1, std::min(cap, n_local));
+    if (!params().dist_p2p && P > 1) s = grow(&c.staging, &c.staging_bytes, 2 * sizeof(K) * half);
+    {
+        pp_status sa = ensure_ag(c, RW * (P + 1));
+        if (sa == PP_OK) sa = c.init_overlap(C, C * B + C);
+        if (sa != PP_OK) return sa;  // without them this rank cannot take part (as partition_multi)
+    }
+    if (s == PP_OK && params().dist_fault == 1 && params().dist_fault_rank == me) {
+        set_error("injected local failure (dist_fault = 1)");
+        s = PP_E_INTERNAL;
+    }
+    uint64_t* rec = c.d_ag + RW * P;
+    uint64_t* d_tchk = c.d_cnt + C * B;  // the local partitions' splits
+    // 1. per-chunk predecessor counts -> rec[5 + C ..]
+    if (s == PP_OK && n_local > 0) {
+        tp.local_begin();
+        chunk_count_kernel<K><<<dim3(B, (unsigned)C), 256, 0, st>>>(shard, n_local, L, pivot, c.d_cnt);
+        chunk_count_reduce_kernel<<<1, 256, 0, st>>>(c.d_cnt, B, (uint32_t)C, rec + 5 + C);
+        note_launches(2);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) s = cuda_fail(e, "chunk count");
+        const pp_status s2 = tp.local_end(st);
+        if (s == PP_OK) s = s2;
+    } else if (cudaMemsetAsync(rec + 5 + C, 0, 8 * C, st) != cudaSuccess) {
+        s = cuda_fail(cudaGetLastError(), "memset");
+    }
+    cudaEventRecord(c.ev[1], st);
+    std::vector<uint64_t> head(5 + C);
+    head[0] = (uint64_t)s;
+    head[1] = sizeof(K);
+    head[2] = (uint64_t)pivot;
+    head[3] = C;
+    head[4] = n_local;
+    for (uint64_t k = 0; k < C; ++k) head[5 + k] = chi(k) - clo(k);
+    cudaError_t e = cudaMemcpyAsync(rec, head.data(), 8 * head.size(), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "dist record H2D");
+    // 2. all-gather the records (status agreement included) -> K and the plan
+    pp_status sg = tp.allgather(rec, c.d_ag, 8 * RW, st);
+    if (sg != PP_OK) return sg;
+    cudaEventRecord(c.ev[2], st);
+    std::vector<uint64_t> all(RW * P);
+    e = cudaMemcpyAsync(all.data(), c.d_ag, 8 * RW * P, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "dist record D2H");
+    if ((sg = tp.wait(st)) != PP_OK) return sg;
+    for (int q = 0; q < P; ++q)
+        if (all[RW * q] != PP_OK) {
+            if (q != me) set_error("peer rank " + std::to_string(q) + " failed with status " + std::to_string(all[RW * q]));
+            return (pp_status)all[RW * q];
+        }
+    for (int q = 0; q < P; ++q)
+        if (all[RW * q + 1] != sizeof(K) || all[RW * q + 2] != (uint64_t)pivot || all[RW * q + 3] != C) {
+            set_error("pp_partition_dist (dist_overlap): ranks passed different pivots, key types or dist_chunks");
+            return PP_E_INVAL;
+        }
+    const uint64_t U = (uint64_t)P * C;
+    std::vector<uint64_t> ns(U), ts(U), rbase(P, 0);
+    for (int q = 0; q < P; ++q) {
+        if (q > 0) rbase[q] = rbase[q - 1] + all[RW * (q - 1) + 4];
+        for (uint64_t k = 0; k < C; ++k) {
+            ns[q * C + k] = all[RW * q + 5 + k];
+            ts[q * C + k] = all[RW * q + 5 + C + k];
+            if (ts[q * C + k] > ns[q * C + k]) {
+                set_error("pp_partition_dist: corrupt chunk count");
+                return PP_E_INTERNAL;
+            }
+        }
+    }
+    std::vector<Run> uruns;
+    const uint64_t Kg = match_runs(ns.data(), ts.data(), (int)U, uruns);
+    std::vector<std::vector<Run>> by_step(C);  // runs in rank-local offsets, by the step that frees them
+    for (const Run& r : uruns) {
+        const uint64_t qa = r.ra / C, qb = r.rb / C;
+        const uint64_t step = std::max(r.ra % C, r.rb % C);
+        by_step[step].push_back({qa, r.a - rbase[qa], qb, r.b - rbase[qb], r.len});
+    }
+    // 3. every chunk's local partition, enqueued up front on st (an event after each)
+    pp_status sl = PP_OK;
+    tp.local_begin();
+    for (uint64_t k = 0; k < C && sl == PP_OK; ++k) {
+        const uint64_t lo = clo(k), len = chi(k) - lo;
+        if (len > 0) sl = partition_device<K>(shard + lo, len, pivot, st, d_tchk + k, nullptr);
+        else if (cudaMemsetAsync(d_tchk + k, 0, 8, st) != cudaSuccess) sl = cuda_fail(cudaGetLastError(), "memset");
+        if (sl == PP_OK && cudaEventRecord(c.ev_chunk[k], st) != cudaSuccess) sl = cuda_fail(cudaGetLastError(), "event");
+    }
+    {
+        const pp_status s2 = tp.local_end(st);  // loopback: waits; NCCL: no-op
+        if (sl == PP_OK) sl = s2;
+    }
+    // enqueue failures are agreed on before any exchange (kernels keep running)
+    if ((sl = agree(c, sl, c.xst)) != PP_OK) {
+        cudaStreamSynchronize(st);
+        return sl;
+    }
+    // 4. the exchange, step by step on xst
+    uint64_t moved = 0;
+    pp_status sx = PP_OK;
+    if (params().dist_p2p && P > 1) {
+        std::vector<uint64_t> prec(1 + kPeerWords), allp;
+        pp_status se = tp.export_range(shard, prec.data() + 1);
+        prec[0] = (uint64_t)se;
+        sx = ag_host(c, prec.data(), 1 + kPeerWords, allp, c.xst);
+        for (int q = 0; q < P && sx == PP_OK; ++q)
+            if (allp[(1 + kPeerWords) * q] != PP_OK) sx = (pp_status)allp[(1 + kPeerWords) * q];
+        std::vector<K*> ptr(P, nullptr);
+        ptr[me] = shard;
+        for (uint64_t k = 0; k < C && sx == PP_OK; ++k) {
+            if (by_step[k].empty()) continue;  // the same on every rank
+            std::vector<Run> share;
+            p2p_share(by_step[k], me, share);
+            pp_status sk = PP_OK;
+            for (const Run& p : share)
+                for (uint64_t q : {p.ra, p.rb}) {
+                    if (ptr[q] || sk != PP_OK) continue;
+                    void* d = nullptr;
+                    sk = tp.import_range(&allp[(1 + kPeerWords) * q + 1], &d);
+                    ptr[q] = static_cast<K*>(d);
+                }
+            if (sk == PP_OK && cudaEventSynchronize(c.ev_chunk[k]) != cudaSuccess)
+                sk = cuda_fail(cudaGetLastError(), "chunk event");
+            // every rank's chunks <= k are final before anyone swaps into them
+            if ((sk = agree(c, sk, c.xst)) != PP_OK) {
+                sx = sk;
+                break;
+            }
+            if (!share.empty()) {
+                std::vector<uint64_t> tri;
+                for (const Run& p : share) {
+                    moved += 2 * p.len * sizeof(K);
+                    tri.push_back(reinterpret_cast<uint64_t>(ptr[p.ra] + p.a));
+                    tri.push_back(reinterpret_cast<uint64_t>(ptr[p.rb] + p.b));
+                    tri.push_back(p.len);
+                }
+                tp.local_begin();
+                sx = swap_ranges_impl<K>(tri.data(), share.size(), c.xst, true, &c.d_swap, &c.d_swap_words);
+                const pp_status s2 = tp.local_end(c.xst);
+                if (sx == PP_OK) sx = s2;
+            }
+        }
+    } else {  // P = 1 too: the rank's own chunks trade by local swaps
+        StagedState ss;
+        for (uint64_t k = 0; k < C && sx == PP_OK; ++k) {
+            if (by_step[k].empty()) continue;
+            if (cudaStreamWaitEvent(c.xst, c.ev_chunk[k], 0) != cudaSuccess) {
+                sx = cuda_fail(cudaGetLastError(), "chunk order");
+                break;
+            }
+            // runs between two chunks of this rank (only the rank holding K has
+            // them) are local swaps; the others go through the staged rounds
+            std::vector<Run> cross;
+            std::vector<uint64_t> tri;
+            for (const Run& r : by_step[k]) {
+                if (r.ra != r.rb) {
+                    cross.push_back(r);
+                } else if ((int)r.ra == me) {
+                    tri.push_back(reinterpret_cast<uint64_t>(shard + r.a));
+                    tri.push_back(reinterpret_cast<uint64_t>(shard + r.b));
+                    tri.push_back(r.len);
+                }
+            }
+            if (!tri.empty()) {
+                tp.local_begin();
+                sx = swap_ranges_impl<K>(tri.data(), tri.size() / 3, c.xst, false, &c.d_swap, &c.d_swap_words);
+                const pp_status s2 = tp.local_end(c.xst);
+                if (sx == PP_OK) sx = s2;
+                if (sx != PP_OK) break;
+            }
+            std::vector<Piece> pcs;
+            schedule_rounds(cross, P, cap, pcs);
+            sx = staged_rounds<K>(c, shard, pcs, half, c.xst, ss, moved);
+        }
+        if (sx == PP_OK) sx = staged_join(c, c.xst, ss);
+    }
+    // 5. join, check the local splits against the counts, agree
+    if (cudaEventRecord(c.ev[4], c.xst) != cudaSuccess || cudaStreamWaitEvent(st, c.ev[4], 0) != cudaSuccess ||
+        cudaEventRecord(c.ev[3], st) != cudaSuccess) {
+        if (sx == PP_OK) sx = cuda_fail(cudaGetLastError(), "dist join");
+    }
+    if (sx == PP_OK) sx = tp.wait(c.xst);
+    std::vector<uint64_t> tchk(C, 0);
+    if (cudaMemcpyAsync(tchk.data(), d_tchk, 8 * C, cudaMemcpyDeviceToHost, st) != cudaSuccess && sx == PP_OK)
+        sx = cuda_fail(cudaGetLastError(), "split check D2H");
+    if (cudaStreamSynchronize(st) != cudaSuccess && sx == PP_OK) sx = cuda_fail(cudaGetLastError(), "dist stream");
+    for (uint64_t k = 0; k < C && sx == PP_OK; ++k)
+        if (tchk[k] != all[RW * me + 5 + C + k]) {
+            set_error("pp_partition_dist (dist_overlap): a chunk's split differs from its count");
+            sx = PP_E_INTERNAL;
+        }
+    // no rank returns (or reads its shard) while a peer may still write into it
+    if ((sx = agree(c, sx, st)) != PP_OK) return sx;
+    float a = 0, b = 0, d = 0;
+    cudaEventElapsedTime(&a, c.ev[0], c.ev[1]);
+    cudaEventElapsedTime(&b, c.ev[1], c.ev[2]);
+    cudaEventElapsedTime(&d, c.ev[2], c.ev[3]);
+    c.last_local_ms = a;   // the count pass
+    c.last_gather_ms = b;
+    c.last_exchange_ms = d;  // local partitions + the overlapped exchange
+    c.last_bytes = moved;
+    if (K_out) *K_out = Kg;
+    return PP_OK;
+}
+
 template <typename K>
 static pp_status partition_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, K pivot, cudaStream_t st,
                                     uint64_t* global_split) {
+    if (params().dist_overlap) return partition_overlap<K>(c, shard, n_local, pivot, st, global_split);
     std::vector<uint64_t> Ks;
     pp_status s = partition_multi<K>(c, shard, {SegPiece{0, n_local, (uint64_t)pivot}}, st, Ks, true);
     if (s == PP_OK && global_split) *global_split = Ks[0];

@@ -62,6 +62,9 @@ struct Params {
     int64_t dist_timeout_ms = 600000;  // distributed calls: a wait longer than this aborts (PP_E_NCCL on every rank)
     int64_t dist_fault = 0;        // test hook (loopback): 1 = rank dist_fault_rank fails its local step, 2 = it never arrives
     int64_t dist_fault_rank = -1;
+    int64_t dist_overlap = 0;      // pp_partition_dist: 1 = count first, then chunked local partitions whose exchange
+                                   // pieces move while the next chunk is partitioned
+    int64_t dist_chunks = 8;       // dist_overlap: chunks per shard (the same on every rank)
     int64_t dist_small = 1 << 16;  // distributed quicksort: spanning segments <= this are gathered and sorted locally
     int64_t host_chunk = 1 << 23;  // host-buffer partition: keys per streamed chunk (measured best at 1-8 GiB)
     int64_t qs_pivot = 0;          // quicksort level-loop pivot: 0 median of 3 (BJ config 5), 1 Tukey's ninther,

@@ -117,6 +117,41 @@ def p2p_pieces(ns: List[int], ts: List[int], rank: int):
     return out
 
 
+def chunk_bounds(n: int, C: int):
+    """The C chunks [lo, hi) of an n-key shard under dist_overlap: length
+    L = ceil(n / C) rounded up to a multiple of 64 (>= 64); the last chunks
+    may be short or empty."""
+    L = max(64, (-(-n // C) + 63) // 64 * 64) if n else 64
+    return [(min(n, k * L), min(n, (k + 1) * L)) for k in range(C)]
+
+
+def overlap_plan(ns: List[int], chunk_ts: List[List[int]], C: int):
+    """Mirror of the count-first overlapped exchange (param dist_overlap):
+    every chunk of every rank is one unit of `exchange_plan` (a chunk
+    partitioned in place holds its predecessors first, exactly like a shard),
+    and a matched run between chunk c of one rank and chunk c' of another can
+    move once both are partitioned, i.e. at step max(c, c').  Unlike whole
+    shards, two chunks of ONE rank (the rank holding K) can be matched: such
+    a run is a local swap.  Returns
+    (K, steps): steps[k] = [(rank_f, f_local, rank_t, t_local, len, c_f, c_t)]."""
+    P = len(ns)
+    units_n, units_t, owner = [], [], []
+    for r in range(P):
+        for k, (lo, hi) in enumerate(chunk_bounds(ns[r], C)):
+            units_n.append(hi - lo)
+            units_t.append(chunk_ts[r][k])
+            owner.append((r, k))
+    K, plan = exchange_plan(units_n, units_t)
+    base = [0] * P
+    for r in range(1, P):
+        base[r] = base[r - 1] + ns[r - 1]
+    steps = [[] for _ in range(C)]
+    for tr in plan:
+        (ra, ca), (rb, cb) = owner[tr.rank_f], owner[tr.rank_t]
+        steps[max(ca, cb)].append((ra, tr.f - base[ra], rb, tr.t - base[rb], tr.length, ca, cb))
+    return K, steps
+
+
 def my_ops(pieces: List[Transfer], rank: int, base: int):
     """The (peer, local_offset, length) swaps this rank takes part in."""
     ops = []

@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from dist_mirror import Partitioner, exchange_plan, my_ops, schedule_rounds
+from dist_mirror import Partitioner, chunk_bounds, exchange_plan, my_ops, overlap_plan, schedule_rounds
 
 
 def _simulate(shards, pivot):
@@ -48,6 +48,43 @@ def test_plan_simulator(P):
         oracle.check_partition(glob, out, pivot, K)
         for tr in plan:
             assert tr.rank_f != tr.rank_t and tr.length > 0
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("C", [1, 2, 3, 8])
+def test_overlap_plan_simulator(P, C):
+    """The count-first overlapped exchange (dist_overlap) by simulation: the
+    per-chunk counts fix the plan before any key moves; at step k every rank
+    partitions its chunk k, then the runs of step k are swapped -- each touches
+    only chunks <= k on both sides (already partitioned, never touched again
+    by a local step) -- and the result is the global partition."""
+    rng = np.random.default_rng(100 * P + C)
+    for trial in range(12):
+        ns = [int(x) for x in rng.integers(0, 700, size=P)]
+        if trial % 3 == 0:
+            ns = [512] * P
+        if trial % 4 == 1 and P > 1:
+            ns[0] = 0
+        glob = rng.integers(0, 50, size=sum(ns)).astype(np.uint64)
+        pivot = int(rng.integers(0, 51))
+        shards = [x.copy() for x in np.split(glob, np.cumsum(ns)[:-1])] if P > 1 else [glob.copy()]
+        bounds = [chunk_bounds(n, C) for n in ns]
+        cts = [[oracle.count(shards[r][lo:hi], pivot) for lo, hi in bounds[r]] for r in range(P)]
+        K, steps = overlap_plan(ns, cts, C)
+        assert K == oracle.count(glob, pivot)
+        for k in range(C):
+            for r in range(P):
+                lo, hi = bounds[r][k]
+                assert oracle.partition_two_pointer(shards[r][lo:hi], pivot) == cts[r][k]
+            for ra, a, rb, b, ln, ca, cb in steps[k]:
+                # a run inside one rank (between two of its chunks) exists only on the rank holding K
+                assert (ra != rb or ca != cb) and ln > 0 and max(ca, cb) == k
+                assert bounds[ra][ca][0] <= a and a + ln <= bounds[ra][ca][1]
+                assert bounds[rb][cb][0] <= b and b + ln <= bounds[rb][cb][1]
+                x = shards[ra][a:a + ln].copy()
+                shards[ra][a:a + ln] = shards[rb][b:b + ln]
+                shards[rb][b:b + ln] = x
+        oracle.check_partition(glob, np.concatenate(shards), pivot, K)
 
 
 def test_plan_adversarial_counts():

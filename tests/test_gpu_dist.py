@@ -264,6 +264,60 @@ def test_loopback_partition(pp, P, dt, p2p):
         pp.reset_params()
 
 
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("dt", [np.uint64, np.uint32])
+@pytest.mark.parametrize("p2p", [0, 1])
+def test_loopback_partition_overlap(pp, P, dt, p2p):
+    """The count-first overlapped exchange (dist_overlap = 1, SURVEY §8(f)
+    #1) through the product code: per-chunk counts, one record all-gather,
+    chunk-unit plan, every chunk's partition enqueued up front, the exchange
+    of step k after chunk k (staged rounds or one-sided swaps, local swaps on
+    the rank holding K); K = the oracle count and the oracle's checks on the
+    whole array, for 1, 3 and 8 chunks per shard, ragged / empty shards,
+    pivots 0, MAX, mid, skewed and random, staging caps 4 KiB and 64 KiB."""
+    from gpu_util import to_dev, to_host
+    rng = np.random.default_rng(5000 * P + 10 * (dt == np.uint64) + p2p)
+    mx = (1 << 64) - 1 if dt == np.uint64 else (1 << 32) - 1
+    pp.pp_set_param("dist_p2p", p2p)
+    pp.pp_set_param("dist_overlap", 1)
+    try:
+        for C in (1, 3, 8):
+            pp.pp_set_param("dist_chunks", C)
+            for total, kind, cap in ((1, "ragged", 1 << 12), (977, "empty", 1 << 12), (300_007, "ragged", 1 << 12),
+                                     (1_000_003, "empty", 1 << 16)):
+                ns = _shards(rng, total, P, kind) if P > 1 else [total]
+                a = _keys(rng, total, dt, "uniform")
+                pp.pp_dist_set_staging(cap)
+                for pivot in (0, mx, (mx + 1) // 2, int(mx // 100), int(rng.integers(0, mx, dtype=dt))):
+                    t = to_dev(a)
+                    K = pp.pp_partition_dist_loopback(t, ns, pivot)
+                    assert K == oracle.count(a, pivot), (C, total, pivot)
+                    oracle.check_partition(a, to_host(t, dt), pivot, K)
+    finally:
+        pp.pp_dist_set_staging(256 << 20)
+        pp.reset_params()
+
+
+def test_dist_overlap_single_rank(pp):
+    """dist_overlap through the NCCL transport on a one-rank communicator
+    (count pass, record all-gather, chunked local partitions; the rank's
+    chunks exchange among themselves by local swaps) and its timing record."""
+    from gpu_util import to_dev
+    pp.pp_set_param("dist_overlap", 1)
+    try:
+        for dt, n, p, C in ((np.uint64, 1 << 20, 1 << 63, 8), (np.uint64, 3_000_017, 1 << 61, 5),
+                            (np.uint32, 2_000_003, 1 << 31, 3), (np.uint64, 0, 5, 8)):
+            pp.pp_set_param("dist_chunks", C)
+            a = (synth.uniform_u64_np(n, 78) if dt == np.uint64 else synth.uniform_u32_np(n, 78))
+            t = to_dev(a) if n else torch.empty(0, dtype=torch.int64, device="cuda")
+            K = pp.pp_partition_dist(t, p)
+            oracle.check_partition(a, t.cpu().numpy().view(dt), p, K)
+            tm = pp.pp_dist_last_timing()
+            assert tm["local_ms"] >= 0 and tm["exchange_ms"] >= 0 and tm["bytes"] == 0
+    finally:
+        pp.reset_params()
+
+
 def test_loopback_partition_deterministic(pp):
     """Two runs of the loopback exchange give identical bytes (EREW
     determinism): the plan and the pieces are a pure function
@@ -381,6 +435,8 @@ def test_loopback_fuzz(pp):
             pp.pp_set_param("dist_p2p", int(rng.integers(0, 2)))
             pp.pp_set_param("dist_small", int(rng.choice([64, 5000, 1 << 16])))
             pp.pp_set_param("qs_pivot", int(rng.integers(0, 3)))
+            pp.pp_set_param("dist_overlap", int(rng.integers(0, 2)))
+            pp.pp_set_param("dist_chunks", int(rng.choice([1, 2, 5, 8])))
             pp.pp_dist_set_staging(int(rng.choice([16, 4096, 1 << 20, 256 << 20])))
             ctx = (trial, P, dt, total, ns, alpha)
             if rng.random() < 0.5:
