@@ -64,6 +64,18 @@ struct GroupCfgT {
 template <typename K>
 using GroupCfg = GroupCfgT<K, sizeof(K) == 8 ? PP_U64_LINE : PP_U32_LINE, sizeof(K) == 8 ? PP_U64_NT : PP_U32_NT,
                            sizeof(K) == 8 ? PP_U64_PF : PP_U32_PF, false, false, sizeof(K) == 4>;
+// The partition's own group kernel: u32 with 3 lines in flight per end (41 KiB
+// of shared memory: 5 CTAs per SM instead of 4 -- the u32 engine is
+// issue-bound, more resident warps hide more of it): config 4 measured 2-3%
+// faster (1.40 -> 1.37 ms partitioned, 1.43 -> 1.39 alternating / reverse);
+// the quicksort's level kernel keeps GroupCfg (mixed there: -5% median-of-3
+// uniform, +3% duplicate-heavy).
+#ifndef PP_U32_PART_PF
+#define PP_U32_PART_PF 3
+#endif
+template <typename K>
+using PartGroupCfg = GroupCfgT<K, sizeof(K) == 8 ? PP_U64_LINE : PP_U32_LINE, sizeof(K) == 8 ? PP_U64_NT : PP_U32_NT,
+                               sizeof(K) == 8 ? PP_U64_PF : PP_U32_PART_PF, false, false, sizeof(K) == 4>;
 
 // Line index of the j-th line (group order) of group gi: G_i(j) of
 // PAPER.md:963-969 in 0-based form, j*g + ((X[j] + i) mod g).

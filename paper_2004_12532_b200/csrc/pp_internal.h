@@ -71,6 +71,8 @@ struct Params {
                                    // 2 median of 31 samples (the per-CTA recursion takes the ninther for 1, 2)
     int64_t qs_deep = -1;          // quicksort levels: segments deeper than this use the ninther pivot (-1 auto:
                                    // 2 log2(n) + 16; 0: always)
+    int64_t qs_prio = -1;          // quicksort: level loop on high-priority streams, early recursion / bins low
+                                   // (-1 auto = on, 0 off, 1 on)
     int64_t qs_heavy = 1 << 22;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
 };
 Params& params();

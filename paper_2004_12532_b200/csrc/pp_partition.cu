@@ -266,13 +266,13 @@ struct VariantInfo {
 
 template <typename K, int V>
 struct VariantCfg;
-// 0: the default configuration (pp_group.cuh GroupCfg)
-template <typename K> struct VariantCfg<K, 0> { using type = GroupCfg<K>; };
+// 0: the default configuration (pp_group.cuh PartGroupCfg)
+template <typename K> struct VariantCfg<K, 0> { using type = PartGroupCfg<K>; };
 // 1: the same with X = 0 (the Strided Algorithm), selected by
 // the "strided" param (seed 0): a separate instantiation, since a runtime
 // branch on the seed made the compiler unswitch the whole engine (-7%)
 template <typename K> struct VariantCfg<K, 1> {
-    using D = GroupCfg<K>;
+    using D = PartGroupCfg<K>;
     using type = GroupCfgT<K, D::LK * (int)sizeof(K), D::NT, D::PF, D::TMA_STORE, true, D::PAR_ISSUE>;
 };
 constexpr int STRIDED_VARIANT = 1;

@@ -530,17 +530,25 @@ __device__ __forceinline__ int key_bits(K v) {
     return sizeof(K) == 8 ? 64 - __clzll((long long)v) : 32 - __clz((int)v);
 }
 
-// Bin sort leaf_algo 6: the counting sort of qs_leaf_bucket_kernel with the
-// keys staged in shared memory (input order) and 16-bit key INDICES
-// scattered and ranked instead of the keys: NT = 512 threads x 16 keys,
-// 2 PLEAF buckets (16-bit counts packed two per word).  After the scan every
-// key keeps (its position, its slot in the bucket, the bucket's size) packed
-// in one register, so the index array can then reuse the counters' memory:
-// 96 KiB of shared memory and <= 64 registers -- two CTAs share an SM and
-// one's HBM loads, barriers and scans overlap the other's work (the
-// 1024-thread kernel holds its keys in registers: one CTA per SM).  A bin
-// with a crowded bucket is left untouched and tagged (BIN_HANDOFF in its
-// length word) for qs_leaf_handoff_kernel, launched right after.
+// Bin sort: a counting sort of one bin (<= PLEAF keys) in shared memory.  The
+// keys are staged in input order; bucket d = (key - min) >> sh over 2 PLEAF
+// buckets (16-bit counts packed two per word, one shared-memory atomic per
+// key returns its slot in the bucket); one block scan gives the bucket starts;
+// every key keeps (position, slot, bucket size) packed in one register, so the
+// 16-bit INDEX array scattered next reuses the counters' memory.  The key in
+// slot 0 of a bucket of c > 1 keys marks the run [start, start + c) in a
+// byte array; the thread owning the run's first position (16 positions per
+// thread) insertion-sorts that run of indices by key (runs are disjoint; c <=
+// BK_MAX_RUN).  The keys are then gathered through the indices into
+// coalesced stores.  16384-key bins: 1024 threads, 208 KiB, one CTA per SM;
+// 8192-key bins: 512 threads, two CTAs per SM.  A bin with a crowded bucket
+// (> BK_MAX_RUN keys while sh > 0) is left untouched and tagged (BIN_HANDOFF
+// in its length word) for qs_leaf_handoff_kernel, launched right after.
+// (Round 2: the per-run insertion sort replaced a per-key rank loop -- each
+// key of a multi-key bucket counted the bucket's smaller keys, divergent
+// across the warp -- 37% of the kernel's instructions; the kernel time barely
+// moved, 3.69 -> 3.66 ms per 2^28-key sort: it is bound by its HBM load
+// latency at one CTA per SM, not by issue.)
 template <typename K, int PLEAF, int NT>
 __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kernel(K* __restrict__ keys,
                                                             const uint64_t* __restrict__ leaf_lo,
@@ -553,6 +561,8 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     K* ks = reinterpret_cast<K*>(lsm);                          // [PLEAF] keys, input order
     uint32_t* cw = reinterpret_cast<uint32_t*>(ks + PLEAF);     // [NWD + 1] packed counts, then starts
     uint16_t* ix = reinterpret_cast<uint16_t*>(cw);             // [PLEAF] key indices (after the starts are read)
+    uint8_t* rs = reinterpret_cast<uint8_t*>(cw + NWD + 4);     // [PLEAF] size of the bucket starting here (> 1 only)
+    static_assert(PLEAF / NT == 16, "one 16-byte run-start word per thread");
     __shared__ K rmn[NW], rmx[NW];
     __shared__ uint64_t sw[32];
     __shared__ int handoff;
@@ -574,6 +584,7 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     }
 #pragma unroll
     for (int j = 0; j < WPT; ++j) cw[j * NT + tid] = 0u;
+    reinterpret_cast<uint4*>(rs)[tid] = make_uint4(0u, 0u, 0u, 0u);  // PLEAF / NT = 16 bytes per thread
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const K a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -663,32 +674,53 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
 #pragma unroll
     for (int r = 0; r < E; ++r) {
         const uint32_t i = (uint32_t)r * NT + tid;
-        if (i < len) ix[meta[r] & 0x3FFFu] = (uint16_t)i;
+        if (i < len) {
+            const uint32_t p = meta[r] & 0x3FFFu, c = meta[r] >> 20;
+            ix[p] = (uint16_t)i;
+            if (sh > 0 && ((meta[r] >> 14) & 63u) == 0u && c > 1u) rs[p] = (uint8_t)c;  // slot 0 marks the run
+        }
     }
     __syncthreads();
-    if (sh > 0) {  // final place inside the bucket: smaller keys, ties by scatter slot
+    if (sh > 0) {
+        // keys of one bucket sit in scatter order at [b0, b0 + c): the thread
+        // owning position b0 (16 consecutive positions per thread) sorts that
+        // run of indices by key -- insertion sort, c <= BK_MAX_RUN (a crowded
+        // bin was handed off); runs are disjoint, so no two threads touch the
+        // same index.  Equal keys are equal bytes: their order never shows.
+        const uint4 w4 = reinterpret_cast<const uint4*>(rs)[tid];
+        if ((w4.x | w4.y | w4.z | w4.w) != 0u) {
+            const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-        for (int r = 0; r < E; ++r) {
-            const uint32_t i = (uint32_t)r * NT + tid;
-            const uint32_t c = meta[r] >> 20;
-            if (i < len && c > 1) {
-                const K x = ks[i];
-                const uint32_t p = meta[r] & 0x3FFFu, slot = (meta[r] >> 14) & 63u, b0 = p - slot;
-                uint32_t q = b0;
+            for (int q = 0; q < 4; ++q) {
+                uint32_t w = wv[q];
+                while (w != 0u) {
+                    const int bpos = (__ffs(w) - 1) >> 3;  // lowest nonzero byte
+                    const uint32_t c = (w >> (8 * bpos)) & 0xFFu;
+                    w &= ~(0xFFu << (8 * bpos));
+                    const uint32_t b0 = tid * 16u + (uint32_t)(q * 4 + bpos);
+                    if (c == 2u) {
+                        const uint16_t a = ix[b0], b = ix[b0 + 1];
+                        if (ks[b] < ks[a]) {
+                            ix[b0] = b;
+                            ix[b0 + 1] = a;
+                        }
+                    } else {
 #pragma unroll 1
-                for (uint32_t k = 0; k + 1 < c; ++k) {  // the bucket's other keys (skip its own slot)
-                    const uint32_t m = b0 + k + (k >= slot);
-                    const K y = ks[ix[m]];
-                    q += (y < x) | ((y == x) & (m < p));
+                        for (uint32_t m = 1; m < c; ++m) {
+                            const uint16_t x = ix[b0 + m];
+                            const K kx = ks[x];
+                            uint32_t j = m;
+                            while (j > 0) {
+                                const uint16_t y = ix[b0 + j - 1];
+                                if (!(ks[y] > kx)) break;
+                                ix[b0 + j] = y;
+                                --j;
+                            }
+                            ix[b0 + j] = x;
+                        }
+                    }
                 }
-                meta[r] = (meta[r] & ~0x3FFFu) | q | 0x80000000u;  // moved
             }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < E; ++r) {
-            const uint32_t i = (uint32_t)r * NT + tid;
-            if (i < len && (meta[r] & 0x80000000u)) ix[meta[r] & 0x3FFFu] = (uint16_t)i;
         }
         __syncthreads();
     }
@@ -1128,7 +1160,7 @@ template uint64_t quicksort_workspace_bound<uint64_t>(uint64_t);
 template uint64_t quicksort_workspace_bound<uint32_t>(uint64_t);
 
 template <typename K>
-pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
+static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     using C = GroupCfg<K>;
     using LC = LeafCfg<K>;
     const Params& P = params();
@@ -1201,16 +1233,20 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         bool inflight = false;
         int id = 0;
     };
-    static cudaStream_t lane_st1 = nullptr;
+    static cudaStream_t lane_st1 = nullptr, lane_hi1 = nullptr;
     static cudaEvent_t lane_ev[3] = {nullptr, nullptr, nullptr};
     if (!lane_st1) {
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
         cudaStreamCreateWithFlags(&lane_st1, cudaStreamNonBlocking);
+        cudaStreamCreateWithPriority(&lane_hi1, cudaStreamNonBlocking, greatest);
         for (auto& x : lane_ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
     }
     Lane lanes[2];
     lanes[0].st = st;
     lanes[0].done = lane_ev[0];
-    lanes[1].st = lane_st1;
+    lanes[1].st = P.qs_prio != 0 ? lane_hi1 : lane_st1;
+    cudaStream_t lane_st1_used = lanes[1].st;
     lanes[1].done = lane_ev[1];
     lanes[1].id = 1;
     lanes[0].cur.push_back({0, n, 0, rule_at(0), 0});
@@ -1232,13 +1268,13 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         constexpr int HL = LC::LEAF, HN = HL / LEAF_E;
         if (LEAF > (uint64_t)HL) {  // bins of <= 2 LC::LEAF keys: 1024 threads, one CTA per SM
             constexpr int PL = 2 * HL, BNT = 1024;
-            const size_t smem = sizeof(K) * PL + 4 * PL + 16;
+            const size_t smem = sizeof(K) * PL + 4 * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
             qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
         } else {  // bins of <= LC::LEAF keys: 512 threads, two CTAs per SM
             constexpr int PL = HL, BNT = 512;
-            const size_t smem = sizeof(K) * PL + 4 * PL + 16;
+            const size_t smem = sizeof(K) * PL + 4 * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
             qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
@@ -1653,7 +1689,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         lanes[1].depth = lanes[0].depth;
         c0.resize(cut);
         e = cudaEventRecord(lane_ev[2], st);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(lane_st1, lane_ev[2], 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(lane_st1_used, lane_ev[2], 0);
         if (e != cudaSuccess) return cuda_fail(e, "quicksort lanes");
         if ((ps = launch_level(lanes[0])) != PP_OK) return ps;
         if ((ps = launch_level(lanes[1])) != PP_OK) return ps;
@@ -1669,7 +1705,7 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
             }
         }
         // lane 1's last work precedes whatever follows on `st`
-        e = cudaEventRecord(lane_ev[2], lane_st1);
+        e = cudaEventRecord(lane_ev[2], lane_st1_used);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, lane_ev[2], 0);
         if (e != cudaSuccess) return cuda_fail(e, "quicksort lanes");
     }
@@ -1775,6 +1811,35 @@ pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
         last_stats().aux_bytes = user_workspace(&uw, &ub) ? g_qs_user_base + g_qs_peak : g_qws_bytes;
     }
     return PP_OK;
+}
+
+// Stream priorities (param qs_prio, default on): the level loop -- the
+// critical path -- runs on high-priority streams (lane 0 on an internal one
+// ordered after the caller's stream by events, lane 1 on its own), the early
+// per-CTA recursion and bin sorts stay at the lowest priority, so whenever
+// CTAs of both are pending the SMs that free up go to the level kernels (a
+// 16384-key bin sort holds a whole SM: 208 KiB of shared memory).
+template <typename K>
+pp_status quicksort_device(K* keys, uint64_t n, cudaStream_t st) {
+    if (params().qs_prio == 0) return quicksort_device_impl<K>(keys, n, st);
+    static cudaStream_t hi0 = nullptr;
+    static cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    if (!hi0) {
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        if (cudaStreamCreateWithPriority(&hi0, cudaStreamNonBlocking, greatest) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming) != cudaSuccess)
+            return cuda_fail(cudaGetLastError(), "quicksort priority stream");
+    }
+    cudaError_t e = cudaEventRecord(ev_in, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(hi0, ev_in, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "quicksort priority stream order");
+    const pp_status s = quicksort_device_impl<K>(keys, n, hi0);
+    e = cudaEventRecord(ev_out, hi0);  // whatever the caller enqueues next sees the sorted keys
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_out, 0);
+    if (e != cudaSuccess && s == PP_OK) return cuda_fail(e, "quicksort priority stream join");
+    return s;
 }
 
 template pp_status quicksort_device<uint64_t>(uint64_t*, uint64_t, cudaStream_t);
