@@ -558,33 +558,57 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     static_assert((1 << NBITS) == NB && WPT >= 1 && PLEAF <= (1 << 14), "bin geometry");
     static_assert(BK_MAX_RUN < 64, "bucket size fits the 6-bit field");
     extern __shared__ __align__(16) unsigned char lsm[];
-    K* ks = reinterpret_cast<K*>(lsm);                          // [PLEAF] keys, input order
-    uint32_t* cw = reinterpret_cast<uint32_t*>(ks + PLEAF);     // [NWD + 1] packed counts, then starts
-    uint16_t* ix = reinterpret_cast<uint16_t*>(cw);             // [PLEAF] key indices (after the starts are read)
-    uint8_t* rs = reinterpret_cast<uint8_t*>(cw + NWD + 4);     // [PLEAF] size of the bucket starting here (> 1 only)
-    static_assert(PLEAF / NT == 16, "one 16-byte run-start word per thread");
     __shared__ K rmn[NW], rmx[NW];
     __shared__ uint64_t sw[32];
     __shared__ int handoff;
+    __shared__ __align__(8) uint64_t lbar;
     const K KMAX = (K)~(K)0;
     const uint64_t lo = leaf_lo[blockIdx.x];
     const uint32_t len = leaf_len[blockIdx.x];
     if (len < 2) return;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // the 16-B aligned body of the bin arrives by ONE bulk copy (TMA); the
+    // <= 16 / sizeof(K) - 1 keys before it and after it by plain loads.  The
+    // keys are staged at lsm + 16 - head * sizeof(K) so that the body lands
+    // 16-B aligned too.
+    constexpr uint32_t VK = 16 / sizeof(K);
+    uint32_t head = (uint32_t)(((16u - ((uint32_t)reinterpret_cast<uintptr_t>(keys + lo) & 15u)) & 15u) / sizeof(K));
+    head = head < len ? head : len;
+    const uint32_t nbody = (len - head) / VK * VK, tail0 = head + nbody;
+    K* ks = reinterpret_cast<K*>(lsm + 16) - head;               // [PLEAF] keys, input order
+    uint32_t* cw = reinterpret_cast<uint32_t*>(lsm + 16 + sizeof(K) * PLEAF);  // [NWD + 1] packed counts, then starts
+    uint16_t* ix = reinterpret_cast<uint16_t*>(cw);             // [PLEAF] key indices (after the starts are read)
+    uint8_t* rs = reinterpret_cast<uint8_t*>(cw + NWD + 4);     // [PLEAF] size of the bucket starting here (> 1 only)
+    static_assert(PLEAF / NT == 16, "one 16-byte run-start word per thread");
+    if (tid == 0) {
+        mbar_init(&lbar, 1);
+        fence_mbar_init();
+        if (nbody > 0) {
+            mbar_expect_tx(&lbar, nbody * (uint32_t)sizeof(K));
+            bulk_g2s(ks + head, keys + lo + head, nbody * (uint32_t)sizeof(K), &lbar);
+        }
+    }
+    if (tid < head) ks[tid] = __ldcs(keys + lo + tid);
+    if (tid < len - tail0) ks[tail0 + tid] = __ldcs(keys + lo + tail0 + tid);
+#pragma unroll
+    for (int j = 0; j < WPT; ++j) cw[j * NT + tid] = 0u;
+    reinterpret_cast<uint4*>(rs)[tid] = make_uint4(0u, 0u, 0u, 0u);  // PLEAF / NT = 16 bytes per thread
+    if (tid == 0) {
+        handoff = 0;
+        cw[NWD] = len;  // the end of the last bucket
+    }
+    __syncthreads();  // the barrier is initialised (and the head / tail keys are staged)
+    if (nbody > 0) mbar_wait(&lbar, 0);
     K mn = KMAX, mx = 0;
 #pragma unroll
     for (int r = 0; r < E; ++r) {
         const uint32_t i = (uint32_t)r * NT + tid;
         if (i < len) {
-            const K v = __ldcs(keys + lo + i);
-            ks[i] = v;
+            const K v = ks[i];
             mn = v < mn ? v : mn;
             mx = v > mx ? v : mx;
         }
     }
-#pragma unroll
-    for (int j = 0; j < WPT; ++j) cw[j * NT + tid] = 0u;
-    reinterpret_cast<uint4*>(rs)[tid] = make_uint4(0u, 0u, 0u, 0u);  // PLEAF / NT = 16 bytes per thread
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const K a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -594,10 +618,6 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     if (lane == 0) {
         rmn[warp] = mn;
         rmx[warp] = mx;
-    }
-    if (tid == 0) {
-        handoff = 0;
-        cw[NWD] = len;  // the end of the last bucket
     }
     __syncthreads();
     if (warp == 0) {
@@ -724,11 +744,16 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
         }
         __syncthreads();
     }
+    // gather through the indices; 16-B stores for the aligned body
+    for (uint32_t q = tid; q < nbody / VK; q += NT) {
+        const uint32_t j = head + q * VK;
+        Vec16<K> v;
 #pragma unroll
-    for (int r = 0; r < E; ++r) {
-        const uint32_t j = (uint32_t)r * NT + tid;
-        if (j < len) __stcs(keys + lo + j, ks[ix[j]]);
+        for (int e = 0; e < (int)VK; ++e) v.v[e] = ks[ix[j + e]];
+        __stcs(reinterpret_cast<uint4*>(keys + lo + j), *reinterpret_cast<const uint4*>(&v));
     }
+    if (tid < head) __stcs(keys + lo + tid, ks[ix[tid]]);
+    if (tid < len - tail0) __stcs(keys + lo + tail0 + tid, ks[ix[tail0 + tid]]);
 }
 
 // ===========================================================================
@@ -1263,18 +1288,22 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     // sorts `cnt` bins (lo, len) of <= LEAF keys each, len 0 = empty slot:
     // the index-staged counting sort, then the merge sort of the bins it handed
     // off (crowded buckets)
+    // PP_QS_SKIP (measurement only, the output is then NOT sorted): bit 0
+    // skips the bin sorts, bit 1 the per-CTA recursion and the bin sorts -- the
+    // time the rest takes
+    static const int qs_skip = getenv("PP_QS_SKIP") ? atoi(getenv("PP_QS_SKIP")) : 0;
     auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
-        if (cnt == 0) return cudaSuccess;
+        if (cnt == 0 || (qs_skip & 3)) return cudaSuccess;
         constexpr int HL = LC::LEAF, HN = HL / LEAF_E;
         if (LEAF > (uint64_t)HL) {  // bins of <= 2 LC::LEAF keys: 1024 threads, one CTA per SM
             constexpr int PL = 2 * HL, BNT = 1024;
-            const size_t smem = sizeof(K) * PL + 4 * PL + 16 + PL;
+            const size_t smem = 16 + sizeof(K) * PL + 4 * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
             qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
         } else {  // bins of <= LC::LEAF keys: 512 threads, two CTAs per SM
             constexpr int PL = HL, BNT = 512;
-            const size_t smem = sizeof(K) * PL + 4 * PL + 16 + PL;
+            const size_t smem = 16 + sizeof(K) * PL + 4 * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
             qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
@@ -1291,6 +1320,7 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     auto launch_small = [&](uint64_t cnt, const uint64_t* slo, const uint32_t* sln, const uint64_t* sbase,
                             uint64_t* blo, uint32_t* bln, GroupOut* scr, uint64_t* prof, cudaStream_t s3) {
         using S = SmallCfg<K>;
+        if (qs_skip & 2) return cudaSuccess;  // (measurement only; the bin sorts are skipped too)
         cudaFuncSetAttribute(qs_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
         qs_small_kernel<K><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln, (uint32_t)LEAF,
                                                                   P.seed, scr, prof,
