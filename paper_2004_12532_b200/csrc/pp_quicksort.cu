@@ -567,16 +567,16 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     const uint32_t len = leaf_len[blockIdx.x];
     if (len < 2) return;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // the 16-B aligned body of the bin arrives by ONE bulk copy (TMA); the
-    // <= 16 / sizeof(K) - 1 keys before it and after it by plain loads.  The
-    // keys are staged at lsm + 16 - head * sizeof(K) so that the body lands
-    // 16-B aligned too.
-    constexpr uint32_t VK = 16 / sizeof(K);
-    uint32_t head = (uint32_t)(((16u - ((uint32_t)reinterpret_cast<uintptr_t>(keys + lo) & 15u)) & 15u) / sizeof(K));
+    // the 32-B aligned body of the bin arrives by ONE bulk copy (TMA) and
+    // leaves by 32-B stores; the < 32 / sizeof(K) keys before it and after it
+    // by plain loads / stores.  The keys are staged at lsm + 32 - head *
+    // sizeof(K) so that the body lands aligned in shared memory too.
+    constexpr uint32_t VK = 32 / sizeof(K);
+    uint32_t head = (uint32_t)(((32u - ((uint32_t)reinterpret_cast<uintptr_t>(keys + lo) & 31u)) & 31u) / sizeof(K));
     head = head < len ? head : len;
     const uint32_t nbody = (len - head) / VK * VK, tail0 = head + nbody;
-    K* ks = reinterpret_cast<K*>(lsm + 16) - head;               // [PLEAF] keys, input order
-    uint32_t* cw = reinterpret_cast<uint32_t*>(lsm + 16 + sizeof(K) * PLEAF);  // [NWD + 1] packed counts, then starts
+    K* ks = reinterpret_cast<K*>(lsm + 32) - head;               // [PLEAF] keys, input order
+    uint32_t* cw = reinterpret_cast<uint32_t*>(lsm + 32 + sizeof(K) * PLEAF);  // [NWD + 1] packed counts, then starts
     uint16_t* ix = reinterpret_cast<uint16_t*>(cw);             // [PLEAF] key indices (after the starts are read)
     uint8_t* rs = reinterpret_cast<uint8_t*>(cw + NWD + 4);     // [PLEAF] size of the bucket starting here (> 1 only)
     static_assert(PLEAF / NT == 16, "one 16-byte run-start word per thread");
@@ -648,7 +648,8 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
         meta[r] = 0u;
         if (i < len) {
             const uint32_t d = (uint32_t)((ks[i] - mn) >> sh), hs = (d & 1u) * 16u;
-            meta[r] = (atomicAdd(&cw[d >> 1], 1u << hs) >> hs) & 0xFFFFu;  // the slot (for now)
+            // the slot (14 bits) and the bucket (15 bits), kept for the next phase
+            meta[r] = ((atomicAdd(&cw[d >> 1], 1u << hs) >> hs) & 0xFFFFu) | (d << 16);
         }
     }
     __syncthreads();
@@ -682,11 +683,11 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     for (int r = 0; r < E; ++r) {
         const uint32_t i = (uint32_t)r * NT + tid;
         if (i < len) {
-            const uint32_t d = (uint32_t)((ks[i] - mn) >> sh);
+            const uint32_t d = meta[r] >> 16;
             const uint32_t w = cw[d >> 1];
             const uint32_t b0 = (d & 1u) ? w >> 16 : w & 0xFFFFu;
             const uint32_t b1 = (d & 1u) ? cw[(d >> 1) + 1] & 0xFFFFu : w >> 16;
-            const uint32_t slot = meta[r];
+            const uint32_t slot = meta[r] & 0xFFFFu;
             meta[r] = (b0 + slot) | ((slot & 63u) << 14) | (min(b1 - b0, 63u) << 20);
         }
     }
@@ -744,13 +745,18 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
         }
         __syncthreads();
     }
-    // gather through the indices; 16-B stores for the aligned body
+    // gather through the indices; 32-B stores (STG.256) for the aligned body
     for (uint32_t q = tid; q < nbody / VK; q += NT) {
         const uint32_t j = head + q * VK;
-        Vec16<K> v;
+        union {
+            K k[VK];
+            unsigned long long w[4];
+        } v;
 #pragma unroll
-        for (int e = 0; e < (int)VK; ++e) v.v[e] = ks[ix[j + e]];
-        __stcs(reinterpret_cast<uint4*>(keys + lo + j), *reinterpret_cast<const uint4*>(&v));
+        for (int e = 0; e < (int)VK; ++e) v.k[e] = ks[ix[j + e]];
+        asm volatile("st.global.cs.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(keys + lo + j), "l"(v.w[0]), "l"(v.w[1]),
+                     "l"(v.w[2]), "l"(v.w[3])
+                     : "memory");
     }
     if (tid < head) __stcs(keys + lo + tid, ks[ix[tid]]);
     if (tid < len - tail0) __stcs(keys + lo + tail0 + tid, ks[ix[tail0 + tid]]);
@@ -1297,13 +1303,13 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         constexpr int HL = LC::LEAF, HN = HL / LEAF_E;
         if (LEAF > (uint64_t)HL) {  // bins of <= 2 LC::LEAF keys: 1024 threads, one CTA per SM
             constexpr int PL = 2 * HL, BNT = 1024;
-            const size_t smem = 16 + sizeof(K) * PL + 4 * PL + 16 + PL;
+            const size_t smem = 32 + sizeof(K) * PL + 4 * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
             qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
         } else {  // bins of <= LC::LEAF keys: 512 threads, two CTAs per SM
             constexpr int PL = HL, BNT = 512;
-            const size_t smem = 16 + sizeof(K) * PL + 4 * PL + 16 + PL;
+            const size_t smem = 32 + sizeof(K) * PL + 4 * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
             qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
