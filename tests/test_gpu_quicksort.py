@@ -83,11 +83,13 @@ def test_medium_sizes(pp, dt, mx):
                                     {"qs_lanes": 1}, {"qs_lanes": 2}, {"qs_lanes": 2, "qs_small": 1 << 17},
                                     {"qs_early": 1}, {"qs_early": 1, "qs_lanes": 1}, {"qs_early": 0},
                                     {"qs_deep": 0}, {"qs_deep": 3}, {"qs_deep": 0, "qs_cta_max": 1 << 12},
-                                    {"qs_pivot": 1}, {"qs_pivot": 2}, {"qs_pivot": 2, "qs_cta_max": 1 << 16}])
+                                    {"qs_pivot": 1}, {"qs_pivot": 2}, {"qs_pivot": 2, "qs_cta_max": 1 << 16},
+                                    {"qs_prio": 0}, {"qs_prio": 0, "qs_lanes": 1}])
 def test_qs_parameters(pp, dt, mx, params):
     """Bin sizes (both bin-sort CTA shapes), level balancing, the
-    heavy-segment batched cleanup, the per-CTA recursion and the Strided
-    offsets all give the oracle's sorted output."""
+    heavy-segment batched cleanup, the per-CTA recursion, the Strided
+    offsets and the stream layout without priorities (qs_prio = 0: lane 0
+    on the caller's stream) all give the oracle's sorted output."""
     rng = np.random.default_rng(4)
     for n in (5000, 300_007):
         for a in list(_cases(dt, mx, n, rng))[:3]:
