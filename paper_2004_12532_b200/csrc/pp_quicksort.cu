@@ -775,10 +775,16 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
 // lane per line), 32 KiB sort buffers: 4 CTAs per SM (independent recursions
 // hide each other's latency).  (256-thread / 8 KiB-line and 2-in-flight
 // configurations measured slower in round 1 and were removed.)
+#ifndef PP_SMALL_PF  // A/B builds only (tools/ab_build.py; 3 and 2 measured slower)
+#define PP_SMALL_PF 4
+#endif
+#ifndef PP_SMALL_MINB
+#define PP_SMALL_MINB 4
+#endif
 template <typename K>
 struct SmallCfg {
-    static constexpr int NT = 128, MINB = 4;
-    using GC = GroupCfgT<K, 4096, 128, 4, false, false, true>;
+    static constexpr int NT = 128, MINB = PP_SMALL_MINB;
+    using GC = GroupCfgT<K, 4096, 128, PP_SMALL_PF, false, false, true>;
     static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 2048 : 4096;
     static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);
     static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
@@ -1300,6 +1306,23 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     static const int qs_skip = getenv("PP_QS_SKIP") ? atoi(getenv("PP_QS_SKIP")) : 0;
     auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
         if (cnt == 0 || (qs_skip & 3)) return cudaSuccess;
+        static const bool bin_stats = getenv("PP_QS_BINSTATS") != nullptr;  // measurement only: bin sizes
+        if (bin_stats) {
+            std::vector<uint32_t> h(cnt);
+            cudaStreamSynchronize(bst);
+            cudaMemcpy(h.data(), d_len, 4 * cnt, cudaMemcpyDeviceToHost);
+            uint64_t hist[6] = {0, 0, 0, 0, 0, 0}, keys_in = 0, nonempty = 0;
+            for (uint32_t x : h) {
+                const uint32_t l = x & ~0x80000000u;
+                if (l >= 2) ++nonempty;
+                keys_in += l;
+                hist[l < 2 ? 0 : l <= 2048 ? 1 : l <= 4096 ? 2 : l <= 8192 ? 3 : l <= 12288 ? 4 : 5]++;
+            }
+            fprintf(stderr, "qs bins: slots=%llu nonempty=%llu keys=%llu  <2:%llu <=2K:%llu <=4K:%llu <=8K:%llu <=12K:%llu >12K:%llu\n",
+                    (unsigned long long)cnt, (unsigned long long)nonempty, (unsigned long long)keys_in,
+                    (unsigned long long)hist[0], (unsigned long long)hist[1], (unsigned long long)hist[2],
+                    (unsigned long long)hist[3], (unsigned long long)hist[4], (unsigned long long)hist[5]);
+        }
         constexpr int HL = LC::LEAF, HN = HL / LEAF_E;
         if (LEAF > (uint64_t)HL) {  // bins of <= 2 LC::LEAF keys: 1024 threads, one CTA per SM
             constexpr int PL = 2 * HL, BNT = 1024;
