@@ -23,7 +23,7 @@ import synth  # noqa: E402
 
 
 def family(name):
-    for f in ("qs_pivot", "qs_group", "qs_hv_", "qs_cleanup", "qs_small", "qs_leaf_bidx", "qs_leaf_handoff",
+    for f in ("qs_pivot", "qs_group", "qs_hv_", "qs_cleanup", "qs_small", "qs_cluster", "qs_leaf_bidx", "qs_leaf_handoff",
               "ss_group", "reduce_count", "scan_swap", "qs_seg", "qs_"):
         if f in name:
             return f.rstrip("_")
