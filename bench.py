@@ -395,35 +395,15 @@ def main():
 
     overlap = None
     if dist_on:
-        # the count-first overlapped exchange (param dist_overlap, SURVEY
-        # §8(f) #1): same input, same step bracket, a few steps, max over ranks
-        pp.pp_set_param("dist_overlap", 1)
-        ov_ms, ov_ph, ov_split = [], [], None
-        for i in range(min(args.steps, 5) + 1):
-            restore()
-            sync_all()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(stream)
-            step()
-            e.record(stream)
-            sync_all()
-            if i:  # the first one warms the path up
-                ov_ms.append(s.elapsed_time(e))
-                ov_ph.append(pp.pp_dist_last_timing())
-            ov_split = last_split[0]
-        pp.pp_set_param("dist_overlap", 0)
-        t = torch.tensor(ov_ms, dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ov_ms = [float(x) for x in t.tolist()]
-        loc = [sum(p[f] for p in ov_ph) / len(ov_ph) for f in ("local_ms", "gather_ms", "exchange_ms", "bytes")]
-        tt = torch.tensor(loc, dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        cm, gm2, pxm, xb2 = (float(x) for x in tt.tolist())
-        overlap = {"ms_per_step": sum(ov_ms) / len(ov_ms), "steps": len(ov_ms),
-                   "keys_per_s": n_total / (sum(ov_ms) / len(ov_ms) / 1e3),
-                   "count_ms": cm, "allgather_ms": gm2, "partition_and_exchange_ms": pxm, "bytes_per_gpu": xb2,
-                   "chunks": pp.pp_get_param("dist_chunks"), "split_matches_default": ov_split == last_split[0],
-                   "timing": "same bracket as the timed steps (barrier + synchronize, CUDA events, max over ranks)"}
+        try:
+            main_split = last_split[0]
+            overlap = measure_overlap(pp, torch, dist, dev, stream, args, restore, step, sync_all, last_split, n_total)
+            overlap["split_matches_default"] = overlap.pop("split") == main_split
+            last_split[0] = main_split
+        except Exception as ex:  # an extra: the headline line must still print
+            overlap = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+        finally:
+            pp.pp_set_param("dist_overlap", 0)
 
     value = n_total * args.steps / (tot_ms / 1e3)
     ms_per_step = tot_ms / args.steps
@@ -497,6 +477,39 @@ def main():
         pp.pp_dist_finalize()
         dist.destroy_process_group()
     return 0
+
+
+def measure_overlap(pp, torch, dist, dev, stream, args, restore, step, sync_all, last_split, n_total):
+    """The count-first overlapped exchange (param dist_overlap, SURVEY §8(f)
+    #1) at N > 1: same input, same step bracket, a few steps, max over ranks."""
+    pp.pp_set_param("dist_overlap", 1)
+    ov_ms, ov_ph, ov_split = [], [], None
+    for i in range(min(args.steps, 5) + 1):
+        restore()
+        sync_all()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        step()
+        e.record(stream)
+        sync_all()
+        if i:  # the first one warms the path up
+            ov_ms.append(s.elapsed_time(e))
+            ov_ph.append(pp.pp_dist_last_timing())
+        ov_split = last_split[0]
+    pp.pp_set_param("dist_overlap", 0)
+    default_split = ov_split
+    t = torch.tensor(ov_ms, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ov_ms = [float(x) for x in t.tolist()]
+    loc = [sum(p[f] for p in ov_ph) / len(ov_ph) for f in ("local_ms", "gather_ms", "exchange_ms", "bytes")]
+    tt = torch.tensor(loc, dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    cm, gm2, pxm, xb2 = (float(x) for x in tt.tolist())
+    return {"ms_per_step": sum(ov_ms) / len(ov_ms), "steps": len(ov_ms),
+            "keys_per_s": n_total / (sum(ov_ms) / len(ov_ms) / 1e3),
+            "count_ms": cm, "allgather_ms": gm2, "partition_and_exchange_ms": pxm, "bytes_per_gpu": xb2,
+            "chunks": pp.pp_get_param("dist_chunks"), "split": default_split,
+            "timing": "same bracket as the timed steps (barrier + synchronize, CUDA events, max over ranks)"}
 
 
 def e2e(pp, torch, dist, rank, ws, off, n, args):
