@@ -64,17 +64,24 @@ struct GroupCfgT {
 template <typename K>
 using GroupCfg = GroupCfgT<K, sizeof(K) == 8 ? PP_U64_LINE : PP_U32_LINE, sizeof(K) == 8 ? PP_U64_NT : PP_U32_NT,
                            sizeof(K) == 8 ? PP_U64_PF : PP_U32_PF, false, false, sizeof(K) == 4>;
-// The partition's own group kernel: u32 with 3 lines in flight per end (41 KiB
-// of shared memory: 5 CTAs per SM instead of 4 -- the u32 engine is
-// issue-bound, more resident warps hide more of it): config 4 measured 2-3%
-// faster (1.40 -> 1.37 ms partitioned, 1.43 -> 1.39 alternating / reverse);
-// the quicksort's level kernel keeps GroupCfg (mixed there: -5% median-of-3
-// uniform, +3% duplicate-heavy).
+// The partition's own group kernel for u32: 8 KiB lines (b = 2048 keys), 256
+// threads, 2 lines in flight per end (64 KiB of shared memory, 3 CTAs per
+// SM).  The u32 engine is issue-bound (per-line control and barriers over
+// 1024 keys with 4 KiB lines); twice the keys per line halve that overhead.
+// Config 4 (round 2, profiles/r06_u32_part_configs.txt): 1.37-1.40 ms with
+// 4 KiB / 128 threads / 3 in flight (itself -2-3% from 4 in flight) ->
+// 1.32-1.37 ms.  The quicksort's level kernel keeps GroupCfg.
 #ifndef PP_U32_PART_PF
-#define PP_U32_PART_PF 3
+#define PP_U32_PART_PF 2
+#endif
+#ifndef PP_U32_PART_LINE
+#define PP_U32_PART_LINE 8192
+#endif
+#ifndef PP_U32_PART_NT
+#define PP_U32_PART_NT 256
 #endif
 template <typename K>
-using PartGroupCfg = GroupCfgT<K, sizeof(K) == 8 ? PP_U64_LINE : PP_U32_LINE, sizeof(K) == 8 ? PP_U64_NT : PP_U32_NT,
+using PartGroupCfg = GroupCfgT<K, sizeof(K) == 8 ? PP_U64_LINE : PP_U32_PART_LINE, sizeof(K) == 8 ? PP_U64_NT : PP_U32_PART_NT,
                                sizeof(K) == 8 ? PP_U64_PF : PP_U32_PART_PF, false, false, sizeof(K) == 4>;
 
 // Line index of the j-th line (group order) of group gi: G_i(j) of
