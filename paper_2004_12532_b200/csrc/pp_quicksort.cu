@@ -579,7 +579,8 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     uint32_t* cw = reinterpret_cast<uint32_t*>(lsm + 32 + sizeof(K) * PLEAF);  // [NWD + 1] packed counts, then starts
     uint16_t* ix = reinterpret_cast<uint16_t*>(cw);             // [PLEAF] key indices (after the starts are read)
     uint8_t* rs = reinterpret_cast<uint8_t*>(cw + NWD + 4);     // [PLEAF] size of the bucket starting here (> 1 only)
-    static_assert(PLEAF / NT == 16, "one 16-byte run-start word per thread");
+    constexpr int RW = PLEAF / NT / 16;  // 16-byte run-start words per thread
+    static_assert(RW >= 1 && RW * 16 * NT == PLEAF, "16-byte run-start words per thread");
     if (tid == 0) {
         mbar_init(&lbar, 1);
         fence_mbar_init();
@@ -592,7 +593,8 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     if (tid < len - tail0) ks[tail0 + tid] = __ldcs(keys + lo + tail0 + tid);
 #pragma unroll
     for (int j = 0; j < WPT; ++j) cw[j * NT + tid] = 0u;
-    reinterpret_cast<uint4*>(rs)[tid] = make_uint4(0u, 0u, 0u, 0u);  // PLEAF / NT = 16 bytes per thread
+#pragma unroll
+    for (int j = 0; j < RW; ++j) reinterpret_cast<uint4*>(rs)[tid * RW + j] = make_uint4(0u, 0u, 0u, 0u);
     if (tid == 0) {
         handoff = 0;
         cw[NWD] = len;  // the end of the last bucket
@@ -708,7 +710,9 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
         // run of indices by key -- insertion sort, c <= BK_MAX_RUN (a crowded
         // bin was handed off); runs are disjoint, so no two threads touch the
         // same index.  Equal keys are equal bytes: their order never shows.
-        const uint4 w4 = reinterpret_cast<const uint4*>(rs)[tid];
+#pragma unroll 1
+        for (int rw = 0; rw < RW; ++rw) {
+        const uint4 w4 = reinterpret_cast<const uint4*>(rs)[tid * RW + rw];
         if ((w4.x | w4.y | w4.z | w4.w) != 0u) {
             const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
                     const int bpos = (__ffs(w) - 1) >> 3;  // lowest nonzero byte
                     const uint32_t c = (w >> (8 * bpos)) & 0xFFu;
                     w &= ~(0xFFu << (8 * bpos));
-                    const uint32_t b0 = tid * 16u + (uint32_t)(q * 4 + bpos);
+                    const uint32_t b0 = (tid * RW + rw) * 16u + (uint32_t)(q * 4 + bpos);
                     if (c == 2u) {
                         const uint16_t a = ix[b0], b = ix[b0 + 1];
                         if (ks[b] < ks[a]) {
@@ -743,6 +747,7 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
                 }
             }
         }
+        }  // rw
         __syncthreads();
     }
     // gather through the indices; 32-B stores (STG.256) for the aligned body
@@ -1325,7 +1330,10 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         }
         constexpr int HL = LC::LEAF, HN = HL / LEAF_E;
         if (LEAF > (uint64_t)HL) {  // bins of <= 2 LC::LEAF keys: 1024 threads, one CTA per SM
-            constexpr int PL = 2 * HL, BNT = 1024;
+#ifndef PP_BIN16_NT  // A/B builds only (512 threads x 32 keys measured 6% slower: the bin sort needs the warps)
+#define PP_BIN16_NT 1024
+#endif
+            constexpr int PL = 2 * HL, BNT = PP_BIN16_NT;
             const size_t smem = 32 + sizeof(K) * PL + 4 * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
