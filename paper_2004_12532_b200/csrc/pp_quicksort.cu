@@ -525,6 +525,9 @@ __global__ void __launch_bounds__(NT) qs_leaf_handoff_kernel(K* __restrict__ key
 
 
 constexpr uint32_t BK_MAX_RUN = 48;
+#ifndef PP_BIN_BX  // buckets per bin key slot (A/B builds only: 1 -- 176 KiB, leaves room for a per-CTA recursion CTA -- measured +0.3%)
+#define PP_BIN_BX 2
+#endif
 template <typename K>
 __device__ __forceinline__ int key_bits(K v) {
     return sizeof(K) == 8 ? 64 - __clzll((long long)v) : 32 - __clz((int)v);
@@ -553,8 +556,9 @@ template <typename K, int PLEAF, int NT>
 __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kernel(K* __restrict__ keys,
                                                             const uint64_t* __restrict__ leaf_lo,
                                                             uint32_t* __restrict__ leaf_len) {
-    constexpr int E = PLEAF / NT, NW = NT / 32, NB = 2 * PLEAF, NWD = NB / 2, WPT = NWD / NT;
-    constexpr int NBITS = PLEAF == 16384 ? 15 : PLEAF == 8192 ? 14 : PLEAF == 4096 ? 13 : PLEAF == 2048 ? 12 : 11;
+    constexpr int E = PLEAF / NT, NW = NT / 32, NB = PP_BIN_BX * PLEAF, NWD = NB / 2, WPT = NWD / NT;
+    constexpr int NBITS = (PLEAF == 16384 ? 14 : PLEAF == 8192 ? 13 : PLEAF == 4096 ? 12 : PLEAF == 2048 ? 11 : 10) +
+                          (PP_BIN_BX == 2 ? 1 : 0);
     static_assert((1 << NBITS) == NB && WPT >= 1 && PLEAF <= (1 << 14), "bin geometry");
     static_assert(BK_MAX_RUN < 64, "bucket size fits the 6-bit field");
     extern __shared__ __align__(16) unsigned char lsm[];
@@ -1334,13 +1338,13 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
 #define PP_BIN16_NT 1024
 #endif
             constexpr int PL = 2 * HL, BNT = PP_BIN16_NT;
-            const size_t smem = 32 + sizeof(K) * PL + 4 * PL + 16 + PL;
+            const size_t smem = 32 + sizeof(K) * PL + 2 * PP_BIN_BX * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
             qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
         } else {  // bins of <= LC::LEAF keys: 512 threads, two CTAs per SM
             constexpr int PL = HL, BNT = 512;
-            const size_t smem = 32 + sizeof(K) * PL + 4 * PL + 16 + PL;
+            const size_t smem = 32 + sizeof(K) * PL + 2 * PP_BIN_BX * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
             qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
