@@ -790,10 +790,13 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
 #ifndef PP_SMALL_MINB
 #define PP_SMALL_MINB 4
 #endif
+#ifndef PP_SMALL_LINE  // A/B builds only (8 KiB / 2 in flight: -0.7%, not adopted)
+#define PP_SMALL_LINE 4096
+#endif
 template <typename K>
 struct SmallCfg {
     static constexpr int NT = 128, MINB = PP_SMALL_MINB;
-    using GC = GroupCfgT<K, 4096, 128, PP_SMALL_PF, false, false, true>;
+    using GC = GroupCfgT<K, PP_SMALL_LINE, 128, PP_SMALL_PF, false, false, true>;
     static constexpr uint32_t LEAFC = sizeof(K) == 8 ? 2048 : 4096;
     static constexpr size_t SORT = 2 * (LEAFC + LEAFC / 8) * sizeof(K);
     static constexpr size_t SMEM = GC::SMEM > SORT ? GC::SMEM : SORT;
