@@ -555,7 +555,8 @@ __device__ __forceinline__ int key_bits(K v) {
 template <typename K, int PLEAF, int NT>
 __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kernel(K* __restrict__ keys,
                                                             const uint64_t* __restrict__ leaf_lo,
-                                                            uint32_t* __restrict__ leaf_len) {
+                                                            uint32_t* __restrict__ leaf_len,
+                                                            const uint64_t* __restrict__ leaf_kb) {
     constexpr int E = PLEAF / NT, NW = NT / 32, NB = PP_BIN_BX * PLEAF, NWD = NB / 2, WPT = NWD / NT;
     constexpr int NBITS = (PLEAF == 16384 ? 14 : PLEAF == 8192 ? 13 : PLEAF == 4096 ? 12 : PLEAF == 2048 ? 11 : 10) +
                           (PP_BIN_BX == 2 ? 1 : 0);
@@ -606,6 +607,12 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     __syncthreads();  // the barrier is initialised (and the head / tail keys are staged)
     if (nbody > 0) mbar_wait(&lbar, 0);
     K mn = KMAX, mx = 0;
+    if (leaf_kb) {
+        // key bounds of the bin from the quicksort's pivots (every key in
+        // [kmin, kmax]): no min / max pass over the keys
+        mn = (K)leaf_kb[2 * (uint64_t)blockIdx.x];
+        mx = (K)leaf_kb[2 * (uint64_t)blockIdx.x + 1];
+    } else {
 #pragma unroll
     for (int r = 0; r < E; ++r) {
         const uint32_t i = (uint32_t)r * NT + tid;
@@ -643,6 +650,7 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     __syncthreads();
     mn = rmn[0];
     mx = rmx[0];
+    }
     if (mn == mx) return;
     const int bits = key_bits<K>(mx - mn);
     const int sh = bits > NBITS ? bits - NBITS : 0;
@@ -920,26 +928,29 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
     qs_small_kernel(K* __restrict__ keys, const uint64_t* __restrict__ seg_lo, const uint32_t* __restrict__ seg_len,
                     const uint64_t* __restrict__ slot_base, uint64_t* __restrict__ bin_lo,
                     uint32_t* __restrict__ bin_len, uint32_t leaf, uint64_t seed, GroupOut* __restrict__ scratch,
-                    uint64_t* __restrict__ prof, int ninther) {
+                    uint64_t* __restrict__ prof, int ninther, const uint64_t* __restrict__ seg_kb,
+                    uint64_t* __restrict__ bin_kb) {
     using S = SmallCfg<K>;
     constexpr int DEPTH = 64, LEFT_FIRST_MAX = 40;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ Ctl sc;
     __shared__ uint64_t red[S::NT / 32];
     __shared__ uint64_t st_lo[DEPTH], st_hi[DEPTH], st_p[DEPTH];
+    __shared__ uint64_t st_kmin[DEPTH], st_kmax[DEPTH];  // key bounds of the range (from the pivots above it)
     __shared__ int st_mode[DEPTH];
     __shared__ int sp;
     const K KMAX = (K)~(K)0;
     K* A = reinterpret_cast<K*>(smem);
     K* B = A + lpad(S::LEAFC);
-    // bin state (thread 0 only): open bin [blo, bhi), slots used
-    uint64_t blo = 0, bhi = 0;
+    // bin state (thread 0 only): open bin [blo, bhi) with key bounds [bkmin, bkmax], slots used
+    uint64_t blo = 0, bhi = 0, bkmin = 0, bkmax = 0;
     uint32_t used = 0;
     const uint64_t base = slot_base[blockIdx.x];
     const uint32_t cap = (uint32_t)qs_bin_cap(seg_len[blockIdx.x], leaf);
-    auto push = [&](uint64_t lo, uint64_t hi, int mode, uint64_t p) {  // thread 0
+    auto push = [&](uint64_t lo, uint64_t hi, int mode, uint64_t p, uint64_t kmn, uint64_t kmx) {  // thread 0
         const int s = sp;
         st_lo[s] = lo; st_hi[s] = hi; st_mode[s] = mode; st_p[s] = p;
+        st_kmin[s] = kmn; st_kmax[s] = kmx;
         sp = s + 1;
     };
     auto emit = [&]() {  // thread 0: close the open bin
@@ -947,16 +958,21 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
             if (used < cap) {
                 bin_lo[base + used] = blo;
                 bin_len[base + used] = (uint32_t)(bhi - blo);
+                if (bin_kb) {
+                    bin_kb[2 * (base + used)] = bkmin;
+                    bin_kb[2 * (base + used) + 1] = bkmax;
+                }
                 ++used;
             } else {
-                push(blo, bhi, QM_PIVOT | QM_INCTA, 0);
+                push(blo, bhi, QM_PIVOT | QM_INCTA, 0, bkmin, bkmax);
             }
         }
         blo = bhi = 0;
     };
     if (threadIdx.x == 0) {
         sp = 0;
-        push(seg_lo[blockIdx.x], seg_lo[blockIdx.x] + seg_len[blockIdx.x], QM_PIVOT, 0);
+        push(seg_lo[blockIdx.x], seg_lo[blockIdx.x] + seg_len[blockIdx.x], QM_PIVOT, 0,
+             seg_kb ? seg_kb[2 * (uint64_t)blockIdx.x] : 0, seg_kb ? seg_kb[2 * (uint64_t)blockIdx.x + 1] : (uint64_t)KMAX);
     }
     __syncthreads();
     // optional phase profile (debug, PP_QS_PROF): cycles in pivot / partition / merge sort, counts
@@ -971,6 +987,7 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
         }
         const int top = sp - 1;
         const uint64_t lo = st_lo[top], hi = st_hi[top], pm = st_p[top];
+        const uint64_t kmn = st_kmin[top], kmx = st_kmax[top];
         const int mode = st_mode[top];
         __syncthreads();
         if (threadIdx.x == 0) sp = top;
@@ -978,9 +995,16 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
         const int incta = mode & QM_INCTA;
         if (!incta && len <= leaf) {  // a leaf: into the open bin (thread 0), or a new bin
             if (threadIdx.x == 0 && len > 0) {
-                if (bhi == lo && hi - blo <= leaf) bhi = hi;
-                else if (blo == hi && bhi - lo <= leaf) blo = lo;
-                else { emit(); blo = lo; bhi = hi; }
+                if (bhi == lo && hi - blo <= leaf) {
+                    bhi = hi;
+                    bkmax = kmx > bkmax ? kmx : bkmax;
+                } else if (blo == hi && bhi - lo <= leaf) {
+                    blo = lo;
+                    bkmin = kmn < bkmin ? kmn : bkmin;
+                } else {
+                    emit();
+                    blo = lo; bhi = hi; bkmin = kmn; bkmax = kmx;
+                }
             }
             __syncthreads();
             continue;
@@ -1023,20 +1047,27 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
                                                prof ? pr : nullptr);
         if (prof) { const uint64_t t1 = clock64(); pr[1] += t1 - t0; pr[4] += 1; pr[6] += len; t0 = t1; }
         if (threadIdx.x == 0) {
+            // key bounds of the parts: left keys < p, right keys >= p
+            const uint64_t pu = (uint64_t)p;
             if ((mode & QM_LE) == 0 && k == 0) {
                 // p is the minimum: split by x <= p next (reading R14); all == MAX: final
-                if (p != KMAX) push(lo, hi, QM_LE | incta, (uint64_t)(K)(p + 1));
+                if (p != KMAX) push(lo, hi, QM_LE | incta, (uint64_t)(K)(p + 1), pu, kmx);
             } else if (mode & QM_LE) {
-                push(lo + k, hi, QM_PIVOT | incta, 0);  // [lo, lo+k) is all == p: final, skipped
+                push(lo + k, hi, QM_PIVOT | incta, 0, pu, kmx);  // [lo, lo+k) is all == p - 1: final, skipped
             } else if (incta || sp >= LEFT_FIRST_MAX) {
                 // smaller part first (stack depth <= log2 len from here)
                 const bool left_small = k < len - k;
-                if (left_small) { push(lo + k, hi, QM_PIVOT | incta, 0); push(lo, lo + k, QM_PIVOT | incta, 0); }
-                else { push(lo, lo + k, QM_PIVOT | incta, 0); push(lo + k, hi, QM_PIVOT | incta, 0); }
+                if (left_small) {
+                    push(lo + k, hi, QM_PIVOT | incta, 0, pu, kmx);
+                    push(lo, lo + k, QM_PIVOT | incta, 0, kmn, pu - 1);
+                } else {
+                    push(lo, lo + k, QM_PIVOT | incta, 0, kmn, pu - 1);
+                    push(lo + k, hi, QM_PIVOT | incta, 0, pu, kmx);
+                }
             } else {
                 // left part first: leaves come out in array order
-                push(lo + k, hi, QM_PIVOT, 0);
-                push(lo, lo + k, QM_PIVOT, 0);
+                push(lo + k, hi, QM_PIVOT, 0, pu, kmx);
+                push(lo, lo + k, QM_PIVOT, 0, kmn, pu - 1);
             }
         }
         __syncthreads();
@@ -1202,7 +1233,7 @@ uint64_t quicksort_workspace_bound(uint64_t n) {
     // early per-CTA recursion lists (every small segment, all bin slots), beside the lanes
     const uint64_t s_max = n / (q.LEAF + 1) + 1, slot_max = 2 * (n / q.LEAF) + 6 * s_max + 6;
     const size_t early = al256(8 * s_max) + al256(4 * s_max) + al256(8 * s_max) + al256(sizeof(GroupOut) * s_max) +
-                         al256(8 * slot_max) + al256(4 * slot_max);
+                         al256(8 * slot_max) + al256(4 * slot_max) + al256(16 * s_max) + al256(16 * slot_max);
     return std::max(2 * level + early, lists);  // two level lanes + early lists (quicksort_device), or the final lists
 }
 template uint64_t quicksort_workspace_bound<uint64_t>(uint64_t);
@@ -1228,6 +1259,7 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     struct HSeg {
         uint64_t lo, hi, pivot;
         uint32_t mode, depth;
+        uint64_t kmin, kmax;  // every key of the segment is in [kmin, kmax] (the pivots above it)
     };
     // Deep segments (an adversarial order can make median-of-3 peel off a few
     // keys per level) take the ninther instead (R14 fixes only the default
@@ -1242,9 +1274,11 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     std::vector<uint64_t> leaf_lo, small_lo;
     std::vector<uint32_t> leaf_len, small_len;
     std::vector<uint64_t> small_base_v{0};  // bin-slot offset of each small segment (prefix of qs_bin_cap)
+    std::vector<uint64_t> small_kb;         // key bounds (kmin, kmax) of each small segment
     // segments in (LEAF, SMALL] finish in one CTA each (qs_small_kernel)
     const uint64_t SMALL = geom.SMALL;
-    auto add_child = [&](std::vector<HSeg>& next, uint64_t lo, uint64_t hi, uint32_t depth) {
+    auto add_child = [&](std::vector<HSeg>& next, uint64_t lo, uint64_t hi, uint32_t depth, uint64_t kmin,
+                         uint64_t kmax) {
         const uint64_t len = hi - lo;
         if (len <= 1) return;
         if (len <= LEAF) {
@@ -1257,8 +1291,10 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
             small_lo.push_back(lo);
             small_len.push_back((uint32_t)len);
             small_base_v.push_back(small_base_v.back() + qs_bin_cap(len, LEAF));
+            small_kb.push_back(kmin);
+            small_kb.push_back(kmax);
         } else {
-            next.push_back({lo, hi, 0, rule_at(depth), depth});
+            next.push_back({lo, hi, 0, rule_at(depth), depth, kmin, kmax});
         }
     };
     // The level loop runs in up to two LANES: while some segment takes the
@@ -1298,10 +1334,10 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     cudaStream_t lane_st1_used = lanes[1].st;
     lanes[1].done = lane_ev[1];
     lanes[1].id = 1;
-    lanes[0].cur.push_back({0, n, 0, rule_at(0), 0});
+    lanes[0].cur.push_back({0, n, 0, rule_at(0), 0, 0, (uint64_t)KMAX});
     if (n <= SMALL) {
         lanes[0].cur.clear();
-        add_child(lanes[0].cur, 0, n, 0);
+        add_child(lanes[0].cur, 0, n, 0, 0, (uint64_t)KMAX);
     }
     cudaError_t e;
     cudaFuncSetAttribute(qs_group_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -1316,7 +1352,9 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     // skips the bin sorts, bit 1 the per-CTA recursion and the bin sorts -- the
     // time the rest takes
     static const int qs_skip = getenv("PP_QS_SKIP") ? atoi(getenv("PP_QS_SKIP")) : 0;
-    auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst) -> cudaError_t {
+    // d_kb (optional): key bounds (kmin, kmax) per slot -- the bin sort skips its min / max pass
+    auto sort_bins = [&](const uint64_t* d_lo, const uint32_t* d_len, uint64_t cnt, cudaStream_t bst,
+                         const uint64_t* d_kb = nullptr) -> cudaError_t {
         if (cnt == 0 || (qs_skip & 3)) return cudaSuccess;
         static const bool bin_stats = getenv("PP_QS_BINSTATS") != nullptr;  // measurement only: bin sizes
         if (bin_stats) {
@@ -1344,13 +1382,15 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
             const size_t smem = 32 + sizeof(K) * PL + 2 * PP_BIN_BX * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
+            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len),
+                                                                               d_kb);
         } else {  // bins of <= LC::LEAF keys: 512 threads, two CTAs per SM
             constexpr int PL = HL, BNT = 512;
             const size_t smem = 32 + sizeof(K) * PL + 2 * PP_BIN_BX * PL + 16 + PL;
             cudaFuncSetAttribute(qs_leaf_bidx_kernel<K, PL, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
-            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len));
+            qs_leaf_bidx_kernel<K, PL, BNT><<<(unsigned)cnt, BNT, smem, bst>>>(keys, d_lo, const_cast<uint32_t*>(d_len),
+                                                                               d_kb);
         }
         const size_t msmem = sizeof(K) * lpad_host(2 * HL);
         cudaFuncSetAttribute(qs_leaf_handoff_kernel<K, HL, HN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1362,13 +1402,15 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     };
     // the per-CTA recursion over `cnt` small segments (lists on the device)
     auto launch_small = [&](uint64_t cnt, const uint64_t* slo, const uint32_t* sln, const uint64_t* sbase,
-                            uint64_t* blo, uint32_t* bln, GroupOut* scr, uint64_t* prof, cudaStream_t s3) {
+                            uint64_t* blo, uint32_t* bln, GroupOut* scr, uint64_t* prof, cudaStream_t s3,
+                            const uint64_t* skb = nullptr, uint64_t* bkb = nullptr) {
         using S = SmallCfg<K>;
         if (qs_skip & 2) return cudaSuccess;  // (measurement only; the bin sorts are skipped too)
         cudaFuncSetAttribute(qs_small_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
         qs_small_kernel<K><<<(unsigned)cnt, S::NT, S::SMEM, s3>>>(keys, slo, sln, sbase, blo, bln, (uint32_t)LEAF,
                                                                   P.seed, scr, prof,
-                                                                  P.qs_pivot == 2 ? 2 : (P.qs_deep == 0 || P.qs_pivot == 1) ? 1 : 0);
+                                                                  P.qs_pivot == 2 ? 2 : (P.qs_deep == 0 || P.qs_pivot == 1) ? 1 : 0,
+                                                                  skb, bkb);
         note_launches(1);
         return cudaGetLastError();
     };
@@ -1394,8 +1436,9 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         (uint64_t)(P.qs_early_min > 0 ? P.qs_early_min : (sizeof(K) == 8 ? 4 : 2)) * (uint64_t)sm_count();
     const uint64_t s_max = n / (LEAF + 1) + 1, slot_max = 2 * (n / LEAF) + 6 * s_max + 6;
     const size_t e_sloB = al256(8 * s_max), e_slnB = al256(4 * s_max), e_sbB = al256(8 * s_max);
-    const size_t e_scrB = al256(sizeof(GroupOut) * s_max), e_bloB = al256(8 * slot_max);
-    const size_t earlyB = early ? e_sloB + e_slnB + e_sbB + e_scrB + e_bloB + al256(4 * slot_max) : 0;
+    const size_t e_scrB = al256(sizeof(GroupOut) * s_max), e_bloB = al256(8 * slot_max), e_blnB = al256(4 * slot_max);
+    const size_t e_skbB = al256(16 * s_max), e_bkbB = al256(16 * slot_max);  // key bounds: segments, bins
+    const size_t earlyB = early ? e_sloB + e_slnB + e_sbB + e_scrB + e_bloB + e_blnB + e_skbB + e_bkbB : 0;
     unsigned char* ws_all = static_cast<unsigned char*>(qs_workspace(2 * lane_half + earlyB));
     if (!ws_all) return PP_E_NOMEM;
     unsigned char* ew = ws_all + 2 * lane_half;
@@ -1405,6 +1448,8 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     GroupOut* d_escr = reinterpret_cast<GroupOut*>(ew + e_sloB + e_slnB + e_sbB);
     uint64_t* d_eblo = reinterpret_cast<uint64_t*>(ew + e_sloB + e_slnB + e_sbB + e_scrB);
     uint32_t* d_ebln = reinterpret_cast<uint32_t*>(ew + e_sloB + e_slnB + e_sbB + e_scrB + e_bloB);
+    uint64_t* d_eskb = reinterpret_cast<uint64_t*>(ew + e_sloB + e_slnB + e_sbB + e_scrB + e_bloB + e_blnB);
+    uint64_t* d_ebkb = reinterpret_cast<uint64_t*>(ew + e_sloB + e_slnB + e_sbB + e_scrB + e_bloB + e_blnB + e_skbB);
     static cudaStream_t early_st = nullptr, early_bst = nullptr;  // recursion; bin sorts
     static cudaEvent_t early_ev[64];
     if (!early_st) {
@@ -1424,13 +1469,16 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(d_esbase + b, small_base_v.data() + b, 8 * cnt, cudaMemcpyHostToDevice, early_st);
         if (e == cudaSuccess)
-            e = launch_small(cnt, d_eslo + b, d_esln + b, d_esbase + b, d_eblo, d_ebln, d_escr + b, nullptr, early_st);
+            e = cudaMemcpyAsync(d_eskb + 2 * b, small_kb.data() + 2 * b, 16 * cnt, cudaMemcpyHostToDevice, early_st);
+        if (e == cudaSuccess)
+            e = launch_small(cnt, d_eslo + b, d_esln + b, d_esbase + b, d_eblo, d_ebln, d_escr + b, nullptr, early_st,
+                             d_eskb + 2 * b, d_ebkb);
         cudaEvent_t ev = early_ev[early_nb++ % 64];
         if (e == cudaSuccess) e = cudaEventRecord(ev, early_st);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(early_bst, ev, 0);
         if (e == cudaSuccess)
             e = sort_bins(d_eblo + small_base_v[b], d_ebln + small_base_v[b], small_base_v[en] - small_base_v[b],
-                          early_bst);
+                          early_bst, d_ebkb + 2 * small_base_v[b]);
         return e == cudaSuccess ? PP_OK : cuda_fail(e, "quicksort early small batch");
     };
 
@@ -1716,16 +1764,18 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         L.next.clear();
         auto visit = [&](const HSeg& sg, uint64_t p, uint64_t k) {
             const uint32_t d = sg.depth + 1;
+            // key bounds of the parts: left keys < p, right keys >= p
             if (sg.mode != 1) {
                 if (k == 0) {
                     // p is the segment minimum; split by x <= p next (unless all == MAX)
-                    if ((K)p != KMAX) L.next.push_back({sg.lo, sg.hi, (uint64_t)(K)(p + 1), 1, d});
+                    if ((K)p != KMAX) L.next.push_back({sg.lo, sg.hi, (uint64_t)(K)(p + 1), 1, d, p, sg.kmax});
                 } else {
-                    add_child(L.next, sg.lo, sg.lo + k, d);
-                    add_child(L.next, sg.lo + k, sg.hi, d);
+                    add_child(L.next, sg.lo, sg.lo + k, d, sg.kmin, p - 1);
+                    add_child(L.next, sg.lo + k, sg.hi, d, p, sg.kmax);
                 }
             } else {
-                add_child(L.next, sg.lo + k, sg.hi, d);  // [lo, lo+k) is all equal: final
+                // split by x < sg.pivot (= min + 1): [lo, lo+k) is all equal: final
+                add_child(L.next, sg.lo + k, sg.hi, d, sg.pivot, sg.kmax);
             }
         };
         for (size_t mi = 0; mi < nmid; ++mi) visit(L.cur[L.mid_idx[mi]], L.pivots_h[L.mid_idx[mi]], L.splits_h[mi]);
