@@ -525,9 +525,9 @@ __global__ void __launch_bounds__(NT) qs_leaf_handoff_kernel(K* __restrict__ key
 
 
 constexpr uint32_t BK_MAX_RUN = 48;
-#ifndef PP_BIN_BX  // buckets per bin key slot (A/B builds only: 1 -- 176 KiB, leaves room for a per-CTA recursion CTA -- measured +0.3%)
+// buckets per key slot of a bin (1 -- 176 KiB, room for a co-resident per-CTA
+// recursion CTA -- measured +0.3%; 2 also leaves the run list its space)
 #define PP_BIN_BX 2
-#endif
 template <typename K>
 __device__ __forceinline__ int key_bits(K v) {
     return sizeof(K) == 8 ? 64 - __clzll((long long)v) : 32 - __clz((int)v);
@@ -566,6 +566,7 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     __shared__ K rmn[NW], rmx[NW];
     __shared__ uint64_t sw[32];
     __shared__ int handoff;
+    __shared__ uint32_t nruns;  // runs of >= 3 keys listed for pass B of the run sort
     __shared__ __align__(8) uint64_t lbar;
     const K KMAX = (K)~(K)0;
     const uint64_t lo = leaf_lo[blockIdx.x];
@@ -602,6 +603,7 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     for (int j = 0; j < RW; ++j) reinterpret_cast<uint4*>(rs)[tid * RW + j] = make_uint4(0u, 0u, 0u, 0u);
     if (tid == 0) {
         handoff = 0;
+        nruns = 0u;
         cw[NWD] = len;  // the end of the last bucket
     }
     __syncthreads();  // the barrier is initialised (and the head / tail keys are staged)
@@ -717,49 +719,59 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
     }
     __syncthreads();
     if (sh > 0) {
-        // keys of one bucket sit in scatter order at [b0, b0 + c): the thread
-        // owning position b0 (16 consecutive positions per thread) sorts that
-        // run of indices by key -- insertion sort, c <= BK_MAX_RUN (a crowded
-        // bin was handed off); runs are disjoint, so no two threads touch the
-        // same index.  Equal keys are equal bytes: their order never shows.
+        // keys of one bucket sit in scatter order at [b0, b0 + c): sort each
+        // such run of indices by key (runs are disjoint; equal keys are equal
+        // bytes, their order never shows).  Pass A: the thread owning position
+        // b0 (16 consecutive positions per thread) orders every run of TWO
+        // with one predicated compare-exchange; runs of >= 3 (c <= BK_MAX_RUN:
+        // a crowded bin was handed off) are appended to a list in the
+        // counters' free second half.  Pass B: the list, one run per thread,
+        // insertion sort -- so a warp's lanes never idle behind one lane's
+        // long run.
+        static_assert(PP_BIN_BX == 2, "the run list lives in the counters' second half");
+        uint32_t* runs = cw + NWD / 2;  // ix takes the first half; room for PLEAF runs
 #pragma unroll 1
         for (int rw = 0; rw < RW; ++rw) {
-        const uint4 w4 = reinterpret_cast<const uint4*>(rs)[tid * RW + rw];
-        if ((w4.x | w4.y | w4.z | w4.w) != 0u) {
-            const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+            const uint4 w4 = reinterpret_cast<const uint4*>(rs)[tid * RW + rw];
+            if ((w4.x | w4.y | w4.z | w4.w) != 0u) {
+                const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t w = wv[q];
-                while (w != 0u) {
-                    const int bpos = (__ffs(w) - 1) >> 3;  // lowest nonzero byte
-                    const uint32_t c = (w >> (8 * bpos)) & 0xFFu;
-                    w &= ~(0xFFu << (8 * bpos));
-                    const uint32_t b0 = (tid * RW + rw) * 16u + (uint32_t)(q * 4 + bpos);
-                    if (c == 2u) {
-                        const uint16_t a = ix[b0], b = ix[b0 + 1];
-                        if (ks[b] < ks[a]) {
-                            ix[b0] = b;
-                            ix[b0 + 1] = a;
-                        }
-                    } else {
-#pragma unroll 1
-                        for (uint32_t m = 1; m < c; ++m) {
-                            const uint16_t x = ix[b0 + m];
-                            const K kx = ks[x];
-                            uint32_t j = m;
-                            while (j > 0) {
-                                const uint16_t y = ix[b0 + j - 1];
-                                if (!(ks[y] > kx)) break;
-                                ix[b0 + j] = y;
-                                --j;
+                for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                    for (int bb = 0; bb < 4; ++bb) {
+                        const uint32_t c = (wv[q] >> (8 * bb)) & 0xFFu;
+                        const uint32_t b0 = (tid * RW + rw) * 16u + (uint32_t)(q * 4 + bb);
+                        if (c == 2u) {
+                            const uint16_t a = ix[b0], b = ix[b0 + 1];
+                            if (ks[b] < ks[a]) {
+                                ix[b0] = b;
+                                ix[b0 + 1] = a;
                             }
-                            ix[b0 + j] = x;
+                        } else if (c > 2u) {
+                            runs[atomicAdd(&nruns, 1u)] = b0 | (c << 16);
                         }
                     }
                 }
             }
         }
-        }  // rw
+        __syncthreads();
+        const uint32_t nr = nruns;
+        for (uint32_t r = tid; r < nr; r += NT) {
+            const uint32_t b0 = runs[r] & 0xFFFFu, c = runs[r] >> 16;
+#pragma unroll 1
+            for (uint32_t m = 1; m < c; ++m) {
+                const uint16_t x = ix[b0 + m];
+                const K kx = ks[x];
+                uint32_t j = m;
+                while (j > 0) {
+                    const uint16_t y = ix[b0 + j - 1];
+                    if (!(ks[y] > kx)) break;
+                    ix[b0 + j] = y;
+                    --j;
+                }
+                ix[b0 + j] = x;
+            }
+        }
         __syncthreads();
     }
     // gather through the indices; 32-B stores (STG.256) for the aligned body
