@@ -322,7 +322,12 @@ pp_status pp_quicksort_last_stats(uint64_t *out6);
  * of 31 evenly spaced keys: better balanced splits, fewer levels; also the
  * distributed quicksort's rule for segments spanning ranks), "qs_deep" (segments deeper
  * than this take Tukey's ninther instead of the median of 3; -1 auto =
- * 2 log2(n) + 16, 0 = always); "host_chunk", "bps_nt";
+ * 2 log2(n) + 16, 0 = always), "qs_dev" (1: once a lane's segments are all
+ * below qs_heavy, every next level's segment list is built on the device by
+ * one kernel -- children, group counts, longest-first order compacted by
+ * scans -- and two levels per lane are in flight without a host round trip;
+ * default 0: the host builds each level, measured 0.2-2% faster because the
+ * two lanes already hide its work); "host_chunk", "bps_nt";
  * multi-GPU: "dist_p2p", "dist_timeout_ms", "dist_small" (distributed
  * quicksort: spanning segments of <= this many keys are gathered and sorted
  * locally), "dist_overlap" (1: pp_partition_dist counts every chunk of the

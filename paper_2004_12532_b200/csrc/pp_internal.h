@@ -74,6 +74,10 @@ struct Params {
     int64_t qs_prio = -1;          // quicksort: level loop on high-priority streams, early recursion / bins low
                                    // (-1 auto = on, 0 off, 1 on)
     int64_t qs_heavy = 1 << 22;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
+    int64_t qs_dev = 0;            // quicksort: 1 = levels whose segments are all < qs_heavy are built on the
+                                   // device (qs_build_kernel), two levels in flight per lane; 0 (default) = the
+                                   // host builds every level (measured 0.2-2% faster: the two lanes already hide
+                                   // the host's work, the builder's ~13 us sit on a lane's critical path)
 };
 Params& params();
 

@@ -40,7 +40,14 @@ struct QSeg {
     uint32_t mode;     // 0: pivot = median-of-3 (computed on device); 1: pivot given (x <= p step);
                        // 2: pivot = ninther; 3: median of 31 samples (computed on device; param
                        // qs_pivot, and segments deeper than QS_DEEP take at least the ninther)
-    uint32_t pad;
+    uint32_t pad;      // device-built levels (qs_dev): the segment's depth
+};
+
+// Counts of a device-built level list (qs_dev): the kernels of the level read
+// them instead of launch arguments, so the host can enqueue the level before
+// the list exists (grids are host-side upper bounds; surplus CTAs exit).
+struct QDevCtl {
+    uint64_t nmid, gtot, err, pad;
 };
 
 template <typename K>
@@ -87,8 +94,9 @@ __global__ void qs_sample_kernel(const K* __restrict__ keys, QsSamplePos pos, in
 
 template <typename K>
 __global__ void __launch_bounds__(256) qs_pivot_kernel(const K* __restrict__ keys, QSeg* __restrict__ segs,
-                                                       uint64_t nseg) {
+                                                       uint64_t nseg, const QDevCtl* __restrict__ dc = nullptr) {
     const int lane = threadIdx.x & 31;
+    if (dc) nseg = dc->nmid;
     for (uint64_t s = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nseg;
          s += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
         const QSeg q = segs[s];  // uniform over the warp
@@ -119,11 +127,16 @@ __device__ __forceinline__ uint64_t seg_head(const K* keys, uint64_t lo, uint64_
 template <typename K>
 __global__ void __launch_bounds__(GroupCfg<K>::NT) qs_group_kernel(K* __restrict__ keys,
                                                                    const QSeg* __restrict__ segs, uint64_t nseg,
-                                                                   uint64_t seed, GroupOut* __restrict__ gout) {
+                                                                   uint64_t seed, GroupOut* __restrict__ gout,
+                                                                   const QDevCtl* __restrict__ dc = nullptr) {
     extern __shared__ __align__(128) unsigned char smem[];
     using C = GroupCfg<K>;
     griddep_wait();  // PDL launch: the pivots come from qs_pivot_kernel
     const uint64_t task = blockIdx.x;
+    if (dc) {  // device-built level: the grid is an upper bound
+        if (task >= dc->gtot) return;
+        nseg = dc->nmid;
+    }
     // segment of this task: last s with gbase <= task
     uint64_t lo = 0, hi = nseg;
     while (hi - lo > 1) {
@@ -143,10 +156,12 @@ __global__ void __launch_bounds__(GroupCfg<K>::NT) qs_group_kernel(K* __restrict
 template <typename K, int NT, int EPT>
 __global__ void __launch_bounds__(NT) qs_cleanup_kernel(K* __restrict__ keys, const QSeg* __restrict__ segs,
                                                          const GroupOut* __restrict__ gout,
-                                                         uint64_t* __restrict__ splits, uint64_t heavy) {
+                                                         uint64_t* __restrict__ splits, uint64_t heavy,
+                                                         const QDevCtl* __restrict__ dc = nullptr) {
     using C = GroupCfg<K>;
     extern __shared__ __align__(16) unsigned char csm[];
     griddep_wait();  // PDL launch: gout comes from qs_group_kernel
+    if (dc && blockIdx.x >= dc->nmid) return;  // device-built level: the grid is an upper bound
     if (heavy && segs[blockIdx.x].hi - segs[blockIdx.x].lo >= heavy) return;  // batched multi-CTA cleanup
     StreamBuf<NT, EPT>& sb = *reinterpret_cast<StreamBuf<NT, EPT>*>(csm);
     __shared__ uint64_t red[4][NT / 32];
@@ -288,6 +303,300 @@ __global__ void __launch_bounds__(SW_NT, 3) qs_hv_swap_kernel(K* __restrict__ ke
                  HV_PTR(uint64_t, rk), blockIdx.x, gridDim.x);
 }
 #undef HV_PTR
+
+// ---------------------------------------------------------------------------
+// Device-built levels (param qs_dev; SURVEY §8(a) a9 "next-level segment list
+// compacted by scan"): one CTA turns a level's list, its pivots and its splits
+// into the next level's list of mid segments -- the same children (P:1701-1732
+// with reading R14's x <= p step), group counts, straggler take-back and
+// longest-first order as the host loop (launch_level / finish_level) -- so the
+// host can enqueue the next level before this one has run.  Small and leaf
+// children stay with the host, which reads every level back one level behind
+// (their per-CTA recursion and bin sorts run on other streams anyway).
+// Deterministic: block scans and a stable per-warp counting sort, no atomics.
+// ---------------------------------------------------------------------------
+struct QBuildArgs {
+    uint64_t small;     // mid children are longer than this (SMALL)
+    uint64_t g_target;  // G_TARGET
+    uint64_t minl;      // MINL: at least this many lines per group
+    uint64_t slots;     // G_TARGET / qs_waves: CTA slots of one wave
+    uint64_t nmax;      // capacity of the next list (<= QB_NMAX)
+    uint32_t rule;      // level pivot rule (QSeg.mode of new segments) ...
+    uint32_t deep;      // ... and the depth past which median of 3 becomes the ninther
+};
+constexpr int QB_NT = 1024, QB_NW = QB_NT / 32, QB_NBK = 512;
+constexpr uint64_t QB_NMAX = (uint64_t)QB_NBK * QB_NW;  // histogram entries; lists of <= QB_NMAX / 2 (shared memory)
+
+// exclusive scan of one value per thread over the CTA; *tot = the sum
+__device__ __forceinline__ uint64_t qb_scan(uint64_t v, uint64_t* wsum, uint64_t* tot) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint64_t z = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += y;
+        }
+        wsum[lane] = z;
+    }
+    __syncthreads();
+    const uint64_t r = x - v + (w ? wsum[w - 1] : 0);
+    *tot = wsum[QB_NW - 1];
+    __syncthreads();
+    return r;
+}
+
+// maximum over the CTA
+__device__ __forceinline__ uint64_t qb_max(uint64_t v, uint64_t* wsum) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, (uint64_t)__shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) wsum[w] = v;
+    __syncthreads();
+    uint64_t r = 0;
+#pragma unroll 8
+    for (int i = 0; i < QB_NW; ++i) r = max(r, wsum[i]);
+    __syncthreads();
+    return r;
+}
+
+struct QChild {
+    uint64_t lo, hi, pivot, kmin, kmax;
+    uint32_t mode;
+};
+// the mid children of one segment (host: finish_level's visit + add_child)
+template <typename K>
+__device__ __forceinline__ int qb_children(const QSeg& q, uint64_t k, uint64_t kmin, uint64_t kmax,
+                                           const QBuildArgs& a, QChild (&c)[2]) {
+    const K KMAX = (K)~(K)0;
+    const uint32_t d = q.pad + 1;
+    const uint32_t mrule = (d > a.deep && a.rule == 0) ? 2u : a.rule;
+    int n = 0;
+    auto add = [&](uint64_t lo, uint64_t hi, uint64_t kmn, uint64_t kmx) {
+        if (hi - lo > a.small) c[n++] = QChild{lo, hi, 0, kmn, kmx, mrule};
+    };
+    const uint64_t p = q.pivot;
+    if (q.mode != 1) {
+        if (k == 0) {
+            // p is the segment minimum: split by x <= p next (unless all == MAX)
+            if ((K)p != KMAX) c[n++] = QChild{q.lo, q.hi, (uint64_t)(K)(p + 1), p, kmax, 1u};
+        } else {
+            add(q.lo, q.lo + k, kmin, p - 1);  // keys < p
+            add(q.lo + k, q.hi, p, kmax);      // keys >= p
+        }
+    } else {
+        add(q.lo + k, q.hi, q.pivot, kmax);  // [lo, lo+k) is all equal: final
+    }
+    return n;
+}
+
+__device__ __forceinline__ uint32_t qb_bucket(uint64_t nl, uint64_t g) {  // host: launch_level's LPT buckets
+    const uint64_t lpg = max((uint64_t)1, (nl << 10) / g);
+    const int oct = 63 - __clzll((long long)lpg);
+    const int sub = oct >= 3 ? (int)((lpg >> (oct - 3)) & 7) : (int)((lpg << (3 - oct)) & 7);
+    return (uint32_t)(QB_NBK - 1 - (oct * 8 + sub));
+}
+
+template <typename K>
+__global__ void __launch_bounds__(QB_NT) qs_build_kernel(const K* __restrict__ keys, const QSeg* __restrict__ cur,
+                                                         const uint64_t* __restrict__ ckb,
+                                                         const QDevCtl* __restrict__ cc,
+                                                         const uint64_t* __restrict__ splits, QSeg* tmp,
+                                                         uint64_t* tkb, QSeg* __restrict__ nxt,
+                                                         uint64_t* __restrict__ nkb, QDevCtl* __restrict__ nc,
+                                                         QBuildArgs a) {
+    using C = GroupCfg<K>;
+    extern __shared__ __align__(16) uint32_t qbs[];
+    uint32_t* hist = qbs;                 // [QB_NBK][QB_NW] counts, then offsets; later g by list position
+    uint32_t* pos = qbs + QB_NMAX;        // per child: rank in its warp's bucket, then its list position
+    uint32_t* gs = pos + a.nmax;          // per child: groups
+    uint32_t* nls = gs + a.nmax;          // per child: lines of its aligned region
+    __shared__ uint64_t wsum[QB_NW];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const uint64_t N = cc->nmid;
+    // 1. mid children of this thread's segments (contiguous runs: list order), compacted by a scan
+    const uint64_t ipt = (N + QB_NT - 1) / QB_NT;
+    const uint64_t s0 = min(N, (uint64_t)t * ipt), s1 = min(N, s0 + ipt);
+    uint64_t cnt = 0;
+    for (uint64_t i = s0; i < s1; ++i) {
+        QChild c[2];
+        cnt += qb_children<K>(cur[i], splits[i], ckb[2 * i], ckb[2 * i + 1], a, c);
+    }
+    uint64_t M = 0;
+    uint64_t off = qb_scan(cnt, wsum, &M);
+    if (M > a.nmax) {  // impossible: mid children are disjoint and longer than SMALL
+        if (t == 0) *nc = QDevCtl{0, 0, 1, 0};
+        return;
+    }
+    uint64_t lines = 0;
+    for (uint64_t i = s0; i < s1; ++i) {
+        QChild c[2];
+        const QSeg q = cur[i];
+        const int m = qb_children<K>(q, splits[i], ckb[2 * i], ckb[2 * i + 1], a, c);
+        for (int j = 0; j < m; ++j, ++off) {
+            const uint64_t len = c[j].hi - c[j].lo;
+            const uint64_t nl = (len - seg_head<K>(keys, c[j].lo, len)) / C::LK;  // lines of the aligned region
+            QSeg x;
+            x.lo = c[j].lo;
+            x.hi = c[j].hi;
+            x.pivot = c[j].pivot;
+            x.gbase = nl;  // (lines until the list is ordered)
+            x.g = 0;
+            x.mode = c[j].mode;
+            x.pad = q.pad + 1;
+            tmp[off] = x;
+            tkb[2 * off] = c[j].kmin;
+            tkb[2 * off + 1] = c[j].kmax;
+            nls[off] = (uint32_t)nl;
+            lines += nl;
+        }
+    }
+    uint64_t mid_lines = 0;
+    qb_scan(lines, wsum, &mid_lines);  // (its barriers publish tmp to the CTA)
+    // 2. groups per child: round(lines / L*) within [1, lines / MINL], L* = lines of the level / G_TARGET
+    const double Lstar = fmax(1.0, (double)mid_lines / (double)a.g_target);
+    uint64_t gsum = 0;
+    for (uint64_t j = t; j < M; j += QB_NT) {
+        const uint64_t nl = nls[j];
+        const uint64_t cap = max((uint64_t)1, nl / a.minl);
+        const uint64_t want = (uint64_t)((double)nl / Lstar + 0.5);
+        const uint64_t g = max((uint64_t)1, min(cap, want));
+        gs[j] = (uint32_t)g;
+        gsum += g;
+    }
+    uint64_t gtot = 0;
+    qb_scan(gsum, wsum, &gtot);
+    // 3. a few CTAs past a whole number of waves: take them back round robin over
+    //    the children by groups, descending (ties: list order), as the host does.
+    //    Pass r takes one from every child with g >= r + 2, so R full passes and
+    //    then the first m children of that order (all have g >= R + 2).
+    const uint64_t excess = gtot > a.slots ? gtot % a.slots : 0;
+    if (excess > 0 && excess <= a.slots / 16) {
+        uint64_t left = excess, R = 0, m = 0;
+        for (;;) {
+            uint64_t c = 0, cr = 0;
+            for (uint64_t j = t; j < M; j += QB_NT) c += gs[j] >= R + 2 ? 1 : 0;
+            qb_scan(c, wsum, &cr);
+            if (cr == 0) break;         // nothing left to take (the host's loop ends there too)
+            if (cr >= left) { m = left; break; }
+            left -= cr;
+            ++R;
+        }
+        // the m-th largest g (Gs) and the children above it (above < m)
+        uint64_t Gs = 0, above = 0;
+        if (m > 0) {
+            uint64_t lo = R + 2, hi = 1;  // count(g >= lo) >= m holds; find the largest such lo
+            uint64_t gm = 0;
+            for (uint64_t j = t; j < M; j += QB_NT) gm = max(gm, (uint64_t)gs[j]);
+            hi = qb_max(gm, wsum) + 1;  // count(g >= hi) = 0 < m
+            while (hi - lo > 1) {
+                const uint64_t mid = (lo + hi) >> 1;
+                uint64_t c = 0, cm = 0;
+                for (uint64_t j = t; j < M; j += QB_NT) c += gs[j] >= mid ? 1 : 0;
+                qb_scan(c, wsum, &cm);
+                if (cm >= m) lo = mid; else hi = mid;
+            }
+            Gs = lo;
+            uint64_t c = 0;
+            for (uint64_t j = t; j < M; j += QB_NT) c += gs[j] > Gs ? 1 : 0;
+            qb_scan(c, wsum, &above);
+        }
+        // ties at Gs in list order: contiguous runs per thread for the scan
+        const uint64_t ipm = (M + QB_NT - 1) / QB_NT;
+        const uint64_t j0 = min(M, (uint64_t)t * ipm), j1 = min(M, j0 + ipm);
+        uint64_t ties = 0, tot = 0;
+        for (uint64_t j = j0; j < j1; ++j) ties += (m > 0 && gs[j] == Gs) ? 1 : 0;
+        uint64_t trank = qb_scan(ties, wsum, &tot);
+        uint64_t dsum = 0;
+        for (uint64_t j = j0; j < j1; ++j) {
+            const uint64_t g = gs[j];
+            uint64_t dec = min(R, g - 1);
+            if (m > 0 && (g > Gs || (g == Gs && trank++ < m - above))) dec += 1;
+            gs[j] = (uint32_t)(g - dec);
+            dsum += dec;
+        }
+        uint64_t dtot = 0;
+        qb_scan(dsum, wsum, &dtot);
+        gtot -= dtot;
+    }
+    // 4. longest-first order: stable counting sort by bucket of lines per group
+    //    (each warp owns a contiguous run of children and its own histogram row)
+    for (uint64_t e = t; e < QB_NMAX; e += QB_NT) hist[e] = 0;
+    __syncthreads();
+    const uint64_t ipw = (M + QB_NW - 1) / QB_NW;
+    const uint64_t w0 = min(M, (uint64_t)w * ipw), w1 = min(M, w0 + ipw);
+    for (uint64_t b = w0; b < w1; b += 32) {
+        const uint64_t j = b + lane;
+        const bool act = j < w1;
+        const uint32_t bk = act ? qb_bucket(nls[j], gs[j]) : 0xffffffffu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+        uint32_t base = 0;
+        if (act) base = hist[bk * QB_NW + w];
+        __syncwarp();
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1));
+        if (act && rank == 0) hist[bk * QB_NW + w] = base + __popc(peers);
+        __syncwarp();
+        if (act) pos[j] = base + rank;
+    }
+    __syncthreads();
+    {   // bucket-major, warp-minor offsets
+        constexpr int EPT = (int)(QB_NMAX / QB_NT);
+        uint32_t loc[EPT];
+        uint64_t sum = 0;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+            loc[i] = hist[t * EPT + i];
+            sum += loc[i];
+        }
+        uint64_t tot = 0;
+        uint64_t ex = qb_scan(sum, wsum, &tot);
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+            hist[t * EPT + i] = (uint32_t)ex;
+            ex += loc[i];
+        }
+    }
+    __syncthreads();
+    for (uint64_t b = w0; b < w1; b += 32) {
+        const uint64_t j = b + lane;
+        if (j < w1) pos[j] += hist[qb_bucket(nls[j], gs[j]) * QB_NW + w];
+    }
+    __syncthreads();
+    // 5. first task of each child: exclusive scan of g in list order (hist now holds g by position)
+    for (uint64_t j = t; j < M; j += QB_NT) hist[pos[j]] = gs[j];
+    __syncthreads();
+    {
+        const uint64_t ipm = (M + QB_NT - 1) / QB_NT;
+        const uint64_t j0 = min(M, (uint64_t)t * ipm), j1 = min(M, j0 + ipm);
+        uint64_t sum = 0, tot = 0;
+        for (uint64_t j = j0; j < j1; ++j) sum += hist[j];
+        uint64_t ex = qb_scan(sum, wsum, &tot);
+        for (uint64_t j = j0; j < j1; ++j) {
+            const uint32_t g = hist[j];
+            hist[j] = (uint32_t)ex;
+            ex += g;
+        }
+    }
+    __syncthreads();
+    for (uint64_t j = t; j < M; j += QB_NT) {
+        const uint32_t d = pos[j];
+        QSeg x = tmp[j];
+        x.g = gs[j];
+        x.gbase = hist[d];
+        nxt[d] = x;
+        nkb[2 * (uint64_t)d] = tkb[2 * j];
+        nkb[2 * (uint64_t)d + 1] = tkb[2 * j + 1];
+    }
+    if (t == 0) *nc = QDevCtl{M, gtot, 0, 0};
+}
 
 // Leaf sort: one CTA sorts one segment of <= LEAF keys with a bitonic
 // network (padding with the maximum key, never stored back).  Each thread
@@ -1231,6 +1540,29 @@ static size_t qs_level_bound(uint64_t n) {  // one level's region (any level, an
     return al256(al256(sizeof(QSeg) * nmid) + al256(sizeof(GroupOut) * gtot) + al256(8 * (nmid + nbig + 1)) +
                  al256(4 * (nh + 1)) + hv_layout().stride * nh);
 }
+// Device-built levels (qs_dev): per lane, two level lists and their key
+// bounds (ping-pong), the builder's scratch list, two count blocks, the group
+// outputs and the splits; pinned: one readback per list parity.
+struct QDevLayout {
+    size_t listB, kbB, goutB, splB, laneB, pinParB, pinB;
+};
+template <typename K>
+static QDevLayout qdev_layout(uint64_t nm, uint64_t g_target) {
+    QDevLayout D;
+    D.listB = al256(sizeof(QSeg) * nm);
+    D.kbB = al256(16 * nm);
+    D.goutB = al256(sizeof(GroupOut) * (g_target + nm + 2));
+    D.splB = al256(8 * nm);
+    D.laneB = 3 * D.listB + 3 * D.kbB + 256 + D.goutB + D.splB;
+    D.pinParB = D.listB + D.kbB + D.splB + 256;
+    D.pinB = 2 * D.pinParB + 256;
+    return D;
+}
+template <typename K>
+static bool qdev_on(uint64_t n) {  // param qs_dev (default off) and a list that fits the builder
+    const QsGeom q = qs_geom<K>();
+    return params().qs_dev != 0 && n / (q.SMALL + 1) + 1 <= QB_NMAX / 2 && q.SMALL >= q.LEAF;
+}
 template <typename K>
 uint64_t quicksort_workspace_bound(uint64_t n) {
     const QsGeom q = qs_geom<K>();
@@ -1246,7 +1578,9 @@ uint64_t quicksort_workspace_bound(uint64_t n) {
     const uint64_t s_max = n / (q.LEAF + 1) + 1, slot_max = 2 * (n / q.LEAF) + 6 * s_max + 6;
     const size_t early = al256(8 * s_max) + al256(4 * s_max) + al256(8 * s_max) + al256(sizeof(GroupOut) * s_max) +
                          al256(8 * slot_max) + al256(4 * slot_max) + al256(16 * s_max) + al256(16 * slot_max);
-    return std::max(2 * level + early, lists);  // two level lanes + early lists (quicksort_device), or the final lists
+    const size_t dev = qdev_on<K>(n) ? 2 * qdev_layout<K>(n / (q.SMALL + 1) + 1, q.G_TARGET).laneB : 0;
+    // two level lanes + early lists + device-built lanes (quicksort_device), or the final lists
+    return std::max(2 * level + early + dev, lists);
 }
 template uint64_t quicksort_workspace_bound<uint64_t>(uint64_t);
 template uint64_t quicksort_workspace_bound<uint32_t>(uint64_t);
@@ -1329,6 +1663,13 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         uint64_t nmid = 0, nbig = 0, gtot = 0, depth = 0;
         bool inflight = false;
         int id = 0;
+        // device-built levels (qs_dev): up to two levels in flight, oldest first
+        bool dev = false;
+        int dq = 0;
+        int qpar[2] = {0, 1};           // list parity of each level in flight
+        uint64_t qexact = 0;            // segments of the oldest level in flight (the host knows it exactly)
+        unsigned char* dreg = nullptr;  // device region (QDevLayout)
+        unsigned char* dpin = nullptr;  // pinned readbacks
     };
     static cudaStream_t lane_st1 = nullptr, lane_hi1 = nullptr;
     static cudaEvent_t lane_ev[3] = {nullptr, nullptr, nullptr};
@@ -1432,10 +1773,16 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     const uint64_t nh_max = HEAVY ? n / HEAVY + 1 : 1;
     const size_t pin_sB = al256(sizeof(QSeg) * nmid_max), pin_spB = al256(8 * (nmid_max + nbig_max + 1));
     const size_t pin_lane = pin_sB + pin_spB + al256(4 * nh_max);
-    unsigned char* pin_all = qs_pinned(2 * pin_lane);
+    // device-built levels (param qs_dev): regions per lane
+    const bool dev_on = qdev_on<K>(n);
+    const uint64_t NM = nmid_max;
+    const QDevLayout DL = qdev_layout<K>(NM, G_TARGET);
+    unsigned char* pin_all = qs_pinned(2 * pin_lane + (dev_on ? 2 * DL.pinB : 0));
     if (!pin_all) return PP_E_NOMEM;
     lanes[0].pin = pin_all;
     lanes[1].pin = pin_all + pin_lane;
+    if (dev_on)
+        for (int i = 0; i < 2; ++i) lanes[i].dpin = pin_all + 2 * pin_lane + (size_t)i * DL.pinB;
     // bytes of each lane's device region: the level bound up front (a few MB
     // at 2^28 keys), so a growing level never has to drain the other lane
     const size_t lane_half = qs_level_bound<K>(n);
@@ -1451,9 +1798,12 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     const size_t e_scrB = al256(sizeof(GroupOut) * s_max), e_bloB = al256(8 * slot_max), e_blnB = al256(4 * slot_max);
     const size_t e_skbB = al256(16 * s_max), e_bkbB = al256(16 * slot_max);  // key bounds: segments, bins
     const size_t earlyB = early ? e_sloB + e_slnB + e_sbB + e_scrB + e_bloB + e_blnB + e_skbB + e_bkbB : 0;
-    unsigned char* ws_all = static_cast<unsigned char*>(qs_workspace(2 * lane_half + earlyB));
+    const size_t devB = dev_on ? 2 * DL.laneB : 0;
+    unsigned char* ws_all = static_cast<unsigned char*>(qs_workspace(2 * lane_half + earlyB + devB));
     if (!ws_all) return PP_E_NOMEM;
     unsigned char* ew = ws_all + 2 * lane_half;
+    if (dev_on)
+        for (int i = 0; i < 2; ++i) lanes[i].dreg = ws_all + 2 * lane_half + earlyB + (size_t)i * DL.laneB;
     uint64_t* d_eslo = reinterpret_cast<uint64_t*>(ew);
     uint32_t* d_esln = reinterpret_cast<uint32_t*>(ew + e_sloB);
     uint64_t* d_esbase = reinterpret_cast<uint64_t*>(ew + e_sloB + e_slnB);
@@ -1496,10 +1846,9 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
 
     // classify a lane's segments, upload its level, launch its kernels and
     // the readback; records L.done (L.inflight = false if nothing to do)
-    auto launch_level = [&](Lane& L) -> pp_status {
-        L.inflight = false;
-        if (L.cur.empty()) return PP_OK;
-        g_qs_stats.levels = std::max<uint64_t>(g_qs_stats.levels, ++L.depth);
+    // the level's mid segments with their group counts, in launch order (LPT);
+    // big ones into L.big_idx; returns the level's total groups
+    auto plan_mids = [&](Lane& L) -> uint64_t {
         L.mids.clear();
         L.big_idx.clear();
         L.mid_idx.clear();
@@ -1598,6 +1947,14 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
                 gtot += q.g;
             }
         }
+        return gtot;
+    };
+    auto launch_level = [&](Lane& L) -> pp_status {
+        L.inflight = false;
+        if (L.cur.empty()) return PP_OK;
+        g_qs_stats.levels = std::max<uint64_t>(g_qs_stats.levels, ++L.depth);
+        const uint64_t gtot = plan_mids(L);
+        std::vector<QSeg>& mids = L.mids;
         const uint64_t nmid = mids.size(), nbig = L.big_idx.size();
         L.nmid = nmid;
         for (const HSeg& sg : L.cur) g_qs_stats.level_keys += sg.hi - sg.lo;  // every key of the level is partitioned
@@ -1694,7 +2051,7 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
             qs_pivot_kernel<K><<<(unsigned)((nmid + 7) / 8), 256, 0, lst>>>(keys, d_segs, nmid);
             if (lvl_prof) cudaEventRecord(L.lev[0], lst);
             e = qs_launch_pdl(qs_group_kernel<K>, dim3((unsigned)gtot), C::NT, C::SMEM, lst, keys, d_segs, nmid,
-                              P.seed, d_gout);
+                              P.seed, d_gout, (const QDevCtl*)nullptr);
             if (e != cudaSuccess) return cuda_fail(e, "quicksort group launch");
             if (lvl_prof) cudaEventRecord(L.lev[1], lst);
             if (nh > 0) {
@@ -1724,11 +2081,13 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
                 cudaFuncSetAttribute(qs_cleanup_kernel<K, NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sm);
                 e = qs_launch_pdl(qs_cleanup_kernel<K, NT, EPT>, dim3((unsigned)nmid), NT, sm, lst, keys,
-                                  (const QSeg*)d_segs, (const GroupOut*)d_gout, d_splits, HEAVY);
+                                  (const QSeg*)d_segs, (const GroupOut*)d_gout, d_splits, HEAVY,
+                                  (const QDevCtl*)nullptr);
             } else {
                 const size_t sm = sizeof(StreamBuf<SW_NT, SW_EPT2>);
                 e = qs_launch_pdl(qs_cleanup_kernel<K, SW_NT, SW_EPT2>, dim3((unsigned)nmid), SW_NT, sm, lst, keys,
-                                  (const QSeg*)d_segs, (const GroupOut*)d_gout, d_splits, HEAVY);
+                                  (const QSeg*)d_segs, (const GroupOut*)d_gout, d_splits, HEAVY,
+                                  (const QDevCtl*)nullptr);
             }
             if (e != cudaSuccess) return cuda_fail(e, "quicksort cleanup launch");
             if (lvl_prof) cudaEventRecord(L.lev[2], lst);
@@ -1751,6 +2110,25 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         return PP_OK;
     };
 
+    // the children of a partitioned segment (pivot p, split k): mid ones into
+    // `next`, small and leaf ones into the lists of the per-CTA recursion
+    // (qs_build_kernel computes the same mid children on the device)
+    auto visit = [&](std::vector<HSeg>& next, const HSeg& sg, uint64_t p, uint64_t k) {
+        const uint32_t d = sg.depth + 1;
+        // key bounds of the parts: left keys < p, right keys >= p
+        if (sg.mode != 1) {
+            if (k == 0) {
+                // p is the segment minimum; split by x <= p next (unless all == MAX)
+                if ((K)p != KMAX) next.push_back({sg.lo, sg.hi, (uint64_t)(K)(p + 1), 1, d, p, sg.kmax});
+            } else {
+                add_child(next, sg.lo, sg.lo + k, d, sg.kmin, p - 1);
+                add_child(next, sg.lo + k, sg.hi, d, p, sg.kmax);
+            }
+        } else {
+            // split by x < sg.pivot (= min + 1): [lo, lo+k) is all equal: final
+            add_child(next, sg.lo + k, sg.hi, d, sg.pivot, sg.kmax);
+        }
+    };
     // wait for a lane's level, read its splits and build its next segment list
     auto finish_level = [&](Lane& L) -> pp_status {
         e = cudaEventSynchronize(L.done);
@@ -1774,27 +2152,193 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         }
         // ---- next level ----
         L.next.clear();
-        auto visit = [&](const HSeg& sg, uint64_t p, uint64_t k) {
-            const uint32_t d = sg.depth + 1;
-            // key bounds of the parts: left keys < p, right keys >= p
-            if (sg.mode != 1) {
-                if (k == 0) {
-                    // p is the segment minimum; split by x <= p next (unless all == MAX)
-                    if ((K)p != KMAX) L.next.push_back({sg.lo, sg.hi, (uint64_t)(K)(p + 1), 1, d, p, sg.kmax});
-                } else {
-                    add_child(L.next, sg.lo, sg.lo + k, d, sg.kmin, p - 1);
-                    add_child(L.next, sg.lo + k, sg.hi, d, p, sg.kmax);
-                }
-            } else {
-                // split by x < sg.pivot (= min + 1): [lo, lo+k) is all equal: final
-                add_child(L.next, sg.lo + k, sg.hi, d, sg.pivot, sg.kmax);
-            }
-        };
-        for (size_t mi = 0; mi < nmid; ++mi) visit(L.cur[L.mid_idx[mi]], L.pivots_h[L.mid_idx[mi]], L.splits_h[mi]);
+        for (size_t mi = 0; mi < nmid; ++mi)
+            visit(L.next, L.cur[L.mid_idx[mi]], L.pivots_h[L.mid_idx[mi]], L.splits_h[mi]);
         for (size_t bi = 0; bi < nbig; ++bi)
-            visit(L.cur[L.big_idx[bi]], L.pivots_h[L.big_idx[bi]], L.splits_h[nmid + bi]);
+            visit(L.next, L.cur[L.big_idx[bi]], L.pivots_h[L.big_idx[bi]], L.splits_h[nmid + bi]);
         L.cur.swap(L.next);
         return PP_OK;
+    };
+
+    // ---- device-built levels (param qs_dev) ----
+    // Once a lane's segments are all below HEAVY (one CTA cleans each), every
+    // next level is built on the device by qs_build_kernel, and the host keeps
+    // two levels in flight per lane: it enqueues level l+2 (grids sized by the
+    // bound 2 x its parent level's count, surplus CTAs exit) as soon as it has
+    // read level l back, and takes the small and leaf children from that
+    // readback (same visit as the host loop; the device's count of mid
+    // children is checked against the host's).  No host round trip sits
+    // between two levels of a lane.
+    static cudaEvent_t dev_ev[2][2];
+    static bool dev_ev_made = false;
+    if (dev_on && !dev_ev_made) {
+        for (auto& a : dev_ev)
+            for (auto& x : a) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+        dev_ev_made = true;
+    }
+    struct DevPtr {
+        QSeg* list[2];
+        QSeg* tmp;
+        uint64_t* kb[2];
+        uint64_t* tkb;
+        QDevCtl* ctl;  // [2]: the count block of list 0 and list 1
+        GroupOut* gout;
+        uint64_t* splits;
+    };
+    auto dev_ptr = [&](const Lane& L) {
+        DevPtr D;
+        unsigned char* b = L.dreg;
+        D.list[0] = reinterpret_cast<QSeg*>(b);
+        D.list[1] = reinterpret_cast<QSeg*>(b + DL.listB);
+        D.tmp = reinterpret_cast<QSeg*>(b + 2 * DL.listB);
+        b += 3 * DL.listB;
+        D.kb[0] = reinterpret_cast<uint64_t*>(b);
+        D.kb[1] = reinterpret_cast<uint64_t*>(b + DL.kbB);
+        D.tkb = reinterpret_cast<uint64_t*>(b + 2 * DL.kbB);
+        b += 3 * DL.kbB;
+        D.ctl = reinterpret_cast<QDevCtl*>(b);
+        b += 256;
+        D.gout = reinterpret_cast<GroupOut*>(b);
+        D.splits = reinterpret_cast<uint64_t*>(b + DL.goutB);
+        return D;
+    };
+    // pinned readback of parity par: [segs][kb][splits][next count block]
+    auto pin_segs = [&](const Lane& L, int par) { return reinterpret_cast<QSeg*>(L.dpin + (size_t)par * DL.pinParB); };
+    auto pin_kb = [&](const Lane& L, int par) {
+        return reinterpret_cast<uint64_t*>(L.dpin + (size_t)par * DL.pinParB + DL.listB);
+    };
+    auto pin_spl = [&](const Lane& L, int par) {
+        return reinterpret_cast<uint64_t*>(L.dpin + (size_t)par * DL.pinParB + DL.listB + DL.kbB);
+    };
+    auto pin_ctl = [&](const Lane& L, int par) {
+        return reinterpret_cast<QDevCtl*>(L.dpin + (size_t)par * DL.pinParB + DL.listB + DL.kbB + DL.splB);
+    };
+    QBuildArgs QA;
+    QA.small = SMALL;
+    QA.g_target = G_TARGET;
+    QA.minl = MINL;
+    QA.slots = G_TARGET / (uint64_t)std::max<int64_t>(P.qs_waves, 1);
+    QA.nmax = NM;
+    QA.rule = RULE;
+    QA.deep = QS_DEEP;
+    const size_t qb_smem = 4 * (QB_NMAX + 3 * NM);
+    if (dev_on) cudaFuncSetAttribute(qs_build_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qb_smem);
+    // enqueue the level whose list has parity par (at most `bound` segments)
+    auto dev_enqueue = [&](Lane& L, int par, uint64_t bound) -> pp_status {
+        const DevPtr D = dev_ptr(L);
+        const cudaStream_t lst = L.st;
+        QSeg* segs = D.list[par];
+        const QDevCtl* cc = D.ctl + par;
+        bound = std::max<uint64_t>(bound, 1);
+        qs_pivot_kernel<K><<<(unsigned)((bound + 7) / 8), 256, 0, lst>>>(keys, segs, 0, cc);
+        e = qs_launch_pdl(qs_group_kernel<K>, dim3((unsigned)(G_TARGET + bound + 1)), C::NT, C::SMEM, lst, keys,
+                          (const QSeg*)segs, (uint64_t)0, P.seed, D.gout, cc);
+        if (e == cudaSuccess) {
+            if (bound <= (uint64_t)sm_count()) {
+                constexpr int NT = 512, EPT = 8;
+                const size_t sm = sizeof(StreamBuf<NT, EPT>);
+                cudaFuncSetAttribute(qs_cleanup_kernel<K, NT, EPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sm);
+                e = qs_launch_pdl(qs_cleanup_kernel<K, NT, EPT>, dim3((unsigned)bound), NT, sm, lst, keys,
+                                  (const QSeg*)segs, (const GroupOut*)D.gout, D.splits, HEAVY, cc);
+            } else {
+                const size_t sm = sizeof(StreamBuf<SW_NT, SW_EPT2>);
+                e = qs_launch_pdl(qs_cleanup_kernel<K, SW_NT, SW_EPT2>, dim3((unsigned)bound), SW_NT, sm, lst, keys,
+                                  (const QSeg*)segs, (const GroupOut*)D.gout, D.splits, HEAVY, cc);
+            }
+        }
+        if (e == cudaSuccess) {
+            qs_build_kernel<K><<<1, QB_NT, qb_smem, lst>>>(keys, segs, D.kb[par], cc, D.splits, D.tmp, D.tkb,
+                                                           D.list[par ^ 1], D.kb[par ^ 1], D.ctl + (par ^ 1), QA);
+            e = cudaGetLastError();
+        }
+        note_launches(4);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(pin_segs(L, par), segs, sizeof(QSeg) * bound, cudaMemcpyDeviceToHost, lst);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(pin_kb(L, par), D.kb[par], 16 * bound, cudaMemcpyDeviceToHost, lst);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(pin_spl(L, par), D.splits, 8 * bound, cudaMemcpyDeviceToHost, lst);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(pin_ctl(L, par), D.ctl + (par ^ 1), sizeof(QDevCtl), cudaMemcpyDeviceToHost, lst);
+        if (e == cudaSuccess) e = cudaEventRecord(dev_ev[L.id][par], lst);
+        return e == cudaSuccess ? PP_OK : cuda_fail(e, "quicksort device-built level");
+    };
+    // switch a lane to device-built levels: its current list goes up once
+    auto dev_start = [&](Lane& L) -> pp_status {
+        const uint64_t gtot = plan_mids(L);
+        const uint64_t nm = L.mids.size();
+        const DevPtr D = dev_ptr(L);
+        QSeg* ps = pin_segs(L, 0);
+        uint64_t* pk = pin_kb(L, 0);
+        for (uint64_t i = 0; i < nm; ++i) {
+            const HSeg& sg = L.cur[L.mid_idx[i]];
+            ps[i] = L.mids[i];
+            ps[i].pad = sg.depth;
+            pk[2 * i] = sg.kmin;
+            pk[2 * i + 1] = sg.kmax;
+        }
+        QDevCtl* pc = reinterpret_cast<QDevCtl*>(L.dpin + 2 * DL.pinParB);
+        *pc = QDevCtl{nm, gtot, 0, 0};
+        const cudaStream_t lst = L.st;
+        e = cudaMemcpyAsync(D.list[0], ps, sizeof(QSeg) * nm, cudaMemcpyHostToDevice, lst);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(D.kb[0], pk, 16 * nm, cudaMemcpyHostToDevice, lst);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(D.ctl, pc, sizeof(QDevCtl), cudaMemcpyHostToDevice, lst);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort device-built level H2D");
+        L.dev = true;
+        L.cur.clear();
+        pp_status ps0 = dev_enqueue(L, 0, nm);
+        if (ps0 != PP_OK) return ps0;
+        if ((ps0 = dev_enqueue(L, 1, std::min<uint64_t>(NM, 2 * nm))) != PP_OK) return ps0;
+        L.qpar[0] = 0;
+        L.qpar[1] = 1;
+        L.dq = 2;
+        L.qexact = nm;
+        L.inflight = true;
+        return PP_OK;
+    };
+    // read the oldest level of a device-built lane back, take its small and
+    // leaf children, enqueue the level after the next one
+    auto dev_step = [&](Lane& L) -> pp_status {
+        const int par = L.qpar[0];
+        e = cudaEventSynchronize(dev_ev[L.id][par]);
+        if (e != cudaSuccess) return cuda_fail(e, "quicksort device-built level");
+        const uint64_t nm = L.qexact;
+        const QSeg* ps = pin_segs(L, par);
+        const uint64_t* pk = pin_kb(L, par);
+        const uint64_t* pspl = pin_spl(L, par);
+        const QDevCtl pc = *pin_ctl(L, par);
+        if (nm > 0) g_qs_stats.levels = std::max<uint64_t>(g_qs_stats.levels, ++L.depth);
+        L.next.clear();
+        for (uint64_t i = 0; i < nm; ++i) {
+            const QSeg& q = ps[i];
+            const HSeg sg{q.lo, q.hi, q.pivot, q.mode, q.pad, pk[2 * i], pk[2 * i + 1]};
+            g_qs_stats.level_keys += q.hi - q.lo;
+            visit(L.next, sg, q.pivot, pspl[i]);
+        }
+        const uint64_t nnext = L.next.size();
+        L.next.clear();
+        if (pc.err != 0 || pc.nmid != nnext) {
+            set_error("quicksort: the device-built level list disagrees with the host's children");
+            return PP_E_INTERNAL;
+        }
+        L.qpar[0] = L.qpar[1];
+        L.dq = 1;
+        L.qexact = nnext;
+        if (nnext == 0) {  // the level in flight has no segments: the lane is done
+            L.dq = 0;
+            L.inflight = false;
+            return PP_OK;
+        }
+        const int np = L.qpar[0] ^ 1;
+        pp_status s2 = dev_enqueue(L, np, std::min<uint64_t>(NM, 2 * nnext));
+        if (s2 != PP_OK) return s2;
+        L.qpar[1] = np;
+        L.dq = 2;
+        return PP_OK;
+    };
+    auto dev_ready = [&](const Lane& L) {
+        if (!dev_on || L.cur.empty()) return false;
+        for (const HSeg& sg : L.cur)
+            if (sg.hi - sg.lo >= BIG || (HEAVY && sg.hi - sg.lo >= HEAVY)) return false;
+        return true;
     };
 
     // phase 1: one lane while big segments exist (or fewer than two segments)
@@ -1827,13 +2371,17 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         e = cudaEventRecord(lane_ev[2], st);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(lane_st1_used, lane_ev[2], 0);
         if (e != cudaSuccess) return cuda_fail(e, "quicksort lanes");
-        if ((ps = launch_level(lanes[0])) != PP_OK) return ps;
-        if ((ps = launch_level(lanes[1])) != PP_OK) return ps;
+        for (Lane& L : lanes)
+            if ((ps = dev_ready(L) ? dev_start(L) : launch_level(L)) != PP_OK) return ps;
         while (lanes[0].inflight || lanes[1].inflight) {
             for (Lane& L : lanes) {
                 if (!L.inflight) continue;
-                if ((ps = finish_level(L)) != PP_OK) return ps;
-                if ((ps = launch_level(L)) != PP_OK) return ps;
+                if (L.dev) {
+                    if ((ps = dev_step(L)) != PP_OK) return ps;
+                } else {
+                    if ((ps = finish_level(L)) != PP_OK) return ps;
+                    if ((ps = dev_ready(L) ? dev_start(L) : launch_level(L)) != PP_OK) return ps;
+                }
                 if (early && small_lo.size() - small_done >= early_min) {
                     if ((ps = small_batch(small_done, small_lo.size())) != PP_OK) return ps;
                     small_done = small_lo.size();

@@ -68,11 +68,14 @@ def test_small_sizes(pp, dt, mx):
 
 
 @pytest.mark.parametrize("dt,mx", [(np.uint64, U64_MAX), (np.uint32, U32_MAX)])
-def test_medium_sizes(pp, dt, mx):
+@pytest.mark.parametrize("dev", [0, 1])
+def test_medium_sizes(pp, dt, mx, dev):
+    """Host-built (qs_dev = 0) and device-built (qs_dev = 1: qs_build_kernel
+    makes every lane level below qs_heavy) level loops."""
     rng = np.random.default_rng(2)
     for n in (100_003, 1 << 20, 3_000_017):
         for a in _cases(dt, mx, n, rng):
-            out = _sort_gpu(pp, a, 3)
+            out = _sort_gpu(pp, a, 3, qs_dev=dev)
             assert np.array_equal(out, _oracle_sorted(a)), n
 
 
@@ -84,12 +87,19 @@ def test_medium_sizes(pp, dt, mx):
                                     {"qs_early": 1}, {"qs_early": 1, "qs_lanes": 1}, {"qs_early": 0},
                                     {"qs_deep": 0}, {"qs_deep": 3}, {"qs_deep": 0, "qs_cta_max": 1 << 12},
                                     {"qs_pivot": 1}, {"qs_pivot": 2}, {"qs_pivot": 2, "qs_cta_max": 1 << 16},
-                                    {"qs_prio": 0}, {"qs_prio": 0, "qs_lanes": 1}])
+                                    {"qs_prio": 0}, {"qs_prio": 0, "qs_lanes": 1},
+                                    {"qs_dev": 1}, {"qs_dev": 1, "qs_heavy": 0},
+                                    {"qs_dev": 1, "qs_heavy": 0, "qs_waves": 16},
+                                    {"qs_dev": 1, "qs_heavy": 0, "qs_pivot": 2},
+                                    {"qs_dev": 1, "qs_heavy": 0, "qs_small": 1 << 17},
+                                    {"qs_dev": 1, "qs_heavy": 0, "qs_pivot": 1, "leaf": 1000}])
 def test_qs_parameters(pp, dt, mx, params):
     """Bin sizes (both bin-sort CTA shapes), level balancing, the
     heavy-segment batched cleanup, the per-CTA recursion, the Strided
-    offsets and the stream layout without priorities (qs_prio = 0: lane 0
-    on the caller's stream) all give the oracle's sorted output."""
+    offsets, the stream layout without priorities (qs_prio = 0: lane 0
+    on the caller's stream) and the device-built levels (qs_dev = 1, from the
+    first lane level on with qs_heavy = 0) all give the oracle's sorted
+    output."""
     rng = np.random.default_rng(4)
     for n in (5000, 300_007):
         for a in list(_cases(dt, mx, n, rng))[:3]:
@@ -110,7 +120,8 @@ def test_big_path_forced(pp):
 def test_config5_full(pp, kind):
     """n = 2^28 u64 (BASELINE config 5), byte for byte against the oracle's
     serial quicksort of the same seed-regenerated input (north_star (4);
-    ~25 s of host time per input)."""
+    ~25 s of host time per input); both level loops (host-built, and
+    device-built with qs_dev = 1)."""
     n = 1 << 28
     if kind == "uniform":
         t = synth.uniform_u64_torch(n, synth.SEEDS["c5"], "cuda")
@@ -118,10 +129,18 @@ def test_config5_full(pp, kind):
     else:
         t = synth.mod_range_u64_torch(n, synth.SEEDS["c5"], 1000, "cuda")
         ref = synth.mod_range_u64_np(n, synth.SEEDS["c5"], 1000)
+    t2 = t.clone()
     pp.pp_quicksort(t)
     oracle.quicksort(ref)
     out = t.cpu().numpy().view(np.uint64)
     assert np.array_equal(out, ref)
+    # the device-built level loop (qs_dev = 1) on the same input
+    pp.pp_set_param("qs_dev", 1)
+    try:
+        pp.pp_quicksort(t2)
+    finally:
+        pp.reset_params()
+    assert np.array_equal(t2.cpu().numpy().view(np.uint64), ref)
 
 
 @pytest.mark.parametrize("leaf", [0, 1000, 4096, 8192, 12000, 10240])
