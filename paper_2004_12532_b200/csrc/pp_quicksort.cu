@@ -17,7 +17,9 @@
 //     qs_leaf_handoff_kernel).
 // Pivot: median of A[lo], A[lo+(len-1)/2], A[hi-1]; split by x < p; when that
 // split is empty (p is the segment minimum) the next level splits by x <= p
-// and the left part (all == p) is final (reading R14).
+// and the left part (all == p) is final (reading R14).  Every
+// segment carries the bounds [kmin, kmax] its ancestors' pivots imply; when
+// they collapse to one value the segment is all equal keys and final.
 #include <algorithm>
 #include <chrono>
 #include <functional>
@@ -381,13 +383,13 @@ __device__ __forceinline__ int qb_children(const QSeg& q, uint64_t k, uint64_t k
     const uint32_t mrule = (d > a.deep && a.rule == 0) ? 2u : a.rule;
     int n = 0;
     auto add = [&](uint64_t lo, uint64_t hi, uint64_t kmn, uint64_t kmx) {
-        if (hi - lo > a.small) c[n++] = QChild{lo, hi, 0, kmn, kmx, mrule};
+        if (hi - lo > a.small && kmn != kmx) c[n++] = QChild{lo, hi, 0, kmn, kmx, mrule};  // kmn == kmx: all equal
     };
     const uint64_t p = q.pivot;
     if (q.mode != 1) {
         if (k == 0) {
-            // p is the segment minimum: split by x <= p next (unless all == MAX)
-            if ((K)p != KMAX) c[n++] = QChild{q.lo, q.hi, (uint64_t)(K)(p + 1), p, kmax, 1u};
+            // p is the segment minimum: split by x <= p next (unless p is the bound: all equal)
+            if (p != kmax) c[n++] = QChild{q.lo, q.hi, (uint64_t)(K)(p + 1), p, kmax, 1u};
         } else {
             add(q.lo, q.lo + k, kmin, p - 1);  // keys < p
             add(q.lo + k, q.hi, p, kmax);      // keys >= p
@@ -1627,6 +1629,9 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
                          uint64_t kmax) {
         const uint64_t len = hi - lo;
         if (len <= 1) return;
+        // the pivots above it pin every key to [kmin, kmax]: a single value
+        // means the segment is all equal keys -- final, no pass
+        if (kmin == kmax) return;
         if (len <= LEAF) {
             leaf_lo.push_back(lo);
             leaf_len.push_back((uint32_t)len);
@@ -2118,8 +2123,9 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         // key bounds of the parts: left keys < p, right keys >= p
         if (sg.mode != 1) {
             if (k == 0) {
-                // p is the segment minimum; split by x <= p next (unless all == MAX)
-                if ((K)p != KMAX) next.push_back({sg.lo, sg.hi, (uint64_t)(K)(p + 1), 1, d, p, sg.kmax});
+                // p is the segment minimum; split by x <= p next (p == kmax, e.g.
+                // all == MAX: every key equals p -- final)
+                if (p != sg.kmax) next.push_back({sg.lo, sg.hi, (uint64_t)(K)(p + 1), 1, d, p, sg.kmax});
             } else {
                 add_child(next, sg.lo, sg.lo + k, d, sg.kmin, p - 1);
                 add_child(next, sg.lo + k, sg.hi, d, p, sg.kmax);
