@@ -712,10 +712,13 @@ def extras(pp, torch, synth, dev, stream, flush, args):
         else:
             q0 = synth.mod_range_u64_torch(nq, synth.SEEDS["c5"], 1000, dev)
         q = torch.empty_like(q0)
-        for rule in ("median3", "median31"):
+        # (and the device-built level loop, qs_dev = 1, with median-of-3 pivots)
+        for rule in ("median3", "median31", "median3_devlevels"):
             pp.reset_params()
             if rule == "median31":
                 pp.pp_set_param("qs_pivot", 2)
+            if rule == "median3_devlevels":
+                pp.pp_set_param("qs_dev", 1)
             ts = []
             for i in range(3):
                 q.copy_(q0)
@@ -735,8 +738,10 @@ def extras(pp, torch, synth, dev, stream, flush, args):
             # least one pass over the small segments, the bin sort one over all n
             model = 16 * (qs["level_keys"] + qs["small_keys"] + nq)
             peak, _ = peaks()
-            res[f"quicksort_{kind}_2^28" + ("" if rule == "median3" else "_median31")] = {
-                "keys_per_s": nq / (ms / 1e3), "ms": ms, "pivot": rule, "stats": qs,
+            res[f"quicksort_{kind}_2^28" + {"median3": "", "median31": "_median31",
+                                             "median3_devlevels": "_devlevels"}[rule]] = {
+                "keys_per_s": nq / (ms / 1e3), "ms": ms, "pivot": rule.split("_")[0], "stats": qs,
+                "levels_built_on": "device" if rule.endswith("devlevels") else "host",
                 "roofline": {"bound": "hbm", "model_bytes": model, "achieved": model / (ms / 1e3) / 1e9,
                              "peak": peak, "unit": "GB/s", "frac": model / (ms / 1e3) / 1e9 / peak,
                              "model": "2*w*(level_keys + small_keys + n): levels + one per-CTA recursion pass + "
