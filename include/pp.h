@@ -309,6 +309,17 @@ pp_status pp_last_stats(uint64_t *out13);
  * directly), nsmall (number of such small segments)}.  bench.py derives the
  * quicksort's algorithmic bytes from these. */
 pp_status pp_quicksort_last_stats(uint64_t *out6);
+/* EREW shadow-writer audit (the GPU analogue of SPEC's
+ * element-level auditor S:62-70 for the EREW claim of PAPER.md:229-238).
+ * Only the debug build libpp_audit.so (compiled with -DPP_AUDIT=1) implements
+ * it; the product libpp.so returns PP_E_INVAL.  d_shadow: device array of n
+ * zeroed uint32 counters owned by the caller, one per key of the device range
+ * [keys, keys + n) (key_bytes 4 or 8).  While set, every store of a key by
+ * the partition's kernels (pp_partition_* and its cleanup tails, all paths)
+ * adds 1 (the Smoothed Striding group kernel) or 1 << 16 (the cleanup
+ * kernels) to that key's counter.  d_shadow = NULL switches it off.  Not
+ * thread safe with concurrent calls; debugging / tests only. */
+pp_status pp_audit_set(uint32_t *d_shadow, const void *keys, uint64_t n, int key_bytes);
 /* Tunables (tests / benchmarks): "g", "min_lines_per_group", "small_n",
  * "path" (0 auto, 1 single-CTA, 2 smoothed striding, 3 cleanup only), "tile",
  * "ranks", "seed", "strided" (1: X = 0, the Strided Algorithm PAPER.md:796-825,

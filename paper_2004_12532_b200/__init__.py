@@ -119,6 +119,7 @@ def load(build_if_missing: bool = True):
         "pp_ipc_close_all": ([], st),
         "pp_dist_last_timing": ([ctypes.POINTER(ctypes.c_double)], st),
         "pp_quicksort_last_stats": ([P64], st),
+        "pp_audit_set": ([vp, vp, u64, ctypes.c_int], st),
         "pp_partition_dist_loopback_u64": ([vp, P64, ctypes.c_int, u64, P64], st),
         "pp_partition_dist_loopback_u32": ([vp, P64, ctypes.c_int, u32, P64], st),
         "pp_quicksort_dist_loopback_u64": ([vp, P64, ctypes.c_int], st),
@@ -335,6 +336,19 @@ def pp_last_stats() -> dict:
 
 
 QS_STAT_KEYS = ("n", "levels", "level_keys", "small_keys", "leaf_keys", "nsmall")
+
+
+def pp_audit_set(shadow, keys=None) -> None:
+    """EREW shadow-writer audit (libpp_audit.so only, include/pp.h): `shadow`
+    is a zeroed int32 tensor with one counter per key of `keys` (same
+    device); None switches the audit off."""
+    import torch
+    if shadow is None:
+        _check(load().pp_audit_set(None, None, 0, 0), "pp_audit_set")
+        return
+    assert shadow.dtype == torch.int32 and shadow.numel() == keys.numel() and shadow.device == keys.device
+    _check(load().pp_audit_set(shadow.data_ptr(), keys.data_ptr(), keys.numel(), keys.element_size()),
+           "pp_audit_set")
 
 
 def pp_quicksort_last_stats() -> dict:

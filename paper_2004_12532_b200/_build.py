@@ -11,6 +11,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpp.so")
+# the EREW shadow-writer audit build (-DPP_AUDIT=1; tests only, include/pp.h pp_audit_set)
+LIB_AUDIT = os.path.join(PKG, "libpp_audit.so")
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17",
@@ -29,10 +31,10 @@ def deps():
         os.path.join(ROOT, "include", "pp.h")]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
@@ -50,17 +52,19 @@ def nccl_paths():
     return "/usr/include", "libnccl.so.2"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, audit: bool = False) -> str:
     """Compile every .cu to an object in parallel (one nvcc per source; no
-    device code crosses translation units), then link libpp.so."""
-    if not force and up_to_date():
-        return LIB
+    device code crosses translation units), then link libpp.so (audit=True:
+    the EREW audit build libpp_audit.so, -DPP_AUDIT=1, its own objects)."""
+    lib_out = LIB_AUDIT if audit else LIB
+    if not force and up_to_date(lib_out):
+        return lib_out
     nvcc = os.environ.get("NVCC", "nvcc")
     nccl_inc, nccl_lib = nccl_paths()
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build_audit" if audit else "build")
     os.makedirs(objdir, exist_ok=True)
     common = [nvcc, *NVCC_FLAGS[:-1], "-I", os.path.join(ROOT, "include"), "-I", nccl_inc,
-              f'-DPP_NCCL_LIB="{nccl_lib}"']
+              f'-DPP_NCCL_LIB="{nccl_lib}"'] + (["-DPP_AUDIT=1"] if audit else [])
     jobs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
@@ -73,11 +77,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
         list(ex.map(run, [c for _, c in jobs]))
-    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp",
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib_out + ".tmp",
             *[o for o, _ in jobs], "-ldl"]
     run(link)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib_out + ".tmp", lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":

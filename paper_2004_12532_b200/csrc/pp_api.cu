@@ -800,6 +800,15 @@ pp_status pp_last_stats(uint64_t* out) {
     return PP_OK;
 }
 
+pp_status pp_audit_set(uint32_t* d_shadow, const void* keys, uint64_t n, int key_bytes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (d_shadow != nullptr && (keys == nullptr || (key_bytes != 4 && key_bytes != 8))) {
+        set_error("pp_audit_set: keys and key_bytes (4 or 8) required with a shadow array");
+        return PP_E_INVAL;
+    }
+    return audit_set_partition(d_shadow, keys, d_shadow ? n : 0, (uint32_t)(key_bytes > 0 ? key_bytes : 8));
+}
+
 pp_status pp_quicksort_last_stats(uint64_t* out6) {
     std::lock_guard<std::mutex> lk(g_mu);
     return quicksort_last_stats(out6);

@@ -18,6 +18,33 @@ template <typename K>
 __device__ __forceinline__ bool is_pred(K x, K pivot) { return x < pivot; }
 
 // ---------------------------------------------------------------------------
+// EREW shadow-writer audit (the GPU analogue of SPEC's
+// element-level auditor S:62-70).  Only in the separate
+// debug library libpp_audit.so (-DPP_AUDIT=1): every store of a key by the
+// partition's kernels adds `inc` to a per-key counter -- 1 for the group
+// kernel (the partial step), 1 << 16 for the cleanup kernels -- so the test
+// can assert that each key is written at most once per phase.  The product
+// library compiles every PP_AUDIT_W to nothing (and has no atomics).
+// ---------------------------------------------------------------------------
+#if PP_AUDIT
+struct AuditState {
+    uint32_t* shadow;  // one counter per key of [base, base + n keys)
+    uint64_t base, n, kb;
+};
+static __device__ AuditState g_audit;  // per translation unit (set for pp_partition.cu's kernels)
+__device__ __forceinline__ void audit_w(const void* p, uint32_t inc) {
+    const AuditState a = g_audit;
+    if (a.shadow == nullptr) return;
+    const uint64_t off = (uint64_t)(uintptr_t)p - a.base;
+    if (off % a.kb == 0 && off / a.kb < a.n) atomicAdd(a.shadow + off / a.kb, inc);
+}
+#define PP_AUDIT_W(p, inc) ::pp::audit_w((const void*)(p), (inc))
+#else
+#define PP_AUDIT_W(p, inc) ((void)0)
+#endif
+constexpr uint32_t AUDIT_GROUP = 1u, AUDIT_CLEANUP = 1u << 16;
+
+// ---------------------------------------------------------------------------
 // Smoothed Striding chunk offsets X[j] in {0..g-1}, computed on the fly (the
 // paper stores s words of X; recomputing costs ~10 integer
 // ops per line and no memory).

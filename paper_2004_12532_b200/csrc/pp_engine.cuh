@@ -243,8 +243,14 @@ __device__ __forceinline__ void swap_pair(K* __restrict__ keys, const Dirty& d, 
     for (int k = 0; k < EPT; ++k) {
         const uint64_t off = (uint64_t)k * NT + threadIdx.x;
         const uint32_t il = ps.rl[k] - ra, ir = ps.rr[k] - rb;
-        if (((ps.fl >> k) & 1u) && il < npairs) keys[vreal(d, uL + off)] = pb.rval[il];
-        if (((ps.fr >> k) & 1u) && ir < npairs) keys[vreal(d, uR + off)] = pb.lval[ir];
+        if (((ps.fl >> k) & 1u) && il < npairs) {
+            keys[vreal(d, uL + off)] = pb.rval[il];
+            PP_AUDIT_W(keys + vreal(d, uL + off), AUDIT_CLEANUP);
+        }
+        if (((ps.fr >> k) & 1u) && ir < npairs) {
+            keys[vreal(d, uR + off)] = pb.lval[ir];
+            PP_AUDIT_W(keys + vreal(d, uR + off), AUDIT_CLEANUP);
+        }
     }
     __syncthreads();
 }
@@ -305,6 +311,8 @@ __device__ void walk_swap_stream(K* __restrict__ keys, const Dirty& d, K pivot, 
             const K a = keys[pl], b = keys[pr];
             keys[pl] = b;
             keys[pr] = a;
+            PP_AUDIT_W(keys + pl, AUDIT_CLEANUP);
+            PP_AUDIT_W(keys + pr, AUDIT_CLEANUP);
         }
         hl += m;
         hr += m;
@@ -862,6 +870,8 @@ __device__ void scan_swap_body(K* __restrict__ keys, Ctl* __restrict__ ctl, K pi
                 const K a = keys[pl], b = keys[pr];
                 keys[pl] = b;
                 keys[pr] = a;
+                PP_AUDIT_W(keys + pl, AUDIT_CLEANUP);
+                PP_AUDIT_W(keys + pr, AUDIT_CLEANUP);
             }
             __syncthreads();
         }

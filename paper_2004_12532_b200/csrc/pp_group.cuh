@@ -193,11 +193,17 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
                 bulk_s2g(dst, src, LBYTES);
                 bulk_commit();
             }
+#if PP_AUDIT
+            for (int e = tid; e < LK; e += NT) PP_AUDIT_W(dst + e, AUDIT_GROUP);
+#endif
         } else {
 #pragma unroll
             for (int q = 0; q < VPT; ++q) {
                 const int off = (q * NT + tid) * VEC;
                 *reinterpret_cast<uint4*>(dst + off) = *reinterpret_cast<const uint4*>(src + off);
+#if PP_AUDIT
+                for (int e = 0; e < VEC; ++e) PP_AUDIT_W(dst + off + e, AUDIT_GROUP);
+#endif
             }
         }
     };
@@ -336,6 +342,7 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
         for (int e = tid; e < LK; e += NT) {
             const uint32_t q = base + e;
             dst[e] = (q < tp) ? tpool[(th + q) & PMASK] : fpool[(fh + (q - tp)) & PMASK];
+            PP_AUDIT_W(dst + e, AUDIT_GROUP);
         }
     }
     if constexpr (C::TMA_STORE) {

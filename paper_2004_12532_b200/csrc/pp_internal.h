@@ -102,6 +102,8 @@ uint64_t quicksort_workspace_bound(uint64_t n);
 
 template <typename K>
 pp_status partition_device(K* keys, uint64_t n, K pivot, cudaStream_t st, uint64_t* d_split, Ctl** ctl_out);
+// EREW shadow-writer audit (libpp_audit.so; PP_E_INVAL in the product library)
+pp_status audit_set_partition(uint32_t* shadow, const void* base, uint64_t n, uint32_t key_bytes);
 
 template <typename K>
 pp_status ss_groups_device(K* keys, uint64_t n, K pivot, uint64_t g, cudaStream_t st, uint64_t* T_host,

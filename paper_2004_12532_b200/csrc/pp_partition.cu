@@ -567,4 +567,18 @@ template pp_status ss_groups_device<uint64_t>(uint64_t*, uint64_t, uint64_t, uin
 template pp_status ss_groups_device<uint32_t>(uint32_t*, uint64_t, uint32_t, uint64_t, cudaStream_t, uint64_t*,
                                               uint64_t*, uint64_t*, uint64_t*);
 
+// EREW shadow-writer audit (libpp_audit.so only): point this translation
+// unit's kernels (the partition pipeline) at a counter array; nullptr stops it.
+pp_status audit_set_partition(uint32_t* shadow, const void* base, uint64_t n, uint32_t key_bytes) {
+#if PP_AUDIT
+    AuditState a{shadow, (uint64_t)(uintptr_t)base, n, key_bytes};
+    const cudaError_t e = cudaMemcpyToSymbol(g_audit, &a, sizeof(a));
+    return e == cudaSuccess ? PP_OK : cuda_fail(e, "audit state");
+#else
+    (void)shadow; (void)base; (void)n; (void)key_bytes;
+    set_error("pp_audit_set: this is the product library; the EREW audit lives in libpp_audit.so");
+    return PP_E_INVAL;
+#endif
+}
+
 }  // namespace pp
