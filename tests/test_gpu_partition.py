@@ -193,6 +193,42 @@ def test_ss_groups_parity(pp, dt):
         assert np.array_equal(np.sort(out), np.sort(a))
 
 
+@pytest.mark.parametrize("kind", ["uniform", "whole_lines"])
+def test_ss_groups_prop42_bounds(pp, kind):
+    """The GPU's per-group outputs obey the paper's statements about the
+    Smoothed Striding step (Prop. 4.2, 1140-1150, 1160-1166),
+    on a full-chunk layout with g = 16 groups of s = 1024 lines: each group's
+    first successor lies within g*b of g*T_i; every group's predecessor
+    fraction is within the Hoeffding + union-bound delta of the array's
+    (eps = 1e-6); the window is below 4 n delta'."""
+    from gpu_util import to_dev
+    rng = np.random.default_rng(1166)
+    g = 16
+    info0 = pp.pp_ss_groups(to_dev(np.zeros(1 << 16, dtype=np.uint64)), 1, g)[3]
+    b = info0["line_keys"]
+    s = 1024
+    n = g * s * b
+    if kind == "uniform":
+        a = rng.integers(0, U64_MAX, size=n, dtype=np.uint64, endpoint=True)
+        p = 1 << 63
+    else:  # every line all-predecessor or all-successor: the largest per-line variance
+        lines = rng.integers(0, 2, size=n // b).astype(bool)
+        a = np.where(np.repeat(lines, b), np.uint64(1), np.uint64(3)).astype(np.uint64)
+        p = 2
+    mu = float(np.mean(a < np.uint64(p)))
+    T, vlo, vhi, info = pp.pp_ss_groups(to_dev(a), p, g)
+    assert info["g"] == g and info["head"] == 0 and info["n_lines"] == g * s
+    eps = 1e-6
+    for i in range(g):
+        if int(T[i]) < s * b:
+            assert abs(int(vlo[i]) - g * int(T[i])) <= g * b, (i, int(vlo[i]), int(T[i]))
+    delta = np.sqrt(np.log(2 * g / eps) / (2 * s))
+    mui = T.astype(np.float64) / (s * b)
+    assert np.all(np.abs(mui - mu) < delta), (float(np.abs(mui - mu).max()), delta)
+    assert int(vhi.max()) - int(vlo.min()) < 4 * n * np.sqrt(np.log(n / eps) / s)
+    assert int(T.sum()) == oracle.count(a, p)
+
+
 def test_async_and_stats(pp):
     from gpu_util import to_dev
     n = 1 << 20

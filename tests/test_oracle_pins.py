@@ -344,3 +344,48 @@ def test_bps_partition_random(dt):
                     b = a.copy()
                     k = oracle.partition_bps(b, p, B)
                     oracle.check_partition(a, b, p, k)
+
+
+def _prop42_inputs(rng, n_lines, b, g):
+    """Uniform keys, and whole-line patterns (every line all-predecessor or
+    all-successor with probability 1/2: the largest per-line variance the
+    proof's Y_i(j) in [0, 1] allow)."""
+    n = n_lines * b
+    uni = rng.integers(0, 1 << 63, size=n, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    lines = rng.integers(0, 2, size=n_lines).astype(bool)
+    whole = np.where(np.repeat(lines, b), np.uint64(1), np.uint64(3)).astype(np.uint64)
+    return [(uni, 1 << 63), (whole, 2)]
+
+
+def _check_prop42(T, vlo, n_lines, b, g, mu, eps):
+    """PAPER.md:1160-1166 (0-based): group i's first successor lies in the
+    chunk of its (T_i)-th element, so |v_i - g T_i| <= g b
+    (Hoeffding + union bound over the g groups): with probability >= 1 - eps
+    every |mu_i - mu| < delta, delta = sqrt(ln(2 g / eps) / (2 s)); Prop. 4.2
+    (PAPER.md:1086-1099): v_max - v_min < 4 n delta' with
+    s = ln(n / eps) / delta'^2."""
+    s = n_lines // g
+    n = n_lines * b
+    for i in range(g):
+        if int(T[i]) < s * b:
+            assert abs(int(vlo[i]) - g * int(T[i])) <= g * b, (i, int(vlo[i]), int(T[i]))
+    delta = np.sqrt(np.log(2 * g / eps) / (2 * s))
+    mui = T.astype(np.float64) / (s * b)
+    assert np.all(np.abs(mui - mu) < delta), (float(np.abs(mui - mu).max()), delta)
+    d2 = np.sqrt(np.log(n / eps) / s)
+    assert int(vlo.max()) - int(vlo.min()) < 4 * n * d2
+
+
+def test_prop42_smoothed_striding_bounds():
+    """The oracle's Smoothed Striding step obeys Prop. 4.2's statements on
+    full-chunk layouts (n_lines a multiple of g), over several offset draws."""
+    rng = np.random.default_rng(1099)
+    g, b, s = 16, 8, 4096
+    n_lines = g * s
+    for a, p in _prop42_inputs(rng, n_lines, b, g):
+        mu = float(np.mean(a < np.uint64(p)))
+        for seed in (1, 2, 3):
+            X = synth.ss_offsets(seed, s, g)
+            T, vlo, _ = oracle.ss_groups(a, 0, n_lines, b, g, X, p)
+            assert int(T.sum()) == oracle.count(a, p)
+            _check_prop42(T, vlo, n_lines, b, g, mu, 1e-6)
