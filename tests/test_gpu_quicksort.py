@@ -121,7 +121,8 @@ def test_config5_full(pp, kind):
     """n = 2^28 u64 (BASELINE config 5), byte for byte against the oracle's
     serial quicksort of the same seed-regenerated input (north_star (4);
     ~25 s of host time per input); both level loops (host-built, and
-    device-built with qs_dev = 1)."""
+    device-built with qs_dev = 1), and the 8-GPU form through 8 emulated
+    ranks."""
     n = 1 << 28
     if kind == "uniform":
         t = synth.uniform_u64_torch(n, synth.SEEDS["c5"], "cuda")
@@ -130,6 +131,7 @@ def test_config5_full(pp, kind):
         t = synth.mod_range_u64_torch(n, synth.SEEDS["c5"], 1000, "cuda")
         ref = synth.mod_range_u64_np(n, synth.SEEDS["c5"], 1000)
     t2 = t.clone()
+    t8 = t.clone()
     pp.pp_quicksort(t)
     oracle.quicksort(ref)
     out = t.cpu().numpy().view(np.uint64)
@@ -141,6 +143,12 @@ def test_config5_full(pp, kind):
     finally:
         pp.reset_params()
     assert np.array_equal(t2.cpu().numpy().view(np.uint64), ref)
+    # config 5 on 8 GPUs: the distributed quicksort (spanning segments
+    # partitioned across ranks, the rest sorted locally) with 8 emulated ranks
+    # of 2^25 keys on this GPU (loopback transport, the product code path)
+    del t2
+    pp.pp_quicksort_dist_loopback(t8, [n // 8] * 8)
+    assert np.array_equal(t8.cpu().numpy().view(np.uint64), ref)
 
 
 @pytest.mark.parametrize("leaf", [0, 1000, 4096, 8192, 12000, 10240])
