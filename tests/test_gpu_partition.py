@@ -1,4 +1,5 @@
 """GPU parity: the CUDA partition (through the C ABI) against the CPU oracle."""
+import functools
 import os
 
 import numpy as np
@@ -363,6 +364,7 @@ def test_config2_full(pp, mu):
     assert st["aux_bytes"] < 0.001 * n * 8
 
 
+@functools.lru_cache(maxsize=None)
 def _oracle_count_c3(n: int, p: int, chunk: int = 1 << 27) -> int:
     """K = #keys < p over the seed-regenerated c3 input, computed by the
     oracle chunk by chunk on the host (threads: numpy and the ctypes oracle
@@ -385,13 +387,33 @@ def test_config3_single_gpu_full(pp):
     keys and the regenerated input's keys in it are gathered and sorted with
     the library sort and compared element by element.  Given (1) and (2),
     whole-array multiset equality is equivalent to the per-side check (3)."""
-    from gpu_util import order_key, order_pivot
     n = 1 << 33
     p = 1 << 63
-    K_oracle = _oracle_count_c3(n, p)
     t = torch.empty(n, dtype=torch.int64, device="cuda")
     synth.uniform_u64_torch(n, synth.SEEDS["c3"], "cuda", out=t, chunk=1 << 27)
     split = pp.pp_partition(t, p)
+    _check_c3_exact(t, n, p, split)
+
+
+@pytest.mark.parametrize("P", [2, 8])
+def test_config3_loopback_ranks_full(pp, P):
+    """BASELINE config 3 at P = 2 and 8: the same 2^33 keys as P contiguous
+    shards of 2^33 / P (key i depends only on the global index i), partitioned
+    by the distributed code (local partitions, all-gather of the counts, the
+    planned exchange of misplaced ranges) with P emulated ranks on this GPU
+    (loopback transport), checked exactly like the single-GPU run: the GLOBAL
+    array is the partition of P:272-281."""
+    n = 1 << 33
+    p = 1 << 63
+    t = torch.empty(n, dtype=torch.int64, device="cuda")
+    synth.uniform_u64_torch(n, synth.SEEDS["c3"], "cuda", out=t, chunk=1 << 27)
+    split = pp.pp_partition_dist_loopback(t, [n // P] * P, p)
+    _check_c3_exact(t, n, p, split)
+
+
+def _check_c3_exact(t, n, p, split):
+    from gpu_util import order_key, order_pivot
+    K_oracle = _oracle_count_c3(n, p)
     assert split == K_oracle
     pv = order_pivot(p, torch.int64)
     C = 1 << 28
