@@ -1332,7 +1332,9 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
             __syncthreads();
             continue;
         }
-        if (len <= 1) {
+        if (len <= 1 || (kmn == kmx && !incta)) {
+            // (kmn == kmx: the pivots above it pin every key to one value --
+            // all equal and final, like the x <= p step's left part)
             __syncthreads();
             continue;
         }
@@ -1373,8 +1375,8 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
             // key bounds of the parts: left keys < p, right keys >= p
             const uint64_t pu = (uint64_t)p;
             if ((mode & QM_LE) == 0 && k == 0) {
-                // p is the minimum: split by x <= p next (reading R14); all == MAX: final
-                if (p != KMAX) push(lo, hi, QM_LE | incta, (uint64_t)(K)(p + 1), pu, kmx);
+                // p is the minimum: split by x <= p next (reading R14); p == kmx (e.g. all == MAX): final
+                if (pu != kmx) push(lo, hi, QM_LE | incta, (uint64_t)(K)(p + 1), pu, kmx);  // (== kmx: all equal)
             } else if (mode & QM_LE) {
                 push(lo + k, hi, QM_PIVOT | incta, 0, pu, kmx);  // [lo, lo+k) is all == p - 1: final, skipped
             } else if (incta || sp >= LEFT_FIRST_MAX) {

@@ -43,8 +43,9 @@ def main():
         if kind == "uniform":
             q0 = (synth.uniform_u64_torch(n, synth.SEEDS["c5"], "cuda") if args.dtype == "u64"
                   else synth.uniform_u32_torch(n, synth.SEEDS["c5"], "cuda"))
-        else:
-            q0 = synth.mod_range_u64_torch(n, synth.SEEDS["c5"], 1000, "cuda")
+        else:  # dup1000, dup10000, ...: keys uniform in [0, m)
+            m = int(kind[3:]) if kind.startswith("dup") and kind[3:].isdigit() else 1000
+            q0 = synth.mod_range_u64_torch(n, synth.SEEDS["c5"], m, "cuda")
             if args.dtype == "u32":
                 q0 = q0.to(torch.int32)
         inputs[kind] = (q0, lib_sorted(q0))
