@@ -43,6 +43,7 @@ struct QSeg {
                        // 2: pivot = ninther; 3: median of 31 samples (computed on device; param
                        // qs_pivot, and segments deeper than QS_DEEP take at least the ninther)
     uint32_t pad;      // device-built levels (qs_dev): the segment's depth
+    uint64_t kmin;     // every key of the segment is >= kmin (the pivots above it)
 };
 
 // Counts of a device-built level list (qs_dev): the kernels of the level read
@@ -84,6 +85,17 @@ __device__ __forceinline__ K warp_median31(const K* keys, uint64_t lo, uint64_t 
     return __shfl_sync(0xffffffffu, v, 15);  // the 16th smallest of the 31 samples
 }
 
+// A sampled pivot equal to the segment's lower bound kmin (every key >= kmin)
+// would make the x < p split empty and cost a pass before the x <= p step
+// (reading R14); splitting by x < kmin + 1 instead is that x <= p step at
+// once: the left part (all == kmin, non-empty since p is a key) is final, the
+// right part strictly smaller.  kmin < KMAX here (a segment whose bounds are
+// one value is dropped as all equal).
+template <typename K>
+__host__ __device__ __forceinline__ uint64_t pivot_above_bound(K p, uint64_t kmin) {
+    return (uint64_t)p == kmin ? (uint64_t)(K)(p + 1) : (uint64_t)p;
+}
+
 // Sample keys of a big segment (host-computed pivot): one launch writing into
 // pinned host memory (mapped, UVA) instead of one pageable 8-byte copy each.
 struct QsSamplePos {
@@ -105,16 +117,17 @@ __global__ void __launch_bounds__(256) qs_pivot_kernel(const K* __restrict__ key
         const uint64_t len = q.hi - q.lo;
         if (q.mode == 3) {
             const K p = warp_median31<K>(keys, q.lo, len, lane);
-            if (lane == 0) segs[s].pivot = (uint64_t)p;
+            if (lane == 0) segs[s].pivot = pivot_above_bound<K>(p, q.kmin);
         } else if (lane == 0 && q.mode == 0) {
-            segs[s].pivot = (uint64_t)median3<K>(keys[q.lo], keys[q.lo + (len - 1) / 2], keys[q.hi - 1]);
+            segs[s].pivot = pivot_above_bound<K>(
+                median3<K>(keys[q.lo], keys[q.lo + (len - 1) / 2], keys[q.hi - 1]), q.kmin);
         } else if (lane == 0 && q.mode == 2) {
             K m[3];
 #pragma unroll
             for (int t = 0; t < 3; ++t)
                 m[t] = median3<K>(keys[ninther_pos<K>(q.lo, len, 3 * t)], keys[ninther_pos<K>(q.lo, len, 3 * t + 1)],
                                   keys[ninther_pos<K>(q.lo, len, 3 * t + 2)]);
-            segs[s].pivot = (uint64_t)median3<K>(m[0], m[1], m[2]);
+            segs[s].pivot = pivot_above_bound<K>(median3<K>(m[0], m[1], m[2]), q.kmin);
         }
     }
 }
@@ -454,6 +467,7 @@ __global__ void __launch_bounds__(QB_NT) qs_build_kernel(const K* __restrict__ k
             x.g = 0;
             x.mode = c[j].mode;
             x.pad = q.pad + 1;
+            x.kmin = c[j].kmin;
             tmp[off] = x;
             tkb[2 * off] = c[j].kmin;
             tkb[2 * off + 1] = c[j].kmax;
@@ -1367,6 +1381,7 @@ __global__ void __launch_bounds__(SmallCfg<K>::NT, SmallCfg<K>::MINB)
             }
         }
         else p = (K)pm;
+        if ((mode & QM_LE) == 0 && kmn < kmx) p = (K)pivot_above_bound<K>(p, kmn);  // (p == kmn: the x <= p step now)
         if (prof) { const uint64_t t1 = clock64(); pr[0] += t1 - t0; t0 = t1; }
         const uint64_t k = cta_partition<K>(keys + lo, len, p, seed, smem, scratch + blockIdx.x, &sc, red,
                                                prof ? pr : nullptr);
@@ -1880,6 +1895,7 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
             q.pivot = L.cur[i].pivot;
             q.mode = L.cur[i].mode;
             q.pad = 0;
+            q.kmin = L.cur[i].kmin;
             // lines of the aligned region (host mirror of seg_head)
             const uint64_t addr = (uint64_t)(uintptr_t)(keys + q.lo);
             uint64_t h = ((16 - (addr & 15)) & 15) / sizeof(K);
@@ -2043,6 +2059,7 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
                     std::sort(v, v + 31);
                     p = (uint64_t)v[15];
                 }
+                p = pivot_above_bound<K>((K)p, sg.kmin);
             }
             L.pivots_h[L.big_idx[bi]] = p;
             pp_status ps = partition_device<K>(keys + sg.lo, sg.hi - sg.lo, (K)p, lst, d_splits + nmid + bi, nullptr);
