@@ -4,7 +4,7 @@ Every kernel family of libpp.so runs once per case at sizes the sanitizer
 finishes quickly, each result checked against the oracle (so a tool run is
 also a parity run).  Usage (on the GPU box):
 
-    compute-sanitizer --tool racecheck python tools/sanitize.py [--only NAME]
+    compute-sanitizer --tool racecheck python tests/sanitize_run.py [--only NAME]
 
 tools/sanitize.sh runs memcheck / racecheck / synccheck / initcheck over it
 and keeps the logs under profiles/.

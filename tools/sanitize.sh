@@ -14,7 +14,7 @@ for tool in memcheck racecheck synccheck initcheck; do
     [ "$tool" = "memcheck" ] && extra="--leak-check no"
     [ "$tool" = "racecheck" ] && extra="--racecheck-report all"
     timeout 1500 compute-sanitizer --tool $tool $extra --error-exitcode 99 --print-limit 50 \
-      python tools/sanitize.py --only $c > "$OUT/sanitize_${tool}_${c}.log" 2>&1
+      python tests/sanitize_run.py --only $c > "$OUT/sanitize_${tool}_${c}.log" 2>&1
     rc=$?
     echo "$tool $c exit $rc" >> "$OUT/status.txt"
     grep -E "ERROR SUMMARY|RACECHECK SUMMARY|hazard|Error" "$OUT/sanitize_${tool}_${c}.log" | tail -3 >> "$OUT/status.txt"
