@@ -1,4 +1,6 @@
-"""Small-n workloads for compute-sanitizer.
+"""Small-n workloads for compute-sanitizer --
+test infrastructure (it imports oracle/).  compute-sanitizer is closed on this
+GPU pool; tools/sanitize.sh keeps the recipe for others.
 
 Every kernel family of libpp.so runs once per case at sizes the sanitizer
 finishes quickly, each result checked against the oracle (so a tool run is
