@@ -338,6 +338,7 @@ struct QBuildArgs {
     uint64_t nmax;      // capacity of the next list (<= QB_NMAX)
     uint32_t rule;      // level pivot rule (QSeg.mode of new segments) ...
     uint32_t deep;      // ... and the depth past which median of 3 becomes the ninther
+    uint32_t pivots;    // 1: compute the next level's pivots here (rules 0 and 2; no pivot kernel then)
 };
 constexpr int QB_NT = 1024, QB_NW = QB_NT / 32, QB_NBK = 512;
 constexpr uint64_t QB_NMAX = (uint64_t)QB_NBK * QB_NW;  // histogram entries; lists of <= QB_NMAX / 2 (shared memory)
@@ -463,6 +464,23 @@ __global__ void __launch_bounds__(QB_NT) qs_build_kernel(const K* __restrict__ k
             x.lo = c[j].lo;
             x.hi = c[j].hi;
             x.pivot = c[j].pivot;
+            if (a.pivots && c[j].mode != 1u) {
+                // the next level's pivot (its keys are final now): median of 3,
+                // or the ninther past the depth guard; at the lower bound, kmin + 1
+                K pk;
+                if (c[j].mode == 2u) {
+                    K m[3];
+#pragma unroll
+                    for (int t3 = 0; t3 < 3; ++t3)
+                        m[t3] = median3<K>(keys[ninther_pos<K>(x.lo, len, 3 * t3)],
+                                           keys[ninther_pos<K>(x.lo, len, 3 * t3 + 1)],
+                                           keys[ninther_pos<K>(x.lo, len, 3 * t3 + 2)]);
+                    pk = median3<K>(m[0], m[1], m[2]);
+                } else {
+                    pk = median3<K>(keys[x.lo], keys[x.lo + (len - 1) / 2], keys[x.hi - 1]);
+                }
+                x.pivot = pivot_above_bound<K>(pk, c[j].kmin);
+            }
             x.gbase = nl;  // (lines until the list is ordered)
             x.g = 0;
             x.mode = c[j].mode;
@@ -2246,16 +2264,18 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     QA.nmax = NM;
     QA.rule = RULE;
     QA.deep = QS_DEEP;
+    QA.pivots = RULE != 3 ? 1u : 0u;  // the median of 31 needs a warp per segment: the pivot kernel keeps it
+    const bool dev_pivot_kernel = QA.pivots == 0;
     const size_t qb_smem = 4 * (QB_NMAX + 3 * NM);
     if (dev_on) cudaFuncSetAttribute(qs_build_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qb_smem);
     // enqueue the level whose list has parity par (at most `bound` segments)
-    auto dev_enqueue = [&](Lane& L, int par, uint64_t bound) -> pp_status {
+    auto dev_enqueue = [&](Lane& L, int par, uint64_t bound, bool need_pivots) -> pp_status {
         const DevPtr D = dev_ptr(L);
         const cudaStream_t lst = L.st;
         QSeg* segs = D.list[par];
         const QDevCtl* cc = D.ctl + par;
         bound = std::max<uint64_t>(bound, 1);
-        qs_pivot_kernel<K><<<(unsigned)((bound + 7) / 8), 256, 0, lst>>>(keys, segs, 0, cc);
+        if (need_pivots) qs_pivot_kernel<K><<<(unsigned)((bound + 7) / 8), 256, 0, lst>>>(keys, segs, 0, cc);
         e = qs_launch_pdl(qs_group_kernel<K>, dim3((unsigned)(G_TARGET + bound + 1)), C::NT, C::SMEM, lst, keys,
                           (const QSeg*)segs, (uint64_t)0, P.seed, D.gout, cc);
         if (e == cudaSuccess) {
@@ -2277,7 +2297,7 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
                                                            D.list[par ^ 1], D.kb[par ^ 1], D.ctl + (par ^ 1), QA);
             e = cudaGetLastError();
         }
-        note_launches(4);
+        note_launches(need_pivots ? 4 : 3);
         if (e == cudaSuccess) e = cudaMemcpyAsync(pin_segs(L, par), segs, sizeof(QSeg) * bound, cudaMemcpyDeviceToHost, lst);
         if (e == cudaSuccess) e = cudaMemcpyAsync(pin_kb(L, par), D.kb[par], 16 * bound, cudaMemcpyDeviceToHost, lst);
         if (e == cudaSuccess) e = cudaMemcpyAsync(pin_spl(L, par), D.splits, 8 * bound, cudaMemcpyDeviceToHost, lst);
@@ -2309,9 +2329,9 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         if (e != cudaSuccess) return cuda_fail(e, "quicksort device-built level H2D");
         L.dev = true;
         L.cur.clear();
-        pp_status ps0 = dev_enqueue(L, 0, nm);
+        pp_status ps0 = dev_enqueue(L, 0, nm, true);  // (the host's list: pivots on the device)
         if (ps0 != PP_OK) return ps0;
-        if ((ps0 = dev_enqueue(L, 1, std::min<uint64_t>(NM, 2 * nm))) != PP_OK) return ps0;
+        if ((ps0 = dev_enqueue(L, 1, std::min<uint64_t>(NM, 2 * nm), dev_pivot_kernel)) != PP_OK) return ps0;
         L.qpar[0] = 0;
         L.qpar[1] = 1;
         L.dq = 2;
@@ -2353,7 +2373,7 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
             return PP_OK;
         }
         const int np = L.qpar[0] ^ 1;
-        pp_status s2 = dev_enqueue(L, np, std::min<uint64_t>(NM, 2 * nnext));
+        pp_status s2 = dev_enqueue(L, np, std::min<uint64_t>(NM, 2 * nnext), dev_pivot_kernel);
         if (s2 != PP_OK) return s2;
         L.qpar[1] = np;
         L.dq = 2;
