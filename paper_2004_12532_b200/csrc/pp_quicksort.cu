@@ -1080,17 +1080,19 @@ __global__ void __launch_bounds__(NT, PLEAF >= 16384 ? 1 : 2) qs_leaf_bidx_kerne
                 const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                    for (int bb = 0; bb < 4; ++bb) {
-                        const uint32_t c = (wv[q] >> (8 * bb)) & 0xFFu;
-                        const uint32_t b0 = (tid * RW + rw) * 16u + (uint32_t)(q * 4 + bb);
+                    // visit only the run starts (nonzero bytes) of this word
+                    for (uint32_t w = wv[q]; w != 0u;) {
+                        const uint32_t bb = (uint32_t)(__ffs(w) - 1) >> 3;
+                        const uint32_t c = (w >> (8 * bb)) & 0xFFu;
+                        w &= ~(0xFFu << (8 * bb));
+                        const uint32_t b0 = (tid * RW + rw) * 16u + (uint32_t)q * 4u + bb;
                         if (c == 2u) {
                             const uint16_t a = ix[b0], b = ix[b0 + 1];
                             if (ks[b] < ks[a]) {
                                 ix[b0] = b;
                                 ix[b0 + 1] = a;
                             }
-                        } else if (c > 2u) {
+                        } else {
                             runs[atomicAdd(&nruns, 1u)] = b0 | (c << 16);
                         }
                     }
