@@ -338,7 +338,9 @@ pp_status pp_audit_set(uint32_t *d_shadow, const void *keys, uint64_t n, int key
  * one kernel -- children, group counts, longest-first order compacted by
  * scans -- and two levels per lane are in flight without a host round trip;
  * default 0: the host builds each level, measured 0.2-2% faster because the
- * two lanes already hide its work); "host_chunk", "bps_nt";
+ * two lanes already hide its work), "qs_dev_check" (test hook: every
+ * device-built list is compared with the host's plan of it, PP_E_INTERNAL on
+ * a difference); "host_chunk", "bps_nt";
  * multi-GPU: "dist_p2p", "dist_timeout_ms", "dist_small" (distributed
  * quicksort: spanning segments of <= this many keys are gathered and sorted
  * locally), "dist_overlap" (1: pp_partition_dist counts every chunk of the

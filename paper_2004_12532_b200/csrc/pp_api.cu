@@ -839,6 +839,7 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "qs_heavy") P.qs_heavy = value;
     else if (k == "qs_prio") P.qs_prio = value;
     else if (k == "qs_dev") P.qs_dev = value;
+    else if (k == "qs_dev_check") P.qs_dev_check = value;
     else if (k == "host_chunk") P.host_chunk = value;
     else if (k == "dist_p2p") P.dist_p2p = value ? 1 : 0;
     else if (k == "dist_timeout_ms") P.dist_timeout_ms = value < 1 ? 1 : value;
@@ -882,6 +883,7 @@ int64_t pp_get_param(const char* name) {
     if (k == "qs_heavy") return P.qs_heavy;
     if (k == "qs_prio") return P.qs_prio;
     if (k == "qs_dev") return P.qs_dev;
+    if (k == "qs_dev_check") return P.qs_dev_check;
     if (k == "host_chunk") return P.host_chunk;
     if (k == "dist_p2p") return P.dist_p2p;
     if (k == "dist_timeout_ms") return P.dist_timeout_ms;

@@ -74,6 +74,7 @@ struct Params {
     int64_t qs_prio = -1;          // quicksort: level loop on high-priority streams, early recursion / bins low
                                    // (-1 auto = on, 0 off, 1 on)
     int64_t qs_heavy = 1 << 22;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
+    int64_t qs_dev_check = 0;      // test hook: compare each device-built level list with the host's plan of it
     int64_t qs_dev = 0;            // quicksort: 1 = levels whose segments are all < qs_heavy are built on the
                                    // device (qs_build_kernel), two levels in flight per lane; 0 (default) = the
                                    // host builds every level (measured 0.2-2% faster: the two lanes already hide

@@ -1712,6 +1712,9 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         uint64_t qexact = 0;            // segments of the oldest level in flight (the host knows it exactly)
         unsigned char* dreg = nullptr;  // device region (QDevLayout)
         unsigned char* dpin = nullptr;  // pinned readbacks
+        std::vector<QSeg> dev_expect;   // qs_dev_check: the host's plan of the next device-built list
+        std::vector<uint64_t> dev_expect_kb;
+        bool dev_expect_valid = false;
     };
     static cudaStream_t lane_st1 = nullptr, lane_hi1 = nullptr;
     static cudaEvent_t lane_ev[3] = {nullptr, nullptr, nullptr};
@@ -2353,6 +2356,23 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
         const uint64_t* pspl = pin_spl(L, par);
         const QDevCtl pc = *pin_ctl(L, par);
         if (nm > 0) g_qs_stats.levels = std::max<uint64_t>(g_qs_stats.levels, ++L.depth);
+        if (P.qs_dev_check && L.dev_expect_valid) {
+            // test hook (param qs_dev_check): this device-built list must be the
+            // host's plan of the same children -- order, groups, first tasks,
+            // depth, mode, bounds (pivots of modes 0 / 2 / 3 are device data)
+            bool same = L.dev_expect.size() == nm;
+            for (uint64_t i = 0; same && i < nm; ++i) {
+                const QSeg& a = ps[i];
+                const QSeg& b = L.dev_expect[i];
+                same = a.lo == b.lo && a.hi == b.hi && a.g == b.g && a.gbase == b.gbase && a.mode == b.mode &&
+                       a.pad == b.pad && a.kmin == b.kmin && (a.mode != 1 || a.pivot == b.pivot) &&
+                       pk[2 * i] == L.dev_expect_kb[2 * i] && pk[2 * i + 1] == L.dev_expect_kb[2 * i + 1];
+            }
+            if (!same) {
+                set_error("quicksort: the device-built level list differs from the host's plan (qs_dev_check)");
+                return PP_E_INTERNAL;
+            }
+        }
         L.next.clear();
         for (uint64_t i = 0; i < nm; ++i) {
             const QSeg& q = ps[i];
@@ -2361,6 +2381,24 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
             visit(L.next, sg, q.pivot, pspl[i]);
         }
         const uint64_t nnext = L.next.size();
+        L.dev_expect_valid = false;
+        if (P.qs_dev_check && nnext > 0) {
+            // the host's plan of these children, checked against the list the
+            // device builds from them when that level is read back (the next
+            // step of this lane)
+            std::swap(L.cur, L.next);
+            plan_mids(L);
+            L.dev_expect = L.mids;
+            L.dev_expect_kb.clear();
+            for (size_t i = 0; i < L.mids.size(); ++i) {
+                const HSeg& sg = L.cur[L.mid_idx[i]];
+                L.dev_expect[i].pad = sg.depth;
+                L.dev_expect_kb.push_back(sg.kmin);
+                L.dev_expect_kb.push_back(sg.kmax);
+            }
+            std::swap(L.cur, L.next);
+            L.dev_expect_valid = true;
+        }
         L.next.clear();
         if (pc.err != 0 || pc.nmid != nnext) {
             set_error("quicksort: the device-built level list disagrees with the host's children");

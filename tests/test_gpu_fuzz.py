@@ -114,6 +114,7 @@ QUICKSORT_PARAMS = [
     {"qs_pivot": 1}, {"qs_pivot": 2}, {"qs_deep": 0},
     {"qs_early": 1}, {"qs_early": 1, "qs_small": 1 << 17, "qs_cta_max": 1 << 19},
     {"qs_dev": 1}, {"qs_dev": 1, "qs_heavy": 0}, {"qs_dev": 1, "qs_heavy": 0, "qs_pivot": 2},
+    {"qs_dev": 1, "qs_dev_check": 1, "qs_heavy": 0}, {"qs_dev": 1, "qs_dev_check": 1, "qs_heavy": 0, "qs_waves": 8},
 ]
 
 

@@ -92,14 +92,19 @@ def test_medium_sizes(pp, dt, mx, dev):
                                     {"qs_dev": 1, "qs_heavy": 0, "qs_waves": 16},
                                     {"qs_dev": 1, "qs_heavy": 0, "qs_pivot": 2},
                                     {"qs_dev": 1, "qs_heavy": 0, "qs_small": 1 << 17},
-                                    {"qs_dev": 1, "qs_heavy": 0, "qs_pivot": 1, "leaf": 1000}])
+                                    {"qs_dev": 1, "qs_heavy": 0, "qs_pivot": 1, "leaf": 1000},
+                                    {"qs_dev": 1, "qs_dev_check": 1, "qs_heavy": 0},
+                                    {"qs_dev": 1, "qs_dev_check": 1, "qs_heavy": 0, "qs_waves": 16},
+                                    {"qs_dev": 1, "qs_dev_check": 1, "qs_heavy": 0, "qs_pivot": 2}])
 def test_qs_parameters(pp, dt, mx, params):
     """Bin sizes (both bin-sort CTA shapes), level balancing, the
     heavy-segment batched cleanup, the per-CTA recursion, the Strided
     offsets, the stream layout without priorities (qs_prio = 0: lane 0
     on the caller's stream) and the device-built levels (qs_dev = 1, from the
     first lane level on with qs_heavy = 0) all give the oracle's sorted
-    output."""
+    output; with qs_dev_check every device-built level list must equal the
+    host's plan of the same children (order, groups incl. the straggler
+    take-back, first tasks, depth, bounds)."""
     rng = np.random.default_rng(4)
     for n in (5000, 300_007):
         for a in list(_cases(dt, mx, n, rng))[:3]:
@@ -242,3 +247,26 @@ def test_deep_segments_take_the_ninther(pp):
                 pp.reset_params()
             assert np.array_equal(to_host(t, np.uint64), ref), params
         assert max(levels) <= 2 * min(levels) + 4, levels
+
+
+@pytest.mark.parametrize("kind", ["uniform", "dup1000"])
+def test_device_built_levels_match_host_plan(pp, kind):
+    """qs_dev = 1 with qs_dev_check: at every device-built level of a 2^25-key
+    config-5-like sort the list qs_build_kernel made equals the host's plan
+    of the same children (order, group counts incl. the straggler take-back,
+    first tasks, depth, bounds), and the output is sorted."""
+    from gpu_util import to_dev, to_host
+    n = 1 << 25
+    a = synth.uniform_u64_np(n, 5) if kind == "uniform" else synth.mod_range_u64_np(n, 5, 1000)
+    ref = np.sort(a)
+    for extra in ({}, {"qs_waves": 16}, {"qs_heavy": 0}, {"qs_heavy": 0, "qs_pivot": 2}):
+        t = to_dev(a)
+        pp.pp_set_param("qs_dev", 1)
+        pp.pp_set_param("qs_dev_check", 1)
+        try:
+            for k, v in extra.items():
+                pp.pp_set_param(k, v)
+            pp.pp_quicksort(t)
+        finally:
+            pp.reset_params()
+        assert np.array_equal(to_host(t, np.uint64), ref), extra
