@@ -1356,7 +1356,9 @@ template pp_status partition_dist<uint32_t>(uint32_t*, uint64_t, uint32_t, cudaS
 //   * segments > `small` keys: ONE batched partition_multi for all of them
 //     (one record all-gather, one exchange); a segment whose pivot is its
 //     minimum (split 0) is re-partitioned next level by "x <= p" (pivot p+1),
-//     whose left part (all == p) is final;
+//     whose left part (all == p) is final; every segment carries the bounds
+//     its ancestors' pivots imply: bounds of one value = all equal, final; a
+//     pivot equal to the lower bound splits by x < kmin + 1 at once;
 //   * segments <= `small`: ONE all-gather of every rank's pieces of all of
 //     them; each participating rank sorts the whole segment locally and keeps
 //     its part.
@@ -1394,15 +1396,24 @@ static pp_status quicksort_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, cuda
         uint64_t lo, hi;
         bool leq;  // re-partition by x <= pivot (the pivot was the minimum)
         uint64_t pivot;
+        uint64_t kmin, kmax;  // every key of the segment is in [kmin, kmax] (the pivots above it)
     };
     std::vector<Seg> segs;
-    if (N > 1) segs.push_back({0, N, false, 0});
+    if (N > 1) segs.push_back({0, N, false, 0, 0, KMAXU});
     cudaError_t e;
     while (true) {
         std::vector<Seg> big, sm, nxt;
+        // (a segment whose bounds are one value is all equal keys: final, no round)
         for (const Seg& sg : segs)
-            if (sg.hi - sg.lo > 1 && owner(sg.lo) != owner(sg.hi - 1)) (sg.hi - sg.lo <= small ? sm : big).push_back(sg);
+            if (sg.hi - sg.lo > 1 && sg.kmin != sg.kmax && owner(sg.lo) != owner(sg.hi - 1))
+                (sg.hi - sg.lo <= small ? sm : big).push_back(sg);
         if (big.empty() && sm.empty()) break;
+        static const bool dprof = getenv("PP_QS_DIST_PROF") != nullptr;  // measurement: rounds per sort
+        if (dprof && me == 0) {
+            uint64_t kb = 0;
+            for (const Seg& sg : big) kb += sg.hi - sg.lo;
+            fprintf(stderr, "qs dist round: big=%zu (%llu keys) small=%zu\n", big.size(), (unsigned long long)kb, sm.size());
+        }
         // ---- pivots: one all-gather of the sample keys of this level ----
         // median of 3 (A[lo], A[mid], A[hi-1]; R14), or of 31 evenly spaced keys
         // with qs_pivot = 2 (the single-GPU level loop's rule)
@@ -1450,6 +1461,8 @@ static pp_status quicksort_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, cuda
                     si += NSMP;
                     std::sort(v.begin(), v.end());
                     p = v[NSMP / 2];
+                    // at the lower bound the x < p split is empty: split by x < kmin + 1 now
+                    if (p == sg.kmin) p = (uint64_t)(K)(p + 1);
                 }
                 piv[k] = p;
                 uint64_t a, b;
@@ -1463,12 +1476,13 @@ static pp_status quicksort_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, cuda
                 const Seg& sg = big[k];
                 const uint64_t kk = Ks[k], p = piv[k];
                 if (sg.leq) {
-                    nxt.push_back({sg.lo + kk, sg.hi, false, 0});  // [lo, lo+kk) all == p: final
+                    nxt.push_back({sg.lo + kk, sg.hi, false, 0, p + 1, sg.kmax});  // [lo, lo+kk) all == p: final
                 } else if (kk == 0) {
-                    if (p != KMAXU) nxt.push_back({sg.lo, sg.hi, true, p});  // else: all keys equal the maximum
+                    // every key >= p; p == kmax (e.g. all == MAX): all equal, final
+                    if (p != sg.kmax) nxt.push_back({sg.lo, sg.hi, true, p, p, sg.kmax});
                 } else {
-                    nxt.push_back({sg.lo, sg.lo + kk, false, 0});
-                    nxt.push_back({sg.lo + kk, sg.hi, false, 0});
+                    nxt.push_back({sg.lo, sg.lo + kk, false, 0, sg.kmin, p - 1});
+                    nxt.push_back({sg.lo + kk, sg.hi, false, 0, p, sg.kmax});
                 }
             }
         }
