@@ -839,6 +839,7 @@ pp_status pp_set_param(const char* name, int64_t value) {
     else if (k == "qs_heavy") P.qs_heavy = value;
     else if (k == "qs_prio") P.qs_prio = value;
     else if (k == "qs_dev") P.qs_dev = value;
+    else if (k == "dist_split") P.dist_split = value ? 1 : 0;
     else if (k == "qs_dev_check") P.qs_dev_check = value;
     else if (k == "host_chunk") P.host_chunk = value;
     else if (k == "dist_p2p") P.dist_p2p = value ? 1 : 0;
@@ -883,6 +884,7 @@ int64_t pp_get_param(const char* name) {
     if (k == "qs_heavy") return P.qs_heavy;
     if (k == "qs_prio") return P.qs_prio;
     if (k == "qs_dev") return P.qs_dev;
+    if (k == "dist_split") return P.dist_split;
     if (k == "qs_dev_check") return P.qs_dev_check;
     if (k == "host_chunk") return P.host_chunk;
     if (k == "dist_p2p") return P.dist_p2p;

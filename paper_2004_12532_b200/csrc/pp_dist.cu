@@ -1417,7 +1417,10 @@ static pp_status quicksort_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, cuda
         // ---- pivots: one all-gather of the sample keys of this level ----
         // median of 3 (A[lo], A[mid], A[hi-1]; R14), or of 31 evenly spaced keys
         // with qs_pivot = 2 (the single-GPU level loop's rule)
-        const int NSMP = params().qs_pivot == 2 ? 31 : 3;
+        // (param dist_split = 1: 63 evenly spaced keys, and the pivot is the sample
+        // quantile of the rank boundary inside the segment -- see below)
+        const bool bsplit = params().dist_split != 0;
+        const int NSMP = bsplit ? 63 : params().qs_pivot == 2 ? 31 : 3;
         std::vector<uint64_t> spos;  // NSMP per segment needing a sample
         for (const Seg& sg : big)
             if (!sg.leq) {
@@ -1427,7 +1430,9 @@ static pp_status quicksort_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, cuda
                     spos.push_back(sg.lo + (len - 1) / 2);
                     spos.push_back(sg.hi - 1);
                 } else {
-                    for (uint64_t j = 0; j < 31; ++j) spos.push_back(sg.lo + (len - 1) / 30 * j + ((len - 1) % 30) * j / 30);
+                    const uint64_t d = (uint64_t)NSMP - 1;
+                    for (uint64_t j = 0; j < (uint64_t)NSMP; ++j)
+                        spos.push_back(sg.lo + (len - 1) / d * j + ((len - 1) % d) * j / d);
                 }
             }
         std::vector<uint64_t> sval;
@@ -1461,6 +1466,21 @@ static pp_status quicksort_dist_ctx(DistCtx& c, K* shard, uint64_t n_local, cuda
                     si += NSMP;
                     std::sort(v.begin(), v.end());
                     p = v[NSMP / 2];
+                    if (bsplit) {
+                        // the rank boundary inside the segment nearest its middle; the
+                        // pivot is the sample quantile of its position, so the split
+                        // lands near the boundary and the spanning part shrinks by
+                        // ~1/NSMP per round instead of ~1/2
+                        const uint64_t mid = sg.lo + (sg.hi - sg.lo) / 2;
+                        uint64_t bnd = 0, best = ~0ull;
+                        for (int r = 1; r < P; ++r)
+                            if (base[r] > sg.lo && base[r] < sg.hi) {
+                                const uint64_t dd = base[r] > mid ? base[r] - mid : mid - base[r];
+                                if (dd < best) { best = dd; bnd = base[r]; }
+                            }
+                        const double f = (double)(bnd - sg.lo) / (double)(sg.hi - sg.lo);
+                        p = v[std::min<size_t>((size_t)(f * (NSMP - 1) + 0.5), (size_t)NSMP - 1)];
+                    }
                     // at the lower bound the x < p split is empty: split by x < kmin + 1 now
                     if (p == sg.kmin) p = (uint64_t)(K)(p + 1);
                 }

@@ -65,6 +65,8 @@ struct Params {
     int64_t dist_overlap = 0;      // pp_partition_dist: 1 = count first, then chunked local partitions whose exchange
                                    // pieces move while the next chunk is partitioned
     int64_t dist_chunks = 8;       // dist_overlap: chunks per shard (the same on every rank)
+    int64_t dist_split = 0;        // distributed quicksort: 1 = pivots of spanning segments at the sample quantile
+                                   // of their rank boundary (63 samples; fewer distributed rounds), 0 = R14's rule
     int64_t dist_small = 1 << 16;  // distributed quicksort: spanning segments <= this are gathered and sorted locally
     int64_t host_chunk = 1 << 23;  // host-buffer partition: keys per streamed chunk (measured best at 1-8 GiB)
     int64_t qs_pivot = 0;          // quicksort level-loop pivot: 0 median of 3 (BJ config 5), 1 Tukey's ninther,

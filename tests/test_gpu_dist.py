@@ -362,6 +362,30 @@ def test_loopback_quicksort(pp, P, dt):
         pp.reset_params()
 
 
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_loopback_quicksort_boundary_split(pp, P):
+    """dist_split = 1 (pivots of spanning segments at the sample quantile of
+    their rank boundary): the same global sort, byte for byte against
+    oracle.quicksort, on ragged / empty / equal shards and duplicate keys."""
+    from gpu_util import to_dev, to_host
+    rng = np.random.default_rng(91 * P)
+    try:
+        pp.pp_set_param("dist_split", 1)
+        for total, kind, dk, small in ((200_003, "ragged", "uniform", 1000), (300_001, "empty", "dup", 1000),
+                                       (100_000, "equal", "equal", 1000), (1 << 20, "ragged", "uniform", 1 << 16),
+                                       (1 << 20, "equal", "dup", 1 << 12)):
+            pp.pp_set_param("dist_small", small)
+            ns = _shards(rng, total, P, kind)
+            a = _keys(rng, total, np.uint64, dk)
+            t = to_dev(a)
+            pp.pp_quicksort_dist_loopback(t, ns)
+            ref = a.copy()
+            oracle.quicksort(ref)
+            assert np.array_equal(to_host(t, np.uint64), ref), (total, kind, dk, small)
+    finally:
+        pp.reset_params()
+
+
 def test_loopback_quicksort_p2p(pp):
     """The distributed quicksort with the one-sided exchange."""
     from gpu_util import to_dev, to_host

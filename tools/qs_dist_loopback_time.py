@@ -25,8 +25,12 @@ def main():
     ap.add_argument("--P", type=int, default=8)
     ap.add_argument("--kinds", default="uniform,dup1000")
     ap.add_argument("--reps", type=int, default=3)  # (>= 1)
+    ap.add_argument("--params", default="", help="k=v,k=v library params")
     a = ap.parse_args()
     pp.load(build_if_missing=False)
+    for kv in filter(None, a.params.split(",")):
+        k, v = kv.split("=")
+        pp.pp_set_param(k, int(v))
     n = 1 << a.n
     for kind in a.kinds.split(","):
         q0 = (synth.uniform_u64_torch(n, synth.SEEDS["c5"], "cuda") if kind == "uniform"
@@ -42,7 +46,8 @@ def main():
             e.record()
             torch.cuda.synchronize()
             ts.append(s.elapsed_time(e))
-        print({"kind": kind, "P": a.P, "ms": sorted(ts[1:])[len(ts[1:]) // 2], "lib": os.path.basename(pp.LIB_PATH)})
+        print({"kind": kind, "P": a.P, "params": a.params, "ms": sorted(ts[1:])[len(ts[1:]) // 2],
+               "lib": os.path.basename(pp.LIB_PATH)})
 
 
 if __name__ == "__main__":
