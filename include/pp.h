@@ -343,7 +343,9 @@ pp_status pp_audit_set(uint32_t *d_shadow, const void *keys, uint64_t n, int key
  * a difference); "host_chunk", "bps_nt";
  * multi-GPU: "dist_p2p", "dist_timeout_ms", "dist_small" (distributed
  * quicksort: spanning segments of <= this many keys are gathered and sorted
- * locally), "dist_overlap" (1: pp_partition_dist counts every chunk of the
+ * locally), "dist_split" (1: the pivot of a segment spanning ranks is the
+ * quantile of its rank boundary among 63 samples -- fewer distributed rounds;
+ * 0 default: the level loop's rule), "dist_overlap" (1: pp_partition_dist counts every chunk of the
  * shard first, all-gathers the counts, then partitions the "dist_chunks"
  * chunks in order while the exchange of each finished chunk runs on a second
  * stream -- SURVEY §8(f) #1; same result contract), "dist_chunks" (default
