@@ -333,7 +333,9 @@ pp_status pp_audit_set(uint32_t *d_shadow, const void *keys, uint64_t n, int key
  * of 31 evenly spaced keys: better balanced splits, fewer levels; also the
  * distributed quicksort's rule for segments spanning ranks), "qs_deep" (segments deeper
  * than this take Tukey's ninther instead of the median of 3; -1 auto =
- * 2 log2(n) + 16, 0 = always), "qs_dev" (1: once a lane's segments are all
+ * 2 log2(n) + 16, 0 = always), "qs_prio" (-1 auto = on: the level loop on
+ * high-priority streams, the early recursion / bin sorts at low priority; 0
+ * off), "qs_dev" (1: once a lane's segments are all
  * below qs_heavy, every next level's segment list is built on the device by
  * one kernel -- children, group counts, longest-first order compacted by
  * scans -- and two levels per lane are in flight without a host round trip;

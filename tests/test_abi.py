@@ -81,3 +81,23 @@ def test_no_atomics_in_sass():
     assert not bad, bad[:5]
     assert allowed_hits > 0  # the scoped exception is real (the bin sort is built)
     assert "UBLKCP" in sass  # the group kernel stages lines with the bulk-copy (TMA) engine
+
+
+def test_every_documented_tunable_round_trips():
+    """Every tunable the header documents (include/pp.h, the "Tunables"
+    comment) exists in the library and only those: set, read back, and
+    pp_reset_params restores the default."""
+    import re
+    hdr = open(pp.HEADER).read()
+    i = hdr.index("/* Tunables")
+    documented = set(re.findall(r'"([a-z][a-z0-9_]*)"', hdr[i:hdr.index("*/", i)]))
+    src = open(os.path.join(os.path.dirname(pp.__file__), "csrc", "pp_api.cu")).read()
+    assert documented == set(re.findall(r'k == "([a-z0-9_]*)"', src))
+    pp.reset_params()
+    for name in sorted(documented):
+        default = pp.pp_get_param(name)
+        assert default != -(1 << 63), name
+        pp.pp_set_param(name, 1)
+        assert pp.pp_get_param(name) in (1, 0), name  # (boolean or clamped tunables may map 1 to themselves)
+        pp.reset_params()
+        assert pp.pp_get_param(name) == default, name
