@@ -56,8 +56,8 @@ struct Params {
                                    // streams as soon as their levels complete (overlapping the remaining levels);
                                    // -1 auto (= on), 0 off, 1 on
     int64_t qs_early_min = 0;      // quicksort early recursion: batch when >= this x #SM small segments are final
-                                   // (0 auto: 4 for u64, 2 for u32 -- measured)
-    int64_t qs_minl = 0;           // quicksort: at least this many lines per group for mid segments (0 auto: 128 KiB)
+                                   // (0 auto: 8 for u64, 2 for u32 -- measured)
+    int64_t qs_minl = 0;           // quicksort: at least this many lines per group for mid segments (0 auto: 64)
     int64_t dist_p2p = 0;          // pp_partition_dist: 1 = one-sided exchange over CUDA-IPC peer mappings (no staging)
     int64_t dist_timeout_ms = 600000;  // distributed calls: a wait longer than this aborts (PP_E_NCCL on every rank)
     int64_t dist_fault = 0;        // test hook (loopback): 1 = rank dist_fault_rank fails its local step, 2 = it never arrives
@@ -75,7 +75,7 @@ struct Params {
                                    // 2 log2(n) + 16; 0: always)
     int64_t qs_prio = -1;          // quicksort: level loop on high-priority streams, early recursion / bins low
                                    // (-1 auto = on, 0 off, 1 on)
-    int64_t qs_heavy = 1 << 22;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
+    int64_t qs_heavy = 1 << 21;    // quicksort: mid segments >= this get the batched multi-CTA cleanup (0 = off)
     int64_t qs_dev_check = 0;      // test hook: compare each device-built level list with the host's plan of it
     int64_t qs_dev = 0;            // quicksort: 1 = levels whose segments are all < qs_heavy are built on the
                                    // device (qs_build_kernel), two levels in flight per lane; 0 (default) = the

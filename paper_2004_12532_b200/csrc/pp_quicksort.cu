@@ -1632,9 +1632,10 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     const QsGeom geom = qs_geom<K>();
     const uint64_t LEAF = geom.LEAF, BIG = geom.BIG, G_TARGET = geom.G_TARGET, HEAVY = geom.HEAVY;
     const HvLayout HVL = hv_layout();
-    // at least this many lines per group (mid segments); auto: 128 KiB of keys
-    // per group (16 lines u64, 32 lines u32 -- the best of a same-box sweep for each)
-    const uint64_t MINL = P.qs_minl > 0 ? (uint64_t)P.qs_minl : std::max<uint64_t>(1, (128u << 10) / (C::LK * sizeof(K)));
+    // at least this many lines per group (mid segments); auto: 64 lines (512 KiB
+    // of keys per group u64, 256 KiB u32 -- re-swept at the end of round 2: fewer,
+    // longer groups for the small late segments; was 128 KiB)
+    const uint64_t MINL = P.qs_minl > 0 ? (uint64_t)P.qs_minl : 64;
     const K KMAX = (K)~(K)0;
     g_qs_user_base = al256(partition_workspace_bound(n));
     g_qs_peak = 0;
@@ -1837,7 +1838,7 @@ static pp_status quicksort_device_impl(K* keys, uint64_t n, cudaStream_t st) {
     const bool early = P.qs_early != 0;  // -1 auto = on
     // batch size of the early recursion: x #SM segments (auto: 4 for u64, 2 for u32 -- measured)
     const uint64_t early_min =
-        (uint64_t)(P.qs_early_min > 0 ? P.qs_early_min : (sizeof(K) == 8 ? 4 : 2)) * (uint64_t)sm_count();
+        (uint64_t)(P.qs_early_min > 0 ? P.qs_early_min : (sizeof(K) == 8 ? 8 : 2)) * (uint64_t)sm_count();
     const uint64_t s_max = n / (LEAF + 1) + 1, slot_max = 2 * (n / LEAF) + 6 * s_max + 6;
     const size_t e_sloB = al256(8 * s_max), e_slnB = al256(4 * s_max), e_sbB = al256(8 * s_max);
     const size_t e_scrB = al256(sizeof(GroupOut) * s_max), e_bloB = al256(8 * slot_max), e_blnB = al256(4 * slot_max);
