@@ -35,17 +35,19 @@ def main():
     ap.add_argument("--dtype", default="u64")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--rounds", type=int, default=2)
+    ap.add_argument("--seed", type=int, default=None, help="input seed (default: config 5's)")
     args = ap.parse_args()
     pp.load(build_if_missing=False)
     n = 1 << args.n
+    seed = synth.SEEDS["c5"] if args.seed is None else args.seed
     inputs = {}
     for kind in args.kinds.split(","):
         if kind == "uniform":
-            q0 = (synth.uniform_u64_torch(n, synth.SEEDS["c5"], "cuda") if args.dtype == "u64"
-                  else synth.uniform_u32_torch(n, synth.SEEDS["c5"], "cuda"))
+            q0 = (synth.uniform_u64_torch(n, seed, "cuda") if args.dtype == "u64"
+                  else synth.uniform_u32_torch(n, seed, "cuda"))
         else:  # dup1000, dup10000, ...: keys uniform in [0, m)
             m = int(kind[3:]) if kind.startswith("dup") and kind[3:].isdigit() else 1000
-            q0 = synth.mod_range_u64_torch(n, synth.SEEDS["c5"], m, "cuda")
+            q0 = synth.mod_range_u64_torch(n, seed, m, "cuda")
             if args.dtype == "u32":
                 q0 = q0.to(torch.int32)
         inputs[kind] = (q0, lib_sorted(q0))
