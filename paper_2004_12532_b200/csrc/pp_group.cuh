@@ -125,6 +125,24 @@ __device__ __forceinline__ void warp_prefix16(const uint16_t* cnt16, int nw, int
     tot = carry;
 }
 
+// The same by warp shuffles: lane i < NW holds warp i's count, an inclusive
+// shuffle scan over the NW lanes, two broadcasts -- ~12 instructions per warp
+// and line instead of the packed-word arithmetic's ~45, but a longer chain of
+// dependent shuffles (used where the engine is issue-bound: 8+ warps).
+template <int NW>
+__device__ __forceinline__ void warp_prefix_shfl(const uint16_t* cnt16, int warp, int lane, uint32_t& woff,
+                                                 uint32_t& tot) {
+    uint32_t c = lane < NW ? (uint32_t)cnt16[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < NW; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, c, o);
+        if (lane >= o) c += y;
+    }
+    tot = __shfl_sync(0xffffffffu, c, NW - 1);
+    const uint32_t before = __shfl_sync(0xffffffffu, c, warp > 0 ? warp - 1 : 0);
+    woff = warp > 0 ? before : 0u;
+}
+
 // One CTA partitions group gi of the region (n_lines full lines of LK keys).
 // The group's lines in group order are consumed from both ends; predecessors
 // and successors are appended to two shared-memory pools; a front line is
@@ -263,7 +281,11 @@ __device__ void ss_group_engine(typename C::Key* __restrict__ region, uint64_t n
         __syncthreads();  // (A) warp totals visible; previous write phase finished
         const uint32_t cur_line = slot_line[bi];  // written by thread 0 before an earlier barrier
         uint32_t woff, tot;
-        warp_prefix16(wcnt, NW, warp, woff, tot);
+        // 8+ warps (the u32 partition engine, issue-bound): shuffles, -0.5-1% on
+        // config 4; 4 warps (u64, the quicksort levels): the packed words, whose
+        // shorter dependency chain measured 7% faster at config 2
+        if constexpr (NW >= 8) warp_prefix_shfl<NW>(wcnt, warp, lane, woff, tot);
+        else warp_prefix16(wcnt, NW, warp, woff, tot);
         const uint32_t toff = tt + woff;
         const uint32_t foff = ft + (uint32_t)(warp * 32 * KPT) - woff;
         uint32_t acc = 0;
